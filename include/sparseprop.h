@@ -1,0 +1,186 @@
+/*
+ * sparseprop.h -- C ABI of the B200-native SparseProp hot path.
+ *
+ * SparseProp (arXiv 2302.04852): forward and backward of linear and 2-D
+ * convolution layers whose weights carry a fixed, arbitrary, unstructured
+ * sparsity mask, with work linear in nnz.  "P<n>" = PAPER.md line n.
+ *
+ * Conventions (all entry points):
+ *  - Every tensor pointer is a DEVICE pointer (cudaMalloc'd / torch CUDA
+ *    storage) to fp32, int32 or uint8 as typed, unless stated otherwise.
+ *  - Linear weights are W (R x C) = out x in (PyTorch nn.Linear.weight
+ *    order); the paper's O = X W (P141) is our Y = W X with W = W_paper^T.
+ *  - Linear activations are [features x B] row-major, batch contiguous:
+ *    the paper's transposed layout X^T (P183 §3.2).
+ *  - Conv activations are CHWN [C][H][W][B], batch last: the paper's
+ *    permuted SparseConv layout (P293 §3.3).  Conv weights are the dense
+ *    [OC][IC][KH][KW] tensor flattened to R = OC rows, C = IC*KH*KW columns.
+ *  - Outputs are OVERWRITTEN, never accumulated.  Empty rows / columns give
+ *    zeros.  Any B >= 1 is accepted (vector fast paths and scalar tails).
+ *  - Every compute call only enqueues work on `stream` (a cudaStream_t
+ *    passed as void*; NULL = legacy default stream) and never synchronises
+ *    the host; asynchronous device faults surface at the caller's next sync.
+ *    sp_weight_create synchronises `stream` exactly once (to learn nnz).
+ *  - No atomics anywhere: results are bitwise run-to-run reproducible.
+ *  - Errors: every call returns sp_status; no C++ exception crosses the
+ *    ABI.  Arguments are validated before any launch; launch failures are
+ *    reported as SP_ERR_CUDA.  sp_last_error() gives a thread-local message.
+ *  - Handles are immutable in structure after creation and may be shared
+ *    across streams and host threads; the vals buffer is mutable in place
+ *    (the optimizer writes it) and the caller orders such writes.
+ */
+#ifndef SPARSEPROP_H
+#define SPARSEPROP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sp_weight_s *sp_weight_t; /* opaque: index structure + vals */
+typedef void *sp_stream_t;               /* a cudaStream_t */
+
+typedef enum {
+    SP_OK = 0,
+    SP_ERR_NULL = 1,       /* a required pointer was NULL */
+    SP_ERR_SHAPE = 2,      /* non-positive or inconsistent sizes */
+    SP_ERR_OVERFLOW = 3,   /* nnz, an index or a size does not fit int32 */
+    SP_ERR_ALLOC = 4,      /* device allocation failed */
+    SP_ERR_CUDA = 5,       /* a CUDA runtime / launch error */
+    SP_ERR_BAD_HANDLE = 6  /* handle NULL or destroyed */
+} sp_status;
+
+/* Conv geometry, stride 1 (stride > 1 is out of scope).
+ * OH = H + 2*pad - KH + 1, OW = W + 2*pad - KW + 1 (P223 generalised by
+ * Alg. 2's pad, P317-P320).  C_out/C_in*KH*KW must match the handle. */
+typedef struct {
+    int32_t B, C_in, H, W, C_out, KH, KW, pad;
+} sp_conv_geom;
+
+/* ---------------------------------------------------------------------- */
+/* Weight handle: CSR (P153-P154) + CSC/transposed index copy (P183)      */
+/* ---------------------------------------------------------------------- */
+
+/* Build the handle from a dense R x C fp32 weight and an R x C uint8 mask
+ * (both device, row-major).  The STRUCTURE is the mask (nonzero byte =
+ * kept; on-mask zero values are stored, off-mask values ignored).  Builds
+ *   row_ptr[R+1], col_idx[nnz] (ascending per row), vals[nnz] (CSR order),
+ *   col_ptr[C+1], row_idx[nnz] (ascending per column),
+ *   perm[nnz] (CSC slot k -> CSR slot holding the same (r, c)),
+ * deterministically on the device, then synchronises `stream` once to read
+ * nnz.  R, C >= 1; R*C and nnz must fit int32 (else SP_ERR_OVERFLOW).
+ * The handle owns all its device buffers. */
+sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8_t *mask,
+                           sp_stream_t stream, sp_weight_t *out);
+
+/* Frees the handle's buffers (after synchronising `stream`). */
+sp_status sp_weight_destroy(sp_weight_t W, sp_stream_t stream);
+
+/* nnz, R, C of a handle (-1 on a bad handle). */
+int64_t sp_weight_nnz(sp_weight_t W);
+int64_t sp_weight_rows(sp_weight_t W);
+int64_t sp_weight_cols(sp_weight_t W);
+
+/* Device pointer to the handle-owned vals[nnz] (CSR order), writable in
+ * place (e.g. by sp_sgd).  Lifetime = the handle's. */
+sp_status sp_weight_vals(sp_weight_t W, float **vals);
+
+/* Device pointers to the handle-owned index arrays (read-only). */
+sp_status sp_weight_indices(sp_weight_t W, const int32_t **row_ptr, const int32_t **col_idx,
+                            const int32_t **col_ptr, const int32_t **row_idx,
+                            const int32_t **perm);
+
+/* Scatter an nnz-length device buffer (vals or a gradient, CSR order) into a
+ * dense R x C device buffer: exact +0.0 off the mask. */
+sp_status sp_weight_to_dense(sp_weight_t W, const float *nz, float *dense_out,
+                             sp_stream_t stream);
+
+/* ---------------------------------------------------------------------- */
+/* Linear layer (P141-P151 §3.2)                                          */
+/* ---------------------------------------------------------------------- */
+
+/* Forward SpMM: Y[r][b] = sum_{j in row r} vals[j] * X[col_idx[j]][b].
+ * X: [C x B], Y: [R x B].  (P141 "O = XW", transposed per P183.) */
+sp_status sp_linear_fwd(sp_weight_t W, const float *X, float *Y, int64_t B, sp_stream_t stream);
+
+/* Input-gradient SpMM, Eq. (1) (P143-P145): dX = W^T dY, gather form driven
+ * by the CSC copy, each dX row produced by exactly one warp (no atomics):
+ * dX[c][b] = sum_{k in col c} vals[perm[k]] * dY[row_idx[k]][b].
+ * dY: [R x B], dX: [C x B]. */
+sp_status sp_linear_bwd_input(sp_weight_t W, const float *dY, float *dX, int64_t B,
+                              sp_stream_t stream);
+
+/* Weight-gradient SDDMM, Eq. (2) (P146-P148, P151, P173 "nnz
+ * dot-products"): dW[j] = sum_b dY[r_j][b] * X[c_j][b] for every nonzero j
+ * (CSR order); nothing is computed off the mask.  X: [C x B], dY: [R x B],
+ * dW: [nnz]. */
+sp_status sp_linear_bwd_weight(sp_weight_t W, const float *X, const float *dY, float *dW,
+                               int64_t B, sp_stream_t stream);
+
+/* Fused epilogue variants used by the data-parallel MLP step (north star
+ * cfg5): identical arithmetic plus an elementwise epilogue in the same
+ * kernel.
+ *  sp_linear_fwd_relu:        Y = max(W X, 0)              (ReLU)
+ *  sp_linear_bwd_input_relu:  dX = (W^T dY) * [H > 0]      (ReLU', with
+ *      H the saved post-ReLU activation [C x B]; ReLU'(0) = 0) */
+sp_status sp_linear_fwd_relu(sp_weight_t W, const float *X, float *Y, int64_t B,
+                             sp_stream_t stream);
+sp_status sp_linear_bwd_input_relu(sp_weight_t W, const float *dY, const float *H, float *dX,
+                                   int64_t B, sp_stream_t stream);
+
+/* ---------------------------------------------------------------------- */
+/* 2-D convolution, stride 1, CHWN (P222-P248 §3.3, Alg. 2 P297-P347)     */
+/* ---------------------------------------------------------------------- */
+
+/* Forward, Eq. (3) with padding, implicit im2col that visits only the
+ * stored taps (P248): Y[oc][p][q][b] = sum over nonzeros (ic,x,y) of row oc
+ * of w * X[ic][p+x-pad][q+y-pad][b] (0 outside).  X: [C_in][H][W][B],
+ * Y: [C_out][OH][OW][B]. */
+sp_status sp_conv2d_fwd(sp_weight_t W, const sp_conv_geom *g, const float *X, float *Y,
+                        sp_stream_t stream);
+
+/* Input gradient, Eq. (4) (P231-P238, bounds clipped per SURVEY C6):
+ * dX[ic][m][n][b] = sum_{(x,y)} sum_{oc in CSC column (ic,x,y)}
+ *                   w * dY[oc][m+pad-x][n+pad-y][b] over valid outputs.
+ * Gather form (no atomics).  dY: [C_out][OH][OW][B], dX: [C_in][H][W][B]. */
+sp_status sp_conv2d_bwd_input(sp_weight_t W, const sp_conv_geom *g, const float *dY, float *dX,
+                              sp_stream_t stream);
+
+/* Weight gradient, Eq. (5) (P240-P246), only at the nonzeros (P248):
+ * dW[j=(oc,ic,x,y)] = sum_{p,q valid, b} dY[oc][p][q][b] *
+ *                     X[ic][p+x-pad][q+y-pad][b].  dW: [nnz], CSR order of
+ * the flattened filter == the paper's (oc, ic, x, y) storage order. */
+sp_status sp_conv2d_bwd_weight(sp_weight_t W, const sp_conv_geom *g, const float *X,
+                               const float *dY, float *dW, sp_stream_t stream);
+
+/* ---------------------------------------------------------------------- */
+/* Step helpers for the data-parallel sparse MLP (north star cfg5)        */
+/* ---------------------------------------------------------------------- */
+
+/* dY = Y - T and loss_partial = 1/2 sum (Y - T)^2 over n elements (SURVEY
+ * C18).  loss_out: ONE device float; the sum is a fixed-order two-level
+ * tree (deterministic).  `scratch` must hold sp_mse_scratch_floats(n)
+ * device floats. */
+int64_t sp_mse_scratch_floats(int64_t n);
+sp_status sp_mse_grad(const float *Y, const float *T, float *dY, float *loss_out,
+                      float *scratch, int64_t n, sp_stream_t stream);
+
+/* Plain SGD on the kept weights only: vals[j] -= lr * dW[j]. */
+sp_status sp_sgd(float *vals, const float *dW, int64_t nnz, float lr, sp_stream_t stream);
+
+/* Thread-local message for the last non-OK status on this thread. */
+const char *sp_last_error(void);
+
+/* Number of kernels this library has launched in the process so far
+ * (provenance: bench.py reports the delta over its timed region). */
+uint64_t sp_launch_count(void);
+
+/* Library build string (arch, version) for provenance in bench records. */
+const char *sp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPARSEPROP_H */

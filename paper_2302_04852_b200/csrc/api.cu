@@ -1,0 +1,253 @@
+// api.cu -- the extern "C" boundary of libsparseprop (include/sparseprop.h).
+// Argument validation, handle lifetime, dispatch to the kernels.  No C++
+// exception crosses the ABI; every entry point returns sp_status.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <new>
+#include <string>
+
+#include "sp_internal.cuh"
+
+namespace sp {
+
+static thread_local std::string g_err;
+static std::atomic<unsigned long long> g_launches{0};
+
+void count_launches(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+sp_status check_launch(const char *what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string(what) + ": " + cudaGetErrorString(e));
+        return SP_ERR_CUDA;
+    }
+    return SP_OK;
+}
+
+}  // namespace sp
+
+using namespace sp;
+
+namespace {
+
+constexpr int64_t kI32Max = 2147483647LL;
+
+sp_status fail(sp_status s, const std::string &msg) {
+    set_error(msg);
+    return s;
+}
+
+bool ok_handle(sp_weight_t w) { return w != nullptr && w->magic == SP_MAGIC; }
+
+#define SP_CHECK_HANDLE(w, fn) \
+    if (!ok_handle(w)) return fail(SP_ERR_BAD_HANDLE, std::string(fn) + ": bad or destroyed handle")
+
+sp_status check_B(int64_t B, int64_t rows_a, int64_t rows_b, const char *fn) {
+    if (B < 1) return fail(SP_ERR_SHAPE, std::string(fn) + ": B must be >= 1");
+    if (rows_a * B > (int64_t)1 << 40 || rows_b * B > (int64_t)1 << 40)
+        return fail(SP_ERR_OVERFLOW, std::string(fn) + ": activation too large");
+    return SP_OK;
+}
+
+sp_status check_geom(sp_weight_t w, const sp_conv_geom *g, const char *fn) {
+    if (!g) return fail(SP_ERR_NULL, std::string(fn) + ": geometry is NULL");
+    if (g->B < 1 || g->C_in < 1 || g->H < 1 || g->W < 1 || g->C_out < 1 || g->KH < 1 || g->KW < 1 ||
+        g->pad < 0)
+        return fail(SP_ERR_SHAPE, std::string(fn) + ": non-positive conv dimension");
+    const int64_t OH = (int64_t)g->H + 2 * g->pad - g->KH + 1;
+    const int64_t OW = (int64_t)g->W + 2 * g->pad - g->KW + 1;
+    if (OH < 1 || OW < 1) return fail(SP_ERR_SHAPE, std::string(fn) + ": empty output");
+    if (w->R != g->C_out || w->C != (int64_t)g->C_in * g->KH * g->KW)
+        return fail(SP_ERR_SHAPE, std::string(fn) + ": weight handle does not match C_out x C_in*KH*KW");
+    const int64_t nx = (int64_t)g->C_in * g->H * g->W * g->B;
+    const int64_t ny = (int64_t)g->C_out * OH * OW * g->B;
+    if (nx > ((int64_t)1 << 40) || ny > ((int64_t)1 << 40))
+        return fail(SP_ERR_OVERFLOW, std::string(fn) + ": activation too large");
+    return SP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *sp_last_error(void) { return g_err.c_str(); }
+
+uint64_t sp_launch_count(void) { return g_launches.load(); }
+
+const char *sp_version(void) { return "libsparseprop 0.1 sm_100a fp32 (CUDA cores, no atomics)"; }
+
+sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8_t *mask,
+                           sp_stream_t stream, sp_weight_t *out) {
+    if (!out) return fail(SP_ERR_NULL, "sp_weight_create: out is NULL");
+    *out = nullptr;
+    if (!dense || !mask) return fail(SP_ERR_NULL, "sp_weight_create: dense or mask is NULL");
+    if (R < 1 || C < 1) return fail(SP_ERR_SHAPE, "sp_weight_create: R and C must be >= 1");
+    if (R > kI32Max || C > kI32Max || R * C > kI32Max)
+        return fail(SP_ERR_OVERFLOW, "sp_weight_create: R*C must fit int32");
+    sp_weight_s *w = new (std::nothrow) sp_weight_s();
+    if (!w) return fail(SP_ERR_ALLOC, "sp_weight_create: host allocation failed");
+    w->magic = SP_MAGIC;
+    const sp_status s = build_weight(R, C, dense, mask, S(stream), w);
+    if (s != SP_OK) {
+        cudaFree(w->row_ptr);
+        cudaFree(w->col_idx);
+        cudaFree(w->vals);
+        cudaFree(w->col_ptr);
+        cudaFree(w->row_idx);
+        cudaFree(w->perm);
+        cudaFree(w->row_of);
+        w->magic = 0;
+        delete w;
+        return s;
+    }
+    *out = w;
+    return SP_OK;
+}
+
+sp_status sp_weight_destroy(sp_weight_t w, sp_stream_t stream) {
+    SP_CHECK_HANDLE(w, "sp_weight_destroy");
+    cudaStreamSynchronize(S(stream));
+    cudaFree(w->row_ptr);
+    cudaFree(w->col_idx);
+    cudaFree(w->vals);
+    cudaFree(w->col_ptr);
+    cudaFree(w->row_idx);
+    cudaFree(w->perm);
+    cudaFree(w->row_of);
+    w->magic = 0;
+    delete w;
+    return SP_OK;
+}
+
+int64_t sp_weight_nnz(sp_weight_t w) { return ok_handle(w) ? w->nnz : -1; }
+int64_t sp_weight_rows(sp_weight_t w) { return ok_handle(w) ? w->R : -1; }
+int64_t sp_weight_cols(sp_weight_t w) { return ok_handle(w) ? w->C : -1; }
+
+sp_status sp_weight_vals(sp_weight_t w, float **vals) {
+    SP_CHECK_HANDLE(w, "sp_weight_vals");
+    if (!vals) return fail(SP_ERR_NULL, "sp_weight_vals: out is NULL");
+    *vals = w->vals;
+    return SP_OK;
+}
+
+sp_status sp_weight_indices(sp_weight_t w, const int32_t **row_ptr, const int32_t **col_idx,
+                            const int32_t **col_ptr, const int32_t **row_idx, const int32_t **perm) {
+    SP_CHECK_HANDLE(w, "sp_weight_indices");
+    if (row_ptr) *row_ptr = w->row_ptr;
+    if (col_idx) *col_idx = w->col_idx;
+    if (col_ptr) *col_ptr = w->col_ptr;
+    if (row_idx) *row_idx = w->row_idx;
+    if (perm) *perm = w->perm;
+    return SP_OK;
+}
+
+sp_status sp_weight_to_dense(sp_weight_t w, const float *nz, float *dense_out, sp_stream_t stream) {
+    SP_CHECK_HANDLE(w, "sp_weight_to_dense");
+    if (!dense_out || (!nz && w->nnz > 0)) return fail(SP_ERR_NULL, "sp_weight_to_dense: NULL buffer");
+    launch_to_dense(w, nz, dense_out, S(stream));
+    return check_launch("sp_weight_to_dense");
+}
+
+static sp_status linear_fwd_impl(sp_weight_t w, const float *X, float *Y, int64_t B, int epi,
+                                 sp_stream_t stream, const char *fn) {
+    SP_CHECK_HANDLE(w, fn);
+    if (!X || !Y) return fail(SP_ERR_NULL, std::string(fn) + ": NULL tensor");
+    sp_status s = check_B(B, w->R, w->C, fn);
+    if (s != SP_OK) return s;
+    launch_spmm(w->R, w->C, B, w->row_ptr, w->col_idx, nullptr, w->vals, X, Y, nullptr, epi,
+                w->max_row_nnz, S(stream));
+    return check_launch(fn);
+}
+
+sp_status sp_linear_fwd(sp_weight_t w, const float *X, float *Y, int64_t B, sp_stream_t stream) {
+    return linear_fwd_impl(w, X, Y, B, EPI_NONE, stream, "sp_linear_fwd");
+}
+
+sp_status sp_linear_fwd_relu(sp_weight_t w, const float *X, float *Y, int64_t B, sp_stream_t stream) {
+    return linear_fwd_impl(w, X, Y, B, EPI_RELU, stream, "sp_linear_fwd_relu");
+}
+
+static sp_status linear_dx_impl(sp_weight_t w, const float *dY, const float *H, float *dX, int64_t B,
+                                int epi, sp_stream_t stream, const char *fn) {
+    SP_CHECK_HANDLE(w, fn);
+    if (!dY || !dX || (epi == EPI_GATE && !H)) return fail(SP_ERR_NULL, std::string(fn) + ": NULL tensor");
+    sp_status s = check_B(B, w->R, w->C, fn);
+    if (s != SP_OK) return s;
+    launch_spmm(w->C, w->R, B, w->col_ptr, w->row_idx, w->perm, w->vals, dY, dX, H, epi,
+                w->max_col_nnz, S(stream));
+    return check_launch(fn);
+}
+
+sp_status sp_linear_bwd_input(sp_weight_t w, const float *dY, float *dX, int64_t B, sp_stream_t stream) {
+    return linear_dx_impl(w, dY, nullptr, dX, B, EPI_NONE, stream, "sp_linear_bwd_input");
+}
+
+sp_status sp_linear_bwd_input_relu(sp_weight_t w, const float *dY, const float *H, float *dX, int64_t B,
+                                   sp_stream_t stream) {
+    return linear_dx_impl(w, dY, H, dX, B, EPI_GATE, stream, "sp_linear_bwd_input_relu");
+}
+
+sp_status sp_linear_bwd_weight(sp_weight_t w, const float *X, const float *dY, float *dW, int64_t B,
+                               sp_stream_t stream) {
+    SP_CHECK_HANDLE(w, "sp_linear_bwd_weight");
+    if (!X || !dY || (!dW && w->nnz > 0)) return fail(SP_ERR_NULL, "sp_linear_bwd_weight: NULL tensor");
+    sp_status s = check_B(B, w->R, w->C, "sp_linear_bwd_weight");
+    if (s != SP_OK) return s;
+    s = launch_sddmm(w, X, dY, dW, B, S(stream));
+    if (s != SP_OK) return s;
+    return check_launch("sp_linear_bwd_weight");
+}
+
+sp_status sp_conv2d_fwd(sp_weight_t w, const sp_conv_geom *g, const float *X, float *Y, sp_stream_t stream) {
+    SP_CHECK_HANDLE(w, "sp_conv2d_fwd");
+    sp_status s = check_geom(w, g, "sp_conv2d_fwd");
+    if (s != SP_OK) return s;
+    if (!X || !Y) return fail(SP_ERR_NULL, "sp_conv2d_fwd: NULL tensor");
+    launch_conv_fwd(w, *g, X, Y, S(stream));
+    return check_launch("sp_conv2d_fwd");
+}
+
+sp_status sp_conv2d_bwd_input(sp_weight_t w, const sp_conv_geom *g, const float *dY, float *dX,
+                              sp_stream_t stream) {
+    SP_CHECK_HANDLE(w, "sp_conv2d_bwd_input");
+    sp_status s = check_geom(w, g, "sp_conv2d_bwd_input");
+    if (s != SP_OK) return s;
+    if (!dY || !dX) return fail(SP_ERR_NULL, "sp_conv2d_bwd_input: NULL tensor");
+    launch_conv_bwd_input(w, *g, dY, dX, S(stream));
+    return check_launch("sp_conv2d_bwd_input");
+}
+
+sp_status sp_conv2d_bwd_weight(sp_weight_t w, const sp_conv_geom *g, const float *X, const float *dY,
+                               float *dW, sp_stream_t stream) {
+    SP_CHECK_HANDLE(w, "sp_conv2d_bwd_weight");
+    sp_status s = check_geom(w, g, "sp_conv2d_bwd_weight");
+    if (s != SP_OK) return s;
+    if (!X || !dY || (!dW && w->nnz > 0)) return fail(SP_ERR_NULL, "sp_conv2d_bwd_weight: NULL tensor");
+    s = launch_conv_bwd_weight(w, *g, X, dY, dW, S(stream));
+    if (s != SP_OK) return s;
+    return check_launch("sp_conv2d_bwd_weight");
+}
+
+int64_t sp_mse_scratch_floats(int64_t n) { return mse_scratch_floats(n); }
+
+sp_status sp_mse_grad(const float *Y, const float *T, float *dY, float *loss_out, float *scratch, int64_t n,
+                      sp_stream_t stream) {
+    if (!Y || !T || !dY || !loss_out || !scratch) return fail(SP_ERR_NULL, "sp_mse_grad: NULL tensor");
+    if (n < 1) return fail(SP_ERR_SHAPE, "sp_mse_grad: n must be >= 1");
+    if (reinterpret_cast<uintptr_t>(scratch) & 7) return fail(SP_ERR_SHAPE, "sp_mse_grad: scratch must be 8-byte aligned");
+    launch_mse(Y, T, dY, loss_out, scratch, n, S(stream));
+    return check_launch("sp_mse_grad");
+}
+
+sp_status sp_sgd(float *vals, const float *dW, int64_t nnz, float lr, sp_stream_t stream) {
+    if ((!vals || !dW) && nnz > 0) return fail(SP_ERR_NULL, "sp_sgd: NULL tensor");
+    if (nnz < 0) return fail(SP_ERR_SHAPE, "sp_sgd: nnz < 0");
+    launch_sgd(vals, dW, nnz, lr, S(stream));
+    return check_launch("sp_sgd");
+}
+
+}  // extern "C"

@@ -1,0 +1,314 @@
+// conv.cu -- sparse-filter 2-D convolution, stride 1, CHWN (batch-last)
+// layout (the paper's SparseConv layout, P293).  SURVEY §8(a) rows a-5..a-7.
+//
+// The filter [OC][IC][KH][KW] is the handle's R = OC x C = IC*KH*KW CSR
+// (column (ic, x, y) = (ic*KH + x)*KW + y), so row oc lists exactly the
+// stored taps of output channel oc in the paper's (oc, ic, x, y) order
+// (P251).  Implicit im2col: each stored tap is visited directly; pruned taps
+// cost nothing (P248).
+//
+//  fwd   (Eq. 3, P224):  warp per (oc, p, q-chunk), lanes over batch, VEC
+//        batch elements per lane, QC output columns in registers.
+//  dX    (Eq. 4, P231):  warp per (ic, m, n-chunk), gather over the CSC
+//        column of every tap (x, y): no atomics.
+//  dW    (Eq. 5, P240):  warp per (oc, 32 consecutive taps); dot products over
+//        (p, q, b) with a warp transpose-reduce at the end.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+
+#include "sp_internal.cuh"
+#include "tile.cuh"
+
+namespace sp {
+namespace {
+
+struct Geo {
+    int B, IC, H, W, OC, KH, KW, pad, OH, OW;
+};
+
+template <int VEC>
+__device__ __forceinline__ void ldg_vec(const float *p, float (&v)[VEC], bool vec_ok, int nvalid) {
+    if (vec_ok && nvalid == VEC) {
+        if constexpr (VEC == 1) v[0] = __ldg(p);
+        if constexpr (VEC == 2) {
+            float2 t = __ldg(reinterpret_cast<const float2 *>(p));
+            v[0] = t.x;
+            v[1] = t.y;
+        }
+        if constexpr (VEC == 4) {
+            float4 t = __ldg(reinterpret_cast<const float4 *>(p));
+            v[0] = t.x;
+            v[1] = t.y;
+            v[2] = t.z;
+            v[3] = t.w;
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) v[e] = e < nvalid ? __ldg(p + e) : 0.f;
+    }
+}
+
+template <int VEC>
+__device__ __forceinline__ void stg_vec(float *p, const float (&v)[VEC], bool vec_ok, int nvalid) {
+    if (vec_ok && nvalid == VEC) {
+        if constexpr (VEC == 1) *p = v[0];
+        if constexpr (VEC == 2) *reinterpret_cast<float2 *>(p) = make_float2(v[0], v[1]);
+        if constexpr (VEC == 4) *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e)
+            if (e < nvalid) p[e] = v[e];
+    }
+}
+
+// ---------------------------------------------------------------- forward
+template <int VEC, int QC>
+__global__ void __launch_bounds__(256)
+    conv_fwd_kernel(Geo g, int nqc, const int32_t *__restrict__ row_ptr,
+                    const int32_t *__restrict__ col_idx, const float *__restrict__ vals,
+                    const float *__restrict__ X, float *__restrict__ Y) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t nbc = (g.B + 32 * VEC - 1) / (32 * VEC);
+    // warp -> (oc, p, q-chunk, b-chunk), b-chunk fastest
+    int64_t t = wid;
+    const int bc = (int)(t % nbc);
+    t /= nbc;
+    const int qc = (int)(t % nqc);
+    t /= nqc;
+    const int p = (int)(t % g.OH);
+    const int oc = (int)(t / g.OH);
+    if (oc >= g.OC) return;
+    const int q0 = qc * QC;
+    const int b = bc * 32 * VEC + lane * VEC;
+    const int nvalid = min(VEC, max(0, g.B - b));
+    const bool vec_ok = (g.B % VEC) == 0;
+    const int KK = g.KH * g.KW;
+
+    float acc[QC][VEC];
+#pragma unroll
+    for (int q = 0; q < QC; ++q)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[q][v] = 0.f;
+
+    const int beg = __ldg(row_ptr + oc), end = __ldg(row_ptr + oc + 1);
+    for (int j0 = beg; j0 < end; j0 += 32) {
+        const int j = j0 + lane;
+        const int cl = j < end ? __ldg(col_idx + j) : 0;
+        const float wl = j < end ? __ldg(vals + j) : 0.f;
+        const int n = min(32, end - j0);
+        for (int s = 0; s < n; ++s) {
+            const int c = __shfl_sync(kFull, cl, s);
+            const float w = __shfl_sync(kFull, wl, s);
+            const int ic = c / KK, rem = c - ic * KK;
+            const int x = rem / g.KW, y = rem - x * g.KW;
+            const int ih = p + x - g.pad;
+            if (ih < 0 || ih >= g.H) continue;
+            const float *src = X + ((int64_t)ic * g.H + ih) * g.W * g.B;
+#pragma unroll
+            for (int q = 0; q < QC; ++q) {
+                const int iw = q0 + q + y - g.pad;
+                if (q0 + q < g.OW && iw >= 0 && iw < g.W) {
+                    float xv[VEC];
+                    ldg_vec<VEC>(src + (int64_t)iw * g.B + b, xv, vec_ok, nvalid);
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) acc[q][v] = fmaf(w, xv[v], acc[q][v]);
+                }
+            }
+        }
+    }
+    if (nvalid <= 0) return;
+#pragma unroll
+    for (int q = 0; q < QC; ++q) {
+        if (q0 + q >= g.OW) break;
+        stg_vec<VEC>(Y + (((int64_t)oc * g.OH + p) * g.OW + q0 + q) * g.B + b, acc[q], vec_ok, nvalid);
+    }
+}
+
+// ---------------------------------------------------------------- dX
+template <int VEC, int QC>
+__global__ void __launch_bounds__(256)
+    conv_dx_kernel(Geo g, int nqc, const int32_t *__restrict__ col_ptr,
+                   const int32_t *__restrict__ row_idx, const int32_t *__restrict__ perm,
+                   const float *__restrict__ vals, const float *__restrict__ dY,
+                   float *__restrict__ dX) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t nbc = (g.B + 32 * VEC - 1) / (32 * VEC);
+    int64_t t = wid;
+    const int bc = (int)(t % nbc);
+    t /= nbc;
+    const int qc = (int)(t % nqc);
+    t /= nqc;
+    const int m = (int)(t % g.H);
+    const int ic = (int)(t / g.H);
+    if (ic >= g.IC) return;
+    const int n0 = qc * QC;
+    const int b = bc * 32 * VEC + lane * VEC;
+    const int nvalid = min(VEC, max(0, g.B - b));
+    const bool vec_ok = (g.B % VEC) == 0;
+
+    float acc[QC][VEC];
+#pragma unroll
+    for (int q = 0; q < QC; ++q)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[q][v] = 0.f;
+
+    for (int x = 0; x < g.KH; ++x) {
+        const int p = m + g.pad - x;
+        if (p < 0 || p >= g.OH) continue;
+        for (int y = 0; y < g.KW; ++y) {
+            const int col = (ic * g.KH + x) * g.KW + y;
+            const int beg = __ldg(col_ptr + col), end = __ldg(col_ptr + col + 1);
+            for (int k0 = beg; k0 < end; k0 += 32) {
+                const int k = k0 + lane;
+                const int ocl = k < end ? __ldg(row_idx + k) : 0;
+                const float wl = k < end ? __ldg(vals + __ldg(perm + k)) : 0.f;
+                const int cnt = min(32, end - k0);
+                for (int s = 0; s < cnt; ++s) {
+                    const int oc = __shfl_sync(kFull, ocl, s);
+                    const float w = __shfl_sync(kFull, wl, s);
+                    const float *src = dY + ((int64_t)oc * g.OH + p) * g.OW * g.B;
+#pragma unroll
+                    for (int q = 0; q < QC; ++q) {
+                        const int oq = n0 + q + g.pad - y;
+                        if (n0 + q < g.W && oq >= 0 && oq < g.OW) {
+                            float dv[VEC];
+                            ldg_vec<VEC>(src + (int64_t)oq * g.B + b, dv, vec_ok, nvalid);
+#pragma unroll
+                            for (int v = 0; v < VEC; ++v) acc[q][v] = fmaf(w, dv[v], acc[q][v]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    if (nvalid <= 0) return;
+#pragma unroll
+    for (int q = 0; q < QC; ++q) {
+        if (n0 + q >= g.W) break;
+        stg_vec<VEC>(dX + (((int64_t)ic * g.H + m) * g.W + n0 + q) * g.B + b, acc[q], vec_ok, nvalid);
+    }
+}
+
+// ---------------------------------------------------------------- dW
+template <int VEC>
+__global__ void __launch_bounds__(256)
+    conv_dw_kernel(Geo g, int groups_per_row, const int32_t *__restrict__ row_ptr,
+                   const int32_t *__restrict__ col_idx, const float *__restrict__ X,
+                   const float *__restrict__ dY, float *__restrict__ dW) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int oc = (int)(wid / groups_per_row);
+    const int grp = (int)(wid % groups_per_row);
+    if (oc >= g.OC) return;
+    const int beg = __ldg(row_ptr + oc) + grp * 32, end = __ldg(row_ptr + oc + 1);
+    if (beg >= end) return;
+    const int n = min(32, end - beg);
+    const int KK = g.KH * g.KW;
+    const int c = lane < n ? __ldg(col_idx + beg + lane) : 0;
+    const int ic_l = c / KK, rem = c - ic_l * KK;
+    const int x_l = rem / g.KW, y_l = rem - (rem / g.KW) * g.KW;
+    const bool vec_ok = (g.B % VEC) == 0;
+
+    float acc[32];
+#pragma unroll
+    for (int t = 0; t < 32; ++t) acc[t] = 0.f;
+
+    for (int p = 0; p < g.OH; ++p) {
+        for (int q = 0; q < g.OW; ++q) {
+            const float *dsrc = dY + (((int64_t)oc * g.OH + p) * g.OW + q) * g.B;
+            for (int b0 = 0; b0 < g.B; b0 += 32 * VEC) {
+                const int b = b0 + lane * VEC;
+                const int nvalid = min(VEC, max(0, g.B - b));
+                float dv[VEC];
+                ldg_vec<VEC>(dsrc + b, dv, vec_ok, nvalid);
+#pragma unroll
+                for (int t = 0; t < 32; ++t) {
+                    const int ic = __shfl_sync(kFull, ic_l, t);
+                    const int ih = p + __shfl_sync(kFull, x_l, t) - g.pad;
+                    const int iw = q + __shfl_sync(kFull, y_l, t) - g.pad;
+                    if (t < n && ih >= 0 && ih < g.H && iw >= 0 && iw < g.W) {
+                        float xv[VEC];
+                        ldg_vec<VEC>(X + (((int64_t)ic * g.H + ih) * g.W + iw) * g.B + b, xv,
+                                     vec_ok, nvalid);
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) acc[t] = fmaf(dv[v], xv[v], acc[t]);
+                    }
+                }
+            }
+        }
+    }
+    const float s = transpose_reduce32(acc, lane);
+    if (lane < n) dW[beg + lane] = s;
+}
+
+Geo mk(const sp_conv_geom &c) {
+    Geo g;
+    g.B = c.B;
+    g.IC = c.C_in;
+    g.H = c.H;
+    g.W = c.W;
+    g.OC = c.C_out;
+    g.KH = c.KH;
+    g.KW = c.KW;
+    g.pad = c.pad;
+    g.OH = c.H + 2 * c.pad - c.KH + 1;
+    g.OW = c.W + 2 * c.pad - c.KW + 1;
+    return g;
+}
+
+constexpr int QC = 8;
+
+}  // namespace
+
+void launch_conv_fwd(const sp_weight_s *w, const sp_conv_geom &cg, const float *X, float *Y,
+                     cudaStream_t st) {
+    const Geo g = mk(cg);
+    const int nqc = (g.OW + QC - 1) / QC;
+    auto go = [&](auto kern, int vec) {
+        const int64_t nbc = (g.B + 32 * vec - 1) / (32 * vec);
+        const int64_t warps = (int64_t)g.OC * g.OH * nqc * nbc;
+        count_launches(1);
+        kern<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(g, nqc, w->row_ptr, w->col_idx, w->vals, X, Y);
+    };
+    if (g.B <= 32) go(conv_fwd_kernel<1, QC>, 1);
+    else if (g.B <= 64 || (g.B & 3)) go(conv_fwd_kernel<2, QC>, 2);
+    else go(conv_fwd_kernel<4, QC>, 4);
+}
+
+void launch_conv_bwd_input(const sp_weight_s *w, const sp_conv_geom &cg, const float *dY, float *dX,
+                           cudaStream_t st) {
+    const Geo g = mk(cg);
+    const int nqc = (g.W + QC - 1) / QC;
+    auto go = [&](auto kern, int vec) {
+        const int64_t nbc = (g.B + 32 * vec - 1) / (32 * vec);
+        const int64_t warps = (int64_t)g.IC * g.H * nqc * nbc;
+        count_launches(1);
+        kern<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(g, nqc, w->col_ptr, w->row_idx, w->perm,
+                                                          w->vals, dY, dX);
+    };
+    if (g.B <= 32) go(conv_dx_kernel<1, QC>, 1);
+    else if (g.B <= 64 || (g.B & 3)) go(conv_dx_kernel<2, QC>, 2);
+    else go(conv_dx_kernel<4, QC>, 4);
+}
+
+sp_status launch_conv_bwd_weight(const sp_weight_s *w, const sp_conv_geom &cg, const float *X,
+                                 const float *dY, float *dW, cudaStream_t st) {
+    const Geo g = mk(cg);
+    if (w->nnz == 0) return SP_OK;
+    const int gpr = (w->max_row_nnz + 31) / 32;
+    const int64_t warps = (int64_t)g.OC * gpr;
+    auto go = [&](auto kern) {
+        count_launches(1);
+        kern<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(g, gpr, w->row_ptr, w->col_idx, X, dY, dW);
+    };
+    if (g.B <= 32) go(conv_dw_kernel<1>);
+    else if (g.B <= 64 || (g.B & 3)) go(conv_dw_kernel<2>);
+    else go(conv_dw_kernel<4>);
+    return SP_OK;
+}
+
+}  // namespace sp

@@ -1,0 +1,91 @@
+// tile.cuh -- shared-memory staging of a dense activation tile and warp
+// helpers used by the SpMM and SDDMM kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sp {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+template <int VEC>
+struct VecT;
+template <>
+struct VecT<1> {
+    using T = float;
+};
+template <>
+struct VecT<2> {
+    using T = float2;
+};
+template <>
+struct VecT<4> {
+    using T = float4;
+};
+
+template <int VEC>
+__device__ __forceinline__ void lds_vec(const float *p, float (&v)[VEC]) {
+    if constexpr (VEC == 1) {
+        v[0] = *p;
+    } else if constexpr (VEC == 2) {
+        float2 t = *reinterpret_cast<const float2 *>(p);
+        v[0] = t.x;
+        v[1] = t.y;
+    } else {
+        float4 t = *reinterpret_cast<const float4 *>(p);
+        v[0] = t.x;
+        v[1] = t.y;
+        v[2] = t.z;
+        v[3] = t.w;
+    }
+}
+
+// Stage rows [k0, k0+nk) x batch columns [b0, b0+BT) of a row-major
+// [nrows x B] fp32 activation into smem tile[nk][BT] (row stride BT),
+// zero-filling batch columns >= B.  16-byte vector path when B % 4 == 0.
+template <int BT, int NT>
+__device__ __forceinline__ void stage_tile(float *__restrict__ tile, const float *__restrict__ src,
+                                           int64_t k0, int nk, int64_t B, int64_t b0, bool vec4) {
+    constexpr int Q = BT / 4;  // float4 chunks per tile row (BT >= 32)
+    const int total = nk * Q;
+    if (vec4) {
+        for (int i = threadIdx.x; i < total; i += NT) {
+            const int k = i / Q, q = (i - k * Q) * 4;
+            const int64_t b = b0 + q;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (b < B) v = __ldg(reinterpret_cast<const float4 *>(src + (k0 + k) * B + b));
+            *reinterpret_cast<float4 *>(tile + k * BT + q) = v;
+        }
+    } else {
+        for (int i = threadIdx.x; i < total; i += NT) {
+            const int k = i / Q, q = (i - k * Q) * 4;
+            const int64_t b = b0 + q;
+            const float *s = src + (k0 + k) * B + b;
+            float4 v;
+            v.x = b + 0 < B ? __ldg(s + 0) : 0.f;
+            v.y = b + 1 < B ? __ldg(s + 1) : 0.f;
+            v.z = b + 2 < B ? __ldg(s + 2) : 0.f;
+            v.w = b + 3 < B ? __ldg(s + 3) : 0.f;
+            *reinterpret_cast<float4 *>(tile + k * BT + q) = v;
+        }
+    }
+}
+
+// Warp transpose-reduce of 32 per-lane partials: on return, lane t holds
+// sum over lanes of acc[t] (in acc[0]).  31 shuffles for 32 sums.
+__device__ __forceinline__ float transpose_reduce32(float (&acc)[32], int lane) {
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const bool up = (lane & s) != 0;
+#pragma unroll
+        for (int i = 0; i < s; ++i) {
+            const float send = up ? acc[i] : acc[i + s];
+            const float keep = up ? acc[i + s] : acc[i];
+            acc[i] = keep + __shfl_xor_sync(kFull, send, s);
+        }
+    }
+    return acc[0];
+}
+
+}  // namespace sp

@@ -1,0 +1,183 @@
+"""Data-parallel sparse MLP step (north star cfg5).
+
+`blocks` x [W1 (d_ff x d_model) sparse, ReLU, W2 (d_model x d_ff) sparse],
+MSE loss L = 1/2 sum (Y - T)^2.  One process per GPU; rank g
+owns the contiguous token shard [g T/G, (g+1) T/G) as its own [feat x T/G]
+buffers.  The only exchange is an all_reduce(SUM) of the nnz-length dW value
+buffers (one flat buffer, bucketed in reverse layer order and launched on a
+side stream as soon as a bucket's SDDMMs are done, overlapping the rest of the
+backward).  Then plain SGD on the kept weights.
+
+Every arithmetic step runs in libsparseprop's kernels (fwd SpMM + fused ReLU,
+CSC-driven dX SpMM + fused ReLU' gate, SDDMM, MSE, SGD).  The `ops` object is
+the only thing this module calls for arithmetic; `CudaOps` is the product.
+Tests substitute a CPU oracle-backed `ops` to exercise the sharding /
+bucketing / all_reduce logic with gloo on CPU (tests/test_dp_gloo.py).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+class CudaOps:
+    """The product arithmetic: libsparseprop through its C ABI."""
+
+    def __init__(self):
+        from . import sparseprop as sp
+        self.sp = sp
+        sp.lib()
+
+    def create(self, dense, mask):
+        return self.sp.sp_weight_create(dense, mask)
+
+    def vals(self, W):
+        return W.vals
+
+    def fwd(self, W, X, Y, relu):
+        return self.sp.sp_linear_fwd(W, X, Y, relu=relu)
+
+    def dx(self, W, dY, dX, H=None):
+        return self.sp.sp_linear_bwd_input(W, dY, dX, H=H)
+
+    def dw(self, W, X, dY, dW):
+        return self.sp.sp_linear_bwd_weight(W, X, dY, dW)
+
+    def mse(self, Y, T, dY, loss, scratch):
+        self.sp.sp_mse_grad(Y, T, dY, loss, scratch)
+
+    def mse_scratch(self, n):
+        return self.sp.sp_mse_scratch_floats(n)
+
+    def sgd(self, vals, dW, lr):
+        self.sp.sp_sgd(vals, dW, lr)
+
+
+class SparseMLP:
+    """cfg5 model state + one training step on this rank's token shard."""
+
+    def __init__(self, layers, T_local: int, device, ops=None, group=None, bucket_blocks: int = 3,
+                 keep_dx0: bool = True):
+        """layers: list of (w1, m1, w2, m2) host arrays (synth.mlp_case)."""
+        self.ops = ops if ops is not None else CudaOps()
+        self.device = torch.device(device)
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+        self.blocks = len(layers)
+        self.d_model = layers[0][0].shape[1]
+        self.d_ff = layers[0][0].shape[0]
+        self.T = T_local
+        self.keep_dx0 = keep_dx0
+        f32 = dict(dtype=torch.float32, device=self.device)
+        self.W = []
+        for (w1, m1, w2, m2) in layers:
+            W1 = self.ops.create(torch.as_tensor(w1).to(self.device), torch.as_tensor(m1).to(self.device))
+            W2 = self.ops.create(torch.as_tensor(w2).to(self.device), torch.as_tensor(m2).to(self.device))
+            self.W.append((W1, W2))
+        # one flat dW buffer; per-layer views; buckets in reverse block order
+        sizes = [(W1.nnz, W2.nnz) for (W1, W2) in self.W]
+        self.nnz_total = sum(a + b for a, b in sizes)
+        self.dW_flat = torch.zeros(self.nnz_total, **f32)
+        self.dW = []
+        off = 0
+        self.block_range = []
+        for (a, b) in sizes:
+            self.dW.append((self.dW_flat[off:off + a], self.dW_flat[off + a:off + a + b]))
+            self.block_range.append((off, off + a + b))
+            off += a + b
+        self.buckets = []  # (first_block, last_block, lo, hi); launched when first_block's dW done
+        l = self.blocks - 1
+        while l >= 0:
+            first = max(0, l - bucket_blocks + 1)
+            self.buckets.append((first, l, self.block_range[first][0], self.block_range[l][1]))
+            l = first - 1
+        # activations: X_l [d_model x T] (l = 0..blocks), H_l [d_ff x T]
+        self.X = [torch.empty(self.d_model, T_local, **f32) for _ in range(self.blocks + 1)]
+        self.H = [torch.empty(self.d_ff, T_local, **f32) for _ in range(self.blocks)]
+        self.dY = torch.empty(self.d_model, T_local, **f32)
+        self.dYb = torch.empty(self.d_model, T_local, **f32)
+        self.dZ = torch.empty(self.d_ff, T_local, **f32)
+        self.dX0 = torch.empty(self.d_model, T_local, **f32)
+        self.target = torch.empty(self.d_model, T_local, **f32)
+        self.loss = torch.zeros(1, **f32)
+        self.mse_scratch = torch.empty(max(2, self.ops.mse_scratch(self.d_model * T_local)), **f32)
+        self.is_cuda = self.device.type == "cuda"
+        self.comm_stream = torch.cuda.Stream(device=self.device) if (self.is_cuda and self.world > 1) else None
+
+    # ------------------------------------------------------------------
+    def set_batch(self, X0: torch.Tensor, target: torch.Tensor, non_blocking: bool = True):
+        """Copy this rank's shard (host pinned or device) into the resident buffers."""
+        self.X[0].copy_(X0, non_blocking=non_blocking)
+        self.target.copy_(target, non_blocking=non_blocking)
+
+    def forward(self):
+        ops = self.ops
+        for l, (W1, W2) in enumerate(self.W):
+            ops.fwd(W1, self.X[l], self.H[l], relu=True)          # H = max(W1 X, 0)
+            ops.fwd(W2, self.H[l], self.X[l + 1], relu=False)     # X' = W2 H
+        ops.mse(self.X[self.blocks], self.target, self.dY, self.loss, self.mse_scratch)
+        return self.loss
+
+    def backward(self, allreduce: bool = True):
+        ops = self.ops
+        comm = allreduce and self.world > 1
+        pending = []
+        bi = 0
+        dY, dYn = self.dY, self.dYb
+        for l in range(self.blocks - 1, -1, -1):
+            W1, W2 = self.W[l]
+            dW1, dW2 = self.dW[l]
+            ops.dw(W2, self.H[l], dY, dW2)                        # dW2 = SDDMM(dY, H)
+            ops.dx(W2, dY, self.dZ, H=self.H[l])                  # dZ = (W2^T dY) * [H > 0]
+            ops.dw(W1, self.X[l], self.dZ, dW1)                   # dW1 = SDDMM(dZ, X)
+            if l > 0 or self.keep_dx0:
+                out = self.dX0 if l == 0 else dYn
+                ops.dx(W1, self.dZ, out)                          # dX = W1^T dZ
+                if l > 0:
+                    dY, dYn = dYn, dY
+            if comm and bi < len(self.buckets) and self.buckets[bi][0] == l:
+                lo, hi = self.buckets[bi][2], self.buckets[bi][3]
+                pending.append(self._launch_allreduce(self.dW_flat[lo:hi]))
+                bi += 1
+        if comm:
+            self._wait(pending)
+
+    def _launch_allreduce(self, buf):
+        if self.comm_stream is not None:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(self.device))
+            self.comm_stream.wait_event(ev)
+            with torch.cuda.stream(self.comm_stream):
+                dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
+            return None
+        return dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+
+    def _wait(self, pending):
+        if self.comm_stream is not None:
+            torch.cuda.current_stream(self.device).wait_stream(self.comm_stream)
+        else:
+            for w in pending:
+                if w is not None:
+                    w.wait()
+
+    def sgd(self, lr: float):
+        for (W1, W2), (d1, d2) in zip(self.W, self.dW):
+            self.ops.sgd(self.ops.vals(W1), d1, lr)
+            self.ops.sgd(self.ops.vals(W2), d2, lr)
+
+    def step(self, lr: float, allreduce: bool = True):
+        """forward -> loss -> backward (+ bucketed all_reduce of dW) -> SGD.
+        Returns the (device) local loss tensor."""
+        loss = self.forward()
+        self.backward(allreduce=allreduce)
+        self.sgd(lr)
+        return loss
+
+    def step_flops(self) -> int:
+        """Effective FLOPs of one step on this rank: 2*nnz*B per product
+        (BASELINE metric): 3 products per layer (fwd, dX, dW),
+        minus the first layer's dX when it is not kept."""
+        total = sum(3 * 2 * (W1.nnz + W2.nnz) * self.T for (W1, W2) in self.W)
+        if not self.keep_dx0:
+            total -= 2 * self.W[0][0].nnz * self.T
+        return total

@@ -1,0 +1,325 @@
+"""Thin ctypes binding of libsparseprop (include/sparseprop.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels of csrc/.  Tensors are torch CUDA tensors (fp32 / uint8 / int32,
+contiguous); streams default to torch's current stream.  There is NO CPU
+fallback: without the built library or a CUDA device every call raises.
+
+Function names are the C names; `SparseWeight` is a convenience owner of an
+sp_weight_t handle.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsparseprop.so")
+
+SP_STATUS = {0: "SP_OK", 1: "SP_ERR_NULL", 2: "SP_ERR_SHAPE", 3: "SP_ERR_OVERFLOW",
+             4: "SP_ERR_ALLOC", 5: "SP_ERR_CUDA", 6: "SP_ERR_BAD_HANDLE"}
+
+# every symbol include/sparseprop.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "sp_weight_create", "sp_weight_destroy", "sp_weight_nnz", "sp_weight_rows", "sp_weight_cols",
+    "sp_weight_vals", "sp_weight_indices", "sp_weight_to_dense", "sp_linear_fwd",
+    "sp_linear_bwd_input", "sp_linear_bwd_weight", "sp_linear_fwd_relu",
+    "sp_linear_bwd_input_relu", "sp_conv2d_fwd", "sp_conv2d_bwd_input", "sp_conv2d_bwd_weight",
+    "sp_mse_scratch_floats", "sp_mse_grad", "sp_sgd", "sp_last_error", "sp_version",
+    "sp_launch_count",
+]
+
+
+class SparsePropError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{SP_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class sp_conv_geom(ct.Structure):
+    _fields_ = [(n, ct.c_int32) for n in ("B", "C_in", "H", "W", "C_out", "KH", "KW", "pad")]
+
+
+_lib = None
+
+
+def lib() -> ct.CDLL:
+    """Load libsparseprop.so (built by __graft_entry__.build()); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; "
+                              "g.build()'` (no CPU fallback exists)")
+        L = ct.CDLL(LIB_PATH)
+        vp, i64, st = ct.c_void_p, ct.c_int64, ct.c_int
+        sig = {
+            "sp_weight_create": (st, [i64, i64, vp, vp, vp, ct.POINTER(vp)]),
+            "sp_weight_destroy": (st, [vp, vp]),
+            "sp_weight_nnz": (i64, [vp]), "sp_weight_rows": (i64, [vp]), "sp_weight_cols": (i64, [vp]),
+            "sp_weight_vals": (st, [vp, ct.POINTER(vp)]),
+            "sp_weight_indices": (st, [vp] + [ct.POINTER(vp)] * 5),
+            "sp_weight_to_dense": (st, [vp, vp, vp, vp]),
+            "sp_linear_fwd": (st, [vp, vp, vp, i64, vp]),
+            "sp_linear_fwd_relu": (st, [vp, vp, vp, i64, vp]),
+            "sp_linear_bwd_input": (st, [vp, vp, vp, i64, vp]),
+            "sp_linear_bwd_input_relu": (st, [vp, vp, vp, vp, i64, vp]),
+            "sp_linear_bwd_weight": (st, [vp, vp, vp, vp, i64, vp]),
+            "sp_conv2d_fwd": (st, [vp, ct.POINTER(sp_conv_geom), vp, vp, vp]),
+            "sp_conv2d_bwd_input": (st, [vp, ct.POINTER(sp_conv_geom), vp, vp, vp]),
+            "sp_conv2d_bwd_weight": (st, [vp, ct.POINTER(sp_conv_geom), vp, vp, vp, vp]),
+            "sp_mse_scratch_floats": (i64, [i64]),
+            "sp_mse_grad": (st, [vp, vp, vp, vp, vp, i64, vp]),
+            "sp_sgd": (st, [vp, vp, i64, ct.c_float, vp]),
+            "sp_last_error": (ct.c_char_p, []),
+            "sp_version": (ct.c_char_p, []),
+            "sp_launch_count": (ct.c_uint64, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise SparsePropError(status, lib().sp_last_error().decode())
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if isinstance(stream, torch.cuda.Stream) else int(stream)
+
+
+def _dev(t: torch.Tensor, dtype, name: str) -> int:
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name}: expected a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name}: must be a CUDA tensor (libsparseprop has no CPU path)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    return t.data_ptr()
+
+
+def version() -> str:
+    return lib().sp_version().decode()
+
+
+def launch_count() -> int:
+    """Kernels launched by libsparseprop so far in this process."""
+    return int(lib().sp_launch_count())
+
+
+class SparseWeight:
+    """Owner of an sp_weight_t: CSR + CSC index copy + vals, all on the device."""
+
+    def __init__(self, dense: torch.Tensor, mask: torch.Tensor, stream=None):
+        if dense.dim() == 4:  # conv filter [OC][IC][KH][KW]
+            self.filter_shape = tuple(dense.shape)
+            dense = dense.reshape(dense.shape[0], -1)
+            mask = mask.reshape(mask.shape[0], -1)
+        else:
+            self.filter_shape = None
+        if dense.dim() != 2 or dense.shape != mask.shape:
+            raise ValueError("dense and mask must be R x C (or matching 4-D conv filters)")
+        R, C = dense.shape
+        h = ct.c_void_p()
+        _check(lib().sp_weight_create(R, C, _dev(dense.contiguous(), torch.float32, "dense"),
+                                      _dev(mask.contiguous(), torch.uint8, "mask"), _stream(stream),
+                                      ct.byref(h)))
+        self.handle = h
+        self.R, self.C = int(R), int(C)
+        self.nnz = int(lib().sp_weight_nnz(h))
+        self.device = dense.device
+        p = ct.c_void_p()
+        _check(lib().sp_weight_vals(h, ct.byref(p)))
+        self._vals_ptr = p.value
+
+    # -- zero-copy views of the handle-owned device buffers ------------------
+    def _view(self, ptr: int, n: int, dtype) -> torch.Tensor:
+        if n == 0:
+            return torch.empty(0, dtype=dtype, device=self.device)
+        typestr = {torch.float32: "<f4", torch.int32: "<i4"}[dtype]
+
+        class _CAI:
+            __cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                        "version": 3, "strides": None, "stream": None}
+        t = torch.as_tensor(_CAI(), device=self.device)
+        t._sp_owner = self  # keep the handle alive while the view lives
+        return t
+
+    @property
+    def vals(self) -> torch.Tensor:
+        """Mutable fp32 view of vals[nnz] (CSR order), zero-copy."""
+        if getattr(self, "_vals_t", None) is None:
+            self._vals_t = self._view(self._vals_ptr, self.nnz, torch.float32)
+        return self._vals_t
+
+    def indices(self) -> dict:
+        ps = [ct.c_void_p() for _ in range(5)]
+        _check(lib().sp_weight_indices(self.handle, *[ct.byref(p) for p in ps]))
+        names = ["row_ptr", "col_idx", "col_ptr", "row_idx", "perm"]
+        sizes = [self.R + 1, self.nnz, self.C + 1, self.nnz, self.nnz]
+        return {n: self._view(p.value, s, torch.int32) for n, p, s in zip(names, ps, sizes)}
+
+    def to_dense(self, nz: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        nz = self.vals if nz is None else nz
+        out = torch.empty(self.R, self.C, dtype=torch.float32, device=self.device)
+        sp_weight_to_dense(self, nz, out, stream)
+        return out
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            lib().sp_weight_destroy(self.handle, _stream(None))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------
+# C-named wrappers (argument marshalling only)
+# ---------------------------------------------------------------------------
+def sp_weight_create(dense: torch.Tensor, mask: torch.Tensor, stream=None) -> SparseWeight:
+    return SparseWeight(dense, mask, stream)
+
+
+def sp_weight_to_dense(W: SparseWeight, nz: torch.Tensor, out: torch.Tensor, stream=None):
+    _check(lib().sp_weight_to_dense(W.handle, _dev(nz, torch.float32, "nz") if W.nnz else None,
+                                    _dev(out, torch.float32, "out"), _stream(stream)))
+    return out
+
+
+def _B(t: torch.Tensor, rows: int, name: str) -> int:
+    if t.dim() != 2 or t.shape[0] != rows:
+        raise ValueError(f"{name}: expected [{rows} x B], got {tuple(t.shape)}")
+    return int(t.shape[1])
+
+
+def sp_linear_fwd(W: SparseWeight, X: torch.Tensor, Y: torch.Tensor | None = None, stream=None,
+                  relu: bool = False) -> torch.Tensor:
+    B = _B(X, W.C, "X")
+    if Y is None:
+        Y = torch.empty(W.R, B, dtype=torch.float32, device=X.device)
+    _B(Y, W.R, "Y")
+    f = lib().sp_linear_fwd_relu if relu else lib().sp_linear_fwd
+    _check(f(W.handle, _dev(X, torch.float32, "X"), _dev(Y, torch.float32, "Y"), B, _stream(stream)))
+    return Y
+
+
+def sp_linear_fwd_relu(W, X, Y=None, stream=None):
+    return sp_linear_fwd(W, X, Y, stream, relu=True)
+
+
+def sp_linear_bwd_input(W: SparseWeight, dY: torch.Tensor, dX: torch.Tensor | None = None,
+                        stream=None, H: torch.Tensor | None = None) -> torch.Tensor:
+    B = _B(dY, W.R, "dY")
+    if dX is None:
+        dX = torch.empty(W.C, B, dtype=torch.float32, device=dY.device)
+    _B(dX, W.C, "dX")
+    if H is None:
+        _check(lib().sp_linear_bwd_input(W.handle, _dev(dY, torch.float32, "dY"),
+                                         _dev(dX, torch.float32, "dX"), B, _stream(stream)))
+    else:
+        _B(H, W.C, "H")
+        _check(lib().sp_linear_bwd_input_relu(W.handle, _dev(dY, torch.float32, "dY"),
+                                              _dev(H, torch.float32, "H"),
+                                              _dev(dX, torch.float32, "dX"), B, _stream(stream)))
+    return dX
+
+
+def sp_linear_bwd_input_relu(W, dY, H, dX=None, stream=None):
+    return sp_linear_bwd_input(W, dY, dX, stream, H=H)
+
+
+def sp_linear_bwd_weight(W: SparseWeight, X: torch.Tensor, dY: torch.Tensor,
+                         dW: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    B = _B(X, W.C, "X")
+    if _B(dY, W.R, "dY") != B:
+        raise ValueError("X and dY batch sizes differ")
+    if dW is None:
+        dW = torch.empty(W.nnz, dtype=torch.float32, device=X.device)
+    if dW.numel() != W.nnz:
+        raise ValueError("dW must have nnz elements")
+    _check(lib().sp_linear_bwd_weight(W.handle, _dev(X, torch.float32, "X"),
+                                      _dev(dY, torch.float32, "dY"),
+                                      _dev(dW, torch.float32, "dW") if W.nnz else None, B,
+                                      _stream(stream)))
+    return dW
+
+
+def conv_geom(W: SparseWeight, B: int, H: int, Wd: int, pad: int) -> sp_conv_geom:
+    if W.filter_shape is None:
+        raise ValueError("handle was not created from a 4-D conv filter")
+    OC, IC, KH, KW = W.filter_shape
+    return sp_conv_geom(B, IC, H, Wd, OC, KH, KW, pad)
+
+
+def _geo_out(g: sp_conv_geom):
+    return g.H + 2 * g.pad - g.KH + 1, g.W + 2 * g.pad - g.KW + 1
+
+
+def sp_conv2d_fwd(W: SparseWeight, g: sp_conv_geom, X: torch.Tensor, Y: torch.Tensor | None = None,
+                  stream=None) -> torch.Tensor:
+    OH, OW = _geo_out(g)
+    if tuple(X.shape) != (g.C_in, g.H, g.W, g.B):
+        raise ValueError("X must be CHWN [C_in][H][W][B]")
+    if Y is None:
+        Y = torch.empty(g.C_out, OH, OW, g.B, dtype=torch.float32, device=X.device)
+    _check(lib().sp_conv2d_fwd(W.handle, ct.byref(g), _dev(X, torch.float32, "X"),
+                               _dev(Y, torch.float32, "Y"), _stream(stream)))
+    return Y
+
+
+def sp_conv2d_bwd_input(W: SparseWeight, g: sp_conv_geom, dY: torch.Tensor,
+                        dX: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    OH, OW = _geo_out(g)
+    if tuple(dY.shape) != (g.C_out, OH, OW, g.B):
+        raise ValueError("dY must be CHWN [C_out][OH][OW][B]")
+    if dX is None:
+        dX = torch.empty(g.C_in, g.H, g.W, g.B, dtype=torch.float32, device=dY.device)
+    _check(lib().sp_conv2d_bwd_input(W.handle, ct.byref(g), _dev(dY, torch.float32, "dY"),
+                                     _dev(dX, torch.float32, "dX"), _stream(stream)))
+    return dX
+
+
+def sp_conv2d_bwd_weight(W: SparseWeight, g: sp_conv_geom, X: torch.Tensor, dY: torch.Tensor,
+                         dW: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    if dW is None:
+        dW = torch.empty(W.nnz, dtype=torch.float32, device=X.device)
+    _check(lib().sp_conv2d_bwd_weight(W.handle, ct.byref(g), _dev(X, torch.float32, "X"),
+                                      _dev(dY, torch.float32, "dY"),
+                                      _dev(dW, torch.float32, "dW") if W.nnz else None,
+                                      _stream(stream)))
+    return dW
+
+
+def sp_mse_scratch_floats(n: int) -> int:
+    return int(lib().sp_mse_scratch_floats(n))
+
+
+def sp_mse_grad(Y: torch.Tensor, T: torch.Tensor, dY: torch.Tensor, loss: torch.Tensor,
+                scratch: torch.Tensor, stream=None):
+    n = Y.numel()
+    if T.numel() != n or dY.numel() != n:
+        raise ValueError("Y, T, dY sizes differ")
+    _check(lib().sp_mse_grad(_dev(Y, torch.float32, "Y"), _dev(T, torch.float32, "T"),
+                             _dev(dY, torch.float32, "dY"), _dev(loss, torch.float32, "loss"),
+                             _dev(scratch, torch.float32, "scratch"), n, _stream(stream)))
+
+
+def sp_sgd(vals: torch.Tensor, dW: torch.Tensor, lr: float, stream=None):
+    n = vals.numel()
+    if dW.numel() != n:
+        raise ValueError("vals and dW sizes differ")
+    _check(lib().sp_sgd(_dev(vals, torch.float32, "vals") if n else None,
+                        _dev(dW, torch.float32, "dW") if n else None, n, ct.c_float(lr),
+                        _stream(stream)))

@@ -1,0 +1,73 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every
+symbol include/sparseprop.h declares, and validates arguments before any
+launch (no compute call is made here)."""
+import ctypes as ct
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "sparseprop.h")
+
+
+def _declared():
+    src = open(HDR).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sp_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2302_04852_b200 import _build, sparseprop
+    _build.build()
+    return sparseprop.lib()
+
+
+def test_header_lists_the_north_star_entry_points():
+    names = _declared()
+    for n in ["sp_weight_create", "sp_linear_fwd", "sp_linear_bwd_input", "sp_linear_bwd_weight",
+              "sp_conv2d_fwd", "sp_conv2d_bwd_input", "sp_conv2d_bwd_weight"]:
+        assert n in names
+
+
+def test_every_declared_symbol_is_exported(L):
+    from paper_2302_04852_b200 import sparseprop
+    out = subprocess.check_output(["nm", "-D", "--defined-only", sparseprop.LIB_PATH], text=True)
+    exported = set(re.findall(r"\bT (sp_[a-z0-9_]+)", out))
+    missing = [n for n in _declared() if n not in exported]
+    assert not missing, missing
+    assert sorted(sparseprop.EXPORTS) == _declared()
+
+
+def test_built_for_sm100a(L):
+    from paper_2302_04852_b200 import sparseprop
+    out = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "--list-elf", sparseprop.LIB_PATH],
+                                  text=True)
+    assert "sm_100a" in out
+
+
+def test_argument_validation_without_gpu(L):
+    from paper_2302_04852_b200 import sparseprop as sp
+    h = ct.c_void_p()
+    assert L.sp_weight_create(4, 4, None, None, None, ct.byref(h)) == 1          # SP_ERR_NULL
+    assert "NULL" in L.sp_last_error().decode()
+    assert L.sp_weight_create(0, 4, 1, 1, None, ct.byref(h)) == 2                # SP_ERR_SHAPE
+    assert L.sp_weight_create(1 << 20, 1 << 20, 1, 1, None, ct.byref(h)) == 3    # SP_ERR_OVERFLOW
+    assert L.sp_weight_create(4, 4, 1, 1, None, None) == 1
+    assert L.sp_linear_fwd(None, 1, 1, 8, None) == 6                              # SP_ERR_BAD_HANDLE
+    assert L.sp_linear_bwd_input(None, 1, 1, 8, None) == 6
+    assert L.sp_linear_bwd_weight(None, 1, 1, 1, 8, None) == 6
+    assert L.sp_conv2d_fwd(None, None, 1, 1, None) == 6
+    assert L.sp_weight_nnz(None) == -1
+    assert L.sp_sgd(None, None, 5, ct.c_float(0.1), None) == 1
+    assert L.sp_mse_grad(None, None, None, None, None, 5, None) == 1
+    assert "sm_100a" in sp.version()
+
+
+def test_binding_refuses_cpu_tensors(L):
+    torch = pytest.importorskip("torch")
+    from paper_2302_04852_b200 import sparseprop as sp
+    with pytest.raises(ValueError, match="CUDA"):
+        sp.sp_weight_create(torch.zeros(4, 4), torch.zeros(4, 4, dtype=torch.uint8))

@@ -1,0 +1,235 @@
+"""GPU parity: libsparseprop (through its C ABI) vs the fp64 oracle on the same
+seeded inputs.  Index structure bit-exact; fp32 values within the north-star
+bar max|err| <= 1e-4 * max|ref| + 1e-6 per output tensor."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from conftest import tol_ok
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+NT = min(8, oracle.threads_available())
+
+
+@pytest.fixture(scope="module")
+def sp():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    from paper_2302_04852_b200 import _build, sparseprop
+    _build.build()
+    return sparseprop
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _assert_tol(name, got, ref):
+    ok, err, bound = tol_ok(got, ref)
+    assert ok, f"{name}: max|err| {err:.3e} > bound {bound:.3e}"
+
+
+def check_linear(sp, W, mask, X, dY, tag=""):
+    """Run fwd / dX / dW on the GPU and compare everything with the oracle."""
+    Wg = sp.sp_weight_create(_dev(W), _dev(mask))
+    Xg, dYg = _dev(X), _dev(dY)
+    Y = sp.sp_linear_fwd(Wg, Xg)
+    dX = sp.sp_linear_bwd_input(Wg, dYg)
+    dW = sp.sp_linear_bwd_weight(Wg, Xg, dYg)
+    torch.cuda.synchronize()
+    S = oracle.csr_from_mask(W, mask)
+    idx = {k: _np(v) for k, v in Wg.indices().items()}
+    # structure: bit-exact
+    assert Wg.nnz == S.nnz, tag
+    for k, ref in (("row_ptr", S.row_ptr), ("col_idx", S.col_idx), ("col_ptr", S.col_ptr),
+                   ("row_idx", S.row_idx), ("perm", S.perm)):
+        assert np.array_equal(idx[k], ref), f"{tag} {k}"
+    assert np.array_equal(_np(Wg.vals), S.vals.astype(np.float32)), tag
+    if S.nnz:
+        ones = sp.sp_weight_to_dense(Wg, torch.ones(S.nnz, device="cuda"),
+                                     torch.empty(W.shape, device="cuda"))
+        assert np.array_equal(_np(ones) != 0, mask != 0), tag
+    # values
+    _assert_tol(f"{tag} Y", _np(Y), oracle.linear_fwd(S, X, NT))
+    _assert_tol(f"{tag} dX", _np(dX), oracle.linear_bwd_input(S, dY, NT))
+    refW = oracle.linear_bwd_weight(S, X, dY, NT)
+    _assert_tol(f"{tag} dW", _np(dW), refW)
+    # densified dW: exactly +0.0 off the mask
+    if S.nnz:
+        D = _np(Wg.to_dense(dW))
+        off = D[mask == 0]
+        assert np.all(off == 0.0) and not np.any(np.signbit(off)), tag
+    return Wg, Y, dX, dW
+
+
+# ---------------------------------------------------------------- configs
+def test_cfg1(sp):
+    c = synth.linear_case(**synth.CFG["cfg1"])
+    check_linear(sp, c["W"], c["mask"], c["X"], c["dY"], "cfg1")
+
+
+@pytest.mark.parametrize("name", ["cfg2a", "cfg2b"])
+def test_cfg2(sp, name):
+    c = synth.linear_case(**synth.CFG[name])
+    check_linear(sp, c["W"], c["mask"], c["X"], c["dY"], name)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "zipf"])
+@pytest.mark.parametrize("sparsity", synth.CFG4_SPARSITIES)
+def test_cfg4(sp, sparsity, kind):
+    cfg = synth.cfg4(sparsity, kind)
+    c = synth.linear_case(cfg["R"], cfg["C"], cfg["B"], cfg["density"], cfg["wvar"], cfg["seed"], kind)
+    check_linear(sp, c["W"], c["mask"], c["X"], c["dY"], f"cfg4 {kind} {sparsity}")
+
+
+def test_paper_shape_B902(sp):
+    # P366: (M,N) = (768, 3072), (B,M) = (902, 768); B not a multiple of 4 (S75)
+    c = synth.linear_case(3072, 768, 902, 0.1, 1.0 / 768, 990)
+    check_linear(sp, c["W"], c["mask"], c["X"], c["dY"], "paper B=902")
+
+
+# ---------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("R,C,B,d", [
+    (1, 1, 1, 1.0), (1, 7, 3, 0.5), (7, 1, 5, 0.5), (37, 53, 1, 0.2), (64, 48, 33, 0.15),
+    (200, 130, 3, 0.05), (129, 257, 67, 0.3), (300, 41, 130, 0.5), (96, 1500, 9, 0.02),
+    (1200, 64, 200, 0.01), (40, 40, 1024, 1.0)])
+def test_ragged_shapes(sp, R, C, B, d):
+    c = synth.linear_case(R, C, B, d, 1.0 / C, R * 1000 + C * 10 + B)
+    check_linear(sp, c["W"], c["mask"], c["X"], c["dY"], f"{R}x{C} B={B}")
+
+
+def test_empty_mask(sp):
+    g = synth.rng(5)
+    W = synth.normal(g, (33, 17), 1.0)
+    X = synth.normal(g, (17, 40), 1.0)
+    dY = synth.normal(g, (33, 40), 1.0)
+    Wg = sp.sp_weight_create(_dev(W), _dev(np.zeros((33, 17), np.uint8)))
+    assert Wg.nnz == 0
+    Y = sp.sp_linear_fwd(Wg, _dev(X), torch.full((33, 40), 7.0, device="cuda"))
+    dX = sp.sp_linear_bwd_input(Wg, _dev(dY), torch.full((17, 40), 7.0, device="cuda"))
+    dW = sp.sp_linear_bwd_weight(Wg, _dev(X), _dev(dY))
+    torch.cuda.synchronize()
+    assert np.all(_np(Y) == 0) and np.all(_np(dX) == 0) and dW.numel() == 0
+
+
+def test_empty_rows_and_columns(sp):
+    g = synth.rng(6)
+    mask = synth.bernoulli_mask(g, 80, 70, 0.2)
+    mask[5:20] = 0
+    mask[:, 30:45] = 0
+    W = synth.normal(g, (80, 70), 1.0 / 70)
+    X = synth.normal(g, (70, 65), 1.0)
+    dY = synth.normal(g, (80, 65), 1.0)
+    _, Y, dX, _ = check_linear(sp, W, mask, X, dY, "empty rows/cols")
+    assert np.all(_np(Y)[5:20] == 0) and np.all(_np(dX)[30:45] == 0)
+
+
+def test_on_mask_zero_values_are_stored(sp):
+    g = synth.rng(7)
+    mask = synth.bernoulli_mask(g, 50, 60, 0.3)
+    W = synth.normal(g, (50, 60), 0.1)
+    W[mask.astype(bool) & (g.random((50, 60)) < 0.3)] = 0.0
+    X = synth.normal(g, (60, 36), 1.0)
+    dY = synth.normal(g, (50, 36), 1.0)
+    Wg, *_ = check_linear(sp, W, mask, X, dY, "on-mask zeros")
+    assert Wg.nnz == int(mask.sum())
+
+
+# ---------------------------------------------------------------- properties
+def test_bitwise_determinism_and_batch_invariance(sp):
+    c = synth.linear_case(3072, 768, 512, 0.05, 1.0 / 768, 77)
+    Wg = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))
+    X, dY = _dev(c["X"]), _dev(c["dY"])
+    outs = [(sp.sp_linear_fwd(Wg, X), sp.sp_linear_bwd_input(Wg, dY), sp.sp_linear_bwd_weight(Wg, X, dY))
+            for _ in range(2)]
+    torch.cuda.synchronize()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    # forward of a token is independent of the batch it is in (fixed per-element order)
+    Y_sub = sp.sp_linear_fwd(Wg, X[:, :96].contiguous())
+    Y_one = sp.sp_linear_fwd(Wg, X[:, 5:6].contiguous())
+    torch.cuda.synchronize()
+    assert torch.equal(Y_sub, outs[0][0][:, :96])
+    assert torch.equal(Y_one[:, 0], outs[0][0][:, 5])
+
+
+def test_relu_epilogues(sp):
+    c = synth.linear_case(300, 200, 70, 0.1, 1.0 / 200, 88)
+    S = oracle.csr_from_mask(c["W"], c["mask"])
+    Wg = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))
+    H = sp.sp_linear_fwd_relu(Wg, _dev(c["X"]))
+    torch.cuda.synchronize()
+    ref = np.maximum(oracle.linear_fwd(S, c["X"]), 0.0)
+    _assert_tol("relu fwd", _np(H), ref)
+    # gate: dX = (W^T dY) * [Hg > 0] with an arbitrary gate tensor with exact zeros
+    g = synth.rng(89)
+    gate = synth.normal(g, (200, 70), 1.0)
+    gate[g.random((200, 70)) < 0.3] = 0.0
+    dX = sp.sp_linear_bwd_input_relu(Wg, _dev(c["dY"]), _dev(gate))
+    torch.cuda.synchronize()
+    refx = oracle.linear_bwd_input(S, c["dY"]) * (gate > 0)
+    _assert_tol("relu' dX", _np(dX), refx)
+    assert np.all(_np(dX)[gate <= 0] == 0)
+
+
+def test_mse_and_sgd(sp):
+    g = synth.rng(90)
+    Y = synth.normal(g, (768, 1000), 1.0)
+    T = synth.normal(g, (768, 1000), 1.0)
+    dY = torch.empty(768, 1000, device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    scratch = torch.empty(sp.sp_mse_scratch_floats(Y.size), device="cuda")
+    sp.sp_mse_grad(_dev(Y), _dev(T), dY, loss, scratch)
+    torch.cuda.synchronize()
+    d = Y.astype(np.float64) - T
+    assert np.array_equal(_np(dY), (Y - T).astype(np.float32))
+    assert float(loss) == pytest.approx(0.5 * float(np.sum(d * d)), rel=1e-6)
+    v = synth.normal(g, 1000, 1.0)
+    w = synth.normal(g, 1000, 1.0)
+    vt = _dev(v)
+    sp.sp_sgd(vt, _dev(w), 0.01)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(_np(vt), v.astype(np.float64) - 0.01 * w, rtol=1e-6, atol=1e-7)
+
+
+# ---------------------------------------------------------------- conv
+def check_conv(sp, c, tag):
+    OC, IC, KH, KW, pad = c["OC"], c["IC"], c["KH"], c["KW"], c["pad"]
+    Wg = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))
+    g = sp.conv_geom(Wg, c["B"], c["H"], c["Wd"], pad)
+    X, dYg = _dev(c["X"]), _dev(c["dY"])
+    Y = sp.sp_conv2d_fwd(Wg, g, X)
+    dX = sp.sp_conv2d_bwd_input(Wg, g, dYg)
+    dW = sp.sp_conv2d_bwd_weight(Wg, g, X, dYg)
+    torch.cuda.synchronize()
+    F = oracle.conv_format(c["W"], c["mask"])
+    Xn, dOn = oracle.chwn_to_nchw(c["X"]), oracle.chwn_to_nchw(c["dY"])
+    _assert_tol(f"{tag} Y", _np(Y), oracle.nchw_to_chwn(oracle.conv2d_fwd(F, Xn, pad, NT)))
+    rdX, rdW = oracle.conv2d_bwd(F, Xn, dOn, pad)
+    _assert_tol(f"{tag} dX", _np(dX), oracle.nchw_to_chwn(rdX))
+    _assert_tol(f"{tag} dW", _np(dW), rdW)
+    # the handle's CSR over the flattened filter is the paper's (oc, ic, x, y) order
+    S = oracle.csr_from_mask(c["W"].reshape(OC, -1), c["mask"].reshape(OC, -1))
+    assert np.array_equal(_np(Wg.indices()["col_idx"]), S.col_idx)
+    assert Wg.nnz == F.nnz
+
+
+def test_cfg3_conv(sp):
+    check_conv(sp, synth.conv_case(**synth.CFG["cfg3"]), "cfg3")
+
+
+@pytest.mark.parametrize("B,IC,OC,H,W,K,pad,d", [
+    (3, 6, 5, 9, 9, 3, 1, 0.1), (8, 128 // 8, 256 // 8, 7, 7, 3, 1, 0.05), (2, 4, 3, 6, 5, 3, 0, 0.4),
+    (1, 2, 2, 5, 5, 5, 2, 0.6), (5, 3, 2, 4, 6, 1, 0, 0.7), (33, 8, 16, 10, 10, 3, 1, 0.2),
+    (64, 16, 16, 17, 19, 3, 1, 0.1), (130, 4, 4, 3, 3, 3, 1, 0.5)])
+def test_conv_shapes(sp, B, IC, OC, H, W, K, pad, d):
+    c = synth.conv_case(OC=OC, IC=IC, H=H, W=W, KH=K, KW=K, pad=pad, B=B, density=d,
+                        wvar=1.0 / (IC * K * K), seed=B * 7 + IC + OC + H)
+    check_conv(sp, c, f"conv B={B} IC={IC} OC={OC} {H}x{W} K={K} pad={pad}")
