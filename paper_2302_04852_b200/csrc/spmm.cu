@@ -26,69 +26,117 @@
 namespace sp {
 namespace {
 
+struct SpmmArgs {
+    int64_t rows, inner, B;
+    int KC, nkb;
+    const int32_t *ptr, *idx, *perm;
+    const float *vals, *in;
+    float *out;
+    const float *gate;
+};
+
+// v2: grid.x = row blocks (fastest, so the CTAs sharing one batch slice of
+// `in` run together and hit L2), grid.y = batch slices.  `in` column blocks
+// are double-buffered in shared memory with cp.async (LDGSTS).  Each warp keeps,
+// per owned row, a 32-entry window of (index, value) in registers (one lane per
+// entry, loaded coalesced) that persists across column blocks; entries are
+// broadcast with shuffles.
 template <int VEC, int RPW, int NW, bool CSC, int EPI>
-__global__ void __launch_bounds__(NW * 32)
-    spmm_tiled_kernel(int64_t rows, int64_t inner, int64_t B, int KC,
-                      const int32_t *__restrict__ ptr, const int32_t *__restrict__ idx,
-                      const int32_t *__restrict__ perm, const float *__restrict__ vals,
-                      const float *__restrict__ in, float *__restrict__ out,
-                      const float *__restrict__ gate) {
+__global__ void __launch_bounds__(NW * 32, 1) spmm_tiled_kernel(const SpmmArgs a) {
     constexpr int BT = 32 * VEC;
     constexpr int NT = NW * 32;
-    extern __shared__ __align__(16) float tile[];  // [KC][BT]
+    extern __shared__ __align__(16) float smem[];  // [2][KC][BT]
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t b0 = (int64_t)blockIdx.x * BT;
-    const int64_t r0 = (int64_t)blockIdx.y * (NW * RPW);
+    const int64_t r0 = (int64_t)blockIdx.x * (NW * RPW);
+    const int64_t b0 = (int64_t)blockIdx.y * BT;
+    const int64_t B = a.B;
     const bool vec4 = (B & 3) == 0;
+    const size_t tile_sz = (size_t)a.KC * BT;
+    (void)tile_sz;
 
+    // kick off the first tile before touching the index structure
+    stage_any<BT, NT>(smem, a.in, 0, (int)std::min<int64_t>(a.KC, a.inner), B, b0, vec4);
+    cp_async_commit();
+
+    // Per owned row: cursor, end, window base, and this lane's window entry
+    // (smem byte offset of its column relative to column 0, and its value).
     float acc[RPW][VEC];
-    int cur[RPW], end[RPW];
+    int cur[RPW], end[RPW], wb[RPW], cw[RPW], co[RPW];
+    float ww[RPW];
 #pragma unroll
     for (int i = 0; i < RPW; ++i) {
         const int64_t r = r0 + warp + (int64_t)i * NW;
-        cur[i] = r < rows ? __ldg(ptr + r) : 0;
-        end[i] = r < rows ? __ldg(ptr + r + 1) : 0;
+        cur[i] = r < a.rows ? __ldg(a.ptr + r) : 0;
+        end[i] = r < a.rows ? __ldg(a.ptr + r + 1) : 0;
+        wb[i] = cur[i];
 #pragma unroll
         for (int v = 0; v < VEC; ++v) acc[i][v] = 0.f;
     }
+    auto load_window = [&](int i) {
+        const int k = wb[i] + lane;
+        const bool ok = k < end[i];
+        cw[i] = ok ? __ldg(a.idx + k) : INT_MAX;
+        ww[i] = ok ? (CSC ? __ldg(a.vals + __ldg(a.perm + k)) : __ldg(a.vals + k)) : 0.f;
+        co[i] = ok ? cw[i] * (BT * 4) : 0;
+    };
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) load_window(i);
 
-    for (int64_t kb0 = 0; kb0 < inner; kb0 += KC) {
-        const int nk = (int)std::min<int64_t>(KC, inner - kb0);
-        const int kb1 = (int)(kb0 + nk);
-        __syncthreads();  // previous tile fully consumed
-        stage_tile<BT, NT>(tile, in, kb0, nk, B, b0, vec4);
+    for (int kb = 0; kb < a.nkb; ++kb) {
+        const int64_t kb0 = (int64_t)kb * a.KC;
+        if (kb + 1 < a.nkb) {
+            const int64_t n0 = kb0 + a.KC;
+            stage_any<BT, NT>(smem + ((kb + 1) & 1) * tile_sz, a.in, n0, (int)std::min<int64_t>(a.KC, a.inner - n0),
+                              B, b0, vec4);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
         __syncthreads();
-        const float *tl = tile + lane * VEC;
-        const int ckb0 = (int)kb0;
+        const int kb1 = (int)std::min<int64_t>(kb0 + a.KC, a.inner);
+        // byte base such that base + c*BT*4 addresses tile row (c - kb0), this lane's VEC
+        const char *base = reinterpret_cast<const char *>(smem + (kb & 1) * tile_sz + lane * VEC) -
+                           (size_t)kb0 * BT * 4;
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
-            // Row i's segment inside this column block, 32 entries at a time:
-            // lanes load (index, value) coalesced, then broadcast by shuffle.
             while (cur[i] < end[i]) {
-                const int k = cur[i] + lane;
-                int c = INT_MAX;
-                float w = 0.f;
-                if (k < end[i]) {
-                    c = __ldg(idx + k);
-                    w = CSC ? __ldg(vals + __ldg(perm + k)) : __ldg(vals + k);
+                int t0 = cur[i] - wb[i];
+                if (t0 >= 32) {  // window exhausted: reload (warp-uniform)
+                    wb[i] = cur[i];
+                    t0 = 0;
+                    load_window(i);
                 }
-                const unsigned bal = __ballot_sync(kFull, c < kb1);
-                const int n = __popc(bal);  // columns ascending: a prefix
-                if (n == 0) break;
-#pragma unroll 4
-                for (int t = 0; t < n; ++t) {
-                    const int ct = __shfl_sync(kFull, c, t);
-                    const float wt = __shfl_sync(kFull, w, t);
-                    float x[VEC];
-                    lds_vec<VEC>(tl + (ct - ckb0) * BT, x);
+                const int L = __popc(__ballot_sync(kFull, cw[i] < kb1));  // ascending: a prefix
+                if (L <= t0) break;
+                // entries t0 .. L-1, 8 at a time: shuffles, then 8 independent
+                // LDS, then the FMAs (entries past L get weight 0, offset 0).
+                for (int g = t0; g < L; g += 8) {
+                    int off[8];
+                    float w[8];
 #pragma unroll
-                    for (int v = 0; v < VEC; ++v) acc[i][v] = fmaf(wt, x[v], acc[i][v]);
+                    for (int u = 0; u < 8; ++u) {
+                        const int t = g + u;
+                        const int o = __shfl_sync(kFull, co[i], t);  // lane index wraps mod 32
+                        const float x = __shfl_sync(kFull, ww[i], t);
+                        off[u] = t < L ? o : (int)((size_t)kb0 * BT * 4);
+                        w[u] = t < L ? x : 0.f;
+                    }
+                    float xv[8][VEC];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        lds_vec<VEC>(reinterpret_cast<const float *>(base + off[u]), xv[u]);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) acc[i][v] = fmaf(w[u], xv[u][v], acc[i][v]);
                 }
-                cur[i] += n;
-                if (n < 32) break;
+                cur[i] = wb[i] + L;
+                if (L < 32) break;  // column block (or row) ended inside the window
             }
         }
+        __syncthreads();  // everyone done with this buffer before it is refilled
     }
 
     // Epilogue: ReLU / ReLU' gate fused; each element written once.
@@ -96,24 +144,23 @@ __global__ void __launch_bounds__(NW * 32)
 #pragma unroll
     for (int i = 0; i < RPW; ++i) {
         const int64_t r = r0 + warp + (int64_t)i * NW;
-        if (r >= rows) continue;
+        if (r >= a.rows) continue;
         float o[VEC];
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
-            float a = acc[i][v];
-            if (EPI == EPI_RELU) a = fmaxf(a, 0.f);
+            float x = acc[i][v];
+            if (EPI == EPI_RELU) x = fmaxf(x, 0.f);
             if (EPI == EPI_GATE) {
                 const int64_t b = bl + v;
-                const float g = b < B ? __ldg(gate + r * B + b) : 0.f;
-                a = g > 0.f ? a : 0.f;
+                const float g = b < B ? __ldg(a.gate + r * B + b) : 0.f;
+                x = g > 0.f ? x : 0.f;
             }
-            o[v] = a;
+            o[v] = x;
         }
-        float *dst = out + r * B + bl;
+        float *dst = a.out + r * B + bl;
         if (vec4 && VEC > 1 && bl + VEC <= B) {
             if constexpr (VEC == 2) *reinterpret_cast<float2 *>(dst) = make_float2(o[0], o[1]);
-            if constexpr (VEC == 4)
-                *reinterpret_cast<float4 *>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+            if constexpr (VEC == 4) *reinterpret_cast<float4 *>(dst) = make_float4(o[0], o[1], o[2], o[3]);
         } else {
 #pragma unroll
             for (int v = 0; v < VEC; ++v)
@@ -123,21 +170,25 @@ __global__ void __launch_bounds__(NW * 32)
 }
 
 constexpr int kNumSMs = 148;
-constexpr int kTileBudget = 96 * 1024;  // bytes of smem tile per CTA
+constexpr int kSmemBudget = 192 * 1024;  // two tile buffers per CTA, 1 CTA / SM
 
 template <int VEC, int RPW, int NW, bool CSC>
 void launch_cfg(int64_t rows, int64_t inner, int64_t B, const int32_t *ptr, const int32_t *idx,
                 const int32_t *perm, const float *vals, const float *in, float *out,
                 const float *gate, int epi, cudaStream_t st) {
     constexpr int BT = 32 * VEC;
-    int KC = (int)std::min<int64_t>(kTileBudget / (BT * 4), inner);
+    int KC = (int)std::min<int64_t>(kSmemBudget / (2 * BT * 4), inner);
     KC = std::max(KC, 1);
-    const size_t smem = (size_t)KC * BT * sizeof(float);
-    dim3 grid((unsigned)((B + BT - 1) / BT), (unsigned)((rows + NW * RPW - 1) / (NW * RPW)));
+    // balance the column blocks (same count, smallest equal size)
+    const int nkb = (int)((inner + KC - 1) / KC);
+    KC = (int)((inner + nkb - 1) / nkb);
+    const size_t smem = (size_t)2 * KC * BT * sizeof(float);
+    SpmmArgs a{rows, inner, B, KC, nkb, ptr, idx, perm, vals, in, out, gate};
+    dim3 grid((unsigned)((rows + NW * RPW - 1) / (NW * RPW)), (unsigned)((B + BT - 1) / BT));
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         count_launches(1);
-        kern<<<grid, NW * 32, smem, st>>>(rows, inner, B, KC, ptr, idx, perm, vals, in, out, gate);
+        kern<<<grid, NW * 32, smem, st>>>(a);
     };
     if (epi == EPI_RELU)
         launch(spmm_tiled_kernel<VEC, RPW, NW, CSC, EPI_RELU>);
@@ -151,19 +202,19 @@ template <int VEC, bool CSC>
 void launch_vec(int64_t rows, int64_t inner, int64_t B, const int32_t *ptr, const int32_t *idx,
                 const int32_t *perm, const float *vals, const float *in, float *out,
                 const float *gate, int epi, cudaStream_t st) {
-    // Largest row block (fewest re-reads of `in` through L2) that still
-    // gives >= 2 CTAs per SM.
-    constexpr int NW = 8;
+    // Largest row block (fewest L2 re-reads of `in`) that still fills the
+    // 148 SMs with >= 2 waves of CTAs.
+    constexpr int NW = 16;
     const int64_t slices = (B + 32 * VEC - 1) / (32 * VEC);
     auto ctas = [&](int rpw) { return slices * ((rows + NW * rpw - 1) / (NW * rpw)); };
-    if (ctas(16) >= 2 * kNumSMs)
-        launch_cfg<VEC, 16, NW, CSC>(rows, inner, B, ptr, idx, perm, vals, in, out, gate, epi, st);
-    else if (ctas(8) >= 2 * kNumSMs)
+    if (ctas(8) >= 2 * kNumSMs)
         launch_cfg<VEC, 8, NW, CSC>(rows, inner, B, ptr, idx, perm, vals, in, out, gate, epi, st);
     else if (ctas(4) >= 2 * kNumSMs)
         launch_cfg<VEC, 4, NW, CSC>(rows, inner, B, ptr, idx, perm, vals, in, out, gate, epi, st);
-    else
+    else if (ctas(2) >= kNumSMs)
         launch_cfg<VEC, 2, NW, CSC>(rows, inner, B, ptr, idx, perm, vals, in, out, gate, epi, st);
+    else
+        launch_cfg<VEC, 1, NW, CSC>(rows, inner, B, ptr, idx, perm, vals, in, out, gate, epi, st);
 }
 
 }  // namespace

@@ -72,6 +72,44 @@ __device__ __forceinline__ void stage_tile(float *__restrict__ tile, const float
     }
 }
 
+// ---- cp.async (LDGSTS) helpers: 16-byte global->shared copies that bypass
+// registers; src_bytes = 0 zero-fills the destination.
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Asynchronous version of stage_tile for B % 4 == 0 (16-byte aligned rows):
+// issues the copies and returns; the caller commits / waits.
+template <int BT, int NT>
+__device__ __forceinline__ void stage_tile_async(float *__restrict__ tile, const float *__restrict__ src,
+                                                 int64_t k0, int nk, int64_t B, int64_t b0) {
+    constexpr int Q = BT / 4;
+    const int total = nk * Q;
+    for (int i = threadIdx.x; i < total; i += NT) {
+        const int k = i / Q, q = (i - k * Q) * 4;
+        const int64_t b = b0 + q;
+        const bool in = b < B;
+        cp_async16(tile + k * BT + q, src + (k0 + k) * B + (in ? b : 0), in ? 16 : 0);
+    }
+}
+
+// Stage a tile either asynchronously (vec4) or synchronously (ragged B).
+template <int BT, int NT>
+__device__ __forceinline__ void stage_any(float *tile, const float *src, int64_t k0, int nk, int64_t B,
+                                          int64_t b0, bool vec4) {
+    if (vec4)
+        stage_tile_async<BT, NT>(tile, src, k0, nk, B, b0);
+    else
+        stage_tile<BT, NT>(tile, src, k0, nk, B, b0, false);
+}
+
 // Warp transpose-reduce of 32 per-lane partials: on return, lane t holds
 // sum over lanes of acc[t] (in acc[0]).  31 shuffles for 32 sums.
 __device__ __forceinline__ float transpose_reduce32(float (&acc)[32], int lane) {
