@@ -20,7 +20,8 @@
  *  - Every compute call only enqueues work on `stream` (a cudaStream_t
  *    passed as void*; NULL = legacy default stream) and never synchronises
  *    the host; asynchronous device faults surface at the caller's next sync.
- *    sp_weight_create synchronises `stream` exactly once (to learn nnz).
+ *    sp_weight_create synchronises `stream` (twice: to learn nnz and the
+ *    tile sizes of its cached schedule); compute calls never do.
  *  - No atomics anywhere: results are bitwise run-to-run reproducible.
  *  - Errors: every call returns sp_status; no C++ exception crosses the
  *    ABI.  Arguments are validated before any launch; launch failures are
@@ -68,8 +69,9 @@ typedef struct {
  *   row_ptr[R+1], col_idx[nnz] (ascending per row), vals[nnz] (CSR order),
  *   col_ptr[C+1], row_idx[nnz] (ascending per column),
  *   perm[nnz] (CSC slot k -> CSR slot holding the same (r, c)),
- * deterministically on the device, then synchronises `stream` once to read
- * nnz.  R, C >= 1; R*C and nnz must fit int32 (else SP_ERR_OVERFLOW).
+ * plus the tiled copies of both orientations the kernels stream (row blocks x
+ * column blocks), deterministically on the device; it
+ * synchronises `stream` twice (to read nnz and the tile maxima).  R, C >= 1; R*C and nnz must fit int32 (else SP_ERR_OVERFLOW).
  * The handle owns all its device buffers. */
 sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8_t *mask,
                            sp_stream_t stream, sp_weight_t *out);

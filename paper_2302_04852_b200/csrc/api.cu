@@ -100,6 +100,7 @@ sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8
         cudaFree(w->row_idx);
         cudaFree(w->perm);
         cudaFree(w->row_of);
+        free_tilings(w);
         w->magic = 0;
         delete w;
         return s;
@@ -118,6 +119,7 @@ sp_status sp_weight_destroy(sp_weight_t w, sp_stream_t stream) {
     cudaFree(w->row_idx);
     cudaFree(w->perm);
     cudaFree(w->row_of);
+    free_tilings(w);
     w->magic = 0;
     delete w;
     return SP_OK;
@@ -158,8 +160,7 @@ static sp_status linear_fwd_impl(sp_weight_t w, const float *X, float *Y, int64_
     if (!X || !Y) return fail(SP_ERR_NULL, std::string(fn) + ": NULL tensor");
     sp_status s = check_B(B, w->R, w->C, fn);
     if (s != SP_OK) return s;
-    launch_spmm(w->R, w->C, B, w->row_ptr, w->col_idx, nullptr, w->vals, X, Y, nullptr, epi,
-                w->max_row_nnz, S(stream));
+    launch_spmm(w, 0, B, X, Y, nullptr, epi, S(stream));
     return check_launch(fn);
 }
 
@@ -177,8 +178,7 @@ static sp_status linear_dx_impl(sp_weight_t w, const float *dY, const float *H, 
     if (!dY || !dX || (epi == EPI_GATE && !H)) return fail(SP_ERR_NULL, std::string(fn) + ": NULL tensor");
     sp_status s = check_B(B, w->R, w->C, fn);
     if (s != SP_OK) return s;
-    launch_spmm(w->C, w->R, B, w->col_ptr, w->row_idx, w->perm, w->vals, dY, dX, H, epi,
-                w->max_col_nnz, S(stream));
+    launch_spmm(w, 1, B, dY, dX, H, epi, S(stream));
     return check_launch(fn);
 }
 

@@ -133,6 +133,68 @@ __global__ void to_dense_kernel(int64_t nnz, int64_t C, const int32_t *__restric
     if (j < nnz) dense[(int64_t)row_of[j] * C + col_idx[j]] = nz[j];
 }
 
+// ---- tilings ----
+__device__ __forceinline__ int lower_bound_i32(const int32_t *a, int lo, int hi, int key) {
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// thread per (row, column block): entries of the row inside the block
+__global__ void til_count_kernel(int64_t rows, int nkb, int KC, int RB, const int32_t *__restrict__ ptr,
+                                 const int32_t *__restrict__ idx, int32_t *__restrict__ cnt) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid >= rows * nkb) return;
+    const int64_t r = tid / nkb;
+    const int kb = (int)(tid - r * nkb);
+    const int lo = lower_bound_i32(idx, ptr[r], ptr[r + 1], kb * KC);
+    const int hi = lower_bound_i32(idx, lo, ptr[r + 1], (kb + 1) * KC);
+    const int64_t rb = r / RB, lr = r - rb * RB;
+    cnt[(rb * nkb + kb) * RB + lr] = hi - lo;
+}
+
+__global__ void til_fill_kernel(int64_t rows, int nkb, int KC, int RB, const int32_t *__restrict__ ptr,
+                                const int32_t *__restrict__ idx, const int32_t *__restrict__ slotmap,
+                                const int32_t *__restrict__ seg, const float *__restrict__ vals,
+                                int2 *__restrict__ ent, int32_t *__restrict__ vidx) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid >= rows * nkb) return;
+    const int64_t r = tid / nkb;
+    const int kb = (int)(tid - r * nkb);
+    const int lo = lower_bound_i32(idx, ptr[r], ptr[r + 1], kb * KC);
+    const int hi = lower_bound_i32(idx, lo, ptr[r + 1], (kb + 1) * KC);
+    const int64_t rb = r / RB, lr = r - rb * RB;
+    int e = seg[(rb * nkb + kb) * RB + lr];
+    for (int t = lo; t < hi; ++t, ++e) {
+        const int slot = slotmap ? slotmap[t] : t;
+        ent[e] = make_int2(idx[t] - kb * KC, __float_as_int(vals[slot]));
+        vidx[e] = slot;
+    }
+}
+
+// max over tiles of the tile's entry count (single block, fixed order)
+__global__ void til_max_kernel(int64_t ntiles, int RB, const int32_t *__restrict__ seg, int64_t *__restrict__ out) {
+    __shared__ int32_t sh[256];
+    int32_t m = 0;
+    for (int64_t t = threadIdx.x; t < ntiles; t += blockDim.x) m = max(m, seg[(t + 1) * RB] - seg[t * RB]);
+    sh[threadIdx.x] = m;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) sh[threadIdx.x] = max(sh[threadIdx.x], sh[threadIdx.x + o]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
+__global__ void til_refresh_kernel(int64_t nnz, const int32_t *__restrict__ vidx, const float *__restrict__ vals,
+                                   int2 *__restrict__ ent) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < nnz) ent[e].y = __float_as_int(__ldg(vals + __ldg(vidx + e)));
+}
+
 template <typename T>
 cudaError_t dmalloc(T **p, int64_t n) {
     return cudaMalloc((void **)p, (size_t)(n > 0 ? n : 1) * sizeof(T));
@@ -194,6 +256,17 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
     csc_compact_kernel<<<(unsigned)((C + 127) / 128), 128, 0, st>>>(R, C, mask, slot, w->col_ptr,
                                                                    w->row_idx, w->perm);
     SP_TRY(cudaGetLastError());
+    {
+        const sp_status ts = build_tilings(w, st);
+        if (ts != SP_OK) {
+            set_error("sp_weight_create: tiling build failed");
+            cudaFreeAsync(slot, st);
+            cudaFreeAsync(rcnt, st);
+            cudaFreeAsync(ccnt, st);
+            cudaFreeAsync(info, st);
+            return ts;
+        }
+    }
     // Temporaries are freed in stream order (no second host sync).
     cudaFreeAsync(slot, st);
     cudaFreeAsync(rcnt, st);
@@ -208,6 +281,72 @@ fail:
     set_error(std::string("sp_weight_create: ") + cudaGetErrorString(e));
     return e == cudaErrorMemoryAllocation ? SP_ERR_ALLOC : SP_ERR_CUDA;
 #undef SP_TRY
+}
+
+sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
+    int64_t *info = nullptr, *mx = nullptr;
+    if (cudaMallocAsync((void **)&info, 2 * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
+    if (cudaMallocAsync((void **)&mx, 4 * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
+    for (int o = 0; o < 2; ++o) {
+        const int64_t rows = o == 0 ? w->R : w->C, inner = o == 0 ? w->C : w->R;
+        const int32_t *ptr = o == 0 ? w->row_ptr : w->col_ptr;
+        const int32_t *idx = o == 0 ? w->col_idx : w->row_idx;
+        const int32_t *slotmap = o == 0 ? nullptr : w->perm;
+        for (int v = 0; v < 2; ++v) {
+            sp_tiling &t = w->til[o][v];
+            t.RB = kTilRB[v];
+            t.KC = kTilKC[v];
+            t.rows = rows;
+            t.inner = inner;
+            t.nrb = (int)((rows + t.RB - 1) / t.RB);
+            t.nkb = (int)((inner + t.KC - 1) / t.KC);
+            const int64_t nseg = (int64_t)t.nrb * t.nkb * t.RB;
+            int32_t *cnt = nullptr;
+            if (dmalloc(&t.seg, nseg + 1) != cudaSuccess || dmalloc(&t.ent, w->nnz + 8) != cudaSuccess ||
+                dmalloc(&t.vidx, w->nnz) != cudaSuccess ||
+                cudaMallocAsync((void **)&cnt, (size_t)nseg * sizeof(int32_t), st) != cudaSuccess) {
+                cudaFreeAsync(info, st);
+                cudaFreeAsync(mx, st);
+                return SP_ERR_ALLOC;
+            }
+            cudaMemsetAsync(cnt, 0, (size_t)nseg * sizeof(int32_t), st);
+            cudaMemsetAsync(t.ent, 0, (size_t)(w->nnz + 8) * sizeof(int2), st);
+            const int64_t nt = rows * t.nkb;
+            til_count_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, t.nkb, t.KC, t.RB, ptr, idx, cnt);
+            scan_kernel<<<1, kScanThreads, 0, st>>>(nseg, cnt, t.seg, info);
+            til_fill_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, t.nkb, t.KC, t.RB, ptr, idx,
+                                                                         slotmap, t.seg, w->vals, t.ent, t.vidx);
+            til_max_kernel<<<1, 256, 0, st>>>((int64_t)t.nrb * t.nkb, t.RB, t.seg, mx + (o * 2 + v));
+            cudaFreeAsync(cnt, st);
+        }
+    }
+    int64_t h[4];
+    cudaMemcpyAsync(h, mx, sizeof(h), cudaMemcpyDeviceToHost, st);
+    const cudaError_t e = cudaStreamSynchronize(st);  // second (last) host sync of sp_weight_create
+    for (int o = 0; o < 2; ++o)
+        for (int v = 0; v < 2; ++v) w->til[o][v].max_tile = (int32_t)h[o * 2 + v];
+    cudaFreeAsync(info, st);
+    cudaFreeAsync(mx, st);
+    return (e == cudaSuccess && cudaGetLastError() == cudaSuccess) ? SP_OK : SP_ERR_CUDA;
+}
+
+void free_tilings(sp_weight_s *w) {
+    for (auto &o : w->til)
+        for (auto &t : o) {
+            cudaFree(t.seg);
+            cudaFree(t.ent);
+            cudaFree(t.vidx);
+            t.seg = nullptr;
+            t.ent = nullptr;
+            t.vidx = nullptr;
+        }
+}
+
+void launch_refresh(const sp_tiling &t, const float *vals, int64_t nnz, cudaStream_t st) {
+    if (nnz > 0) {
+        count_launches(1);
+        til_refresh_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, st>>>(nnz, t.vidx, vals, t.ent);
+    }
 }
 
 void launch_to_dense(const sp_weight_s *w, const float *nz, float *dense, cudaStream_t st) {

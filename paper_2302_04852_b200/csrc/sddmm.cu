@@ -2,20 +2,23 @@
 // row a-4:  dW[j] = sum_b dY[r_j][b] * X[c_j][b]  for every nonzero j (CSR
 // order), Eq. (2) (P146-P148) restricted to the mask (P151, P173).
 //
-// Design: a CTA owns a block of RB = NW*RPW rows and a batch
-// range split (blockIdx.x); it walks that range in slices of BT = 32*VEC.
-// Per slice, each warp holds dY[r][slice] of its RPW rows in registers and
-// streams X[:, slice] through shared memory in column blocks (coalesced
-// 16-byte loads).  Per nonzero, each lane accumulates a VEC-long partial dot
-// into one of 32 register accumulators; every 32 nonzeros a warp
-// transpose-reduce (31 shuffles) leaves lane t with the slice sum of nonzero
-// t, which lane t adds into the split's partial buffer (one owner per
-// element, fixed order).  A final fixed-order pass sums the splits.  No
-// atomics: bitwise reproducible.
+// Design.  It uses the handle's tiled structure of one
+// orientation, chosen so that the operand staged through shared memory is the
+// one with the smaller feature dimension (fewer L2 re-reads):
+//   CSR tiling (rows r):    register operand dY[r], staged operand X  [C x B]
+//   CSC tiling (rows c):    register operand X[c],  staged operand dY [R x B]
+// A CTA owns one row block (RB rows) and a batch split (whole slices of BT =
+// 32*VEC columns).  For each (slice, column block) the staged tile [KC x BT] is
+// double-buffered with cp.async; each warp holds the register-operand slices
+// of its RPW rows.  Rows are handled in pairs: up to 16 entries of each row of
+// the pair feed 32 register accumulators (lane-partial dots over VEC batch
+// elements), one warp transpose-reduce (31 shuffles) turns them into 32 slice
+// sums, and lane t adds its sum into the split's partial buffer (entry order,
+// one owner per element).  A final fixed-order pass sums the splits and
+// scatters to CSR order through vidx.  No atomics: bitwise reproducible.
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <climits>
 
 #include "sp_internal.cuh"
 #include "tile.cuh"
@@ -25,65 +28,81 @@ namespace {
 
 struct SddmmArgs {
     int64_t nrow, F, B;
-    int KC, nkb, spl;  // column block, #column blocks, slices per split
-    const int32_t *ptr, *idx;
-    const float *regop;   // [nrow x B]: operand kept in registers (one row per warp row)
-    const float *smemop;  // [F x B]: operand staged through shared memory
-    float *part;          // [nsplit x nnz] slice-split partials (slot order of ptr/idx)
+    int KC, nkb, spl;        // column block, #column blocks, slices per split
+    int cap;                 // entry-buffer capacity when entries are staged
+    const int32_t *seg;
+    const int2 *ent;
+    const int32_t *vidx;
+    const float *regop;      // [nrow x B]
+    const float *smemop;     // [F x B]
+    float *part;             // [nsplit x nnz] in entry order (or dW if direct)
     int64_t nnz;
+    int direct;              // single split: write dW[vidx[e]] directly
 };
 
-// v2: grid.x = row blocks (fastest), grid.y = batch splits.  Orientation:
-//   CSR (TRANS=false): rows r, regop = dY, smemop = X, slot j (CSR order)
-//   CSC (TRANS=true):  rows c, regop = X,  smemop = dY, slot k (CSC order),
-// whichever stages the smaller feature dimension (fewer L2 re-reads).  The
-// (slice, column block) tiles are double-buffered with cp.async.  Per row, a
-// 32-entry index window persists across the column blocks of a slice; each
-// segment's partial dots go to 32 register accumulators and one warp
-// transpose-reduce, and lane t adds the slice sum into part[split][slot t].
-template <int VEC, int RPW, int NW>
-__global__ void __launch_bounds__(NW * 32, 1) sddmm_tiled_kernel(const SddmmArgs a) {
+__device__ __forceinline__ void prefetch_l1(const void *p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+template <int VEC>
+__device__ __forceinline__ float dotv(const float (&a)[VEC], const float *p) {
+    float x[VEC];
+    lds_vec<VEC>(p, x);
+    float d = 0.f;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) d = fmaf(a[v], x[v], d);
+    return d;
+}
+
+template <int VEC, int RPW, int NW, bool SENT>
+__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) sddmm_tiled_kernel(const SddmmArgs a) {
+    static_assert(RPW % 2 == 0, "rows are processed in pairs");
     constexpr int BT = 32 * VEC;
     constexpr int NT = NW * 32;
-    extern __shared__ __align__(16) float smem[];  // [2][KC][BT]
+    constexpr int RB = NW * RPW;
+    extern __shared__ __align__(16) float smem[];  // [2][KC][BT] floats, then [2][cap+2] int2
+    int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * a.KC * BT);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t r0 = (int64_t)blockIdx.x * (NW * RPW);
+    const int rb = blockIdx.x;
     const int64_t B = a.B;
     const int64_t s_lo = (int64_t)blockIdx.y * a.spl * BT;
-    const int nsl = (int)std::min<int64_t>(a.spl, (B - s_lo + BT - 1) / BT);  // slices in this split
+    const int nsl = (int)std::min<int64_t>(a.spl, (B - s_lo + BT - 1) / BT);
     const int ntile = nsl * a.nkb;
-    float *P = a.part + (int64_t)blockIdx.y * a.nnz;
+    float *P = a.part + (a.direct ? 0 : (int64_t)blockIdx.y * a.nnz);
     const bool vec4 = (B & 3) == 0;
     const size_t tile_sz = (size_t)a.KC * BT;
+    const int32_t *segw = a.seg + (int64_t)rb * a.nkb * RB + warp * RPW;
 
-    auto stage = [&](int q, int buf) {
+    // stage tile q (activations, and the entries when SENT); returns the
+    // (even) index of the first staged entry
+    auto stage = [&](int q, int buf) -> int {
         const int s = q / a.nkb, kb = q - s * a.nkb;
         const int64_t k0 = (int64_t)kb * a.KC;
         stage_any<BT, NT>(smem + buf * tile_sz, a.smemop, k0, (int)std::min<int64_t>(a.KC, a.F - k0), B,
                           s_lo + (int64_t)s * BT, vec4);
+        if constexpr (SENT) {
+            const int64_t tb = ((int64_t)rb * a.nkb + kb) * RB;
+            const int e0 = __ldg(a.seg + tb) & ~1, e1 = __ldg(a.seg + tb + RB);
+            const int n16 = (e1 - e0 + 1) >> 1;
+            int2 *dst = ents + buf * (a.cap + 2);
+            for (int i = threadIdx.x; i < n16; i += NT) cp_async16(dst + 2 * i, a.ent + e0 + 2 * i, 16);
+            return e0;
+        }
+        return 0;
     };
-    stage(0, 0);
+    int ea = stage(0, 0);
     cp_async_commit();
 
-    int beg[RPW], end[RPW], cur[RPW], cw[RPW], co[RPW];
-#pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-        const int64_t r = r0 + warp + (int64_t)i * NW;
-        beg[i] = r < a.nrow ? __ldg(a.ptr + r) : 0;
-        end[i] = r < a.nrow ? __ldg(a.ptr + r + 1) : 0;
-    }
     float rv[RPW][VEC];
-
+    int sg = 0;
     for (int q = 0; q < ntile; ++q) {
         const int s = q / a.nkb, kb = q - s * a.nkb;
-        const int64_t b0 = s_lo + (int64_t)s * BT;
-        if (kb == 0) {
-            // new slice: this warp's register-operand rows and fresh windows
-            const int64_t bl = b0 + lane * VEC;
+        if (kb == 0) {  // new slice: this warp's register-operand rows
+            const int64_t bl = s_lo + (int64_t)s * BT + lane * VEC;
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
-                const int64_t r = r0 + warp + (int64_t)i * NW;
+                const int64_t r = (int64_t)rb * RB + warp * RPW + i;
                 const float *src = a.regop + r * B + bl;
                 if (r < a.nrow && vec4 && VEC == 4 && bl + 4 <= B) {
                     const float4 t = __ldg(reinterpret_cast<const float4 *>(src));
@@ -97,106 +116,95 @@ __global__ void __launch_bounds__(NW * 32, 1) sddmm_tiled_kernel(const SddmmArgs
 #pragma unroll
                     for (int v = 0; v < VEC; ++v) rv[i][v] = (r < a.nrow && bl + v < B) ? __ldg(src + v) : 0.f;
                 }
-                cur[i] = beg[i];
-                const int k = beg[i] + lane;
-                cw[i] = k < end[i] ? __ldg(a.idx + k) : INT_MAX;
-                co[i] = k < end[i] ? cw[i] * (BT * 4) : 0;
             }
         }
+        sg = lane <= RPW ? __ldg(segw + (int64_t)kb * RB + lane) : 0;
+        int ean = 0;
         if (q + 1 < ntile) {
-            stage(q + 1, (q + 1) & 1);
+            ean = stage(q + 1, (q + 1) & 1);
             cp_async_commit();
+            if constexpr (!SENT) {  // entries of the next column block into L1
+                const int kbn = (q + 1) % a.nkb;
+                const int sn = lane <= RPW ? __ldg(segw + (int64_t)kbn * RB + lane) : 0;
+                const int e0 = __shfl_sync(kFull, sn, 0), e1 = __shfl_sync(kFull, sn, RPW);
+                for (int l = (e0 >> 4) + lane; l < ((e1 + 15) >> 4); l += 32)
+                    prefetch_l1(a.ent + ((int64_t)l << 4));
+            }
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
         __syncthreads();
-        const int64_t kb0 = (int64_t)kb * a.KC;
-        const int kb1 = (int)std::min<int64_t>(kb0 + a.KC, a.F);
-        const char *base = reinterpret_cast<const char *>(smem + (q & 1) * tile_sz + lane * VEC) -
-                           (size_t)kb0 * BT * 4;
+        const float *tl = smem + (q & 1) * tile_sz + lane * VEC;
+        const int2 *es = SENT ? ents + (q & 1) * (a.cap + 2) - ea : a.ent;
 #pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-            while (cur[i] < end[i]) {
-                // window base wb = cur rounded so that the window holds cur
-                const int wb = beg[i] + ((cur[i] - beg[i]) & ~31);
-                const int t0 = cur[i] - wb;
-                if (t0 == 0 && cur[i] != beg[i]) {  // crossed into a new window
-                    const int k = wb + lane;
-                    cw[i] = k < end[i] ? __ldg(a.idx + k) : INT_MAX;
-                    co[i] = k < end[i] ? cw[i] * (BT * 4) : 0;
-                }
-                const int L = __popc(__ballot_sync(kFull, cw[i] < kb1));
-                if (L <= t0) break;
-                // entries t0..L-1 -> acc[u], u = t - t0 (static index), 8 at a time
+        for (int m = 0; m < RPW; m += 2) {
+            int pa = __shfl_sync(kFull, sg, m);
+            const int a1 = __shfl_sync(kFull, sg, m + 1);
+            int pb = a1;
+            const int b1 = __shfl_sync(kFull, sg, m + 2);
+            while (pa < a1 || pb < b1) {
+                const int na = min(16, a1 - pa), nb = min(16, b1 - pb);
                 float acc[32];
 #pragma unroll
                 for (int u = 0; u < 32; ++u) acc[u] = 0.f;
-                const int n = L - t0;
 #pragma unroll
-                for (int g = 0; g < 32; g += 8) {
-                    if (g >= n) break;
-                    int off[8];
+                for (int g = 0; g < 16; g += 4) {
+                    if (g < na) {
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int o = __shfl_sync(kFull, co[i], t0 + g + u);  // wraps mod 32
-                        off[u] = (g + u < n) ? o : (int)((size_t)kb0 * BT * 4);
+                        for (int u = g; u < g + 4; ++u)
+                            if (u < na) acc[u] = dotv<VEC>(rv[m], tl + (SENT ? es[pa + u].x : __ldg(&a.ent[pa + u].x)) * BT);
                     }
-                    float xv[8][VEC];
+                    if (g < nb) {
 #pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        lds_vec<VEC>(reinterpret_cast<const float *>(base + off[u]), xv[u]);
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        float d = 0.f;
-#pragma unroll
-                        for (int v = 0; v < VEC; ++v) d = fmaf(rv[i][v], xv[u][v], d);
-                        acc[g + u] = (g + u < n) ? d : 0.f;
+                        for (int u = g; u < g + 4; ++u)
+                            if (u < nb) acc[16 + u] = dotv<VEC>(rv[m + 1], tl + (SENT ? es[pb + u].x : __ldg(&a.ent[pb + u].x)) * BT);
                     }
                 }
                 const float sum = transpose_reduce32(acc, lane);
-                if (lane < n) {
-                    float *p = P + cur[i] + lane;
+                const int u = lane & 15;
+                const bool mine = lane < 16 ? u < na : u < nb;
+                if (mine) {
+                    const int e = (lane < 16 ? pa : pb) + u;
+                    float *p = a.direct ? P + __ldg(a.vidx + e) : P + e;
                     *p = (s == 0) ? sum : *p + sum;
                 }
-                cur[i] = wb + L;
-                if (L < 32) break;
+                pa += na;
+                pb += nb;
             }
         }
         __syncthreads();
+        ea = ean;
     }
 }
 
-// dW[perm ? perm[k] : k] = sum_s part[s][k], s ascending.
+// dW[vidx[e]] = sum_s part[s][e], s ascending.
 __global__ void split_reduce_kernel(int64_t nnz, int nsplit, const float *__restrict__ part,
-                                    const int32_t *__restrict__ perm, float *__restrict__ dW) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= nnz) return;
-    float s = part[k];
-    for (int i = 1; i < nsplit; ++i) s += part[(int64_t)i * nnz + k];
-    dW[perm ? perm[k] : k] = s;
+                                    const int32_t *__restrict__ vidx, float *__restrict__ dW) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nnz) return;
+    float s = part[e];
+    for (int i = 1; i < nsplit; ++i) s += part[(int64_t)i * nnz + e];
+    dW[vidx[e]] = s;
 }
 
 constexpr int kNumSMs = 148;
-constexpr int kSmemBudget = 192 * 1024;
 
 template <int VEC, int RPW, int NW>
-sp_status launch_cfg(const sp_weight_s *w, const float *X, const float *dY, float *dW, int64_t B,
-                     cudaStream_t st) {
+sp_status launch_cfg(const sp_weight_s *w, const sp_tiling &t, const float *regop, const float *smemop,
+                     float *dW, int64_t B, int ctas_per_sm, cudaStream_t st) {
     constexpr int BT = 32 * VEC;
-    const bool trans = w->C > w->R;  // stage the smaller feature dimension
-    const int64_t nrow = trans ? w->C : w->R, F = trans ? w->R : w->C, nnz = w->nnz;
+    const int64_t nnz = w->nnz;
     const int64_t slices = (B + BT - 1) / BT;
-    const int64_t rblocks = (nrow + NW * RPW - 1) / (NW * RPW);
-    int64_t nsplit = std::max<int64_t>(1, std::min<int64_t>(slices, (2 * kNumSMs + rblocks - 1) / rblocks));
+    const int64_t want = (int64_t)ctas_per_sm * kNumSMs;
+    int64_t nsplit = std::max<int64_t>(1, std::min<int64_t>(slices, (want + t.nrb - 1) / t.nrb));
     const int64_t spl = (slices + nsplit - 1) / nsplit;
     nsplit = (slices + spl - 1) / spl;
-    int KC = (int)std::min<int64_t>(kSmemBudget / (2 * BT * 4), F);
-    KC = std::max(KC, 1);
-    const int nkb = (int)((F + KC - 1) / KC);
-    KC = (int)((F + nkb - 1) / nkb);
-    const size_t smem = (size_t)2 * KC * BT * sizeof(float);
-    const bool direct = nsplit == 1 && !trans;
+    const size_t tiles = (size_t)2 * t.KC * BT * sizeof(float);
+    const int cap = (t.max_tile + 2 + 3) & ~3;  // keeps both entry buffers 16-byte aligned
+    const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)(227 * 1024) / (NW == 8 ? 2 : 1);
+    const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
+    const bool direct = nsplit == 1;
     float *part = dW;
     if (!direct) {
         if (cudaMallocAsync((void **)&part, (size_t)(nsplit * nnz) * sizeof(float), st) != cudaSuccess) {
@@ -204,18 +212,24 @@ sp_status launch_cfg(const sp_weight_s *w, const float *X, const float *dY, floa
             return SP_ERR_ALLOC;
         }
     }
-    SddmmArgs a{nrow, F, B, KC, nkb, (int)spl, trans ? w->col_ptr : w->row_ptr,
-                trans ? w->row_idx : w->col_idx, trans ? X : dY, trans ? dY : X, part, nnz};
-    auto kern = sddmm_tiled_kernel<VEC, RPW, NW>;
+    SddmmArgs a{t.rows, t.inner, B, t.KC, t.nkb, (int)spl, cap, t.seg, t.ent, t.vidx, regop, smemop, part, nnz,
+                direct ? 1 : 0};
+    auto kern = sent ? sddmm_tiled_kernel<VEC, RPW, NW, true> : sddmm_tiled_kernel<VEC, RPW, NW, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     count_launches(direct ? 1 : 2);
-    kern<<<dim3((unsigned)rblocks, (unsigned)nsplit), NW * 32, smem, st>>>(a);
+    kern<<<dim3((unsigned)t.nrb, (unsigned)nsplit), NW * 32, smem, st>>>(a);
     if (!direct) {
-        split_reduce_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, st>>>(nnz, (int)nsplit, part,
-                                                                           trans ? w->perm : nullptr, dW);
+        split_reduce_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, st>>>(nnz, (int)nsplit, part, t.vidx, dW);
         cudaFreeAsync(part, st);
     }
     return SP_OK;
+}
+
+template <int VEC>
+sp_status launch_vec(const sp_weight_s *w, const sp_tiling &t, int var, const float *regop,
+                     const float *smemop, float *dW, int64_t B, cudaStream_t st) {
+    if (var == 0) return launch_cfg<VEC, 8, 16>(w, t, regop, smemop, dW, B, 2, st);
+    return launch_cfg<VEC, 4, 8>(w, t, regop, smemop, dW, B, 4, st);
 }
 
 }  // namespace
@@ -223,9 +237,16 @@ sp_status launch_cfg(const sp_weight_s *w, const float *X, const float *dY, floa
 sp_status launch_sddmm(const sp_weight_s *w, const float *X, const float *dY, float *dW, int64_t B,
                        cudaStream_t st) {
     if (w->nnz == 0) return SP_OK;
-    if (B <= 32) return launch_cfg<1, 8, 16>(w, X, dY, dW, B, st);
-    if (B <= 64 || (B & 3) != 0) return launch_cfg<2, 8, 16>(w, X, dY, dW, B, st);
-    return launch_cfg<4, 8, 16>(w, X, dY, dW, B, st);
+    const int orient = w->C > w->R ? 1 : 0;  // stage the smaller feature dimension
+    const float *regop = orient ? X : dY;
+    const float *smemop = orient ? dY : X;
+    const int vec = B <= 32 ? 1 : (B <= 64 || (B & 3)) ? 2 : 4;
+    // small problems (few row blocks and slices) use the small tiling
+    const int var = (int64_t)w->til[orient][0].nrb * ((B + 32 * vec - 1) / (32 * vec)) < kNumSMs ? 1 : 0;
+    const sp_tiling &t = w->til[orient][var];
+    if (vec == 4) return launch_vec<4>(w, t, var, regop, smemop, dW, B, st);
+    if (vec == 2) return launch_vec<2>(w, t, var, regop, smemop, dW, B, st);
+    return launch_vec<1>(w, t, var, regop, smemop, dW, B, st);
 }
 
 }  // namespace sp

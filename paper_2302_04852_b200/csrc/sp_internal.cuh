@@ -13,6 +13,22 @@
 
 #define SP_MAGIC 0x53505731u /* "SPW1" */
 
+// A tiled copy of one orientation's index structure (built once per handle,
+// DESIGN.md §5): rows are grouped in row blocks of RB, the inner dimension in
+// column blocks of KC.  Entries are ordered (row block, column block, local
+// row, column); segment (t = rb*nkb + kb, local row lr) is
+// [seg[t*RB + lr], seg[t*RB + lr + 1]).  ent[e] = (column - kb*KC, value bits)
+// with the value refreshed from vals[vidx[e]] before use; vidx[e] is the CSR
+// slot of the entry.
+struct sp_tiling {
+    int RB, KC, nrb, nkb;
+    int64_t rows, inner;
+    int32_t *seg;   // [nrb*nkb*RB + 1]
+    int2 *ent;      // [nnz + 8] (padded)
+    int32_t *vidx;  // [nnz]
+    int32_t max_tile;  // max entries in one (row block, column block) tile
+};
+
 struct sp_weight_s {
     uint32_t magic;
     int64_t R, C, nnz;
@@ -27,7 +43,13 @@ struct sp_weight_s {
     // row of every CSR slot (for the SDDMM chunk walk and to_dense)
     int32_t *row_of;
     int32_t max_row_nnz, max_col_nnz;
+    // tilings: [orientation 0 = CSR rows, 1 = CSC columns][variant 0 = big, 1 = small]
+    sp_tiling til[2][2];
 };
+
+// Tiling variants (RB rows per CTA, KC inner columns per shared-memory tile).
+constexpr int kTilRB[2] = {128, 32};
+constexpr int kTilKC[2] = {192, 96};
 
 namespace sp {
 
@@ -45,15 +67,18 @@ inline cudaStream_t S(sp_stream_t s) { return reinterpret_cast<cudaStream_t>(s);
 sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *mask,
                        cudaStream_t st, sp_weight_s *w);
 void launch_to_dense(const sp_weight_s *w, const float *nz, float *dense, cudaStream_t st);
+sp_status build_tilings(sp_weight_s *w, cudaStream_t st);
+void free_tilings(sp_weight_s *w);
+// ent[e].y = bits(vals[vidx[e]]) for one tiling (before an SpMM launch)
+void launch_refresh(const sp_tiling &t, const float *vals, int64_t nnz, cudaStream_t st);
 
 // ---- spmm.cu ----
 // Epilogue codes for the SpMM kernels.
 enum Epi { EPI_NONE = 0, EPI_RELU = 1, EPI_GATE = 2 };
-// out[r][b] = epi(sum_k val(k) * in[idx[k]][b]) over k in [ptr[r], ptr[r+1]),
-// val(k) = vals[perm ? perm[k] : k].  rows = #out rows, inner = #in rows.
-void launch_spmm(int64_t rows, int64_t inner, int64_t B, const int32_t *ptr, const int32_t *idx,
-                 const int32_t *perm, const float *vals, const float *in, float *out,
-                 const float *gate, int epi, int max_seg, cudaStream_t st);
+// out[r][b] = epi(sum over row r of the orientation: w * in[col][b]);
+// orient 0: forward (CSR, rows = R, inner = C); 1: dX (CSC, rows = C, inner = R).
+void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out,
+                 const float *gate, int epi, cudaStream_t st);
 
 // ---- sddmm.cu ----
 // dW[j] = sum_b dY[row(j)][b] * X[col_idx[j]][b]

@@ -1,24 +1,27 @@
 // spmm.cu -- forward SpMM (K2, sp_linear_fwd) and CSC-driven input-gradient
 // SpMM (K3, sp_linear_bwd_input).  SURVEY §8(a) rows a-2, a-3.
 //
-//   out[r][b] = epi( sum_{k in [ptr[r], ptr[r+1])} val(k) * in[idx[k]][b] )
-//   forward (P141):  ptr=row_ptr, idx=col_idx, val(k)=vals[k]
-//   dX (Eq. 1):      ptr=col_ptr, idx=row_idx, val(k)=vals[perm[k]]
+//   out[r][b] = epi( sum over the entries (c, w) of row r of w * in[c][b] )
+//   forward (P141):  rows of the CSR      (out = Y [R x B],  in = X  [C x B])
+//   dX (Eq. 1):      rows of the CSC copy (out = dX [C x B], in = dY [R x B]),
+//                    w = vals[perm[k]]  -- gather form, no atomics.
 //
-// Design: one CTA owns a batch slice of BT = 32*VEC columns
-// and a block of RB = NW*RPW rows.  The dense operand `in` is streamed
-// through shared memory in column blocks of KC rows (the "activation tile
-// staged in shared memory" of the north star), coalesced 16-byte loads along
-// the batch.  Each warp owns RPW interleaved rows and keeps their VEC-wide
-// accumulators in registers across column blocks; per nonzero every lane
-// does VEC FMAs against tile[c][lane*VEC ..] (batch-contiguous vector LDS).
-// Each output element is produced by exactly one lane, so there are no
-// atomics and the summation order (k ascending) is fixed: bitwise
-// reproducible and independent of B and of the launch shape along B.
+// Design: the handle carries a tiled copy of each orientation
+// (row blocks of RB rows x column blocks of KC inner columns; entries of one
+// (row block, column block, row) segment are contiguous and store the
+// block-local column and the value).  A CTA owns one row block and one batch
+// slice of BT = 32*VEC columns.  The `in` tile [KC x BT] of each column block
+// is double-buffered in shared memory with cp.async (LDGSTS), coalesced
+// 16-byte copies along the batch.  Each warp owns RPW consecutive rows and
+// keeps their VEC-wide accumulators in registers across column blocks.  Per
+// entry: one warp-uniform 8-byte load of (column, value) (L1-resident: the
+// next tile's entries are prefetched while the current one computes), one
+// vector LDS of tile[column][lane*VEC..], VEC FFMAs.  Every output element is
+// produced by exactly one lane in a fixed order (entries ascending): no
+// atomics, bitwise reproducible, independent of B and of the grid.
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <climits>
 
 #include "sp_internal.cuh"
 #include "tile.cuh"
@@ -28,122 +31,111 @@ namespace {
 
 struct SpmmArgs {
     int64_t rows, inner, B;
-    int KC, nkb;
-    const int32_t *ptr, *idx, *perm;
-    const float *vals, *in;
+    int KC, nkb, cap;  // cap: entry-buffer capacity (entries) when staged
+    const int32_t *seg;
+    const int2 *ent;
+    const float *in;
     float *out;
     const float *gate;
 };
 
-// v2: grid.x = row blocks (fastest, so the CTAs sharing one batch slice of
-// `in` run together and hit L2), grid.y = batch slices.  `in` column blocks
-// are double-buffered in shared memory with cp.async (LDGSTS).  Each warp keeps,
-// per owned row, a 32-entry window of (index, value) in registers (one lane per
-// entry, loaded coalesced) that persists across column blocks; entries are
-// broadcast with shuffles.
-template <int VEC, int RPW, int NW, bool CSC, int EPI>
-__global__ void __launch_bounds__(NW * 32, 1) spmm_tiled_kernel(const SpmmArgs a) {
+__device__ __forceinline__ void prefetch_l1(const void *p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+// Prefetch into L1 the entry lines [e0, e1) (128-byte lines = 16 entries).
+__device__ __forceinline__ void prefetch_entries(const int2 *ent, int e0, int e1, int lane) {
+    const int l0 = e0 >> 4, l1 = (e1 + 15) >> 4;
+    for (int l = l0 + lane; l < l1; l += 32) prefetch_l1(ent + ((int64_t)l << 4));
+}
+
+// SENT: the tile's entries are staged in shared memory too (cp.async, next
+// tile's entries prefetched with its activation tile); otherwise entries are
+// read with warp-uniform global loads (tiles larger than the entry buffer).
+template <int VEC, int RPW, int NW, int EPI, bool SENT>
+__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) spmm_tiled_kernel(const SpmmArgs a) {
     constexpr int BT = 32 * VEC;
     constexpr int NT = NW * 32;
-    extern __shared__ __align__(16) float smem[];  // [2][KC][BT]
+    constexpr int RB = NW * RPW;
+    extern __shared__ __align__(16) float smem[];  // [2][KC][BT] floats, then [2][cap+2] int2
+    int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * a.KC * BT);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t r0 = (int64_t)blockIdx.x * (NW * RPW);
+    const int rb = blockIdx.x;
     const int64_t b0 = (int64_t)blockIdx.y * BT;
     const int64_t B = a.B;
     const bool vec4 = (B & 3) == 0;
     const size_t tile_sz = (size_t)a.KC * BT;
-    (void)tile_sz;
 
-    // kick off the first tile before touching the index structure
+    // stage the entries of tile kb into buffer buf; returns the (even) index
+    // of the first staged entry
+    auto stage_ent = [&](int kb, int buf) -> int {
+        const int64_t tb = ((int64_t)rb * a.nkb + kb) * RB;
+        const int e0 = __ldg(a.seg + tb) & ~1, e1 = __ldg(a.seg + tb + RB);
+        const int n16 = (e1 - e0 + 1) >> 1;
+        int2 *dst = ents + buf * (a.cap + 2);
+        for (int i = threadIdx.x; i < n16; i += NT) cp_async16(dst + 2 * i, a.ent + e0 + 2 * i, 16);
+        return e0;
+    };
+
     stage_any<BT, NT>(smem, a.in, 0, (int)std::min<int64_t>(a.KC, a.inner), B, b0, vec4);
+    int ea = 0;
+    if constexpr (SENT) ea = stage_ent(0, 0);
     cp_async_commit();
 
-    // Per owned row: cursor, end, window base, and this lane's window entry
-    // (smem byte offset of its column relative to column 0, and its value).
+    // lane l <= RPW holds the l-th segment bound of this warp's rows in the
+    // current tile (rows rb*RB + warp*RPW + i).
+    const int32_t *segw = a.seg + (int64_t)rb * a.nkb * RB + warp * RPW;
+    int sg = lane <= RPW ? __ldg(segw + lane) : 0;
+    if constexpr (!SENT) prefetch_entries(a.ent, __shfl_sync(kFull, sg, 0), __shfl_sync(kFull, sg, RPW), lane);
+
     float acc[RPW][VEC];
-    int cur[RPW], end[RPW], wb[RPW], cw[RPW], co[RPW];
-    float ww[RPW];
 #pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-        const int64_t r = r0 + warp + (int64_t)i * NW;
-        cur[i] = r < a.rows ? __ldg(a.ptr + r) : 0;
-        end[i] = r < a.rows ? __ldg(a.ptr + r + 1) : 0;
-        wb[i] = cur[i];
+    for (int i = 0; i < RPW; ++i)
 #pragma unroll
         for (int v = 0; v < VEC; ++v) acc[i][v] = 0.f;
-    }
-    auto load_window = [&](int i) {
-        const int k = wb[i] + lane;
-        const bool ok = k < end[i];
-        cw[i] = ok ? __ldg(a.idx + k) : INT_MAX;
-        ww[i] = ok ? (CSC ? __ldg(a.vals + __ldg(a.perm + k)) : __ldg(a.vals + k)) : 0.f;
-        co[i] = ok ? cw[i] * (BT * 4) : 0;
-    };
-#pragma unroll
-    for (int i = 0; i < RPW; ++i) load_window(i);
 
     for (int kb = 0; kb < a.nkb; ++kb) {
-        const int64_t kb0 = (int64_t)kb * a.KC;
+        int sgn = 0, ean = 0;
         if (kb + 1 < a.nkb) {
-            const int64_t n0 = kb0 + a.KC;
+            const int64_t n0 = (int64_t)(kb + 1) * a.KC;
             stage_any<BT, NT>(smem + ((kb + 1) & 1) * tile_sz, a.in, n0, (int)std::min<int64_t>(a.KC, a.inner - n0),
                               B, b0, vec4);
+            if constexpr (SENT) ean = stage_ent(kb + 1, (kb + 1) & 1);
             cp_async_commit();
+            sgn = lane <= RPW ? __ldg(segw + (int64_t)(kb + 1) * RB + lane) : 0;
+            if constexpr (!SENT)
+                prefetch_entries(a.ent, __shfl_sync(kFull, sgn, 0), __shfl_sync(kFull, sgn, RPW), lane);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
         __syncthreads();
-        const int kb1 = (int)std::min<int64_t>(kb0 + a.KC, a.inner);
-        // byte base such that base + c*BT*4 addresses tile row (c - kb0), this lane's VEC
-        const char *base = reinterpret_cast<const char *>(smem + (kb & 1) * tile_sz + lane * VEC) -
-                           (size_t)kb0 * BT * 4;
+        const float *tl = smem + (kb & 1) * tile_sz + lane * VEC;
+        const int2 *es = SENT ? ents + (kb & 1) * (a.cap + 2) - ea : a.ent;
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
-            while (cur[i] < end[i]) {
-                int t0 = cur[i] - wb[i];
-                if (t0 >= 32) {  // window exhausted: reload (warp-uniform)
-                    wb[i] = cur[i];
-                    t0 = 0;
-                    load_window(i);
-                }
-                const int L = __popc(__ballot_sync(kFull, cw[i] < kb1));  // ascending: a prefix
-                if (L <= t0) break;
-                // entries t0 .. L-1, 8 at a time: shuffles, then 8 independent
-                // LDS, then the FMAs (entries past L get weight 0, offset 0).
-                for (int g = t0; g < L; g += 8) {
-                    int off[8];
-                    float w[8];
+            const int s0 = __shfl_sync(kFull, sg, i), s1 = __shfl_sync(kFull, sg, i + 1);
+#pragma unroll 4
+            for (int e = s0; e < s1; ++e) {
+                const int2 en = SENT ? es[e] : __ldg(a.ent + e);
+                float x[VEC];
+                lds_vec<VEC>(tl + en.x * BT, x);
+                const float w = __int_as_float(en.y);
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int t = g + u;
-                        const int o = __shfl_sync(kFull, co[i], t);  // lane index wraps mod 32
-                        const float x = __shfl_sync(kFull, ww[i], t);
-                        off[u] = t < L ? o : (int)((size_t)kb0 * BT * 4);
-                        w[u] = t < L ? x : 0.f;
-                    }
-                    float xv[8][VEC];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        lds_vec<VEC>(reinterpret_cast<const float *>(base + off[u]), xv[u]);
-#pragma unroll
-                    for (int u = 0; u < 8; ++u)
-#pragma unroll
-                        for (int v = 0; v < VEC; ++v) acc[i][v] = fmaf(w[u], xv[u][v], acc[i][v]);
-                }
-                cur[i] = wb[i] + L;
-                if (L < 32) break;  // column block (or row) ended inside the window
+                for (int v = 0; v < VEC; ++v) acc[i][v] = fmaf(w, x[v], acc[i][v]);
             }
         }
         __syncthreads();  // everyone done with this buffer before it is refilled
+        sg = sgn;
+        ea = ean;
     }
 
     // Epilogue: ReLU / ReLU' gate fused; each element written once.
     const int64_t bl = b0 + lane * VEC;
 #pragma unroll
     for (int i = 0; i < RPW; ++i) {
-        const int64_t r = r0 + warp + (int64_t)i * NW;
+        const int64_t r = (int64_t)rb * RB + warp * RPW + i;
         if (r >= a.rows) continue;
         float o[VEC];
 #pragma unroll
@@ -170,70 +162,61 @@ __global__ void __launch_bounds__(NW * 32, 1) spmm_tiled_kernel(const SpmmArgs a
 }
 
 constexpr int kNumSMs = 148;
-constexpr int kSmemBudget = 192 * 1024;  // two tile buffers per CTA, 1 CTA / SM
+constexpr int kSmemLimit = 227 * 1024;  // per SM, usable by CTAs
 
-template <int VEC, int RPW, int NW, bool CSC>
-void launch_cfg(int64_t rows, int64_t inner, int64_t B, const int32_t *ptr, const int32_t *idx,
-                const int32_t *perm, const float *vals, const float *in, float *out,
-                const float *gate, int epi, cudaStream_t st) {
+template <int VEC, int RPW, int NW>
+void launch_cfg(const sp_tiling &t, int64_t B, const float *in, float *out, const float *gate, int epi,
+                cudaStream_t st) {
     constexpr int BT = 32 * VEC;
-    int KC = (int)std::min<int64_t>(kSmemBudget / (2 * BT * 4), inner);
-    KC = std::max(KC, 1);
-    // balance the column blocks (same count, smallest equal size)
-    const int nkb = (int)((inner + KC - 1) / KC);
-    KC = (int)((inner + nkb - 1) / nkb);
-    const size_t smem = (size_t)2 * KC * BT * sizeof(float);
-    SpmmArgs a{rows, inner, B, KC, nkb, ptr, idx, perm, vals, in, out, gate};
-    dim3 grid((unsigned)((rows + NW * RPW - 1) / (NW * RPW)), (unsigned)((B + BT - 1) / BT));
+    const size_t tiles = (size_t)2 * t.KC * BT * sizeof(float);
+    // stage the entries too when both buffers fit next to the activation tiles
+    const int cap = (t.max_tile + 2 + 3) & ~3;  // keeps both entry buffers 16-byte aligned
+    const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)kSmemLimit / (NW == 8 ? 2 : 1);
+    const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
+    SpmmArgs a{t.rows, t.inner, B, t.KC, t.nkb, cap, t.seg, t.ent, in, out, gate};
+    dim3 grid((unsigned)t.nrb, (unsigned)((B + BT - 1) / BT));
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         count_launches(1);
         kern<<<grid, NW * 32, smem, st>>>(a);
     };
-    if (epi == EPI_RELU)
-        launch(spmm_tiled_kernel<VEC, RPW, NW, CSC, EPI_RELU>);
-    else if (epi == EPI_GATE)
-        launch(spmm_tiled_kernel<VEC, RPW, NW, CSC, EPI_GATE>);
-    else
-        launch(spmm_tiled_kernel<VEC, RPW, NW, CSC, EPI_NONE>);
+    if (sent) {
+        if (epi == EPI_RELU) launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_RELU, true>);
+        else if (epi == EPI_GATE) launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_GATE, true>);
+        else launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_NONE, true>);
+    } else {
+        if (epi == EPI_RELU) launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_RELU, false>);
+        else if (epi == EPI_GATE) launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_GATE, false>);
+        else launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_NONE, false>);
+    }
 }
 
-template <int VEC, bool CSC>
-void launch_vec(int64_t rows, int64_t inner, int64_t B, const int32_t *ptr, const int32_t *idx,
-                const int32_t *perm, const float *vals, const float *in, float *out,
-                const float *gate, int epi, cudaStream_t st) {
-    // Largest row block (fewest L2 re-reads of `in`) that still fills the
-    // 148 SMs with >= 2 waves of CTAs.
-    constexpr int NW = 16;
-    const int64_t slices = (B + 32 * VEC - 1) / (32 * VEC);
-    auto ctas = [&](int rpw) { return slices * ((rows + NW * rpw - 1) / (NW * rpw)); };
-    if (ctas(8) >= 2 * kNumSMs)
-        launch_cfg<VEC, 8, NW, CSC>(rows, inner, B, ptr, idx, perm, vals, in, out, gate, epi, st);
-    else if (ctas(4) >= 2 * kNumSMs)
-        launch_cfg<VEC, 4, NW, CSC>(rows, inner, B, ptr, idx, perm, vals, in, out, gate, epi, st);
-    else if (ctas(2) >= kNumSMs)
-        launch_cfg<VEC, 2, NW, CSC>(rows, inner, B, ptr, idx, perm, vals, in, out, gate, epi, st);
-    else
-        launch_cfg<VEC, 1, NW, CSC>(rows, inner, B, ptr, idx, perm, vals, in, out, gate, epi, st);
+// variant 0: RB = 128 = 16 warps x 8 rows, KC = 192 (1 CTA / SM);
+// variant 1: RB = 32 = 8 warps x 4 rows, KC = 96 (2 CTAs / SM).
+template <int VEC>
+void launch_variant(const sp_tiling &t, int v, int64_t B, const float *in, float *out, const float *gate,
+                    int epi, cudaStream_t st) {
+    if (v == 0) launch_cfg<VEC, 8, 16>(t, B, in, out, gate, epi, st);
+    else launch_cfg<VEC, 4, 8>(t, B, in, out, gate, epi, st);
 }
 
 }  // namespace
 
-void launch_spmm(int64_t rows, int64_t inner, int64_t B, const int32_t *ptr, const int32_t *idx,
-                 const int32_t *perm, const float *vals, const float *in, float *out,
-                 const float *gate, int epi, int max_seg, cudaStream_t st) {
-    (void)max_seg;
-    const bool csc = perm != nullptr;
-    if (B <= 32) {
-        if (csc) launch_vec<1, true>(rows, inner, B, ptr, idx, perm, vals, in, out, gate, epi, st);
-        else launch_vec<1, false>(rows, inner, B, ptr, idx, perm, vals, in, out, gate, epi, st);
-    } else if (B <= 64 || (B & 3) != 0) {
-        if (csc) launch_vec<2, true>(rows, inner, B, ptr, idx, perm, vals, in, out, gate, epi, st);
-        else launch_vec<2, false>(rows, inner, B, ptr, idx, perm, vals, in, out, gate, epi, st);
-    } else {
-        if (csc) launch_vec<4, true>(rows, inner, B, ptr, idx, perm, vals, in, out, gate, epi, st);
-        else launch_vec<4, false>(rows, inner, B, ptr, idx, perm, vals, in, out, gate, epi, st);
-    }
+void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out,
+                 const float *gate, int epi, cudaStream_t st) {
+    // Choose the largest row block and batch vector that still fill the GPU.
+    int vec = B <= 32 ? 1 : (B <= 64 || (B & 3)) ? 2 : 4;
+    int var = 0;
+    auto ctas = [&](int v, int vv) {
+        return (int64_t)w->til[orient][v].nrb * ((B + 32 * vv - 1) / (32 * vv));
+    };
+    if (ctas(0, vec) < 2 * kNumSMs) var = 1;
+    while (var == 1 && vec > 1 && ctas(1, vec) < 2 * kNumSMs) vec >>= 1;
+    const sp_tiling &t = w->til[orient][var];
+    launch_refresh(t, w->vals, w->nnz, st);
+    if (vec == 4) launch_variant<4>(t, var, B, in, out, gate, epi, st);
+    else if (vec == 2) launch_variant<2>(t, var, B, in, out, gate, epi, st);
+    else launch_variant<1>(t, var, B, in, out, gate, epi, st);
 }
 
 }  // namespace sp
