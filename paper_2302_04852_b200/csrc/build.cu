@@ -8,6 +8,7 @@
 // path (masks change "only a few times", P428).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "sp_internal.cuh"
@@ -153,7 +154,7 @@ __global__ void til_count_kernel(int64_t rows, int nkb, int KC, int RB, const in
     const int lo = lower_bound_i32(idx, ptr[r], ptr[r + 1], kb * KC);
     const int hi = lower_bound_i32(idx, lo, ptr[r + 1], (kb + 1) * KC);
     const int64_t rb = r / RB, lr = r - rb * RB;
-    cnt[(rb * nkb + kb) * RB + lr] = hi - lo;
+    cnt[(rb * nkb + kb) * RB + lr] = (hi - lo + kTilPad - 1) & ~(kTilPad - 1);  // padded segment
 }
 
 __global__ void til_fill_kernel(int64_t rows, int nkb, int KC, int RB, const int32_t *__restrict__ ptr,
@@ -170,8 +171,13 @@ __global__ void til_fill_kernel(int64_t rows, int nkb, int KC, int RB, const int
     int e = seg[(rb * nkb + kb) * RB + lr];
     for (int t = lo; t < hi; ++t, ++e) {
         const int slot = slotmap ? slotmap[t] : t;
-        ent[e] = make_int2(idx[t] - kb * KC, __float_as_int(vals[slot]));
+        ent[e] = make_int2((idx[t] - kb * KC) * kTilRowBytes, __float_as_int(vals[slot]));
         vidx[e] = slot;
+    }
+    const int pad = ((hi - lo + kTilPad - 1) & ~(kTilPad - 1)) - (hi - lo);
+    for (int t = 0; t < pad; ++t, ++e) {  // padding: tile row 0, weight 0, no slot
+        ent[e] = make_int2(0, 0);
+        vidx[e] = -1;
     }
 }
 
@@ -192,7 +198,10 @@ __global__ void til_max_kernel(int64_t ntiles, int RB, const int32_t *__restrict
 __global__ void til_refresh_kernel(int64_t nnz, const int32_t *__restrict__ vidx, const float *__restrict__ vals,
                                    int2 *__restrict__ ent) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < nnz) ent[e].y = __float_as_int(__ldg(vals + __ldg(vidx + e)));
+    if (e < nnz) {
+        const int v = __ldg(vidx + e);
+        if (v >= 0) ent[e].y = __float_as_int(__ldg(vals + v));
+    }
 }
 
 template <typename T>
@@ -285,7 +294,7 @@ fail:
 
 sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
     int64_t *info = nullptr, *mx = nullptr;
-    if (cudaMallocAsync((void **)&info, 2 * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
+    if (cudaMallocAsync((void **)&info, 8 * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
     if (cudaMallocAsync((void **)&mx, 4 * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
     for (int o = 0; o < 2; ++o) {
         const int64_t rows = o == 0 ? w->R : w->C, inner = o == 0 ? w->C : w->R;
@@ -301,30 +310,38 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
             t.nrb = (int)((rows + t.RB - 1) / t.RB);
             t.nkb = (int)((inner + t.KC - 1) / t.KC);
             const int64_t nseg = (int64_t)t.nrb * t.nkb * t.RB;
+            // upper bound on the padded entry count (each segment pads < kTilPad)
+            const int64_t cap = w->nnz + (kTilPad - 1) * std::min<int64_t>(nseg, w->nnz) + 8;
+            t.cap_ent = cap;
             int32_t *cnt = nullptr;
-            if (dmalloc(&t.seg, nseg + 1) != cudaSuccess || dmalloc(&t.ent, w->nnz + 8) != cudaSuccess ||
-                dmalloc(&t.vidx, w->nnz) != cudaSuccess ||
+            if (dmalloc(&t.seg, nseg + 1) != cudaSuccess || dmalloc(&t.ent, cap) != cudaSuccess ||
+                dmalloc(&t.vidx, cap) != cudaSuccess ||
                 cudaMallocAsync((void **)&cnt, (size_t)nseg * sizeof(int32_t), st) != cudaSuccess) {
                 cudaFreeAsync(info, st);
                 cudaFreeAsync(mx, st);
                 return SP_ERR_ALLOC;
             }
             cudaMemsetAsync(cnt, 0, (size_t)nseg * sizeof(int32_t), st);
-            cudaMemsetAsync(t.ent, 0, (size_t)(w->nnz + 8) * sizeof(int2), st);
+            cudaMemsetAsync(t.ent, 0, (size_t)cap * sizeof(int2), st);
+            cudaMemsetAsync(t.vidx, 0xff, (size_t)cap * sizeof(int32_t), st);  // -1: no slot
             const int64_t nt = rows * t.nkb;
             til_count_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, t.nkb, t.KC, t.RB, ptr, idx, cnt);
-            scan_kernel<<<1, kScanThreads, 0, st>>>(nseg, cnt, t.seg, info);
+            scan_kernel<<<1, kScanThreads, 0, st>>>(nseg, cnt, t.seg, info + 2 * (o * 2 + v));
             til_fill_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, t.nkb, t.KC, t.RB, ptr, idx,
                                                                          slotmap, t.seg, w->vals, t.ent, t.vidx);
             til_max_kernel<<<1, 256, 0, st>>>((int64_t)t.nrb * t.nkb, t.RB, t.seg, mx + (o * 2 + v));
             cudaFreeAsync(cnt, st);
         }
     }
-    int64_t h[4];
+    int64_t h[4], hi[8];
     cudaMemcpyAsync(h, mx, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hi, info, sizeof(hi), cudaMemcpyDeviceToHost, st);
     const cudaError_t e = cudaStreamSynchronize(st);  // second (last) host sync of sp_weight_create
     for (int o = 0; o < 2; ++o)
-        for (int v = 0; v < 2; ++v) w->til[o][v].max_tile = (int32_t)h[o * 2 + v];
+        for (int v = 0; v < 2; ++v) {
+            w->til[o][v].max_tile = (int32_t)h[o * 2 + v];
+            w->til[o][v].npad = hi[2 * (o * 2 + v)];  // padded entry total
+        }
     cudaFreeAsync(info, st);
     cudaFreeAsync(mx, st);
     return (e == cudaSuccess && cudaGetLastError() == cudaSuccess) ? SP_OK : SP_ERR_CUDA;
@@ -345,7 +362,7 @@ void free_tilings(sp_weight_s *w) {
 void launch_refresh(const sp_tiling &t, const float *vals, int64_t nnz, cudaStream_t st) {
     if (nnz > 0) {
         count_launches(1);
-        til_refresh_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, st>>>(nnz, t.vidx, vals, t.ent);
+        til_refresh_kernel<<<(unsigned)((t.npad + 255) / 256), 256, 0, st>>>(t.npad, t.vidx, vals, t.ent);
     }
 }
 

@@ -135,8 +135,13 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) sddmm_tiled_kernel(c
             cp_async_wait<0>();
         }
         __syncthreads();
-        const float *tl = smem + (q & 1) * tile_sz + lane * VEC;
+        constexpr int SH = VEC == 4 ? 0 : VEC == 2 ? 1 : 2;
+        const char *tb = reinterpret_cast<const char *>(smem + (q & 1) * tile_sz + lane * VEC);
         const int2 *es = SENT ? ents + (q & 1) * (a.cap + 2) - ea : a.ent;
+        auto xrow = [&](int e) -> const float * {
+            const int off = SENT ? es[e].x : __ldg(&a.ent[e].x);
+            return reinterpret_cast<const float *>(tb + (off >> SH));
+        };
 #pragma unroll
         for (int m = 0; m < RPW; m += 2) {
             int pa = __shfl_sync(kFull, sg, m);
@@ -144,6 +149,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) sddmm_tiled_kernel(c
             int pb = a1;
             const int b1 = __shfl_sync(kFull, sg, m + 2);
             while (pa < a1 || pb < b1) {
+                // segments are padded to multiples of 4: whole groups only
                 const int na = min(16, a1 - pa), nb = min(16, b1 - pb);
                 float acc[32];
 #pragma unroll
@@ -152,13 +158,11 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) sddmm_tiled_kernel(c
                 for (int g = 0; g < 16; g += 4) {
                     if (g < na) {
 #pragma unroll
-                        for (int u = g; u < g + 4; ++u)
-                            if (u < na) acc[u] = dotv<VEC>(rv[m], tl + (SENT ? es[pa + u].x : __ldg(&a.ent[pa + u].x)) * BT);
+                        for (int u = g; u < g + 4; ++u) acc[u] = dotv<VEC>(rv[m], xrow(pa + u));
                     }
                     if (g < nb) {
 #pragma unroll
-                        for (int u = g; u < g + 4; ++u)
-                            if (u < nb) acc[16 + u] = dotv<VEC>(rv[m + 1], tl + (SENT ? es[pb + u].x : __ldg(&a.ent[pb + u].x)) * BT);
+                        for (int u = g; u < g + 4; ++u) acc[16 + u] = dotv<VEC>(rv[m + 1], xrow(pb + u));
                     }
                 }
                 const float sum = transpose_reduce32(acc, lane);
@@ -166,8 +170,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) sddmm_tiled_kernel(c
                 const bool mine = lane < 16 ? u < na : u < nb;
                 if (mine) {
                     const int e = (lane < 16 ? pa : pb) + u;
-                    float *p = a.direct ? P + __ldg(a.vidx + e) : P + e;
-                    *p = (s == 0) ? sum : *p + sum;
+                    if (a.direct) {
+                        const int v = __ldg(a.vidx + e);
+                        if (v >= 0) P[v] = (s == 0) ? sum : P[v] + sum;
+                    } else {
+                        P[e] = (s == 0) ? sum : P[e] + sum;
+                    }
                 }
                 pa += na;
                 pb += nb;
@@ -183,9 +191,11 @@ __global__ void split_reduce_kernel(int64_t nnz, int nsplit, const float *__rest
                                     const int32_t *__restrict__ vidx, float *__restrict__ dW) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= nnz) return;
+    const int v = vidx[e];
+    if (v < 0) return;  // padding entry
     float s = part[e];
     for (int i = 1; i < nsplit; ++i) s += part[(int64_t)i * nnz + e];
-    dW[vidx[e]] = s;
+    dW[v] = s;
 }
 
 constexpr int kNumSMs = 148;
@@ -194,9 +204,9 @@ template <int VEC, int RPW, int NW>
 sp_status launch_cfg(const sp_weight_s *w, const sp_tiling &t, const float *regop, const float *smemop,
                      float *dW, int64_t B, int ctas_per_sm, cudaStream_t st) {
     constexpr int BT = 32 * VEC;
-    const int64_t nnz = w->nnz;
+    const int64_t nnz = t.npad;  // partials are kept per (padded) entry
     const int64_t slices = (B + BT - 1) / BT;
-    const int64_t want = (int64_t)ctas_per_sm * kNumSMs;
+    const int64_t want = (int64_t)ctas_per_sm * kNumSMs * 4;  // >= 4 waves: small tail
     int64_t nsplit = std::max<int64_t>(1, std::min<int64_t>(slices, (want + t.nrb - 1) / t.nrb));
     const int64_t spl = (slices + nsplit - 1) / nsplit;
     nsplit = (slices + spl - 1) / spl;

@@ -4,6 +4,7 @@
 // translation units of the CUDA path.  Nothing here is shared with oracle/.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -26,7 +27,9 @@ struct sp_tiling {
     int32_t *seg;   // [nrb*nkb*RB + 1]
     int2 *ent;      // [nnz + 8] (padded)
     int32_t *vidx;  // [nnz]
-    int32_t max_tile;  // max entries in one (row block, column block) tile
+    int32_t max_tile;  // max (padded) entries in one (row block, column block) tile
+    int64_t npad;      // padded entry total (segments padded to kTilPad with weight-0 entries)
+    int64_t cap_ent;   // allocated entries
 };
 
 struct sp_weight_s {
@@ -50,6 +53,12 @@ struct sp_weight_s {
 // Tiling variants (RB rows per CTA, KC inner columns per shared-memory tile).
 constexpr int kTilRB[2] = {128, 32};
 constexpr int kTilKC[2] = {192, 96};
+// Segments are padded to a multiple of kTilPad entries (weight 0, tile row 0,
+// vidx -1) so the kernels run tail-free groups of 4.  Entry columns are stored
+// as byte offsets of a 128-float tile row (kTilRowBytes); kernels with
+// narrower tiles shift them down.
+constexpr int kTilPad = 4;
+constexpr int kTilRowBytes = 512;
 
 namespace sp {
 
@@ -62,6 +71,12 @@ void count_launches(int n);
 sp_status check_launch(const char *what);
 
 inline cudaStream_t S(sp_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- tmap.cu ----
+// Tensor map of a row-major fp32 [rows x B] activation (B % 4 == 0) with a
+// box of `box_rows` rows x `box_cols` batch columns, no swizzle, zero OOB
+// fill.  Returns false if the driver entry point is unavailable.
+bool make_tmap_2d(CUtensorMap *map, const float *base, int64_t rows, int64_t B, int box_cols, int box_rows);
 
 // ---- build.cu ----
 sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *mask,

@@ -32,6 +32,7 @@ namespace {
 struct SpmmArgs {
     int64_t rows, inner, B;
     int KC, nkb, cap;  // cap: entry-buffer capacity (entries) when staged
+    int tma;           // 1: stage with TMA (tensor map valid), 0: synchronous path
     const int32_t *seg;
     const int2 *ent;
     const float *in;
@@ -49,39 +50,59 @@ __device__ __forceinline__ void prefetch_entries(const int2 *ent, int e0, int e1
     for (int l = l0 + lane; l < l1; l += 32) prefetch_l1(ent + ((int64_t)l << 4));
 }
 
-// SENT: the tile's entries are staged in shared memory too (cp.async, next
-// tile's entries prefetched with its activation tile); otherwise entries are
-// read with warp-uniform global loads (tiles larger than the entry buffer).
+// SENT: the tile's entries are staged in shared memory too (next tile's
+// entries arrive with its activation tile); otherwise entries are read with
+// warp-uniform global loads (tiles larger than the entry buffer).
+// Staging: B % 4 == 0 -> TMA bulk copies (one per tile row, UBLKCP) issued by
+// warp 0 into a double buffer, completion on one mbarrier per buffer;
+// otherwise (ragged B) a synchronous per-element path.
 template <int VEC, int RPW, int NW, int EPI, bool SENT>
-__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) spmm_tiled_kernel(const SpmmArgs a) {
+__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
+    spmm_tiled_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr int BT = 32 * VEC;
     constexpr int NT = NW * 32;
     constexpr int RB = NW * RPW;
-    extern __shared__ __align__(16) float smem[];  // [2][KC][BT] floats, then [2][cap+2] int2
+    extern __shared__ __align__(128) float smem[];  // [2][KC][BT] floats, [2][cap+2] int2
+    __shared__ uint64_t full[2];
     int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * a.KC * BT);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int rb = blockIdx.x;
     const int64_t b0 = (int64_t)blockIdx.y * BT;
     const int64_t B = a.B;
-    const bool vec4 = (B & 3) == 0;
+    const bool vec4 = a.tma != 0;  // TMA path (B % 4 == 0 and a tensor map)
     const size_t tile_sz = (size_t)a.KC * BT;
+    const int ebuf = a.cap + 2;
 
-    // stage the entries of tile kb into buffer buf; returns the (even) index
-    // of the first staged entry
-    auto stage_ent = [&](int kb, int buf) -> int {
+    if (threadIdx.x == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    // issue tile kb into buffer buf (warp 0 only, TMA path); returns the even
+    // index of the first staged entry
+    auto entry_range = [&](int kb, int &e0, int &e1) {
         const int64_t tb = ((int64_t)rb * a.nkb + kb) * RB;
-        const int e0 = __ldg(a.seg + tb) & ~1, e1 = __ldg(a.seg + tb + RB);
-        const int n16 = (e1 - e0 + 1) >> 1;
-        int2 *dst = ents + buf * (a.cap + 2);
-        for (int i = threadIdx.x; i < n16; i += NT) cp_async16(dst + 2 * i, a.ent + e0 + 2 * i, 16);
-        return e0;
+        e0 = __ldg(a.seg + tb) & ~1;
+        e1 = __ldg(a.seg + tb + RB);
     };
-
-    stage_any<BT, NT>(smem, a.in, 0, (int)std::min<int64_t>(a.KC, a.inner), B, b0, vec4);
-    int ea = 0;
-    if constexpr (SENT) ea = stage_ent(0, 0);
-    cp_async_commit();
+    auto issue = [&](int kb, int buf) {
+        const int64_t k0 = (int64_t)kb * a.KC;
+        const int nk = (int)std::min<int64_t>(a.KC, a.inner - k0);
+        int e0 = 0, e1 = 0;
+        if constexpr (SENT) entry_range(kb, e0, e1);
+        (void)nk;
+        const unsigned eb = SENT ? (unsigned)(((e1 - e0) * 8 + 15) & ~15) : 0u;
+        if (lane == 0) {
+            // the box is always KC x BT floats (OOB rows / columns zero-filled)
+            mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
+            tma_load_2d(smem + buf * tile_sz, &tmap, (int)b0, (int)k0, &full[buf]);
+            if (eb) tma_load_1d(ents + buf * ebuf, a.ent + e0, eb, &full[buf]);
+        }
+    };
+    if (vec4 && warp == 0) issue(0, 0);
 
     // lane l <= RPW holds the l-th segment bound of this warp's rows in the
     // current tile (rows rb*RB + warp*RPW + i).
@@ -96,39 +117,55 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) spmm_tiled_kernel(co
         for (int v = 0; v < VEC; ++v) acc[i][v] = 0.f;
 
     for (int kb = 0; kb < a.nkb; ++kb) {
-        int sgn = 0, ean = 0;
+        const int buf = kb & 1;
+        int sgn = 0;
         if (kb + 1 < a.nkb) {
-            const int64_t n0 = (int64_t)(kb + 1) * a.KC;
-            stage_any<BT, NT>(smem + ((kb + 1) & 1) * tile_sz, a.in, n0, (int)std::min<int64_t>(a.KC, a.inner - n0),
-                              B, b0, vec4);
-            if constexpr (SENT) ean = stage_ent(kb + 1, (kb + 1) & 1);
-            cp_async_commit();
+            if (vec4 && warp == 0) issue(kb + 1, buf ^ 1);
             sgn = lane <= RPW ? __ldg(segw + (int64_t)(kb + 1) * RB + lane) : 0;
             if constexpr (!SENT)
                 prefetch_entries(a.ent, __shfl_sync(kFull, sgn, 0), __shfl_sync(kFull, sgn, RPW), lane);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
         }
-        __syncthreads();
-        const float *tl = smem + (kb & 1) * tile_sz + lane * VEC;
-        const int2 *es = SENT ? ents + (kb & 1) * (a.cap + 2) - ea : a.ent;
+        int ea = 0;
+        if (vec4) {
+            mbar_wait(&full[buf], (kb >> 1) & 1);
+            if constexpr (SENT) {
+                int e1;
+                entry_range(kb, ea, e1);
+            }
+        } else {  // ragged B: synchronous staging of this tile
+            const int64_t k0 = (int64_t)kb * a.KC;
+            stage_tile<BT, NT>(smem + buf * tile_sz, a.in, k0, (int)std::min<int64_t>(a.KC, a.inner - k0), B, b0,
+                               false);
+            if constexpr (SENT) {
+                int e1;
+                entry_range(kb, ea, e1);
+                for (int i = threadIdx.x; i < e1 - ea; i += NT) ents[buf * ebuf + i] = __ldg(a.ent + ea + i);
+            }
+            __syncthreads();
+        }
+        // tile row byte offsets are stored for 128-float rows; narrower tiles shift
+        constexpr int SH = VEC == 4 ? 0 : VEC == 2 ? 1 : 2;
+        const char *tb = reinterpret_cast<const char *>(smem + buf * tile_sz + lane * VEC);
+        const int2 *es = SENT ? ents + buf * ebuf - ea : a.ent;
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
             const int s0 = __shfl_sync(kFull, sg, i), s1 = __shfl_sync(kFull, sg, i + 1);
-#pragma unroll 4
-            for (int e = s0; e < s1; ++e) {
-                const int2 en = SENT ? es[e] : __ldg(a.ent + e);
-                float x[VEC];
-                lds_vec<VEC>(tl + en.x * BT, x);
-                const float w = __int_as_float(en.y);
+            // segments are padded to multiples of 4 (weight-0 entries): no tail
+            for (int e = s0; e < s1; e += 4) {
+                int2 en[4];
 #pragma unroll
-                for (int v = 0; v < VEC; ++v) acc[i][v] = fmaf(w, x[v], acc[i][v]);
+                for (int u = 0; u < 4; ++u) en[u] = SENT ? es[e + u] : __ldg(a.ent + e + u);
+                float x[4][VEC];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) lds_vec<VEC>(reinterpret_cast<const float *>(tb + (en[u].x >> SH)), x[u]);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) acc[i][v] = fmaf(__int_as_float(en[u].y), x[u][v], acc[i][v]);
             }
         }
         __syncthreads();  // everyone done with this buffer before it is refilled
         sg = sgn;
-        ea = ean;
     }
 
     // Epilogue: ReLU / ReLU' gate fused; each element written once.
@@ -162,7 +199,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) spmm_tiled_kernel(co
 }
 
 constexpr int kNumSMs = 148;
-constexpr int kSmemLimit = 227 * 1024;  // per SM, usable by CTAs
+constexpr int kSmemLimit = 226 * 1024;  // per SM, usable by CTAs (minus static mbarriers)
 
 template <int VEC, int RPW, int NW>
 void launch_cfg(const sp_tiling &t, int64_t B, const float *in, float *out, const float *gate, int epi,
@@ -173,12 +210,14 @@ void launch_cfg(const sp_tiling &t, int64_t B, const float *in, float *out, cons
     const int cap = (t.max_tile + 2 + 3) & ~3;  // keeps both entry buffers 16-byte aligned
     const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)kSmemLimit / (NW == 8 ? 2 : 1);
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
-    SpmmArgs a{t.rows, t.inner, B, t.KC, t.nkb, cap, t.seg, t.ent, in, out, gate};
+    CUtensorMap tmap{};
+    const bool tma = (B & 3) == 0 && make_tmap_2d(&tmap, in, t.inner, B, BT, t.KC);
+    SpmmArgs a{t.rows, t.inner, B, t.KC, t.nkb, cap, tma ? 1 : 0, t.seg, t.ent, in, out, gate};
     dim3 grid((unsigned)t.nrb, (unsigned)((B + BT - 1) / BT));
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         count_launches(1);
-        kern<<<grid, NW * 32, smem, st>>>(a);
+        kern<<<grid, NW * 32, smem, st>>>(a, tmap);
     };
     if (sent) {
         if (epi == EPI_RELU) launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_RELU, true>);

@@ -2,6 +2,7 @@
 // helpers used by the SpMM and SDDMM kernels.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -108,6 +109,65 @@ __device__ __forceinline__ void stage_any(float *tile, const float *src, int64_t
         stage_tile_async<BT, NT>(tile, src, k0, nk, B, b0);
     else
         stage_tile<BT, NT>(tile, src, k0, nk, B, b0, false);
+}
+
+// ---- TMA (cp.async.bulk) + mbarrier helpers ------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+// make mbarrier inits visible to the async (TMA) proxy
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        "@!P bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> shared (UBLKCP), completion counted on `bar`.
+// bytes % 16 == 0, both addresses 16-byte aligned.
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// 2-D tensor TMA (UTMALDG): box at (batch c0, row c1) of the tensor map into
+// dst; out-of-bounds rows / batch columns are zero-filled by the hardware.
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Issue (from one warp) the TMA copies of rows [k0, k0+nk) x batch columns
+// [b0, b0 + min(BT, B-b0)) of a [rows x B] activation (B % 4 == 0) into
+// tile[nk][BT], plus optionally `ebytes` of entries, all on `bar`.
+template <int BT>
+__device__ __forceinline__ void tma_stage_tile(float *tile, const float *src, int64_t k0, int nk, int64_t B,
+                                               int64_t b0, uint64_t *bar, void *edst, const void *esrc,
+                                               unsigned ebytes, int lane) {
+    const int ncol = (int)(B - b0 < BT ? B - b0 : BT);
+    const unsigned rb = (unsigned)ncol * 4u;
+    if (lane == 0) mbar_arrive_expect_tx(bar, rb * (unsigned)nk + ebytes);
+    __syncwarp();
+    for (int k = lane; k < nk; k += 32) tma_load_1d(tile + (size_t)k * BT, src + (k0 + k) * B + b0, rb, bar);
+    if (lane == 0 && ebytes) tma_load_1d(edst, esrc, ebytes, bar);
 }
 
 // Warp transpose-reduce of 32 per-lane partials: on return, lane t holds
