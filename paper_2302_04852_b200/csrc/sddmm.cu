@@ -30,6 +30,7 @@ struct SddmmArgs {
     int64_t nrow, F, B;
     int KC, nkb, spl;        // column block, #column blocks, slices per split
     int cap;                 // entry-buffer capacity when entries are staged
+    int tma;                 // 1: TMA staging (tensor map valid), 0: synchronous path
     const int32_t *seg;
     const int2 *ent;
     const int32_t *vidx;
@@ -55,12 +56,14 @@ __device__ __forceinline__ float dotv(const float (&a)[VEC], const float *p) {
 }
 
 template <int VEC, int RPW, int NW, bool SENT>
-__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) sddmm_tiled_kernel(const SddmmArgs a) {
+__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
+    sddmm_tiled_kernel(const SddmmArgs a, const __grid_constant__ CUtensorMap tmap) {
     static_assert(RPW % 2 == 0, "rows are processed in pairs");
     constexpr int BT = 32 * VEC;
     constexpr int NT = NW * 32;
     constexpr int RB = NW * RPW;
-    extern __shared__ __align__(16) float smem[];  // [2][KC][BT] floats, then [2][cap+2] int2
+    extern __shared__ __align__(128) float smem[];  // [2][KC][BT] floats, then [2][cap+2] int2
+    __shared__ uint64_t full[2];
     int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * a.KC * BT);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -74,25 +77,30 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) sddmm_tiled_kernel(c
     const size_t tile_sz = (size_t)a.KC * BT;
     const int32_t *segw = a.seg + (int64_t)rb * a.nkb * RB + warp * RPW;
 
-    // stage tile q (activations, and the entries when SENT); returns the
-    // (even) index of the first staged entry
-    auto stage = [&](int q, int buf) -> int {
-        const int s = q / a.nkb, kb = q - s * a.nkb;
-        const int64_t k0 = (int64_t)kb * a.KC;
-        stage_any<BT, NT>(smem + buf * tile_sz, a.smemop, k0, (int)std::min<int64_t>(a.KC, a.F - k0), B,
-                          s_lo + (int64_t)s * BT, vec4);
-        if constexpr (SENT) {
-            const int64_t tb = ((int64_t)rb * a.nkb + kb) * RB;
-            const int e0 = __ldg(a.seg + tb) & ~1, e1 = __ldg(a.seg + tb + RB);
-            const int n16 = (e1 - e0 + 1) >> 1;
-            int2 *dst = ents + buf * (a.cap + 2);
-            for (int i = threadIdx.x; i < n16; i += NT) cp_async16(dst + 2 * i, a.ent + e0 + 2 * i, 16);
-            return e0;
-        }
-        return 0;
+    const int ebuf = a.cap + 2;
+    const bool tma = a.tma != 0;
+    if (threadIdx.x == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto entry_range = [&](int kb, int &e0, int &e1) {
+        const int64_t tb = ((int64_t)rb * a.nkb + kb) * RB;
+        e0 = __ldg(a.seg + tb) & ~1;
+        e1 = __ldg(a.seg + tb + RB);
     };
-    int ea = stage(0, 0);
-    cp_async_commit();
+    // tile q = (slice q / nkb, column block q % nkb): TMA issue by one thread
+    auto issue = [&](int q, int buf) {
+        const int s = q / a.nkb, kb = q - s * a.nkb;
+        int e0 = 0, e1 = 0;
+        if constexpr (SENT) entry_range(kb, e0, e1);
+        const unsigned eb = SENT ? (unsigned)(((e1 - e0) * 8 + 15) & ~15) : 0u;
+        mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
+        tma_load_2d(smem + buf * tile_sz, &tmap, (int)(s_lo + (int64_t)s * BT), kb * a.KC, &full[buf]);
+        if (eb) tma_load_1d(ents + buf * ebuf, a.ent + e0, eb, &full[buf]);
+    };
+    if (tma && threadIdx.x == 0) issue(0, 0);
 
     float rv[RPW][VEC];
     int sg = 0;
@@ -119,10 +127,9 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) sddmm_tiled_kernel(c
             }
         }
         sg = lane <= RPW ? __ldg(segw + (int64_t)kb * RB + lane) : 0;
-        int ean = 0;
+        const int buf = q & 1;
         if (q + 1 < ntile) {
-            ean = stage(q + 1, (q + 1) & 1);
-            cp_async_commit();
+            if (tma && threadIdx.x == 0) issue(q + 1, buf ^ 1);
             if constexpr (!SENT) {  // entries of the next column block into L1
                 const int kbn = (q + 1) % a.nkb;
                 const int sn = lane <= RPW ? __ldg(segw + (int64_t)kbn * RB + lane) : 0;
@@ -130,14 +137,28 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) sddmm_tiled_kernel(c
                 for (int l = (e0 >> 4) + lane; l < ((e1 + 15) >> 4); l += 32)
                     prefetch_l1(a.ent + ((int64_t)l << 4));
             }
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
         }
-        __syncthreads();
+        int ea = 0;
+        if (tma) {
+            mbar_wait(&full[buf], (q >> 1) & 1);
+            if constexpr (SENT) {
+                int e1;
+                entry_range(kb, ea, e1);
+            }
+        } else {  // ragged B: synchronous staging of this tile
+            const int64_t k0 = (int64_t)kb * a.KC;
+            stage_tile<BT, NT>(smem + buf * tile_sz, a.smemop, k0, (int)std::min<int64_t>(a.KC, a.F - k0), B,
+                               s_lo + (int64_t)s * BT, false);
+            if constexpr (SENT) {
+                int e1;
+                entry_range(kb, ea, e1);
+                for (int i = threadIdx.x; i < e1 - ea; i += NT) ents[buf * ebuf + i] = __ldg(a.ent + ea + i);
+            }
+            __syncthreads();
+        }
         constexpr int SH = VEC == 4 ? 0 : VEC == 2 ? 1 : 2;
-        const char *tb = reinterpret_cast<const char *>(smem + (q & 1) * tile_sz + lane * VEC);
-        const int2 *es = SENT ? ents + (q & 1) * (a.cap + 2) - ea : a.ent;
+        const char *tb = reinterpret_cast<const char *>(smem + buf * tile_sz + lane * VEC);
+        const int2 *es = SENT ? ents + buf * ebuf - ea : a.ent;
         auto xrow = [&](int e) -> const float * {
             const int off = SENT ? es[e].x : __ldg(&a.ent[e].x);
             return reinterpret_cast<const float *>(tb + (off >> SH));
@@ -181,8 +202,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) sddmm_tiled_kernel(c
                 pb += nb;
             }
         }
-        __syncthreads();
-        ea = ean;
+        __syncthreads();  // buffer free before it is refilled
     }
 }
 
@@ -212,7 +232,7 @@ sp_status launch_cfg(const sp_weight_s *w, const sp_tiling &t, const float *rego
     nsplit = (slices + spl - 1) / spl;
     const size_t tiles = (size_t)2 * t.KC * BT * sizeof(float);
     const int cap = (t.max_tile + 2 + 3) & ~3;  // keeps both entry buffers 16-byte aligned
-    const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)(227 * 1024) / (NW == 8 ? 2 : 1);
+    const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)(226 * 1024) / (NW == 8 ? 2 : 1);
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
     const bool direct = nsplit == 1;
     float *part = dW;
@@ -222,12 +242,14 @@ sp_status launch_cfg(const sp_weight_s *w, const sp_tiling &t, const float *rego
             return SP_ERR_ALLOC;
         }
     }
-    SddmmArgs a{t.rows, t.inner, B, t.KC, t.nkb, (int)spl, cap, t.seg, t.ent, t.vidx, regop, smemop, part, nnz,
-                direct ? 1 : 0};
+    CUtensorMap tmap{};
+    const bool tma = (B & 3) == 0 && make_tmap_2d(&tmap, smemop, t.inner, B, BT, t.KC);
+    SddmmArgs a{t.rows, t.inner, B, t.KC, t.nkb, (int)spl, cap, tma ? 1 : 0, t.seg, t.ent, t.vidx, regop, smemop,
+                part, nnz, direct ? 1 : 0};
     auto kern = sent ? sddmm_tiled_kernel<VEC, RPW, NW, true> : sddmm_tiled_kernel<VEC, RPW, NW, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     count_launches(direct ? 1 : 2);
-    kern<<<dim3((unsigned)t.nrb, (unsigned)nsplit), NW * 32, smem, st>>>(a);
+    kern<<<dim3((unsigned)t.nrb, (unsigned)nsplit), NW * 32, smem, st>>>(a, tmap);
     if (!direct) {
         split_reduce_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, st>>>(nnz, (int)nsplit, part, t.vidx, dW);
         cudaFreeAsync(part, st);
