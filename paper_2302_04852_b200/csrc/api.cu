@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
 #include <cstdio>
 #include <new>
 #include <string>
@@ -88,6 +89,25 @@ sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8
     if (R < 1 || C < 1) return fail(SP_ERR_SHAPE, "sp_weight_create: R and C must be >= 1");
     if (R > kI32Max || C > kI32Max || R * C > kI32Max)
         return fail(SP_ERR_OVERFLOW, "sp_weight_create: R*C must fit int32");
+    {
+        // Scratch buffers (SDDMM split partials) come from the stream-ordered
+        // default pool; keep freed memory cached instead of returning it to
+        // the OS at every synchronisation (which made launches pay page
+        // mapping costs).  Once per device.
+        static std::mutex mu;
+        static bool done[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev >= 0 && dev < 64 && !done[dev]) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            done[dev] = true;
+        }
+    }
     sp_weight_s *w = new (std::nothrow) sp_weight_s();
     if (!w) return fail(SP_ERR_ALLOC, "sp_weight_create: host allocation failed");
     w->magic = SP_MAGIC;

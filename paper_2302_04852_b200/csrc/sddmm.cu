@@ -159,9 +159,22 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
         constexpr int SH = VEC == 4 ? 0 : VEC == 2 ? 1 : 2;
         const char *tb = reinterpret_cast<const char *>(smem + buf * tile_sz + lane * VEC);
         const int2 *es = SENT ? ents + buf * ebuf - ea : a.ent;
-        auto xrow = [&](int e) -> const float * {
-            const int off = SENT ? es[e].x : __ldg(&a.ent[e].x);
-            return reinterpret_cast<const float *>(tb + (off >> SH));
+        // dot of the register-operand slice with tile row of entry e (0 for padding)
+        auto dot_e = [&](const float(&r)[VEC], int off) -> float {
+            float x[VEC];
+            lds_row_or_zero<VEC, SH>(tb, off, x);
+            float d = 0.f;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) d = fmaf(r[v], x[v], d);
+            return d;
+        };
+        auto offs4 = [&](int e, int (&o)[4]) {
+            const int4 p01 = ld_entry_pair(SENT ? es + e : a.ent + e, SENT);
+            const int4 p23 = ld_entry_pair(SENT ? es + e + 2 : a.ent + e + 2, SENT);
+            o[0] = p01.x;
+            o[1] = p01.z;
+            o[2] = p23.x;
+            o[3] = p23.z;
         };
 #pragma unroll
         for (int m = 0; m < RPW; m += 2) {
@@ -178,12 +191,16 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
 #pragma unroll
                 for (int g = 0; g < 16; g += 4) {
                     if (g < na) {
+                        int o[4];
+                        offs4(pa + g, o);
 #pragma unroll
-                        for (int u = g; u < g + 4; ++u) acc[u] = dotv<VEC>(rv[m], xrow(pa + u));
+                        for (int u = 0; u < 4; ++u) acc[g + u] = dot_e(rv[m], o[u]);
                     }
                     if (g < nb) {
+                        int o[4];
+                        offs4(pb + g, o);
 #pragma unroll
-                        for (int u = g; u < g + 4; ++u) acc[16 + u] = dotv<VEC>(rv[m + 1], xrow(pb + u));
+                        for (int u = 0; u < 4; ++u) acc[16 + g + u] = dot_e(rv[m + 1], o[u]);
                     }
                 }
                 const float sum = transpose_reduce32(acc, lane);

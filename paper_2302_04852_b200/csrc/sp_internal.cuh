@@ -53,8 +53,9 @@ struct sp_weight_s {
 // Tiling variants (RB rows per CTA, KC inner columns per shared-memory tile).
 constexpr int kTilRB[2] = {128, 32};
 constexpr int kTilKC[2] = {192, 96};
-// Segments are padded to a multiple of kTilPad entries (weight 0, tile row 0,
-// vidx -1) so the kernels run tail-free groups of 4.  Entry columns are stored
+// Segments are padded to a multiple of kTilPad entries (offset -1 = no load,
+// weight 0, vidx -1) so the kernels run tail-free groups of 4; every segment
+// starts at a multiple of 4 entries (16-byte aligned pairs).  Entry columns are stored
 // as byte offsets of a 128-float tile row (kTilRowBytes); kernels with
 // narrower tiles shift them down.
 constexpr int kTilPad = 4;

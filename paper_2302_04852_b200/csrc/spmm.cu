@@ -152,16 +152,19 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
             const int s0 = __shfl_sync(kFull, sg, i), s1 = __shfl_sync(kFull, sg, i + 1);
             // segments are padded to multiples of 4 (weight-0 entries): no tail
             for (int e = s0; e < s1; e += 4) {
-                int2 en[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) en[u] = SENT ? es[e + u] : __ldg(a.ent + e + u);
+                // 4 entries in two 16-byte broadcast loads
+                const int4 p01 = ld_entry_pair(SENT ? es + e : a.ent + e, SENT);
+                const int4 p23 = ld_entry_pair(SENT ? es + e + 2 : a.ent + e + 2, SENT);
+                const int off[4] = {p01.x, p01.z, p23.x, p23.z};
+                const float w[4] = {__int_as_float(p01.y), __int_as_float(p01.w), __int_as_float(p23.y),
+                                    __int_as_float(p23.w)};
                 float x[4][VEC];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) lds_vec<VEC>(reinterpret_cast<const float *>(tb + (en[u].x >> SH)), x[u]);
+                for (int u = 0; u < 4; ++u) lds_row_or_zero<VEC, SH>(tb, off[u], x[u]);
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
 #pragma unroll
-                    for (int v = 0; v < VEC; ++v) acc[i][v] = fmaf(__int_as_float(en[u].y), x[u][v], acc[i][v]);
+                    for (int v = 0; v < VEC; ++v) acc[i][v] = fmaf(w[u], x[u][v], acc[i][v]);
             }
         }
         __syncthreads();  // everyone done with this buffer before it is refilled

@@ -42,6 +42,20 @@ __device__ __forceinline__ void lds_vec(const float *p, float (&v)[VEC]) {
     }
 }
 
+// Two consecutive (offset, value) entries in one 16-byte load.
+__device__ __forceinline__ int4 ld_entry_pair(const int2 *p, bool smem) {
+    return smem ? *reinterpret_cast<const int4 *>(p) : __ldg(reinterpret_cast<const int4 *>(p));
+}
+
+// VEC-wide load of tile row `off` (bytes from `tb`) or zeros for a padding
+// entry (off < 0): the predicated-off load costs no shared-memory bandwidth.
+template <int VEC, int SH>
+__device__ __forceinline__ void lds_row_or_zero(const char *tb, int off, float (&v)[VEC]) {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) v[i] = 0.f;
+    if (off >= 0) lds_vec<VEC>(reinterpret_cast<const float *>(tb + (off >> SH)), v);
+}
+
 // Stage rows [k0, k0+nk) x batch columns [b0, b0+BT) of a row-major
 // [nrows x B] fp32 activation into smem tile[nk][BT] (row stride BT),
 // zero-filling batch columns >= B.  16-byte vector path when B % 4 == 0.
