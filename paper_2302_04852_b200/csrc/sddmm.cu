@@ -263,10 +263,12 @@ sp_status launch_cfg(const sp_weight_s *w, const sp_tiling &t, const float *rego
     const bool tma = (B & 3) == 0 && make_tmap_2d(&tmap, smemop, t.inner, B, BT, t.KC);
     SddmmArgs a{t.rows, t.inner, B, t.KC, t.nkb, (int)spl, cap, tma ? 1 : 0, t.seg, t.ent, t.vidx, regop, smemop,
                 part, nnz, direct ? 1 : 0};
-    auto kern = sent ? sddmm_tiled_kernel<VEC, RPW, NW, true> : sddmm_tiled_kernel<VEC, RPW, NW, false>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     count_launches(direct ? 1 : 2);
-    kern<<<dim3((unsigned)t.nrb, (unsigned)nsplit), NW * 32, smem, st>>>(a, tmap);
+    {
+        auto kern = sent ? sddmm_tiled_kernel<VEC, RPW, NW, true> : sddmm_tiled_kernel<VEC, RPW, NW, false>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<dim3((unsigned)t.nrb, (unsigned)nsplit), NW * 32, smem, st>>>(a, tmap);
+    }
     if (!direct) {
         split_reduce_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, st>>>(nnz, (int)nsplit, part, t.vidx, dW);
         cudaFreeAsync(part, st);

@@ -10,6 +10,8 @@ namespace sp {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
 template <int VEC>
 struct VecT;
 template <>
@@ -47,13 +49,49 @@ __device__ __forceinline__ int4 ld_entry_pair(const int2 *p, bool smem) {
     return smem ? *reinterpret_cast<const int4 *>(p) : __ldg(reinterpret_cast<const int4 *>(p));
 }
 
+// Predicated shared loads (no branch: the destination keeps its prior value
+// when the predicate is false, so callers pre-zero it).
+__device__ __forceinline__ void lds128_pred(float4 &v, const void *p, bool pred) {
+    asm volatile(
+        "{\n.reg .pred q;\nsetp.ne.b32 q, %4, 0;\n@q ld.shared.v4.f32 {%0, %1, %2, %3}, [%5];\n}\n"
+        : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w)
+        : "r"((int)pred), "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void lds64_pred(float2 &v, const void *p, bool pred) {
+    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q ld.shared.v2.f32 {%0, %1}, [%3];\n}\n"
+                 : "+f"(v.x), "+f"(v.y)
+                 : "r"((int)pred), "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void lds32_pred(float &v, const void *p, bool pred) {
+    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %1, 0;\n@q ld.shared.f32 %0, [%2];\n}\n"
+                 : "+f"(v)
+                 : "r"((int)pred), "r"(smem_u32(p)));
+}
+
 // VEC-wide load of tile row `off` (bytes from `tb`) or zeros for a padding
-// entry (off < 0): the predicated-off load costs no shared-memory bandwidth.
+// entry (off < 0): the predicated-off load costs no shared-memory bandwidth
+// and no branch.
 template <int VEC, int SH>
 __device__ __forceinline__ void lds_row_or_zero(const char *tb, int off, float (&v)[VEC]) {
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) v[i] = 0.f;
-    if (off >= 0) lds_vec<VEC>(reinterpret_cast<const float *>(tb + (off >> SH)), v);
+    const bool ok = off >= 0;
+    const void *p = tb + (ok ? (off >> SH) : 0);
+    if constexpr (VEC == 4) {
+        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+        lds128_pred(t, p, ok);
+        v[0] = t.x;
+        v[1] = t.y;
+        v[2] = t.z;
+        v[3] = t.w;
+    } else if constexpr (VEC == 2) {
+        float2 t = make_float2(0.f, 0.f);
+        lds64_pred(t, p, ok);
+        v[0] = t.x;
+        v[1] = t.y;
+    } else {
+        float t = 0.f;
+        lds32_pred(t, p, ok);
+        v[0] = t;
+    }
 }
 
 // Stage rows [k0, k0+nk) x batch columns [b0, b0+BT) of a row-major
@@ -126,7 +164,6 @@ __device__ __forceinline__ void stage_any(float *tile, const float *src, int64_t
 }
 
 // ---- TMA (cp.async.bulk) + mbarrier helpers ------------------------------
-__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
