@@ -252,9 +252,9 @@ def main():
     barrier()
 
     # ---- per-kernel breakdown (same stream, events around each launch) ----
-    kt = {"fwd_spmm": [], "dx_spmm": [], "sddmm": []}
+    kt = {"fwd_spmm": [], "dx_spmm": [], "sddmm": [], "bwd_fused": []}
     ops = model.ops
-    orig = {k: getattr(ops, k) for k in ("fwd", "dx", "dw")}
+    orig = {k: getattr(ops, k) for k in ("fwd", "dx", "dw", "bwd")}
 
     def wrap(name, key):
         f = orig[name]
@@ -268,13 +268,14 @@ def main():
             return r
         return g
     ops.fwd, ops.dx, ops.dw = wrap("fwd", "fwd_spmm"), wrap("dx", "dx_spmm"), wrap("dw", "sddmm")
+    ops.bwd = wrap("bwd", "bwd_fused")
     ksteps = max(3, min(args.steps, 10))
     for _ in range(ksteps):
         model.step(args.lr)
     torch.cuda.synchronize()
-    ops.fwd, ops.dx, ops.dw = orig["fwd"], orig["dx"], orig["dw"]
+    ops.fwd, ops.dx, ops.dw, ops.bwd = orig["fwd"], orig["dx"], orig["dw"], orig["bwd"]
     clk = clocks.stop()
-    ktime = {k: sum(s.elapsed_time(e) for s, e in v) / ksteps for k, v in kt.items()}  # ms per step
+    ktime = {k: sum(s.elapsed_time(e) for s, e in v) / ksteps for k, v in kt.items() if v}  # ms per step
 
     # ---- end-to-end through the public API: host buffers in, loss out -----
     torch.cuda.synchronize()
@@ -312,8 +313,9 @@ def main():
         fp32_peak = fp32_peak_tflops(sm_max)
         # dominant kernel class and its live roofline fraction
         dom = max(ktime, key=ktime.get)
-        # each class runs one 2*nnz*B product per layer per step (24 launches)
-        fl = sum(2 * (W1.nnz + W2.nnz) * model.T for W1, W2 in model.W)
+        # fwd / dx / dw classes run one 2*nnz*B product per layer per step; the
+        # fused backward runs two (dX and dW) per launch
+        fl = sum(2 * (W1.nnz + W2.nnz) * model.T for W1, W2 in model.W) * (2 if dom == "bwd_fused" else 1)
         achieved = fl / (ktime[dom] * 1e-3) / 1e12
         step_roof_ms = model.step_flops() / (fp32_peak * 1e12) * 1e3
         line = {

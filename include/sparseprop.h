@@ -131,6 +131,21 @@ sp_status sp_linear_fwd_relu(sp_weight_t W, const float *X, float *Y, int64_t B,
 sp_status sp_linear_bwd_input_relu(sp_weight_t W, const float *dY, const float *H, float *dX,
                                    int64_t B, sp_stream_t stream);
 
+/* Fused backward (the paper's Alg. 1 "single pass",
+ * P173/P187-P220, made atomic-free by driving it from the CSC copy): ONE pass
+ * over the nonzeros produces both
+ *   dX = W^T dY                       (as sp_linear_bwd_input)
+ *   dW = (dY X^T) restricted to mask  (as sp_linear_bwd_weight)
+ * reading each staged dY element once for both products.
+ * sp_linear_bwd_relu additionally gates dX by [H > 0] (H: [C x B]).
+ * X: [C x B], dY: [R x B], dX: [C x B], dW: [nnz].  Falls back to the two
+ * separate kernels when B % 4 != 0, B < 128 or the problem is too small to
+ * fill the GPU (same results within the fp32 tolerance). */
+sp_status sp_linear_bwd(sp_weight_t W, const float *X, const float *dY, float *dX, float *dW, int64_t B,
+                        sp_stream_t stream);
+sp_status sp_linear_bwd_relu(sp_weight_t W, const float *X, const float *dY, const float *H, float *dX,
+                             float *dW, int64_t B, sp_stream_t stream);
+
 /* ---------------------------------------------------------------------- */
 /* 2-D convolution, stride 1, CHWN (P222-P248 §3.3, Alg. 2 P297-P347)     */
 /* ---------------------------------------------------------------------- */

@@ -222,6 +222,34 @@ sp_status sp_linear_bwd_weight(sp_weight_t w, const float *X, const float *dY, f
     return check_launch("sp_linear_bwd_weight");
 }
 
+static sp_status linear_bwd_impl(sp_weight_t w, const float *X, const float *dY, const float *H, float *dX,
+                                 float *dW, int64_t B, sp_stream_t stream, const char *fn) {
+    SP_CHECK_HANDLE(w, fn);
+    if (!X || !dY || !dX || (!dW && w->nnz > 0)) return fail(SP_ERR_NULL, std::string(fn) + ": NULL tensor");
+    sp_status s = check_B(B, w->R, w->C, fn);
+    if (s != SP_OK) return s;
+    s = launch_bwd_fused(w, X, dY, H, dX, dW, B, S(stream));
+    if (s == SP_ERR_SHAPE) {  // fused path not applicable: the two separate products
+        launch_spmm(w, 1, B, dY, dX, H, H ? EPI_GATE : EPI_NONE, S(stream));
+        s = check_launch(fn);
+        if (s != SP_OK) return s;
+        s = launch_sddmm(w, X, dY, dW, B, S(stream));
+    }
+    if (s != SP_OK) return s;
+    return check_launch(fn);
+}
+
+sp_status sp_linear_bwd(sp_weight_t w, const float *X, const float *dY, float *dX, float *dW, int64_t B,
+                        sp_stream_t stream) {
+    return linear_bwd_impl(w, X, dY, nullptr, dX, dW, B, stream, "sp_linear_bwd");
+}
+
+sp_status sp_linear_bwd_relu(sp_weight_t w, const float *X, const float *dY, const float *H, float *dX, float *dW,
+                             int64_t B, sp_stream_t stream) {
+    if (!H) return fail(SP_ERR_NULL, "sp_linear_bwd_relu: H is NULL");
+    return linear_bwd_impl(w, X, dY, H, dX, dW, B, stream, "sp_linear_bwd_relu");
+}
+
 sp_status sp_conv2d_fwd(sp_weight_t w, const sp_conv_geom *g, const float *X, float *Y, sp_stream_t stream) {
     SP_CHECK_HANDLE(w, "sp_conv2d_fwd");
     sp_status s = check_geom(w, g, "sp_conv2d_fwd");

@@ -1,0 +1,249 @@
+// fused.cu -- fused CSC-driven linear backward: one pass
+// over the nonzeros computes both backward products,
+//   dX[c][b] = sum_{r in col c} w(r,c) * dY[r][b]      (Eq. 1, P143-P145)
+//   dW(r,c)  = sum_b dY[r][b] * X[c][b]                (Eq. 2, P146-P148)
+// which is the paper's Algorithm 1 "single pass" (P173, P187-P220: per
+// nonzero, one fmadd updates dX and one accumulates the dW dot product) made
+// atomic-free by driving it from the CSC copy: every dX row is owned by one
+// warp and every dW entry by one lane of one CTA per batch split.
+//
+// Structure = the CSC tiling of the handle (rows = W columns c, inner = W
+// rows r).  A CTA owns a row block of RB columns and a batch split; per slice
+// of 128 batch columns it streams dY[r-block][slice] tiles (2-D TMA, double
+// buffered) and holds X[c][slice] of its RPW rows in registers.  Per entry
+// (r, w) one 16-byte LDS of dY[r][lane*4..] feeds BOTH 4 FMAs into the dX
+// accumulator of row c and a 4-term partial dot into one of 32 register
+// accumulators (dW), so the shared-memory traffic that bounds the separate
+// kernels is paid once for 2x the FLOPs.  dW slice partials are reduced per
+// row pair with one warp transpose-reduce and added into the split's partial
+// buffer; dX is written (optionally gated by H > 0, the fused ReLU') at the
+// end of each slice.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "sp_internal.cuh"
+#include "tile.cuh"
+
+namespace sp {
+namespace {
+
+struct FusedArgs {
+    int64_t nrow, F, B;
+    int KC, nkb, spl, cap;
+    const int32_t *seg;
+    const int2 *ent;
+    const int32_t *vidx;
+    const float *X;   // [nrow x B] register operand (layer input)
+    const float *dY;  // [F x B] staged operand (output gradient)
+    const float *H;   // [nrow x B] optional ReLU' gate for dX
+    float *dX;        // [nrow x B]
+    float *part;      // [nsplit x npad] or dW (direct)
+    int64_t npad;
+    int direct;
+};
+
+template <int RPW, int NW, bool GATE, bool SENT>
+__global__ void __launch_bounds__(NW * 32, 1)
+    bwd_fused_kernel(const FusedArgs a, const __grid_constant__ CUtensorMap tmap) {
+    static_assert(RPW % 2 == 0, "rows are processed in pairs");
+    constexpr int VEC = 4;
+    constexpr int BT = 32 * VEC;
+    constexpr int RB = NW * RPW;
+    constexpr int SH = 0;
+    extern __shared__ __align__(128) float smem[];  // [2][KC][BT] floats, then [2][cap+2] int2
+    __shared__ uint64_t full[2];
+    int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * a.KC * BT);
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int rb = blockIdx.x;
+    const int64_t B = a.B;
+    const int64_t s_lo = (int64_t)blockIdx.y * a.spl * BT;
+    const int nsl = (int)std::min<int64_t>(a.spl, (B - s_lo + BT - 1) / BT);
+    const int ntile = nsl * a.nkb;
+    float *P = a.part + (a.direct ? 0 : (int64_t)blockIdx.y * a.npad);
+    const size_t tile_sz = (size_t)a.KC * BT;
+    const int ebuf = a.cap + 2;
+    const int32_t *segw = a.seg + (int64_t)rb * a.nkb * RB + warp * RPW;
+    const int64_t r_base = (int64_t)rb * RB + warp * RPW;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto entry_range = [&](int kb, int &e0, int &e1) {
+        const int64_t tb = ((int64_t)rb * a.nkb + kb) * RB;
+        e0 = __ldg(a.seg + tb) & ~1;
+        e1 = __ldg(a.seg + tb + RB);
+    };
+    auto issue = [&](int q, int buf) {
+        const int s = q / a.nkb, kb = q - s * a.nkb;
+        int e0 = 0, e1 = 0;
+        if constexpr (SENT) entry_range(kb, e0, e1);
+        const unsigned eb = SENT ? (unsigned)(((e1 - e0) * 8 + 15) & ~15) : 0u;
+        mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
+        tma_load_2d(smem + buf * tile_sz, &tmap, (int)(s_lo + (int64_t)s * BT), kb * a.KC, &full[buf]);
+        if (eb) tma_load_1d(ents + buf * ebuf, a.ent + e0, eb, &full[buf]);
+    };
+    if (threadIdx.x == 0) issue(0, 0);
+
+    float rv[RPW][VEC], dx[RPW][VEC];
+    for (int q = 0; q < ntile; ++q) {
+        const int s = q / a.nkb, kb = q - s * a.nkb;
+        const int buf = q & 1;
+        const int64_t bl = s_lo + (int64_t)s * BT + lane * VEC;
+        if (kb == 0) {  // new slice: X rows into registers, dX accumulators reset
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                const int64_t r = r_base + i;
+                const float4 t = (r < a.nrow && bl + 4 <= B)
+                                     ? __ldg(reinterpret_cast<const float4 *>(a.X + r * B + bl))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+                rv[i][0] = t.x;
+                rv[i][1] = t.y;
+                rv[i][2] = t.z;
+                rv[i][3] = t.w;
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) dx[i][v] = 0.f;
+            }
+        }
+        const int sg = lane <= RPW ? __ldg(segw + (int64_t)kb * RB + lane) : 0;
+        if (q + 1 < ntile && threadIdx.x == 0) issue(q + 1, buf ^ 1);
+        mbar_wait(&full[buf], (q >> 1) & 1);
+        int ea = 0;
+        if constexpr (SENT) {
+            int e1;
+            entry_range(kb, ea, e1);
+        }
+        const char *tb = reinterpret_cast<const char *>(smem + buf * tile_sz + lane * VEC);
+        const int2 *es = SENT ? ents + buf * ebuf - ea : a.ent;
+#pragma unroll
+        for (int m = 0; m < RPW; m += 2) {
+            int pa = __shfl_sync(kFull, sg, m);
+            const int a1 = __shfl_sync(kFull, sg, m + 1);
+            int pb = a1;
+            const int b1 = __shfl_sync(kFull, sg, m + 2);
+            while (pa < a1 || pb < b1) {
+                const int na = min(16, a1 - pa), nb = min(16, b1 - pb);  // multiples of 4
+                float acc[32];
+#pragma unroll
+                for (int u = 0; u < 32; ++u) acc[u] = 0.f;
+#pragma unroll
+                for (int gq = 0; gq < 16; gq += 4) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {  // h = 0: row m (entries pa..), 1: row m+1 (pb..)
+                        if (gq < (h ? nb : na)) {
+                            const int e = (h ? pb : pa) + gq;
+                            const int4 p01 = ld_entry_pair(SENT ? es + e : a.ent + e, SENT);
+                            const int4 p23 = ld_entry_pair(SENT ? es + e + 2 : a.ent + e + 2, SENT);
+                            const int off[4] = {p01.x, p01.z, p23.x, p23.z};
+                            const float w[4] = {__int_as_float(p01.y), __int_as_float(p01.w), __int_as_float(p23.y),
+                                                __int_as_float(p23.w)};
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                float x[VEC];
+                                lds_row_or_zero<VEC, SH>(tb, off[u], x);
+                                float d = 0.f;
+#pragma unroll
+                                for (int v = 0; v < VEC; ++v) {
+                                    dx[m + h][v] = fmaf(w[u], x[v], dx[m + h][v]);  // dX  (Eq. 1)
+                                    d = fmaf(rv[m + h][v], x[v], d);                 // dW  (Eq. 2)
+                                }
+                                acc[16 * h + gq + u] = d;
+                            }
+                        }
+                    }
+                }
+                const float sum = transpose_reduce32(acc, lane);
+                const int u = lane & 15;
+                if (lane < 16 ? u < na : u < nb) {
+                    const int e = (lane < 16 ? pa : pb) + u;
+                    if (a.direct) {
+                        const int v = __ldg(a.vidx + e);
+                        if (v >= 0) P[v] = (s == 0) ? sum : P[v] + sum;
+                    } else {
+                        P[e] = (s == 0) ? sum : P[e] + sum;
+                    }
+                }
+                pa += na;
+                pb += nb;
+            }
+        }
+        if (kb == a.nkb - 1) {  // slice done: dX rows (ReLU' gate fused)
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                const int64_t r = r_base + i;
+                if (r >= a.nrow || bl >= B) continue;
+                float o[VEC];
+                if (GATE) {
+                    const float4 hv = __ldg(reinterpret_cast<const float4 *>(a.H + r * B + bl));
+                    o[0] = hv.x > 0.f ? dx[i][0] : 0.f;
+                    o[1] = hv.y > 0.f ? dx[i][1] : 0.f;
+                    o[2] = hv.z > 0.f ? dx[i][2] : 0.f;
+                    o[3] = hv.w > 0.f ? dx[i][3] : 0.f;
+                } else {
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) o[v] = dx[i][v];
+                }
+                *reinterpret_cast<float4 *>(a.dX + r * B + bl) = make_float4(o[0], o[1], o[2], o[3]);
+            }
+        }
+        __syncthreads();  // buffer free before it is refilled
+    }
+}
+
+constexpr int kNumSMs = 148;
+
+}  // namespace
+
+sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY, const float *H, float *dX,
+                           float *dW, int64_t B, cudaStream_t st) {
+    // fused path: B % 4 == 0, at least one full slice, the big CSC tiling
+    if ((B & 3) != 0 || B < 128 || w->nnz == 0) return SP_ERR_SHAPE;
+    constexpr int RPW = 8, NW = 16, BT = 128;
+    const sp_tiling &t = w->til[1][0];
+    const int64_t slices = (B + BT - 1) / BT;
+    if ((int64_t)t.nrb * slices < kNumSMs) return SP_ERR_SHAPE;  // too little parallelism: use the separate kernels
+    CUtensorMap tmap{};
+    if (!make_tmap_2d(&tmap, dY, t.inner, B, BT, t.KC)) return SP_ERR_SHAPE;
+    const int64_t want = 2LL * kNumSMs * 4;
+    int64_t nsplit = std::max<int64_t>(1, std::min<int64_t>(slices, (want + t.nrb - 1) / t.nrb));
+    const int64_t spl = (slices + nsplit - 1) / nsplit;
+    nsplit = (slices + spl - 1) / spl;
+    const size_t tiles = (size_t)2 * t.KC * BT * sizeof(float);
+    const int cap = (t.max_tile + 2 + 3) & ~3;
+    const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)(226 * 1024);
+    const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
+    const bool direct = nsplit == 1;
+    float *part = dW;
+    if (!direct) {
+        if (cudaMallocAsync((void **)&part, (size_t)(nsplit * t.npad) * sizeof(float), st) != cudaSuccess) {
+            set_error("sp_linear_bwd: scratch allocation failed");
+            return SP_ERR_ALLOC;
+        }
+    }
+    launch_refresh(t, w->vals, w->nnz, st);  // CSC-tiled weights from vals (through perm)
+    FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, (int)spl, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
+                direct ? 1 : 0};
+    auto pick = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<dim3((unsigned)t.nrb, (unsigned)nsplit), NW * 32, smem, st>>>(a, tmap);
+    };
+    count_launches(direct ? 1 : 2);
+    if (H) {
+        if (sent) pick(bwd_fused_kernel<RPW, NW, true, true>);
+        else pick(bwd_fused_kernel<RPW, NW, true, false>);
+    } else {
+        if (sent) pick(bwd_fused_kernel<RPW, NW, false, true>);
+        else pick(bwd_fused_kernel<RPW, NW, false, false>);
+    }
+    if (!direct) {
+        launch_split_reduce(t.npad, (int)nsplit, part, t.vidx, dW, st);
+        cudaFreeAsync(part, st);
+    }
+    return SP_OK;
+}
+
+}  // namespace sp

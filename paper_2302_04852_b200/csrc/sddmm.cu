@@ -285,6 +285,11 @@ sp_status launch_vec(const sp_weight_s *w, const sp_tiling &t, int var, const fl
 
 }  // namespace
 
+void launch_split_reduce(int64_t npad, int nsplit, const float *part, const int32_t *vidx, float *dW,
+                         cudaStream_t st) {
+    split_reduce_kernel<<<(unsigned)((npad + 255) / 256), 256, 0, st>>>(npad, nsplit, part, vidx, dW);
+}
+
 sp_status launch_sddmm(const sp_weight_s *w, const float *X, const float *dY, float *dW, int64_t B,
                        cudaStream_t st) {
     if (w->nnz == 0) return SP_OK;

@@ -101,6 +101,18 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
 sp_status launch_sddmm(const sp_weight_s *w, const float *X, const float *dY, float *dW,
                        int64_t B, cudaStream_t st);
 
+// dW[vidx[e]] = sum_s part[s][e] over a tiling's padded entries
+void launch_split_reduce(int64_t npad, int nsplit, const float *part, const int32_t *vidx, float *dW,
+                         cudaStream_t st);
+
+// ---- fused.cu ----
+// One CSC-driven pass for both backward products of a linear layer (the
+// paper's Alg. 1 single pass, P173, made atomic-free):
+//   dX = (W^T dY) [* (H > 0) if H]   and   dW = SDDMM(dY, X).
+// Returns SP_ERR_SHAPE if the fused path does not apply (caller falls back).
+sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY, const float *H, float *dX,
+                           float *dW, int64_t B, cudaStream_t st);
+
 // ---- conv.cu ----
 void launch_conv_fwd(const sp_weight_s *w, const sp_conv_geom &g, const float *X, float *Y,
                      cudaStream_t st);

@@ -43,6 +43,10 @@ class CudaOps:
     def dw(self, W, X, dY, dW):
         return self.sp.sp_linear_bwd_weight(W, X, dY, dW)
 
+    def bwd(self, W, X, dY, dX, dW, H=None):
+        """Fused backward (one CSC-driven pass): dX [* (H > 0)] and dW."""
+        return self.sp.sp_linear_bwd(W, X, dY, dX, dW, H=H)
+
     def mse(self, Y, T, dY, loss, scratch):
         self.sp.sp_mse_grad(Y, T, dY, loss, scratch)
 
@@ -57,7 +61,7 @@ class SparseMLP:
     """cfg5 model state + one training step on this rank's token shard."""
 
     def __init__(self, layers, T_local: int, device, ops=None, group=None, bucket_blocks: int = 3,
-                 keep_dx0: bool = True):
+                 keep_dx0: bool = True, fused: bool = True):
         """layers: list of (w1, m1, w2, m2) host arrays (synth.mlp_case)."""
         self.ops = ops if ops is not None else CudaOps()
         self.device = torch.device(device)
@@ -68,6 +72,7 @@ class SparseMLP:
         self.d_ff = layers[0][0].shape[0]
         self.T = T_local
         self.keep_dx0 = keep_dx0
+        self.fused = fused
         f32 = dict(dtype=torch.float32, device=self.device)
         self.W = []
         for (w1, m1, w2, m2) in layers:
@@ -124,17 +129,23 @@ class SparseMLP:
         pending = []
         bi = 0
         dY, dYn = self.dY, self.dYb
+        fused = self.fused and hasattr(ops, "bwd")
         for l in range(self.blocks - 1, -1, -1):
             W1, W2 = self.W[l]
             dW1, dW2 = self.dW[l]
-            ops.dw(W2, self.H[l], dY, dW2)                        # dW2 = SDDMM(dY, H)
-            ops.dx(W2, dY, self.dZ, H=self.H[l])                  # dZ = (W2^T dY) * [H > 0]
-            ops.dw(W1, self.X[l], self.dZ, dW1)                   # dW1 = SDDMM(dZ, X)
-            if l > 0 or self.keep_dx0:
-                out = self.dX0 if l == 0 else dYn
-                ops.dx(W1, self.dZ, out)                          # dX = W1^T dZ
-                if l > 0:
-                    dY, dYn = dYn, dY
+            out = self.dX0 if l == 0 else dYn
+            if fused:
+                # one CSC-driven pass per layer (dX and dW together)
+                ops.bwd(W2, self.H[l], dY, self.dZ, dW2, H=self.H[l])  # dZ = (W2^T dY)*[H>0], dW2
+                ops.bwd(W1, self.X[l], self.dZ, out, dW1)               # dX = W1^T dZ, dW1
+            else:
+                ops.dw(W2, self.H[l], dY, dW2)                        # dW2 = SDDMM(dY, H)
+                ops.dx(W2, dY, self.dZ, H=self.H[l])                  # dZ = (W2^T dY) * [H > 0]
+                ops.dw(W1, self.X[l], self.dZ, dW1)                   # dW1 = SDDMM(dZ, X)
+                if l > 0 or self.keep_dx0:
+                    ops.dx(W1, self.dZ, out)                          # dX = W1^T dZ
+            if l > 0:
+                dY, dYn = dYn, dY
             if comm and bi < len(self.buckets) and self.buckets[bi][0] == l:
                 lo, hi = self.buckets[bi][2], self.buckets[bi][3]
                 pending.append(self._launch_allreduce(self.dW_flat[lo:hi]))

@@ -28,7 +28,7 @@ EXPORTS = [
     "sp_linear_bwd_input", "sp_linear_bwd_weight", "sp_linear_fwd_relu",
     "sp_linear_bwd_input_relu", "sp_conv2d_fwd", "sp_conv2d_bwd_input", "sp_conv2d_bwd_weight",
     "sp_mse_scratch_floats", "sp_mse_grad", "sp_sgd", "sp_last_error", "sp_version",
-    "sp_launch_count",
+    "sp_launch_count", "sp_linear_bwd", "sp_linear_bwd_relu",
 ]
 
 
@@ -75,6 +75,8 @@ def lib() -> ct.CDLL:
             "sp_last_error": (ct.c_char_p, []),
             "sp_version": (ct.c_char_p, []),
             "sp_launch_count": (ct.c_uint64, []),
+            "sp_linear_bwd": (st, [vp, vp, vp, vp, vp, i64, vp]),
+            "sp_linear_bwd_relu": (st, [vp, vp, vp, vp, vp, vp, i64, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -254,6 +256,35 @@ def sp_linear_bwd_weight(W: SparseWeight, X: torch.Tensor, dY: torch.Tensor,
                                       _dev(dW, torch.float32, "dW") if W.nnz else None, B,
                                       _stream(stream)))
     return dW
+
+
+def sp_linear_bwd(W: SparseWeight, X: torch.Tensor, dY: torch.Tensor, dX: torch.Tensor | None = None,
+                  dW: torch.Tensor | None = None, stream=None, H: torch.Tensor | None = None):
+    """Fused backward: (dX = W^T dY [* (H > 0)], dW = SDDMM(dY, X)) in one pass."""
+    B = _B(X, W.C, "X")
+    if _B(dY, W.R, "dY") != B:
+        raise ValueError("X and dY batch sizes differ")
+    if dX is None:
+        dX = torch.empty(W.C, B, dtype=torch.float32, device=X.device)
+    _B(dX, W.C, "dX")
+    if dW is None:
+        dW = torch.empty(W.nnz, dtype=torch.float32, device=X.device)
+    if dW.numel() != W.nnz:
+        raise ValueError("dW must have nnz elements")
+    dwp = _dev(dW, torch.float32, "dW") if W.nnz else None
+    if H is None:
+        _check(lib().sp_linear_bwd(W.handle, _dev(X, torch.float32, "X"), _dev(dY, torch.float32, "dY"),
+                                   _dev(dX, torch.float32, "dX"), dwp, B, _stream(stream)))
+    else:
+        _B(H, W.C, "H")
+        _check(lib().sp_linear_bwd_relu(W.handle, _dev(X, torch.float32, "X"), _dev(dY, torch.float32, "dY"),
+                                        _dev(H, torch.float32, "H"), _dev(dX, torch.float32, "dX"), dwp, B,
+                                        _stream(stream)))
+    return dX, dW
+
+
+def sp_linear_bwd_relu(W, X, dY, H, dX=None, dW=None, stream=None):
+    return sp_linear_bwd(W, X, dY, dX, dW, stream, H=H)
 
 
 def conv_geom(W: SparseWeight, B: int, H: int, Wd: int, pad: int) -> sp_conv_geom:

@@ -46,6 +46,10 @@ class OracleOps:
     def dw(self, W, X, dY, dW):
         dW.copy_(torch.from_numpy(oracle.linear_bwd_weight(W.S, X.numpy(), dY.numpy())))
 
+    def bwd(self, W, X, dY, dX, dW, H=None):
+        self.dw(W, X, dY, dW)
+        self.dx(W, dY, dX, H=H)
+
     def mse(self, Y, T, dY, loss, scratch):
         d = Y.numpy().astype(np.float64) - T.numpy()
         dY.copy_(torch.from_numpy(d))
@@ -66,14 +70,14 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, T, q):
+def _worker(rank, world, port, T, q, fused):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2302_04852_b200.dp import SparseMLP
     c = synth.mlp_case(blocks=3, d_model=12, d_ff=20, T=T, density=0.3, seed=123)
     lo, hi = synth.token_shard(T, world, rank)
-    m = SparseMLP(c["layers"], hi - lo, "cpu", ops=OracleOps(), bucket_blocks=2)
+    m = SparseMLP(c["layers"], hi - lo, "cpu", ops=OracleOps(), bucket_blocks=2, fused=fused)
     m.set_batch(torch.from_numpy(c["X0"][:, lo:hi].copy()), torch.from_numpy(c["target"][:, lo:hi].copy()),
                 non_blocking=False)
     loss = m.forward().clone()
@@ -85,13 +89,14 @@ def _worker(rank, world, port, T, q):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("world", [2])
-def test_dp_gloo_matches_full_batch(world):
+def test_dp_gloo_matches_full_batch(world, fused):
     T = 10
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, T, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, T, q, fused)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=120) for _ in range(world)])

@@ -233,3 +233,32 @@ def test_conv_shapes(sp, B, IC, OC, H, W, K, pad, d):
     c = synth.conv_case(OC=OC, IC=IC, H=H, W=W, KH=K, KW=K, pad=pad, B=B, density=d,
                         wvar=1.0 / (IC * K * K), seed=B * 7 + IC + OC + H)
     check_conv(sp, c, f"conv B={B} IC={IC} OC={OC} {H}x{W} K={K} pad={pad}")
+
+
+# ---------------------------------------------------------------- fused backward (F1)
+@pytest.mark.parametrize("R,C,B,d,gate", [
+    (3072, 768, 2048, 0.05, False), (768, 3072, 2048, 0.05, True), (3072, 768, 16384, 0.05, True),
+    (1000, 900, 384, 0.2, False),     # fused, ragged row blocks
+    (300, 200, 902, 0.1, True),       # B % 4 != 0 -> separate kernels
+    (200, 100, 96, 0.3, False),       # B < 128 -> separate kernels
+])
+def test_fused_backward(sp, R, C, B, d, gate):
+    c = synth.linear_case(R, C, B, d, 1.0 / C, R + C + B)
+    S = oracle.csr_from_mask(c["W"], c["mask"])
+    Wg = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))
+    H = None
+    if gate:
+        H = synth.normal(synth.rng(R + B), (C, B), 1.0)
+        H[H < 0] = 0.0                      # a post-ReLU activation (exact zeros)
+    dX, dW = sp.sp_linear_bwd(Wg, _dev(c["X"]), _dev(c["dY"]), H=None if H is None else _dev(H))
+    torch.cuda.synchronize()
+    refx = oracle.linear_bwd_input(S, c["dY"], NT)
+    if gate:
+        refx = refx * (H > 0)
+    _assert_tol("fused dX", _np(dX), refx)
+    _assert_tol("fused dW", _np(dW), oracle.linear_bwd_weight(S, c["X"], c["dY"], NT))
+    # same arithmetic as the separate kernels: dX bitwise equal to sp_linear_bwd_input
+    dX2 = sp.sp_linear_bwd_input(Wg, _dev(c["dY"]), H=None if H is None else _dev(H))
+    torch.cuda.synchronize()
+    if B >= 128 and B % 4 == 0:
+        np.testing.assert_allclose(_np(dX), _np(dX2), rtol=1e-6, atol=1e-6)
