@@ -123,7 +123,8 @@ class SparseMLP:
         ops.mse(self.X[self.blocks], self.target, self.dY, self.loss, self.mse_scratch)
         return self.loss
 
-    def backward(self, allreduce: bool = True):
+    def backward(self, allreduce: bool = True, trace: list | None = None):
+        """trace (tests only): receives (l, dY_in, dZ, dX_out) clones per block."""
         ops = self.ops
         comm = allreduce and self.world > 1
         pending = []
@@ -144,6 +145,8 @@ class SparseMLP:
                 ops.dw(W1, self.X[l], self.dZ, dW1)                   # dW1 = SDDMM(dZ, X)
                 if l > 0 or self.keep_dx0:
                     ops.dx(W1, self.dZ, out)                          # dX = W1^T dZ
+            if trace is not None:
+                trace.append((l, dY.clone(), self.dZ.clone(), out.clone()))
             if l > 0:
                 dY, dYn = dYn, dY
             if comm and bi < len(self.buckets) and self.buckets[bi][0] == l:

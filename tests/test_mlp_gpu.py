@@ -1,0 +1,77 @@
+"""cfg5 data-parallel MLP step on the GPU vs the oracle (SURVEY §8(c) C19:
+layer-local parity -- the oracle recomputes every layer from the GPU's own
+saved inputs -- plus end-to-end loss agreement and the ReLU-flip count)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from conftest import tol_ok
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+NT = min(8, oracle.threads_available())
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _ok(name, got, ref):
+    ok, err, bound = tol_ok(got, ref)
+    assert ok, f"{name}: max|err| {err:.3e} > {bound:.3e}"
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_mlp_step_layer_local_parity(fused):
+    from paper_2302_04852_b200.dp import SparseMLP
+    T = 1024
+    c = synth.mlp_case(blocks=12, d_model=768, d_ff=3072, T=T, density=0.05, seed=5)
+    m = SparseMLP(c["layers"], T, "cuda", fused=fused)
+    m.set_batch(torch.from_numpy(c["X0"]), torch.from_numpy(c["target"]), non_blocking=False)
+    loss = float(m.forward())
+    trace = []
+    m.backward(allreduce=False, trace=trace)
+    torch.cuda.synchronize()
+    S = [(oracle.csr_from_mask(w1, m1), oracle.csr_from_mask(w2, m2)) for (w1, m1, w2, m2) in c["layers"]]
+    # forward, layer-local
+    for l, (S1, S2) in enumerate(S):
+        X = _np(m.X[l])
+        H = _np(m.H[l])
+        _ok(f"H[{l}]", H, np.maximum(oracle.linear_fwd(S1, X, NT), 0.0))
+        _ok(f"X[{l + 1}]", _np(m.X[l + 1]), oracle.linear_fwd(S2, H, NT))
+    Y = _np(m.X[12]).astype(np.float64)
+    d = Y - c["target"]
+    assert loss == pytest.approx(0.5 * float(np.sum(d * d)), rel=1e-5)
+    # backward, layer-local from the GPU's own dY_in of each block
+    for (l, dY_in, dZ, dX_out) in trace:
+        S1, S2 = S[l]
+        X, H, dYl = _np(m.X[l]), _np(m.H[l]), _np(dY_in)
+        refZ = oracle.linear_bwd_input(S2, dYl, NT) * (H > 0)
+        _ok(f"dZ[{l}]", _np(dZ), refZ)
+        dW1, dW2 = m.dW[l]
+        _ok(f"dW2[{l}]", _np(dW2), oracle.linear_bwd_weight(S2, H, dYl, NT))
+        _ok(f"dW1[{l}]", _np(dW1), oracle.linear_bwd_weight(S1, X, _np(dZ), NT))
+        _ok(f"dX[{l}]", _np(dX_out), oracle.linear_bwd_input(S1, _np(dZ), NT))
+    # end to end against the oracle's own full forward: loss and flip count
+    ref = oracle.mlp_step(S, c["X0"], c["target"], NT)
+    assert loss == pytest.approx(ref["loss"], rel=1e-4)
+    flips = sum(int(np.sum((_np(m.H[l]) > 0) != (ref["acts"][l][1] > 0))) for l in range(12))
+    assert flips < 1e-4 * 12 * 3072 * T, flips
+
+
+def test_mlp_sgd_updates_only_kept_weights():
+    from paper_2302_04852_b200.dp import SparseMLP
+    c = synth.mlp_case(blocks=2, d_model=768, d_ff=3072, T=256, density=0.05, seed=6)
+    m = SparseMLP(c["layers"], 256, "cuda")
+    m.set_batch(torch.from_numpy(c["X0"]), torch.from_numpy(c["target"]), non_blocking=False)
+    before = [(W1.vals.clone(), W2.vals.clone()) for W1, W2 in m.W]
+    m.step(1e-3)
+    torch.cuda.synchronize()
+    for l, ((W1, W2), (b1, b2), (d1, d2)) in enumerate(zip(m.W, before, m.dW)):
+        np.testing.assert_allclose(_np(W1.vals), _np(b1) - 1e-3 * _np(d1), rtol=1e-6, atol=1e-7)
+        np.testing.assert_allclose(_np(W2.vals), _np(b2) - 1e-3 * _np(d2), rtol=1e-6, atol=1e-7)
+        # dW densifies to exact zeros off each layer's mask
+        for Wh, dd, mask in ((W1, d1, c["layers"][l][1]), (W2, d2, c["layers"][l][3])):
+            D = _np(Wh.to_dense(dd))
+            assert np.all(D[mask == 0] == 0.0)
