@@ -76,6 +76,16 @@ typedef struct {
 sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8_t *mask,
                            sp_stream_t stream, sp_weight_t *out);
 
+/* Same as sp_weight_create for a conv filter [C_out][C_in][KH][KW] (dense and
+ * mask on the device in that order; R = C_out, C = C_in*KH*KW), plus the
+ * per-tap tilings the conv kernels stream: implicit im2col by taps -- each
+ * filter tap (x, y) is an OC x IC sparse matrix applied to a shifted view of
+ * the spatially padded activation (Eq. 3, P224; pruned taps skipped, P248).
+ * Synchronises `stream`.  Handles from sp_weight_create also work with the
+ * conv entry points (through slower direct kernels). */
+sp_status sp_weight_create_conv(int32_t C_out, int32_t C_in, int32_t KH, int32_t KW, const float *dense,
+                                const uint8_t *mask, sp_stream_t stream, sp_weight_t *out);
+
 /* Frees the handle's buffers (after synchronising `stream`). */
 sp_status sp_weight_destroy(sp_weight_t W, sp_stream_t stream);
 

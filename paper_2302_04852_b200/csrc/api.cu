@@ -129,6 +129,21 @@ sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8
     return SP_OK;
 }
 
+sp_status sp_weight_create_conv(int32_t C_out, int32_t C_in, int32_t KH, int32_t KW, const float *dense,
+                                const uint8_t *mask, sp_stream_t stream, sp_weight_t *out) {
+    if (C_out < 1 || C_in < 1 || KH < 1 || KW < 1)
+        return fail(SP_ERR_SHAPE, "sp_weight_create_conv: dimensions must be >= 1");
+    sp_status s = sp_weight_create(C_out, (int64_t)C_in * KH * KW, dense, mask, stream, out);
+    if (s != SP_OK) return s;
+    s = build_conv_taps(*out, C_out, C_in, KH, KW, S(stream));
+    if (s != SP_OK) {
+        sp_weight_destroy(*out, stream);
+        *out = nullptr;
+        return fail(s, "sp_weight_create_conv: tap tiling build failed");
+    }
+    return SP_OK;
+}
+
 sp_status sp_weight_destroy(sp_weight_t w, sp_stream_t stream) {
     SP_CHECK_HANDLE(w, "sp_weight_destroy");
     cudaStreamSynchronize(S(stream));

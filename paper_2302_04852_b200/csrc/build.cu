@@ -348,15 +348,20 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
 }
 
 void free_tilings(sp_weight_s *w) {
+    auto fr = [](sp_tiling &t) {
+        cudaFree(t.seg);
+        cudaFree(t.ent);
+        cudaFree(t.vidx);
+        t.seg = nullptr;
+        t.ent = nullptr;
+        t.vidx = nullptr;
+    };
     for (auto &o : w->til)
-        for (auto &t : o) {
-            cudaFree(t.seg);
-            cudaFree(t.ent);
-            cudaFree(t.vidx);
-            t.seg = nullptr;
-            t.ent = nullptr;
-            t.vidx = nullptr;
-        }
+        for (auto &t : o) fr(t);
+    for (auto &o : w->tap)
+        for (auto &t : o) fr(t);
+    if (w->tapdev) cudaFree(w->tapdev);
+    w->tapdev = nullptr;
 }
 
 void launch_refresh(const sp_tiling &t, const float *vals, int64_t nnz, cudaStream_t st) {
@@ -364,6 +369,21 @@ void launch_refresh(const sp_tiling &t, const float *vals, int64_t nnz, cudaStre
         count_launches(1);
         til_refresh_kernel<<<(unsigned)((t.npad + 255) / 256), 256, 0, st>>>(t.npad, t.vidx, vals, t.ent);
     }
+}
+
+// ent[e].y = vals[vidx[e]] for every tap tiling of one orientation (grid.y = tap)
+__global__ void til_refresh_taps_kernel(const TapDev *__restrict__ taps, const float *__restrict__ vals) {
+    const TapDev t = taps[blockIdx.y];
+    int2 *ent = const_cast<int2 *>(t.ent);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < t.npad; e += (int64_t)gridDim.x * blockDim.x) {
+        const int v = __ldg(t.vidx + e);
+        if (v >= 0) ent[e].y = __float_as_int(__ldg(vals + v));
+    }
+}
+
+void launch_refresh_taps(const sp_weight_s *w, int orient, int ntap, cudaStream_t st) {
+    count_launches(1);
+    til_refresh_taps_kernel<<<dim3(64, ntap), 256, 0, st>>>(w->tapdev + orient * kMaxTaps, w->vals);
 }
 
 void launch_to_dense(const sp_weight_s *w, const float *nz, float *dense, cudaStream_t st) {

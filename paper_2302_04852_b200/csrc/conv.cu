@@ -245,6 +245,38 @@ __global__ void __launch_bounds__(256)
     if (lane < n) dW[beg + lane] = s;
 }
 
+// dst[c][i][j][b] = src[c][i - top][j - left][b] (zero outside), B % 4 == 0
+__global__ void pad_kernel(int64_t Cc, int Hs, int Ws, int Hd, int Wd, int top, int left, int64_t B4,
+                           const float4 *__restrict__ src, float4 *__restrict__ dst) {
+    const int64_t total = Cc * Hd * Wd * B4;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i % B4;
+        int64_t t = i / B4;
+        const int j = (int)(t % Wd);
+        t /= Wd;
+        const int h = (int)(t % Hd);
+        const int64_t c = t / Hd;
+        const int hs = h - top, ws = j - left;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (hs >= 0 && hs < Hs && ws >= 0 && ws < Ws) v = __ldg(src + ((c * Hs + hs) * Ws + ws) * B4 + b);
+        dst[i] = v;
+    }
+}
+
+void launch_pad(int64_t Cc, int Hs, int Ws, int Hd, int Wd, int top, int left, int64_t B, const float *src, float *dst,
+                cudaStream_t st) {
+    count_launches(1);
+    pad_kernel<<<148 * 8, 256, 0, st>>>(Cc, Hs, Ws, Hd, Wd, top, left, B / 4, reinterpret_cast<const float4 *>(src),
+                                        reinterpret_cast<float4 *>(dst));
+}
+
+// The tap-tiled path applies (handle built by sp_weight_create_conv, B % 4 == 0,
+// pad <= K - 1 so the transposed conv's padding is non-negative).
+bool tap_path(const sp_weight_s *w, const Geo &g) {
+    return w->tapdev != nullptr && w->conv_kh == g.KH && w->conv_kw == g.KW && g.KH * g.KW <= kMaxTaps &&
+           (g.B & 3) == 0 && g.pad <= g.KH - 1 && g.pad <= g.KW - 1;
+}
+
 Geo mk(const sp_conv_geom &c) {
     Geo g;
     g.B = c.B;
@@ -267,6 +299,22 @@ constexpr int QC = 8;
 void launch_conv_fwd(const sp_weight_s *w, const sp_conv_geom &cg, const float *X, float *Y,
                      cudaStream_t st) {
     const Geo g = mk(cg);
+    if (tap_path(w, g)) {
+        // Y[oc] = sum_taps W_xy . shift_{(x*Wp + y)*B}(X_pad)  (Eq. 3 by taps)
+        const int Hp = g.H + 2 * g.pad, Wp = g.W + 2 * g.pad;
+        const int64_t Lp = (int64_t)Hp * Wp * g.B;
+        float *Xp = nullptr;
+        if (cudaMallocAsync((void **)&Xp, (size_t)(g.IC * Lp) * sizeof(float), st) == cudaSuccess) {
+            launch_pad(g.IC, g.H, g.W, Hp, Wp, g.pad, g.pad, g.B, X, Xp, st);
+            int sh[kMaxTaps];
+            for (int x = 0; x < g.KH; ++x)
+                for (int y = 0; y < g.KW; ++y) sh[x * g.KW + y] = (x * Wp + y) * g.B;
+            launch_refresh_taps(w, 0, g.KH * g.KW, st);
+            const bool ok = launch_conv_spmm(w, 0, g.B, Xp, Lp, Y, sh, g.KH * g.KW, Wp, g.OH, g.OW, st);
+            cudaFreeAsync(Xp, st);
+            if (ok) return;
+        }
+    }
     const int nqc = (g.OW + QC - 1) / QC;
     auto go = [&](auto kern, int vec) {
         const int64_t nbc = (g.B + 32 * vec - 1) / (32 * vec);
@@ -282,6 +330,23 @@ void launch_conv_fwd(const sp_weight_s *w, const sp_conv_geom &cg, const float *
 void launch_conv_bwd_input(const sp_weight_s *w, const sp_conv_geom &cg, const float *dY, float *dX,
                            cudaStream_t st) {
     const Geo g = mk(cg);
+    if (tap_path(w, g)) {
+        // transposed conv by taps (Eq. 4): dY padded by K-1-pad, shifts (K-1-x, K-1-y)
+        const int ph = g.KH - 1 - g.pad, pw = g.KW - 1 - g.pad;
+        const int Hq = g.OH + 2 * ph, Wq = g.OW + 2 * pw;
+        const int64_t Lq = (int64_t)Hq * Wq * g.B;
+        float *Dp = nullptr;
+        if (cudaMallocAsync((void **)&Dp, (size_t)(g.OC * Lq) * sizeof(float), st) == cudaSuccess) {
+            launch_pad(g.OC, g.OH, g.OW, Hq, Wq, ph, pw, g.B, dY, Dp, st);
+            int sh[kMaxTaps];
+            for (int x = 0; x < g.KH; ++x)
+                for (int y = 0; y < g.KW; ++y) sh[x * g.KW + y] = ((g.KH - 1 - x) * Wq + (g.KW - 1 - y)) * g.B;
+            launch_refresh_taps(w, 1, g.KH * g.KW, st);
+            const bool ok = launch_conv_spmm(w, 1, g.B, Dp, Lq, dX, sh, g.KH * g.KW, Wq, g.H, g.W, st);
+            cudaFreeAsync(Dp, st);
+            if (ok) return;
+        }
+    }
     const int nqc = (g.W + QC - 1) / QC;
     auto go = [&](auto kern, int vec) {
         const int64_t nbc = (g.B + 32 * vec - 1) / (32 * vec);
@@ -299,6 +364,27 @@ sp_status launch_conv_bwd_weight(const sp_weight_s *w, const sp_conv_geom &cg, c
                                  const float *dY, float *dW, cudaStream_t st) {
     const Geo g = mk(cg);
     if (w->nnz == 0) return SP_OK;
+    if (tap_path(w, g)) {
+        // dW_xy = SDDMM over the virtual output space (Eq. 5 by taps): dY laid
+        // out with row width Wp (zeros for q >= OW) against shifted X_pad
+        const int Hp = g.H + 2 * g.pad, Wp = g.W + 2 * g.pad;
+        const int64_t Lp = (int64_t)Hp * Wp * g.B, Lv = (int64_t)g.OH * Wp * g.B;
+        float *Xp = nullptr, *Dv = nullptr;
+        if (cudaMallocAsync((void **)&Xp, (size_t)(g.IC * Lp) * sizeof(float), st) == cudaSuccess &&
+            cudaMallocAsync((void **)&Dv, (size_t)(g.OC * Lv) * sizeof(float), st) == cudaSuccess) {
+            launch_pad(g.IC, g.H, g.W, Hp, Wp, g.pad, g.pad, g.B, X, Xp, st);
+            launch_pad(g.OC, g.OH, g.OW, g.OH, Wp, 0, 0, g.B, dY, Dv, st);
+            int sh[kMaxTaps];
+            for (int x = 0; x < g.KH; ++x)
+                for (int y = 0; y < g.KW; ++y) sh[x * g.KW + y] = (x * Wp + y) * g.B;
+            const bool ok = launch_conv_sddmm(w, g.B, Dv, Xp, Lv, Lp, sh, g.KH * g.KW, dW, st);
+            cudaFreeAsync(Xp, st);
+            cudaFreeAsync(Dv, st);
+            if (ok) return SP_OK;
+        } else {
+            if (Xp) cudaFreeAsync(Xp, st);
+        }
+    }
     const int gpr = (w->max_row_nnz + 31) / 32;
     const int64_t warps = (int64_t)g.OC * gpr;
     auto go = [&](auto kern) {

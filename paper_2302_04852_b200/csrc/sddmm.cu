@@ -39,6 +39,12 @@ struct SddmmArgs {
     float *part;             // [nsplit x nnz] in entry order (or dW if direct)
     int64_t nnz;
     int direct;              // single split: write dW[vidx[e]] directly
+    // conv (CONV=true): grid.z = tap; tap t uses taps[t]'s tiling, reads the
+    // padded activation shifted by sh[t] columns, and keeps its partials at
+    // part[split*nnz + tapbase[t] + e] (nnz = total padded entries of all taps)
+    const TapDev *taps;
+    int sh[kMaxTaps];
+    int64_t tapbase[kMaxTaps];
 };
 
 __device__ __forceinline__ void prefetch_l1(const void *p) {
@@ -55,9 +61,20 @@ __device__ __forceinline__ float dotv(const float (&a)[VEC], const float *p) {
     return d;
 }
 
-template <int VEC, int RPW, int NW, bool SENT>
+template <int VEC, int RPW, int NW, bool SENT, bool CONV>
 __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
-    sddmm_tiled_kernel(const SddmmArgs a, const __grid_constant__ CUtensorMap tmap) {
+    sddmm_tiled_kernel(const SddmmArgs a_, const __grid_constant__ CUtensorMap tmap) {
+    // conv: select this CTA's tap (grid.z) -- its tiling, shift and partials
+    SddmmArgs a = a_;
+    int shift = 0;
+    if constexpr (CONV) {
+        const TapDev td = a_.taps[blockIdx.z];
+        a.seg = td.seg;
+        a.ent = td.ent;
+        a.vidx = td.vidx;
+        shift = a_.sh[blockIdx.z];
+        a.part = a_.part + a_.tapbase[blockIdx.z];
+    }
     static_assert(RPW % 2 == 0, "rows are processed in pairs");
     constexpr int BT = 32 * VEC;
     constexpr int NT = NW * 32;
@@ -97,7 +114,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
         if constexpr (SENT) entry_range(kb, e0, e1);
         const unsigned eb = SENT ? (unsigned)(((e1 - e0) * 8 + 15) & ~15) : 0u;
         mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
-        tma_load_2d(smem + buf * tile_sz, &tmap, (int)(s_lo + (int64_t)s * BT), kb * a.KC, &full[buf]);
+        tma_load_2d(smem + buf * tile_sz, &tmap, (int)(s_lo + (int64_t)s * BT) + shift, kb * a.KC, &full[buf]);
         if (eb) tma_load_1d(ents + buf * ebuf, a.ent + e0, eb, &full[buf]);
     };
     if (tma && threadIdx.x == 0) issue(0, 0);
@@ -262,10 +279,10 @@ sp_status launch_cfg(const sp_weight_s *w, const sp_tiling &t, const float *rego
     CUtensorMap tmap{};
     const bool tma = (B & 3) == 0 && make_tmap_2d(&tmap, smemop, t.inner, B, BT, t.KC);
     SddmmArgs a{t.rows, t.inner, B, t.KC, t.nkb, (int)spl, cap, tma ? 1 : 0, t.seg, t.ent, t.vidx, regop, smemop,
-                part, nnz, direct ? 1 : 0};
+                part, nnz, direct ? 1 : 0, nullptr, {}, {}};
     count_launches(direct ? 1 : 2);
     {
-        auto kern = sent ? sddmm_tiled_kernel<VEC, RPW, NW, true> : sddmm_tiled_kernel<VEC, RPW, NW, false>;
+        auto kern = sent ? sddmm_tiled_kernel<VEC, RPW, NW, true, false> : sddmm_tiled_kernel<VEC, RPW, NW, false, false>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<dim3((unsigned)t.nrb, (unsigned)nsplit), NW * 32, smem, st>>>(a, tmap);
     }
@@ -283,7 +300,69 @@ sp_status launch_vec(const sp_weight_s *w, const sp_tiling &t, int var, const fl
     return launch_cfg<VEC, 4, 8>(w, t, regop, smemop, dW, B, 4, st);
 }
 
+// conv: dW[vidx_t[e]] = sum_s part[s][tapbase_t + e]  (grid.y = tap)
+__global__ void conv_split_reduce_kernel(const TapDev *__restrict__ taps, const int64_t *__restrict__ tapbase,
+                                         int64_t totpad, int nsplit, const float *__restrict__ part,
+                                         float *__restrict__ dW) {
+    const TapDev t = taps[blockIdx.y];
+    const int64_t base = tapbase[blockIdx.y];
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < t.npad; e += (int64_t)gridDim.x * blockDim.x) {
+        const int v = t.vidx[e];
+        if (v < 0) continue;
+        float s = part[base + e];
+        for (int i = 1; i < nsplit; ++i) s += part[(int64_t)i * totpad + base + e];
+        dW[v] = s;
+    }
+}
+
 }  // namespace
+
+bool launch_conv_sddmm(const sp_weight_s *w, int64_t B, const float *dYv, const float *Xp, int64_t Lv, int64_t Lp,
+                       const int *sh, int ntap, float *dW, cudaStream_t st) {
+    (void)B;
+    constexpr int VEC = 4, RPW = 8, NW = 16, BT = 128;
+    const sp_tiling &t0 = w->tap[0][0];  // rows oc, inner ic
+    CUtensorMap tmap{};
+    if (!make_tmap_2d(&tmap, Xp, t0.inner, Lp, BT, t0.KC)) return false;
+    int64_t tapbase[kMaxTaps] = {};
+    int64_t tot = 0;
+    int mx = 0;
+    for (int t = 0; t < ntap; ++t) {
+        tapbase[t] = tot;
+        tot += w->tap[t][0].npad;
+        mx = std::max(mx, w->tap[t][0].max_tile);
+    }
+    const int64_t slices = (Lv + BT - 1) / BT;
+    const int64_t want = 2LL * kNumSMs * 4;
+    const int64_t units = (int64_t)t0.nrb * ntap;
+    int64_t nsplit = std::max<int64_t>(1, std::min<int64_t>(slices, (want + units - 1) / units));
+    const int64_t spl = (slices + nsplit - 1) / nsplit;
+    nsplit = (slices + spl - 1) / spl;
+    const int cap = (mx + 2 + 3) & ~3;
+    const size_t tiles = (size_t)2 * t0.KC * BT * sizeof(float);
+    const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)(226 * 1024);
+    const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
+    float *part = nullptr;
+    int64_t *tb_dev = nullptr;
+    if (cudaMallocAsync((void **)&part, (size_t)(nsplit * tot) * sizeof(float), st) != cudaSuccess ||
+        cudaMallocAsync((void **)&tb_dev, sizeof(tapbase), st) != cudaSuccess)
+        return false;
+    cudaMemcpyAsync(tb_dev, tapbase, sizeof(tapbase), cudaMemcpyHostToDevice, st);
+    SddmmArgs a{t0.rows, t0.inner, Lv, t0.KC, t0.nkb, (int)spl, cap, 1, nullptr, nullptr, nullptr, dYv, Xp,
+                part, tot, 0, w->tapdev, {}, {}};
+    for (int t = 0; t < ntap; ++t) {
+        a.sh[t] = sh[t];
+        a.tapbase[t] = tapbase[t];
+    }
+    auto kern = sent ? sddmm_tiled_kernel<VEC, RPW, NW, true, true> : sddmm_tiled_kernel<VEC, RPW, NW, false, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    count_launches(2);
+    kern<<<dim3((unsigned)t0.nrb, (unsigned)nsplit, (unsigned)ntap), NW * 32, smem, st>>>(a, tmap);
+    conv_split_reduce_kernel<<<dim3(64, ntap), 256, 0, st>>>(w->tapdev, tb_dev, tot, (int)nsplit, part, dW);
+    cudaFreeAsync(part, st);
+    cudaFreeAsync(tb_dev, st);
+    return true;
+}
 
 void launch_split_reduce(int64_t npad, int nsplit, const float *part, const int32_t *vidx, float *dW,
                          cudaStream_t st) {

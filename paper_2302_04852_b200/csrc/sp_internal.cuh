@@ -14,6 +14,16 @@
 
 #define SP_MAGIC 0x53505731u /* "SPW1" */
 
+constexpr int kMaxTaps = 25;  // conv filters up to 5x5 use the tap-tiled kernels
+
+// Device view of one tap tiling (conv kernels index these by tap).
+struct TapDev {
+    const int32_t *seg;
+    const int2 *ent;
+    const int32_t *vidx;
+    int64_t npad;
+};
+
 // A tiled copy of one orientation's index structure (built once per handle,
 // DESIGN.md §5): rows are grouped in row blocks of RB, the inner dimension in
 // column blocks of KC.  Entries are ordered (row block, column block, local
@@ -48,6 +58,12 @@ struct sp_weight_s {
     int32_t max_row_nnz, max_col_nnz;
     // tilings: [orientation 0 = CSR rows, 1 = CSC columns][variant 0 = big, 1 = small]
     sp_tiling til[2][2];
+    // conv handles (sp_weight_create_conv): filter taps and, per tap (x, y),
+    // tilings of the OC x IC tap matrix W_xy -- [0]: rows oc / inner ic,
+    // [1]: rows ic / inner oc -- whose vidx are slots of THIS handle's CSR.
+    int conv_kh, conv_kw;
+    sp_tiling tap[kMaxTaps][2];
+    struct TapDev *tapdev;  // device copy of the tap tilings' pointers [2][kMaxTaps]
 };
 
 // Tiling variants (RB rows per CTA, KC inner columns per shared-memory tile).
@@ -112,6 +128,17 @@ void launch_split_reduce(int64_t npad, int nsplit, const float *part, const int3
 // Returns SP_ERR_SHAPE if the fused path does not apply (caller falls back).
 sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY, const float *H, float *dX,
                            float *dW, int64_t B, cudaStream_t st);
+
+bool launch_conv_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, int64_t Lp, float *out,
+                      const int *sh, int ntap, int64_t Wv, int64_t OHv, int64_t OWv, cudaStream_t st);
+void launch_refresh_taps(const sp_weight_s *w, int orient, int ntap, cudaStream_t st);
+bool launch_conv_sddmm(const sp_weight_s *w, int64_t B, const float *dYv, const float *Xp, int64_t Lv, int64_t Lp,
+                       const int *sh, int ntap, float *dW, cudaStream_t st);
+
+// ---- conv_taps.cu ----
+// Build the per-tap tilings of a conv handle (host-side, once, after
+// build_weight); frees with free_tilings.
+sp_status build_conv_taps(sp_weight_s *w, int OC, int IC, int KH, int KW, cudaStream_t st);
 
 // ---- conv.cu ----
 void launch_conv_fwd(const sp_weight_s *w, const sp_conv_geom &g, const float *X, float *Y,

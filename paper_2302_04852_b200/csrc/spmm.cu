@@ -38,6 +38,14 @@ struct SpmmArgs {
     const float *in;
     float *out;
     const float *gate;
+    // conv (CONV=true): the tile sequence runs over (tap, column block); tap t
+    // uses taps[t]'s tiling and reads the padded input shifted by sh[t]
+    // columns; output column n = ((p*Wv) + q)*B + b is stored compactly to
+    // out[r][p][q][b] when p < OHv, q < OWv.
+    int ntap;
+    const TapDev *taps;
+    int sh[kMaxTaps];
+    int64_t Wv, OHv, OWv;
 };
 
 __device__ __forceinline__ void prefetch_l1(const void *p) {
@@ -53,10 +61,10 @@ __device__ __forceinline__ void prefetch_entries(const int2 *ent, int e0, int e1
 // SENT: the tile's entries are staged in shared memory too (next tile's
 // entries arrive with its activation tile); otherwise entries are read with
 // warp-uniform global loads (tiles larger than the entry buffer).
-// Staging: B % 4 == 0 -> TMA bulk copies (one per tile row, UBLKCP) issued by
-// warp 0 into a double buffer, completion on one mbarrier per buffer;
-// otherwise (ragged B) a synchronous per-element path.
-template <int VEC, int RPW, int NW, int EPI, bool SENT>
+// Staging: B % 4 == 0 -> a 2-D TMA box per tile + a 1-D bulk copy of its
+// entries, issued by one thread into a double buffer, completion on one
+// mbarrier per buffer; otherwise (ragged B) a synchronous per-element path.
+template <int VEC, int RPW, int NW, int EPI, bool SENT, bool CONV>
 __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
     spmm_tiled_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr int BT = 32 * VEC;
@@ -70,9 +78,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
     const int rb = blockIdx.x;
     const int64_t b0 = (int64_t)blockIdx.y * BT;
     const int64_t B = a.B;
-    const bool vec4 = a.tma != 0;  // TMA path (B % 4 == 0 and a tensor map)
+    const bool vec4 = CONV || a.tma != 0;  // TMA path (B % 4 == 0 and a tensor map)
     const size_t tile_sz = (size_t)a.KC * BT;
     const int ebuf = a.cap + 2;
+    const int ntile = CONV ? a.ntap * a.nkb : a.nkb;
 
     if (threadIdx.x == 0) {
         mbar_init(&full[0], 1);
@@ -81,34 +90,39 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
     }
     __syncthreads();
 
-    // issue tile kb into buffer buf (warp 0 only, TMA path); returns the even
-    // index of the first staged entry
-    auto entry_range = [&](int kb, int &e0, int &e1) {
-        const int64_t tb = ((int64_t)rb * a.nkb + kb) * RB;
-        e0 = __ldg(a.seg + tb) & ~1;
-        e1 = __ldg(a.seg + tb + RB);
+    // tile q -> (tap t, column block kb) and its tiling arrays
+    auto tap_of = [&](int q) { return CONV ? q / a.nkb : 0; };
+    auto kb_of = [&](int q) { return CONV ? q - (q / a.nkb) * a.nkb : q; };
+    auto seg_of = [&](int t) -> const int32_t * { return CONV ? a.taps[t].seg : a.seg; };
+    auto ent_of = [&](int t) -> const int2 * { return CONV ? a.taps[t].ent : a.ent; };
+    auto entry_range = [&](int q, int &e0, int &e1) {
+        const int64_t tb = ((int64_t)rb * a.nkb + kb_of(q)) * RB;
+        const int32_t *sgp = seg_of(tap_of(q));
+        e0 = __ldg(sgp + tb) & ~1;
+        e1 = __ldg(sgp + tb + RB);
     };
-    auto issue = [&](int kb, int buf) {
-        const int64_t k0 = (int64_t)kb * a.KC;
-        const int nk = (int)std::min<int64_t>(a.KC, a.inner - k0);
+    // issue tile q into buffer buf (one thread, TMA path)
+    auto issue = [&](int q, int buf) {
+        const int t = tap_of(q);
+        const int64_t k0 = (int64_t)kb_of(q) * a.KC;
         int e0 = 0, e1 = 0;
-        if constexpr (SENT) entry_range(kb, e0, e1);
-        (void)nk;
+        if constexpr (SENT) entry_range(q, e0, e1);
         const unsigned eb = SENT ? (unsigned)(((e1 - e0) * 8 + 15) & ~15) : 0u;
-        if (lane == 0) {
-            // the box is always KC x BT floats (OOB rows / columns zero-filled)
-            mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
-            tma_load_2d(smem + buf * tile_sz, &tmap, (int)b0, (int)k0, &full[buf]);
-            if (eb) tma_load_1d(ents + buf * ebuf, a.ent + e0, eb, &full[buf]);
-        }
+        // the box is always KC x BT floats (OOB rows / columns zero-filled)
+        mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
+        tma_load_2d(smem + buf * tile_sz, &tmap, (int)(b0 + (CONV ? a.sh[t] : 0)), (int)k0, &full[buf]);
+        if (eb) tma_load_1d(ents + buf * ebuf, ent_of(t) + e0, eb, &full[buf]);
     };
-    if (vec4 && warp == 0) issue(0, 0);
+    if (vec4 && threadIdx.x == 0) issue(0, 0);
 
-    // lane l <= RPW holds the l-th segment bound of this warp's rows in the
-    // current tile (rows rb*RB + warp*RPW + i).
-    const int32_t *segw = a.seg + (int64_t)rb * a.nkb * RB + warp * RPW;
-    int sg = lane <= RPW ? __ldg(segw + lane) : 0;
-    if constexpr (!SENT) prefetch_entries(a.ent, __shfl_sync(kFull, sg, 0), __shfl_sync(kFull, sg, RPW), lane);
+    // lane l <= RPW holds the l-th segment bound of this warp's rows in tile q
+    // (rows rb*RB + warp*RPW + i).
+    auto seg_bounds = [&](int q) -> int {
+        const int32_t *segw = seg_of(tap_of(q)) + ((int64_t)rb * a.nkb + kb_of(q)) * RB + warp * RPW;
+        return lane <= RPW ? __ldg(segw + lane) : 0;
+    };
+    int sg = seg_bounds(0);
+    if constexpr (!SENT) prefetch_entries(ent_of(0), __shfl_sync(kFull, sg, 0), __shfl_sync(kFull, sg, RPW), lane);
 
     float acc[RPW][VEC];
 #pragma unroll
@@ -116,29 +130,31 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
 #pragma unroll
         for (int v = 0; v < VEC; ++v) acc[i][v] = 0.f;
 
-    for (int kb = 0; kb < a.nkb; ++kb) {
-        const int buf = kb & 1;
+    for (int q = 0; q < ntile; ++q) {
+        const int buf = q & 1;
+        const int kb = kb_of(q);
         int sgn = 0;
-        if (kb + 1 < a.nkb) {
-            if (vec4 && warp == 0) issue(kb + 1, buf ^ 1);
-            sgn = lane <= RPW ? __ldg(segw + (int64_t)(kb + 1) * RB + lane) : 0;
+        if (q + 1 < ntile) {
+            if (vec4 && threadIdx.x == 0) issue(q + 1, buf ^ 1);
+            sgn = seg_bounds(q + 1);
             if constexpr (!SENT)
-                prefetch_entries(a.ent, __shfl_sync(kFull, sgn, 0), __shfl_sync(kFull, sgn, RPW), lane);
+                prefetch_entries(ent_of(tap_of(q + 1)), __shfl_sync(kFull, sgn, 0), __shfl_sync(kFull, sgn, RPW),
+                                 lane);
         }
         int ea = 0;
         if (vec4) {
-            mbar_wait(&full[buf], (kb >> 1) & 1);
+            mbar_wait(&full[buf], (q >> 1) & 1);
             if constexpr (SENT) {
                 int e1;
-                entry_range(kb, ea, e1);
+                entry_range(q, ea, e1);
             }
-        } else {  // ragged B: synchronous staging of this tile
+        } else {  // ragged B: synchronous staging of this tile (never CONV)
             const int64_t k0 = (int64_t)kb * a.KC;
             stage_tile<BT, NT>(smem + buf * tile_sz, a.in, k0, (int)std::min<int64_t>(a.KC, a.inner - k0), B, b0,
                                false);
             if constexpr (SENT) {
                 int e1;
-                entry_range(kb, ea, e1);
+                entry_range(q, ea, e1);
                 for (int i = threadIdx.x; i < e1 - ea; i += NT) ents[buf * ebuf + i] = __ldg(a.ent + ea + i);
             }
             __syncthreads();
@@ -146,15 +162,16 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
         // tile row byte offsets are stored for 128-float rows; narrower tiles shift
         constexpr int SH = VEC == 4 ? 0 : VEC == 2 ? 1 : 2;
         const char *tb = reinterpret_cast<const char *>(smem + buf * tile_sz + lane * VEC);
-        const int2 *es = SENT ? ents + buf * ebuf - ea : a.ent;
+        const int2 *gent = ent_of(tap_of(q));
+        const int2 *es = SENT ? ents + buf * ebuf - ea : gent;
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
             const int s0 = __shfl_sync(kFull, sg, i), s1 = __shfl_sync(kFull, sg, i + 1);
             // segments are padded to multiples of 4 (weight-0 entries): no tail
             for (int e = s0; e < s1; e += 4) {
                 // 4 entries in two 16-byte broadcast loads
-                const int4 p01 = ld_entry_pair(SENT ? es + e : a.ent + e, SENT);
-                const int4 p23 = ld_entry_pair(SENT ? es + e + 2 : a.ent + e + 2, SENT);
+                const int4 p01 = ld_entry_pair(es + e, SENT);
+                const int4 p23 = ld_entry_pair(es + e + 2, SENT);
                 const int off[4] = {p01.x, p01.z, p23.x, p23.z};
                 const float w[4] = {__int_as_float(p01.y), __int_as_float(p01.w), __int_as_float(p23.y),
                                     __int_as_float(p23.w)};
@@ -171,8 +188,26 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
         sg = sgn;
     }
 
-    // Epilogue: ReLU / ReLU' gate fused; each element written once.
     const int64_t bl = b0 + lane * VEC;
+    if constexpr (CONV) {
+        // compact store of the valid output columns (VEC-aligned groups share (p, q))
+        const int64_t pq = bl / B, b = bl - pq * B;
+        const int64_t qq = pq % a.Wv, pp = pq / a.Wv;
+        if (pp >= a.OHv || qq >= a.OWv) return;
+        const int64_t col = (pp * a.OWv + qq) * B + b, rowlen = a.OHv * a.OWv * B;
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+            const int64_t r = (int64_t)rb * RB + warp * RPW + i;
+            if (r >= a.rows) continue;
+            float *dst = a.out + r * rowlen + col;
+            if constexpr (VEC == 4) *reinterpret_cast<float4 *>(dst) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+            else
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) dst[v] = acc[i][v];
+        }
+        return;
+    }
+    // Epilogue: ReLU / ReLU' gate fused; each element written once.
 #pragma unroll
     for (int i = 0; i < RPW; ++i) {
         const int64_t r = (int64_t)rb * RB + warp * RPW + i;
@@ -190,7 +225,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
             o[v] = x;
         }
         float *dst = a.out + r * B + bl;
-        if (vec4 && VEC > 1 && bl + VEC <= B) {
+        if ((B & 3) == 0 && VEC > 1 && bl + VEC <= B) {
             if constexpr (VEC == 2) *reinterpret_cast<float2 *>(dst) = make_float2(o[0], o[1]);
             if constexpr (VEC == 4) *reinterpret_cast<float4 *>(dst) = make_float4(o[0], o[1], o[2], o[3]);
         } else {
@@ -215,7 +250,7 @@ void launch_cfg(const sp_tiling &t, int64_t B, const float *in, float *out, cons
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
     CUtensorMap tmap{};
     const bool tma = (B & 3) == 0 && make_tmap_2d(&tmap, in, t.inner, B, BT, t.KC);
-    SpmmArgs a{t.rows, t.inner, B, t.KC, t.nkb, cap, tma ? 1 : 0, t.seg, t.ent, in, out, gate};
+    SpmmArgs a{t.rows, t.inner, B, t.KC, t.nkb, cap, tma ? 1 : 0, t.seg, t.ent, in, out, gate, 0, nullptr, {}, 0, 0, 0};
     dim3 grid((unsigned)t.nrb, (unsigned)((B + BT - 1) / BT));
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -223,13 +258,13 @@ void launch_cfg(const sp_tiling &t, int64_t B, const float *in, float *out, cons
         kern<<<grid, NW * 32, smem, st>>>(a, tmap);
     };
     if (sent) {
-        if (epi == EPI_RELU) launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_RELU, true>);
-        else if (epi == EPI_GATE) launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_GATE, true>);
-        else launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_NONE, true>);
+        if (epi == EPI_RELU) launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_RELU, true, false>);
+        else if (epi == EPI_GATE) launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_GATE, true, false>);
+        else launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_NONE, true, false>);
     } else {
-        if (epi == EPI_RELU) launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_RELU, false>);
-        else if (epi == EPI_GATE) launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_GATE, false>);
-        else launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_NONE, false>);
+        if (epi == EPI_RELU) launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_RELU, false, false>);
+        else if (epi == EPI_GATE) launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_GATE, false, false>);
+        else launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_NONE, false, false>);
     }
 }
 
@@ -242,7 +277,47 @@ void launch_variant(const sp_tiling &t, int v, int64_t B, const float *in, float
     else launch_cfg<VEC, 4, 8>(t, B, in, out, gate, epi, st);
 }
 
+template <int VEC>
+bool conv_spmm_vec(const sp_weight_s *w, int orient, int64_t B, const float *in, int64_t Lp, float *out,
+                   const int *sh, int ntap, int64_t Wv, int64_t OHv, int64_t OWv, cudaStream_t st) {
+    constexpr int RPW = 8, NW = 16, BT = 32 * VEC;
+    const sp_tiling &t0 = w->tap[0][orient];
+    CUtensorMap tmap{};
+    if (!make_tmap_2d(&tmap, in, t0.inner, Lp, BT, t0.KC)) return false;
+    int mx = 0;
+    for (int t = 0; t < ntap; ++t) mx = std::max(mx, w->tap[t][orient].max_tile);
+    const int cap = (mx + 2 + 3) & ~3;
+    const size_t tiles = (size_t)2 * t0.KC * BT * sizeof(float);
+    const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)kSmemLimit;
+    const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
+    SpmmArgs a{t0.rows, t0.inner, B, t0.KC, t0.nkb, cap, 1, nullptr, nullptr, nullptr, out, nullptr,
+               ntap, w->tapdev + orient * kMaxTaps, {}, Wv, OHv, OWv};
+    for (int t = 0; t < ntap; ++t) a.sh[t] = sh[t];
+    const int64_t Nv = OHv * Wv * B;
+    dim3 grid((unsigned)t0.nrb, (unsigned)((Nv + BT - 1) / BT));
+    auto launch = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        count_launches(1);
+        kern<<<grid, NW * 32, smem, st>>>(a, tmap);
+    };
+    if (sent) launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_NONE, true, true>);
+    else launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_NONE, false, true>);
+    return true;
+}
+
 }  // namespace
+
+// Conv products as tap-tiled SpMM (see conv.cu): in = padded activation
+// [inner x Lp], taps[t] tilings of orientation `orient`, shift sh[t] columns;
+// virtual output columns Nv = OHv * Wv * B stored compactly.  Narrower batch
+// slices when the grid would not fill two waves.
+bool launch_conv_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, int64_t Lp, float *out,
+                      const int *sh, int ntap, int64_t Wv, int64_t OHv, int64_t OWv, cudaStream_t st) {
+    const int64_t Nv = OHv * Wv * B;
+    if ((int64_t)w->tap[0][orient].nrb * ((Nv + 127) / 128) >= 2 * kNumSMs)
+        return conv_spmm_vec<4>(w, orient, B, in, Lp, out, sh, ntap, Wv, OHv, OWv, st);
+    return conv_spmm_vec<2>(w, orient, B, in, Lp, out, sh, ntap, Wv, OHv, OWv, st);
+}
 
 void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out,
                  const float *gate, int epi, cudaStream_t st) {

@@ -28,7 +28,7 @@ EXPORTS = [
     "sp_linear_bwd_input", "sp_linear_bwd_weight", "sp_linear_fwd_relu",
     "sp_linear_bwd_input_relu", "sp_conv2d_fwd", "sp_conv2d_bwd_input", "sp_conv2d_bwd_weight",
     "sp_mse_scratch_floats", "sp_mse_grad", "sp_sgd", "sp_last_error", "sp_version",
-    "sp_launch_count", "sp_linear_bwd", "sp_linear_bwd_relu",
+    "sp_launch_count", "sp_linear_bwd", "sp_linear_bwd_relu", "sp_weight_create_conv",
 ]
 
 
@@ -76,6 +76,7 @@ def lib() -> ct.CDLL:
             "sp_version": (ct.c_char_p, []),
             "sp_launch_count": (ct.c_uint64, []),
             "sp_linear_bwd": (st, [vp, vp, vp, vp, vp, i64, vp]),
+            "sp_weight_create_conv": (st, [ct.c_int32] * 4 + [vp, vp, vp, ct.POINTER(vp)]),
             "sp_linear_bwd_relu": (st, [vp, vp, vp, vp, vp, vp, i64, vp]),
         }
         for name, (res, args) in sig.items():
@@ -131,9 +132,15 @@ class SparseWeight:
             raise ValueError("dense and mask must be R x C (or matching 4-D conv filters)")
         R, C = dense.shape
         h = ct.c_void_p()
-        _check(lib().sp_weight_create(R, C, _dev(dense.contiguous(), torch.float32, "dense"),
-                                      _dev(mask.contiguous(), torch.uint8, "mask"), _stream(stream),
-                                      ct.byref(h)))
+        if self.filter_shape is not None:
+            OC, IC, KH, KW = self.filter_shape
+            _check(lib().sp_weight_create_conv(OC, IC, KH, KW, _dev(dense.contiguous(), torch.float32, "dense"),
+                                               _dev(mask.contiguous(), torch.uint8, "mask"), _stream(stream),
+                                               ct.byref(h)))
+        else:
+            _check(lib().sp_weight_create(R, C, _dev(dense.contiguous(), torch.float32, "dense"),
+                                          _dev(mask.contiguous(), torch.uint8, "mask"), _stream(stream),
+                                          ct.byref(h)))
         self.handle = h
         self.R, self.C = int(R), int(C)
         self.nnz = int(lib().sp_weight_nnz(h))
