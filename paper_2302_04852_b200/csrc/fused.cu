@@ -143,15 +143,12 @@ __global__ void __launch_bounds__(NW * 32, 1)
                                                 __int_as_float(p23.w)};
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
+                                // padding entries (offset -1): predicated-off load, x = 0, so
+                                // non-finite activations cannot leak into other rows
                                 float x[VEC];
                                 lds_row_or_zero<VEC, SH>(tb, off[u], x);
-                                float d = 0.f;
-#pragma unroll
-                                for (int v = 0; v < VEC; ++v) {
-                                    dx[m + h][v] = fmaf(w[u], x[v], dx[m + h][v]);  // dX  (Eq. 1)
-                                    d = fmaf(rv[m + h][v], x[v], d);                 // dW  (Eq. 2)
-                                }
-                                acc[16 * h + gq + u] = d;
+                                fma_bcast<VEC>(dx[m + h], w[u], x);           // dX  (Eq. 1)
+                                acc[16 * h + gq + u] = dot_vec<VEC>(rv[m + h], x);  // dW  (Eq. 2)
                             }
                         }
                     }

@@ -178,12 +178,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
         const int2 *es = SENT ? ents + buf * ebuf - ea : a.ent;
         // dot of the register-operand slice with tile row of entry e (0 for padding)
         auto dot_e = [&](const float(&r)[VEC], int off) -> float {
+            // padding entries (offset -1) read tile row 0; their slot is never written
             float x[VEC];
-            lds_row_or_zero<VEC, SH>(tb, off, x);
-            float d = 0.f;
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) d = fmaf(r[v], x[v], d);
-            return d;
+            lds_vec<VEC>(reinterpret_cast<const float *>(tb + (max(off, 0) >> SH)), x);
+            return dot_vec<VEC>(r, x);
         };
         auto offs4 = [&](int e, int (&o)[4]) {
             const int4 p01 = ld_entry_pair(SENT ? es + e : a.ent + e, SENT);

@@ -179,9 +179,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
 #pragma unroll
                 for (int u = 0; u < 4; ++u) lds_row_or_zero<VEC, SH>(tb, off[u], x[u]);
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int v = 0; v < VEC; ++v) acc[i][v] = fmaf(w[u], x[u][v], acc[i][v]);
+                for (int u = 0; u < 4; ++u) fma_bcast<VEC>(acc[i], w[u], x[u]);
             }
         }
         __syncthreads();  // everyone done with this buffer before it is refilled

@@ -221,6 +221,37 @@ __device__ __forceinline__ void tma_stage_tile(float *tile, const float *src, in
     if (lane == 0 && ebytes) tma_load_1d(edst, esrc, ebytes, bar);
 }
 
+// ---- packed FP32 math (sm_100 FFMA2 / FMUL2: two lanes per instruction,
+// each element rounded exactly like fmaf / fmul) ----------------------------
+template <int VEC>
+__device__ __forceinline__ void fma_bcast(float (&acc)[VEC], float w, const float (&x)[VEC]) {
+    if constexpr (VEC == 1) {
+        acc[0] = fmaf(w, x[0], acc[0]);
+    } else {
+        const float2 ww = make_float2(w, w);
+#pragma unroll
+        for (int v = 0; v < VEC; v += 2) {
+            const float2 r = __ffma2_rn(ww, make_float2(x[v], x[v + 1]), make_float2(acc[v], acc[v + 1]));
+            acc[v] = r.x;
+            acc[v + 1] = r.y;
+        }
+    }
+}
+
+// sum_v a[v] * x[v] with paired products (order: (a0x0 + a2x2) + (a1x1 + a3x3))
+template <int VEC>
+__device__ __forceinline__ float dot_vec(const float (&a)[VEC], const float (&x)[VEC]) {
+    if constexpr (VEC == 1) {
+        return a[0] * x[0];
+    } else {
+        float2 p = __fmul2_rn(make_float2(a[0], a[1]), make_float2(x[0], x[1]));
+#pragma unroll
+        for (int v = 2; v < VEC; v += 2)
+            p = __ffma2_rn(make_float2(a[v], a[v + 1]), make_float2(x[v], x[v + 1]), p);
+        return p.x + p.y;
+    }
+}
+
 // Warp transpose-reduce of 32 per-lane partials: on return, lane t holds
 // sum over lanes of acc[t] (in acc[0]).  31 shuffles for 32 sums.
 __device__ __forceinline__ float transpose_reduce32(float (&acc)[32], int lane) {
