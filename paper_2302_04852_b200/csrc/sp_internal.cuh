@@ -112,6 +112,13 @@ enum Epi { EPI_NONE = 0, EPI_RELU = 1, EPI_GATE = 2 };
 void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out,
                  const float *gate, int epi, cudaStream_t st);
 
+// ---- gather.cu (very sparse / small regime: no shared-memory staging) ----
+bool gather_preferred(const sp_weight_s *w, int orient, int64_t B);
+void launch_spmm_gather(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out,
+                        const float *gate, int epi, cudaStream_t st);
+void launch_sddmm_gather(const sp_weight_s *w, const float *X, const float *dY, float *dW, int64_t B,
+                         cudaStream_t st);
+
 // ---- sddmm.cu ----
 // dW[j] = sum_b dY[row(j)][b] * X[col_idx[j]][b]
 sp_status launch_sddmm(const sp_weight_s *w, const float *X, const float *dY, float *dW,

@@ -319,6 +319,14 @@ bool launch_conv_spmm(const sp_weight_s *w, int orient, int64_t B, const float *
 
 void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out,
                  const float *gate, int epi, cudaStream_t st) {
+    if (w->nnz == 0 || gather_preferred(w, orient, B)) {  // staging would move more bytes than gathering
+        if (w->nnz == 0) {
+            cudaMemsetAsync(out, 0, (size_t)((orient == 0 ? w->R : w->C) * B) * sizeof(float), st);
+            return;
+        }
+        launch_spmm_gather(w, orient, B, in, out, gate, epi, st);
+        return;
+    }
     // Choose the largest row block and batch vector that still fill the GPU.
     int vec = B <= 32 ? 1 : (B <= 64 || (B & 3)) ? 2 : 4;
     int var = 0;
