@@ -115,12 +115,12 @@ def run_oracle_sample(target_s: float = 15.0):
     dX) on a token sample, repeated until ~target_s of CPU work.  Returns
     (GFLOP/s, cores, sample description, seconds)."""
     import oracle
-    c = synth.mlp_case(blocks=1, d_model=CFG["d_model"], d_ff=CFG["d_ff"], T=256,
+    c = synth.mlp_case(blocks=1, d_model=CFG["d_model"], d_ff=CFG["d_ff"], T=2048,
                        density=CFG["density"], seed=CFG["seed"])
     w1, m1, w2, m2 = c["layers"][0]
     S1, S2 = oracle.csr_from_mask(w1, m1), oracle.csr_from_mask(w2, m2)
     nt = oracle.threads_available()
-    T = 256
+    T = 2048
     X = c["X0"][:, :T]
     tgt = c["target"][:, :T]
     flops_one = 6 * (S1.nnz + S2.nnz) * T

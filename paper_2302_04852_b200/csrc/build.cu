@@ -175,8 +175,8 @@ __global__ void til_fill_kernel(int64_t rows, int nkb, int KC, int RB, const int
         vidx[e] = slot;
     }
     const int pad = ((hi - lo + kTilPad - 1) & ~(kTilPad - 1)) - (hi - lo);
-    for (int t = 0; t < pad; ++t, ++e) {  // padding: sentinel offset -1 (no load), weight 0, no slot
-        ent[e] = make_int2(-1, 0);
+    for (int t = 0; t < pad; ++t, ++e) {  // padding: offset -kTilRowBytes (zero row / no load), weight 0, no slot
+        ent[e] = make_int2(-kTilRowBytes, 0);
         vidx[e] = -1;
     }
 }

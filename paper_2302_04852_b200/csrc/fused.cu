@@ -51,9 +51,11 @@ __global__ void __launch_bounds__(NW * 32, 1)
     constexpr int BT = 32 * VEC;
     constexpr int RB = NW * RPW;
     constexpr int SH = 0;
-    extern __shared__ __align__(128) float smem[];  // [2][KC][BT] floats, then [2][cap+2] int2
+    // [2][zero row + KC rows][BT] floats, then [2][cap+2] int2.  The zero row in
+    // front of each tile is what padding entries (offset -one row) read.
+    extern __shared__ __align__(128) float smem[];
     __shared__ uint64_t full[2];
-    int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * a.KC * BT);
+    int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * (a.KC + 1) * BT);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int rb = blockIdx.x;
@@ -62,7 +64,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const int nsl = (int)std::min<int64_t>(a.spl, (B - s_lo + BT - 1) / BT);
     const int ntile = nsl * a.nkb;
     float *P = a.part + (a.direct ? 0 : (int64_t)blockIdx.y * a.npad);
-    const size_t tile_sz = (size_t)a.KC * BT;
+    const size_t tile_sz = (size_t)a.KC * BT;  // TMA bytes per tile
+    const size_t buf_sz = tile_sz + BT;         // zero row + tile
     const int ebuf = a.cap + 2;
     const int32_t *segw = a.seg + (int64_t)rb * a.nkb * RB + warp * RPW;
     const int64_t r_base = (int64_t)rb * RB + warp * RPW;
@@ -71,6 +74,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
         mbar_init(&full[0], 1);
         mbar_init(&full[1], 1);
         fence_mbar_init();
+    }
+    for (int i = threadIdx.x; i < BT; i += NW * 32) {
+        smem[i] = 0.f;
+        smem[buf_sz + i] = 0.f;
     }
     __syncthreads();
     auto entry_range = [&](int kb, int &e0, int &e1) {
@@ -84,7 +91,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         if constexpr (SENT) entry_range(kb, e0, e1);
         const unsigned eb = SENT ? (unsigned)(((e1 - e0) * 8 + 15) & ~15) : 0u;
         mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
-        tma_load_2d(smem + buf * tile_sz, &tmap, (int)(s_lo + (int64_t)s * BT), kb * a.KC, &full[buf]);
+        tma_load_2d(smem + buf * buf_sz + BT, &tmap, (int)(s_lo + (int64_t)s * BT), kb * a.KC, &full[buf]);
         if (eb) tma_load_1d(ents + buf * ebuf, a.ent + e0, eb, &full[buf]);
     };
     if (threadIdx.x == 0) issue(0, 0);
@@ -117,7 +124,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
             int e1;
             entry_range(kb, ea, e1);
         }
-        const char *tb = reinterpret_cast<const char *>(smem + buf * tile_sz + lane * VEC);
+        const char *tb = reinterpret_cast<const char *>(smem + buf * buf_sz + BT + lane * VEC);
         const int2 *es = SENT ? ents + buf * ebuf - ea : a.ent;
 #pragma unroll
         for (int m = 0; m < RPW; m += 2) {
@@ -143,10 +150,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
                                                 __int_as_float(p23.w)};
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
-                                // padding entries (offset -1): predicated-off load, x = 0, so
-                                // non-finite activations cannot leak into other rows
+                                // padding entries read the zero row (x = 0 exactly, so
+                                // non-finite activations cannot leak into other rows)
                                 float x[VEC];
-                                lds_row_or_zero<VEC, SH>(tb, off[u], x);
+                                lds_vec<VEC>(reinterpret_cast<const float *>(tb + off[u]), x);
                                 fma_bcast<VEC>(dx[m + h], w[u], x);           // dX  (Eq. 1)
                                 acc[16 * h + gq + u] = dot_vec<VEC>(rv[m + h], x);  // dW  (Eq. 2)
                             }
@@ -209,7 +216,7 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     int64_t nsplit = std::max<int64_t>(1, std::min<int64_t>(slices, (want + t.nrb - 1) / t.nrb));
     const int64_t spl = (slices + nsplit - 1) / nsplit;
     nsplit = (slices + spl - 1) / spl;
-    const size_t tiles = (size_t)2 * t.KC * BT * sizeof(float);
+    const size_t tiles = (size_t)2 * (t.KC + 1) * BT * sizeof(float);
     const int cap = (t.max_tile + 2 + 3) & ~3;
     const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)(226 * 1024);
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);

@@ -69,9 +69,11 @@ struct sp_weight_s {
 // Tiling variants (RB rows per CTA, KC inner columns per shared-memory tile).
 constexpr int kTilRB[2] = {128, 32};
 constexpr int kTilKC[2] = {192, 96};
-// Segments are padded to a multiple of kTilPad entries (offset -1 = no load,
+// Segments are padded to a multiple of kTilPad entries (offset -kTilRowBytes,
 // weight 0, vidx -1) so the kernels run tail-free groups of 4; every segment
-// starts at a multiple of 4 entries (16-byte aligned pairs).  Entry columns are stored
+// starts at a multiple of 4 entries (16-byte aligned pairs).  A padding
+// entry's offset addresses the all-zero row kernels keep just before a tile
+// (or is skipped by a predicated load).  Entry columns are stored
 // as byte offsets of a 128-float tile row (kTilRowBytes); kernels with
 // narrower tiles shift them down.
 constexpr int kTilPad = 4;
