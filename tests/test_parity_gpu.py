@@ -225,7 +225,25 @@ def test_cfg3_conv(sp):
     check_conv(sp, synth.conv_case(**synth.CFG["cfg3"]), "cfg3")
 
 
+def test_conv_handle_matches_linear_handle_and_is_deterministic(sp):
+    c = synth.conv_case(OC=32, IC=16, H=10, W=10, KH=3, KW=3, pad=1, B=16, density=0.2, wvar=1.0 / 144, seed=77)
+    Wc = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))                      # conv handle (taps)
+    Wl = sp.sp_weight_create(_dev(c["W"].reshape(32, -1)), _dev(c["mask"].reshape(32, -1)))
+    for k, v in Wc.indices().items():
+        assert torch.equal(v, Wl.indices()[k]), k
+    g = sp.conv_geom(Wc, 16, 10, 10, 1)
+    X, dY = _dev(c["X"]), _dev(c["dY"])
+    runs = [(sp.sp_conv2d_fwd(Wc, g, X), sp.sp_conv2d_bwd_input(Wc, g, dY), sp.sp_conv2d_bwd_weight(Wc, g, X, dY))
+            for _ in range(2)]
+    torch.cuda.synchronize()
+    for a, b in zip(*runs):
+        assert torch.equal(a, b)
+
+
 @pytest.mark.parametrize("B,IC,OC,H,W,K,pad,d", [
+    (8, 4, 6, 9, 9, 7, 3, 0.3),      # 49 taps > tap-path limit -> direct kernels
+    (8, 4, 6, 8, 8, 3, 3, 0.3),      # pad > K-1 -> direct kernels
+    (4, 300, 140, 5, 6, 3, 1, 0.05),  # several row / column blocks on the tap path
     (3, 6, 5, 9, 9, 3, 1, 0.1), (8, 128 // 8, 256 // 8, 7, 7, 3, 1, 0.05), (2, 4, 3, 6, 5, 3, 0, 0.4),
     (1, 2, 2, 5, 5, 5, 2, 0.6), (5, 3, 2, 4, 6, 1, 0, 0.7), (33, 8, 16, 10, 10, 3, 1, 0.2),
     (64, 16, 16, 17, 19, 3, 1, 0.1), (130, 4, 4, 3, 3, 3, 1, 0.5)])
