@@ -146,28 +146,29 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t *a, int lo, int hi,
 
 // thread per (row, column block): entries of the row inside the block
 __global__ void til_count_kernel(int64_t rows, int nkb, int KC, int RB, const int32_t *__restrict__ ptr,
-                                 const int32_t *__restrict__ idx, int32_t *__restrict__ cnt) {
+                                 const int32_t *__restrict__ idx, const int32_t *__restrict__ rowpos,
+                                 int32_t *__restrict__ cnt) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (tid >= rows * nkb) return;
     const int64_t r = tid / nkb;
     const int kb = (int)(tid - r * nkb);
     const int lo = lower_bound_i32(idx, ptr[r], ptr[r + 1], kb * KC);
     const int hi = lower_bound_i32(idx, lo, ptr[r + 1], (kb + 1) * KC);
-    const int64_t rb = r / RB, lr = r - rb * RB;
+    const int64_t pos = rowpos[r], rb = pos / RB, lr = pos - rb * RB;
     cnt[(rb * nkb + kb) * RB + lr] = (hi - lo + kTilPad - 1) & ~(kTilPad - 1);  // padded segment
 }
 
 __global__ void til_fill_kernel(int64_t rows, int nkb, int KC, int RB, const int32_t *__restrict__ ptr,
                                 const int32_t *__restrict__ idx, const int32_t *__restrict__ slotmap,
-                                const int32_t *__restrict__ seg, const float *__restrict__ vals,
-                                int2 *__restrict__ ent, int32_t *__restrict__ vidx) {
+                                const int32_t *__restrict__ rowpos, const int32_t *__restrict__ seg,
+                                const float *__restrict__ vals, int2 *__restrict__ ent, int32_t *__restrict__ vidx) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (tid >= rows * nkb) return;
     const int64_t r = tid / nkb;
     const int kb = (int)(tid - r * nkb);
     const int lo = lower_bound_i32(idx, ptr[r], ptr[r + 1], kb * KC);
     const int hi = lower_bound_i32(idx, lo, ptr[r + 1], (kb + 1) * KC);
-    const int64_t rb = r / RB, lr = r - rb * RB;
+    const int64_t pos = rowpos[r], rb = pos / RB, lr = pos - rb * RB;
     int e = seg[(rb * nkb + kb) * RB + lr];
     for (int t = lo; t < hi; ++t, ++e) {
         const int slot = slotmap ? slotmap[t] : t;
@@ -292,7 +293,45 @@ fail:
 #undef SP_TRY
 }
 
+// nnz-balanced placement of rows into tiled positions (SURVEY §7 "nnz-balanced
+// scheduling"): rows sorted by length are dealt in snake order over the row
+// blocks, and within a block round-robin (snake) over the NW warps, so every
+// CTA and every warp gets a similar share of heavy and light rows (Zipf masks).
+// rowpos[r] = tiled position, rowmap[pos] = r (or -1 for unused positions).
+static void balanced_rows(const std::vector<int32_t> &ptr, int64_t rows, int RB, int NW, std::vector<int32_t> &rowpos,
+                          std::vector<int32_t> &rowmap) {
+    const int64_t nrb = (rows + RB - 1) / RB;
+    const int RPW = RB / NW;
+    std::vector<int32_t> order(rows);
+    for (int64_t r = 0; r < rows; ++r) order[r] = (int32_t)r;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t a, int32_t b) { return ptr[a + 1] - ptr[a] > ptr[b + 1] - ptr[b]; });
+    rowpos.assign(rows, 0);
+    rowmap.assign(nrb * RB, -1);
+    std::vector<int32_t> used(nrb, 0);
+    int64_t k = 0;
+    for (int64_t round = 0; k < rows; ++round) {
+        for (int64_t j = 0; j < nrb && k < rows; ++j) {
+            const int64_t blk = (round & 1) ? nrb - 1 - j : j;
+            if (used[blk] >= RB) continue;
+            const int s = used[blk]++;
+            const int wr = s / NW, wi = (wr & 1) ? NW - 1 - (s % NW) : s % NW;  // snake over warps
+            const int64_t pos = blk * RB + (int64_t)wi * RPW + wr;
+            rowpos[order[k]] = (int32_t)pos;
+            rowmap[pos] = order[k];
+            ++k;
+        }
+    }
+}
+
 sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
+    // host copies of the row / column pointers for the balanced placement
+    std::vector<int32_t> hptr[2];
+    hptr[0].resize(w->R + 1);
+    hptr[1].resize(w->C + 1);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(hptr[0].data(), w->row_ptr, (w->R + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost);
+    cudaMemcpy(hptr[1].data(), w->col_ptr, (w->C + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost);
     int64_t *info = nullptr, *mx = nullptr;
     if (cudaMallocAsync((void **)&info, 8 * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
     if (cudaMallocAsync((void **)&mx, 4 * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
@@ -321,14 +360,24 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
                 cudaFreeAsync(mx, st);
                 return SP_ERR_ALLOC;
             }
+            {
+                std::vector<int32_t> rowpos, rowmap;
+                balanced_rows(hptr[o], rows, t.RB, kTilNW[v], rowpos, rowmap);
+                if (dmalloc(&t.rowpos, rows) != cudaSuccess || dmalloc(&t.rowmap, (int64_t)t.nrb * t.RB) != cudaSuccess)
+                    return SP_ERR_ALLOC;
+                cudaMemcpy(t.rowpos, rowpos.data(), rows * sizeof(int32_t), cudaMemcpyHostToDevice);
+                cudaMemcpy(t.rowmap, rowmap.data(), (size_t)t.nrb * t.RB * sizeof(int32_t), cudaMemcpyHostToDevice);
+            }
             cudaMemsetAsync(cnt, 0, (size_t)nseg * sizeof(int32_t), st);
             cudaMemsetAsync(t.ent, 0, (size_t)cap * sizeof(int2), st);
             cudaMemsetAsync(t.vidx, 0xff, (size_t)cap * sizeof(int32_t), st);  // -1: no slot
             const int64_t nt = rows * t.nkb;
-            til_count_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, t.nkb, t.KC, t.RB, ptr, idx, cnt);
+            til_count_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, t.nkb, t.KC, t.RB, ptr, idx,
+                                                                          t.rowpos, cnt);
             scan_kernel<<<1, kScanThreads, 0, st>>>(nseg, cnt, t.seg, info + 2 * (o * 2 + v));
             til_fill_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, t.nkb, t.KC, t.RB, ptr, idx,
-                                                                         slotmap, t.seg, w->vals, t.ent, t.vidx);
+                                                                         slotmap, t.rowpos, t.seg, w->vals, t.ent,
+                                                                         t.vidx);
             til_max_kernel<<<1, 256, 0, st>>>((int64_t)t.nrb * t.nkb, t.RB, t.seg, mx + (o * 2 + v));
             cudaFreeAsync(cnt, st);
         }
@@ -352,9 +401,13 @@ void free_tilings(sp_weight_s *w) {
         cudaFree(t.seg);
         cudaFree(t.ent);
         cudaFree(t.vidx);
+        cudaFree(t.rowpos);
+        cudaFree(t.rowmap);
         t.seg = nullptr;
         t.ent = nullptr;
         t.vidx = nullptr;
+        t.rowpos = nullptr;
+        t.rowmap = nullptr;
     };
     for (auto &o : w->til)
         for (auto &t : o) fr(t);

@@ -41,6 +41,7 @@ struct FusedArgs {
     float *part;      // [nsplit x npad] or dW (direct)
     int64_t npad;
     int direct;
+    const int32_t *rowmap;  // tiled position -> row of X / dX (-1 unused)
 };
 
 template <int RPW, int NW, bool GATE, bool SENT>
@@ -104,8 +105,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
         if (kb == 0) {  // new slice: X rows into registers, dX accumulators reset
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
-                const int64_t r = r_base + i;
-                const float4 t = (r < a.nrow && bl + 4 <= B)
+                const int64_t r = __ldg(a.rowmap + r_base + i);
+                const float4 t = (r >= 0 && r < a.nrow && bl + 4 <= B)
                                      ? __ldg(reinterpret_cast<const float4 *>(a.X + r * B + bl))
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
                 rv[i][0] = t.x;
@@ -178,8 +179,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
         if (kb == a.nkb - 1) {  // slice done: dX rows (ReLU' gate fused)
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
-                const int64_t r = r_base + i;
-                if (r >= a.nrow || bl >= B) continue;
+                const int64_t r = __ldg(a.rowmap + r_base + i);
+                if (r < 0 || r >= a.nrow || bl >= B) continue;
                 float o[VEC];
                 if (GATE) {
                     const float4 hv = __ldg(reinterpret_cast<const float4 *>(a.H + r * B + bl));
@@ -230,7 +231,7 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     }
     launch_refresh(t, w->vals, w->nnz, st);  // CSC-tiled weights from vals (through perm)
     FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, (int)spl, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
-                direct ? 1 : 0};
+                direct ? 1 : 0, t.rowmap};
     auto pick = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<dim3((unsigned)t.nrb, (unsigned)nsplit), NW * 32, smem, st>>>(a, tmap);

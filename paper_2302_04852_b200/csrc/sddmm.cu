@@ -39,6 +39,7 @@ struct SddmmArgs {
     float *part;             // [nsplit x nnz] in entry order (or dW if direct)
     int64_t nnz;
     int direct;              // single split: write dW[vidx[e]] directly
+    const int32_t *rowmap;   // tiled position -> register-operand row (nullptr: identity)
     // conv (CONV=true): grid.z = tap; tap t uses taps[t]'s tiling, reads the
     // padded activation shifted by sh[t] columns, and keeps its partials at
     // part[split*nnz + tapbase[t] + e] (nnz = total padded entries of all taps)
@@ -127,7 +128,9 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
             const int64_t bl = s_lo + (int64_t)s * BT + lane * VEC;
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
-                const int64_t r = (int64_t)rb * RB + warp * RPW + i;
+                const int64_t tpos = (int64_t)rb * RB + warp * RPW + i;
+                int64_t r = a.rowmap ? (int64_t)__ldg(a.rowmap + tpos) : tpos;
+                if (r < 0) r = a.nrow;  // unused position: zeros
                 const float *src = a.regop + r * B + bl;
                 if (r < a.nrow && vec4 && VEC == 4 && bl + 4 <= B) {
                     const float4 t = __ldg(reinterpret_cast<const float4 *>(src));
@@ -277,7 +280,7 @@ sp_status launch_cfg(const sp_weight_s *w, const sp_tiling &t, const float *rego
     CUtensorMap tmap{};
     const bool tma = (B & 3) == 0 && make_tmap_2d(&tmap, smemop, t.inner, B, BT, t.KC);
     SddmmArgs a{t.rows, t.inner, B, t.KC, t.nkb, (int)spl, cap, tma ? 1 : 0, t.seg, t.ent, t.vidx, regop, smemop,
-                part, nnz, direct ? 1 : 0, nullptr, {}, {}};
+                part, nnz, direct ? 1 : 0, t.rowmap, nullptr, {}, {}};
     count_launches(direct ? 1 : 2);
     {
         auto kern = sent ? sddmm_tiled_kernel<VEC, RPW, NW, true, false> : sddmm_tiled_kernel<VEC, RPW, NW, false, false>;
@@ -347,7 +350,7 @@ bool launch_conv_sddmm(const sp_weight_s *w, int64_t B, const float *dYv, const 
         return false;
     cudaMemcpyAsync(tb_dev, tapbase, sizeof(tapbase), cudaMemcpyHostToDevice, st);
     SddmmArgs a{t0.rows, t0.inner, Lv, t0.KC, t0.nkb, (int)spl, cap, 1, nullptr, nullptr, nullptr, dYv, Xp,
-                part, tot, 0, w->tapdev, {}, {}};
+                part, tot, 0, nullptr, w->tapdev, {}, {}};
     for (int t = 0; t < ntap; ++t) {
         a.sh[t] = sh[t];
         a.tapbase[t] = tapbase[t];

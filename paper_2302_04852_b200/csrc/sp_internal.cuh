@@ -40,6 +40,10 @@ struct sp_tiling {
     int32_t max_tile;  // max (padded) entries in one (row block, column block) tile
     int64_t npad;      // padded entry total (segments padded to kTilPad with weight-0 entries)
     int64_t cap_ent;   // allocated entries
+    // nnz-balanced row placement: tiled position -> row (-1 unused) and back;
+    // rowmap == nullptr means identity (conv tap tilings)
+    int32_t *rowpos;   // [rows]
+    int32_t *rowmap;   // [nrb * RB]
 };
 
 struct sp_weight_s {
@@ -69,6 +73,7 @@ struct sp_weight_s {
 // Tiling variants (RB rows per CTA, KC inner columns per shared-memory tile).
 constexpr int kTilRB[2] = {128, 32};
 constexpr int kTilKC[2] = {192, 96};
+constexpr int kTilNW[2] = {16, 8};  // warps per CTA of the kernels using each variant (RB = NW * RPW)
 // Segments are padded to a multiple of kTilPad entries (offset -kTilRowBytes,
 // weight 0, vidx -1) so the kernels run tail-free groups of 4; every segment
 // starts at a multiple of 4 entries (16-byte aligned pairs).  A padding

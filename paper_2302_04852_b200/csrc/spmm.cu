@@ -38,6 +38,7 @@ struct SpmmArgs {
     const float *in;
     float *out;
     const float *gate;
+    const int32_t *rowmap;  // tiled position -> output row (nullptr: identity)
     // conv (CONV=true): the tile sequence runs over (tap, column block); tap t
     // uses taps[t]'s tiling and reads the padded input shifted by sh[t]
     // columns; output column n = ((p*Wv) + q)*B + b is stored compactly to
@@ -197,7 +198,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
         for (int i = 0; i < RPW; ++i) {
             const int64_t r = (int64_t)rb * RB + warp * RPW + i;
             if (r >= a.rows) continue;
-            float *dst = a.out + r * rowlen + col;
+            float *dst = a.out + r * rowlen + col;  // (tap tilings keep the identity row order)
             if constexpr (VEC == 4) *reinterpret_cast<float4 *>(dst) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
             else
 #pragma unroll
@@ -208,8 +209,9 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
     // Epilogue: ReLU / ReLU' gate fused; each element written once.
 #pragma unroll
     for (int i = 0; i < RPW; ++i) {
-        const int64_t r = (int64_t)rb * RB + warp * RPW + i;
-        if (r >= a.rows) continue;
+        const int64_t tpos = (int64_t)rb * RB + warp * RPW + i;
+        const int64_t r = a.rowmap ? (int64_t)__ldg(a.rowmap + tpos) : tpos;
+        if (r < 0 || r >= a.rows) continue;
         float o[VEC];
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
@@ -248,7 +250,8 @@ void launch_cfg(const sp_tiling &t, int64_t B, const float *in, float *out, cons
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
     CUtensorMap tmap{};
     const bool tma = (B & 3) == 0 && make_tmap_2d(&tmap, in, t.inner, B, BT, t.KC);
-    SpmmArgs a{t.rows, t.inner, B, t.KC, t.nkb, cap, tma ? 1 : 0, t.seg, t.ent, in, out, gate, 0, nullptr, {}, 0, 0, 0};
+    SpmmArgs a{t.rows, t.inner, B, t.KC, t.nkb, cap, tma ? 1 : 0, t.seg, t.ent, in, out, gate, t.rowmap,
+               0, nullptr, {}, 0, 0, 0};
     dim3 grid((unsigned)t.nrb, (unsigned)((B + BT - 1) / BT));
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -288,7 +291,7 @@ bool conv_spmm_vec(const sp_weight_s *w, int orient, int64_t B, const float *in,
     const size_t tiles = (size_t)2 * t0.KC * BT * sizeof(float);
     const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)kSmemLimit;
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
-    SpmmArgs a{t0.rows, t0.inner, B, t0.KC, t0.nkb, cap, 1, nullptr, nullptr, nullptr, out, nullptr,
+    SpmmArgs a{t0.rows, t0.inner, B, t0.KC, t0.nkb, cap, 1, nullptr, nullptr, nullptr, out, nullptr, nullptr,
                ntap, w->tapdev + orient * kMaxTaps, {}, Wv, OHv, OWv};
     for (int t = 0; t < ntap; ++t) a.sh[t] = sh[t];
     const int64_t Nv = OHv * Wv * B;
