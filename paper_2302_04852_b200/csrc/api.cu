@@ -120,6 +120,7 @@ sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8
         cudaFree(w->row_idx);
         cudaFree(w->perm);
         cudaFree(w->row_of);
+        cudaFree(w->chunk_ptr);
         free_tilings(w);
         w->magic = 0;
         delete w;
@@ -154,6 +155,7 @@ sp_status sp_weight_destroy(sp_weight_t w, sp_stream_t stream) {
     cudaFree(w->row_idx);
     cudaFree(w->perm);
     cudaFree(w->row_of);
+    cudaFree(w->chunk_ptr);
     free_tilings(w);
     w->magic = 0;
     delete w;

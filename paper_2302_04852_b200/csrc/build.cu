@@ -127,6 +127,11 @@ __global__ void csc_compact_kernel(int64_t R, int64_t C, const uint8_t *__restri
     }
 }
 
+__global__ void chunk_count_kernel(int64_t R, const int32_t *__restrict__ row_ptr, int32_t *__restrict__ cnt) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < R) cnt[r] = (row_ptr[r + 1] - row_ptr[r] + 31) >> 5;
+}
+
 __global__ void to_dense_kernel(int64_t nnz, int64_t C, const int32_t *__restrict__ row_of,
                                 const int32_t *__restrict__ col_idx, const float *__restrict__ nz,
                                 float *__restrict__ dense) {
@@ -266,6 +271,10 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
     csc_compact_kernel<<<(unsigned)((C + 127) / 128), 128, 0, st>>>(R, C, mask, slot, w->col_ptr,
                                                                    w->row_idx, w->perm);
     SP_TRY(cudaGetLastError());
+    // gather-SDDMM work list: chunks of <= 32 consecutive nonzeros of one row
+    SP_TRY(dmalloc(&w->chunk_ptr, R + 1));
+    chunk_count_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(R, w->row_ptr, rcnt);
+    scan_kernel<<<1, kScanThreads, 0, st>>>(R, rcnt, w->chunk_ptr, info);
     {
         const sp_status ts = build_tilings(w, st);
         if (ts != SP_OK) {

@@ -86,20 +86,26 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-// dW[j] = sum_b dY[row(j)][b] * X[col_idx[j]][b]; warp per (row, 32 entries),
-// looping over the whole batch; one transpose-reduce at the end.
+// dW[j] = sum_b dY[row(j)][b] * X[col_idx[j]][b]; warp per chunk of <= 32
+// consecutive nonzeros of one row (work list chunk_ptr: balanced for skewed
+// rows), looping over the whole batch; one transpose-reduce at the end.
 template <int VEC>
 __global__ void __launch_bounds__(256)
-    sddmm_gather_kernel(int64_t R, int64_t B, int chunks_per_row, const int32_t *__restrict__ row_ptr,
-                        const int32_t *__restrict__ col_idx, const float *__restrict__ X,
-                        const float *__restrict__ dY, float *__restrict__ dW) {
+    sddmm_gather_kernel(int64_t R, int64_t B, const int32_t *__restrict__ chunk_ptr,
+                        const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col_idx,
+                        const float *__restrict__ X, const float *__restrict__ dY, float *__restrict__ dW) {
     const int lane = threadIdx.x & 31;
     const int64_t wid = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int64_t r = wid / chunks_per_row;
-    if (r >= R) return;
-    const int j0 = __ldg(row_ptr + r) + (int)(wid - r * chunks_per_row) * 32;
+    if (wid >= __ldg(chunk_ptr + R)) return;
+    int64_t lo = 0, hi = R;  // row r with chunk_ptr[r] <= wid < chunk_ptr[r+1]
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(chunk_ptr + mid) <= wid) lo = mid;
+        else hi = mid;
+    }
+    const int64_t r = lo;
+    const int j0 = __ldg(row_ptr + r) + (int)(wid - __ldg(chunk_ptr + r)) * 32;
     const int end = __ldg(row_ptr + r + 1);
-    if (j0 >= end) return;
     const int n = min(32, end - j0);
     const int cl = lane < n ? __ldg(col_idx + j0 + lane) : 0;
     const bool vec = (B % VEC) == 0;
@@ -129,12 +135,13 @@ __global__ void __launch_bounds__(256)
 
 // Gather path wins when staging would move more bytes than gathering:
 // nrb * inner (tile rows streamed per batch column) > nnz (rows gathered).
-bool gather_preferred(const sp_weight_s *w, int orient, int64_t B) {
-    // one warp walks a whole row here: skewed rows (Zipf) would serialise the
-    // tail, so only balanced structures take this path
+bool gather_preferred(const sp_weight_s *w, int orient, int64_t B, bool chunked) {
+    // the gather SpMM walks a whole row per warp: skewed rows (Zipf) would
+    // serialise the tail, so only balanced structures take it (the SDDMM's
+    // 32-nonzero chunks are balanced by construction)
     const int64_t rows = orient == 0 ? w->R : w->C;
     const int64_t mx = orient == 0 ? w->max_row_nnz : w->max_col_nnz;
-    if ((double)mx > 4.0 * (double)w->nnz / (double)rows + 64.0) return false;
+    if (!chunked && (double)mx > 4.0 * (double)w->nnz / (double)rows + 64.0) return false;
     const sp_tiling &t = w->til[orient][1];  // the smallest tiling the tiled path would fall back to
     const sp_tiling &t0 = w->til[orient][0];
     const int64_t slices = (B + 127) / 128;
@@ -172,11 +179,10 @@ void launch_spmm_gather(const sp_weight_s *w, int orient, int64_t B, const float
 
 void launch_sddmm_gather(const sp_weight_s *w, const float *X, const float *dY, float *dW, int64_t B,
                          cudaStream_t st) {
-    const int cpr = std::max(1, (w->max_row_nnz + 31) / 32);
-    const int64_t warps = w->R * cpr;
+    const int64_t warps = w->nnz / 32 + w->R;  // >= number of chunks
     auto go = [&](auto kern) {
         count_launches(1);
-        kern<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(w->R, B, cpr, w->row_ptr, w->col_idx, X, dY, dW);
+        kern<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(w->R, B, w->chunk_ptr, w->row_ptr, w->col_idx, X, dY, dW);
     };
     if (B >= 128) go(sddmm_gather_kernel<4>);
     else if (B >= 64) go(sddmm_gather_kernel<2>);

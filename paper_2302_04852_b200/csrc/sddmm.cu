@@ -373,7 +373,7 @@ void launch_split_reduce(int64_t npad, int nsplit, const float *part, const int3
 sp_status launch_sddmm(const sp_weight_s *w, const float *X, const float *dY, float *dW, int64_t B,
                        cudaStream_t st) {
     if (w->nnz == 0) return SP_OK;
-    if (gather_preferred(w, 0, B)) {
+    if (gather_preferred(w, 0, B, true)) {
         launch_sddmm_gather(w, X, dY, dW, B, st);
         return SP_OK;
     }

@@ -60,6 +60,7 @@ struct sp_weight_s {
     // row of every CSR slot (for the SDDMM chunk walk and to_dense)
     int32_t *row_of;
     int32_t max_row_nnz, max_col_nnz;
+    int32_t *chunk_ptr;  // [R+1] exclusive scan of ceil(row nnz / 32) (gather SDDMM work list)
     // tilings: [orientation 0 = CSR rows, 1 = CSC columns][variant 0 = big, 1 = small]
     sp_tiling til[2][2];
     // conv handles (sp_weight_create_conv): filter taps and, per tap (x, y),
@@ -120,7 +121,7 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
                  const float *gate, int epi, cudaStream_t st);
 
 // ---- gather.cu (very sparse / small regime: no shared-memory staging) ----
-bool gather_preferred(const sp_weight_s *w, int orient, int64_t B);
+bool gather_preferred(const sp_weight_s *w, int orient, int64_t B, bool chunked = false);
 void launch_spmm_gather(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out,
                         const float *gate, int epi, cudaStream_t st);
 void launch_sddmm_gather(const sp_weight_s *w, const float *X, const float *dY, float *dW, int64_t B,
