@@ -141,6 +141,17 @@ def main():
             if a.quick:
                 break
     recs.append(linear("paper_B902", 3072, 768, 902, 0.1, 1.0 / 768, 990, reps=a.reps))
+    # runtime linear in nnz (SPEC S578-S586 idea): least-squares fit over the cfg4 sweep
+    for kind in ("uniform", "zipf"):
+        pts = [(r["nnz"], r["t_fwd_bwd_us"]) for r in recs if r["config"] == "cfg4" and r.get("mask") == kind]
+        if len(pts) >= 3:
+            x = np.array([p[0] for p in pts], dtype=np.float64)
+            y = np.array([p[1] for p in pts], dtype=np.float64)
+            A = np.vstack([x, np.ones_like(x)]).T
+            (slope, icpt), *_ = np.linalg.lstsq(A, y, rcond=None)
+            r2 = 1.0 - float(np.sum((y - A @ [slope, icpt]) ** 2)) / float(np.sum((y - y.mean()) ** 2))
+            recs.append({"config": "cfg4_linearity", "mask": kind, "slope_us_per_Mnnz": round(slope * 1e6, 3),
+                         "intercept_us": round(icpt, 2), "r2": round(r2, 4), "points": len(pts)})
     out = open(a.out, "w") if a.out else sys.stdout
     for r in recs:
         out.write(json.dumps(r) + "\n")
