@@ -108,6 +108,11 @@ sp_status sp_weight_indices(sp_weight_t W, const int32_t **row_ptr, const int32_
 sp_status sp_weight_to_dense(sp_weight_t W, const float *nz, float *dense_out,
                              sp_stream_t stream);
 
+/* Adjoint of sp_weight_to_dense: nz_out[j] = dense[r_j][c_j] for every stored
+ * (r_j, c_j) (CSR order).  Restricts a dense R x C gradient to the mask (the
+ * dense path of the §4.2 dispatcher, P427). */
+sp_status sp_weight_gather(sp_weight_t W, const float *dense, float *nz_out, sp_stream_t stream);
+
 /* ---------------------------------------------------------------------- */
 /* Linear layer (P141-P151 §3.2)                                          */
 /* ---------------------------------------------------------------------- */

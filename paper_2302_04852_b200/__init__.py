@@ -8,6 +8,8 @@ the C ABI in include/sparseprop.h (libsparseprop.so, built in-tree).
     W = sp.sp_weight_create(dense_cuda, mask_cuda)
     Y = sp.sp_linear_fwd(W, X)            # X [C x B] -> Y [R x B]
 
-`dp` holds the data-parallel sparse MLP step (north star cfg5).
+`nn` holds drop-in `SparseLinear` / `SparseConv2d` modules with the paper's
+§4.2 dense/sparse dispatcher; `dp` the data-parallel sparse MLP step (north
+star cfg5); `prune` magnitude pruning and the GMP schedule (mask updates).
 """
-__all__ = ["sparseprop", "dp"]
+__all__ = ["sparseprop", "nn", "dp", "prune"]

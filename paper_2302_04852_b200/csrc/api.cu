@@ -191,6 +191,13 @@ sp_status sp_weight_to_dense(sp_weight_t w, const float *nz, float *dense_out, s
     return check_launch("sp_weight_to_dense");
 }
 
+sp_status sp_weight_gather(sp_weight_t w, const float *dense, float *nz_out, sp_stream_t stream) {
+    SP_CHECK_HANDLE(w, "sp_weight_gather");
+    if (!dense || (!nz_out && w->nnz > 0)) return fail(SP_ERR_NULL, "sp_weight_gather: NULL buffer");
+    launch_gather_dense(w, dense, nz_out, S(stream));
+    return check_launch("sp_weight_gather");
+}
+
 static sp_status linear_fwd_impl(sp_weight_t w, const float *X, float *Y, int64_t B, int epi,
                                  sp_stream_t stream, const char *fn) {
     SP_CHECK_HANDLE(w, fn);

@@ -127,6 +127,13 @@ __global__ void csc_compact_kernel(int64_t R, int64_t C, const uint8_t *__restri
     }
 }
 
+__global__ void gather_dense_kernel(int64_t nnz, int64_t C, const int32_t *__restrict__ row_of,
+                                    const int32_t *__restrict__ col_idx, const float *__restrict__ dense,
+                                    float *__restrict__ nz) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < nnz) nz[j] = dense[(int64_t)row_of[j] * C + col_idx[j]];
+}
+
 __global__ void chunk_count_kernel(int64_t R, const int32_t *__restrict__ row_ptr, int32_t *__restrict__ cnt) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r < R) cnt[r] = (row_ptr[r + 1] - row_ptr[r] + 31) >> 5;
@@ -446,6 +453,14 @@ __global__ void til_refresh_taps_kernel(const TapDev *__restrict__ taps, const f
 void launch_refresh_taps(const sp_weight_s *w, int orient, int ntap, cudaStream_t st) {
     count_launches(1);
     til_refresh_taps_kernel<<<dim3(64, ntap), 256, 0, st>>>(w->tapdev + orient * kMaxTaps, w->vals);
+}
+
+void launch_gather_dense(const sp_weight_s *w, const float *dense, float *nz, cudaStream_t st) {
+    if (w->nnz > 0) {
+        count_launches(1);
+        gather_dense_kernel<<<(unsigned)((w->nnz + 255) / 256), 256, 0, st>>>(w->nnz, w->C, w->row_of, w->col_idx,
+                                                                              dense, nz);
+    }
 }
 
 void launch_to_dense(const sp_weight_s *w, const float *nz, float *dense, cudaStream_t st) {

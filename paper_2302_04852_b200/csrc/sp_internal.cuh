@@ -107,6 +107,7 @@ bool make_tmap_2d(CUtensorMap *map, const float *base, int64_t rows, int64_t B, 
 sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *mask,
                        cudaStream_t st, sp_weight_s *w);
 void launch_to_dense(const sp_weight_s *w, const float *nz, float *dense, cudaStream_t st);
+void launch_gather_dense(const sp_weight_s *w, const float *dense, float *nz, cudaStream_t st);
 sp_status build_tilings(sp_weight_s *w, cudaStream_t st);
 void free_tilings(sp_weight_s *w);
 // ent[e].y = bits(vals[vidx[e]]) for one tiling (before an SpMM launch)

@@ -1,0 +1,214 @@
+"""Drop-in PyTorch modules over libsparseprop (the paper's "two Pytorch modules,
+one for linear and one for convolution layers", P358 §4) and the §4.2
+dense/sparse dispatcher (P427-P429).
+
+`SparseLinear` / `SparseConv2d` hold their kept weights as a Parameter that IS
+the handle's vals buffer (zero-copy), so any torch optimizer updates the
+weights the kernels read.  Autograd runs the library's kernels: forward SpMM,
+and the fused CSC-driven backward (dX and dW in one pass) -- dW is produced
+only at the nonzeros.  Layouts: `SparseLinear` takes PyTorch's [N, in] inputs
+(transposed to the kernels' batch-contiguous [in, N] internally) or, with
+feature_major=True, [in, N] directly; `SparseConv2d` takes NCHW (permuted to
+the kernels' CHWN) or, with batch_last=True, CHWN directly.
+
+Dispatcher (P427-P429): a module less than 80 % sparse runs dense; at >= 80 %
+the first forward+backward on a probe batch is timed both ways (CUDA events)
+and the faster implementation is kept until the mask changes
+(`set_mask`).  The dense path is a cuBLAS / cuDNN call on the densified
+weight (sp_weight_to_dense) with its gradient restricted to the mask by
+sp_weight_gather -- both libsparseprop kernels.  `timer` can be replaced
+(tests use a fake one).
+"""
+from __future__ import annotations
+
+import torch
+import torch.nn.functional as F
+
+from . import sparseprop as sp
+
+DENSE_BELOW = 0.80  # P427: "dense ... as long as they are less than 80% sparse"
+
+
+# ---------------------------------------------------------------------------
+# autograd functions (feature-major / batch-last layouts; kernels only)
+# ---------------------------------------------------------------------------
+class _SparseLinearFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, xt, vals, W):  # xt [in, N] contiguous
+        ctx.W = W
+        ctx.save_for_backward(xt)
+        return sp.sp_linear_fwd(W, xt)
+
+    @staticmethod
+    def backward(ctx, gy):
+        (xt,) = ctx.saved_tensors
+        dX, dW = sp.sp_linear_bwd(ctx.W, xt, gy.contiguous())
+        return dX, dW, None
+
+
+class _DenseMaskedFn(torch.autograd.Function):
+    """Dense path: y = W_dense @ x with W_dense = to_dense(vals); dvals = gather(dW_dense)."""
+
+    @staticmethod
+    def forward(ctx, xt, vals, W):
+        Wd = W.to_dense(vals)
+        ctx.W = W
+        ctx.save_for_backward(xt, Wd)
+        return Wd @ xt
+
+    @staticmethod
+    def backward(ctx, gy):
+        xt, Wd = ctx.saved_tensors
+        dX = Wd.t() @ gy
+        dvals = sp.sp_weight_gather(ctx.W, gy @ xt.t())
+        return dX, dvals, None
+
+
+class _SparseConvFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, vals, W, g):  # x CHWN contiguous
+        ctx.W, ctx.g = W, g
+        ctx.save_for_backward(x)
+        return sp.sp_conv2d_fwd(W, g, x)
+
+    @staticmethod
+    def backward(ctx, gy):
+        (x,) = ctx.saved_tensors
+        gy = gy.contiguous()
+        dX = sp.sp_conv2d_bwd_input(ctx.W, ctx.g, gy)
+        dW = sp.sp_conv2d_bwd_weight(ctx.W, ctx.g, x, gy)
+        return dX, dW, None, None
+
+
+class _DenseConvFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, vals, W, g):  # x CHWN
+        Wd = W.to_dense(vals).view(W.filter_shape)
+        xn = x.permute(3, 0, 1, 2)
+        ctx.W, ctx.g = W, g
+        ctx.save_for_backward(xn, Wd)
+        return F.conv2d(xn, Wd, padding=g.pad).permute(1, 2, 3, 0).contiguous()
+
+    @staticmethod
+    def backward(ctx, gy):
+        xn, Wd = ctx.saved_tensors
+        gyn = gy.permute(3, 0, 1, 2)
+        dxn = torch.nn.grad.conv2d_input(xn.shape, Wd, gyn, padding=ctx.g.pad)
+        dWd = torch.nn.grad.conv2d_weight(xn, Wd.shape, gyn, padding=ctx.g.pad)
+        dvals = sp.sp_weight_gather(ctx.W, dWd.reshape(Wd.shape[0], -1))
+        return dxn.permute(1, 2, 3, 0).contiguous(), dvals, None, None
+
+
+# ---------------------------------------------------------------------------
+# dispatcher (P427-P429)
+# ---------------------------------------------------------------------------
+def cuda_timer(fn, reps: int = 1) -> float:
+    """Device time (ms) of fn() on the current stream, CUDA events, after one warm-up."""
+    fn()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    e.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def decide(sparsity: float, time_dense, time_sparse, mode: str = "auto") -> str:
+    """The §4.2 rule: forced modes win; below 80 % sparsity -> dense without
+    probing; otherwise the faster of one timed dense and one timed sparse
+    forward+backward."""
+    if mode in ("dense", "sparse"):
+        return mode
+    if sparsity < DENSE_BELOW:
+        return "dense"
+    return "sparse" if time_sparse() <= time_dense() else "dense"
+
+
+class _Dispatching(torch.nn.Module):
+    def __init__(self, mode: str, timer):
+        super().__init__()
+        self.mode = mode
+        self.timer = timer
+        self.impl = None  # decided lazily on the first batch, reset by set_mask
+        self.probe_ms = None
+
+    @property
+    def sparsity(self) -> float:
+        return 1.0 - self.W.nnz / float(self.W.R * self.W.C)
+
+    def _choose(self, x):
+        if self.impl is None:
+            def run(fn):
+                def go():
+                    xx = x.detach().requires_grad_(x.requires_grad)
+                    out = fn(xx)
+                    out.backward(torch.ones_like(out))
+                return lambda: self.timer(go)
+            self.probe_ms = {}
+
+            def td():
+                self.probe_ms["dense"] = run(lambda xx: self._run(xx, "dense"))()
+                return self.probe_ms["dense"]
+
+            def ts():
+                self.probe_ms["sparse"] = run(lambda xx: self._run(xx, "sparse"))()
+                return self.probe_ms["sparse"]
+            self.impl = decide(self.sparsity, td, ts, self.mode)
+            if self.vals.grad is not None:  # probes must not leak gradients
+                self.vals.grad = None
+        return self.impl
+
+
+class SparseLinear(_Dispatching):
+    """y = x W^T with W (out x in) restricted to a fixed mask (no bias)."""
+
+    def __init__(self, weight: torch.Tensor, mask: torch.Tensor, feature_major: bool = False,
+                 mode: str = "auto", timer=cuda_timer):
+        super().__init__(mode, timer)
+        self.feature_major = feature_major
+        self.set_mask(weight, mask)
+
+    def set_mask(self, weight: torch.Tensor, mask: torch.Tensor):
+        """(Re)build the sparse structure (masks change "only a few times", P428)."""
+        self.W = sp.sp_weight_create(weight.detach().float().contiguous(), mask.to(torch.uint8).contiguous())
+        self.vals = torch.nn.Parameter(self.W.vals, requires_grad=True)
+        self.impl = None
+
+    def _run(self, x, impl):
+        xt = x if self.feature_major else x.t()
+        xt = xt.contiguous()
+        fn = _SparseLinearFn if impl == "sparse" else _DenseMaskedFn
+        y = fn.apply(xt, self.vals, self.W)
+        return y if self.feature_major else y.t()
+
+    def forward(self, x):
+        return self._run(x, self._choose(x))
+
+
+class SparseConv2d(_Dispatching):
+    """Stride-1 conv with a fixed sparse filter [OC][IC][KH][KW] (no bias)."""
+
+    def __init__(self, weight: torch.Tensor, mask: torch.Tensor, padding: int = 0, batch_last: bool = False,
+                 mode: str = "auto", timer=cuda_timer):
+        super().__init__(mode, timer)
+        self.padding = padding
+        self.batch_last = batch_last
+        self.set_mask(weight, mask)
+
+    def set_mask(self, weight: torch.Tensor, mask: torch.Tensor):
+        self.W = sp.sp_weight_create(weight.detach().float().contiguous(), mask.to(torch.uint8).contiguous())
+        self.vals = torch.nn.Parameter(self.W.vals, requires_grad=True)
+        self.impl = None
+
+    def _run(self, x, impl):
+        xc = x if self.batch_last else x.permute(1, 2, 3, 0)
+        xc = xc.contiguous()
+        C, H, Wd, B = xc.shape
+        g = sp.conv_geom(self.W, B, H, Wd, self.padding)
+        fn = _SparseConvFn if impl == "sparse" else _DenseConvFn
+        y = fn.apply(xc, self.vals, self.W, g)
+        return y if self.batch_last else y.permute(3, 0, 1, 2)
+
+    def forward(self, x):
+        return self._run(x, self._choose(x))

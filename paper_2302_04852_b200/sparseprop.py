@@ -28,7 +28,7 @@ EXPORTS = [
     "sp_linear_bwd_input", "sp_linear_bwd_weight", "sp_linear_fwd_relu",
     "sp_linear_bwd_input_relu", "sp_conv2d_fwd", "sp_conv2d_bwd_input", "sp_conv2d_bwd_weight",
     "sp_mse_scratch_floats", "sp_mse_grad", "sp_sgd", "sp_last_error", "sp_version",
-    "sp_launch_count", "sp_linear_bwd", "sp_linear_bwd_relu", "sp_weight_create_conv",
+    "sp_launch_count", "sp_linear_bwd", "sp_linear_bwd_relu", "sp_weight_create_conv", "sp_weight_gather",
 ]
 
 
@@ -61,6 +61,7 @@ def lib() -> ct.CDLL:
             "sp_weight_vals": (st, [vp, ct.POINTER(vp)]),
             "sp_weight_indices": (st, [vp] + [ct.POINTER(vp)] * 5),
             "sp_weight_to_dense": (st, [vp, vp, vp, vp]),
+            "sp_weight_gather": (st, [vp, vp, vp, vp]),
             "sp_linear_fwd": (st, [vp, vp, vp, i64, vp]),
             "sp_linear_fwd_relu": (st, [vp, vp, vp, i64, vp]),
             "sp_linear_bwd_input": (st, [vp, vp, vp, i64, vp]),
@@ -205,6 +206,17 @@ def sp_weight_to_dense(W: SparseWeight, nz: torch.Tensor, out: torch.Tensor, str
     _check(lib().sp_weight_to_dense(W.handle, _dev(nz, torch.float32, "nz") if W.nnz else None,
                                     _dev(out, torch.float32, "out"), _stream(stream)))
     return out
+
+
+def sp_weight_gather(W: SparseWeight, dense: torch.Tensor, nz: torch.Tensor | None = None, stream=None):
+    """nz[j] = dense[r_j][c_j] (restrict a dense R x C tensor to the mask)."""
+    if nz is None:
+        nz = torch.empty(W.nnz, dtype=torch.float32, device=dense.device)
+    if tuple(dense.shape[-2:]) != (W.R, W.C) and dense.numel() != W.R * W.C:
+        raise ValueError("dense must hold R x C values")
+    _check(lib().sp_weight_gather(W.handle, _dev(dense.contiguous(), torch.float32, "dense"),
+                                  _dev(nz, torch.float32, "nz") if W.nnz else None, _stream(stream)))
+    return nz
 
 
 def _B(t: torch.Tensor, rows: int, name: str) -> int:

@@ -1,0 +1,74 @@
+"""Drop-in modules (P358) against PyTorch float64 autograd on the masked dense
+weight: outputs and gradients (input and kept weights) for the sparse path,
+the dense path of the dispatcher, and the automatic choice."""
+import numpy as np
+import pytest
+
+import synth
+from conftest import tol_ok
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _ok(name, got, ref):
+    ok, err, bound = tol_ok(got.detach().cpu().double().numpy(), ref.detach().cpu().double().numpy())
+    assert ok, f"{name}: {err:.3e} > {bound:.3e}"
+
+
+@pytest.mark.parametrize("mode", ["sparse", "dense", "auto"])
+@pytest.mark.parametrize("feature_major", [False, True])
+def test_sparse_linear_module(mode, feature_major):
+    from paper_2302_04852_b200.nn import SparseLinear
+    c = synth.linear_case(384, 256, 192, 0.1, 1.0 / 256, 31)
+    m = SparseLinear(torch.from_numpy(c["W"]).cuda(), torch.from_numpy(c["mask"]).cuda(),
+                     feature_major=feature_major, mode=mode)
+    X = torch.from_numpy(c["X"] if feature_major else c["X"].T.copy()).cuda().requires_grad_(True)
+    G = torch.from_numpy(c["dY"] if feature_major else c["dY"].T.copy()).cuda()
+    y = m(X)
+    y.backward(G)
+    torch.cuda.synchronize()
+    # float64 reference
+    Wm = torch.from_numpy(c["W"].astype(np.float64) * c["mask"]).requires_grad_(True)
+    Xr = X.detach().cpu().double().requires_grad_(True)
+    yr = (Wm @ Xr) if feature_major else (Xr @ Wm.t())
+    yr.backward(G.cpu().double())
+    _ok("y", y, yr)
+    _ok("dX", X.grad, Xr.grad)
+    rows, cols = np.nonzero(c["mask"])
+    _ok("dvals", m.vals.grad, Wm.grad[rows, cols])
+    if mode != "auto":
+        assert m.impl == mode
+
+
+def test_sparse_linear_optimizer_updates_kept_weights_only():
+    from paper_2302_04852_b200.nn import SparseLinear
+    c = synth.linear_case(256, 128, 128, 0.05, 1.0 / 128, 32)
+    m = SparseLinear(torch.from_numpy(c["W"]).cuda(), torch.from_numpy(c["mask"]).cuda(), mode="sparse")
+    opt = torch.optim.SGD(m.parameters(), lr=0.1)
+    x = torch.from_numpy(c["X"].T.copy()).cuda()
+    before = m.W.to_dense().cpu().numpy()
+    m(x).pow(2).sum().backward()
+    opt.step()
+    after = m.W.to_dense().cpu().numpy()
+    assert np.all(after[c["mask"] == 0] == 0.0)
+    assert np.any(after[c["mask"] == 1] != before[c["mask"] == 1])
+
+
+@pytest.mark.parametrize("mode", ["sparse", "dense"])
+def test_sparse_conv_module(mode):
+    from paper_2302_04852_b200.nn import SparseConv2d
+    c = synth.conv_case(OC=24, IC=16, H=9, W=9, KH=3, KW=3, pad=1, B=8, density=0.15, wvar=1.0 / 144, seed=33)
+    m = SparseConv2d(torch.from_numpy(c["W"]).cuda(), torch.from_numpy(c["mask"]).cuda(), padding=1, mode=mode)
+    Xn = torch.from_numpy(np.ascontiguousarray(np.transpose(c["X"], (3, 0, 1, 2)))).cuda().requires_grad_(True)
+    Gn = torch.from_numpy(np.ascontiguousarray(np.transpose(c["dY"], (3, 0, 1, 2)))).cuda()
+    y = m(Xn)
+    y.backward(Gn)
+    torch.cuda.synchronize()
+    Wm = torch.from_numpy(c["W"].astype(np.float64) * c["mask"]).requires_grad_(True)
+    Xr = Xn.detach().cpu().double().requires_grad_(True)
+    yr = torch.nn.functional.conv2d(Xr, Wm, padding=1)
+    yr.backward(Gn.cpu().double())
+    _ok("y", y, yr)
+    _ok("dX", Xn.grad, Xr.grad)
+    _ok("dvals", m.vals.grad, Wm.grad[np.nonzero(c["mask"])])
