@@ -72,3 +72,22 @@ def test_sparse_conv_module(mode):
     _ok("y", y, yr)
     _ok("dX", Xn.grad, Xr.grad)
     _ok("dvals", m.vals.grad, Wm.grad[np.nonzero(c["mask"])])
+
+
+def test_gmp_mask_update_rebuilds_and_stays_exact():
+    """F4: prune a module from 80 % to 95 % by magnitude; the rebuilt structure
+    matches a fresh handle built from the pruned weights, and the module still
+    matches the float64 reference."""
+    from paper_2302_04852_b200.nn import SparseLinear
+    from paper_2302_04852_b200.prune import prune_modules
+    c = synth.linear_case(512, 384, 256, 0.2, 1.0 / 384, 34)
+    m = SparseLinear(torch.from_numpy(c["W"]).cuda(), torch.from_numpy(c["mask"]).cuda(), mode="sparse")
+    rep = prune_modules([m], 0.95)
+    assert abs(rep["sparsity"][0] - 0.95) < 1.0 / (512 * 384) + 1e-9
+    assert rep["rebuild_s"] >= 0.0
+    Wd = m.W.to_dense().cpu().double()
+    kept = (m.W.to_dense(torch.ones(m.W.nnz, device="cuda")) != 0).cpu().numpy()
+    assert np.all(kept <= c["mask"].astype(bool))              # nested in the old mask
+    x = torch.from_numpy(c["X"].T.copy()).cuda()
+    y = m(x)
+    _ok("y after pruning", y, x.cpu().double() @ Wd.t())
