@@ -34,6 +34,11 @@ def gmp_target_at(epoch: int, final: float, start: int = 10, end: int = 80, ever
     return initial + (final - initial) * (1.0 - (1.0 - t) ** 3)
 
 
+def _n_keep(sparsity: float, n: int) -> int:
+    """ceil((1 - s) n), robust to the binary representation of s (0.95 etc.)."""
+    return min(n, math.ceil((1.0 - sparsity) * n - 1e-9))
+
+
 def _keep_top(scores: torch.Tensor, n_keep: int) -> torch.Tensor:
     """Boolean mask keeping the n_keep largest scores (ties: smaller index first)."""
     flat = scores.flatten()
@@ -51,8 +56,7 @@ def magnitude_mask(weight: torch.Tensor, sparsity: float, current: torch.Tensor 
     scores = weight.detach().abs().float()
     if current is not None:
         scores = torch.where(current.bool(), scores, torch.full_like(scores, -1.0))
-    n_keep = math.ceil((1.0 - sparsity) * weight.numel())
-    return _keep_top(scores, n_keep)
+    return _keep_top(scores, _n_keep(sparsity, weight.numel()))
 
 
 def global_magnitude_masks(weights: list[torch.Tensor], sparsity: float,
@@ -67,7 +71,7 @@ def global_magnitude_masks(weights: list[torch.Tensor], sparsity: float,
             s = torch.where(currents[i].bool().flatten(), s, torch.full_like(s, -1.0))
         scores.append(s)
     allsc = torch.cat(scores)
-    keep = _keep_top(allsc, math.ceil((1.0 - sparsity) * allsc.numel()))
+    keep = _keep_top(allsc, _n_keep(sparsity, allsc.numel()))
     out, off = [], 0
     for w in weights:
         out.append(keep[off:off + w.numel()].view(w.shape))
