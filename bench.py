@@ -317,6 +317,13 @@ def main():
         # fused backward runs two (dX and dW) per launch
         fl = sum(2 * (W1.nnz + W2.nnz) * model.T for W1, W2 in model.W) * (2 if dom == "bwd_fused" else 1)
         achieved = fl / (ktime[dom] * 1e-3) / 1e12
+        # DRAM traffic per launch of this kernel from the committed ncu --set full capture
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "r1_kernel_traffic.json")
+        if os.path.exists(tf):
+            kt_ = json.load(open(tf)).get("kernels", {}).get(dom)
+            if kt_:
+                traffic = kt_["traffic_bytes_per_launch_mean"]
         step_roof_ms = model.step_flops() / (fp32_peak * 1e12) * 1e3
         line = {
             "metric": "sparse fwd+bwd effective GFLOP/s (2*nnz*B)", "value": value, "unit": "GFLOP/s",
@@ -329,7 +336,8 @@ def main():
                        "l2": "no flush: per-step working set (activations >= 300 MB per rank) > 126 MB L2",
                        "nnz_total": model.nnz_total},
             "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": fp32_peak,
-                         "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": traffic,
+                         "traffic_unit": "bytes per launch (dram read + write, ncu --set full, profiles/)",
                          "peak_source": f"FP32 FMA: 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz "
                                         f"(sm_max_mhz, {peaks['source']})",
                          "per_kernel_ms_per_step": ktime,
