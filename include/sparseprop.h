@@ -20,8 +20,9 @@
  *  - Every compute call only enqueues work on `stream` (a cudaStream_t
  *    passed as void*; NULL = legacy default stream) and never synchronises
  *    the host; asynchronous device faults surface at the caller's next sync.
- *    sp_weight_create synchronises `stream` (twice: to learn nnz and the
- *    tile sizes of its cached schedule); compute calls never do.
+ *    sp_weight_create / sp_weight_create_conv synchronise `stream` several
+ *    times (to read nnz, the per-block row counts and the tile maxima of
+ *    the cached schedule); compute calls never do.
  *  - No atomics anywhere: results are bitwise run-to-run reproducible.
  *  - Errors: every call returns sp_status; no C++ exception crosses the
  *    ABI.  Arguments are validated before any launch; launch failures are
@@ -71,7 +72,8 @@ typedef struct {
  *   perm[nnz] (CSC slot k -> CSR slot holding the same (r, c)),
  * plus the tiled copies of both orientations the kernels stream (row blocks x
  * column blocks), deterministically on the device; it
- * synchronises `stream` twice (to read nnz and the tile maxima).  R, C >= 1; R*C and nnz must fit int32 (else SP_ERR_OVERFLOW).
+ * synchronises `stream` (to read nnz, block row counts and tile maxima).
+ * R, C >= 1; R*C and nnz must fit int32 (else SP_ERR_OVERFLOW).
  * The handle owns all its device buffers. */
 sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8_t *mask,
                            sp_stream_t stream, sp_weight_t *out);
