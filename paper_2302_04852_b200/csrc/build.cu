@@ -208,6 +208,32 @@ __global__ void til_max_kernel(int64_t ntiles, int RB, const int32_t *__restrict
     if (threadIdx.x == 0) *out = sh[0];
 }
 
+// max over (row block, warp) of the warp's padded entries summed over all column
+// blocks (rows rb*RB + w*RPW .. +RPW), single block, fixed order.  Bounds the
+// per-warp dW accumulator columns of the TMEM fused backward.
+__global__ void til_warp_max_kernel(int nrb, int nkb, int RB, int RPW, const int32_t *__restrict__ seg,
+                                    int64_t *__restrict__ out) {
+    __shared__ int32_t sh[256];
+    const int nw = RB / RPW;
+    int32_t m = 0;
+    for (int i = threadIdx.x; i < nrb * nw; i += blockDim.x) {
+        const int rb = i / nw, wi = i - rb * nw;
+        int32_t s = 0;
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int64_t t = ((int64_t)rb * nkb + kb) * RB + (int64_t)wi * RPW;
+            s += seg[t + RPW] - seg[t];
+        }
+        m = max(m, s);
+    }
+    sh[threadIdx.x] = m;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) sh[threadIdx.x] = max(sh[threadIdx.x], sh[threadIdx.x + o]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
 __global__ void til_refresh_kernel(int64_t nnz, const int32_t *__restrict__ vidx, const float *__restrict__ vals,
                                    int2 *__restrict__ ent) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -350,7 +376,7 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
     cudaMemcpy(hptr[1].data(), w->col_ptr, (w->C + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost);
     int64_t *info = nullptr, *mx = nullptr;
     if (cudaMallocAsync((void **)&info, 8 * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
-    if (cudaMallocAsync((void **)&mx, 4 * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
+    if (cudaMallocAsync((void **)&mx, 8 * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
     for (int o = 0; o < 2; ++o) {
         const int64_t rows = o == 0 ? w->R : w->C, inner = o == 0 ? w->C : w->R;
         const int32_t *ptr = o == 0 ? w->row_ptr : w->col_ptr;
@@ -395,16 +421,18 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
                                                                          slotmap, t.rowpos, t.seg, w->vals, t.ent,
                                                                          t.vidx);
             til_max_kernel<<<1, 256, 0, st>>>((int64_t)t.nrb * t.nkb, t.RB, t.seg, mx + (o * 2 + v));
+            til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, t.RB / kTilNW[v], t.seg, mx + 4 + (o * 2 + v));
             cudaFreeAsync(cnt, st);
         }
     }
-    int64_t h[4], hi[8];
+    int64_t h[8], hi[8];
     cudaMemcpyAsync(h, mx, sizeof(h), cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(hi, info, sizeof(hi), cudaMemcpyDeviceToHost, st);
     const cudaError_t e = cudaStreamSynchronize(st);  // second (last) host sync of sp_weight_create
     for (int o = 0; o < 2; ++o)
         for (int v = 0; v < 2; ++v) {
             w->til[o][v].max_tile = (int32_t)h[o * 2 + v];
+            w->til[o][v].max_warp = h[4 + o * 2 + v];
             w->til[o][v].npad = hi[2 * (o * 2 + v)];  // padded entry total
         }
     cudaFreeAsync(info, st);

@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "sp_internal.cuh"
 #include "tile.cuh"
@@ -199,7 +200,264 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
 }
 
+// ---- TMEM variant ----------------------------------------------------------
+// Same pass, two changes that cut the per-entry instruction count:
+//  * no static slot layout: every row walks its (padded) segment in groups of
+//    4 entries, and each group's 4 dW partials are reduced across the warp on
+//    the spot (transpose stages xor 16 / xor 8, then xor 4/2/1: 6 SHFL, 6 SEL,
+//    6 FADD for 4 entries), so short segments waste nothing in the reduction;
+//  * the per-entry dW sums of successive batch slices accumulate in tensor
+//    memory instead of a global read-modify-write: group g of the warp's
+//    per-slice sequence lands in TMEM column g/8, lane 8*u + g%8 (u = entry in
+//    the group), so every column holds 32 entries and one 32x32b access per 8
+//    groups updates them.  The sequence is identical in every slice, and at
+//    the end the warp replays it to write each total to dW (or its split's
+//    partial row).  Warp w owns TMEM lanes 32*(w%4).. and columns
+//    (w/4)*128..+128, i.e. at most 4096 padded entries per warp.
+__device__ __forceinline__ void tm_st1(uint32_t taddr, float v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(__float_as_uint(v))
+                 : "memory");
+}
+__device__ __forceinline__ float tm_ld1(uint32_t taddr) {
+    uint32_t r;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r)
+        : "r"(taddr)
+        : "memory");
+    return __uint_as_float(r);
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// 4 per-lane partials p[u] (entries u of a group) -> lane l holds the warp
+// sum for entry (l >> 3) & 3.  Fixed order: bitwise reproducible.
+__device__ __forceinline__ float reduce4(const float (&p)[4], int lane) {
+    const bool h16 = (lane & 16) != 0, h8 = (lane & 8) != 0;
+    const float sa = h16 ? p[0] : p[2], sb = h16 ? p[1] : p[3];
+    const float ka = h16 ? p[2] : p[0], kb = h16 ? p[3] : p[1];
+    const float ra = ka + __shfl_xor_sync(kFull, sa, 16);
+    const float rb = kb + __shfl_xor_sync(kFull, sb, 16);
+    const float s8 = h8 ? ra : rb, k8 = h8 ? rb : ra;
+    float v = k8 + __shfl_xor_sync(kFull, s8, 8);
+    v += __shfl_xor_sync(kFull, v, 4);
+    v += __shfl_xor_sync(kFull, v, 2);
+    v += __shfl_xor_sync(kFull, v, 1);
+    return v;
+}
+
+// TMEM columns per warp: the NW/4 warps of a lane quarter share its 512 columns
+template <int NW>
+constexpr int tm_cols() { return 512 / (NW / 4); }
+
+template <int RPW, int NW, bool GATE>
+__global__ void __launch_bounds__(NW * 32, 1)
+    bwd_fused_tm_kernel(const FusedArgs a, const __grid_constant__ CUtensorMap tmap) {
+    constexpr int VEC = 4;
+    constexpr int BT = 32 * VEC;
+    constexpr int RB = NW * RPW;
+    static_assert(NW % 4 == 0, "whole TMEM lane quarters");
+    constexpr int kTmCols = tm_cols<NW>();
+    extern __shared__ __align__(128) float smem[];
+    __shared__ uint64_t full[2], empty[2];
+    __shared__ uint32_t tmem_base;
+    int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * (a.KC + 1) * BT);
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int rb = blockIdx.x;
+    const int64_t B = a.B;
+    const int64_t s_lo = (int64_t)blockIdx.y * a.spl * BT;
+    const int nsl = (int)std::min<int64_t>(a.spl, (B - s_lo + BT - 1) / BT);
+    const int ntile = nsl * a.nkb;
+    const size_t tile_sz = (size_t)a.KC * BT;
+    const size_t buf_sz = tile_sz + BT;
+    const int ebuf = a.cap + 2;
+    const int32_t *segw = a.seg + (int64_t)rb * a.nkb * RB + warp * RPW;
+    const int64_t r_base = (int64_t)rb * RB + warp * RPW;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (threadIdx.x == 32) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        mbar_init(&empty[0], NW);  // one arrival per warp when it is done with the buffer
+        mbar_init(&empty[1], NW);
+        fence_mbar_init();
+    }
+    for (int i = threadIdx.x; i < BT; i += NW * 32) {
+        smem[i] = 0.f;
+        smem[buf_sz + i] = 0.f;
+    }
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+    const uint32_t tcol = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * kTmCols);
+
+    auto entry_range = [&](int kb, int &e0, int &e1) {
+        const int64_t tb = ((int64_t)rb * a.nkb + kb) * RB;
+        e0 = __ldg(a.seg + tb) & ~1;
+        e1 = __ldg(a.seg + tb + RB);
+    };
+    auto issue = [&](int q, int buf) {
+        const int s = q / a.nkb, kb = q - s * a.nkb;
+        int e0, e1;
+        entry_range(kb, e0, e1);
+        const unsigned eb = (unsigned)(((e1 - e0) * 8 + 15) & ~15);
+        mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
+        tma_load_2d(smem + buf * buf_sz + BT, &tmap, (int)(s_lo + (int64_t)s * BT), kb * a.KC, &full[buf]);
+        if (eb) tma_load_1d(ents + buf * ebuf, a.ent + e0, eb, &full[buf]);
+    };
+    if (threadIdx.x == 0 && ntile > 0) issue(0, 0);
+
+    float rv[RPW][VEC], dx[RPW][VEC];
+    float keep = 0.f;
+    int cnt = 0;
+    // lane l <= RPW: l-th segment bound of this warp's rows in tile q (prefetched one tile ahead)
+    auto seg_bounds = [&](int q) -> int {
+        const int kb = q % a.nkb;
+        return lane <= RPW ? __ldg(segw + (int64_t)kb * RB + lane) : 0;
+    };
+    int sgn = ntile > 0 ? seg_bounds(0) : 0;
+    for (int q = 0; q < ntile; ++q) {
+        const int s = q / a.nkb, kb = q - s * a.nkb;
+        const int buf = q & 1;
+        const int64_t bl = s_lo + (int64_t)s * BT + lane * VEC;
+        if (kb == 0) {  // new slice: X rows into registers, dX accumulators reset
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                const int64_t r = __ldg(a.rowmap + r_base + i);
+                const float4 t = (r >= 0 && r < a.nrow && bl + 4 <= B)
+                                     ? __ldg(reinterpret_cast<const float4 *>(a.X + r * B + bl))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+                rv[i][0] = t.x;
+                rv[i][1] = t.y;
+                rv[i][2] = t.z;
+                rv[i][3] = t.w;
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) dx[i][v] = 0.f;
+            }
+            cnt = 0;
+        }
+        const int sg = sgn;
+        if (q + 1 < ntile) sgn = seg_bounds(q + 1);
+        if (q + 1 < ntile && threadIdx.x == 0) {
+            // buffer buf^1 last held tile q-1: every warp must be done with it
+            if (q >= 1) mbar_wait(&empty[buf ^ 1], ((q - 1) >> 1) & 1);
+            issue(q + 1, buf ^ 1);
+        }
+        mbar_wait(&full[buf], (q >> 1) & 1);
+        int ea, e1t;
+        entry_range(kb, ea, e1t);
+        const char *tb = reinterpret_cast<const char *>(smem + buf * buf_sz + BT + lane * VEC);
+        const int2 *es = ents + buf * ebuf - ea;
+        auto flush = [&](int col) {
+            const uint32_t ta = tcol + (uint32_t)col;
+            if (s == 0) {
+                tm_st1(ta, keep);
+            } else {
+                const float old = tm_ld1(ta);
+                tm_st1(ta, old + keep);
+            }
+            keep = 0.f;
+        };
+#pragma unroll
+        for (int m = 0; m < RPW; ++m) {
+            const int g0 = __shfl_sync(kFull, sg, m), g1 = __shfl_sync(kFull, sg, m + 1);
+            for (int e = g0; e < g1; e += 4) {
+                const int4 p01 = ld_entry_pair(es + e, true);
+                const int4 p23 = ld_entry_pair(es + e + 2, true);
+                const int off[4] = {p01.x, p01.z, p23.x, p23.z};
+                const float w[4] = {__int_as_float(p01.y), __int_as_float(p01.w), __int_as_float(p23.y),
+                                    __int_as_float(p23.w)};
+                float p[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    // padding entries read the zero row in front of the tile
+                    float x[VEC];
+                    lds_vec<VEC>(reinterpret_cast<const float *>(tb + off[u]), x);
+                    fma_bcast<VEC>(dx[m], w[u], x);   // dX  (Eq. 1)
+                    p[u] = dot_vec<VEC>(rv[m], x);    // dW partial (Eq. 2)
+                }
+                const float v = reduce4(p, lane);
+                if ((lane & 7) == (cnt & 7)) keep = v;
+                ++cnt;
+                if ((cnt & 7) == 0) flush((cnt >> 3) - 1);
+            }
+        }
+        if (kb == a.nkb - 1) {  // slice done: last partial column, dX rows (ReLU' gate fused)
+            if (cnt & 7) flush(cnt >> 3);
+            tm_wait_st();
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                const int64_t r = __ldg(a.rowmap + r_base + i);
+                if (r < 0 || r >= a.nrow || bl >= B) continue;
+                float o[VEC];
+                if (GATE) {
+                    const float4 hv = __ldg(reinterpret_cast<const float4 *>(a.H + r * B + bl));
+                    o[0] = hv.x > 0.f ? dx[i][0] : 0.f;
+                    o[1] = hv.y > 0.f ? dx[i][1] : 0.f;
+                    o[2] = hv.z > 0.f ? dx[i][2] : 0.f;
+                    o[3] = hv.w > 0.f ? dx[i][3] : 0.f;
+                } else {
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) o[v] = dx[i][v];
+                }
+                *reinterpret_cast<float4 *>(a.dX + r * B + bl) = make_float4(o[0], o[1], o[2], o[3]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[buf]);  // this warp is done with the buffer
+    }
+
+    // replay one slice's group sequence: TMEM (column, lane) -> entry, write totals
+    if (nsl > 0) {
+        float *P = a.part + (a.direct ? 0 : (int64_t)blockIdx.y * a.npad);
+        int c2 = 0, my_e = -1;
+        auto out = [&](int col) {
+            const float val = tm_ld1(tcol + (uint32_t)col);
+            if (my_e >= 0) {
+                if (a.direct) {
+                    const int v = __ldg(a.vidx + my_e);
+                    if (v >= 0) P[v] = val;
+                } else {
+                    P[my_e] = val;
+                }
+            }
+            my_e = -1;
+        };
+        for (int kb = 0; kb < a.nkb; ++kb) {
+            const int sg = lane <= RPW ? __ldg(segw + (int64_t)kb * RB + lane) : 0;
+            for (int m = 0; m < RPW; ++m) {
+                const int g0 = __shfl_sync(kFull, sg, m), g1 = __shfl_sync(kFull, sg, m + 1);
+                for (int e = g0; e < g1; e += 4) {
+                    if ((lane & 7) == (c2 & 7)) my_e = e + ((lane >> 3) & 3);
+                    ++c2;
+                    if ((c2 & 7) == 0) out((c2 >> 3) - 1);
+                }
+            }
+        }
+        if (c2 & 7) out(c2 >> 3);
+    }
+    tm_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+}
+
 constexpr int kNumSMs = 148;
+
+// SP_FUSED_TMEM=0 selects the register-slot variant (A/B measurements).
+bool tm_disabled() {
+    static const int v = [] {
+        const char *e = getenv("SP_FUSED_TMEM");
+        return (e && e[0] == '0') ? 1 : 0;
+    }();
+    return v != 0;
+}
 
 }  // namespace
 
@@ -208,19 +466,33 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     // fused path: B % 4 == 0, at least one full slice, the big CSC tiling
     if ((B & 3) != 0 || B < 128 || w->nnz == 0) return SP_ERR_SHAPE;
     constexpr int RPW = 8, NW = 16, BT = 128;
+    constexpr int TRPW = 4, TNW = 32;  // TMEM variant: 32 warps x 4 rows (same 128-row blocks)
     const sp_tiling &t = w->til[1][0];
     const int64_t slices = (B + BT - 1) / BT;
     if ((int64_t)t.nrb * slices < kNumSMs) return SP_ERR_SHAPE;  // too little parallelism: use the separate kernels
     CUtensorMap tmap{};
     if (!make_tmap_2d(&tmap, dY, t.inner, B, BT, t.KC)) return SP_ERR_SHAPE;
-    const int64_t want = 2LL * kNumSMs * 4;
-    int64_t nsplit = std::max<int64_t>(1, std::min<int64_t>(slices, (want + t.nrb - 1) / t.nrb));
-    const int64_t spl = (slices + nsplit - 1) / nsplit;
-    nsplit = (slices + spl - 1) / spl;
     const size_t tiles = (size_t)2 * (t.KC + 1) * BT * sizeof(float);
     const int cap = (t.max_tile + 2 + 3) & ~3;
     const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)(226 * 1024);
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
+    // TMEM variant: staged entries and at most kTmCols*32 padded entries per warp
+    const bool tm = sent && !tm_disabled() && t.max_warp <= (int64_t)tm_cols<TNW>() * 32;  // bound of an 8-row warp covers its 4-row halves
+    int64_t nsplit, spl;
+    if (tm) {
+        // one wave: the largest per-CTA slice count that keeps nrb * nsplit <= #SMs
+        spl = std::max<int64_t>(1, (slices * t.nrb + kNumSMs - 1) / kNumSMs);
+        nsplit = (slices + spl - 1) / spl;
+        while (nsplit * t.nrb > kNumSMs) {
+            ++spl;
+            nsplit = (slices + spl - 1) / spl;
+        }
+    } else {
+        const int64_t want = 2LL * kNumSMs * 4;
+        nsplit = std::max<int64_t>(1, std::min<int64_t>(slices, (want + t.nrb - 1) / t.nrb));
+        spl = (slices + nsplit - 1) / nsplit;
+        nsplit = (slices + spl - 1) / spl;
+    }
     const bool direct = nsplit == 1;
     float *part = dW;
     if (!direct) {
@@ -234,10 +506,13 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
                 direct ? 1 : 0, t.rowmap};
     auto pick = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<dim3((unsigned)t.nrb, (unsigned)nsplit), NW * 32, smem, st>>>(a, tmap);
+        kern<<<dim3((unsigned)t.nrb, (unsigned)nsplit), (tm ? TNW : NW) * 32, smem, st>>>(a, tmap);
     };
     count_launches(direct ? 1 : 2);
-    if (H) {
+    if (tm) {
+        if (H) pick(bwd_fused_tm_kernel<TRPW, TNW, true>);
+        else pick(bwd_fused_tm_kernel<TRPW, TNW, false>);
+    } else if (H) {
         if (sent) pick(bwd_fused_kernel<RPW, NW, true, true>);
         else pick(bwd_fused_kernel<RPW, NW, true, false>);
     } else {

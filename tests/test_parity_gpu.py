@@ -259,6 +259,8 @@ def test_conv_shapes(sp, B, IC, OC, H, W, K, pad, d):
     (1000, 900, 384, 0.2, False),     # fused, ragged row blocks
     (300, 200, 902, 0.1, True),       # B % 4 != 0 -> separate kernels
     (200, 100, 96, 0.3, False),       # B < 128 -> separate kernels
+    (64, 18944, 128, 0.05, True),     # one slice, >= 148 row blocks: dW written directly
+    (2048, 256, 256, 0.5, False),     # > 4096 entries per warp: register-slot variant
 ])
 def test_fused_backward(sp, R, C, B, d, gate):
     c = synth.linear_case(R, C, B, d, 1.0 / C, R + C + B)

@@ -30,7 +30,8 @@ fl = 2 * W.nnz * args.B
 res = {}
 for it in range(args.iters):
     for name, f in (("fwd", lambda: sp.sp_linear_fwd(W, X, Y)), ("dx", lambda: sp.sp_linear_bwd_input(W, dY, dX)),
-                    ("dw", lambda: sp.sp_linear_bwd_weight(W, X, dY, dW))):
+                    ("dw", lambda: sp.sp_linear_bwd_weight(W, X, dY, dW)),
+                    ("bwd_fused", lambda: sp.sp_linear_bwd(W, X, dY, dX, dW))):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         f()
@@ -39,4 +40,5 @@ for it in range(args.iters):
         res.setdefault(name, []).append(s.elapsed_time(e))
 for k, v in res.items():
     t = min(v)
-    print(f"{k}: {t*1e3:.1f} us  {fl / (t*1e-3) / 1e12:.2f} TFLOP/s  ({fl/(t*1e-3)/1e12/74.45*100:.1f}% of FP32 peak)")
+    f = fl * (2 if k == "bwd_fused" else 1)
+    print(f"{k}: {t*1e3:.1f} us  {f / (t*1e-3) / 1e12:.2f} TFLOP/s  ({f/(t*1e-3)/1e12/74.45*100:.1f}% of FP32 peak)")
