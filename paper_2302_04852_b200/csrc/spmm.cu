@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
     constexpr int NT = NW * 32;
     constexpr int RB = NW * RPW;
     extern __shared__ __align__(128) float smem[];  // [2][KC][BT] floats, [2][cap+2] int2
-    __shared__ uint64_t full[2];
+    __shared__ uint64_t full[2], empty[2];
     int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * a.KC * BT);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -87,6 +87,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
     if (threadIdx.x == 0) {
         mbar_init(&full[0], 1);
         mbar_init(&full[1], 1);
+        mbar_init(&empty[0], NW);  // TMA path: one arrival per warp when it is done with a buffer
+        mbar_init(&empty[1], NW);
         fence_mbar_init();
     }
     __syncthreads();
@@ -136,7 +138,11 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
         const int kb = kb_of(q);
         int sgn = 0;
         if (q + 1 < ntile) {
-            if (vec4 && threadIdx.x == 0) issue(q + 1, buf ^ 1);
+            if (vec4 && threadIdx.x == 0) {
+                // buffer buf^1 last held tile q-1: wait until every warp is done with it
+                if (q >= 1) mbar_wait(&empty[buf ^ 1], ((q - 1) >> 1) & 1);
+                issue(q + 1, buf ^ 1);
+            }
             sgn = seg_bounds(q + 1);
             if constexpr (!SENT)
                 prefetch_entries(ent_of(tap_of(q + 1)), __shfl_sync(kFull, sgn, 0), __shfl_sync(kFull, sgn, RPW),
@@ -183,7 +189,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
                 for (int u = 0; u < 4; ++u) fma_bcast<VEC>(acc[i], w[u], x[u]);
             }
         }
-        __syncthreads();  // everyone done with this buffer before it is refilled
+        if (vec4) {  // release the buffer: warps drift up to one tile apart
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[buf]);
+        } else {
+            __syncthreads();  // everyone done with this buffer before it is restaged
+        }
         sg = sgn;
     }
 
