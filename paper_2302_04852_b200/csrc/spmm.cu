@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "sp_internal.cuh"
 #include "tile.cuh"
@@ -248,6 +249,14 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
 }
 
 constexpr int kNumSMs = 148;
+// variant 0 runs as 32 warps x 4 rows (SP_SPMM_NW32=0: 16 warps x 8 rows, for A/B measurements)
+bool spmm_nw32() {
+    static const int v = [] {
+        const char *e = getenv("SP_SPMM_NW32");
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    return v != 0;
+}
 constexpr int kSmemLimit = 226 * 1024;  // per SM, usable by CTAs (minus static mbarriers)
 
 template <int VEC, int RPW, int NW>
@@ -285,7 +294,7 @@ void launch_cfg(const sp_tiling &t, int64_t B, const float *in, float *out, cons
 template <int VEC>
 void launch_variant(const sp_tiling &t, int v, int64_t B, const float *in, float *out, const float *gate,
                     int epi, cudaStream_t st) {
-    if (v == 0) launch_cfg<VEC, 8, 16>(t, B, in, out, gate, epi, st);
+    if (v == 0) { if (spmm_nw32()) launch_cfg<VEC, 4, 32>(t, B, in, out, gate, epi, st); else launch_cfg<VEC, 8, 16>(t, B, in, out, gate, epi, st); }
     else launch_cfg<VEC, 4, 8>(t, B, in, out, gate, epi, st);
 }
 
