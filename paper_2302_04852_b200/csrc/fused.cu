@@ -261,7 +261,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
     static_assert(NW % 4 == 0, "whole TMEM lane quarters");
     constexpr int kTmCols = tm_cols<NW>();
     extern __shared__ __align__(128) float smem[];
-    __shared__ uint64_t full[2], empty[2];
+    __shared__ uint64_t full[2];
+    __shared__ int released[2];  // warps done with each buffer (the last one refills it)
     __shared__ uint32_t tmem_base;
     int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * (a.KC + 1) * BT);
 
@@ -285,8 +286,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
     if (threadIdx.x == 32) {
         mbar_init(&full[0], 1);
         mbar_init(&full[1], 1);
-        mbar_init(&empty[0], NW);  // one arrival per warp when it is done with the buffer
-        mbar_init(&empty[1], NW);
+        released[0] = 0;
+        released[1] = 0;
         fence_mbar_init();
     }
     for (int i = threadIdx.x; i < BT; i += NW * 32) {
@@ -312,7 +313,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
         tma_load_2d(smem + buf * buf_sz + BT, &tmap, (int)(s_lo + (int64_t)s * BT), kb * a.KC, &full[buf]);
         if (eb) tma_load_1d(ents + buf * ebuf, a.ent + e0, eb, &full[buf]);
     };
-    if (threadIdx.x == 0 && ntile > 0) issue(0, 0);
+    if (threadIdx.x == 0) {
+        if (ntile > 0) issue(0, 0);
+        if (ntile > 1) issue(1, 1);
+    }
 
     float rv[RPW][VEC], dx[RPW][VEC];
     float keep = 0.f;
@@ -345,11 +349,6 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
         const int sg = sgn;
         if (q + 1 < ntile) sgn = seg_bounds(q + 1);
-        if (q + 1 < ntile && threadIdx.x == 0) {
-            // buffer buf^1 last held tile q-1: every warp must be done with it
-            if (q >= 1) mbar_wait(&empty[buf ^ 1], ((q - 1) >> 1) & 1);
-            issue(q + 1, buf ^ 1);
-        }
         mbar_wait(&full[buf], (q >> 1) & 1);
         int ea, e1t;
         entry_range(kb, ea, e1t);
@@ -410,8 +409,16 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 *reinterpret_cast<float4 *>(a.dX + r * B + bl) = make_float4(o[0], o[1], o[2], o[3]);
             }
         }
+        // release the buffer; the last warp to finish tile q refills it with tile q+2
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[buf]);  // this warp is done with the buffer
+        if (lane == 0) {
+            __threadfence_block();
+            if (atomicAdd(&released[buf], 1) == NW - 1) {
+                released[buf] = 0;
+                __threadfence_block();
+                if (q + 2 < ntile) issue(q + 2, buf);
+            }
+        }
     }
 
     // replay one slice's group sequence: TMEM (column, lane) -> entry, write totals

@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
     constexpr int NT = NW * 32;
     constexpr int RB = NW * RPW;
     extern __shared__ __align__(128) float smem[];  // [2][KC][BT] floats, [2][cap+2] int2
-    __shared__ uint64_t full[2], empty[2];
+    __shared__ uint64_t full[2];
+    __shared__ int released[2];  // TMA path: warps done with each buffer (the last one refills it)
     int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * a.KC * BT);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -88,8 +89,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
     if (threadIdx.x == 0) {
         mbar_init(&full[0], 1);
         mbar_init(&full[1], 1);
-        mbar_init(&empty[0], NW);  // TMA path: one arrival per warp when it is done with a buffer
-        mbar_init(&empty[1], NW);
+        released[0] = 0;
+        released[1] = 0;
         fence_mbar_init();
     }
     __syncthreads();
@@ -117,7 +118,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
         tma_load_2d(smem + buf * tile_sz, &tmap, (int)(b0 + (CONV ? a.sh[t] : 0)), (int)k0, &full[buf]);
         if (eb) tma_load_1d(ents + buf * ebuf, ent_of(t) + e0, eb, &full[buf]);
     };
-    if (vec4 && threadIdx.x == 0) issue(0, 0);
+    if (vec4 && threadIdx.x == 0) {
+        issue(0, 0);
+        if (ntile > 1) issue(1, 1);
+    }
 
     // lane l <= RPW holds the l-th segment bound of this warp's rows in tile q
     // (rows rb*RB + warp*RPW + i).
@@ -139,11 +143,6 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
         const int kb = kb_of(q);
         int sgn = 0;
         if (q + 1 < ntile) {
-            if (vec4 && threadIdx.x == 0) {
-                // buffer buf^1 last held tile q-1: wait until every warp is done with it
-                if (q >= 1) mbar_wait(&empty[buf ^ 1], ((q - 1) >> 1) & 1);
-                issue(q + 1, buf ^ 1);
-            }
             sgn = seg_bounds(q + 1);
             if constexpr (!SENT)
                 prefetch_entries(ent_of(tap_of(q + 1)), __shfl_sync(kFull, sgn, 0), __shfl_sync(kFull, sgn, RPW),
@@ -190,9 +189,16 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
                 for (int u = 0; u < 4; ++u) fma_bcast<VEC>(acc[i], w[u], x[u]);
             }
         }
-        if (vec4) {  // release the buffer: warps drift up to one tile apart
+        if (vec4) {  // release the buffer; the last warp done with tile q refills it with tile q+2
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[buf]);
+            if (lane == 0) {
+                __threadfence_block();
+                if (atomicAdd(&released[buf], 1) == NW - 1) {
+                    released[buf] = 0;
+                    __threadfence_block();
+                    if (q + 2 < ntile) issue(q + 2, buf);
+                }
+            }
         } else {
             __syncthreads();  // everyone done with this buffer before it is restaged
         }
