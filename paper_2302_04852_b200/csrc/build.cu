@@ -421,7 +421,7 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
                                                                          slotmap, t.rowpos, t.seg, w->vals, t.ent,
                                                                          t.vidx);
             til_max_kernel<<<1, 256, 0, st>>>((int64_t)t.nrb * t.nkb, t.RB, t.seg, mx + (o * 2 + v));
-            til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, t.RB / kTilNW[v], t.seg, mx + 4 + (o * 2 + v));
+            til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, v == 0 ? 4 : t.RB / kTilNW[v], t.seg, mx + 4 + (o * 2 + v));
             cudaFreeAsync(cnt, st);
         }
     }

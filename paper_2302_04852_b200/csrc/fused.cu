@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "sp_internal.cuh"
 #include "tile.cuh"
@@ -43,6 +44,8 @@ struct FusedArgs {
     int64_t npad;
     int direct;
     const int32_t *rowmap;  // tiled position -> row of X / dX (-1 unused)
+    int64_t nslice;         // stream-K kernel: batch slices of BT columns
+    int nrow_blocks;        // stream-K kernel: row blocks of the tiling
 };
 
 template <int RPW, int NW, bool GATE, bool SENT>
@@ -455,12 +458,355 @@ __global__ void __launch_bounds__(NW * 32, 1)
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
 }
 
+// ---- stream-K schedule ------------------------------------------------------
+// The work is the tile sequence (row block rb, batch slice sl, column block kb),
+// rb-major, T = nrb * nslice * nkb tiles; CTA c of G runs the contiguous range
+// [c*T/G, (c+1)*T/G), so every SM gets the same number of tiles (+-1) instead
+// of a whole number of slices.  An item (rb, sl) cut by a range boundary is
+// shared by exactly two CTAs (ranges are longer than nkb): both add their
+// gated dX partial into the pre-zeroed item with fp32 atomics -- two addends on
+// zero give a + b in either order, so the result stays deterministic.  A job is
+// one CTA's run of tiles of one row block: its dW sums (TMEM, as above) go to
+// row (c - first CTA of rb) of the partial buffer, summed per entry in fixed
+// order by job_reduce_kernel.
+__host__ __device__ __forceinline__ int64_t sk_lo(int64_t c, int64_t T, int64_t G) { return c * T / G; }
+__host__ __device__ __forceinline__ int64_t sk_cta(int64_t t, int64_t T, int64_t G) {
+    int64_t c = t * G / T;
+    while (c + 1 < G && sk_lo(c + 1, T, G) <= t) ++c;
+    while (c > 0 && sk_lo(c, T, G) > t) --c;
+    return c;
+}
+
+__device__ __forceinline__ void tm_st4(uint32_t taddr, const float (&v)[4]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(__float_as_uint(v[0])),
+                 "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3]))
+                 : "memory");
+}
+__device__ __forceinline__ void tm_ld4(uint32_t taddr, float (&v)[4]) {
+    uint32_t r0, r1, r2, r3;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+        : "r"(taddr)
+        : "memory");
+    v[0] = __uint_as_float(r0);
+    v[1] = __uint_as_float(r1);
+    v[2] = __uint_as_float(r2);
+    v[3] = __uint_as_float(r3);
+}
+__device__ __forceinline__ void tm_ld4x2(uint32_t ta, float (&v)[4], uint32_t tb, float (&w)[4]) {
+    uint32_t r0, r1, r2, r3, q0, q1, q2, q3;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%8];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4, %5, %6, %7}, [%9];\n"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3), "=r"(q0), "=r"(q1), "=r"(q2), "=r"(q3)
+        : "r"(ta), "r"(tb)
+        : "memory");
+    v[0] = __uint_as_float(r0);
+    v[1] = __uint_as_float(r1);
+    v[2] = __uint_as_float(r2);
+    v[3] = __uint_as_float(r3);
+    w[0] = __uint_as_float(q0);
+    w[1] = __uint_as_float(q1);
+    w[2] = __uint_as_float(q2);
+    w[3] = __uint_as_float(q3);
+}
+
+// TMEM columns of one warp (32 warps: 8 per lane quarter, 64 columns each):
+// [0,16) the X rows of its RPW=4 rows (the dW register operand), [16,32) their
+// dX accumulators, [32,64) dW sums (32 per column: <= 1024 padded entries).
+// Keeping the per-row state in TMEM (loaded per row segment) frees the
+// registers that 32 resident warps need.
+constexpr int kSkRv = 0, kSkDx = 16, kSkDw = 32, kSkDwCols = 32;
+
+template <int RPW, int NW, bool GATE>
+__global__ void __launch_bounds__(NW * 32, 1)
+    bwd_fused_sk_kernel(const FusedArgs a, const __grid_constant__ CUtensorMap tmap) {
+    constexpr int VEC = 4;
+    constexpr int BT = 32 * VEC;
+    constexpr int RB = NW * RPW;
+    static_assert(NW == 32 && RPW == 4, "TMEM column plan: 8 warps per lane quarter, 4 rows each");
+    extern __shared__ __align__(128) float smem[];
+    __shared__ uint64_t full[2];
+    __shared__ int released[2];  // warps done with each buffer (the last one refills it)
+    __shared__ uint32_t tmem_base;
+    int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * (a.KC + 1) * BT);
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t B = a.B;
+    const int64_t T = (int64_t)a.nrow_blocks * a.nslice * a.nkb, G = gridDim.x;
+    const int t0 = (int)sk_lo(blockIdx.x, T, G);  // T < 2^31 (checked by the launcher)
+    const int ntile = (int)sk_lo(blockIdx.x + 1, T, G) - t0;
+    const int nsl = (int)a.nslice;
+    const size_t tile_sz = (size_t)a.KC * BT;
+    const size_t buf_sz = tile_sz + BT;
+    const int ebuf = a.cap + 2;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (threadIdx.x == 32) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        released[0] = 0;
+        released[1] = 0;
+        fence_mbar_init();
+    }
+    for (int i = threadIdx.x; i < BT; i += NW * 32) {
+        smem[i] = 0.f;
+        smem[buf_sz + i] = 0.f;
+    }
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+    const uint32_t tcol = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 64);
+
+    struct Tile {
+        int rb, kb, sl;
+    };
+    auto tile_of = [&](int q) -> Tile {  // 32-bit: used for the first tile and the refills
+        const int t = t0 + q, it = t / a.nkb;
+        Tile id;
+        id.kb = t - it * a.nkb;
+        id.rb = it / nsl;
+        id.sl = it - id.rb * nsl;
+        return id;
+    };
+    auto next_tile = [&](Tile id) -> Tile {
+        if (++id.kb == a.nkb) {
+            id.kb = 0;
+            if (++id.sl == nsl) {
+                id.sl = 0;
+                ++id.rb;
+            }
+        }
+        return id;
+    };
+    auto entry_range = [&](const Tile &id, int &e0, int &e1) {
+        const int64_t tb = ((int64_t)id.rb * a.nkb + id.kb) * RB;
+        e0 = __ldg(a.seg + tb) & ~1;
+        e1 = __ldg(a.seg + tb + RB);
+    };
+    auto issue = [&](int q, int buf) {
+        const Tile id = tile_of(q);
+        int e0, e1;
+        entry_range(id, e0, e1);
+        const unsigned eb = (unsigned)(((e1 - e0) * 8 + 15) & ~15);
+        mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
+        tma_load_2d(smem + buf * buf_sz + BT, &tmap, id.sl * BT, id.kb * a.KC, &full[buf]);
+        if (eb) tma_load_1d(ents + buf * ebuf, a.ent + e0, eb, &full[buf]);
+    };
+    if (threadIdx.x == 0) {
+        if (ntile > 0) issue(0, 0);
+        if (ntile > 1) issue(1, 1);
+    }
+    // this warp's segment bounds of (rb, kb): lane l <= RPW holds the l-th
+    auto segw_of = [&](int rb, int kb) -> const int32_t * {
+        return a.seg + ((int64_t)rb * a.nkb + kb) * RB + warp * RPW;
+    };
+    auto seg_bounds = [&](const Tile &id) -> int {
+        return lane <= RPW ? __ldg(segw_of(id.rb, id.kb) + lane) : 0;
+    };
+
+    // write this job's dW sums (row block rb)
+    auto dump = [&](int rb) {
+        const int64_t job = blockIdx.x - sk_cta((int64_t)rb * a.nslice * a.nkb, T, G);
+        float *P = a.part + job * a.npad;
+        int c2 = 0, my_e = -1;
+        auto out = [&](int col) {
+            const float val = tm_ld1(tcol + kSkDw + (uint32_t)col);
+            if (my_e >= 0) P[my_e] = val;
+            my_e = -1;
+        };
+        for (int kb = 0; kb < a.nkb; ++kb) {
+            const int sg = lane <= RPW ? __ldg(segw_of(rb, kb) + lane) : 0;
+            for (int m = 0; m < RPW; ++m) {
+                const int g0 = __shfl_sync(kFull, sg, m), g1 = __shfl_sync(kFull, sg, m + 1);
+                for (int e = g0; e < g1; e += 4) {
+                    if ((lane & 7) == (c2 & 7)) my_e = e + ((lane >> 3) & 3);
+                    ++c2;
+                    if ((c2 & 7) == 0) out((c2 >> 3) - 1);
+                }
+            }
+        }
+        if (c2 & 7) out(c2 >> 3);
+    };
+
+    float keep = 0.f;
+    int cnt = 0, cur_rb = -1;
+    bool whole = true;  // current item started at kb 0 in this CTA
+    Tile nid = tile_of(0);
+    int sgn = ntile > 0 ? seg_bounds(nid) : 0;
+    for (int q = 0; q < ntile; ++q) {
+        const Tile id = nid;
+        const int buf = q & 1;
+        const int64_t r_base = (int64_t)id.rb * RB + warp * RPW;
+        const int64_t bl = (int64_t)id.sl * BT + lane * VEC;
+        if (id.rb != cur_rb) {  // new job: clear the dW sums
+            if (cur_rb >= 0) dump(cur_rb);
+            for (int c = 0; c < kSkDwCols; ++c) tm_st1(tcol + kSkDw + (uint32_t)c, 0.f);
+            cur_rb = id.rb;
+        }
+        if (q == 0 || id.kb == 0) {  // new item: X rows to TMEM, dX accumulators cleared
+            const float z[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                const int64_t r = __ldg(a.rowmap + r_base + i);
+                const float4 t = (r >= 0 && r < a.nrow && bl + 4 <= B)
+                                     ? __ldg(reinterpret_cast<const float4 *>(a.X + r * B + bl))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float tv[4] = {t.x, t.y, t.z, t.w};
+                tm_st4(tcol + kSkRv + 4 * i, tv);
+                tm_st4(tcol + kSkDx + 4 * i, z);
+            }
+            whole = id.kb == 0;
+            // group index of this tile's first group in the slice sequence
+            cnt = 0;
+            for (int k = 0; k < id.kb; ++k) {
+                const int32_t *sw = segw_of(id.rb, k);
+                cnt += (__ldg(sw + RPW) - __ldg(sw)) >> 2;
+            }
+        }
+        tm_wait_st();  // TMEM stores of earlier tiles land before this tile reads them back
+        const int sg = sgn;
+        nid = next_tile(id);
+        if (q + 1 < ntile) sgn = seg_bounds(nid);
+        mbar_wait(&full[buf], (q >> 1) & 1);
+        int ea, e1t;
+        entry_range(id, ea, e1t);
+        const char *tb = reinterpret_cast<const char *>(smem + buf * buf_sz + BT + lane * VEC);
+        const int2 *es = ents + buf * ebuf - ea;
+        auto flush = [&](int col) {
+            const uint32_t ta = tcol + kSkDw + (uint32_t)col;
+            const float old = tm_ld1(ta);
+            tm_st1(ta, old + keep);
+            keep = 0.f;
+        };
+#pragma unroll 1
+        for (int m = 0; m < RPW; ++m) {
+            const int g0 = __shfl_sync(kFull, sg, m), g1 = __shfl_sync(kFull, sg, m + 1);
+            if (g0 == g1) continue;
+            float rv[VEC], dx[VEC];
+            tm_ld4x2(tcol + kSkRv + 4 * m, rv, tcol + kSkDx + 4 * m, dx);
+            for (int e = g0; e < g1; e += 4) {
+                const int4 p01 = ld_entry_pair(es + e, true);
+                const int4 p23 = ld_entry_pair(es + e + 2, true);
+                const int off[4] = {p01.x, p01.z, p23.x, p23.z};
+                const float w[4] = {__int_as_float(p01.y), __int_as_float(p01.w), __int_as_float(p23.y),
+                                    __int_as_float(p23.w)};
+                float p[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    // padding entries read the zero row in front of the tile
+                    float x[VEC];
+                    lds_vec<VEC>(reinterpret_cast<const float *>(tb + off[u]), x);
+                    fma_bcast<VEC>(dx, w[u], x);   // dX  (Eq. 1)
+                    p[u] = dot_vec<VEC>(rv, x);    // dW partial (Eq. 2)
+                }
+                const float v = reduce4(p, lane);
+                if ((lane & 7) == (cnt & 7)) keep = v;
+                ++cnt;
+                if ((cnt & 7) == 0) flush((cnt >> 3) - 1);
+            }
+            tm_st4(tcol + kSkDx + 4 * m, dx);
+        }
+        if (id.kb == a.nkb - 1 || q == ntile - 1) {  // item done here: partial column, dX rows
+            if (cnt & 7) flush(cnt >> 3);
+            tm_wait_st();
+            const bool split = !whole || id.kb != a.nkb - 1;  // the other part is another CTA's
+#pragma unroll 1
+            for (int i = 0; i < RPW; ++i) {
+                const int64_t r = __ldg(a.rowmap + r_base + i);
+                float o[VEC];
+                tm_ld4(tcol + kSkDx + 4 * i, o);
+                if (r < 0 || r >= a.nrow || bl >= B) continue;
+                if (GATE) {  // ReLU' gate, exact per addend (x * {0,1})
+                    const float4 hv = __ldg(reinterpret_cast<const float4 *>(a.H + r * B + bl));
+                    o[0] = hv.x > 0.f ? o[0] : 0.f;
+                    o[1] = hv.y > 0.f ? o[1] : 0.f;
+                    o[2] = hv.z > 0.f ? o[2] : 0.f;
+                    o[3] = hv.w > 0.f ? o[3] : 0.f;
+                }
+                float *dst = a.dX + r * B + bl;
+                if (split) {
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) atomicAdd(dst + v, o[v]);
+                } else {
+                    *reinterpret_cast<float4 *>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+                }
+            }
+        }
+        // release the buffer; the last warp to finish tile q refills it with tile q+2
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            if (atomicAdd(&released[buf], 1) == NW - 1) {
+                released[buf] = 0;
+                __threadfence_block();
+                if (q + 2 < ntile) issue(q + 2, buf);
+            }
+        }
+    }
+    tm_wait_st();
+    if (cur_rb >= 0) dump(cur_rb);
+    tm_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+}
+
+// zero the dX region (RB rows via rowmap x BT batch columns) of the split items
+__global__ void zero_items_kernel(const int64_t *__restrict__ items, int RB, int BT, int64_t nslice,
+                                  const int32_t *__restrict__ rowmap, int64_t nrow, int64_t B, float *__restrict__ dX) {
+    const int64_t it = items[blockIdx.x];
+    const int64_t rb = it / nslice, sl = it - rb * nslice;
+    for (int i = threadIdx.x; i < RB * (BT / 4); i += blockDim.x) {
+        const int lr = i / (BT / 4), c4 = (i - lr * (BT / 4)) * 4;
+        const int64_t r = rowmap[rb * RB + lr], b = sl * BT + c4;
+        if (r >= 0 && r < nrow && b < B) *reinterpret_cast<float4 *>(dX + r * B + b) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+// dW[vidx[e]] = sum over the jobs of e's row block of part[job][e] (fixed order)
+__global__ void job_reduce_kernel(int64_t npad, int nrb, int nkb, int RB, int64_t nslice, int64_t G,
+                                  const int32_t *__restrict__ seg, const float *__restrict__ part,
+                                  const int32_t *__restrict__ vidx, float *__restrict__ dW) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= npad) return;
+    const int v = vidx[e];
+    if (v < 0) return;
+    // row block of e: entries of rb are [seg[rb*nkb*RB], seg[(rb+1)*nkb*RB])
+    int lo = 0, hi = nrb;  // find the largest rb with seg[rb*nkb*RB] <= e
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (seg[(int64_t)mid * nkb * RB] <= e) lo = mid; else hi = mid;
+    }
+    const int64_t T = (int64_t)nrb * nslice * nkb;
+    const int64_t tl = (int64_t)lo * nslice * nkb;
+    const int64_t nj = sk_cta(tl + nslice * nkb - 1, T, G) - sk_cta(tl, T, G) + 1;
+    float s = 0.f;
+    for (int64_t j = 0; j < nj; ++j) s += part[j * npad + e];
+    dW[v] = s;
+}
+
 constexpr int kNumSMs = 148;
 
 // SP_FUSED_TMEM=0 selects the register-slot variant (A/B measurements).
 bool tm_disabled() {
     static const int v = [] {
         const char *e = getenv("SP_FUSED_TMEM");
+        return (e && e[0] == '0') ? 1 : 0;
+    }();
+    return v != 0;
+}
+
+// SP_FUSED_SK=0 keeps the slice-split grid for the TMEM variant (A/B measurements).
+bool sk_disabled() {
+    static const int v = [] {
+        const char *e = getenv("SP_FUSED_SK");
         return (e && e[0] == '0') ? 1 : 0;
     }();
     return v != 0;
@@ -485,6 +831,45 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
     // TMEM variant: staged entries and at most kTmCols*32 padded entries per warp
     const bool tm = sent && !tm_disabled() && t.max_warp <= (int64_t)tm_cols<TNW>() * 32;  // bound of an 8-row warp covers its 4-row halves
+    // stream-K schedule: one wave of equal tile ranges, each longer than a slice's column blocks
+    const int64_t T = (int64_t)t.nrb * slices * t.nkb;
+    const int64_t G = std::min<int64_t>(kNumSMs, T);
+    if (tm && !sk_disabled() && T / G > t.nkb && T < (1LL << 31) && t.max_warp <= (int64_t)kSkDwCols * 32) {
+        // items (rb, slice) cut by a range boundary: their dX is accumulated by two CTAs
+        std::vector<int64_t> items;
+        for (int64_t c = 1; c < G; ++c) {
+            const int64_t lo = sk_lo(c, T, G);
+            if (lo % t.nkb != 0) items.push_back(lo / t.nkb);
+        }
+        int64_t maxjobs = 1;
+        for (int64_t rb = 0; rb < t.nrb; ++rb) {
+            const int64_t tl = rb * slices * t.nkb;
+            maxjobs = std::max<int64_t>(maxjobs, sk_cta(tl + slices * t.nkb - 1, T, G) - sk_cta(tl, T, G) + 1);
+        }
+        float *part = nullptr;
+        int64_t *ditems = nullptr;
+        if (cudaMallocAsync((void **)&part, (size_t)(maxjobs * t.npad) * sizeof(float), st) != cudaSuccess ||
+            cudaMallocAsync((void **)&ditems, (items.size() + 1) * sizeof(int64_t), st) != cudaSuccess) {
+            set_error("sp_linear_bwd: scratch allocation failed");
+            return SP_ERR_ALLOC;
+        }
+        launch_refresh(t, w->vals, w->nnz, st);  // CSC-tiled weights from vals (through perm)
+        if (!items.empty()) {
+            cudaMemcpyAsync(ditems, items.data(), items.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+            zero_items_kernel<<<(unsigned)items.size(), 256, 0, st>>>(ditems, 128, BT, slices, t.rowmap, t.rows, B, dX);
+        }
+        FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, 0, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
+                    0, t.rowmap, slices, t.nrb};
+        auto kern = H ? bwd_fused_sk_kernel<TRPW, TNW, true> : bwd_fused_sk_kernel<TRPW, TNW, false>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<(unsigned)G, TNW * 32, smem, st>>>(a, tmap);
+        job_reduce_kernel<<<(unsigned)((t.npad + 255) / 256), 256, 0, st>>>(t.npad, t.nrb, t.nkb, 128, slices, G,
+                                                                          t.seg, part, t.vidx, dW);
+        count_launches(items.empty() ? 2 : 3);
+        cudaFreeAsync(part, st);
+        cudaFreeAsync(ditems, st);
+        return SP_OK;
+    }
     int64_t nsplit, spl;
     if (tm) {
         // one wave: the largest per-CTA slice count that keeps nrb * nsplit <= #SMs
@@ -510,7 +895,7 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     }
     launch_refresh(t, w->vals, w->nnz, st);  // CSC-tiled weights from vals (through perm)
     FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, (int)spl, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
-                direct ? 1 : 0, t.rowmap};
+                direct ? 1 : 0, t.rowmap, slices, t.nrb};
     auto pick = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<dim3((unsigned)t.nrb, (unsigned)nsplit), (tm ? TNW : NW) * 32, smem, st>>>(a, tmap);
