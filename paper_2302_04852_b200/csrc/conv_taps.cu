@@ -39,7 +39,7 @@ sp_status tiling_from_host(int64_t rows, int64_t inner, int RB, int KC, const st
         }
     }
     std::vector<int32_t> seg(nseg + 1, 0);
-    for (int64_t i = 0; i < nseg; ++i) seg[i + 1] = seg[i] + ((cnt[i] + kTilPad - 1) & ~(kTilPad - 1));
+    for (int64_t i = 0; i < nseg; ++i) seg[i + 1] = seg[i] + ((cnt[i] + kTapPad - 1) & ~(kTapPad - 1));
     const int64_t npad = seg[nseg];
     std::vector<int2> ent(npad + 8, make_int2(-kTilRowBytes, 0));
     std::vector<int32_t> vid(npad + 8, -1);

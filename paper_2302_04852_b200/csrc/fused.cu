@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
             int pb = a1;
             const int b1 = __shfl_sync(kFull, sg, m + 2);
             while (pa < a1 || pb < b1) {
-                const int na = min(16, a1 - pa), nb = min(16, b1 - pb);  // multiples of 4
+                const int na = min(16, a1 - pa), nb = min(16, b1 - pb);  // even
                 float acc[32];
 #pragma unroll
                 for (int u = 0; u < 32; ++u) acc[u] = 0.f;
@@ -150,9 +150,11 @@ __global__ void __launch_bounds__(NW * 32, 1)
                             const int e = (h ? pb : pa) + gq;
                             const int4 p01 = ld_entry_pair(SENT ? es + e : a.ent + e, SENT);
                             const int4 p23 = ld_entry_pair(SENT ? es + e + 2 : a.ent + e + 2, SENT);
-                            const int off[4] = {p01.x, p01.z, p23.x, p23.z};
-                            const float w[4] = {__int_as_float(p01.y), __int_as_float(p01.w), __int_as_float(p23.y),
-                                                __int_as_float(p23.w)};
+                            // a second pair past the segment reads the zero row with weight 0
+                            const bool h2 = gq + 2 < (h ? nb : na);
+                            const int off[4] = {p01.x, p01.z, h2 ? p23.x : -kTilRowBytes, h2 ? p23.z : -kTilRowBytes};
+                            const float w[4] = {__int_as_float(p01.y), __int_as_float(p01.w),
+                                                h2 ? __int_as_float(p23.y) : 0.f, h2 ? __int_as_float(p23.w) : 0.f};
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
                                 // padding entries read the zero row (x = 0 exactly, so
@@ -376,14 +378,21 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 const int off[4] = {p01.x, p01.z, p23.x, p23.z};
                 const float w[4] = {__int_as_float(p01.y), __int_as_float(p01.w), __int_as_float(p23.y),
                                     __int_as_float(p23.w)};
-                float p[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    // padding entries read the zero row in front of the tile
+                float p[4] = {0.f, 0.f, 0.f, 0.f};
+                // padding entries read the zero row in front of the tile; a second pair
+                // past the segment (length 2 mod 4) is skipped
+                auto entry = [&](int u) {
                     float x[VEC];
                     lds_vec<VEC>(reinterpret_cast<const float *>(tb + off[u]), x);
                     fma_bcast<VEC>(dx[m], w[u], x);   // dX  (Eq. 1)
                     p[u] = dot_vec<VEC>(rv[m], x);    // dW partial (Eq. 2)
+                };
+                if (e + 2 < g1) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) entry(u);
+                } else {
+                    entry(0);
+                    entry(1);
                 }
                 const float v = reduce4(p, lane);
                 if ((lane & 7) == (cnt & 7)) keep = v;
@@ -445,7 +454,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
             for (int m = 0; m < RPW; ++m) {
                 const int g0 = __shfl_sync(kFull, sg, m), g1 = __shfl_sync(kFull, sg, m + 1);
                 for (int e = g0; e < g1; e += 4) {
-                    if ((lane & 7) == (c2 & 7)) my_e = e + ((lane >> 3) & 3);
+                    const int u = (lane >> 3) & 3;
+                    if ((lane & 7) == (c2 & 7)) my_e = u < g1 - e ? e + u : -1;
                     ++c2;
                     if ((c2 & 7) == 0) out((c2 >> 3) - 1);
                 }
@@ -627,7 +637,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
             for (int m = 0; m < RPW; ++m) {
                 const int g0 = __shfl_sync(kFull, sg, m), g1 = __shfl_sync(kFull, sg, m + 1);
                 for (int e = g0; e < g1; e += 4) {
-                    if ((lane & 7) == (c2 & 7)) my_e = e + ((lane >> 3) & 3);
+                    const int u = (lane >> 3) & 3;
+                    if ((lane & 7) == (c2 & 7)) my_e = u < g1 - e ? e + u : -1;
                     ++c2;
                     if ((c2 & 7) == 0) out((c2 >> 3) - 1);
                 }
@@ -666,9 +677,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
             whole = id.kb == 0;
             // group index of this tile's first group in the slice sequence
             cnt = 0;
-            for (int k = 0; k < id.kb; ++k) {
+            for (int k = 0; k < id.kb; ++k) {  // groups of 4 per row segment (a last group may hold 2)
                 const int32_t *sw = segw_of(id.rb, k);
-                cnt += (__ldg(sw + RPW) - __ldg(sw)) >> 2;
+#pragma unroll
+                for (int i = 0; i < RPW; ++i) cnt += (__ldg(sw + i + 1) - __ldg(sw + i) + 3) >> 2;
             }
         }
         tm_wait_st();  // TMEM stores of earlier tiles land before this tile reads them back
@@ -698,14 +710,21 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 const int off[4] = {p01.x, p01.z, p23.x, p23.z};
                 const float w[4] = {__int_as_float(p01.y), __int_as_float(p01.w), __int_as_float(p23.y),
                                     __int_as_float(p23.w)};
-                float p[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    // padding entries read the zero row in front of the tile
+                float p[4] = {0.f, 0.f, 0.f, 0.f};
+                // padding entries read the zero row in front of the tile; a second pair
+                // past the segment (length 2 mod 4) is skipped
+                auto entry = [&](int u) {
                     float x[VEC];
                     lds_vec<VEC>(reinterpret_cast<const float *>(tb + off[u]), x);
                     fma_bcast<VEC>(dx, w[u], x);   // dX  (Eq. 1)
                     p[u] = dot_vec<VEC>(rv, x);    // dW partial (Eq. 2)
+                };
+                if (e + 2 < g1) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) entry(u);
+                } else {
+                    entry(0);
+                    entry(1);
                 }
                 const float v = reduce4(p, lane);
                 if ((lane & 7) == (cnt & 7)) keep = v;

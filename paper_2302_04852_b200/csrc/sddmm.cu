@@ -186,13 +186,14 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
             lds_vec<VEC>(reinterpret_cast<const float *>(tb + (max(off, 0) >> SH)), x);
             return dot_vec<VEC>(r, x);
         };
-        auto offs4 = [&](int e, int (&o)[4]) {
+        // offsets of entries e..e+3; a second pair past the segment (nv == 2) reads row 0
+        auto offs4 = [&](int e, int nv, int (&o)[4]) {
             const int4 p01 = ld_entry_pair(SENT ? es + e : a.ent + e, SENT);
             const int4 p23 = ld_entry_pair(SENT ? es + e + 2 : a.ent + e + 2, SENT);
             o[0] = p01.x;
             o[1] = p01.z;
-            o[2] = p23.x;
-            o[3] = p23.z;
+            o[2] = nv > 2 ? p23.x : -1;
+            o[3] = nv > 2 ? p23.z : -1;
         };
 #pragma unroll
         for (int m = 0; m < RPW; m += 2) {
@@ -201,7 +202,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
             int pb = a1;
             const int b1 = __shfl_sync(kFull, sg, m + 2);
             while (pa < a1 || pb < b1) {
-                // segments are padded to multiples of 4: whole groups only
+                // segments are padded to even lengths: a last group of 2 masks its
+                // second pair (those slots are never written)
                 const int na = min(16, a1 - pa), nb = min(16, b1 - pb);
                 float acc[32];
 #pragma unroll
@@ -210,13 +212,13 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
                 for (int g = 0; g < 16; g += 4) {
                     if (g < na) {
                         int o[4];
-                        offs4(pa + g, o);
+                        offs4(pa + g, na - g, o);
 #pragma unroll
                         for (int u = 0; u < 4; ++u) acc[g + u] = dot_e(rv[m], o[u]);
                     }
                     if (g < nb) {
                         int o[4];
-                        offs4(pb + g, o);
+                        offs4(pb + g, nb - g, o);
 #pragma unroll
                         for (int u = 0; u < 4; ++u) acc[16 + g + u] = dot_e(rv[m + 1], o[u]);
                     }

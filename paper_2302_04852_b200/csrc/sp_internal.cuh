@@ -77,13 +77,16 @@ constexpr int kTilRB[2] = {128, 32};
 constexpr int kTilKC[2] = {192, 96};
 constexpr int kTilNW[2] = {16, 8};  // warps per CTA of the kernels using each variant (RB = NW * RPW)
 // Segments are padded to a multiple of kTilPad entries (offset -kTilRowBytes,
-// weight 0, vidx -1) so the kernels run tail-free groups of 4; every segment
-// starts at a multiple of 4 entries (16-byte aligned pairs).  A padding
-// entry's offset addresses the all-zero row kernels keep just before a tile
-// (or is skipped by a predicated load).  Entry columns are stored
-// as byte offsets of a 128-float tile row (kTilRowBytes); kernels with
-// narrower tiles shift them down.
-constexpr int kTilPad = 4;
+// weight 0, vidx -1), so every segment starts at an even entry (16-byte
+// aligned entry pairs).  Kernels walk segments in groups of 4 entries; a
+// group whose second pair lies past the segment end (segment length = 2 mod 4)
+// masks that pair (no load, weight 0).  A padding entry's offset addresses the
+// all-zero row kernels keep just before a tile (or is skipped by a predicated
+// load).  Entry columns are stored as byte offsets of a 128-float tile row
+// (kTilRowBytes); kernels with narrower tiles shift them down.  Conv tap
+// tilings keep groups of 4 (kTapPad).
+constexpr int kTilPad = 2;
+constexpr int kTapPad = 4;
 constexpr int kTilRowBytes = 512;
 
 namespace sp {

@@ -174,19 +174,27 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
             const int s0 = __shfl_sync(kFull, sg, i), s1 = __shfl_sync(kFull, sg, i + 1);
-            // segments are padded to multiples of 4 (weight-0 entries): no tail
+            // segments are padded to even lengths (weight-0 entries); groups of 4
             for (int e = s0; e < s1; e += 4) {
-                // 4 entries in two 16-byte broadcast loads
+                // 4 entries in two 16-byte broadcast loads; the second pair is masked
+                // (no load, weight 0) when it lies past the segment
                 const int4 p01 = ld_entry_pair(es + e, SENT);
                 const int4 p23 = ld_entry_pair(es + e + 2, SENT);
                 const int off[4] = {p01.x, p01.z, p23.x, p23.z};
                 const float w[4] = {__int_as_float(p01.y), __int_as_float(p01.w), __int_as_float(p23.y),
                                     __int_as_float(p23.w)};
                 float x[4][VEC];
+                if (e + 2 < s1) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) lds_row_or_zero<VEC, SH>(tb, off[u], x[u]);
+                    for (int u = 0; u < 4; ++u) lds_row_or_zero<VEC, SH>(tb, off[u], x[u]);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) fma_bcast<VEC>(acc[i], w[u], x[u]);
+                    for (int u = 0; u < 4; ++u) fma_bcast<VEC>(acc[i], w[u], x[u]);
+                } else {  // last pair of the segment
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) lds_row_or_zero<VEC, SH>(tb, off[u], x[u]);
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) fma_bcast<VEC>(acc[i], w[u], x[u]);
+                }
             }
         }
         if (vec4) {  // release the buffer; the last warp done with tile q refills it with tile q+2
