@@ -777,10 +777,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
 }
 
-// zero the dX region (RB rows via rowmap x BT batch columns) of the split items
-__global__ void zero_items_kernel(const int64_t *__restrict__ items, int RB, int BT, int64_t nslice,
+// zero the dX region (RB rows via rowmap x BT batch columns) of the items cut
+// by a range boundary: block c handles the boundary at the start of CTA c+1
+__global__ void zero_items_kernel(int64_t T, int64_t G, int nkb, int RB, int BT, int64_t nslice,
                                   const int32_t *__restrict__ rowmap, int64_t nrow, int64_t B, float *__restrict__ dX) {
-    const int64_t it = items[blockIdx.x];
+    const int64_t lo = sk_lo(blockIdx.x + 1, T, G);
+    if (lo % nkb == 0) return;  // the boundary falls between items
+    const int64_t it = lo / nkb;
     const int64_t rb = it / nslice, sl = it - rb * nslice;
     for (int i = threadIdx.x; i < RB * (BT / 4); i += blockDim.x) {
         const int lr = i / (BT / 4), c4 = (i - lr * (BT / 4)) * 4;
@@ -854,29 +857,19 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     const int64_t T = (int64_t)t.nrb * slices * t.nkb;
     const int64_t G = std::min<int64_t>(kNumSMs, T);
     if (tm && !sk_disabled() && T / G > t.nkb && T < (1LL << 31) && t.max_warp <= (int64_t)kSkDwCols * 32) {
-        // items (rb, slice) cut by a range boundary: their dX is accumulated by two CTAs
-        std::vector<int64_t> items;
-        for (int64_t c = 1; c < G; ++c) {
-            const int64_t lo = sk_lo(c, T, G);
-            if (lo % t.nkb != 0) items.push_back(lo / t.nkb);
-        }
         int64_t maxjobs = 1;
         for (int64_t rb = 0; rb < t.nrb; ++rb) {
             const int64_t tl = rb * slices * t.nkb;
             maxjobs = std::max<int64_t>(maxjobs, sk_cta(tl + slices * t.nkb - 1, T, G) - sk_cta(tl, T, G) + 1);
         }
         float *part = nullptr;
-        int64_t *ditems = nullptr;
-        if (cudaMallocAsync((void **)&part, (size_t)(maxjobs * t.npad) * sizeof(float), st) != cudaSuccess ||
-            cudaMallocAsync((void **)&ditems, (items.size() + 1) * sizeof(int64_t), st) != cudaSuccess) {
+        if (cudaMallocAsync((void **)&part, (size_t)(maxjobs * t.npad) * sizeof(float), st) != cudaSuccess) {
             set_error("sp_linear_bwd: scratch allocation failed");
             return SP_ERR_ALLOC;
         }
         launch_refresh(t, w->vals, w->nnz, st);  // CSC-tiled weights from vals (through perm)
-        if (!items.empty()) {
-            cudaMemcpyAsync(ditems, items.data(), items.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st);
-            zero_items_kernel<<<(unsigned)items.size(), 256, 0, st>>>(ditems, 128, BT, slices, t.rowmap, t.rows, B, dX);
-        }
+        // items (rb, slice) cut by a range boundary: their dX is accumulated by two CTAs
+        if (G > 1) zero_items_kernel<<<(unsigned)(G - 1), 256, 0, st>>>(T, G, t.nkb, 128, BT, slices, t.rowmap, t.rows, B, dX);
         FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, 0, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
                     0, t.rowmap, slices, t.nrb};
         auto kern = H ? bwd_fused_sk_kernel<TRPW, TNW, true> : bwd_fused_sk_kernel<TRPW, TNW, false>;
@@ -884,9 +877,8 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
         kern<<<(unsigned)G, TNW * 32, smem, st>>>(a, tmap);
         job_reduce_kernel<<<(unsigned)((t.npad + 255) / 256), 256, 0, st>>>(t.npad, t.nrb, t.nkb, 128, slices, G,
                                                                           t.seg, part, t.vidx, dW);
-        count_launches(items.empty() ? 2 : 3);
+        count_launches(G > 1 ? 3 : 2);
         cudaFreeAsync(part, st);
-        cudaFreeAsync(ditems, st);
         return SP_OK;
     }
     int64_t nsplit, spl;

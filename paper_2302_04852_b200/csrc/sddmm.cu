@@ -304,11 +304,14 @@ sp_status launch_vec(const sp_weight_s *w, const sp_tiling &t, int var, const fl
 }
 
 // conv: dW[vidx_t[e]] = sum_s part[s][tapbase_t + e]  (grid.y = tap)
-__global__ void conv_split_reduce_kernel(const TapDev *__restrict__ taps, const int64_t *__restrict__ tapbase,
+struct TapBase {
+    int64_t v[kMaxTaps];
+};
+__global__ void conv_split_reduce_kernel(const TapDev *__restrict__ taps, const TapBase tapbase,
                                          int64_t totpad, int nsplit, const float *__restrict__ part,
                                          float *__restrict__ dW) {
     const TapDev t = taps[blockIdx.y];
-    const int64_t base = tapbase[blockIdx.y];
+    const int64_t base = tapbase.v[blockIdx.y];
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < t.npad; e += (int64_t)gridDim.x * blockDim.x) {
         const int v = t.vidx[e];
         if (v < 0) continue;
@@ -346,11 +349,9 @@ bool launch_conv_sddmm(const sp_weight_s *w, int64_t B, const float *dYv, const 
     const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)(226 * 1024);
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
     float *part = nullptr;
-    int64_t *tb_dev = nullptr;
-    if (cudaMallocAsync((void **)&part, (size_t)(nsplit * tot) * sizeof(float), st) != cudaSuccess ||
-        cudaMallocAsync((void **)&tb_dev, sizeof(tapbase), st) != cudaSuccess)
-        return false;
-    cudaMemcpyAsync(tb_dev, tapbase, sizeof(tapbase), cudaMemcpyHostToDevice, st);
+    if (cudaMallocAsync((void **)&part, (size_t)(nsplit * tot) * sizeof(float), st) != cudaSuccess) return false;
+    TapBase tbv;
+    for (int t = 0; t < kMaxTaps; ++t) tbv.v[t] = tapbase[t];
     SddmmArgs a{t0.rows, t0.inner, Lv, t0.KC, t0.nkb, (int)spl, cap, 1, nullptr, nullptr, nullptr, dYv, Xp,
                 part, tot, 0, nullptr, w->tapdev, {}, {}};
     for (int t = 0; t < ntap; ++t) {
@@ -361,9 +362,8 @@ bool launch_conv_sddmm(const sp_weight_s *w, int64_t B, const float *dYv, const 
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     count_launches(2);
     kern<<<dim3((unsigned)t0.nrb, (unsigned)nsplit, (unsigned)ntap), NW * 32, smem, st>>>(a, tmap);
-    conv_split_reduce_kernel<<<dim3(64, ntap), 256, 0, st>>>(w->tapdev, tb_dev, tot, (int)nsplit, part, dW);
+    conv_split_reduce_kernel<<<dim3(64, ntap), 256, 0, st>>>(w->tapdev, tbv, tot, (int)nsplit, part, dW);
     cudaFreeAsync(part, st);
-    cudaFreeAsync(tb_dev, st);
     return true;
 }
 

@@ -37,22 +37,36 @@ def flush_l2():
 
 
 def timed(fns, reps):
-    """median over reps of the summed event time of fns (each timed separately), ms."""
+    """Per function: median over reps of (a) the CUDA-graph replay time of one
+    call (kernel time, launch overhead removed) and (b) the event time around a
+    direct API call (includes the host-side launch work), ms.  L2 is flushed
+    before every timed repetition."""
     st = torch.cuda.current_stream()
     per = {k: [] for k in fns}
+    api = {k: [] for k in fns}
     for _ in range(3):
         for f in fns.values():
             f()
+    torch.cuda.synchronize()
+    graphs = {}
+    for k, f in fns.items():
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            f()
+        graphs[k] = g
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
     for _ in range(reps):
         for k, f in fns.items():
-            flush_l2()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record(st)
-            f()
-            e.record(st)
-            e.synchronize()
-            per[k].append(s.elapsed_time(e))
-    return {k: float(np.median(v)) for k, v in per.items()}
+            for lst, call in ((per[k], graphs[k].replay), (api[k], f)):
+                flush_l2()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record(st)
+                call()
+                e.record(st)
+                e.synchronize()
+                lst.append(s.elapsed_time(e))
+    return ({k: float(np.median(v)) for k, v in per.items()}, {k: float(np.median(v)) for k, v in api.items()})
 
 
 def linear(name, R, C, B, density, wvar, seed, kind="uniform", reps=10, dense_ctx=True):
@@ -60,25 +74,31 @@ def linear(name, R, C, B, density, wvar, seed, kind="uniform", reps=10, dense_ct
     W = sp.sp_weight_create(torch.from_numpy(c["W"]).cuda(), torch.from_numpy(c["mask"]).cuda())
     X, dY = torch.from_numpy(c["X"]).cuda(), torch.from_numpy(c["dY"]).cuda()
     Y, dX, dW = torch.empty(R, B, device="cuda"), torch.empty(C, B, device="cuda"), torch.empty(max(W.nnz, 1), device="cuda")
-    t = timed({"fwd": lambda: sp.sp_linear_fwd(W, X, Y), "dx": lambda: sp.sp_linear_bwd_input(W, dY, dX),
-               "dw": lambda: sp.sp_linear_bwd_weight(W, X, dY, dW[:W.nnz])}, reps)
+    t, ta = timed({"fwd": lambda: sp.sp_linear_fwd(W, X, Y), "dx": lambda: sp.sp_linear_bwd_input(W, dY, dX),
+                   "dw": lambda: sp.sp_linear_bwd_weight(W, X, dY, dW[:W.nnz]),
+                   "bwd_fused": lambda: sp.sp_linear_bwd(W, X, dY, dX, dW[:W.nnz])}, reps)
+    tf = t.pop("bwd_fused")
+    taf = ta.pop("bwd_fused")
     fl = 2 * W.nnz * B
     byts = {"fwd": 8 * W.nnz + 4 * (R + 1) + 4 * B * (R + C), "dx": 8 * W.nnz + 4 * (C + 1) + 4 * B * (R + C),
             "dw": 8 * W.nnz + 4 * B * (R + C) + 4 * W.nnz}
     rec = {"config": name, "mask": kind, "sparsity": round(1 - density, 4), "R": R, "C": C, "B": B, "nnz": W.nnz,
-           "seed": seed, "l2": "flushed before each timed launch"}
+           "seed": seed, "l2": "flushed before each timed launch", "timing": "CUDA-graph replay of one call (t_*), direct API call (t_api_*)"}
     tot_t = sum(t.values())
     roof = sum(max(fl / FP32, byts[k] / HBM) for k in t)
     rec.update({f"t_{k}_us": round(v * 1e3, 2) for k, v in t.items()})
     rec["t_fwd_bwd_us"] = round(tot_t * 1e3, 2)
+    rec["t_fwd_bwd_fused_us"] = round((t["fwd"] + tf) * 1e3, 2)  # fwd + fused dX/dW (sp_linear_bwd)
+    rec["t_api_fwd_bwd_us"] = round(sum(ta.values()) * 1e3, 2)  # direct API calls incl. host launch work
     rec["eff_gflops"] = round(3 * fl / (tot_t * 1e-3) / 1e9, 1)
+    rec["eff_gflops_fused"] = round(3 * fl / ((t["fwd"] + tf) * 1e-3) / 1e9, 1)
     rec["roofline_us"] = round(roof * 1e6, 2)
     rec["pct_roofline"] = round(100 * roof / (tot_t * 1e-3), 2)
     rec["pct_fp32_peak"] = round(100 * 3 * fl / (tot_t * 1e-3) / FP32, 2)
     if dense_ctx:  # the paper's "dense counterpart" (P363): cuBLAS fp32, TF32 off, masked W
         torch.backends.cuda.matmul.allow_tf32 = False
         Wd = torch.from_numpy(c["W"] * c["mask"]).cuda()
-        td = timed({"fwd": lambda: Wd @ X, "dx": lambda: Wd.t() @ dY, "dw": lambda: dY @ X.t()}, reps)
+        td, _ = timed({"fwd": lambda: Wd @ X, "dx": lambda: Wd.t() @ dY, "dw": lambda: dY @ X.t()}, reps)
         rec["dense_cublas_fp32_us"] = round(sum(td.values()) * 1e3, 2)
     return rec
 
@@ -91,8 +111,8 @@ def conv(name, reps=10, **cfg):
     Y = torch.empty(c["OC"], c["OH"], c["OW"], c["B"], device="cuda")
     dX = torch.empty_like(X)
     dW = torch.empty(W.nnz, device="cuda")
-    t = timed({"fwd": lambda: sp.sp_conv2d_fwd(W, g, X, Y), "dx": lambda: sp.sp_conv2d_bwd_input(W, g, dY, dX),
-               "dw": lambda: sp.sp_conv2d_bwd_weight(W, g, X, dY, dW)}, reps)
+    t, ta = timed({"fwd": lambda: sp.sp_conv2d_fwd(W, g, X, Y), "dx": lambda: sp.sp_conv2d_bwd_input(W, g, dY, dX),
+                   "dw": lambda: sp.sp_conv2d_bwd_weight(W, g, X, dY, dW)}, reps)
     # exact useful FMAs: per tap (x, y), valid output rows x cols (C20)
     m = c["mask"].astype(bool)
     OH, OW, H, Wd, pad = c["OH"], c["OW"], c["H"], c["Wd"], c["pad"]
@@ -106,9 +126,10 @@ def conv(name, reps=10, **cfg):
     tot_t = sum(t.values())
     roof = sum(max(fl / FP32, byts[k] / HBM) for k in t)
     rec = {"config": name, "nnz": W.nnz, "B": c["B"], "geom": f"{c['IC']}->{c['OC']} {H}x{Wd} k{c['KH']} pad{pad}",
-           "l2": "flushed before each timed launch"}
+           "l2": "flushed before each timed launch", "timing": "CUDA-graph replay of one call (t_*), direct API call (t_api_*)"}
     rec.update({f"t_{k}_us": round(v * 1e3, 2) for k, v in t.items()})
     rec["t_fwd_bwd_us"] = round(tot_t * 1e3, 2)
+    rec["t_api_fwd_bwd_us"] = round(sum(ta.values()) * 1e3, 2)
     rec["eff_gflops_exact"] = round(3 * fl / (tot_t * 1e-3) / 1e9, 1)
     rec["eff_gflops_nominal"] = round(3 * fl_nominal / (tot_t * 1e-3) / 1e9, 1)
     rec["roofline_us"] = round(roof * 1e6, 2)
@@ -117,7 +138,7 @@ def conv(name, reps=10, **cfg):
     torch.backends.cudnn.allow_tf32 = False
     Xn = X.permute(3, 0, 1, 2).contiguous()
     Wm = torch.from_numpy(c["W"] * c["mask"]).cuda()
-    td = timed({"fwd": lambda: torch.nn.functional.conv2d(Xn, Wm, padding=pad)}, reps)
+    td, _ = timed({"fwd": lambda: torch.nn.functional.conv2d(Xn, Wm, padding=pad)}, reps)
     rec["dense_cudnn_fp32_fwd_us"] = round(td["fwd"] * 1e3, 2)
     return rec
 
