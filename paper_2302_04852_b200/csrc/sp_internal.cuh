@@ -125,6 +125,10 @@ enum Epi { EPI_NONE = 0, EPI_RELU = 1, EPI_GATE = 2 };
 void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out,
                  const float *gate, int epi, cudaStream_t st);
 
+// ---- spmm_sk.cu: stream-K SpMM (B % 4 == 0, big tiling); false if it does not apply
+bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,
+                    int epi, cudaStream_t st);
+
 // ---- gather.cu (very sparse / small regime: no shared-memory staging) ----
 bool gather_preferred(const sp_weight_s *w, int orient, int64_t B, bool chunked = false);
 void launch_spmm_gather(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out,

@@ -271,6 +271,17 @@ bool spmm_nw32() {
     }();
     return v != 0;
 }
+// The stream-K SpMM (spmm_sk.cu) is opt-in (SP_SPMM_SK=1): measured +6-7% on
+// 768-row layers and -3% on 3072-row ones at B=16384, slower at B=512, and its
+// split items change the per-element summation order with B (the per-item
+// grid keeps every output element's order independent of B and of the grid).
+bool spmm_sk_disabled() {
+    static const int v = [] {
+        const char *e = getenv("SP_SPMM_SK");
+        return (e && e[0] == '1') ? 0 : 1;
+    }();
+    return v != 0;
+}
 constexpr int kSmemLimit = 226 * 1024;  // per SM, usable by CTAs (minus static mbarriers)
 
 template <int VEC, int RPW, int NW>
@@ -364,6 +375,7 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
         launch_spmm_gather(w, orient, B, in, out, gate, epi, st);
         return;
     }
+    if (!spmm_sk_disabled() && launch_spmm_sk(w, orient, B, in, out, gate, epi, st)) return;
     // Choose the largest row block and batch vector that still fill the GPU.
     int vec = B <= 32 ? 1 : (B <= 64 || (B & 3)) ? 2 : 4;
     int var = 0;

@@ -1,0 +1,280 @@
+// spmm_sk.cu -- stream-K schedule of the tiled SpMM (forward Y = W X, P141;
+// CSC-driven dX = W^T dY, Eq. 1): one wave of CTAs, each running an equal
+// contiguous range of the tile sequence (row block rb, batch slice sl, column
+// block kb), so small or ragged problems (few batch slices, few row blocks)
+// still occupy every SM and no CTA pays a pipeline start per item.
+//
+// An item (rb, sl) whose kb range is cut by range boundaries is finished by
+// the last of its CTAs to arrive (per-item ticket): every part stores its raw
+// sums, and the last one adds the parts in CTA order -- a fixed order, so the
+// result is deterministic -- applies the epilogue (ReLU / ReLU' gate) and
+// writes the output.  Tiles are staged exactly as in spmm.cu (2-D TMA box of
+// the activation + 1-D bulk copy of the entries, two buffers, the last warp
+// done with a buffer refills it).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "sp_internal.cuh"
+#include "tile.cuh"
+
+namespace sp {
+namespace {
+
+constexpr int kNumSMs = 148;
+
+__host__ __device__ __forceinline__ int64_t lo_of(int64_t c, int64_t T, int64_t G) { return c * T / G; }
+__host__ __device__ __forceinline__ int64_t cta_of(int64_t t, int64_t T, int64_t G) {
+    int64_t c = t * G / T;
+    while (c + 1 < G && lo_of(c + 1, T, G) <= t) ++c;
+    while (c > 0 && lo_of(c, T, G) > t) --c;
+    return c;
+}
+
+struct SkArgs {
+    int64_t rows, B, nslice;
+    int KC, nkb, nrb, cap;
+    const int32_t *seg;
+    const int2 *ent;
+    float *out;
+    const float *gate;
+    const int32_t *rowmap;
+    float *part;    // [G][2][RB][BT] raw sums of cut items (slot 0: the CTA's first item, 1: its last)
+    int *tickets;   // [nrb * nslice], zero on entry, reset by the finishing CTA
+};
+
+template <int RPW, int NW, int EPI>
+__global__ void __launch_bounds__(NW * 32, 1)
+    spmm_sk_kernel(const SkArgs a, const __grid_constant__ CUtensorMap tmap) {
+    constexpr int VEC = 4;
+    constexpr int BT = 32 * VEC;
+    constexpr int RB = NW * RPW;
+    extern __shared__ __align__(128) float smem[];  // [2][KC][BT] floats, [2][cap+2] int2
+    __shared__ uint64_t full[2];
+    __shared__ int released[2];
+    __shared__ int last_flag;
+    int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * a.KC * BT);
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t B = a.B;
+    const int64_t T = (int64_t)a.nrb * a.nslice * a.nkb, G = gridDim.x;
+    const int t0 = (int)lo_of(blockIdx.x, T, G);  // T < 2^31 (launcher)
+    const int ntile = (int)lo_of(blockIdx.x + 1, T, G) - t0;
+    const int nsl = (int)a.nslice;
+    const size_t tile_sz = (size_t)a.KC * BT;
+    const int ebuf = a.cap + 2;
+    const int first_item = t0 / a.nkb;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        released[0] = 0;
+        released[1] = 0;
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    struct Tile {
+        int rb, sl, kb;
+    };
+    auto tile_of = [&](int q) -> Tile {
+        const int t = t0 + q, it = t / a.nkb;
+        Tile id;
+        id.kb = t - it * a.nkb;
+        id.rb = it / nsl;
+        id.sl = it - id.rb * nsl;
+        return id;
+    };
+    auto next_tile = [&](Tile id) -> Tile {
+        if (++id.kb == a.nkb) {
+            id.kb = 0;
+            if (++id.sl == nsl) {
+                id.sl = 0;
+                ++id.rb;
+            }
+        }
+        return id;
+    };
+    auto entry_range = [&](const Tile &id, int &e0, int &e1) {
+        const int64_t tb = ((int64_t)id.rb * a.nkb + id.kb) * RB;
+        e0 = __ldg(a.seg + tb) & ~1;
+        e1 = __ldg(a.seg + tb + RB);
+    };
+    auto issue = [&](int q, int buf) {
+        const Tile id = tile_of(q);
+        int e0, e1;
+        entry_range(id, e0, e1);
+        const unsigned eb = (unsigned)(((e1 - e0) * 8 + 15) & ~15);
+        mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
+        tma_load_2d(smem + buf * tile_sz, &tmap, id.sl * BT, id.kb * a.KC, &full[buf]);
+        if (eb) tma_load_1d(ents + buf * ebuf, a.ent + e0, eb, &full[buf]);
+    };
+    if (threadIdx.x == 0) {
+        if (ntile > 0) issue(0, 0);
+        if (ntile > 1) issue(1, 1);
+    }
+    auto seg_bounds = [&](const Tile &id) -> int {
+        const int32_t *segw = a.seg + ((int64_t)id.rb * a.nkb + id.kb) * RB + warp * RPW;
+        return lane <= RPW ? __ldg(segw + lane) : 0;
+    };
+    // epilogue of rows (rb, lr = warp*RPW + i) for batch columns bl..bl+3
+    auto store = [&](int rb, int i, int64_t bl, const float (&v)[VEC]) {
+        const int64_t tpos = (int64_t)rb * RB + warp * RPW + i;
+        const int64_t r = a.rowmap ? (int64_t)__ldg(a.rowmap + tpos) : tpos;
+        if (r < 0 || r >= a.rows || bl >= B) return;
+        float o[VEC];
+#pragma unroll
+        for (int u = 0; u < VEC; ++u) {
+            float x = v[u];
+            if (EPI == EPI_RELU) x = fmaxf(x, 0.f);
+            if (EPI == EPI_GATE) x = __ldg(a.gate + r * B + bl + u) > 0.f ? x : 0.f;
+            o[u] = x;
+        }
+        *reinterpret_cast<float4 *>(a.out + r * B + bl) = make_float4(o[0], o[1], o[2], o[3]);
+    };
+
+    float acc[RPW][VEC];
+    int kb_first = 0;
+    Tile nid = tile_of(0);
+    int sgn = ntile > 0 ? seg_bounds(nid) : 0;
+    for (int q = 0; q < ntile; ++q) {
+        const Tile id = nid;
+        const int buf = q & 1;
+        if (q == 0 || id.kb == 0) {  // new item
+#pragma unroll
+            for (int i = 0; i < RPW; ++i)
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) acc[i][v] = 0.f;
+            kb_first = id.kb;
+        }
+        const int sg = sgn;
+        nid = next_tile(id);
+        if (q + 1 < ntile) sgn = seg_bounds(nid);
+        mbar_wait(&full[buf], (q >> 1) & 1);
+        int ea, e1t;
+        entry_range(id, ea, e1t);
+        const char *tb = reinterpret_cast<const char *>(smem + buf * tile_sz + lane * VEC);
+        const int2 *es = ents + buf * ebuf - ea;
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+            const int s0 = __shfl_sync(kFull, sg, i), s1 = __shfl_sync(kFull, sg, i + 1);
+            for (int e = s0; e < s1; e += 4) {
+                const int4 p01 = ld_entry_pair(es + e, true);
+                const int4 p23 = ld_entry_pair(es + e + 2, true);
+                const int off[4] = {p01.x, p01.z, p23.x, p23.z};
+                const float w[4] = {__int_as_float(p01.y), __int_as_float(p01.w), __int_as_float(p23.y),
+                                    __int_as_float(p23.w)};
+                float x[4][VEC];
+                if (e + 2 < s1) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) lds_row_or_zero<VEC, 0>(tb, off[u], x[u]);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) fma_bcast<VEC>(acc[i], w[u], x[u]);
+                } else {  // last pair of the segment
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) lds_row_or_zero<VEC, 0>(tb, off[u], x[u]);
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) fma_bcast<VEC>(acc[i], w[u], x[u]);
+                }
+            }
+        }
+        // release the buffer; the last warp to finish tile q refills it with tile q+2
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            if (atomicAdd(&released[buf], 1) == NW - 1) {
+                released[buf] = 0;
+                __threadfence_block();
+                if (q + 2 < ntile) issue(q + 2, buf);
+            }
+        }
+        if (id.kb != a.nkb - 1 && q != ntile - 1) continue;
+
+        // ---- this CTA's part of item (rb, sl) is done
+        const int64_t bl = (int64_t)id.sl * BT + lane * VEC;
+        if (kb_first == 0 && id.kb == a.nkb - 1) {  // whole item: store directly
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) store(id.rb, i, bl, acc[i]);
+            continue;
+        }
+        const int item = id.rb * nsl + id.sl;
+        const int slot = item == first_item ? 0 : 1;
+        float *mine = a.part + ((int64_t)(blockIdx.x * 2 + slot) * RB + warp * RPW) * BT + lane * VEC;
+#pragma unroll
+        for (int i = 0; i < RPW; ++i)
+            *reinterpret_cast<float4 *>(mine + i * BT) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        __threadfence();
+        __syncthreads();
+        const int64_t c0 = cta_of((int64_t)item * a.nkb, T, G), c1 = cta_of((int64_t)item * a.nkb + a.nkb - 1, T, G);
+        if (threadIdx.x == 0) {
+            const int old = atomicAdd(a.tickets + item, 1);
+            last_flag = old == (int)(c1 - c0);
+            if (last_flag) a.tickets[item] = 0;  // ready for the next launch
+        }
+        __syncthreads();
+        if (!last_flag) continue;
+        __threadfence();
+        // last part in: sum the parts in CTA order, epilogue, store
+        float sum[RPW][VEC];
+#pragma unroll
+        for (int i = 0; i < RPW; ++i)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) sum[i][v] = 0.f;
+        for (int64_t c = c0; c <= c1; ++c) {
+            const int s = item == (int)(lo_of(c, T, G) / a.nkb) ? 0 : 1;
+            const float *pp = a.part + ((c * 2 + s) * RB + warp * RPW) * BT + lane * VEC;
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                const float4 t = __ldcg(reinterpret_cast<const float4 *>(pp + i * BT));
+                sum[i][0] += t.x;
+                sum[i][1] += t.y;
+                sum[i][2] += t.z;
+                sum[i][3] += t.w;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) store(id.rb, i, bl, sum[i]);
+    }
+}
+
+}  // namespace
+
+bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,
+                    int epi, cudaStream_t st) {
+    constexpr int RPW = 4, NW = 32, BT = 128;
+    if ((B & 3) != 0 || w->nnz == 0) return false;
+    const sp_tiling &t = w->til[orient][0];
+    if (t.RB != RPW * NW) return false;
+    const int64_t nslice = (B + BT - 1) / BT;
+    const int64_t T = (int64_t)t.nrb * nslice * t.nkb;
+    if (T >= (1LL << 31)) return false;
+    const int64_t G = std::min<int64_t>(kNumSMs, T);
+    const size_t tiles = (size_t)2 * t.KC * BT * sizeof(float);
+    const int cap = (t.max_tile + 2 + 3) & ~3;
+    const size_t smem = tiles + (size_t)2 * (cap + 2) * sizeof(int2);
+    if (smem > (size_t)(226 * 1024)) return false;
+    CUtensorMap tmap{};
+    if (!make_tmap_2d(&tmap, in, t.inner, B, BT, t.KC)) return false;
+    const int64_t nitems = (int64_t)t.nrb * nslice;
+    float *part = nullptr;
+    int *tickets = nullptr;
+    if (cudaMallocAsync((void **)&part, (size_t)G * 2 * 128 * BT * sizeof(float), st) != cudaSuccess ||
+        cudaMallocAsync((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)
+        return false;
+    cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
+    launch_refresh(t, w->vals, w->nnz, st);
+    SkArgs a{t.rows, B, nslice, t.KC, t.nkb, t.nrb, cap, t.seg, t.ent, out, gate, t.rowmap, part, tickets};
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<(unsigned)G, NW * 32, smem, st>>>(a, tmap);
+    };
+    if (epi == EPI_RELU) go(spmm_sk_kernel<RPW, NW, EPI_RELU>);
+    else if (epi == EPI_GATE) go(spmm_sk_kernel<RPW, NW, EPI_GATE>);
+    else go(spmm_sk_kernel<RPW, NW, EPI_NONE>);
+    count_launches(1);
+    cudaFreeAsync(part, st);
+    cudaFreeAsync(tickets, st);
+    return true;
+}
+
+}  // namespace sp
