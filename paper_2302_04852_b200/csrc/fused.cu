@@ -46,6 +46,8 @@ struct FusedArgs {
     const int32_t *rowmap;  // tiled position -> row of X / dX (-1 unused)
     int64_t nslice;         // stream-K kernel: batch slices of BT columns
     int nrow_blocks;        // stream-K kernel: row blocks of the tiling
+    float *dxpart;          // stream-K kernel: [G][2][RB][BT] raw dX parts of cut items
+    int *tickets;           // stream-K kernel: [nrow_blocks * nslice], zero on entry
 };
 
 template <int RPW, int NW, bool GATE, bool SENT>
@@ -480,6 +482,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
 // row (c - first CTA of rb) of the partial buffer, summed per entry in fixed
 // order by job_reduce_kernel.
 __host__ __device__ __forceinline__ int64_t sk_lo(int64_t c, int64_t T, int64_t G) { return c * T / G; }
+constexpr int kMaxJobTab = 1024;  // job_reduce_kernel's table of CTA range starts
 __host__ __device__ __forceinline__ int64_t sk_cta(int64_t t, int64_t T, int64_t G) {
     int64_t c = t * G / T;
     while (c + 1 < G && sk_lo(c + 1, T, G) <= t) ++c;
@@ -542,12 +545,14 @@ __global__ void __launch_bounds__(NW * 32, 1)
     __shared__ uint64_t full[2];
     __shared__ int released[2];  // warps done with each buffer (the last one refills it)
     __shared__ uint32_t tmem_base;
+    __shared__ int last_flag;
     int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * (a.KC + 1) * BT);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t B = a.B;
     const int64_t T = (int64_t)a.nrow_blocks * a.nslice * a.nkb, G = gridDim.x;
     const int t0 = (int)sk_lo(blockIdx.x, T, G);  // T < 2^31 (checked by the launcher)
+    const int first_item = t0 / a.nkb;
     const int ntile = (int)sk_lo(blockIdx.x + 1, T, G) - t0;
     const int nsl = (int)a.nslice;
     const size_t tile_sz = (size_t)a.KC * BT;
@@ -623,10 +628,20 @@ __global__ void __launch_bounds__(NW * 32, 1)
     };
 
     // write this job's dW sums (row block rb)
-    auto dump = [&](int rb) {
+    // column block kb of row block rb is touched by the job running tiles
+    // [ja, ja + len) of rb (local tile indices, slice-major)
+    auto touched = [&](int kb, int ka, int len) -> bool {  // ka = ja % nkb
+        int d = kb - ka;
+        if (d < 0) d += a.nkb;
+        return len >= a.nkb || d < len;
+    };
+    // write this job's dW sums (row block rb, local tiles [ja, ja + len)); column
+    // blocks the job never touched are skipped (job_reduce_kernel skips them too)
+    auto dump = [&](int rb, int ja, int len) {
         const int64_t job = blockIdx.x - sk_cta((int64_t)rb * a.nslice * a.nkb, T, G);
         float *P = a.part + job * a.npad;
         int c2 = 0, my_e = -1;
+        const int ka = ja % a.nkb;
         auto out = [&](int col) {
             const float val = tm_ld1(tcol + kSkDw + (uint32_t)col);
             if (my_e >= 0) P[my_e] = val;
@@ -634,6 +649,14 @@ __global__ void __launch_bounds__(NW * 32, 1)
         };
         for (int kb = 0; kb < a.nkb; ++kb) {
             const int sg = lane <= RPW ? __ldg(segw_of(rb, kb) + lane) : 0;
+            if (!touched(kb, ka, len)) {  // advance the slot sequence past this column block
+                int gs = 0;
+#pragma unroll
+                for (int m = 0; m < RPW; ++m) gs += (__shfl_sync(kFull, sg, m + 1) - __shfl_sync(kFull, sg, m) + 3) >> 2;
+                if ((c2 & 7) != 0 && ((c2 + gs) >> 3) != (c2 >> 3)) out(c2 >> 3);
+                c2 += gs;
+                continue;
+            }
             for (int m = 0; m < RPW; ++m) {
                 const int g0 = __shfl_sync(kFull, sg, m), g1 = __shfl_sync(kFull, sg, m + 1);
                 for (int e = g0; e < g1; e += 4) {
@@ -648,7 +671,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     };
 
     float keep = 0.f;
-    int cnt = 0, cur_rb = -1;
+    int cnt = 0, cur_rb = -1, job_a = 0;  // job_a: first local tile of the current job in its row block
     bool whole = true;  // current item started at kb 0 in this CTA
     Tile nid = tile_of(0);
     int sgn = ntile > 0 ? seg_bounds(nid) : 0;
@@ -658,7 +681,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
         const int64_t r_base = (int64_t)id.rb * RB + warp * RPW;
         const int64_t bl = (int64_t)id.sl * BT + lane * VEC;
         if (id.rb != cur_rb) {  // new job: clear the dW sums
-            if (cur_rb >= 0) dump(cur_rb);
+            if (cur_rb >= 0) dump(cur_rb, job_a, t0 + q - job_a - (int)((int64_t)cur_rb * a.nslice * a.nkb));
+            job_a = t0 + q - (int)((int64_t)id.rb * a.nslice * a.nkb);
             for (int c = 0; c < kSkDwCols; ++c) tm_st1(tcol + kSkDw + (uint32_t)c, 0.f);
             cur_rb = id.rb;
         }
@@ -736,26 +760,68 @@ __global__ void __launch_bounds__(NW * 32, 1)
         if (id.kb == a.nkb - 1 || q == ntile - 1) {  // item done here: partial column, dX rows
             if (cnt & 7) flush(cnt >> 3);
             tm_wait_st();
-            const bool split = !whole || id.kb != a.nkb - 1;  // the other part is another CTA's
-#pragma unroll 1
-            for (int i = 0; i < RPW; ++i) {
+            // ReLU' gate and store of dX rows (rb, warp*RPW + i), batch columns bl..bl+3
+            auto store = [&](int i, float (&o)[VEC]) {
                 const int64_t r = __ldg(a.rowmap + r_base + i);
-                float o[VEC];
-                tm_ld4(tcol + kSkDx + 4 * i, o);
-                if (r < 0 || r >= a.nrow || bl >= B) continue;
-                if (GATE) {  // ReLU' gate, exact per addend (x * {0,1})
+                if (r < 0 || r >= a.nrow || bl >= B) return;
+                if (GATE) {
                     const float4 hv = __ldg(reinterpret_cast<const float4 *>(a.H + r * B + bl));
                     o[0] = hv.x > 0.f ? o[0] : 0.f;
                     o[1] = hv.y > 0.f ? o[1] : 0.f;
                     o[2] = hv.z > 0.f ? o[2] : 0.f;
                     o[3] = hv.w > 0.f ? o[3] : 0.f;
                 }
-                float *dst = a.dX + r * B + bl;
-                if (split) {
+                *reinterpret_cast<float4 *>(a.dX + r * B + bl) = make_float4(o[0], o[1], o[2], o[3]);
+            };
+            if (whole && id.kb == a.nkb - 1) {  // the whole item ran here
+#pragma unroll 1
+                for (int i = 0; i < RPW; ++i) {
+                    float o[VEC];
+                    tm_ld4(tcol + kSkDx + 4 * i, o);
+                    store(i, o);
+                }
+            } else {
+                // cut item: store the raw part; the last CTA of the item to arrive sums the
+                // parts in CTA order (deterministic), gates and stores
+                const int item = id.rb * nsl + id.sl;
+                const int slot = item == first_item ? 0 : 1;
+                float *mine = a.dxpart + ((int64_t)(blockIdx.x * 2 + slot) * RB + warp * RPW) * BT + lane * VEC;
+#pragma unroll 1
+                for (int i = 0; i < RPW; ++i) {
+                    float o[VEC];
+                    tm_ld4(tcol + kSkDx + 4 * i, o);
+                    *reinterpret_cast<float4 *>(mine + i * BT) = make_float4(o[0], o[1], o[2], o[3]);
+                }
+                __threadfence();
+                __syncthreads();
+                const int64_t c0 = sk_cta((int64_t)item * a.nkb, T, G);
+                const int64_t c1 = sk_cta((int64_t)item * a.nkb + a.nkb - 1, T, G);
+                if (threadIdx.x == 0) {
+                    const int old = atomicAdd(a.tickets + item, 1);
+                    last_flag = old == (int)(c1 - c0);
+                }
+                __syncthreads();
+                if (last_flag) {
+                    __threadfence();
+                    float sum[RPW][VEC];
 #pragma unroll
-                    for (int v = 0; v < VEC; ++v) atomicAdd(dst + v, o[v]);
-                } else {
-                    *reinterpret_cast<float4 *>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+                    for (int i = 0; i < RPW; ++i)
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) sum[i][v] = 0.f;
+                    for (int64_t c = c0; c <= c1; ++c) {
+                        const int sc = item == (int)(sk_lo(c, T, G) / a.nkb) ? 0 : 1;
+                        const float *pp = a.dxpart + ((c * 2 + sc) * RB + warp * RPW) * BT + lane * VEC;
+#pragma unroll
+                        for (int i = 0; i < RPW; ++i) {
+                            const float4 t = __ldcg(reinterpret_cast<const float4 *>(pp + i * BT));
+                            sum[i][0] += t.x;
+                            sum[i][1] += t.y;
+                            sum[i][2] += t.z;
+                            sum[i][3] += t.w;
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < RPW; ++i) store(i, sum[i]);
                 }
             }
         }
@@ -771,46 +837,56 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
     }
     tm_wait_st();
-    if (cur_rb >= 0) dump(cur_rb);
+    if (cur_rb >= 0) dump(cur_rb, job_a, t0 + ntile - job_a - (int)((int64_t)cur_rb * a.nslice * a.nkb));
     tm_fence_before();
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
 }
 
-// zero the dX region (RB rows via rowmap x BT batch columns) of the items cut
-// by a range boundary: block c handles the boundary at the start of CTA c+1
-__global__ void zero_items_kernel(int64_t T, int64_t G, int nkb, int RB, int BT, int64_t nslice,
-                                  const int32_t *__restrict__ rowmap, int64_t nrow, int64_t B, float *__restrict__ dX) {
-    const int64_t lo = sk_lo(blockIdx.x + 1, T, G);
-    if (lo % nkb == 0) return;  // the boundary falls between items
-    const int64_t it = lo / nkb;
-    const int64_t rb = it / nslice, sl = it - rb * nslice;
-    for (int i = threadIdx.x; i < RB * (BT / 4); i += blockDim.x) {
-        const int lr = i / (BT / 4), c4 = (i - lr * (BT / 4)) * 4;
-        const int64_t r = rowmap[rb * RB + lr], b = sl * BT + c4;
-        if (r >= 0 && r < nrow && b < B) *reinterpret_cast<float4 *>(dX + r * B + b) = make_float4(0.f, 0.f, 0.f, 0.f);
+// dW[vidx[e]] = sum over the jobs of e's row block that touched e's column
+// block of part[job][e] (fixed order)
+// grid (tile (rb, kb), chunk of 256 entries): warp 0 finds the jobs that
+// touched kb (one lane per candidate CTA), then each entry sums their rows in
+// job order
+__global__ void __launch_bounds__(256) job_reduce_kernel(int64_t npad, int nrb, int nkb, int RB, int64_t nslice,
+                                                         int64_t G, const int32_t *__restrict__ seg,
+                                                         const float *__restrict__ part,
+                                                         const int32_t *__restrict__ vidx, float *__restrict__ dW) {
+    __shared__ int rows[kMaxJobTab];  // part rows (job indices) that touched this tile, ascending
+    __shared__ int nrows;
+    const int tile = blockIdx.x, rb = tile / nkb, kb = tile - rb * nkb;
+    const int64_t e0 = seg[(int64_t)tile * RB] + (int64_t)blockIdx.y * blockDim.x, e1 = seg[(int64_t)(tile + 1) * RB];
+    if (e0 >= e1) return;
+    const int64_t T = (int64_t)nrb * nslice * nkb;
+    const int64_t base = (int64_t)rb * nslice * nkb, end = base + nslice * nkb;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const int64_t c0 = sk_cta(base, T, G), c1 = sk_cta(end - 1, T, G);
+        int n = 0;
+        for (int64_t cb = c0; cb <= c1; cb += 32) {
+            const int64_t c = cb + lane;
+            bool hit = false;
+            if (c <= c1) {
+                const int64_t a = std::max(sk_lo(c, T, G), base) - base;
+                const int64_t len = std::min(sk_lo(c + 1, T, G), end) - base - a;
+                int64_t d = kb - a % nkb;
+                if (d < 0) d += nkb;
+                hit = len >= nkb || d < len;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, hit);
+            if (hit) rows[n + __popc(m & ((1u << lane) - 1))] = (int)(c - c0);
+            n += __popc(m);
+        }
+        if (lane == 0) nrows = n;
     }
-}
-
-// dW[vidx[e]] = sum over the jobs of e's row block of part[job][e] (fixed order)
-__global__ void job_reduce_kernel(int64_t npad, int nrb, int nkb, int RB, int64_t nslice, int64_t G,
-                                  const int32_t *__restrict__ seg, const float *__restrict__ part,
-                                  const int32_t *__restrict__ vidx, float *__restrict__ dW) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= npad) return;
+    __syncthreads();
+    const int64_t e = e0 + threadIdx.x;
+    if (e >= e1) return;
     const int v = vidx[e];
     if (v < 0) return;
-    // row block of e: entries of rb are [seg[rb*nkb*RB], seg[(rb+1)*nkb*RB])
-    int lo = 0, hi = nrb;  // find the largest rb with seg[rb*nkb*RB] <= e
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (seg[(int64_t)mid * nkb * RB] <= e) lo = mid; else hi = mid;
-    }
-    const int64_t T = (int64_t)nrb * nslice * nkb;
-    const int64_t tl = (int64_t)lo * nslice * nkb;
-    const int64_t nj = sk_cta(tl + nslice * nkb - 1, T, G) - sk_cta(tl, T, G) + 1;
+    const int n = nrows;
     float s = 0.f;
-    for (int64_t j = 0; j < nj; ++j) s += part[j * npad + e];
+    for (int j = 0; j < n; ++j) s += part[(int64_t)rows[j] * npad + e];
     dW[v] = s;
 }
 
@@ -844,7 +920,6 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     constexpr int TRPW = 4, TNW = 32;  // TMEM variant: 32 warps x 4 rows (same 128-row blocks)
     const sp_tiling &t = w->til[1][0];
     const int64_t slices = (B + BT - 1) / BT;
-    if ((int64_t)t.nrb * slices < kNumSMs) return SP_ERR_SHAPE;  // too little parallelism: use the separate kernels
     CUtensorMap tmap{};
     if (!make_tmap_2d(&tmap, dY, t.inner, B, BT, t.KC)) return SP_ERR_SHAPE;
     const size_t tiles = (size_t)2 * (t.KC + 1) * BT * sizeof(float);
@@ -856,31 +931,37 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     // stream-K schedule: one wave of equal tile ranges, each longer than a slice's column blocks
     const int64_t T = (int64_t)t.nrb * slices * t.nkb;
     const int64_t G = std::min<int64_t>(kNumSMs, T);
-    if (tm && !sk_disabled() && T / G > t.nkb && T < (1LL << 31) && t.max_warp <= (int64_t)kSkDwCols * 32) {
+    if (tm && !sk_disabled() && T < (1LL << 31) && t.max_warp <= (int64_t)kSkDwCols * 32) {
         int64_t maxjobs = 1;
         for (int64_t rb = 0; rb < t.nrb; ++rb) {
             const int64_t tl = rb * slices * t.nkb;
             maxjobs = std::max<int64_t>(maxjobs, sk_cta(tl + slices * t.nkb - 1, T, G) - sk_cta(tl, T, G) + 1);
         }
-        float *part = nullptr;
-        if (cudaMallocAsync((void **)&part, (size_t)(maxjobs * t.npad) * sizeof(float), st) != cudaSuccess) {
+        float *part = nullptr, *dxpart = nullptr;
+        int *tickets = nullptr;
+        const int64_t nitems = (int64_t)t.nrb * slices;
+        if (cudaMallocAsync((void **)&part, (size_t)(maxjobs * t.npad) * sizeof(float), st) != cudaSuccess ||
+            cudaMallocAsync((void **)&dxpart, (size_t)G * 2 * 128 * BT * sizeof(float), st) != cudaSuccess ||
+            cudaMallocAsync((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess) {
             set_error("sp_linear_bwd: scratch allocation failed");
             return SP_ERR_ALLOC;
         }
+        cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
         launch_refresh(t, w->vals, w->nnz, st);  // CSC-tiled weights from vals (through perm)
-        // items (rb, slice) cut by a range boundary: their dX is accumulated by two CTAs
-        if (G > 1) zero_items_kernel<<<(unsigned)(G - 1), 256, 0, st>>>(T, G, t.nkb, 128, BT, slices, t.rowmap, t.rows, B, dX);
         FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, 0, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
-                    0, t.rowmap, slices, t.nrb};
+                    0, t.rowmap, slices, t.nrb, dxpart, tickets};
         auto kern = H ? bwd_fused_sk_kernel<TRPW, TNW, true> : bwd_fused_sk_kernel<TRPW, TNW, false>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<(unsigned)G, TNW * 32, smem, st>>>(a, tmap);
-        job_reduce_kernel<<<(unsigned)((t.npad + 255) / 256), 256, 0, st>>>(t.npad, t.nrb, t.nkb, 128, slices, G,
-                                                                          t.seg, part, t.vidx, dW);
-        count_launches(G > 1 ? 3 : 2);
+        job_reduce_kernel<<<dim3((unsigned)(t.nrb * t.nkb), (unsigned)((t.max_tile + 255) / 256)), 256, 0, st>>>(
+            t.npad, t.nrb, t.nkb, 128, slices, G, t.seg, part, t.vidx, dW);
+        count_launches(2);
         cudaFreeAsync(part, st);
+        cudaFreeAsync(dxpart, st);
+        cudaFreeAsync(tickets, st);
         return SP_OK;
     }
+    if ((int64_t)t.nrb * slices < kNumSMs) return SP_ERR_SHAPE;  // too little parallelism: use the separate kernels
     int64_t nsplit, spl;
     if (tm) {
         // one wave: the largest per-CTA slice count that keeps nrb * nsplit <= #SMs
@@ -906,7 +987,7 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     }
     launch_refresh(t, w->vals, w->nnz, st);  // CSC-tiled weights from vals (through perm)
     FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, (int)spl, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
-                direct ? 1 : 0, t.rowmap, slices, t.nrb};
+                direct ? 1 : 0, t.rowmap, slices, t.nrb, nullptr, nullptr};
     auto pick = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<dim3((unsigned)t.nrb, (unsigned)nsplit), (tm ? TNW : NW) * 32, smem, st>>>(a, tmap);

@@ -160,6 +160,19 @@ def test_bitwise_determinism_and_batch_invariance(sp):
     assert torch.equal(Y_one[:, 0], outs[0][0][:, 5])
 
 
+def test_fused_backward_bitwise_determinism(sp):
+    """The stream-K fused backward (split items add two gated partials, dW
+    partial rows summed in fixed order) gives bitwise identical results run to run."""
+    c = synth.linear_case(3072, 768, 16384, 0.05, 1.0 / 768, 79)
+    Wg = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))
+    X, dY = _dev(c["X"]), _dev(c["dY"])
+    H = torch.relu(_dev(synth.normal(synth.rng(80), (768, 16384), 1.0)))
+    outs = [sp.sp_linear_bwd(Wg, X, dY, H=H) for _ in range(3)]
+    torch.cuda.synchronize()
+    for o in outs[1:]:
+        assert torch.equal(o[0], outs[0][0]) and torch.equal(o[1], outs[0][1])
+
+
 def test_relu_epilogues(sp):
     c = synth.linear_case(300, 200, 70, 0.1, 1.0 / 200, 88)
     S = oracle.csr_from_mask(c["W"], c["mask"])
