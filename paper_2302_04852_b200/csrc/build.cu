@@ -208,9 +208,10 @@ __global__ void til_max_kernel(int64_t ntiles, int RB, const int32_t *__restrict
     if (threadIdx.x == 0) *out = sh[0];
 }
 
-// max over (row block, warp) of the warp's padded entries summed over all column
-// blocks (rows rb*RB + w*RPW .. +RPW), single block, fixed order.  Bounds the
-// per-warp dW accumulator columns of the TMEM fused backward.
+// max over (row block, warp) of the warp's entry groups (segments walked in
+// groups of 4 entries, a last group may hold 2) summed over all column blocks
+// (rows rb*RB + w*RPW .. +RPW), single block, fixed order.  Bounds the
+// per-warp dW sum columns of the TMEM fused backward (8 groups per column).
 __global__ void til_warp_max_kernel(int nrb, int nkb, int RB, int RPW, const int32_t *__restrict__ seg,
                                     int64_t *__restrict__ out) {
     __shared__ int32_t sh[256];
@@ -221,7 +222,7 @@ __global__ void til_warp_max_kernel(int nrb, int nkb, int RB, int RPW, const int
         int32_t s = 0;
         for (int kb = 0; kb < nkb; ++kb) {
             const int64_t t = ((int64_t)rb * nkb + kb) * RB + (int64_t)wi * RPW;
-            s += seg[t + RPW] - seg[t];
+            for (int r = 0; r < RPW; ++r) s += (seg[t + r + 1] - seg[t + r] + 3) >> 2;
         }
         m = max(m, s);
     }
@@ -432,7 +433,7 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
     for (int o = 0; o < 2; ++o)
         for (int v = 0; v < 2; ++v) {
             w->til[o][v].max_tile = (int32_t)h[o * 2 + v];
-            w->til[o][v].max_warp = h[4 + o * 2 + v];
+            w->til[o][v].max_warp_groups = h[4 + o * 2 + v];
             w->til[o][v].npad = hi[2 * (o * 2 + v)];  // padded entry total
         }
     cudaFreeAsync(info, st);

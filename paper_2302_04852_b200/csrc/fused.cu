@@ -927,11 +927,11 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)(226 * 1024);
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
     // TMEM variant: staged entries and at most kTmCols*32 padded entries per warp
-    const bool tm = sent && !tm_disabled() && t.max_warp <= (int64_t)tm_cols<TNW>() * 32;  // bound of an 8-row warp covers its 4-row halves
+    const bool tm = sent && !tm_disabled() && t.max_warp_groups <= (int64_t)tm_cols<TNW>() * 8;  // 8 groups per TMEM column
     // stream-K schedule: one wave of equal tile ranges, each longer than a slice's column blocks
     const int64_t T = (int64_t)t.nrb * slices * t.nkb;
     const int64_t G = std::min<int64_t>(kNumSMs, T);
-    if (tm && !sk_disabled() && T < (1LL << 31) && t.max_warp <= (int64_t)kSkDwCols * 32) {
+    if (tm && !sk_disabled() && T < (1LL << 31) && t.max_warp_groups <= (int64_t)kSkDwCols * 8) {
         int64_t maxjobs = 1;
         for (int64_t rb = 0; rb < t.nrb; ++rb) {
             const int64_t tl = rb * slices * t.nkb;

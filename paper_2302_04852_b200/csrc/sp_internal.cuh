@@ -38,7 +38,8 @@ struct sp_tiling {
     int2 *ent;      // [nnz + 8] (padded)
     int32_t *vidx;  // [nnz]
     int32_t max_tile;  // max (padded) entries in one (row block, column block) tile
-    int64_t max_warp;  // max (padded) entries of 4 consecutive tiled rows (variant 0; RB/NW rows otherwise) over all column blocks
+    int64_t max_warp_groups;  // max entry groups (4 entries, a last one may hold 2) of 4 consecutive tiled rows
+                              // (variant 0; RB/NW rows otherwise) over all column blocks
     int64_t npad;      // padded entry total (segments padded to kTilPad with weight-0 entries)
     int64_t cap_ent;   // allocated entries
     // nnz-balanced row placement: tiled position -> row (-1 unused) and back;

@@ -274,6 +274,8 @@ def test_conv_shapes(sp, B, IC, OC, H, W, K, pad, d):
     (200, 100, 96, 0.3, False),       # B < 128 -> separate kernels
     (64, 18944, 128, 0.05, True),     # one slice, >= 148 row blocks: dW written directly
     (2048, 256, 256, 0.5, False),     # > 4096 entries per warp: register-slot variant
+    (4096, 4096, 256, 0.05, True),    # cfg4@95% shape: at the TMEM dW-column capacity of the stream-K kernel
+    (3072, 768, 512, 0.05, True),     # cfg2 shape: items cut across many CTAs (last-arriver dX sums)
 ])
 def test_fused_backward(sp, R, C, B, d, gate):
     c = synth.linear_case(R, C, B, d, 1.0 / C, R + C + B)
