@@ -94,6 +94,7 @@ def linear(name, R, C, B, density, wvar, seed, kind="uniform", reps=10, dense_ct
     rec["eff_gflops_fused"] = round(3 * fl / ((t["fwd"] + tf) * 1e-3) / 1e9, 1)
     rec["roofline_us"] = round(roof * 1e6, 2)
     rec["pct_roofline"] = round(100 * roof / (tot_t * 1e-3), 2)
+    rec["pct_roofline_fused"] = round(100 * roof / ((t["fwd"] + tf) * 1e-3), 2)  # fwd + sp_linear_bwd
     rec["pct_fp32_peak"] = round(100 * 3 * fl / (tot_t * 1e-3) / FP32, 2)
     if dense_ctx:  # the paper's "dense counterpart" (P363): cuBLAS fp32, TF32 off, masked W
         torch.backends.cuda.matmul.allow_tf32 = False
