@@ -534,10 +534,13 @@ __device__ __forceinline__ void tm_ld4x2(uint32_t ta, float (&v)[4], uint32_t tb
 // registers that 32 resident warps need.
 constexpr int kSkRv = 0, kSkDx = 16, kSkDw = 32, kSkDwCols = 32;
 
-template <int RPW, int NW, bool GATE>
+// DWONLY: the weight gradient alone (sp_linear_bwd_weight): no dX work, the
+// dW sums get the dX columns too (TMEM columns [16,64): <= 384 groups per warp)
+template <int RPW, int NW, bool GATE, bool DWONLY>
 __global__ void __launch_bounds__(NW * 32, 1)
     bwd_fused_sk_kernel(const FusedArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr int VEC = 4;
+    constexpr int DW0 = DWONLY ? kSkDx : kSkDw, DWC = DWONLY ? 2 * kSkDwCols - 16 : kSkDwCols;
     constexpr int BT = 32 * VEC;
     constexpr int RB = NW * RPW;
     static_assert(NW == 32 && RPW == 4, "TMEM column plan: 8 warps per lane quarter, 4 rows each");
@@ -643,7 +646,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         int c2 = 0, my_e = -1;
         const int ka = ja % a.nkb;
         auto out = [&](int col) {
-            const float val = tm_ld1(tcol + kSkDw + (uint32_t)col);
+            const float val = tm_ld1(tcol + DW0 + (uint32_t)col);
             if (my_e >= 0) P[my_e] = val;
             my_e = -1;
         };
@@ -683,7 +686,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         if (id.rb != cur_rb) {  // new job: clear the dW sums
             if (cur_rb >= 0) dump(cur_rb, job_a, t0 + q - job_a - (int)((int64_t)cur_rb * a.nslice * a.nkb));
             job_a = t0 + q - (int)((int64_t)id.rb * a.nslice * a.nkb);
-            for (int c = 0; c < kSkDwCols; ++c) tm_st1(tcol + kSkDw + (uint32_t)c, 0.f);
+            for (int c = 0; c < DWC; ++c) tm_st1(tcol + DW0 + (uint32_t)c, 0.f);
             cur_rb = id.rb;
         }
         if (q == 0 || id.kb == 0) {  // new item: X rows to TMEM, dX accumulators cleared
@@ -696,7 +699,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
                 const float tv[4] = {t.x, t.y, t.z, t.w};
                 tm_st4(tcol + kSkRv + 4 * i, tv);
-                tm_st4(tcol + kSkDx + 4 * i, z);
+                if constexpr (!DWONLY) tm_st4(tcol + kSkDx + 4 * i, z);
             }
             whole = id.kb == 0;
             // group index of this tile's first group in the slice sequence
@@ -717,7 +720,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         const char *tb = reinterpret_cast<const char *>(smem + buf * buf_sz + BT + lane * VEC);
         const int2 *es = ents + buf * ebuf - ea;
         auto flush = [&](int col) {
-            const uint32_t ta = tcol + kSkDw + (uint32_t)col;
+            const uint32_t ta = tcol + DW0 + (uint32_t)col;
             const float old = tm_ld1(ta);
             tm_st1(ta, old + keep);
             keep = 0.f;
@@ -727,7 +730,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
             const int g0 = __shfl_sync(kFull, sg, m), g1 = __shfl_sync(kFull, sg, m + 1);
             if (g0 == g1) continue;
             float rv[VEC], dx[VEC];
-            tm_ld4x2(tcol + kSkRv + 4 * m, rv, tcol + kSkDx + 4 * m, dx);
+            if constexpr (DWONLY)
+                tm_ld4(tcol + kSkRv + 4 * m, rv);
+            else
+                tm_ld4x2(tcol + kSkRv + 4 * m, rv, tcol + kSkDx + 4 * m, dx);
             for (int e = g0; e < g1; e += 4) {
                 const int4 p01 = ld_entry_pair(es + e, true);
                 const int4 p23 = ld_entry_pair(es + e + 2, true);
@@ -740,7 +746,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 auto entry = [&](int u) {
                     float x[VEC];
                     lds_vec<VEC>(reinterpret_cast<const float *>(tb + off[u]), x);
-                    fma_bcast<VEC>(dx, w[u], x);   // dX  (Eq. 1)
+                    if constexpr (!DWONLY) fma_bcast<VEC>(dx, w[u], x);   // dX  (Eq. 1)
                     p[u] = dot_vec<VEC>(rv, x);    // dW partial (Eq. 2)
                 };
                 if (e + 2 < g1) {
@@ -755,9 +761,12 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 ++cnt;
                 if ((cnt & 7) == 0) flush((cnt >> 3) - 1);
             }
-            tm_st4(tcol + kSkDx + 4 * m, dx);
+            if constexpr (!DWONLY) tm_st4(tcol + kSkDx + 4 * m, dx);
         }
-        if (id.kb == a.nkb - 1 || q == ntile - 1) {  // item done here: partial column, dX rows
+        if ((id.kb == a.nkb - 1 || q == ntile - 1) && DWONLY) {  // item done here: partial column
+            if (cnt & 7) flush(cnt >> 3);
+            tm_wait_st();
+        } else if (id.kb == a.nkb - 1 || q == ntile - 1) {  // item done here: partial column, dX rows
             if (cnt & 7) flush(cnt >> 3);
             tm_wait_st();
             // ReLU' gate and store of dX rows (rb, warp*RPW + i), batch columns bl..bl+3
@@ -912,6 +921,67 @@ bool sk_disabled() {
 
 }  // namespace
 
+// Stream-K launch of the TMEM kernel (fused backward, or dW alone when dX is
+// null).  Returns false when it does not apply (ragged B, staged entries do
+// not fit, too many entry groups per warp for the TMEM columns).
+static bool launch_sk(const sp_weight_s *w, const float *X, const float *dY, const float *H, float *dX, float *dW,
+                      int64_t B, cudaStream_t st) {
+    constexpr int TRPW = 4, TNW = 32, BT = 128;
+    if ((B & 3) != 0 || w->nnz == 0) return false;
+    const sp_tiling &t = w->til[1][0];
+    const bool dwonly = dX == nullptr;
+    const int64_t groups_cap = (int64_t)(dwonly ? 2 * kSkDwCols - 16 : kSkDwCols) * 8;
+    if (t.RB != TRPW * TNW || t.max_warp_groups > groups_cap) return false;
+    const int64_t slices = (B + BT - 1) / BT;
+    const int64_t T = (int64_t)t.nrb * slices * t.nkb;
+    if (T >= (1LL << 31)) return false;
+    const int64_t G = std::min<int64_t>(kNumSMs, T);
+    const size_t tiles = (size_t)2 * (t.KC + 1) * BT * sizeof(float);
+    const int cap = (t.max_tile + 2 + 3) & ~3;
+    const size_t smem = tiles + (size_t)2 * (cap + 2) * sizeof(int2);
+    if (smem > (size_t)(226 * 1024)) return false;
+    CUtensorMap tmap{};
+    if (!make_tmap_2d(&tmap, dY, t.inner, B, BT, t.KC)) return false;
+    int64_t maxjobs = 1;
+    for (int64_t rb = 0; rb < t.nrb; ++rb) {
+        const int64_t tl = rb * slices * t.nkb;
+        maxjobs = std::max<int64_t>(maxjobs, sk_cta(tl + slices * t.nkb - 1, T, G) - sk_cta(tl, T, G) + 1);
+    }
+    float *part = nullptr, *dxpart = nullptr;
+    int *tickets = nullptr;
+    const int64_t nitems = (int64_t)t.nrb * slices;
+    if (cudaMallocAsync((void **)&part, (size_t)(maxjobs * t.npad) * sizeof(float), st) != cudaSuccess) return false;
+    if (!dwonly && (cudaMallocAsync((void **)&dxpart, (size_t)G * 2 * 128 * BT * sizeof(float), st) != cudaSuccess ||
+                    cudaMallocAsync((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)) {
+        cudaFreeAsync(part, st);
+        return false;
+    }
+    if (!dwonly) cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
+    launch_refresh(t, w->vals, w->nnz, st);  // CSC-tiled weights from vals (through perm)
+    FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, 0, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
+                0, t.rowmap, slices, t.nrb, dxpart, tickets};
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<(unsigned)G, TNW * 32, smem, st>>>(a, tmap);
+    };
+    if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true>);
+    else if (H) go(bwd_fused_sk_kernel<TRPW, TNW, true, false>);
+    else go(bwd_fused_sk_kernel<TRPW, TNW, false, false>);
+    job_reduce_kernel<<<dim3((unsigned)(t.nrb * t.nkb), (unsigned)((t.max_tile + 255) / 256)), 256, 0, st>>>(
+        t.npad, t.nrb, t.nkb, 128, slices, G, t.seg, part, t.vidx, dW);
+    count_launches(3);  // refresh, kernel, reduce
+    cudaFreeAsync(part, st);
+    if (!dwonly) {
+        cudaFreeAsync(dxpart, st);
+        cudaFreeAsync(tickets, st);
+    }
+    return true;
+}
+
+bool launch_sddmm_sk(const sp_weight_s *w, const float *X, const float *dY, float *dW, int64_t B, cudaStream_t st) {
+    return !sk_disabled() && launch_sk(w, X, dY, nullptr, nullptr, dW, B, st);
+}
+
 sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY, const float *H, float *dX,
                            float *dW, int64_t B, cudaStream_t st) {
     // fused path: B % 4 == 0, at least one full slice, the big CSC tiling
@@ -928,39 +998,7 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
     // TMEM variant: staged entries and at most kTmCols*32 padded entries per warp
     const bool tm = sent && !tm_disabled() && t.max_warp_groups <= (int64_t)tm_cols<TNW>() * 8;  // 8 groups per TMEM column
-    // stream-K schedule: one wave of equal tile ranges, each longer than a slice's column blocks
-    const int64_t T = (int64_t)t.nrb * slices * t.nkb;
-    const int64_t G = std::min<int64_t>(kNumSMs, T);
-    if (tm && !sk_disabled() && T < (1LL << 31) && t.max_warp_groups <= (int64_t)kSkDwCols * 8) {
-        int64_t maxjobs = 1;
-        for (int64_t rb = 0; rb < t.nrb; ++rb) {
-            const int64_t tl = rb * slices * t.nkb;
-            maxjobs = std::max<int64_t>(maxjobs, sk_cta(tl + slices * t.nkb - 1, T, G) - sk_cta(tl, T, G) + 1);
-        }
-        float *part = nullptr, *dxpart = nullptr;
-        int *tickets = nullptr;
-        const int64_t nitems = (int64_t)t.nrb * slices;
-        if (cudaMallocAsync((void **)&part, (size_t)(maxjobs * t.npad) * sizeof(float), st) != cudaSuccess ||
-            cudaMallocAsync((void **)&dxpart, (size_t)G * 2 * 128 * BT * sizeof(float), st) != cudaSuccess ||
-            cudaMallocAsync((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess) {
-            set_error("sp_linear_bwd: scratch allocation failed");
-            return SP_ERR_ALLOC;
-        }
-        cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
-        launch_refresh(t, w->vals, w->nnz, st);  // CSC-tiled weights from vals (through perm)
-        FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, 0, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
-                    0, t.rowmap, slices, t.nrb, dxpart, tickets};
-        auto kern = H ? bwd_fused_sk_kernel<TRPW, TNW, true> : bwd_fused_sk_kernel<TRPW, TNW, false>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<(unsigned)G, TNW * 32, smem, st>>>(a, tmap);
-        job_reduce_kernel<<<dim3((unsigned)(t.nrb * t.nkb), (unsigned)((t.max_tile + 255) / 256)), 256, 0, st>>>(
-            t.npad, t.nrb, t.nkb, 128, slices, G, t.seg, part, t.vidx, dW);
-        count_launches(2);
-        cudaFreeAsync(part, st);
-        cudaFreeAsync(dxpart, st);
-        cudaFreeAsync(tickets, st);
-        return SP_OK;
-    }
+    if (tm && !sk_disabled() && launch_sk(w, X, dY, H, dX, dW, B, st)) return SP_OK;
     if ((int64_t)t.nrb * slices < kNumSMs) return SP_ERR_SHAPE;  // too little parallelism: use the separate kernels
     int64_t nsplit, spl;
     if (tm) {

@@ -379,6 +379,8 @@ sp_status launch_sddmm(const sp_weight_s *w, const float *X, const float *dY, fl
         launch_sddmm_gather(w, X, dY, dW, B, st);
         return SP_OK;
     }
+    // the stream-K TMEM kernel (fused.cu) in its dW-only mode when it applies
+    if (launch_sddmm_sk(w, X, dY, dW, B, st)) return SP_OK;
     const int orient = w->C > w->R ? 1 : 0;  // stage the smaller feature dimension
     const float *regop = orient ? X : dY;
     const float *smemop = orient ? dY : X;

@@ -153,6 +153,8 @@ void launch_split_reduce(int64_t npad, int nsplit, const float *part, const int3
 // Returns SP_ERR_SHAPE if the fused path does not apply (caller falls back).
 sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY, const float *H, float *dX,
                            float *dW, int64_t B, cudaStream_t st);
+// dW alone through the stream-K TMEM kernel; false if it does not apply
+bool launch_sddmm_sk(const sp_weight_s *w, const float *X, const float *dY, float *dW, int64_t B, cudaStream_t st);
 
 bool launch_conv_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, int64_t Lp, float *out,
                       const int *sh, int ntap, int64_t Wv, int64_t OHv, int64_t OWv, cudaStream_t st);
