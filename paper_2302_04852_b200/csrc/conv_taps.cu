@@ -21,6 +21,15 @@ namespace {
 
 // Host build of one tiling from a row-compressed structure (rows ascending,
 // idx ascending within a row) whose entries carry the CSR slot `slot`.
+// Column block of a tap tiling: the inner dimension (a channel count) split into
+// equal blocks of at most kTilKC[0] (256 -> 2 x 128 rather than 192 + 64, so no
+// tile is mostly zero fill), a multiple of 8 rows.
+static int even_kc(int64_t inner) {
+    const int64_t nk = (inner + kTilKC[0] - 1) / kTilKC[0];
+    const int64_t kc = (inner + nk - 1) / nk;
+    return (int)std::max<int64_t>(8, (kc + 7) & ~7);
+}
+
 sp_status tiling_from_host(int64_t rows, int64_t inner, int RB, int KC, const std::vector<int32_t> &ptr,
                            const std::vector<int32_t> &idx, const std::vector<int32_t> &slot, sp_tiling &t) {
     t.RB = RB;
@@ -104,8 +113,8 @@ sp_status build_conv_taps(sp_weight_s *w, int OC, int IC, int KH, int KW, cudaSt
             }
             p1[ic + 1] = (int32_t)i1.size();
         }
-        sp_status s = tiling_from_host(OC, IC, kTilRB[0], kTilKC[0], p0, i0, s0, w->tap[tp][0]);
-        if (s == SP_OK) s = tiling_from_host(IC, OC, kTilRB[0], kTilKC[0], p1, i1, s1, w->tap[tp][1]);
+        sp_status s = tiling_from_host(OC, IC, kTilRB[0], even_kc(IC), p0, i0, s0, w->tap[tp][0]);
+        if (s == SP_OK) s = tiling_from_host(IC, OC, kTilRB[0], even_kc(OC), p1, i1, s1, w->tap[tp][1]);
         if (s != SP_OK) return s;
         for (int o = 0; o < 2; ++o) {
             const sp_tiling &t = w->tap[tp][o];

@@ -129,6 +129,8 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
 // ---- spmm_sk.cu: stream-K SpMM (B % 4 == 0, big tiling); false if it does not apply
 bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,
                     int epi, cudaStream_t st);
+bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in, int64_t Lp, float *out,
+                         const int *sh, int ntap, int64_t Wv, int64_t OHv, int64_t OWv, cudaStream_t st);
 
 // ---- gather.cu (very sparse / small regime: no shared-memory staging) ----
 bool gather_preferred(const sp_weight_s *w, int orient, int64_t B, bool chunked = false);

@@ -282,6 +282,14 @@ bool spmm_sk_disabled() {
     }();
     return v != 0;
 }
+// SP_CONV_SK=0 keeps the per-item conv grids (A/B measurements)
+bool conv_sk_disabled() {
+    static const int v = [] {
+        const char *e = getenv("SP_CONV_SK");
+        return (e && e[0] == '0') ? 1 : 0;
+    }();
+    return v != 0;
+}
 constexpr int kSmemLimit = 226 * 1024;  // per SM, usable by CTAs (minus static mbarriers)
 
 template <int VEC, int RPW, int NW>
@@ -359,6 +367,7 @@ bool conv_spmm_vec(const sp_weight_s *w, int orient, int64_t B, const float *in,
 // slices when the grid would not fill two waves.
 bool launch_conv_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, int64_t Lp, float *out,
                       const int *sh, int ntap, int64_t Wv, int64_t OHv, int64_t OWv, cudaStream_t st) {
+    if (!conv_sk_disabled() && launch_conv_spmm_sk(w, orient, B, in, Lp, out, sh, ntap, Wv, OHv, OWv, st)) return true;
     const int64_t Nv = OHv * Wv * B;
     if ((int64_t)w->tap[0][orient].nrb * ((Nv + 127) / 128) >= 2 * kNumSMs)
         return conv_spmm_vec<4>(w, orient, B, in, Lp, out, sh, ntap, Wv, OHv, OWv, st);

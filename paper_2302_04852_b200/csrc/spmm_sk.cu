@@ -41,9 +41,16 @@ struct SkArgs {
     const int32_t *rowmap;
     float *part;    // [G][2][RB][BT] raw sums of cut items (slot 0: the CTA's first item, 1: its last)
     int *tickets;   // [nrb * nslice], zero on entry, reset by the finishing CTA
+    // conv (CONV = true): an item's tiles run over (tap t, column block); tap t uses
+    // taps[t]'s tiling and reads the padded input shifted by sh[t] columns; output
+    // column n = (p*Wv + q)*B + b is stored compactly to out[r][p][q][b] when p < OHv, q < OWv
+    int ntap;
+    const TapDev *taps;
+    int sh[kMaxTaps];
+    int64_t Wv, OHv, OWv;
 };
 
-template <int RPW, int NW, int EPI>
+template <int RPW, int NW, int EPI, bool CONV>
 __global__ void __launch_bounds__(NW * 32, 1)
     spmm_sk_kernel(const SkArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr int VEC = 4;
@@ -57,13 +64,14 @@ __global__ void __launch_bounds__(NW * 32, 1)
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t B = a.B;
-    const int64_t T = (int64_t)a.nrb * a.nslice * a.nkb, G = gridDim.x;
+    const int tpi = CONV ? a.ntap * a.nkb : a.nkb;  // tiles per item
+    const int64_t T = (int64_t)a.nrb * a.nslice * tpi, G = gridDim.x;
     const int t0 = (int)lo_of(blockIdx.x, T, G);  // T < 2^31 (launcher)
     const int ntile = (int)lo_of(blockIdx.x + 1, T, G) - t0;
     const int nsl = (int)a.nslice;
     const size_t tile_sz = (size_t)a.KC * BT;
     const int ebuf = a.cap + 2;
-    const int first_item = t0 / a.nkb;
+    const int first_item = t0 / tpi;
 
     if (threadIdx.x == 0) {
         mbar_init(&full[0], 1);
@@ -75,19 +83,23 @@ __global__ void __launch_bounds__(NW * 32, 1)
     __syncthreads();
 
     struct Tile {
-        int rb, sl, kb;
+        int rb, sl, r;  // r: tile within the item (tap * nkb + kb for conv)
     };
+    auto tap_of = [&](const Tile &id) { return CONV ? id.r / a.nkb : 0; };
+    auto kb_of = [&](const Tile &id) { return CONV ? id.r - (id.r / a.nkb) * a.nkb : id.r; };
+    auto seg_of = [&](const Tile &id) -> const int32_t * { return CONV ? a.taps[tap_of(id)].seg : a.seg; };
+    auto ent_of = [&](const Tile &id) -> const int2 * { return CONV ? a.taps[tap_of(id)].ent : a.ent; };
     auto tile_of = [&](int q) -> Tile {
-        const int t = t0 + q, it = t / a.nkb;
+        const int t = t0 + q, it = t / tpi;
         Tile id;
-        id.kb = t - it * a.nkb;
+        id.r = t - it * tpi;
         id.rb = it / nsl;
         id.sl = it - id.rb * nsl;
         return id;
     };
     auto next_tile = [&](Tile id) -> Tile {
-        if (++id.kb == a.nkb) {
-            id.kb = 0;
+        if (++id.r == tpi) {
+            id.r = 0;
             if (++id.sl == nsl) {
                 id.sl = 0;
                 ++id.rb;
@@ -96,9 +108,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
         return id;
     };
     auto entry_range = [&](const Tile &id, int &e0, int &e1) {
-        const int64_t tb = ((int64_t)id.rb * a.nkb + id.kb) * RB;
-        e0 = __ldg(a.seg + tb) & ~1;
-        e1 = __ldg(a.seg + tb + RB);
+        const int64_t tb = ((int64_t)id.rb * a.nkb + kb_of(id)) * RB;
+        const int32_t *sgp = seg_of(id);
+        e0 = __ldg(sgp + tb) & ~1;
+        e1 = __ldg(sgp + tb + RB);
     };
     auto issue = [&](int q, int buf) {
         const Tile id = tile_of(q);
@@ -106,20 +119,30 @@ __global__ void __launch_bounds__(NW * 32, 1)
         entry_range(id, e0, e1);
         const unsigned eb = (unsigned)(((e1 - e0) * 8 + 15) & ~15);
         mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
-        tma_load_2d(smem + buf * tile_sz, &tmap, id.sl * BT, id.kb * a.KC, &full[buf]);
-        if (eb) tma_load_1d(ents + buf * ebuf, a.ent + e0, eb, &full[buf]);
+        tma_load_2d(smem + buf * tile_sz, &tmap, id.sl * BT + (CONV ? a.sh[tap_of(id)] : 0), kb_of(id) * a.KC,
+                    &full[buf]);
+        if (eb) tma_load_1d(ents + buf * ebuf, ent_of(id) + e0, eb, &full[buf]);
     };
     if (threadIdx.x == 0) {
         if (ntile > 0) issue(0, 0);
         if (ntile > 1) issue(1, 1);
     }
     auto seg_bounds = [&](const Tile &id) -> int {
-        const int32_t *segw = a.seg + ((int64_t)id.rb * a.nkb + id.kb) * RB + warp * RPW;
+        const int32_t *segw = seg_of(id) + ((int64_t)id.rb * a.nkb + kb_of(id)) * RB + warp * RPW;
         return lane <= RPW ? __ldg(segw + lane) : 0;
     };
     // epilogue of rows (rb, lr = warp*RPW + i) for batch columns bl..bl+3
     auto store = [&](int rb, int i, int64_t bl, const float (&v)[VEC]) {
         const int64_t tpos = (int64_t)rb * RB + warp * RPW + i;
+        if constexpr (CONV) {  // compact store of the valid output columns (tap tilings: identity rows)
+            if (tpos >= a.rows) return;
+            const int64_t pq = bl / B, b = bl - pq * B;
+            const int64_t qq = pq % a.Wv, pp = pq / a.Wv;
+            if (pp >= a.OHv || qq >= a.OWv) return;
+            float *dst = a.out + tpos * (a.OHv * a.OWv * B) + (pp * a.OWv + qq) * B + b;
+            *reinterpret_cast<float4 *>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+            return;
+        }
         const int64_t r = a.rowmap ? (int64_t)__ldg(a.rowmap + tpos) : tpos;
         if (r < 0 || r >= a.rows || bl >= B) return;
         float o[VEC];
@@ -134,18 +157,18 @@ __global__ void __launch_bounds__(NW * 32, 1)
     };
 
     float acc[RPW][VEC];
-    int kb_first = 0;
+    int r_first = 0;
     Tile nid = tile_of(0);
     int sgn = ntile > 0 ? seg_bounds(nid) : 0;
     for (int q = 0; q < ntile; ++q) {
         const Tile id = nid;
         const int buf = q & 1;
-        if (q == 0 || id.kb == 0) {  // new item
+        if (q == 0 || id.r == 0) {  // new item
 #pragma unroll
             for (int i = 0; i < RPW; ++i)
 #pragma unroll
                 for (int v = 0; v < VEC; ++v) acc[i][v] = 0.f;
-            kb_first = id.kb;
+            r_first = id.r;
         }
         const int sg = sgn;
         nid = next_tile(id);
@@ -188,11 +211,11 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 if (q + 2 < ntile) issue(q + 2, buf);
             }
         }
-        if (id.kb != a.nkb - 1 && q != ntile - 1) continue;
+        if (id.r != tpi - 1 && q != ntile - 1) continue;
 
         // ---- this CTA's part of item (rb, sl) is done
         const int64_t bl = (int64_t)id.sl * BT + lane * VEC;
-        if (kb_first == 0 && id.kb == a.nkb - 1) {  // whole item: store directly
+        if (r_first == 0 && id.r == tpi - 1) {  // whole item: store directly
 #pragma unroll
             for (int i = 0; i < RPW; ++i) store(id.rb, i, bl, acc[i]);
             continue;
@@ -205,7 +228,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
             *reinterpret_cast<float4 *>(mine + i * BT) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
         __threadfence();
         __syncthreads();
-        const int64_t c0 = cta_of((int64_t)item * a.nkb, T, G), c1 = cta_of((int64_t)item * a.nkb + a.nkb - 1, T, G);
+        const int64_t c0 = cta_of((int64_t)item * tpi, T, G), c1 = cta_of((int64_t)item * tpi + tpi - 1, T, G);
         if (threadIdx.x == 0) {
             const int old = atomicAdd(a.tickets + item, 1);
             last_flag = old == (int)(c1 - c0);
@@ -221,7 +244,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
             for (int v = 0; v < VEC; ++v) sum[i][v] = 0.f;
         for (int64_t c = c0; c <= c1; ++c) {
-            const int s = item == (int)(lo_of(c, T, G) / a.nkb) ? 0 : 1;
+            const int s = item == (int)(lo_of(c, T, G) / tpi) ? 0 : 1;
             const float *pp = a.part + ((c * 2 + s) * RB + warp * RPW) * BT + lane * VEC;
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
@@ -263,14 +286,54 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
         return false;
     cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
     launch_refresh(t, w->vals, w->nnz, st);
-    SkArgs a{t.rows, B, nslice, t.KC, t.nkb, t.nrb, cap, t.seg, t.ent, out, gate, t.rowmap, part, tickets};
+    SkArgs a{t.rows, B, nslice, t.KC, t.nkb, t.nrb, cap, t.seg, t.ent, out, gate, t.rowmap, part, tickets,
+             0, nullptr, {}, 0, 0, 0};
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<(unsigned)G, NW * 32, smem, st>>>(a, tmap);
     };
-    if (epi == EPI_RELU) go(spmm_sk_kernel<RPW, NW, EPI_RELU>);
-    else if (epi == EPI_GATE) go(spmm_sk_kernel<RPW, NW, EPI_GATE>);
-    else go(spmm_sk_kernel<RPW, NW, EPI_NONE>);
+    if (epi == EPI_RELU) go(spmm_sk_kernel<RPW, NW, EPI_RELU, false>);
+    else if (epi == EPI_GATE) go(spmm_sk_kernel<RPW, NW, EPI_GATE, false>);
+    else go(spmm_sk_kernel<RPW, NW, EPI_NONE, false>);
+    count_launches(1);
+    cudaFreeAsync(part, st);
+    cudaFreeAsync(tickets, st);
+    return true;
+}
+
+// Conv products (see conv.cu) through the stream-K schedule: in = padded
+// activation [inner x Lp], taps[t] tilings of orientation `orient`, shift sh[t]
+// columns; virtual output columns Nv = OHv * Wv * B stored compactly.
+bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in, int64_t Lp, float *out,
+                         const int *sh, int ntap, int64_t Wv, int64_t OHv, int64_t OWv, cudaStream_t st) {
+    constexpr int RPW = 4, NW = 32, BT = 128;
+    const sp_tiling &t0 = w->tap[0][orient];
+    if ((B & 3) != 0 || w->nnz == 0 || t0.RB != RPW * NW) return false;
+    const int64_t Nv = OHv * Wv * B;
+    const int64_t nslice = (Nv + BT - 1) / BT;
+    const int64_t T = (int64_t)t0.nrb * nslice * ntap * t0.nkb;
+    if (T >= (1LL << 31)) return false;
+    const int64_t G = std::min<int64_t>(kNumSMs, T);
+    int mx = 0;
+    for (int t = 0; t < ntap; ++t) mx = std::max(mx, w->tap[t][orient].max_tile);
+    const int cap = (mx + 2 + 3) & ~3;
+    const size_t smem = (size_t)2 * t0.KC * BT * sizeof(float) + (size_t)2 * (cap + 2) * sizeof(int2);
+    if (smem > (size_t)(226 * 1024)) return false;
+    CUtensorMap tmap{};
+    if (!make_tmap_2d(&tmap, in, t0.inner, Lp, BT, t0.KC)) return false;
+    const int64_t nitems = (int64_t)t0.nrb * nslice;
+    float *part = nullptr;
+    int *tickets = nullptr;
+    if (cudaMallocAsync((void **)&part, (size_t)G * 2 * 128 * BT * sizeof(float), st) != cudaSuccess ||
+        cudaMallocAsync((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)
+        return false;
+    cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
+    SkArgs a{t0.rows, B, nslice, t0.KC, t0.nkb, t0.nrb, cap, nullptr, nullptr, out, nullptr, nullptr, part, tickets,
+             ntap, w->tapdev + orient * kMaxTaps, {}, Wv, OHv, OWv};
+    for (int t = 0; t < ntap; ++t) a.sh[t] = sh[t];
+    auto kern = spmm_sk_kernel<RPW, NW, EPI_NONE, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<(unsigned)G, NW * 32, smem, st>>>(a, tmap);
     count_launches(1);
     cudaFreeAsync(part, st);
     cudaFreeAsync(tickets, st);
