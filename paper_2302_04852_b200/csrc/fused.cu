@@ -536,7 +536,7 @@ constexpr int kSkRv = 0, kSkDx = 16, kSkDw = 32, kSkDwCols = 32;
 
 // DWONLY: the weight gradient alone (sp_linear_bwd_weight): no dX work, the
 // dW sums get the dX columns too (TMEM columns [16,64): <= 384 groups per warp)
-template <int RPW, int NW, bool GATE, bool DWONLY>
+template <int RPW, int NW, bool GATE, bool DWONLY, int NBUF>
 __global__ void __launch_bounds__(NW * 32, 1)
     bwd_fused_sk_kernel(const FusedArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr int VEC = 4;
@@ -545,11 +545,11 @@ __global__ void __launch_bounds__(NW * 32, 1)
     constexpr int RB = NW * RPW;
     static_assert(NW == 32 && RPW == 4, "TMEM column plan: 8 warps per lane quarter, 4 rows each");
     extern __shared__ __align__(128) float smem[];
-    __shared__ uint64_t full[2];
-    __shared__ int released[2];  // warps done with each buffer (the last one refills it)
+    __shared__ uint64_t full[NBUF];
+    __shared__ int released[NBUF];  // warps done with each buffer (the last one refills it)
     __shared__ uint32_t tmem_base;
     __shared__ int last_flag;
-    int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * (a.KC + 1) * BT);
+    int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)NBUF * (a.KC + 1) * BT);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t B = a.B;
@@ -568,16 +568,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     if (threadIdx.x == 32) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-        released[0] = 0;
-        released[1] = 0;
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&full[b], 1);
+            released[b] = 0;
+        }
         fence_mbar_init();
     }
-    for (int i = threadIdx.x; i < BT; i += NW * 32) {
-        smem[i] = 0.f;
-        smem[buf_sz + i] = 0.f;
-    }
+    for (int i = threadIdx.x; i < NBUF * BT; i += NW * 32) smem[(i / BT) * buf_sz + i % BT] = 0.f;  // zero rows
     tm_fence_before();
     __syncthreads();
     tm_fence_after();
@@ -618,10 +615,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
         tma_load_2d(smem + buf * buf_sz + BT, &tmap, id.sl * BT, id.kb * a.KC, &full[buf]);
         if (eb) tma_load_1d(ents + buf * ebuf, a.ent + e0, eb, &full[buf]);
     };
-    if (threadIdx.x == 0) {
-        if (ntile > 0) issue(0, 0);
-        if (ntile > 1) issue(1, 1);
-    }
+    if (threadIdx.x == 0)
+        for (int b = 0; b < NBUF && b < ntile; ++b) issue(b, b);
     // this warp's segment bounds of (rb, kb): lane l <= RPW holds the l-th
     auto segw_of = [&](int rb, int kb) -> const int32_t * {
         return a.seg + ((int64_t)rb * a.nkb + kb) * RB + warp * RPW;
@@ -680,7 +675,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     int sgn = ntile > 0 ? seg_bounds(nid) : 0;
     for (int q = 0; q < ntile; ++q) {
         const Tile id = nid;
-        const int buf = q & 1;
+        const int buf = q % NBUF;
         const int64_t r_base = (int64_t)id.rb * RB + warp * RPW;
         const int64_t bl = (int64_t)id.sl * BT + lane * VEC;
         if (id.rb != cur_rb) {  // new job: clear the dW sums
@@ -714,7 +709,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         const int sg = sgn;
         nid = next_tile(id);
         if (q + 1 < ntile) sgn = seg_bounds(nid);
-        mbar_wait(&full[buf], (q >> 1) & 1);
+        mbar_wait(&full[buf], (q / NBUF) & 1);
         int ea, e1t;
         entry_range(id, ea, e1t);
         const char *tb = reinterpret_cast<const char *>(smem + buf * buf_sz + BT + lane * VEC);
@@ -841,7 +836,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
             if (atomicAdd(&released[buf], 1) == NW - 1) {
                 released[buf] = 0;
                 __threadfence_block();
-                if (q + 2 < ntile) issue(q + 2, buf);
+                if (q + NBUF < ntile) issue(q + NBUF, buf);
             }
         }
     }
@@ -936,9 +931,11 @@ static bool launch_sk(const sp_weight_s *w, const float *X, const float *dY, con
     const int64_t T = (int64_t)t.nrb * slices * t.nkb;
     if (T >= (1LL << 31)) return false;
     const int64_t G = std::min<int64_t>(kNumSMs, T);
-    const size_t tiles = (size_t)2 * (t.KC + 1) * BT * sizeof(float);
     const int cap = (t.max_tile + 2 + 3) & ~3;
-    const size_t smem = tiles + (size_t)2 * (cap + 2) * sizeof(int2);
+    // three stages when they fit (drifting warps wait less for the next tile), else two
+    const size_t stage = (size_t)(t.KC + 1) * BT * sizeof(float) + (size_t)(cap + 2) * sizeof(int2);
+    const int nbuf = 3 * stage <= (size_t)(226 * 1024) ? 3 : 2;
+    const size_t smem = nbuf * stage;
     if (smem > (size_t)(226 * 1024)) return false;
     CUtensorMap tmap{};
     if (!make_tmap_2d(&tmap, dY, t.inner, B, BT, t.KC)) return false;
@@ -964,9 +961,15 @@ static bool launch_sk(const sp_weight_s *w, const float *X, const float *dY, con
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<(unsigned)G, TNW * 32, smem, st>>>(a, tmap);
     };
-    if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true>);
-    else if (H) go(bwd_fused_sk_kernel<TRPW, TNW, true, false>);
-    else go(bwd_fused_sk_kernel<TRPW, TNW, false, false>);
+    if (nbuf == 3) {
+        if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, 3>);
+        else if (H) go(bwd_fused_sk_kernel<TRPW, TNW, true, false, 3>);
+        else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 3>);
+    } else {
+        if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, 2>);
+        else if (H) go(bwd_fused_sk_kernel<TRPW, TNW, true, false, 2>);
+        else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 2>);
+    }
     job_reduce_kernel<<<dim3((unsigned)(t.nrb * t.nkb), (unsigned)((t.max_tile + 255) / 256)), 256, 0, st>>>(
         t.npad, t.nrb, t.nkb, 128, slices, G, t.seg, part, t.vidx, dW);
     count_launches(3);  // refresh, kernel, reduce
