@@ -396,7 +396,7 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
             const int64_t cap = w->nnz + (kTilPad - 1) * std::min<int64_t>(nseg, w->nnz) + 8;
             t.cap_ent = cap;
             int32_t *cnt = nullptr;
-            if (dmalloc(&t.seg, nseg + 1) != cudaSuccess || dmalloc(&t.ent, cap) != cudaSuccess ||
+            if (dmalloc(&t.seg, nseg + 8) != cudaSuccess || dmalloc(&t.ent, cap) != cudaSuccess ||
                 dmalloc(&t.vidx, cap) != cudaSuccess ||
                 cudaMallocAsync((void **)&cnt, (size_t)nseg * sizeof(int32_t), st) != cudaSuccess) {
                 cudaFreeAsync(info, st);
@@ -412,6 +412,7 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
                 cudaMemcpy(t.rowmap, rowmap.data(), (size_t)t.nrb * t.RB * sizeof(int32_t), cudaMemcpyHostToDevice);
             }
             cudaMemsetAsync(cnt, 0, (size_t)nseg * sizeof(int32_t), st);
+            cudaMemsetAsync(t.seg + nseg + 1, 0, 7 * sizeof(int32_t), st);  // slack for 16-byte bulk copies of bounds
             cudaMemsetAsync(t.ent, 0, (size_t)cap * sizeof(int2), st);
             cudaMemsetAsync(t.vidx, 0xff, (size_t)cap * sizeof(int32_t), st);  // -1: no slot
             const int64_t nt = rows * t.nkb;
