@@ -188,6 +188,17 @@ sp_status sp_conv2d_bwd_input(sp_weight_t W, const sp_conv_geom *g, const float 
 sp_status sp_conv2d_bwd_weight(sp_weight_t W, const sp_conv_geom *g, const float *X,
                                const float *dY, float *dW, sp_stream_t stream);
 
+/* Both conv backward products in one pass over the nonzeros: the paper's
+ * Algorithm 2 (P297-P347, readings C5) -- per nonzero, one fmadd updates dX
+ * (Eq. 4) and one accumulates dW (Eq. 5) from the same dY value -- driven tap
+ * by tap from the transposed (CSC) index of each tap matrix, so dX needs no
+ * atomics.  Same layouts and results (within rounding) as
+ * sp_conv2d_bwd_input + sp_conv2d_bwd_weight, which it falls back to when
+ * the handle is not a tap-tiled conv handle or B % 4 != 0.  Outputs
+ * overwritten; no host sync. */
+sp_status sp_conv2d_bwd(sp_weight_t W, const sp_conv_geom *g, const float *X, const float *dY,
+                        float *dX, float *dW, sp_stream_t stream);
+
 /* ---------------------------------------------------------------------- */
 /* Step helpers for the data-parallel sparse MLP (north star cfg5)        */
 /* ---------------------------------------------------------------------- */

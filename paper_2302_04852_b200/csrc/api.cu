@@ -304,6 +304,17 @@ sp_status sp_conv2d_bwd_weight(sp_weight_t w, const sp_conv_geom *g, const float
     return check_launch("sp_conv2d_bwd_weight");
 }
 
+sp_status sp_conv2d_bwd(sp_weight_t w, const sp_conv_geom *g, const float *X, const float *dY, float *dX,
+                        float *dW, sp_stream_t stream) {
+    SP_CHECK_HANDLE(w, "sp_conv2d_bwd");
+    sp_status s = check_geom(w, g, "sp_conv2d_bwd");
+    if (s != SP_OK) return s;
+    if (!X || !dY || !dX || (!dW && w->nnz > 0)) return fail(SP_ERR_NULL, "sp_conv2d_bwd: NULL tensor");
+    s = launch_conv_bwd(w, *g, X, dY, dX, dW, S(stream));
+    if (s != SP_OK) return s;
+    return check_launch("sp_conv2d_bwd");
+}
+
 int64_t sp_mse_scratch_floats(int64_t n) { return mse_scratch_floats(n); }
 
 sp_status sp_mse_grad(const float *Y, const float *T, float *dY, float *loss_out, float *scratch, int64_t n,

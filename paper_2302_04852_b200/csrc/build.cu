@@ -459,6 +459,7 @@ void free_tilings(sp_weight_s *w) {
         for (auto &t : o) fr(t);
     for (auto &o : w->tap)
         for (auto &t : o) fr(t);
+    for (auto &t : w->tapf) fr(t);
     if (w->tapdev) cudaFree(w->tapdev);
     w->tapdev = nullptr;
 }

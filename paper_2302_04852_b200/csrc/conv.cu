@@ -360,6 +360,40 @@ void launch_conv_bwd_input(const sp_weight_s *w, const sp_conv_geom &cg, const f
     else go(conv_dx_kernel<4, QC>, 4);
 }
 
+// Both conv backward products in one pass (Alg. 2's single pass by taps):
+// dY padded for the transposed conv, X laid out in dX's virtual columns (row
+// width Wq, zeros beyond W).  Falls back to the separate products.
+static bool conv_bwd_sk(const sp_weight_s *w, const Geo &g, const float *X, const float *dY, float *dX, float *dW,
+                        cudaStream_t st) {
+    if (!tap_path(w, g)) return false;
+    const int ph = g.KH - 1 - g.pad, pw = g.KW - 1 - g.pad;
+    const int Hq = g.OH + 2 * ph, Wq = g.OW + 2 * pw;
+    const int64_t Lq = (int64_t)Hq * Wq * g.B, Nv = (int64_t)g.H * Wq * g.B;
+    float *Dp = nullptr, *Xv = nullptr;
+    if (cudaMallocAsync((void **)&Dp, (size_t)(g.OC * Lq) * sizeof(float), st) != cudaSuccess) return false;
+    if (cudaMallocAsync((void **)&Xv, (size_t)(g.IC * Nv) * sizeof(float), st) != cudaSuccess) {
+        cudaFreeAsync(Dp, st);
+        return false;
+    }
+    launch_pad(g.OC, g.OH, g.OW, Hq, Wq, ph, pw, g.B, dY, Dp, st);
+    launch_pad(g.IC, g.H, g.W, g.H, Wq, 0, 0, g.B, X, Xv, st);
+    int sh[kMaxTaps];
+    for (int x = 0; x < g.KH; ++x)
+        for (int y = 0; y < g.KW; ++y) sh[x * g.KW + y] = ((g.KH - 1 - x) * Wq + (g.KW - 1 - y)) * g.B;
+    const bool ok = launch_conv_bwd_sk(w, Dp, Lq, Xv, Nv, dX, dW, sh, g.KH * g.KW, g.B, Wq, g.H, g.W, st);
+    cudaFreeAsync(Dp, st);
+    cudaFreeAsync(Xv, st);
+    return ok;
+}
+
+sp_status launch_conv_bwd(const sp_weight_s *w, const sp_conv_geom &cg, const float *X, const float *dY, float *dX,
+                          float *dW, cudaStream_t st) {
+    const Geo g = mk(cg);
+    if (w->nnz > 0 && conv_bwd_sk(w, g, X, dY, dX, dW, st)) return SP_OK;
+    launch_conv_bwd_input(w, cg, dY, dX, st);
+    return launch_conv_bwd_weight(w, cg, X, dY, dW, st);
+}
+
 sp_status launch_conv_bwd_weight(const sp_weight_s *w, const sp_conv_geom &cg, const float *X,
                                  const float *dY, float *dW, cudaStream_t st) {
     const Geo g = mk(cg);

@@ -89,7 +89,9 @@ sp_status build_conv_taps(sp_weight_s *w, int OC, int IC, int KH, int KW, cudaSt
     std::vector<int32_t> rp(OC + 1), ci(w->nnz);
     cudaMemcpy(rp.data(), w->row_ptr, (OC + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost);
     if (w->nnz) cudaMemcpy(ci.data(), w->col_idx, w->nnz * sizeof(int32_t), cudaMemcpyDeviceToHost);
-    std::vector<TapDev> td(2 * kMaxTaps);
+    std::vector<TapDev> td(3 * kMaxTaps);
+    constexpr int kFusedRB = 64, kFusedRPW = 2;  // fused conv backward: 32 warps x 2 rows
+    std::vector<int64_t> wgroups((IC + kFusedRB - 1) / kFusedRB * (kFusedRB / kFusedRPW), 0);
     for (int tp = 0; tp < KK; ++tp) {
         // rows oc, inner ic  (entries in (oc, ic) order: col_idx ascending)
         std::vector<int32_t> p0(OC + 1, 0), i0, s0;
@@ -115,12 +117,25 @@ sp_status build_conv_taps(sp_weight_s *w, int OC, int IC, int KH, int KW, cudaSt
         }
         sp_status s = tiling_from_host(OC, IC, kTilRB[0], even_kc(IC), p0, i0, s0, w->tap[tp][0]);
         if (s == SP_OK) s = tiling_from_host(IC, OC, kTilRB[0], even_kc(OC), p1, i1, s1, w->tap[tp][1]);
+        if (s == SP_OK) s = tiling_from_host(IC, OC, kFusedRB, even_kc(OC), p1, i1, s1, w->tapf[tp]);
         if (s != SP_OK) return s;
         for (int o = 0; o < 2; ++o) {
             const sp_tiling &t = w->tap[tp][o];
             td[o * kMaxTaps + tp] = TapDev{t.seg, t.ent, t.vidx, t.npad};
         }
+        const sp_tiling &tf = w->tapf[tp];
+        td[2 * kMaxTaps + tp] = TapDev{tf.seg, tf.ent, tf.vidx, tf.npad};
+        // entry groups (4 entries, a tail may hold 2) per warp of 2 rows, summed over taps
+        const int KCf = tf.KC;
+        for (int ic = 0; ic < IC; ++ic) {
+            std::vector<int32_t> cnt(tf.nkb, 0);
+            for (int32_t k = p1[ic]; k < p1[ic + 1]; ++k) cnt[i1[k] / KCf]++;
+            for (int kb = 0; kb < tf.nkb; ++kb)
+                wgroups[(ic / kFusedRB) * (kFusedRB / kFusedRPW) + (ic % kFusedRB) / kFusedRPW] +=
+                    (((cnt[kb] + kTapPad - 1) & ~(kTapPad - 1)) + 3) / 4;
+        }
     }
+    w->tapf_groups = wgroups.empty() ? 0 : *std::max_element(wgroups.begin(), wgroups.end());
     if (cudaMalloc((void **)&w->tapdev, td.size() * sizeof(TapDev)) != cudaSuccess) return SP_ERR_ALLOC;
     cudaMemcpy(w->tapdev, td.data(), td.size() * sizeof(TapDev), cudaMemcpyHostToDevice);
     return SP_OK;

@@ -48,6 +48,17 @@ struct FusedArgs {
     int nrow_blocks;        // stream-K kernel: row blocks of the tiling
     float *dxpart;          // stream-K kernel: [G][2][RB][BT] raw dX parts of cut items
     int *tickets;           // stream-K kernel: [nrow_blocks * nslice], zero on entry
+    // stream-K kernel, conv (CONV = true): the register operand X is the layer input in
+    // dX's virtual column layout (row stride xstride = Nv); an item's tiles run over
+    // (tap t, column block) with taps[t]'s tiling and the staged operand shifted by sh[t]
+    // columns; dW partial index tapbase[t] + entry; dX column n = (p*Wv + q)*Bc + b is
+    // stored compactly to dX[r][p][q][b] when p < OHv, q < OWv
+    int64_t xstride;
+    int ntap;
+    const TapDev *taps;
+    int sh[kMaxTaps];
+    int64_t tapbase[kMaxTaps];
+    int64_t Bc, Wv, OHv, OWv;
 };
 
 template <int RPW, int NW, bool GATE, bool SENT>
@@ -528,22 +539,26 @@ __device__ __forceinline__ void tm_ld4x2(uint32_t ta, float (&v)[4], uint32_t tb
 }
 
 // TMEM columns of one warp (32 warps: 8 per lane quarter, 64 columns each):
-// [0,16) the X rows of its RPW=4 rows (the dW register operand), [16,32) their
-// dX accumulators, [32,64) dW sums (32 per column: <= 1024 padded entries).
-// Keeping the per-row state in TMEM (loaded per row segment) frees the
-// registers that 32 resident warps need.
-constexpr int kSkRv = 0, kSkDx = 16, kSkDw = 32, kSkDwCols = 32;
+// [0, 4*RPW) the X rows of its RPW rows (the dW register operand), [4*RPW,
+// 8*RPW) their dX accumulators, the rest dW sums (8 groups of 4 entries per
+// column).  Keeping the per-row state in TMEM (loaded per row segment) frees
+// the registers that 32 resident warps need.  RPW = 4 (128-row blocks) for
+// linear layers: 32 dW columns (256 groups); RPW = 2 (64-row blocks) for the
+// fused conv backward: 48 columns.  DWONLY drops the dX columns.
+constexpr int kSkDwCols = 32;  // dW columns of the linear (RPW = 4) plan
+template <int RPW, bool DWONLY>
+constexpr int sk_dw0() { return DWONLY ? 4 * RPW : 8 * RPW; }
+template <int RPW, bool DWONLY>
+constexpr int sk_dwcols() { return 64 - sk_dw0<RPW, DWONLY>(); }
 
-// DWONLY: the weight gradient alone (sp_linear_bwd_weight): no dX work, the
-// dW sums get the dX columns too (TMEM columns [16,64): <= 384 groups per warp)
-template <int RPW, int NW, bool GATE, bool DWONLY, int NBUF>
+template <int RPW, int NW, bool GATE, bool DWONLY, int NBUF, bool CONV>
 __global__ void __launch_bounds__(NW * 32, 1)
     bwd_fused_sk_kernel(const FusedArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr int VEC = 4;
-    constexpr int DW0 = DWONLY ? kSkDx : kSkDw, DWC = DWONLY ? 2 * kSkDwCols - 16 : kSkDwCols;
+    constexpr int RV0 = 0, DX0 = 4 * RPW, DW0 = sk_dw0<RPW, DWONLY>(), DWC = sk_dwcols<RPW, DWONLY>();
     constexpr int BT = 32 * VEC;
     constexpr int RB = NW * RPW;
-    static_assert(NW == 32 && RPW == 4, "TMEM column plan: 8 warps per lane quarter, 4 rows each");
+    static_assert(NW == 32 && (RPW == 4 || RPW == 2), "TMEM column plan: 8 warps per lane quarter, 64 columns each");
     extern __shared__ __align__(128) float smem[];
     __shared__ uint64_t full[NBUF];
     __shared__ int released[NBUF];  // warps done with each buffer (the last one refills it)
@@ -552,10 +567,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
     int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)NBUF * (a.KC + 1) * BT);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t B = a.B;
-    const int64_t T = (int64_t)a.nrow_blocks * a.nslice * a.nkb, G = gridDim.x;
+    const int tpi = CONV ? a.ntap * a.nkb : a.nkb;  // tiles per item
+    const int64_t T = (int64_t)a.nrow_blocks * a.nslice * tpi, G = gridDim.x;
     const int t0 = (int)sk_lo(blockIdx.x, T, G);  // T < 2^31 (checked by the launcher)
-    const int first_item = t0 / a.nkb;
+    const int first_item = t0 / tpi;
     const int ntile = (int)sk_lo(blockIdx.x + 1, T, G) - t0;
     const int nsl = (int)a.nslice;
     const size_t tile_sz = (size_t)a.KC * BT;
@@ -581,19 +596,22 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const uint32_t tcol = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 64);
 
     struct Tile {
-        int rb, kb, sl;
+        int rb, sl, r;  // r: tile within the item (tap * nkb + kb for conv)
     };
+    auto tap_of = [&](int r) { return CONV ? r / a.nkb : 0; };
+    auto kb_of = [&](int r) { return CONV ? r - (r / a.nkb) * a.nkb : r; };
+    auto seg_of = [&](int r) -> const int32_t * { return CONV ? a.taps[tap_of(r)].seg : a.seg; };
     auto tile_of = [&](int q) -> Tile {  // 32-bit: used for the first tile and the refills
-        const int t = t0 + q, it = t / a.nkb;
+        const int t = t0 + q, it = t / tpi;
         Tile id;
-        id.kb = t - it * a.nkb;
+        id.r = t - it * tpi;
         id.rb = it / nsl;
         id.sl = it - id.rb * nsl;
         return id;
     };
     auto next_tile = [&](Tile id) -> Tile {
-        if (++id.kb == a.nkb) {
-            id.kb = 0;
+        if (++id.r == tpi) {
+            id.r = 0;
             if (++id.sl == nsl) {
                 id.sl = 0;
                 ++id.rb;
@@ -602,52 +620,54 @@ __global__ void __launch_bounds__(NW * 32, 1)
         return id;
     };
     auto entry_range = [&](const Tile &id, int &e0, int &e1) {
-        const int64_t tb = ((int64_t)id.rb * a.nkb + id.kb) * RB;
-        e0 = __ldg(a.seg + tb) & ~1;
-        e1 = __ldg(a.seg + tb + RB);
+        const int64_t tb = ((int64_t)id.rb * a.nkb + kb_of(id.r)) * RB;
+        const int32_t *sgp = seg_of(id.r);
+        e0 = __ldg(sgp + tb) & ~1;
+        e1 = __ldg(sgp + tb + RB);
     };
     auto issue = [&](int q, int buf) {
         const Tile id = tile_of(q);
         int e0, e1;
         entry_range(id, e0, e1);
         const unsigned eb = (unsigned)(((e1 - e0) * 8 + 15) & ~15);
+        const int2 *ent = CONV ? a.taps[tap_of(id.r)].ent : a.ent;
         mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
-        tma_load_2d(smem + buf * buf_sz + BT, &tmap, id.sl * BT, id.kb * a.KC, &full[buf]);
-        if (eb) tma_load_1d(ents + buf * ebuf, a.ent + e0, eb, &full[buf]);
+        tma_load_2d(smem + buf * buf_sz + BT, &tmap, id.sl * BT + (CONV ? a.sh[tap_of(id.r)] : 0),
+                    kb_of(id.r) * a.KC, &full[buf]);
+        if (eb) tma_load_1d(ents + buf * ebuf, ent + e0, eb, &full[buf]);
     };
     if (threadIdx.x == 0)
         for (int b = 0; b < NBUF && b < ntile; ++b) issue(b, b);
-    // this warp's segment bounds of (rb, kb): lane l <= RPW holds the l-th
-    auto segw_of = [&](int rb, int kb) -> const int32_t * {
-        return a.seg + ((int64_t)rb * a.nkb + kb) * RB + warp * RPW;
+    // this warp's segment bounds of (rb, tile r): lane l <= RPW holds the l-th
+    auto segw_of = [&](int rb, int r) -> const int32_t * {
+        return seg_of(r) + ((int64_t)rb * a.nkb + kb_of(r)) * RB + warp * RPW;
     };
     auto seg_bounds = [&](const Tile &id) -> int {
-        return lane <= RPW ? __ldg(segw_of(id.rb, id.kb) + lane) : 0;
+        return lane <= RPW ? __ldg(segw_of(id.rb, id.r) + lane) : 0;
     };
 
-    // write this job's dW sums (row block rb)
-    // column block kb of row block rb is touched by the job running tiles
-    // [ja, ja + len) of rb (local tile indices, slice-major)
-    auto touched = [&](int kb, int ka, int len) -> bool {  // ka = ja % nkb
-        int d = kb - ka;
-        if (d < 0) d += a.nkb;
-        return len >= a.nkb || d < len;
+    // tile r of an item is touched by the job running item-local tiles
+    // [ja, ja + len) of its row block (ra = ja % tpi)
+    auto touched = [&](int r, int ra, int len) -> bool {
+        int d = r - ra;
+        if (d < 0) d += tpi;
+        return len >= tpi || d < len;
     };
-    // write this job's dW sums (row block rb, local tiles [ja, ja + len)); column
-    // blocks the job never touched are skipped (job_reduce_kernel skips them too)
+    // write this job's dW sums (row block rb, local tiles [ja, ja + len)); tiles the
+    // job never touched are skipped (job_reduce_kernel skips them too)
     auto dump = [&](int rb, int ja, int len) {
-        const int64_t job = blockIdx.x - sk_cta((int64_t)rb * a.nslice * a.nkb, T, G);
+        const int64_t job = blockIdx.x - sk_cta((int64_t)rb * a.nslice * tpi, T, G);
         float *P = a.part + job * a.npad;
         int c2 = 0, my_e = -1;
-        const int ka = ja % a.nkb;
+        const int ra = ja % tpi;
         auto out = [&](int col) {
             const float val = tm_ld1(tcol + DW0 + (uint32_t)col);
             if (my_e >= 0) P[my_e] = val;
             my_e = -1;
         };
-        for (int kb = 0; kb < a.nkb; ++kb) {
-            const int sg = lane <= RPW ? __ldg(segw_of(rb, kb) + lane) : 0;
-            if (!touched(kb, ka, len)) {  // advance the slot sequence past this column block
+        for (int r = 0; r < tpi; ++r) {
+            const int sg = lane <= RPW ? __ldg(segw_of(rb, r) + lane) : 0;
+            if (!touched(r, ra, len)) {  // advance the slot sequence past this tile
                 int gs = 0;
 #pragma unroll
                 for (int m = 0; m < RPW; ++m) gs += (__shfl_sync(kFull, sg, m + 1) - __shfl_sync(kFull, sg, m) + 3) >> 2;
@@ -655,11 +675,12 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 c2 += gs;
                 continue;
             }
+            const int64_t base = CONV ? a.tapbase[tap_of(r)] : 0;
             for (int m = 0; m < RPW; ++m) {
                 const int g0 = __shfl_sync(kFull, sg, m), g1 = __shfl_sync(kFull, sg, m + 1);
                 for (int e = g0; e < g1; e += 4) {
                     const int u = (lane >> 3) & 3;
-                    if ((lane & 7) == (c2 & 7)) my_e = u < g1 - e ? e + u : -1;
+                    if ((lane & 7) == (c2 & 7)) my_e = u < g1 - e ? (int)(base + e + u) : -1;
                     ++c2;
                     if ((c2 & 7) == 0) out((c2 >> 3) - 1);
                 }
@@ -669,8 +690,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
     };
 
     float keep = 0.f;
-    int cnt = 0, cur_rb = -1, job_a = 0;  // job_a: first local tile of the current job in its row block
-    bool whole = true;  // current item started at kb 0 in this CTA
+    int cnt = 0, cur_rb = -1, job_a = 0;  // job_a: first item-local tile of the current job in its row block
+    bool whole = true;  // current item started at its first tile in this CTA
     Tile nid = tile_of(0);
     int sgn = ntile > 0 ? seg_bounds(nid) : 0;
     for (int q = 0; q < ntile; ++q) {
@@ -679,27 +700,27 @@ __global__ void __launch_bounds__(NW * 32, 1)
         const int64_t r_base = (int64_t)id.rb * RB + warp * RPW;
         const int64_t bl = (int64_t)id.sl * BT + lane * VEC;
         if (id.rb != cur_rb) {  // new job: clear the dW sums
-            if (cur_rb >= 0) dump(cur_rb, job_a, t0 + q - job_a - (int)((int64_t)cur_rb * a.nslice * a.nkb));
-            job_a = t0 + q - (int)((int64_t)id.rb * a.nslice * a.nkb);
+            if (cur_rb >= 0) dump(cur_rb, job_a, t0 + q - job_a - (int)((int64_t)cur_rb * a.nslice * tpi));
+            job_a = t0 + q - (int)((int64_t)id.rb * a.nslice * tpi);
             for (int c = 0; c < DWC; ++c) tm_st1(tcol + DW0 + (uint32_t)c, 0.f);
             cur_rb = id.rb;
         }
-        if (q == 0 || id.kb == 0) {  // new item: X rows to TMEM, dX accumulators cleared
+        if (q == 0 || id.r == 0) {  // new item: X rows to TMEM, dX accumulators cleared
             const float z[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
-                const int64_t r = __ldg(a.rowmap + r_base + i);
-                const float4 t = (r >= 0 && r < a.nrow && bl + 4 <= B)
-                                     ? __ldg(reinterpret_cast<const float4 *>(a.X + r * B + bl))
+                const int64_t r = a.rowmap ? (int64_t)__ldg(a.rowmap + r_base + i) : r_base + i;
+                const float4 t = (r >= 0 && r < a.nrow && bl + 4 <= a.xstride)
+                                     ? __ldg(reinterpret_cast<const float4 *>(a.X + r * a.xstride + bl))
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
                 const float tv[4] = {t.x, t.y, t.z, t.w};
-                tm_st4(tcol + kSkRv + 4 * i, tv);
-                if constexpr (!DWONLY) tm_st4(tcol + kSkDx + 4 * i, z);
+                tm_st4(tcol + RV0 + 4 * i, tv);
+                if constexpr (!DWONLY) tm_st4(tcol + DX0 + 4 * i, z);
             }
-            whole = id.kb == 0;
+            whole = id.r == 0;
             // group index of this tile's first group in the slice sequence
             cnt = 0;
-            for (int k = 0; k < id.kb; ++k) {  // groups of 4 per row segment (a last group may hold 2)
+            for (int k = 0; k < id.r; ++k) {  // groups of 4 per row segment (a last group may hold 2)
                 const int32_t *sw = segw_of(id.rb, k);
 #pragma unroll
                 for (int i = 0; i < RPW; ++i) cnt += (__ldg(sw + i + 1) - __ldg(sw + i) + 3) >> 2;
@@ -726,9 +747,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
             if (g0 == g1) continue;
             float rv[VEC], dx[VEC];
             if constexpr (DWONLY)
-                tm_ld4(tcol + kSkRv + 4 * m, rv);
+                tm_ld4(tcol + RV0 + 4 * m, rv);
             else
-                tm_ld4x2(tcol + kSkRv + 4 * m, rv, tcol + kSkDx + 4 * m, dx);
+                tm_ld4x2(tcol + RV0 + 4 * m, rv, tcol + DX0 + 4 * m, dx);
             for (int e = g0; e < g1; e += 4) {
                 const int4 p01 = ld_entry_pair(es + e, true);
                 const int4 p23 = ld_entry_pair(es + e + 2, true);
@@ -741,8 +762,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 auto entry = [&](int u) {
                     float x[VEC];
                     lds_vec<VEC>(reinterpret_cast<const float *>(tb + off[u]), x);
-                    if constexpr (!DWONLY) fma_bcast<VEC>(dx, w[u], x);   // dX  (Eq. 1)
-                    p[u] = dot_vec<VEC>(rv, x);    // dW partial (Eq. 2)
+                    if constexpr (!DWONLY) fma_bcast<VEC>(dx, w[u], x);   // dX  (Eq. 1 / Eq. 4)
+                    p[u] = dot_vec<VEC>(rv, x);    // dW partial (Eq. 2 / Eq. 5)
                 };
                 if (e + 2 < g1) {
 #pragma unroll
@@ -756,32 +777,43 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 ++cnt;
                 if ((cnt & 7) == 0) flush((cnt >> 3) - 1);
             }
-            if constexpr (!DWONLY) tm_st4(tcol + kSkDx + 4 * m, dx);
+            if constexpr (!DWONLY) tm_st4(tcol + DX0 + 4 * m, dx);
         }
-        if ((id.kb == a.nkb - 1 || q == ntile - 1) && DWONLY) {  // item done here: partial column
+        const bool item_end = id.r == tpi - 1 || q == ntile - 1;
+        if (item_end && DWONLY) {  // item done here: partial column
             if (cnt & 7) flush(cnt >> 3);
             tm_wait_st();
-        } else if (id.kb == a.nkb - 1 || q == ntile - 1) {  // item done here: partial column, dX rows
+        } else if (item_end) {  // item done here: partial column, dX rows
             if (cnt & 7) flush(cnt >> 3);
             tm_wait_st();
-            // ReLU' gate and store of dX rows (rb, warp*RPW + i), batch columns bl..bl+3
+            // (ReLU' gate and) store of dX rows (rb, warp*RPW + i), columns bl..bl+3
             auto store = [&](int i, float (&o)[VEC]) {
+                if constexpr (CONV) {  // compact store of the valid positions (tap tilings: identity rows)
+                    const int64_t r = r_base + i;
+                    if (r >= a.nrow || bl >= a.xstride) return;
+                    const int64_t pq = bl / a.Bc, b = bl - pq * a.Bc;
+                    const int64_t qq = pq % a.Wv, pp = pq / a.Wv;
+                    if (pp >= a.OHv || qq >= a.OWv) return;
+                    float *dst = a.dX + r * (a.OHv * a.OWv * a.Bc) + (pp * a.OWv + qq) * a.Bc + b;
+                    *reinterpret_cast<float4 *>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+                    return;
+                }
                 const int64_t r = __ldg(a.rowmap + r_base + i);
-                if (r < 0 || r >= a.nrow || bl >= B) return;
+                if (r < 0 || r >= a.nrow || bl >= a.B) return;
                 if (GATE) {
-                    const float4 hv = __ldg(reinterpret_cast<const float4 *>(a.H + r * B + bl));
+                    const float4 hv = __ldg(reinterpret_cast<const float4 *>(a.H + r * a.B + bl));
                     o[0] = hv.x > 0.f ? o[0] : 0.f;
                     o[1] = hv.y > 0.f ? o[1] : 0.f;
                     o[2] = hv.z > 0.f ? o[2] : 0.f;
                     o[3] = hv.w > 0.f ? o[3] : 0.f;
                 }
-                *reinterpret_cast<float4 *>(a.dX + r * B + bl) = make_float4(o[0], o[1], o[2], o[3]);
+                *reinterpret_cast<float4 *>(a.dX + r * a.B + bl) = make_float4(o[0], o[1], o[2], o[3]);
             };
-            if (whole && id.kb == a.nkb - 1) {  // the whole item ran here
+            if (whole && id.r == tpi - 1) {  // the whole item ran here
 #pragma unroll 1
                 for (int i = 0; i < RPW; ++i) {
                     float o[VEC];
-                    tm_ld4(tcol + kSkDx + 4 * i, o);
+                    tm_ld4(tcol + DX0 + 4 * i, o);
                     store(i, o);
                 }
             } else {
@@ -793,13 +825,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll 1
                 for (int i = 0; i < RPW; ++i) {
                     float o[VEC];
-                    tm_ld4(tcol + kSkDx + 4 * i, o);
+                    tm_ld4(tcol + DX0 + 4 * i, o);
                     *reinterpret_cast<float4 *>(mine + i * BT) = make_float4(o[0], o[1], o[2], o[3]);
                 }
                 __threadfence();
                 __syncthreads();
-                const int64_t c0 = sk_cta((int64_t)item * a.nkb, T, G);
-                const int64_t c1 = sk_cta((int64_t)item * a.nkb + a.nkb - 1, T, G);
+                const int64_t c0 = sk_cta((int64_t)item * tpi, T, G);
+                const int64_t c1 = sk_cta((int64_t)item * tpi + tpi - 1, T, G);
                 if (threadIdx.x == 0) {
                     const int old = atomicAdd(a.tickets + item, 1);
                     last_flag = old == (int)(c1 - c0);
@@ -813,7 +845,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
                         for (int v = 0; v < VEC; ++v) sum[i][v] = 0.f;
                     for (int64_t c = c0; c <= c1; ++c) {
-                        const int sc = item == (int)(sk_lo(c, T, G) / a.nkb) ? 0 : 1;
+                        const int sc = item == (int)(sk_lo(c, T, G) / tpi) ? 0 : 1;
                         const float *pp = a.dxpart + ((c * 2 + sc) * RB + warp * RPW) * BT + lane * VEC;
 #pragma unroll
                         for (int i = 0; i < RPW; ++i) {
@@ -829,7 +861,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 }
             }
         }
-        // release the buffer; the last warp to finish tile q refills it with tile q+2
+        // release the buffer; the last warp to finish tile q refills it with tile q+NBUF
         __syncwarp();
         if (lane == 0) {
             __threadfence_block();
@@ -841,28 +873,39 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
     }
     tm_wait_st();
-    if (cur_rb >= 0) dump(cur_rb, job_a, t0 + ntile - job_a - (int)((int64_t)cur_rb * a.nslice * a.nkb));
+    if (cur_rb >= 0) dump(cur_rb, job_a, t0 + ntile - job_a - (int)((int64_t)cur_rb * a.nslice * tpi));
     tm_fence_before();
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
 }
 
-// dW[vidx[e]] = sum over the jobs of e's row block that touched e's column
-// block of part[job][e] (fixed order)
-// grid (tile (rb, kb), chunk of 256 entries): warp 0 finds the jobs that
-// touched kb (one lane per candidate CTA), then each entry sums their rows in
-// job order
-__global__ void __launch_bounds__(256) job_reduce_kernel(int64_t npad, int nrb, int nkb, int RB, int64_t nslice,
-                                                         int64_t G, const int32_t *__restrict__ seg,
-                                                         const float *__restrict__ part,
-                                                         const int32_t *__restrict__ vidx, float *__restrict__ dW) {
+// dW[vidx[e]] = sum over the jobs of e's row block that touched e's tile of
+// part[job][base + e] (fixed order).  grid (tap * nrb * nkb + rb * nkb + kb,
+// chunk of 256 entries): warp 0 finds the jobs that touched the tile (one lane
+// per candidate CTA), then each entry sums their rows in job order.  Linear
+// layers: ntap = 1, taps = nullptr (seg / vidx of the tiling, base 0).
+struct JobReduceArgs {
+    int64_t npad, nslice, G;
+    int nrb, nkb, RB, ntap;
+    const int32_t *seg, *vidx;  // linear
+    const TapDev *taps;         // conv
+    int64_t tapbase[kMaxTaps];
+    const float *part;
+    float *dW;
+};
+__global__ void __launch_bounds__(256) job_reduce_kernel(const JobReduceArgs a) {
     __shared__ int rows[kMaxJobTab];  // part rows (job indices) that touched this tile, ascending
     __shared__ int nrows;
-    const int tile = blockIdx.x, rb = tile / nkb, kb = tile - rb * nkb;
-    const int64_t e0 = seg[(int64_t)tile * RB] + (int64_t)blockIdx.y * blockDim.x, e1 = seg[(int64_t)(tile + 1) * RB];
+    const int tpb = a.nrb * a.nkb;
+    const int tap = blockIdx.x / tpb, tile = blockIdx.x - tap * tpb, rb = tile / a.nkb, kb = tile - rb * a.nkb;
+    const int32_t *seg = a.taps ? a.taps[tap].seg : a.seg;
+    const int32_t *vidx = a.taps ? a.taps[tap].vidx : a.vidx;
+    const int64_t base_e = a.taps ? a.tapbase[tap] : 0;
+    const int64_t e0 = seg[(int64_t)tile * a.RB] + (int64_t)blockIdx.y * blockDim.x, e1 = seg[(int64_t)(tile + 1) * a.RB];
     if (e0 >= e1) return;
-    const int64_t T = (int64_t)nrb * nslice * nkb;
-    const int64_t base = (int64_t)rb * nslice * nkb, end = base + nslice * nkb;
+    const int tpi = a.ntap * a.nkb, r = tap * a.nkb + kb;
+    const int64_t T = (int64_t)a.nrb * a.nslice * tpi, G = a.G;
+    const int64_t base = (int64_t)rb * a.nslice * tpi, end = base + a.nslice * tpi;
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
         const int64_t c0 = sk_cta(base, T, G), c1 = sk_cta(end - 1, T, G);
@@ -871,11 +914,11 @@ __global__ void __launch_bounds__(256) job_reduce_kernel(int64_t npad, int nrb, 
             const int64_t c = cb + lane;
             bool hit = false;
             if (c <= c1) {
-                const int64_t a = std::max(sk_lo(c, T, G), base) - base;
-                const int64_t len = std::min(sk_lo(c + 1, T, G), end) - base - a;
-                int64_t d = kb - a % nkb;
-                if (d < 0) d += nkb;
-                hit = len >= nkb || d < len;
+                const int64_t ja = std::max(sk_lo(c, T, G), base) - base;
+                const int64_t len = std::min(sk_lo(c + 1, T, G), end) - base - ja;
+                int64_t d = r - ja % tpi;
+                if (d < 0) d += tpi;
+                hit = len >= tpi || d < len;
             }
             const unsigned m = __ballot_sync(0xffffffffu, hit);
             if (hit) rows[n + __popc(m & ((1u << lane) - 1))] = (int)(c - c0);
@@ -890,8 +933,8 @@ __global__ void __launch_bounds__(256) job_reduce_kernel(int64_t npad, int nrb, 
     if (v < 0) return;
     const int n = nrows;
     float s = 0.f;
-    for (int j = 0; j < n; ++j) s += part[(int64_t)rows[j] * npad + e];
-    dW[v] = s;
+    for (int j = 0; j < n; ++j) s += a.part[(int64_t)rows[j] * a.npad + base_e + e];
+    a.dW[v] = s;
 }
 
 constexpr int kNumSMs = 148;
@@ -925,7 +968,7 @@ static bool launch_sk(const sp_weight_s *w, const float *X, const float *dY, con
     if ((B & 3) != 0 || w->nnz == 0) return false;
     const sp_tiling &t = w->til[1][0];
     const bool dwonly = dX == nullptr;
-    const int64_t groups_cap = (int64_t)(dwonly ? 2 * kSkDwCols - 16 : kSkDwCols) * 8;
+    const int64_t groups_cap = (int64_t)(dwonly ? sk_dwcols<4, true>() : sk_dwcols<4, false>()) * 8;
     if (t.RB != TRPW * TNW || t.max_warp_groups > groups_cap) return false;
     const int64_t slices = (B + BT - 1) / BT;
     const int64_t T = (int64_t)t.nrb * slices * t.nkb;
@@ -956,22 +999,22 @@ static bool launch_sk(const sp_weight_s *w, const float *X, const float *dY, con
     if (!dwonly) cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
     launch_refresh(t, w->vals, w->nnz, st);  // CSC-tiled weights from vals (through perm)
     FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, 0, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
-                0, t.rowmap, slices, t.nrb, dxpart, tickets};
+                0, t.rowmap, slices, t.nrb, dxpart, tickets, B, 1, nullptr, {}, {}, B, 0, 0, 0};
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<(unsigned)G, TNW * 32, smem, st>>>(a, tmap);
     };
     if (nbuf == 3) {
-        if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, 3>);
-        else if (H) go(bwd_fused_sk_kernel<TRPW, TNW, true, false, 3>);
-        else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 3>);
+        if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, 3, false>);
+        else if (H) go(bwd_fused_sk_kernel<TRPW, TNW, true, false, 3, false>);
+        else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 3, false>);
     } else {
-        if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, 2>);
-        else if (H) go(bwd_fused_sk_kernel<TRPW, TNW, true, false, 2>);
-        else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 2>);
+        if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, 2, false>);
+        else if (H) go(bwd_fused_sk_kernel<TRPW, TNW, true, false, 2, false>);
+        else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 2, false>);
     }
-    job_reduce_kernel<<<dim3((unsigned)(t.nrb * t.nkb), (unsigned)((t.max_tile + 255) / 256)), 256, 0, st>>>(
-        t.npad, t.nrb, t.nkb, 128, slices, G, t.seg, part, t.vidx, dW);
+    JobReduceArgs ja{t.npad, slices, G, t.nrb, t.nkb, 128, 1, t.seg, t.vidx, nullptr, {}, part, dW};
+    job_reduce_kernel<<<dim3((unsigned)(t.nrb * t.nkb), (unsigned)((t.max_tile + 255) / 256)), 256, 0, st>>>(ja);
     count_launches(3);  // refresh, kernel, reduce
     cudaFreeAsync(part, st);
     if (!dwonly) {
@@ -983,6 +1026,83 @@ static bool launch_sk(const sp_weight_s *w, const float *X, const float *dY, con
 
 bool launch_sddmm_sk(const sp_weight_s *w, const float *X, const float *dY, float *dW, int64_t B, cudaStream_t st) {
     return !sk_disabled() && launch_sk(w, X, dY, nullptr, nullptr, dW, B, st);
+}
+
+// Conv backward by taps through the stream-K TMEM kernel (the paper's Alg. 2
+// single pass, P297-P347, made atomic-free by the CSC-of-taps drive): rows ic
+// of the 64-row tap tilings (tapf), inner oc; Dp = dY padded for the transposed
+// conv [OC x Lq], Xv = X in dX's virtual layout [IC x Nv] (zero beyond column W);
+// dX (compact CHWN, or null for dW alone) and dW at the conv handle's CSR slots.
+bool launch_conv_bwd_sk(const sp_weight_s *w, const float *Dp, int64_t Lq, const float *Xv, int64_t Nv, float *dX,
+                        float *dW, const int *sh, int ntap, int64_t Bc, int64_t Wv, int64_t OHv, int64_t OWv,
+                        cudaStream_t st) {
+    constexpr int TRPW = 2, TNW = 32, BT = 128, RBF = TRPW * TNW;
+    if (sk_disabled() || (Bc & 3) != 0 || w->nnz == 0 || ntap > kMaxTaps) return false;
+    const sp_tiling &t0 = w->tapf[0];
+    if (t0.RB != RBF || t0.seg == nullptr) return false;
+    const bool dwonly = dX == nullptr;
+    const int64_t groups_cap = (int64_t)(dwonly ? sk_dwcols<TRPW, true>() : sk_dwcols<TRPW, false>()) * 8;
+    if (w->tapf_groups > groups_cap) return false;
+    const int64_t slices = (Nv + BT - 1) / BT;
+    const int64_t T = (int64_t)t0.nrb * slices * ntap * t0.nkb;
+    if (T >= (1LL << 31)) return false;
+    const int64_t G = std::min<int64_t>(kNumSMs, T);
+    int mx = 0;
+    int64_t tapbase[kMaxTaps] = {}, tot = 0;
+    for (int t = 0; t < ntap; ++t) {
+        mx = std::max(mx, w->tapf[t].max_tile);
+        tapbase[t] = tot;
+        tot += w->tapf[t].npad;
+    }
+    const int cap = (mx + 2 + 3) & ~3;
+    const size_t stage = (size_t)(t0.KC + 1) * BT * sizeof(float) + (size_t)(cap + 2) * sizeof(int2);
+    const int nbuf = 3 * stage <= (size_t)(226 * 1024) ? 3 : 2;
+    if (nbuf * stage > (size_t)(226 * 1024)) return false;
+    CUtensorMap tmap{};
+    if (!make_tmap_2d(&tmap, Dp, t0.inner, Lq, BT, t0.KC)) return false;
+    int64_t maxjobs = 1;
+    const int64_t per_rb = slices * ntap * t0.nkb;
+    for (int64_t rb = 0; rb < t0.nrb; ++rb)
+        maxjobs = std::max<int64_t>(maxjobs, sk_cta(rb * per_rb + per_rb - 1, T, G) - sk_cta(rb * per_rb, T, G) + 1);
+    float *part = nullptr, *dxpart = nullptr;
+    int *tickets = nullptr;
+    const int64_t nitems = (int64_t)t0.nrb * slices;
+    if (cudaMallocAsync((void **)&part, (size_t)(maxjobs * tot) * sizeof(float), st) != cudaSuccess) return false;
+    if (!dwonly && (cudaMallocAsync((void **)&dxpart, (size_t)G * 2 * RBF * BT * sizeof(float), st) != cudaSuccess ||
+                    cudaMallocAsync((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)) {
+        cudaFreeAsync(part, st);
+        return false;
+    }
+    if (!dwonly) cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
+    launch_refresh_taps(w, 2, ntap, st);  // fused tap tilings' weights from vals
+    FusedArgs a{t0.rows, t0.inner, Nv, t0.KC, t0.nkb, 0, cap, nullptr, nullptr, nullptr, Xv, Dp, nullptr, dX, part,
+                tot, 0, nullptr, slices, t0.nrb, dxpart, tickets, Nv, ntap, w->tapdev + 2 * kMaxTaps, {}, {},
+                Bc, Wv, OHv, OWv};
+    for (int t = 0; t < ntap; ++t) {
+        a.sh[t] = sh[t];
+        a.tapbase[t] = tapbase[t];
+    }
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(nbuf * stage));
+        kern<<<(unsigned)G, TNW * 32, nbuf * stage, st>>>(a, tmap);
+    };
+    if (nbuf == 3) {
+        if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, 3, true>);
+        else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 3, true>);
+    } else {
+        if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, 2, true>);
+        else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 2, true>);
+    }
+    JobReduceArgs ja{tot, slices, G, t0.nrb, t0.nkb, RBF, ntap, nullptr, nullptr, w->tapdev + 2 * kMaxTaps, {}, part, dW};
+    for (int t = 0; t < ntap; ++t) ja.tapbase[t] = tapbase[t];
+    job_reduce_kernel<<<dim3((unsigned)(ntap * t0.nrb * t0.nkb), (unsigned)((mx + 255) / 256)), 256, 0, st>>>(ja);
+    count_launches(3);  // refresh, kernel, reduce
+    cudaFreeAsync(part, st);
+    if (!dwonly) {
+        cudaFreeAsync(dxpart, st);
+        cudaFreeAsync(tickets, st);
+    }
+    return true;
 }
 
 sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY, const float *H, float *dX,
@@ -1028,7 +1148,7 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     }
     launch_refresh(t, w->vals, w->nnz, st);  // CSC-tiled weights from vals (through perm)
     FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, (int)spl, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
-                direct ? 1 : 0, t.rowmap, slices, t.nrb, nullptr, nullptr};
+                direct ? 1 : 0, t.rowmap, slices, t.nrb, nullptr, nullptr, B, 1, nullptr, {}, {}, B, 0, 0, 0};
     auto pick = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<dim3((unsigned)t.nrb, (unsigned)nsplit), (tm ? TNW : NW) * 32, smem, st>>>(a, tmap);

@@ -70,7 +70,12 @@ struct sp_weight_s {
     // [1]: rows ic / inner oc -- whose vidx are slots of THIS handle's CSR.
     int conv_kh, conv_kw;
     sp_tiling tap[kMaxTaps][2];
-    struct TapDev *tapdev;  // device copy of the tap tilings' pointers [2][kMaxTaps]
+    // [2] of the fused conv backward: rows ic / inner oc in 64-row blocks (the
+    // stream-K TMEM kernel with 2 rows per warp); tapf_groups = max entry groups
+    // of one warp's 2 rows over all taps and column blocks
+    sp_tiling tapf[kMaxTaps];
+    int64_t tapf_groups;
+    struct TapDev *tapdev;  // device copy of the tap tilings' pointers [3][kMaxTaps]: orient 0, 1, fused
 };
 
 // Tiling variants (RB rows per CTA, KC inner columns per shared-memory tile).
@@ -155,6 +160,13 @@ void launch_split_reduce(int64_t npad, int nsplit, const float *part, const int3
 // Returns SP_ERR_SHAPE if the fused path does not apply (caller falls back).
 sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY, const float *H, float *dX,
                            float *dW, int64_t B, cudaStream_t st);
+// conv backward by taps through the stream-K TMEM kernel (dX null: dW alone); false if it does not apply
+bool launch_conv_bwd_sk(const sp_weight_s *w, const float *Dp, int64_t Lq, const float *Xv, int64_t Nv, float *dX,
+                        float *dW, const int *sh, int ntap, int64_t Bc, int64_t Wv, int64_t OHv, int64_t OWv,
+                        cudaStream_t st);
+// fused conv backward (dX and dW); falls back to the separate products
+sp_status launch_conv_bwd(const sp_weight_s *w, const sp_conv_geom &g, const float *X, const float *dY, float *dX,
+                          float *dW, cudaStream_t st);
 // dW alone through the stream-K TMEM kernel; false if it does not apply
 bool launch_sddmm_sk(const sp_weight_s *w, const float *X, const float *dY, float *dW, int64_t B, cudaStream_t st);
 

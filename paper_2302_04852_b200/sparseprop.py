@@ -29,6 +29,7 @@ EXPORTS = [
     "sp_linear_bwd_input_relu", "sp_conv2d_fwd", "sp_conv2d_bwd_input", "sp_conv2d_bwd_weight",
     "sp_mse_scratch_floats", "sp_mse_grad", "sp_sgd", "sp_last_error", "sp_version",
     "sp_launch_count", "sp_linear_bwd", "sp_linear_bwd_relu", "sp_weight_create_conv", "sp_weight_gather",
+    "sp_conv2d_bwd",
 ]
 
 
@@ -70,6 +71,7 @@ def lib() -> ct.CDLL:
             "sp_conv2d_fwd": (st, [vp, ct.POINTER(sp_conv_geom), vp, vp, vp]),
             "sp_conv2d_bwd_input": (st, [vp, ct.POINTER(sp_conv_geom), vp, vp, vp]),
             "sp_conv2d_bwd_weight": (st, [vp, ct.POINTER(sp_conv_geom), vp, vp, vp, vp]),
+            "sp_conv2d_bwd": (st, [vp, ct.POINTER(sp_conv_geom), vp, vp, vp, vp, vp]),
             "sp_mse_scratch_floats": (i64, [i64]),
             "sp_mse_grad": (st, [vp, vp, vp, vp, vp, i64, vp]),
             "sp_sgd": (st, [vp, vp, i64, ct.c_float, vp]),
@@ -339,6 +341,22 @@ def sp_conv2d_bwd_input(W: SparseWeight, g: sp_conv_geom, dY: torch.Tensor,
     _check(lib().sp_conv2d_bwd_input(W.handle, ct.byref(g), _dev(dY, torch.float32, "dY"),
                                      _dev(dX, torch.float32, "dX"), _stream(stream)))
     return dX
+
+
+def sp_conv2d_bwd(W: SparseWeight, g: sp_conv_geom, X: torch.Tensor, dY: torch.Tensor,
+                  dX: torch.Tensor | None = None, dW: torch.Tensor | None = None, stream=None):
+    """Both conv backward products in one pass (Alg. 2 single pass): (dX, dW)."""
+    OH, OW = _geo_out(g)
+    if tuple(dY.shape) != (g.C_out, OH, OW, g.B):
+        raise ValueError("dY must be CHWN [C_out][OH][OW][B]")
+    if dX is None:
+        dX = torch.empty(g.C_in, g.H, g.W, g.B, dtype=torch.float32, device=dY.device)
+    if dW is None:
+        dW = torch.empty(W.nnz, dtype=torch.float32, device=X.device)
+    _check(lib().sp_conv2d_bwd(W.handle, ct.byref(g), _dev(X, torch.float32, "X"), _dev(dY, torch.float32, "dY"),
+                               _dev(dX, torch.float32, "dX"), _dev(dW, torch.float32, "dW") if W.nnz else None,
+                               _stream(stream)))
+    return dX, dW
 
 
 def sp_conv2d_bwd_weight(W: SparseWeight, g: sp_conv_geom, X: torch.Tensor, dY: torch.Tensor,

@@ -228,6 +228,12 @@ def check_conv(sp, c, tag):
     rdX, rdW = oracle.conv2d_bwd(F, Xn, dOn, pad)
     _assert_tol(f"{tag} dX", _np(dX), oracle.nchw_to_chwn(rdX))
     _assert_tol(f"{tag} dW", _np(dW), rdW)
+    # both backward products in one pass (Alg. 2 single pass by taps), run twice: bitwise stable
+    fused = [sp.sp_conv2d_bwd(Wg, g, X, dYg) for _ in range(2)]
+    torch.cuda.synchronize()
+    _assert_tol(f"{tag} fused dX", _np(fused[0][0]), oracle.nchw_to_chwn(rdX))
+    _assert_tol(f"{tag} fused dW", _np(fused[0][1]), rdW)
+    assert torch.equal(fused[0][0], fused[1][0]) and torch.equal(fused[0][1], fused[1][1])
     # the handle's CSR over the flattened filter is the paper's (oc, ic, x, y) order
     S = oracle.csr_from_mask(c["W"].reshape(OC, -1), c["mask"].reshape(OC, -1))
     assert np.array_equal(_np(Wg.indices()["col_idx"]), S.col_idx)

@@ -22,7 +22,8 @@ dW = torch.empty(W.nnz, device="cuda")
 res = {}
 for it in range(args.iters):
     for name, f in (("fwd", lambda: sp.sp_conv2d_fwd(W, g, X, Y)), ("dx", lambda: sp.sp_conv2d_bwd_input(W, g, dY, dX)),
-                    ("dw", lambda: sp.sp_conv2d_bwd_weight(W, g, X, dY, dW))):
+                    ("dw", lambda: sp.sp_conv2d_bwd_weight(W, g, X, dY, dW)),
+                    ("bwd_fused", lambda: sp.sp_conv2d_bwd(W, g, X, dY, dX, dW))):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         f()
