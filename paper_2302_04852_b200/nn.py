@@ -75,8 +75,7 @@ class _SparseConvFn(torch.autograd.Function):
     def backward(ctx, gy):
         (x,) = ctx.saved_tensors
         gy = gy.contiguous()
-        dX = sp.sp_conv2d_bwd_input(ctx.W, ctx.g, gy)
-        dW = sp.sp_conv2d_bwd_weight(ctx.W, ctx.g, x, gy)
+        dX, dW = sp.sp_conv2d_bwd(ctx.W, ctx.g, x, gy)  # both products in one pass (Alg. 2)
         return dX, dW, None, None
 
 

@@ -113,7 +113,10 @@ def conv(name, reps=10, **cfg):
     dX = torch.empty_like(X)
     dW = torch.empty(W.nnz, device="cuda")
     t, ta = timed({"fwd": lambda: sp.sp_conv2d_fwd(W, g, X, Y), "dx": lambda: sp.sp_conv2d_bwd_input(W, g, dY, dX),
-                   "dw": lambda: sp.sp_conv2d_bwd_weight(W, g, X, dY, dW)}, reps)
+                   "dw": lambda: sp.sp_conv2d_bwd_weight(W, g, X, dY, dW),
+                   "bwd_fused": lambda: sp.sp_conv2d_bwd(W, g, X, dY, dX, dW)}, reps)
+    tf = t.pop("bwd_fused")
+    ta.pop("bwd_fused")
     # exact useful FMAs: per tap (x, y), valid output rows x cols (C20)
     m = c["mask"].astype(bool)
     OH, OW, H, Wd, pad = c["OH"], c["OW"], c["H"], c["Wd"], c["pad"]
@@ -130,7 +133,10 @@ def conv(name, reps=10, **cfg):
            "l2": "flushed before each timed launch", "timing": "CUDA-graph replay of one call (t_*), direct API call (t_api_*)"}
     rec.update({f"t_{k}_us": round(v * 1e3, 2) for k, v in t.items()})
     rec["t_fwd_bwd_us"] = round(tot_t * 1e3, 2)
+    rec["t_fwd_bwd_fused_us"] = round((t["fwd"] + tf) * 1e3, 2)  # fwd + sp_conv2d_bwd
     rec["t_api_fwd_bwd_us"] = round(sum(ta.values()) * 1e3, 2)
+    rec["eff_gflops_exact_fused"] = round(3 * fl / ((t["fwd"] + tf) * 1e-3) / 1e9, 1)
+    rec["pct_roofline_fused"] = round(100 * sum(max(fl / FP32, byts[k] / HBM) for k in byts) / ((t["fwd"] + tf) * 1e-3), 2)
     rec["eff_gflops_exact"] = round(3 * fl / (tot_t * 1e-3) / 1e9, 1)
     rec["eff_gflops_nominal"] = round(3 * fl_nominal / (tot_t * 1e-3) / 1e9, 1)
     rec["roofline_us"] = round(roof * 1e6, 2)
