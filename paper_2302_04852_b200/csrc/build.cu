@@ -375,18 +375,33 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
     cudaStreamSynchronize(st);
     cudaMemcpy(hptr[0].data(), w->row_ptr, (w->R + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost);
     cudaMemcpy(hptr[1].data(), w->col_ptr, (w->C + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost);
+    // the tilings: [orientation][variant] plus the CSC tilings of the fused
+    // backward's smaller row blocks (64 and 32 rows, 32 warps x 2 / 1 rows)
+    struct Spec {
+        int o, RB, KC, NWbal, RPWgrp;
+        sp_tiling *t;
+    };
+    const Spec specs[] = {{0, kTilRB[0], kTilKC[0], kTilNW[0], 4, &w->til[0][0]},
+                          {0, kTilRB[1], kTilKC[1], kTilNW[1], kTilRB[1] / kTilNW[1], &w->til[0][1]},
+                          {1, kTilRB[0], kTilKC[0], kTilNW[0], 4, &w->til[1][0]},
+                          {1, kTilRB[1], kTilKC[1], kTilNW[1], kTilRB[1] / kTilNW[1], &w->til[1][1]},
+                          {1, 64, kTilKC[0], 32, 2, &w->til_f[0]},
+                          {1, 32, kTilKC[0], 32, 1, &w->til_f[1]}};
+    constexpr int NS = sizeof(specs) / sizeof(specs[0]);
     int64_t *info = nullptr, *mx = nullptr;
-    if (cudaMallocAsync((void **)&info, 8 * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
-    if (cudaMallocAsync((void **)&mx, 8 * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
-    for (int o = 0; o < 2; ++o) {
+    if (cudaMallocAsync((void **)&info, 2 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
+    if (cudaMallocAsync((void **)&mx, 2 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
+    for (int si = 0; si < NS; ++si) {
+        const Spec &sp_ = specs[si];
+        const int o = sp_.o;
         const int64_t rows = o == 0 ? w->R : w->C, inner = o == 0 ? w->C : w->R;
         const int32_t *ptr = o == 0 ? w->row_ptr : w->col_ptr;
         const int32_t *idx = o == 0 ? w->col_idx : w->row_idx;
         const int32_t *slotmap = o == 0 ? nullptr : w->perm;
-        for (int v = 0; v < 2; ++v) {
-            sp_tiling &t = w->til[o][v];
-            t.RB = kTilRB[v];
-            t.KC = kTilKC[v];
+        {
+            sp_tiling &t = *sp_.t;
+            t.RB = sp_.RB;
+            t.KC = sp_.KC;
             t.rows = rows;
             t.inner = inner;
             t.nrb = (int)((rows + t.RB - 1) / t.RB);
@@ -405,7 +420,7 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
             }
             {
                 std::vector<int32_t> rowpos, rowmap;
-                balanced_rows(hptr[o], rows, t.RB, kTilNW[v], rowpos, rowmap);
+                balanced_rows(hptr[o], rows, t.RB, sp_.NWbal, rowpos, rowmap);
                 if (dmalloc(&t.rowpos, rows) != cudaSuccess || dmalloc(&t.rowmap, (int64_t)t.nrb * t.RB) != cudaSuccess)
                     return SP_ERR_ALLOC;
                 cudaMemcpy(t.rowpos, rowpos.data(), rows * sizeof(int32_t), cudaMemcpyHostToDevice);
@@ -418,25 +433,25 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
             const int64_t nt = rows * t.nkb;
             til_count_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, t.nkb, t.KC, t.RB, ptr, idx,
                                                                           t.rowpos, cnt);
-            scan_kernel<<<1, kScanThreads, 0, st>>>(nseg, cnt, t.seg, info + 2 * (o * 2 + v));
+            scan_kernel<<<1, kScanThreads, 0, st>>>(nseg, cnt, t.seg, info + 2 * si);
             til_fill_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, t.nkb, t.KC, t.RB, ptr, idx,
                                                                          slotmap, t.rowpos, t.seg, w->vals, t.ent,
                                                                          t.vidx);
-            til_max_kernel<<<1, 256, 0, st>>>((int64_t)t.nrb * t.nkb, t.RB, t.seg, mx + (o * 2 + v));
-            til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, v == 0 ? 4 : t.RB / kTilNW[v], t.seg, mx + 4 + (o * 2 + v));
+            til_max_kernel<<<1, 256, 0, st>>>((int64_t)t.nrb * t.nkb, t.RB, t.seg, mx + si);
+            til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp, t.seg, mx + NS + si);
             cudaFreeAsync(cnt, st);
         }
     }
-    int64_t h[8], hi[8];
-    cudaMemcpyAsync(h, mx, sizeof(h), cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(hi, info, sizeof(hi), cudaMemcpyDeviceToHost, st);
+    std::vector<int64_t> h(2 * NS), hi(2 * NS);
+    cudaMemcpyAsync(h.data(), mx, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hi.data(), info, hi.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
     const cudaError_t e = cudaStreamSynchronize(st);  // second (last) host sync of sp_weight_create
-    for (int o = 0; o < 2; ++o)
-        for (int v = 0; v < 2; ++v) {
-            w->til[o][v].max_tile = (int32_t)h[o * 2 + v];
-            w->til[o][v].max_warp_groups = h[4 + o * 2 + v];
-            w->til[o][v].npad = hi[2 * (o * 2 + v)];  // padded entry total
-        }
+    for (int si = 0; si < NS; ++si) {
+        sp_tiling &t = *specs[si].t;
+        t.max_tile = (int32_t)h[si];
+        t.max_warp_groups = h[NS + si];
+        t.npad = hi[2 * si];  // padded entry total
+    }
     cudaFreeAsync(info, st);
     cudaFreeAsync(mx, st);
     return (e == cudaSuccess && cudaGetLastError() == cudaSuccess) ? SP_OK : SP_ERR_CUDA;
@@ -460,6 +475,7 @@ void free_tilings(sp_weight_s *w) {
     for (auto &o : w->tap)
         for (auto &t : o) fr(t);
     for (auto &t : w->tapf) fr(t);
+    for (auto &t : w->til_f) fr(t);
     if (w->tapdev) cudaFree(w->tapdev);
     w->tapdev = nullptr;
 }

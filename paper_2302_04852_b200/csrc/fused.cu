@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     constexpr int RV0 = 0, DX0 = 4 * RPW, DW0 = sk_dw0<RPW, DWONLY>(), DWC = sk_dwcols<RPW, DWONLY>();
     constexpr int BT = 32 * VEC;
     constexpr int RB = NW * RPW;
-    static_assert(NW == 32 && (RPW == 4 || RPW == 2), "TMEM column plan: 8 warps per lane quarter, 64 columns each");
+    static_assert(NW == 32 && (RPW == 4 || RPW == 2 || RPW == 1), "TMEM column plan: 8 warps per lane quarter, 64 columns each");
     extern __shared__ __align__(128) float smem[];
     __shared__ uint64_t full[NBUF];
     __shared__ int released[NBUF];  // warps done with each buffer (the last one refills it)
@@ -962,23 +962,17 @@ bool sk_disabled() {
 // Stream-K launch of the TMEM kernel (fused backward, or dW alone when dX is
 // null).  Returns false when it does not apply (ragged B, staged entries do
 // not fit, too many entry groups per warp for the TMEM columns).
-static bool launch_sk(const sp_weight_s *w, const float *X, const float *dY, const float *H, float *dX, float *dW,
-                      int64_t B, cudaStream_t st) {
-    constexpr int TRPW = 4, TNW = 32, BT = 128;
-    if ((B & 3) != 0 || w->nnz == 0) return false;
-    const sp_tiling &t = w->til[1][0];
+template <int TRPW>
+static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float *X, const float *dY, const float *H,
+                          float *dX, float *dW, int64_t B, cudaStream_t st) {
+    constexpr int TNW = 32, BT = 128, RBT = TRPW * TNW;
     const bool dwonly = dX == nullptr;
-    const int64_t groups_cap = (int64_t)(dwonly ? sk_dwcols<4, true>() : sk_dwcols<4, false>()) * 8;
-    if (t.RB != TRPW * TNW || t.max_warp_groups > groups_cap) return false;
     const int64_t slices = (B + BT - 1) / BT;
     const int64_t T = (int64_t)t.nrb * slices * t.nkb;
     if (T >= (1LL << 31)) return false;
     const int64_t G = std::min<int64_t>(kNumSMs, T);
     const int cap = (t.max_tile + 2 + 3) & ~3;
-    // three stages when they fit (drifting warps wait less for the next tile), else two
-    const size_t stage = (size_t)(t.KC + 1) * BT * sizeof(float) + (size_t)(cap + 2) * sizeof(int2);
-    const int nbuf = 3 * stage <= (size_t)(226 * 1024) ? 3 : 2;
-    const size_t smem = nbuf * stage;
+    const size_t smem = 2 * ((size_t)(t.KC + 1) * BT * sizeof(float) + (size_t)(cap + 2) * sizeof(int2));
     if (smem > (size_t)(226 * 1024)) return false;
     CUtensorMap tmap{};
     if (!make_tmap_2d(&tmap, dY, t.inner, B, BT, t.KC)) return false;
@@ -987,11 +981,12 @@ static bool launch_sk(const sp_weight_s *w, const float *X, const float *dY, con
         const int64_t tl = rb * slices * t.nkb;
         maxjobs = std::max<int64_t>(maxjobs, sk_cta(tl + slices * t.nkb - 1, T, G) - sk_cta(tl, T, G) + 1);
     }
+    if (maxjobs > kMaxJobTab) return false;
     float *part = nullptr, *dxpart = nullptr;
     int *tickets = nullptr;
     const int64_t nitems = (int64_t)t.nrb * slices;
     if (cudaMallocAsync((void **)&part, (size_t)(maxjobs * t.npad) * sizeof(float), st) != cudaSuccess) return false;
-    if (!dwonly && (cudaMallocAsync((void **)&dxpart, (size_t)G * 2 * 128 * BT * sizeof(float), st) != cudaSuccess ||
+    if (!dwonly && (cudaMallocAsync((void **)&dxpart, (size_t)G * 2 * RBT * BT * sizeof(float), st) != cudaSuccess ||
                     cudaMallocAsync((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)) {
         cudaFreeAsync(part, st);
         return false;
@@ -1004,16 +999,10 @@ static bool launch_sk(const sp_weight_s *w, const float *X, const float *dY, con
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<(unsigned)G, TNW * 32, smem, st>>>(a, tmap);
     };
-    if (nbuf == 3) {
-        if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, 3, false>);
-        else if (H) go(bwd_fused_sk_kernel<TRPW, TNW, true, false, 3, false>);
-        else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 3, false>);
-    } else {
-        if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, 2, false>);
-        else if (H) go(bwd_fused_sk_kernel<TRPW, TNW, true, false, 2, false>);
-        else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 2, false>);
-    }
-    JobReduceArgs ja{t.npad, slices, G, t.nrb, t.nkb, 128, 1, t.seg, t.vidx, nullptr, {}, part, dW};
+    if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, 2, false>);
+    else if (H) go(bwd_fused_sk_kernel<TRPW, TNW, true, false, 2, false>);
+    else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 2, false>);
+    JobReduceArgs ja{t.npad, slices, G, t.nrb, t.nkb, RBT, 1, t.seg, t.vidx, nullptr, {}, part, dW};
     job_reduce_kernel<<<dim3((unsigned)(t.nrb * t.nkb), (unsigned)((t.max_tile + 255) / 256)), 256, 0, st>>>(ja);
     count_launches(3);  // refresh, kernel, reduce
     cudaFreeAsync(part, st);
@@ -1022,6 +1011,29 @@ static bool launch_sk(const sp_weight_s *w, const float *X, const float *dY, con
         cudaFreeAsync(tickets, st);
     }
     return true;
+}
+
+// Stream-K launch of the TMEM kernel (fused backward, or dW alone when dX is
+// null).  The CSC tiling is the largest row block whose per-warp entry groups
+// fit the TMEM dW columns: 128 rows (4 per warp), else 64 (2), else 32 (1).
+// Returns false when none applies (ragged B, staged entries do not fit, rows
+// too long -- e.g. Zipf rows with thousands of entries).
+static bool launch_sk(const sp_weight_s *w, const float *X, const float *dY, const float *H, float *dX, float *dW,
+                      int64_t B, cudaStream_t st) {
+    if ((B & 3) != 0 || w->nnz == 0) return false;
+    const bool dw = dX == nullptr;
+    auto fits = [&](const sp_tiling &t, int64_t cols) { return t.seg != nullptr && t.max_warp_groups <= cols * 8; };
+    if (fits(w->til[1][0], dw ? sk_dwcols<4, true>() : sk_dwcols<4, false>()) && w->til[1][0].RB == 128 &&
+        launch_sk_rpw<4>(w, w->til[1][0], X, dY, H, dX, dW, B, st))
+        return true;
+    if (dw) return false;  // dW alone: smaller row blocks lose to the tiled SDDMM (more fill per entry)
+    if (fits(w->til_f[0], sk_dwcols<2, false>()) &&
+        launch_sk_rpw<2>(w, w->til_f[0], X, dY, H, dX, dW, B, st))
+        return true;
+    if (fits(w->til_f[1], sk_dwcols<1, false>()) &&
+        launch_sk_rpw<1>(w, w->til_f[1], X, dY, H, dX, dW, B, st))
+        return true;
+    return false;
 }
 
 bool launch_sddmm_sk(const sp_weight_s *w, const float *X, const float *dY, float *dW, int64_t B, cudaStream_t st) {
@@ -1107,7 +1119,9 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const float *Dp, int64_t Lq, const
 
 sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY, const float *H, float *dX,
                            float *dW, int64_t B, cudaStream_t st) {
-    // fused path: B % 4 == 0, at least one full slice, the big CSC tiling
+    // stream-K TMEM kernel (any B % 4 == 0) when the rows fit its TMEM columns
+    if (!tm_disabled() && !sk_disabled() && launch_sk(w, X, dY, H, dX, dW, B, st)) return SP_OK;
+    // slice-split grids: B % 4 == 0, at least one full slice, the big CSC tiling
     if ((B & 3) != 0 || B < 128 || w->nnz == 0) return SP_ERR_SHAPE;
     constexpr int RPW = 8, NW = 16, BT = 128;
     constexpr int TRPW = 4, TNW = 32;  // TMEM variant: 32 warps x 4 rows (same 128-row blocks)
@@ -1121,7 +1135,6 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
     // TMEM variant: staged entries and at most kTmCols*32 padded entries per warp
     const bool tm = sent && !tm_disabled() && t.max_warp_groups <= (int64_t)tm_cols<TNW>() * 8;  // 8 groups per TMEM column
-    if (tm && !sk_disabled() && launch_sk(w, X, dY, H, dX, dW, B, st)) return SP_OK;
     if ((int64_t)t.nrb * slices < kNumSMs) return SP_ERR_SHAPE;  // too little parallelism: use the separate kernels
     int64_t nsplit, spl;
     if (tm) {

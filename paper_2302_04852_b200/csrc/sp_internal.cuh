@@ -65,6 +65,9 @@ struct sp_weight_s {
     int32_t *chunk_ptr;  // [R+1] exclusive scan of ceil(row nnz / 32) (gather SDDMM work list)
     // tilings: [orientation 0 = CSR rows, 1 = CSC columns][variant 0 = big, 1 = small]
     sp_tiling til[2][2];
+    // CSC tilings of the fused backward for dense-ish rows (KC = 192): [0] 64-row
+    // blocks (32 warps x 2 rows), [1] 32-row blocks (32 warps x 1 row)
+    sp_tiling til_f[2];
     // conv handles (sp_weight_create_conv): filter taps and, per tap (x, y),
     // tilings of the OC x IC tap matrix W_xy -- [0]: rows oc / inner ic,
     // [1]: rows ic / inner oc -- whose vidx are slots of THIS handle's CSR.

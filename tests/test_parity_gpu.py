@@ -283,6 +283,8 @@ def test_conv_shapes(sp, B, IC, OC, H, W, K, pad, d):
     (4096, 4096, 256, 0.05, True),    # cfg4@95% shape: at the TMEM dW-column capacity of the stream-K kernel
     (3072, 768, 512, 0.05, True),     # cfg2 shape: items cut across many CTAs (last-arriver dX sums)
     (500, 300, 200, 0.1, True),       # B % 128 != 0 (a partial last slice), ragged row blocks, gated
+    (4096, 1024, 256, 0.1, False),    # long CSC rows: 64-row tiling, 2 rows per warp
+    (4096, 1024, 256, 0.2, True),     # longer rows: 32-row tiling, 1 row per warp
 ])
 def test_fused_backward(sp, R, C, B, d, gate):
     c = synth.linear_case(R, C, B, d, 1.0 / C, R + C + B)
