@@ -969,7 +969,8 @@ static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float 
     const bool dwonly = dX == nullptr;
     const int64_t slices = (B + BT - 1) / BT;
     const int64_t T = (int64_t)t.nrb * slices * t.nkb;
-    if (T >= (1LL << 31)) return false;
+    // tiny problems (a few tiles) go to the separate kernels: the reduce pass would dominate
+    if (T >= (1LL << 31) || T < 32) return false;
     const int64_t G = std::min<int64_t>(kNumSMs, T);
     const int cap = (t.max_tile + 2 + 3) & ~3;
     const size_t smem = 2 * ((size_t)(t.KC + 1) * BT * sizeof(float) + (size_t)(cap + 2) * sizeof(int2));

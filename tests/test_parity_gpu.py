@@ -301,8 +301,10 @@ def test_fused_backward(sp, R, C, B, d, gate):
         refx = refx * (H > 0)
     _assert_tol("fused dX", _np(dX), refx)
     _assert_tol("fused dW", _np(dW), oracle.linear_bwd_weight(S, c["X"], c["dY"], NT))
-    # same arithmetic as the separate kernels: dX bitwise equal to sp_linear_bwd_input
+    # the separate dX kernel does the same products; the stream-K fused pass only
+    # regroups the sums of items cut between CTAs (a + b): agreement to fp32 rounding
     dX2 = sp.sp_linear_bwd_input(Wg, _dev(c["dY"]), H=None if H is None else _dev(H))
     torch.cuda.synchronize()
     if B >= 128 and B % 4 == 0:
-        np.testing.assert_allclose(_np(dX), _np(dX2), rtol=1e-6, atol=1e-6)
+        a, b = _np(dX), _np(dX2)
+        assert np.max(np.abs(a - b)) <= 1e-5 * max(float(np.max(np.abs(b))), 1e-30)
