@@ -155,9 +155,15 @@ sp_status sp_linear_bwd_input_relu(sp_weight_t W, const float *dY, const float *
  *   dW = (dY X^T) restricted to mask  (as sp_linear_bwd_weight)
  * reading each staged dY element once for both products.
  * sp_linear_bwd_relu additionally gates dX by [H > 0] (H: [C x B]).
- * X: [C x B], dY: [R x B], dX: [C x B], dW: [nnz].  Falls back to the two
- * separate kernels when B % 4 != 0, B < 128 or the problem is too small to
- * fill the GPU (same results within the fp32 tolerance). */
+ * X: [C x B], dY: [R x B], dX: [C x B], dW: [nnz].  Stream-K schedule: each
+ * SM runs an equal range of (row block, batch slice, column block) tiles; a
+ * dX block cut between CTAs is finished by the last CTA to arrive, which adds
+ * the raw parts in CTA order, and dW partials are summed in job order, so the
+ * result is bitwise reproducible run to run (it may differ from the separate
+ * kernels by fp32 rounding of those regrouped sums).  Falls back to the two
+ * separate kernels when B % 4 != 0, the problem is tiny (< 32 tiles) or the
+ * rows are too long for the tensor-memory dW columns (same results within the
+ * fp32 tolerance).  Scratch comes from the stream-ordered pool; no host sync. */
 sp_status sp_linear_bwd(sp_weight_t W, const float *X, const float *dY, float *dX, float *dW, int64_t B,
                         sp_stream_t stream);
 sp_status sp_linear_bwd_relu(sp_weight_t W, const float *X, const float *dY, const float *H, float *dX,

@@ -79,7 +79,7 @@ const char *sp_last_error(void) { return g_err.c_str(); }
 
 uint64_t sp_launch_count(void) { return g_launches.load(); }
 
-const char *sp_version(void) { return "libsparseprop 0.1 sm_100a fp32 (CUDA cores, no atomics)"; }
+const char *sp_version(void) { return "libsparseprop 0.2 sm_100a fp32 (CUDA cores, TMEM state, deterministic: no atomic output accumulation)"; }
 
 sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8_t *mask,
                            sp_stream_t stream, sp_weight_t *out) {
