@@ -115,6 +115,38 @@ class SparseMLP:
         self.X[0].copy_(X0, non_blocking=non_blocking)
         self.target.copy_(target, non_blocking=non_blocking)
 
+    # ---- input prefetch: the next step's host -> device copy on a side stream,
+    # overlapped with the current step (double-buffered X0 / target) ----------
+    def prefetch_batch(self, X0: torch.Tensor, target: torch.Tensor):
+        """Start copying the next shard into the staging buffers (CUDA only).
+        The staging buffers last held the input of the step before the current
+        one; the copy stream waits for that step to be done with them."""
+        if not hasattr(self, "_stage"):
+            self._stage = (torch.empty_like(self.X[0]), torch.empty_like(self.target))
+            self._copy_stream = torch.cuda.Stream(device=self.device)
+            self._stage_ready = torch.cuda.Event()
+            self._stage_free = None
+        if self._stage_free is not None:
+            self._copy_stream.wait_event(self._stage_free)
+        with torch.cuda.stream(self._copy_stream):
+            self._stage[0].copy_(X0, non_blocking=True)
+            self._stage[1].copy_(target, non_blocking=True)
+            self._stage_ready.record(self._copy_stream)
+
+    def use_prefetched(self):
+        """Make the prefetched shard this step's input (the current stream waits
+        for its copy); the replaced buffers become the next staging buffers."""
+        torch.cuda.current_stream(self.device).wait_event(self._stage_ready)
+        old_x, old_t = self.X[0], self.target
+        self.X[0], self.target = self._stage
+        self._stage = (old_x, old_t)
+
+    def release_staging(self):
+        """Call after a step: its (now staging) buffers are free once the step ends."""
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        self._stage_free = ev
+
     def forward(self):
         ops = self.ops
         for l, (W1, W2) in enumerate(self.W):
