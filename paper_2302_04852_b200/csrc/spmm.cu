@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
     extern __shared__ __align__(128) float smem[];  // [2][KC][BT] floats, [2][cap+2] int2
     __shared__ uint64_t full[2];
     __shared__ int released[2];  // TMA path: warps done with each buffer (the last one refills it)
-    int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * a.KC * BT);
+    int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * (a.KC + 1) * BT);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int rb = blockIdx.x;
@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
     const int64_t B = a.B;
     const bool vec4 = CONV || a.tma != 0;  // TMA path (B % 4 == 0 and a tensor map)
     const size_t tile_sz = (size_t)a.KC * BT;
+    const size_t buf_sz = tile_sz + BT;  // a zero row (what padding entries read) + the tile
     const int ebuf = a.cap + 2;
     const int ntile = CONV ? a.ntap * a.nkb : a.nkb;
 
@@ -92,6 +93,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
         released[0] = 0;
         released[1] = 0;
         fence_mbar_init();
+    }
+    for (int i = threadIdx.x; i < BT; i += NT) {  // the zero rows in front of the two tiles
+        smem[i] = 0.f;
+        smem[buf_sz + i] = 0.f;
     }
     __syncthreads();
 
@@ -115,7 +120,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
         const unsigned eb = SENT ? (unsigned)(((e1 - e0) * 8 + 15) & ~15) : 0u;
         // the box is always KC x BT floats (OOB rows / columns zero-filled)
         mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
-        tma_load_2d(smem + buf * tile_sz, &tmap, (int)(b0 + (CONV ? a.sh[t] : 0)), (int)k0, &full[buf]);
+        tma_load_2d(smem + buf * buf_sz + BT, &tmap, (int)(b0 + (CONV ? a.sh[t] : 0)), (int)k0, &full[buf]);
         if (eb) tma_load_1d(ents + buf * ebuf, ent_of(t) + e0, eb, &full[buf]);
     };
     if (vec4 && threadIdx.x == 0) {
@@ -157,7 +162,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
             }
         } else {  // ragged B: synchronous staging of this tile (never CONV)
             const int64_t k0 = (int64_t)kb * a.KC;
-            stage_tile<BT, NT>(smem + buf * tile_sz, a.in, k0, (int)std::min<int64_t>(a.KC, a.inner - k0), B, b0,
+            stage_tile<BT, NT>(smem + buf * buf_sz + BT, a.in, k0, (int)std::min<int64_t>(a.KC, a.inner - k0), B, b0,
                                false);
             if constexpr (SENT) {
                 int e1;
@@ -168,7 +173,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
         }
         // tile row byte offsets are stored for 128-float rows; narrower tiles shift
         constexpr int SH = VEC == 4 ? 0 : VEC == 2 ? 1 : 2;
-        const char *tb = reinterpret_cast<const char *>(smem + buf * tile_sz + lane * VEC);
+        const char *tb = reinterpret_cast<const char *>(smem + buf * buf_sz + BT + lane * VEC);
         const int2 *gent = ent_of(tap_of(q));
         const int2 *es = SENT ? ents + buf * ebuf - ea : gent;
 #pragma unroll
@@ -186,12 +191,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
                 float x[4][VEC];
                 if (e + 2 < s1) {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) lds_row_or_zero<VEC, SH>(tb, off[u], x[u]);
+                    for (int u = 0; u < 4; ++u) lds_vec<VEC>(reinterpret_cast<const float *>(tb + (off[u] >> SH)), x[u]);
 #pragma unroll
                     for (int u = 0; u < 4; ++u) fma_bcast<VEC>(acc[i], w[u], x[u]);
                 } else {  // last pair of the segment
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) lds_row_or_zero<VEC, SH>(tb, off[u], x[u]);
+                    for (int u = 0; u < 2; ++u) lds_vec<VEC>(reinterpret_cast<const float *>(tb + (off[u] >> SH)), x[u]);
 #pragma unroll
                     for (int u = 0; u < 2; ++u) fma_bcast<VEC>(acc[i], w[u], x[u]);
                 }
@@ -296,7 +301,7 @@ template <int VEC, int RPW, int NW>
 void launch_cfg(const sp_tiling &t, int64_t B, const float *in, float *out, const float *gate, int epi,
                 cudaStream_t st) {
     constexpr int BT = 32 * VEC;
-    const size_t tiles = (size_t)2 * t.KC * BT * sizeof(float);
+    const size_t tiles = (size_t)2 * (t.KC + 1) * BT * sizeof(float);
     // stage the entries too when both buffers fit next to the activation tiles
     const int cap = (t.max_tile + 2 + 3) & ~3;  // keeps both entry buffers 16-byte aligned
     const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)kSmemLimit / (NW == 8 ? 2 : 1);
@@ -341,7 +346,7 @@ bool conv_spmm_vec(const sp_weight_s *w, int orient, int64_t B, const float *in,
     int mx = 0;
     for (int t = 0; t < ntap; ++t) mx = std::max(mx, w->tap[t][orient].max_tile);
     const int cap = (mx + 2 + 3) & ~3;
-    const size_t tiles = (size_t)2 * t0.KC * BT * sizeof(float);
+    const size_t tiles = (size_t)2 * (t0.KC + 1) * BT * sizeof(float);
     const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)kSmemLimit;
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
     SpmmArgs a{t0.rows, t0.inner, B, t0.KC, t0.nkb, cap, 1, nullptr, nullptr, nullptr, out, nullptr, nullptr,
