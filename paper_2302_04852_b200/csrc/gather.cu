@@ -142,6 +142,9 @@ bool gather_preferred(const sp_weight_s *w, int orient, int64_t B, bool chunked)
     const int64_t rows = orient == 0 ? w->R : w->C;
     const int64_t mx = orient == 0 ? w->max_row_nnz : w->max_col_nnz;
     if (!chunked && (double)mx > 4.0 * (double)w->nnz / (double)rows + 64.0) return false;
+    // tiny products (well under one wave of tiles) are latency bound: one pass
+    // straight from L2 beats staging tiles
+    if ((double)w->nnz * (double)B < 4.0e6) return true;
     const sp_tiling &t = w->til[orient][1];  // the smallest tiling the tiled path would fall back to
     const sp_tiling &t0 = w->til[orient][0];
     const int64_t slices = (B + 127) / 128;
