@@ -276,16 +276,17 @@ bool spmm_nw32() {
     }();
     return v != 0;
 }
-// The stream-K SpMM (spmm_sk.cu) is opt-in (SP_SPMM_SK=1): measured +6-7% on
-// 768-row layers and -3% on 3072-row ones at B=16384, slower at B=512, and its
-// split items change the per-element summation order with B (the per-item
-// grid keeps every output element's order independent of B and of the grid).
-bool spmm_sk_disabled() {
+// The stream-K SpMM (spmm_sk.cu): SP_SPMM_SK=1 forces it, =0 disables it; by
+// default it runs when the per-item grid is short (< 2 waves of 128-row items)
+// and the items are long (>= 8 column blocks) -- e.g. the 768-row cfg5 layer at
+// a per-rank batch of 2048-4096: +10-17%.  Elsewhere the per-item grid wins
+// (measured) and keeps every output element's order independent of B.
+int spmm_sk_mode() {
     static const int v = [] {
         const char *e = getenv("SP_SPMM_SK");
-        return (e && e[0] == '1') ? 0 : 1;
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
     }();
-    return v != 0;
+    return v;
 }
 // SP_CONV_SK=0 keeps the per-item conv grids (A/B measurements)
 bool conv_sk_disabled() {
@@ -389,7 +390,13 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
         launch_spmm_gather(w, orient, B, in, out, gate, epi, st);
         return;
     }
-    if (!spmm_sk_disabled() && launch_spmm_sk(w, orient, B, in, out, gate, epi, st)) return;
+    {
+        const sp_tiling &t0 = w->til[orient][0];
+        const int64_t items = (int64_t)t0.nrb * ((B + 127) / 128);
+        const int mode = spmm_sk_mode();
+        const bool sk = mode == 1 || (mode < 0 && items < 2 * kNumSMs && t0.nkb >= 8);
+        if (sk && launch_spmm_sk(w, orient, B, in, out, gate, epi, st)) return;
+    }
     // Choose the largest row block and batch vector that still fill the GPU.
     int vec = B <= 32 ? 1 : (B <= 64 || (B & 3)) ? 2 : 4;
     int var = 0;
