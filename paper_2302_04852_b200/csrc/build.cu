@@ -212,7 +212,7 @@ __global__ void til_max_kernel(int64_t ntiles, int RB, const int32_t *__restrict
 // groups of 4 entries, a last group may hold 2) summed over all column blocks
 // (rows rb*RB + w*RPW .. +RPW), single block, fixed order.  Bounds the
 // per-warp dW sum columns of the TMEM fused backward (8 groups per column).
-__global__ void til_warp_max_kernel(int nrb, int nkb, int RB, int RPW, const int32_t *__restrict__ seg,
+__global__ void til_warp_max_kernel(int nrb, int nkb, int RB, int RPW, int GL, const int32_t *__restrict__ seg,
                                     int64_t *__restrict__ out) {
     __shared__ int32_t sh[256];
     const int nw = RB / RPW;
@@ -222,7 +222,7 @@ __global__ void til_warp_max_kernel(int nrb, int nkb, int RB, int RPW, const int
         int32_t s = 0;
         for (int kb = 0; kb < nkb; ++kb) {
             const int64_t t = ((int64_t)rb * nkb + kb) * RB + (int64_t)wi * RPW;
-            for (int r = 0; r < RPW; ++r) s += (seg[t + r + 1] - seg[t + r] + 3) >> 2;
+            for (int r = 0; r < RPW; ++r) s += (seg[t + r + 1] - seg[t + r] + (1 << GL) - 1) >> GL;
         }
         m = max(m, s);
     }
@@ -386,11 +386,16 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
                           {1, kTilRB[0], kTilKC[0], kTilNW[0], 4, &w->til[1][0]},
                           {1, kTilRB[1], kTilKC[1], kTilNW[1], kTilRB[1] / kTilNW[1], &w->til[1][1]},
                           {1, 64, kTilKC[0], 32, 2, &w->til_f[0]},
-                          {1, 32, kTilKC[0], 32, 1, &w->til_f[1]}};
+                          {1, 32, kTilKC[0], 32, 1, &w->til_f[1]},
+                          {1, 96, kTilKC[0], 24, 4, &w->til_f[2]},
+                          {1, 64, kTilKC[0], 16, 4, &w->til_f[3]},
+                          {1, 112, kTilKC[0], 28, 4, &w->til_f[4]},
+                          {1, 56, kTilKC[0], 28, 2, &w->til_f[5]},
+                          {1, 48, kTilKC[0], 24, 2, &w->til_f[6]}};
     constexpr int NS = sizeof(specs) / sizeof(specs[0]);
     int64_t *info = nullptr, *mx = nullptr;
     if (cudaMallocAsync((void **)&info, 2 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
-    if (cudaMallocAsync((void **)&mx, 2 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
+    if (cudaMallocAsync((void **)&mx, 3 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
     for (int si = 0; si < NS; ++si) {
         const Spec &sp_ = specs[si];
         const int o = sp_.o;
@@ -438,11 +443,12 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
                                                                          slotmap, t.rowpos, t.seg, w->vals, t.ent,
                                                                          t.vidx);
             til_max_kernel<<<1, 256, 0, st>>>((int64_t)t.nrb * t.nkb, t.RB, t.seg, mx + si);
-            til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp, t.seg, mx + NS + si);
+            til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp, 2, t.seg, mx + NS + si);
+            til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp, 3, t.seg, mx + 2 * NS + si);
             cudaFreeAsync(cnt, st);
         }
     }
-    std::vector<int64_t> h(2 * NS), hi(2 * NS);
+    std::vector<int64_t> h(3 * NS), hi(2 * NS);
     cudaMemcpyAsync(h.data(), mx, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(hi.data(), info, hi.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
     const cudaError_t e = cudaStreamSynchronize(st);  // second (last) host sync of sp_weight_create
@@ -450,6 +456,7 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
         sp_tiling &t = *specs[si].t;
         t.max_tile = (int32_t)h[si];
         t.max_warp_groups = h[NS + si];
+        t.max_warp_groups8 = h[2 * NS + si];
         t.npad = hi[2 * si];  // padded entry total
     }
     cudaFreeAsync(info, st);

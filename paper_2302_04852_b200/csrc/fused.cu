@@ -538,6 +538,56 @@ __device__ __forceinline__ void tm_ld4x2(uint32_t ta, float (&v)[4], uint32_t tb
     w[3] = __uint_as_float(q3);
 }
 
+__device__ __forceinline__ void tm_st8(uint32_t taddr, const float (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                 "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                 "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+                 "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+                 : "memory");
+}
+__device__ __forceinline__ void tm_ld8(uint32_t taddr, float (&v)[8]) {
+    uint32_t r[8];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+        : "r"(taddr)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tm_ld8x2(uint32_t ta, float (&v)[8], uint32_t tb, float (&w)[8]) {
+    uint32_t r[8], q[8];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%16];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8, %9, %10, %11, %12, %13, %14, %15}, [%17];\n"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7])
+        : "r"(ta), "r"(tb)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        v[i] = __uint_as_float(r[i]);
+        w[i] = __uint_as_float(q[i]);
+    }
+}
+// Half-warp reduce4: 4 per-lane partials of each half-warp's own 4 entries ->
+// lane 16h + l holds the 16-lane sum for entry (l >> 2) & 3 of half h
+// (transpose stages xor 8 / xor 4, then xor 2/1: 5 SHFL for 8 entries).
+__device__ __forceinline__ float reduce4h(const float (&p)[4], int lane) {
+    const bool h8 = (lane & 8) != 0, h4 = (lane & 4) != 0;
+    const float sa = h8 ? p[0] : p[2], sb = h8 ? p[1] : p[3];
+    const float ka = h8 ? p[2] : p[0], kb = h8 ? p[3] : p[1];
+    const float ra = ka + __shfl_xor_sync(kFull, sa, 8);
+    const float rb = kb + __shfl_xor_sync(kFull, sb, 8);
+    const float s4 = h4 ? ra : rb, k4 = h4 ? rb : ra;
+    float v = k4 + __shfl_xor_sync(kFull, s4, 4);
+    v += __shfl_xor_sync(kFull, v, 2);
+    v += __shfl_xor_sync(kFull, v, 1);
+    return v;
+}
+
 // TMEM columns of one warp (32 warps: 8 per lane quarter, 64 columns each):
 // [0, 4*RPW) the X rows of its RPW rows (the dW register operand), [4*RPW,
 // 8*RPW) their dX accumulators, the rest dW sums (8 groups of 4 entries per
@@ -545,20 +595,28 @@ __device__ __forceinline__ void tm_ld4x2(uint32_t ta, float (&v)[4], uint32_t tb
 // the registers that 32 resident warps need.  RPW = 4 (128-row blocks) for
 // linear layers: 32 dW columns (256 groups); RPW = 2 (64-row blocks) for the
 // fused conv backward: 48 columns.  DWONLY drops the dX columns.
-constexpr int kSkDwCols = 32;  // dW columns of the linear (RPW = 4) plan
-template <int RPW, bool DWONLY>
-constexpr int sk_dw0() { return DWONLY ? 4 * RPW : 8 * RPW; }
-template <int RPW, bool DWONLY>
-constexpr int sk_dwcols() { return 64 - sk_dw0<RPW, DWONLY>(); }
+constexpr int kSkDwCols = 32;  // dW columns of the linear (RPW = 4, 32 warps) plan
+// TMEM columns per warp: the NW/4 warps of a lane quarter share its 512 columns
+template <int NW>
+constexpr int sk_cpw() { return (512 / (NW / 4)) & ~7; }
+// HALF: half-warp entries (8 columns per row for the X row and the dX accumulator)
+template <int RPW, bool DWONLY, bool HALF = false>
+constexpr int sk_dw0() { return (DWONLY ? 1 : 2) * RPW * (HALF ? 8 : 4); }
+template <int RPW, bool DWONLY, int NW = 32, bool HALF = false>
+constexpr int sk_dwcols() { return sk_cpw<NW>() - sk_dw0<RPW, DWONLY, HALF>(); }
 
-template <int RPW, int NW, bool GATE, bool DWONLY, int NBUF, bool CONV>
+template <int RPW, int NW, bool GATE, bool DWONLY, int NBUF, bool CONV, bool HALF = false>
 __global__ void __launch_bounds__(NW * 32, 1)
     bwd_fused_sk_kernel(const FusedArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr int VEC = 4;
-    constexpr int RV0 = 0, DX0 = 4 * RPW, DW0 = sk_dw0<RPW, DWONLY>(), DWC = sk_dwcols<RPW, DWONLY>();
+    constexpr int SW = HALF ? 8 : 4;  // TMEM columns per row (X row, dX accumulator)
+    constexpr int RV0 = 0, DX0 = SW * RPW, DW0 = sk_dw0<RPW, DWONLY, HALF>(), DWC = sk_dwcols<RPW, DWONLY, NW, HALF>();
+    // entry groups: GE entries (4: one per warp quarter-sweep; HALF: 8, 4 per half-warp),
+    // 2^GSH groups per TMEM dW column (32 lanes = GE entries x copies)
+    constexpr int GE = HALF ? 8 : 4, GL = HALF ? 3 : 2, GSH = HALF ? 2 : 3, GM = (1 << GSH) - 1;
     constexpr int BT = 32 * VEC;
     constexpr int RB = NW * RPW;
-    static_assert(NW == 32 && (RPW == 4 || RPW == 2 || RPW == 1), "TMEM column plan: 8 warps per lane quarter, 64 columns each");
+    static_assert(NW % 4 == 0 && NW <= 32 && (RPW == 4 || RPW == 2 || RPW == 1), "TMEM column plan: whole lane quarters");
     extern __shared__ __align__(128) float smem[];
     __shared__ uint64_t full[NBUF];
     __shared__ int released[NBUF];  // warps done with each buffer (the last one refills it)
@@ -593,7 +651,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     tm_fence_before();
     __syncthreads();
     tm_fence_after();
-    const uint32_t tcol = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 64);
+    const uint32_t tcol = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * sk_cpw<NW>());
 
     struct Tile {
         int rb, sl, r;  // r: tile within the item (tap * nkb + kb for conv)
@@ -670,23 +728,25 @@ __global__ void __launch_bounds__(NW * 32, 1)
             if (!touched(r, ra, len)) {  // advance the slot sequence past this tile
                 int gs = 0;
 #pragma unroll
-                for (int m = 0; m < RPW; ++m) gs += (__shfl_sync(kFull, sg, m + 1) - __shfl_sync(kFull, sg, m) + 3) >> 2;
-                if ((c2 & 7) != 0 && ((c2 + gs) >> 3) != (c2 >> 3)) out(c2 >> 3);
+                for (int m = 0; m < RPW; ++m)
+                    gs += (__shfl_sync(kFull, sg, m + 1) - __shfl_sync(kFull, sg, m) + GE - 1) >> GL;
+                if ((c2 & GM) != 0 && ((c2 + gs) >> GSH) != (c2 >> GSH)) out(c2 >> GSH);
                 c2 += gs;
                 continue;
             }
             const int64_t base = CONV ? a.tapbase[tap_of(r)] : 0;
             for (int m = 0; m < RPW; ++m) {
                 const int g0 = __shfl_sync(kFull, sg, m), g1 = __shfl_sync(kFull, sg, m + 1);
-                for (int e = g0; e < g1; e += 4) {
-                    const int u = (lane >> 3) & 3;
-                    if ((lane & 7) == (c2 & 7)) my_e = u < g1 - e ? (int)(base + e + u) : -1;
+                for (int e = g0; e < g1; e += GE) {
+                    const int u = HALF ? (lane >> 2) & 3 : (lane >> 3) & 3;
+                    const int idx = HALF ? 2 * u + (lane >> 4) : u;  // entry in the group
+                    if ((lane & GM) == (c2 & GM)) my_e = idx < g1 - e ? (int)(base + e + idx) : -1;
                     ++c2;
-                    if ((c2 & 7) == 0) out((c2 >> 3) - 1);
+                    if ((c2 & GM) == 0) out((c2 >> GSH) - 1);
                 }
             }
         }
-        if (c2 & 7) out(c2 >> 3);
+        if (c2 & GM) out(c2 >> GSH);
     };
 
     float keep = 0.f;
@@ -710,12 +770,18 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
                 const int64_t r = a.rowmap ? (int64_t)__ldg(a.rowmap + r_base + i) : r_base + i;
-                const float4 t = (r >= 0 && r < a.nrow && bl + 4 <= a.xstride)
-                                     ? __ldg(reinterpret_cast<const float4 *>(a.X + r * a.xstride + bl))
-                                     : make_float4(0.f, 0.f, 0.f, 0.f);
-                const float tv[4] = {t.x, t.y, t.z, t.w};
-                tm_st4(tcol + RV0 + 4 * i, tv);
-                if constexpr (!DWONLY) tm_st4(tcol + DX0 + 4 * i, z);
+                // HALF: lane 16h + j holds batch columns 4j.. and 64 + 4j.. of the slice
+                const int64_t bx = HALF ? (int64_t)id.sl * BT + (lane & 15) * VEC : bl;
+#pragma unroll
+                for (int hh = 0; hh < (HALF ? 2 : 1); ++hh) {
+                    const int64_t bc = bx + hh * 64;
+                    const float4 t = (r >= 0 && r < a.nrow && bc + 4 <= a.xstride)
+                                         ? __ldg(reinterpret_cast<const float4 *>(a.X + r * a.xstride + bc))
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+                    const float tv[4] = {t.x, t.y, t.z, t.w};
+                    tm_st4(tcol + RV0 + SW * i + 4 * hh, tv);
+                    if constexpr (!DWONLY) tm_st4(tcol + DX0 + SW * i + 4 * hh, z);
+                }
             }
             whole = id.r == 0;
             // group index of this tile's first group in the slice sequence
@@ -723,7 +789,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
             for (int k = 0; k < id.r; ++k) {  // groups of 4 per row segment (a last group may hold 2)
                 const int32_t *sw = segw_of(id.rb, k);
 #pragma unroll
-                for (int i = 0; i < RPW; ++i) cnt += (__ldg(sw + i + 1) - __ldg(sw + i) + 3) >> 2;
+                for (int i = 0; i < RPW; ++i) cnt += (__ldg(sw + i + 1) - __ldg(sw + i) + GE - 1) >> GL;
             }
         }
         tm_wait_st();  // TMEM stores of earlier tiles land before this tile reads them back
@@ -741,6 +807,50 @@ __global__ void __launch_bounds__(NW * 32, 1)
             tm_st1(ta, old + keep);
             keep = 0.f;
         };
+        if constexpr (HALF) {
+            // half-warp h takes entries h, 2+h, 4+h, 6+h of each group of 8 (segments
+            // have even length, so a group's valid entries are warp-uniform); lane
+            // 16h + j covers batch columns 4j.. and 64 + 4j.. (two 16-byte loads per entry)
+            const char *tbh = reinterpret_cast<const char *>(smem + buf * buf_sz + BT + (lane & 15) * VEC);
+            const int2 *esh = es + (lane >> 4);
+#pragma unroll 1
+            for (int m = 0; m < RPW; ++m) {
+                const int g0 = __shfl_sync(kFull, sg, m), g1 = __shfl_sync(kFull, sg, m + 1);
+                if (g0 == g1) continue;
+                float rv[8], dx[8];
+                if constexpr (DWONLY)
+                    tm_ld8(tcol + RV0 + 8 * m, rv);
+                else
+                    tm_ld8x2(tcol + RV0 + 8 * m, rv, tcol + DX0 + 8 * m, dx);
+                for (int e = g0; e < g1; e += 8) {
+                    float p[4] = {0.f, 0.f, 0.f, 0.f};
+                    auto entry = [&](int u) {
+                        const int2 q = esh[e + 2 * u];
+                        float x[8];
+                        const float4 lo = *reinterpret_cast<const float4 *>(tbh + q.x);
+                        const float4 hi = *reinterpret_cast<const float4 *>(tbh + q.x + 64 * sizeof(float));
+                        x[0] = lo.x, x[1] = lo.y, x[2] = lo.z, x[3] = lo.w;
+                        x[4] = hi.x, x[5] = hi.y, x[6] = hi.z, x[7] = hi.w;
+                        if constexpr (!DWONLY) fma_bcast<8>(dx, __int_as_float(q.y), x);  // dX  (Eq. 1 / Eq. 4)
+                        p[u] = dot_vec<8>(rv, x);  // dW partial (Eq. 2 / Eq. 5)
+                    };
+                    const int rem = g1 - e;  // even
+                    if (rem >= 8) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) entry(u);
+                    } else {  // a short group: entries 0 .. rem/2 - 1 of each half
+                        entry(0);
+                        if (rem > 2) entry(1);
+                        if (rem > 4) entry(2);
+                    }
+                    const float v = reduce4h(p, lane);
+                    if ((lane & GM) == (cnt & GM)) keep = v;
+                    ++cnt;
+                    if ((cnt & GM) == 0) flush((cnt >> GSH) - 1);
+                }
+                if constexpr (!DWONLY) tm_st8(tcol + DX0 + 8 * m, dx);
+            }
+        } else {
 #pragma unroll 1
         for (int m = 0; m < RPW; ++m) {
             const int g0 = __shfl_sync(kFull, sg, m), g1 = __shfl_sync(kFull, sg, m + 1);
@@ -773,19 +883,33 @@ __global__ void __launch_bounds__(NW * 32, 1)
                     entry(1);
                 }
                 const float v = reduce4(p, lane);
-                if ((lane & 7) == (cnt & 7)) keep = v;
+                if ((lane & GM) == (cnt & GM)) keep = v;
                 ++cnt;
-                if ((cnt & 7) == 0) flush((cnt >> 3) - 1);
+                if ((cnt & GM) == 0) flush((cnt >> GSH) - 1);
             }
             if constexpr (!DWONLY) tm_st4(tcol + DX0 + 4 * m, dx);
         }
+        }
         const bool item_end = id.r == tpi - 1 || q == ntile - 1;
         if (item_end && DWONLY) {  // item done here: partial column
-            if (cnt & 7) flush(cnt >> 3);
+            if (cnt & GM) flush(cnt >> GSH);
             tm_wait_st();
         } else if (item_end) {  // item done here: partial column, dX rows
-            if (cnt & 7) flush(cnt >> 3);
+            if (cnt & GM) flush(cnt >> GSH);
             tm_wait_st();
+            // dX row i of this item, batch columns bl..bl+3 (HALF: the two half-warp
+            // partial sums added, low half to lanes 0-15, high half to 16-31)
+            auto load_dx = [&](int i, float (&o)[VEC]) {
+                if constexpr (HALF) {
+                    float lo[4], hi[4];
+                    tm_ld4x2(tcol + DX0 + 8 * i, lo, tcol + DX0 + 8 * i + 4, hi);
+                    const bool h = (lane & 16) != 0;
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) o[v] = (h ? hi[v] : lo[v]) + __shfl_xor_sync(kFull, h ? lo[v] : hi[v], 16);
+                } else {
+                    tm_ld4(tcol + DX0 + 4 * i, o);
+                }
+            };
             // (ReLU' gate and) store of dX rows (rb, warp*RPW + i), columns bl..bl+3
             auto store = [&](int i, float (&o)[VEC]) {
                 if constexpr (CONV) {  // compact store of the valid positions (tap tilings: identity rows)
@@ -813,7 +937,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll 1
                 for (int i = 0; i < RPW; ++i) {
                     float o[VEC];
-                    tm_ld4(tcol + DX0 + 4 * i, o);
+                    load_dx(i, o);
                     store(i, o);
                 }
             } else {
@@ -825,7 +949,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll 1
                 for (int i = 0; i < RPW; ++i) {
                     float o[VEC];
-                    tm_ld4(tcol + DX0 + 4 * i, o);
+                    load_dx(i, o);
                     *reinterpret_cast<float4 *>(mine + i * BT) = make_float4(o[0], o[1], o[2], o[3]);
                 }
                 __threadfence();
@@ -948,6 +1072,25 @@ bool tm_disabled() {
     return v != 0;
 }
 
+// Half-warp entries (8 batch columns per lane, 16-lane dW reductions) unless
+// SP_FUSED_HALF=0 (A/B)
+bool fused_half() {
+    static const int v = [] {
+        const char *e = getenv("SP_FUSED_HALF");
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    return v != 0;
+}
+
+// SP_FUSED_NW=24|16|28: the stream-K kernel with fewer warps x 4 rows (A/B)
+int fused_nw() {
+    static const int v = [] {
+        const char *e = getenv("SP_FUSED_NW");
+        return e ? atoi(e) : 32;
+    }();
+    return v;
+}
+
 // SP_FUSED_SK=0 keeps the slice-split grid for the TMEM variant (A/B measurements).
 bool sk_disabled() {
     static const int v = [] {
@@ -962,17 +1105,18 @@ bool sk_disabled() {
 // Stream-K launch of the TMEM kernel (fused backward, or dW alone when dX is
 // null).  Returns false when it does not apply (ragged B, staged entries do
 // not fit, too many entry groups per warp for the TMEM columns).
-template <int TRPW>
+template <int TRPW, int TNW = 32, bool HALF = false>
 static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float *X, const float *dY, const float *H,
                           float *dX, float *dW, int64_t B, cudaStream_t st) {
-    constexpr int TNW = 32, BT = 128, RBT = TRPW * TNW;
+    constexpr int BT = 128, RBT = TRPW * TNW;
     const bool dwonly = dX == nullptr;
     const int64_t slices = (B + BT - 1) / BT;
     const int64_t T = (int64_t)t.nrb * slices * t.nkb;
     // tiny problems (a few tiles) go to the separate kernels: the reduce pass would dominate
     if (T >= (1LL << 31) || T < 32) return false;
     const int64_t G = std::min<int64_t>(kNumSMs, T);
-    const int cap = (t.max_tile + 2 + 3) & ~3;
+    // HALF reads entry pairs up to 6 entries past a segment (masked): slack in the staging
+    const int cap = (t.max_tile + (HALF ? 8 : 2) + 3) & ~3;
     const size_t smem = 2 * ((size_t)(t.KC + 1) * BT * sizeof(float) + (size_t)(cap + 2) * sizeof(int2));
     if (smem > (size_t)(226 * 1024)) return false;
     CUtensorMap tmap{};
@@ -1000,9 +1144,9 @@ static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float 
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<(unsigned)G, TNW * 32, smem, st>>>(a, tmap);
     };
-    if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, 2, false>);
-    else if (H) go(bwd_fused_sk_kernel<TRPW, TNW, true, false, 2, false>);
-    else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 2, false>);
+    if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, 2, false, HALF>);
+    else if (H) go(bwd_fused_sk_kernel<TRPW, TNW, true, false, 2, false, HALF>);
+    else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 2, false, HALF>);
     JobReduceArgs ja{t.npad, slices, G, t.nrb, t.nkb, RBT, 1, t.seg, t.vidx, nullptr, {}, part, dW};
     job_reduce_kernel<<<dim3((unsigned)(t.nrb * t.nkb), (unsigned)((t.max_tile + 255) / 256)), 256, 0, st>>>(ja);
     count_launches(3);  // refresh, kernel, reduce
@@ -1024,6 +1168,36 @@ static bool launch_sk(const sp_weight_s *w, const float *X, const float *dY, con
     if ((B & 3) != 0 || w->nnz == 0) return false;
     const bool dw = dX == nullptr;
     auto fits = [&](const sp_tiling &t, int64_t cols) { return t.seg != nullptr && t.max_warp_groups <= cols * 8; };
+    auto fits8 = [&](const sp_tiling &t, int64_t cols) { return t.seg != nullptr && t.max_warp_groups8 <= cols * 4; };
+    if (fused_half()) {
+        if (dw && fits8(w->til[1][0], sk_dwcols<4, true, 32, true>()) && w->til[1][0].RB == 128 &&
+            launch_sk_rpw<4, 32, true>(w, w->til[1][0], X, dY, H, dX, dW, B, st))
+            return true;
+        if (!dw && fused_nw() == 28 && fits8(w->til_f[5], sk_dwcols<2, false, 28, true>()) &&
+            launch_sk_rpw<2, 28, true>(w, w->til_f[5], X, dY, H, dX, dW, B, st))
+            return true;
+        if (!dw && fused_nw() == 24 && fits8(w->til_f[6], sk_dwcols<2, false, 24, true>()) &&
+            launch_sk_rpw<2, 24, true>(w, w->til_f[6], X, dY, H, dX, dW, B, st))
+            return true;
+        if (!dw && fused_nw() == 16 && fits8(w->til_f[3], sk_dwcols<4, false, 16, true>()) &&
+            launch_sk_rpw<4, 16, true>(w, w->til_f[3], X, dY, H, dX, dW, B, st))
+            return true;
+        if (!dw && fits8(w->til_f[0], sk_dwcols<2, false, 32, true>()) &&
+            launch_sk_rpw<2, 32, true>(w, w->til_f[0], X, dY, H, dX, dW, B, st))
+            return true;
+        if (!dw && fits8(w->til_f[3], sk_dwcols<4, false, 16, true>()) &&
+            launch_sk_rpw<4, 16, true>(w, w->til_f[3], X, dY, H, dX, dW, B, st))
+            return true;
+    }
+    if (fused_nw() == 24 && fits(w->til_f[2], dw ? sk_dwcols<4, true, 24>() : sk_dwcols<4, false, 24>()) &&
+        launch_sk_rpw<4, 24>(w, w->til_f[2], X, dY, H, dX, dW, B, st))
+        return true;
+    if (fused_nw() == 16 && fits(w->til_f[3], dw ? sk_dwcols<4, true, 16>() : sk_dwcols<4, false, 16>()) &&
+        launch_sk_rpw<4, 16>(w, w->til_f[3], X, dY, H, dX, dW, B, st))
+        return true;
+    if (fused_nw() == 28 && fits(w->til_f[4], dw ? sk_dwcols<4, true, 28>() : sk_dwcols<4, false, 28>()) &&
+        launch_sk_rpw<4, 28>(w, w->til_f[4], X, dY, H, dX, dW, B, st))
+        return true;
     if (fits(w->til[1][0], dw ? sk_dwcols<4, true>() : sk_dwcols<4, false>()) && w->til[1][0].RB == 128 &&
         launch_sk_rpw<4>(w, w->til[1][0], X, dY, H, dX, dW, B, st))
         return true;

@@ -38,6 +38,7 @@ struct sp_tiling {
     int2 *ent;      // [nnz + 8] (padded)
     int32_t *vidx;  // [nnz]
     int32_t max_tile;  // max (padded) entries in one (row block, column block) tile
+    int64_t max_warp_groups8;  // the same in groups of 8 entries (half-warp fused backward)
     int64_t max_warp_groups;  // max entry groups (4 entries, a last one may hold 2) of 4 consecutive tiled rows
                               // (variant 0; RB/NW rows otherwise) over all column blocks
     int64_t npad;      // padded entry total (segments padded to kTilPad with weight-0 entries)
@@ -67,7 +68,7 @@ struct sp_weight_s {
     sp_tiling til[2][2];
     // CSC tilings of the fused backward for dense-ish rows (KC = 192): [0] 64-row
     // blocks (32 warps x 2 rows), [1] 32-row blocks (32 warps x 1 row)
-    sp_tiling til_f[2];
+    sp_tiling til_f[7];  // [2..4]: 96/64/112-row blocks (24/16/28 warps x 4 rows, experimental)
     // conv handles (sp_weight_create_conv): filter taps and, per tap (x, y),
     // tilings of the OC x IC tap matrix W_xy -- [0]: rows oc / inner ic,
     // [1]: rows ic / inner oc -- whose vidx are slots of THIS handle's CSR.
