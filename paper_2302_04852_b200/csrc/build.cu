@@ -391,7 +391,15 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
                           {1, 64, kTilKC[0], 16, 4, &w->til_f[3]},
                           {1, 112, kTilKC[0], 28, 4, &w->til_f[4]},
                           {1, 56, kTilKC[0], 28, 2, &w->til_f[5]},
-                          {1, 48, kTilKC[0], 24, 2, &w->til_f[6]}};
+                          {1, 48, kTilKC[0], 24, 2, &w->til_f[6]},
+                          {0, 112, kTmKC, 28, 4, &w->til_t[0][0]},
+                          {1, 112, kTmKC, 28, 4, &w->til_t[1][0]},
+                          {0, 96, kTmKC, 24, 4, &w->til_t[0][1]},
+                          {1, 96, kTmKC, 24, 4, &w->til_t[1][1]},
+                          {0, 128, kTmKC, 16, 8, &w->til_t[0][2]},
+                          {1, 128, kTmKC, 16, 8, &w->til_t[1][2]},
+                          {0, 256, kTmKC, 16, 16, &w->til_t[0][3]},
+                          {1, 256, kTmKC, 16, 16, &w->til_t[1][3]}};
     constexpr int NS = sizeof(specs) / sizeof(specs[0]);
     int64_t *info = nullptr, *mx = nullptr;
     if (cudaMallocAsync((void **)&info, 2 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
@@ -483,6 +491,8 @@ void free_tilings(sp_weight_s *w) {
         for (auto &t : o) fr(t);
     for (auto &t : w->tapf) fr(t);
     for (auto &t : w->til_f) fr(t);
+    for (auto &o : w->til_t)
+        for (auto &t : o) fr(t);
     if (w->tapdev) cudaFree(w->tapdev);
     w->tapdev = nullptr;
 }

@@ -69,6 +69,9 @@ struct sp_weight_s {
     // CSC tilings of the fused backward for dense-ish rows (KC = 192): [0] 64-row
     // blocks (32 warps x 2 rows), [1] 32-row blocks (32 warps x 1 row)
     sp_tiling til_f[7];  // [2..4]: 96/64/112-row blocks (24/16/28 warps x 4 rows, experimental)
+    // tilings of the TMEM-gather SpMM (spmm_tm.cu): [orientation][variant], KC = kTmKC,
+    // RB = 112 (28 compute warps x 4 rows) / 96 (24 x 4) / 128 (16 x 8) / 256 (16 x 16)
+    sp_tiling til_t[2][4];
     // conv handles (sp_weight_create_conv): filter taps and, per tap (x, y),
     // tilings of the OC x IC tap matrix W_xy -- [0]: rows oc / inner ic,
     // [1]: rows ic / inner oc -- whose vidx are slots of THIS handle's CSR.
@@ -96,6 +99,9 @@ constexpr int kTilNW[2] = {16, 8};  // warps per CTA of the kernels using each v
 // (kTilRowBytes); kernels with narrower tiles shift them down.  Conv tap
 // tilings keep groups of 4 (kTapPad).
 constexpr int kTilPad = 2;
+// inner columns per tile of the TMEM-gather SpMM tilings (til_t): 4 zero + 63 x 4
+// tile columns fill one 256-column TMEM buffer
+constexpr int kTmKC = 63;
 constexpr int kTapPad = 4;
 constexpr int kTilRowBytes = 512;
 
@@ -140,6 +146,11 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
                     int epi, cudaStream_t st);
 bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in, int64_t Lp, float *out,
                          const int *sh, int ntap, int64_t Wv, int64_t OHv, int64_t OWv, cudaStream_t st);
+
+// ---- spmm_tm.cu: TMEM-gather SpMM (B % 4 == 0); false if it does not apply
+int spmm_tm_mode();
+bool launch_spmm_tm(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,
+                    int epi, cudaStream_t st);
 
 // ---- gather.cu (very sparse / small regime: no shared-memory staging) ----
 bool gather_preferred(const sp_weight_s *w, int orient, int64_t B, bool chunked = false);
