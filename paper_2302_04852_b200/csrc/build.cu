@@ -380,32 +380,36 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
     struct Spec {
         int o, RB, KC, NWbal, RPWgrp;
         sp_tiling *t;
+        bool need;  // tilings of A/B variants are built only when their switch is set
     };
-    const Spec specs[] = {{0, kTilRB[0], kTilKC[0], kTilNW[0], 4, &w->til[0][0]},
-                          {0, kTilRB[1], kTilKC[1], kTilNW[1], kTilRB[1] / kTilNW[1], &w->til[0][1]},
-                          {1, kTilRB[0], kTilKC[0], kTilNW[0], 4, &w->til[1][0]},
-                          {1, kTilRB[1], kTilKC[1], kTilNW[1], kTilRB[1] / kTilNW[1], &w->til[1][1]},
-                          {1, 64, kTilKC[0], 32, 2, &w->til_f[0]},
-                          {1, 32, kTilKC[0], 32, 1, &w->til_f[1]},
-                          {1, 96, kTilKC[0], 24, 4, &w->til_f[2]},
-                          {1, 64, kTilKC[0], 16, 4, &w->til_f[3]},
-                          {1, 112, kTilKC[0], 28, 4, &w->til_f[4]},
-                          {1, 56, kTilKC[0], 28, 2, &w->til_f[5]},
-                          {1, 48, kTilKC[0], 24, 2, &w->til_f[6]},
-                          {0, 112, kTmKC, 28, 4, &w->til_t[0][0]},
-                          {1, 112, kTmKC, 28, 4, &w->til_t[1][0]},
-                          {0, 96, kTmKC, 24, 4, &w->til_t[0][1]},
-                          {1, 96, kTmKC, 24, 4, &w->til_t[1][1]},
-                          {0, 128, kTmKC, 16, 8, &w->til_t[0][2]},
-                          {1, 128, kTmKC, 16, 8, &w->til_t[1][2]},
-                          {0, 256, kTmKC, 16, 16, &w->til_t[0][3]},
-                          {1, 256, kTmKC, 16, 16, &w->til_t[1][3]}};
+    const int fnw = fused_nw();
+    const bool tm = spmm_tm_mode() == 1;
+    const Spec specs[] = {{0, kTilRB[0], kTilKC[0], kTilNW[0], 4, &w->til[0][0], true},
+                          {0, kTilRB[1], kTilKC[1], kTilNW[1], kTilRB[1] / kTilNW[1], &w->til[0][1], true},
+                          {1, kTilRB[0], kTilKC[0], kTilNW[0], 4, &w->til[1][0], true},
+                          {1, kTilRB[1], kTilKC[1], kTilNW[1], kTilRB[1] / kTilNW[1], &w->til[1][1], true},
+                          {1, 64, kTilKC[0], 32, 2, &w->til_f[0], true},
+                          {1, 32, kTilKC[0], 32, 1, &w->til_f[1], true},
+                          {1, 96, kTilKC[0], 24, 4, &w->til_f[2], fnw == 24},
+                          {1, 64, kTilKC[0], 16, 4, &w->til_f[3], true},
+                          {1, 112, kTilKC[0], 28, 4, &w->til_f[4], fnw == 28},
+                          {1, 56, kTilKC[0], 28, 2, &w->til_f[5], fnw == 28},
+                          {1, 48, kTilKC[0], 24, 2, &w->til_f[6], fnw == 24},
+                          {0, 112, kTmKC, 28, 4, &w->til_t[0][0], tm},
+                          {1, 112, kTmKC, 28, 4, &w->til_t[1][0], tm},
+                          {0, 96, kTmKC, 24, 4, &w->til_t[0][1], tm},
+                          {1, 96, kTmKC, 24, 4, &w->til_t[1][1], tm},
+                          {0, 128, kTmKC, 16, 8, &w->til_t[0][2], tm},
+                          {1, 128, kTmKC, 16, 8, &w->til_t[1][2], tm},
+                          {0, 256, kTmKC, 16, 16, &w->til_t[0][3], tm},
+                          {1, 256, kTmKC, 16, 16, &w->til_t[1][3], tm}};
     constexpr int NS = sizeof(specs) / sizeof(specs[0]);
     int64_t *info = nullptr, *mx = nullptr;
     if (cudaMallocAsync((void **)&info, 2 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
     if (cudaMallocAsync((void **)&mx, 3 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
     for (int si = 0; si < NS; ++si) {
         const Spec &sp_ = specs[si];
+        if (!sp_.need) continue;  // stays zeroed (seg == nullptr: launchers skip it)
         const int o = sp_.o;
         const int64_t rows = o == 0 ? w->R : w->C, inner = o == 0 ? w->C : w->R;
         const int32_t *ptr = o == 0 ? w->row_ptr : w->col_ptr;
@@ -461,6 +465,7 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
     cudaMemcpyAsync(hi.data(), info, hi.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
     const cudaError_t e = cudaStreamSynchronize(st);  // second (last) host sync of sp_weight_create
     for (int si = 0; si < NS; ++si) {
+        if (!specs[si].need) continue;
         sp_tiling &t = *specs[si].t;
         t.max_tile = (int32_t)h[si];
         t.max_warp_groups = h[NS + si];

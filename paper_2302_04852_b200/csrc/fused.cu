@@ -1082,15 +1082,6 @@ bool fused_half() {
     return v != 0;
 }
 
-// SP_FUSED_NW=24|16|28: the stream-K kernel with fewer warps x 4 rows (A/B)
-int fused_nw() {
-    static const int v = [] {
-        const char *e = getenv("SP_FUSED_NW");
-        return e ? atoi(e) : 32;
-    }();
-    return v;
-}
-
 // SP_FUSED_SK=0 keeps the slice-split grid for the TMEM variant (A/B measurements).
 bool sk_disabled() {
     static const int v = [] {
@@ -1101,6 +1092,16 @@ bool sk_disabled() {
 }
 
 }  // namespace
+
+// SP_FUSED_NW=24|16|28: the stream-K kernel with fewer warps x 4 rows (A/B)
+int fused_nw() {
+    static const int v = [] {
+        const char *e = getenv("SP_FUSED_NW");
+        return e ? atoi(e) : 32;
+    }();
+    return v;
+}
+
 
 // Stream-K launch of the TMEM kernel (fused backward, or dW alone when dX is
 // null).  Returns false when it does not apply (ragged B, staged entries do

@@ -147,6 +147,9 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
 bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in, int64_t Lp, float *out,
                          const int *sh, int ntap, int64_t Wv, int64_t OHv, int64_t OWv, cudaStream_t st);
 
+// ---- fused.cu: warps per CTA of the fused backward (SP_FUSED_NW A/B switch, default 32)
+int fused_nw();
+
 // ---- spmm_tm.cu: TMEM-gather SpMM (B % 4 == 0); false if it does not apply
 int spmm_tm_mode();
 bool launch_spmm_tm(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,
