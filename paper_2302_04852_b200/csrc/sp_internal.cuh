@@ -155,6 +155,11 @@ int spmm_tm_mode();
 bool launch_spmm_tm(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,
                     int epi, cudaStream_t st);
 
+// ---- spmm_hyb.cu: the 32-warp SpMM with the tiles' last rows mirrored in TMEM
+int spmm_hyb_mode();
+bool launch_spmm_hyb(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,
+                     int epi, cudaStream_t st);
+
 // ---- gather.cu (very sparse / small regime: no shared-memory staging) ----
 bool gather_preferred(const sp_weight_s *w, int orient, int64_t B, bool chunked = false);
 void launch_spmm_gather(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out,

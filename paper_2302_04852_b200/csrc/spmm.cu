@@ -391,6 +391,7 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
         return;
     }
     if (spmm_tm_mode() == 1 && launch_spmm_tm(w, orient, B, in, out, gate, epi, st)) return;
+    if (spmm_hyb_mode() == 1 && launch_spmm_hyb(w, orient, B, in, out, gate, epi, st)) return;
     {
         const sp_tiling &t0 = w->til[orient][0];
         const int64_t items = (int64_t)t0.nrb * ((B + 127) / 128);

@@ -1,6 +1,8 @@
-"""GPU parity of the opt-in TMEM-gather SpMM (spmm_tm.cu, SP_SPMM_TM=1) against
-the fp64 oracle, for each of its CTA layouts (SP_SPMM_TM_VAR).  The switches are
-read once per process, so every layout runs in its own interpreter."""
+"""GPU parity of the SpMM kernels that gather from tensor memory against the
+fp64 oracle: the split-source SpMM (spmm_hyb.cu, SP_SPMM_HYB=1) and each CTA
+layout of the opt-in TMEM-gather SpMM (spmm_tm.cu, SP_SPMM_TM=1,
+SP_SPMM_TM_VAR).  The switches are read once per process, so every setting
+runs in its own interpreter."""
 import os
 import subprocess
 import sys
@@ -34,9 +36,11 @@ print("ok", sp.launch_count() if hasattr(sp, "launch_count") else "")
 """
 
 
-@pytest.mark.parametrize("var", [0, 1, 2, 3])
-def test_spmm_tm_layouts_match_oracle(var):
-    env = dict(os.environ, SP_SPMM_TM="1", SP_SPMM_TM_VAR=str(var))
+@pytest.mark.parametrize("switch", [dict(SP_SPMM_HYB="1")] +
+                         [dict(SP_SPMM_TM="1", SP_SPMM_TM_VAR=str(v)) for v in range(4)],
+                         ids=["hyb", "tm0", "tm1", "tm2", "tm3"])
+def test_tmem_spmm_matches_oracle(switch):
+    env = dict(os.environ, **switch)
     env["PYTHONPATH"] = os.pathsep.join([ROOT, os.path.join(ROOT, "tests"), env.get("PYTHONPATH", "")])
     p = subprocess.run([sys.executable, "-c", SCRIPT], env=env, cwd=ROOT, capture_output=True, text=True,
                        timeout=300)
