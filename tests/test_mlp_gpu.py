@@ -75,3 +75,39 @@ def test_mlp_sgd_updates_only_kept_weights():
         for Wh, dd, mask in ((W1, d1, c["layers"][l][1]), (W2, d2, c["layers"][l][3])):
             D = _np(Wh.to_dense(dd))
             assert np.all(D[mask == 0] == 0.0)
+
+
+def test_mlp_full_size_sampled():
+    """cfg5 at its full size in bench.py's launch configuration (16384 tokens on
+    one GPU, fused backward): layer-local parity on 64 sampled token columns
+    for the forward and dX products (columns are independent), and on every
+    nonzero for the dW of the first and last blocks (full batch)."""
+    from paper_2302_04852_b200.dp import SparseMLP
+    T = 16384
+    c = synth.mlp_case(blocks=12, d_model=768, d_ff=3072, T=T, density=0.05, seed=5)
+    m = SparseMLP(c["layers"], T, "cuda")
+    m.set_batch(torch.from_numpy(c["X0"]), torch.from_numpy(c["target"]), non_blocking=False)
+    m.forward()
+    trace = []
+    m.backward(allreduce=False, trace=trace)
+    torch.cuda.synchronize()
+    cols = np.sort(synth.rng(55).choice(T, 64, replace=False))
+    S = [(oracle.csr_from_mask(w1, m1), oracle.csr_from_mask(w2, m2)) for (w1, m1, w2, m2) in c["layers"]]
+    for l in (0, 5, 11):
+        S1, S2 = S[l]
+        X = np.ascontiguousarray(_np(m.X[l])[:, cols])
+        H = np.ascontiguousarray(_np(m.H[l])[:, cols])
+        _ok(f"H[{l}] sampled", H, np.maximum(oracle.linear_fwd(S1, X, NT), 0.0))
+        _ok(f"X[{l + 1}] sampled", _np(m.X[l + 1])[:, cols], oracle.linear_fwd(S2, H, NT))
+    for (l, dY_in, dZ, dX_out) in trace:
+        if l not in (0, 11):
+            continue
+        S1, S2 = S[l]
+        Hs = _np(m.H[l])[:, cols]
+        dYs = np.ascontiguousarray(_np(dY_in)[:, cols])
+        dZs = np.ascontiguousarray(_np(dZ)[:, cols])
+        _ok(f"dZ[{l}] sampled", dZs, oracle.linear_bwd_input(S2, dYs, NT) * (Hs > 0))
+        _ok(f"dX[{l}] sampled", _np(dX_out)[:, cols], oracle.linear_bwd_input(S1, dZs, NT))
+        dW1, dW2 = m.dW[l]
+        _ok(f"dW2[{l}] full batch", _np(dW2), oracle.linear_bwd_weight(S2, _np(m.H[l]), _np(dY_in), NT))
+        _ok(f"dW1[{l}] full batch", _np(dW1), oracle.linear_bwd_weight(S1, _np(m.X[l]), _np(dZ), NT))
