@@ -194,6 +194,26 @@ __global__ void til_fill_kernel(int64_t rows, int nkb, int KC, int RB, const int
     }
 }
 
+// tmsplit[s] for every segment: the first entry whose column lies in the
+// tile's last kHybTC rows, rounded up to an even index (the pair that straddles
+// stays in the shared-memory part), else the segment end.  Padding entries
+// (offset < 0) come last in a segment and never start the TMEM part.
+__global__ void til_split_kernel(int64_t nseg, int KC, const int32_t *__restrict__ seg, const int2 *__restrict__ ent,
+                                 int32_t *__restrict__ split) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nseg) return;
+    const int s0 = seg[s], s1 = seg[s + 1];
+    const int off0 = (KC - kHybTC) * kTilRowBytes;
+    int sp = s1;
+    for (int e = s0; e < s1; ++e)
+        if (ent[e].x >= off0) {
+            sp = e;
+            break;
+        }
+    sp = s0 + ((sp - s0 + 1) & ~1);
+    split[s] = sp < s1 ? sp : s1;
+}
+
 // max over tiles of the tile's entry count (single block, fixed order)
 __global__ void til_max_kernel(int64_t ntiles, int RB, const int32_t *__restrict__ seg, int64_t *__restrict__ out) {
     __shared__ int32_t sh[256];
@@ -455,6 +475,10 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
                                                                          slotmap, t.rowpos, t.seg, w->vals, t.ent,
                                                                          t.vidx);
             til_max_kernel<<<1, 256, 0, st>>>((int64_t)t.nrb * t.nkb, t.RB, t.seg, mx + si);
+            if (si == 0 || si == 2) {  // the big tilings (RB = 128, KC = 192): split-source SpMM
+                if (dmalloc(&t.tmsplit, nseg + 8) != cudaSuccess) return SP_ERR_ALLOC;
+                til_split_kernel<<<(unsigned)((nseg + 255) / 256), 256, 0, st>>>(nseg, t.KC, t.seg, t.ent, t.tmsplit);
+            }
             til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp, 2, t.seg, mx + NS + si);
             til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp, 3, t.seg, mx + 2 * NS + si);
             cudaFreeAsync(cnt, st);
@@ -484,6 +508,8 @@ void free_tilings(sp_weight_s *w) {
         cudaFree(t.vidx);
         cudaFree(t.rowpos);
         cudaFree(t.rowmap);
+        cudaFree(t.tmsplit);
+        t.tmsplit = nullptr;
         t.seg = nullptr;
         t.ent = nullptr;
         t.vidx = nullptr;

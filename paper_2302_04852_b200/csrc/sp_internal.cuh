@@ -47,6 +47,10 @@ struct sp_tiling {
     // rowmap == nullptr means identity (conv tap tilings)
     int32_t *rowpos;   // [rows]
     int32_t *rowmap;   // [nrb * RB]
+    // split-source SpMM (spmm_hyb.cu, big tilings only): tmsplit[s] = the even
+    // entry index from which segment s holds only columns >= KC - kHybTC of its
+    // column block (those tile rows are mirrored in TMEM), or the segment end
+    int32_t *tmsplit;  // [nrb*nkb*RB] (nullptr: not built)
 };
 
 struct sp_weight_s {
@@ -102,6 +106,8 @@ constexpr int kTilPad = 2;
 // inner columns per tile of the TMEM-gather SpMM tilings (til_t): 4 zero + 63 x 4
 // tile columns fill one 256-column TMEM buffer
 constexpr int kTmKC = 63;
+// tile rows the split-source SpMM mirrors in TMEM (the last kHybTC of a tile)
+constexpr int kHybTC = 63;
 constexpr int kTapPad = 4;
 constexpr int kTilRowBytes = 512;
 

@@ -38,13 +38,14 @@ namespace sp {
 namespace {
 
 constexpr int HY_NW = 32, HY_RPW = 4, HY_RB = HY_NW * HY_RPW, HY_BT = 128;
-constexpr int HY_TC = 63;      // tile rows mirrored in TMEM (the last TC of the KC)
+constexpr int HY_TC = kHybTC;  // tile rows mirrored in TMEM (the last TC of the KC)
 constexpr int HY_ISSUE = 8;    // warps issuing a tile's copies
 
 struct HybArgs {
     int64_t rows, B;
     int KC, nkb, cap;
     const int32_t *seg;
+    const int32_t *split;
     const int2 *ent;
     float *out;
     const float *gate;
@@ -105,7 +106,7 @@ __device__ __forceinline__ void hy_gather2(uint32_t t0, uint32_t t1, float (&x)[
         for (int v = 0; v < 4; ++v) x[u][v] = __uint_as_float(r[4 * u + v]);
 }
 
-template <int EPI>
+template <int EPI, bool STATS>
 __global__ void __launch_bounds__(HY_NW * 32, 1) spmm_hyb_kernel(const HybArgs a, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(128) float smem[];  // [2][KC + 1][BT] floats (a zero row before each tile), [2][cap+2] int2
     __shared__ uint64_t full[2], tfull[2];
@@ -121,7 +122,6 @@ __global__ void __launch_bounds__(HY_NW * 32, 1) spmm_hyb_kernel(const HybArgs a
     const int ebuf = a.cap + 2;
     const int ntile = a.nkb;
     const int c0 = a.KC - HY_TC;  // first mirrored tile row
-    const int off0 = c0 * kTilRowBytes;
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base))
@@ -172,9 +172,13 @@ __global__ void __launch_bounds__(HY_NW * 32, 1) spmm_hyb_kernel(const HybArgs a
         issue(0, 0);
         if (ntile > 1) issue(1, 1);
     }
+    // lane l <= RPW: the l-th segment bound of this warp's rows in tile q;
+    // lanes 8 + i: row i's TMEM split (tmsplit)
     auto seg_bounds = [&](int q) -> int {
-        const int32_t *segw = a.seg + ((int64_t)rb * a.nkb + q) * HY_RB + warp * HY_RPW;
-        return lane <= HY_RPW ? __ldg(segw + lane) : 0;
+        const int64_t sb = ((int64_t)rb * a.nkb + q) * HY_RB + warp * HY_RPW;
+        if (lane <= HY_RPW) return __ldg(a.seg + sb + lane);
+        if (lane >= 8 && lane < 8 + HY_RPW) return __ldg(a.split + sb + lane - 8);
+        return 0;
     };
     int sg = seg_bounds(0);
 
@@ -216,48 +220,66 @@ __global__ void __launch_bounds__(HY_NW * 32, 1) spmm_hyb_kernel(const HybArgs a
         auto tc = [&](int off) -> uint32_t { return tcol + (uint32_t)max((off >> 7) + 4 - 4 * c0, 0); };
         bool tm_ok = false;
         unsigned n_tm = 0, n_all = 0;
+        // groups of 4 entries (a last lone pair) of [e0, e1) from shared memory / TMEM
+        auto lds_part = [&](float (&ac)[4], int e0, int e1) {
+            for (int e = e0; e < e1; e += 4) {
+                const int4 p01 = ld_entry_pair(es + e, true);
+                float x[4][4];
+                if (e + 2 < e1) {
+                    const int4 p23 = ld_entry_pair(es + e + 2, true);
+                    lds_vec<4>(reinterpret_cast<const float *>(tb + p01.x), x[0]);
+                    lds_vec<4>(reinterpret_cast<const float *>(tb + p01.z), x[1]);
+                    lds_vec<4>(reinterpret_cast<const float *>(tb + p23.x), x[2]);
+                    lds_vec<4>(reinterpret_cast<const float *>(tb + p23.z), x[3]);
+                    fma_bcast<4>(ac, __int_as_float(p01.y), x[0]);
+                    fma_bcast<4>(ac, __int_as_float(p01.w), x[1]);
+                    fma_bcast<4>(ac, __int_as_float(p23.y), x[2]);
+                    fma_bcast<4>(ac, __int_as_float(p23.w), x[3]);
+                } else {
+                    lds_vec<4>(reinterpret_cast<const float *>(tb + p01.x), x[0]);
+                    lds_vec<4>(reinterpret_cast<const float *>(tb + p01.z), x[1]);
+                    fma_bcast<4>(ac, __int_as_float(p01.y), x[0]);
+                    fma_bcast<4>(ac, __int_as_float(p01.w), x[1]);
+                }
+            }
+        };
+        auto tm_part = [&](float (&ac)[4], int e0, int e1) {
+            for (int e = e0; e < e1; e += 4) {
+                const int4 p01 = ld_entry_pair(es + e, true);
+                float x[4][4];
+                if (e + 2 < e1) {
+                    const int4 p23 = ld_entry_pair(es + e + 2, true);
+                    hy_gather4(tc(p01.x), tc(p01.z), tc(p23.x), tc(p23.z), x);
+                    fma_bcast<4>(ac, __int_as_float(p01.y), x[0]);
+                    fma_bcast<4>(ac, __int_as_float(p01.w), x[1]);
+                    fma_bcast<4>(ac, __int_as_float(p23.y), x[2]);
+                    fma_bcast<4>(ac, __int_as_float(p23.w), x[3]);
+                } else {
+                    hy_gather2(tc(p01.x), tc(p01.z), x);
+                    fma_bcast<4>(ac, __int_as_float(p01.y), x[0]);
+                    fma_bcast<4>(ac, __int_as_float(p01.w), x[1]);
+                }
+            }
+        };
 #pragma unroll
         for (int i = 0; i < HY_RPW; ++i) {
             const int s0 = __shfl_sync(kFull, sg, i), s1 = __shfl_sync(kFull, sg, i + 1);
-            for (int e = s0; e < s1; e += 4) {
-                const int4 p01 = ld_entry_pair(es + e, true);
-                float x[4][4];
-                if (p01.x >= off0 && !tm_ok) {  // mirrored rows: is the copy complete yet?
-                    tm_ok = __shfl_sync(kFull, (int)mbar_test(&tfull[buf], par), 0) != 0;  // warp-uniform
-                    if (tm_ok) hy_after();
-                }
-                const bool use_tm = tm_ok && p01.x >= off0;
-                if (a.stats) {
-                    n_tm += use_tm;
-                    ++n_all;
-                }
-                if (e + 2 < s1) {
-                    const int4 p23 = ld_entry_pair(es + e + 2, true);
-                    if (use_tm) {
-                        hy_gather4(tc(p01.x), tc(p01.z), tc(p23.x), tc(p23.z), x);
-                    } else {
-                        lds_vec<4>(reinterpret_cast<const float *>(tb + p01.x), x[0]);
-                        lds_vec<4>(reinterpret_cast<const float *>(tb + p01.z), x[1]);
-                        lds_vec<4>(reinterpret_cast<const float *>(tb + p23.x), x[2]);
-                        lds_vec<4>(reinterpret_cast<const float *>(tb + p23.z), x[3]);
-                    }
-                    fma_bcast<4>(acc[i], __int_as_float(p01.y), x[0]);
-                    fma_bcast<4>(acc[i], __int_as_float(p01.w), x[1]);
-                    fma_bcast<4>(acc[i], __int_as_float(p23.y), x[2]);
-                    fma_bcast<4>(acc[i], __int_as_float(p23.w), x[3]);
-                } else {  // last pair of the segment
-                    if (use_tm) {
-                        hy_gather2(tc(p01.x), tc(p01.z), x);
-                    } else {
-                        lds_vec<4>(reinterpret_cast<const float *>(tb + p01.x), x[0]);
-                        lds_vec<4>(reinterpret_cast<const float *>(tb + p01.z), x[1]);
-                    }
-                    fma_bcast<4>(acc[i], __int_as_float(p01.y), x[0]);
-                    fma_bcast<4>(acc[i], __int_as_float(p01.w), x[1]);
-                }
+            const int sp = __shfl_sync(kFull, sg, 8 + i);  // [s0, sp): shared memory; [sp, s1): mirrored rows
+            lds_part(acc[i], s0, sp);
+            if (sp < s1 && !tm_ok) {  // is the TMEM copy of this tile complete yet? (non-blocking)
+                tm_ok = __shfl_sync(kFull, (int)mbar_test(&tfull[buf], par), 0) != 0;
+                if (tm_ok) hy_after();
+            }
+            if (tm_ok)
+                tm_part(acc[i], sp, s1);
+            else
+                lds_part(acc[i], sp, s1);
+            if constexpr (STATS) {
+                n_tm += tm_ok ? (unsigned)(s1 - sp) : 0u;
+                n_all += (unsigned)(s1 - s0);
             }
         }
-        if (a.stats && lane == 0) {
+        if (STATS && lane == 0) {
             atomicAdd(a.stats, (unsigned long long)n_tm);
             atomicAdd(a.stats + 1, (unsigned long long)n_all);
         }
@@ -331,7 +353,8 @@ int spmm_hyb_mode() {
 bool launch_spmm_hyb(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,
                      int epi, cudaStream_t st) {
     const sp_tiling &t = w->til[orient][0];
-    if ((B & 3) != 0 || t.seg == nullptr || t.RB != HY_RB || t.KC <= HY_TC || t.nkb == 0) return false;
+    if ((B & 3) != 0 || t.seg == nullptr || t.tmsplit == nullptr || t.RB != HY_RB || t.KC <= HY_TC || t.nkb == 0)
+        return false;
     const size_t tiles = (size_t)2 * (t.KC + 1) * HY_BT * sizeof(float);
     const int cap = (t.max_tile + 2 + 3) & ~3;
     const size_t smem = tiles + (size_t)2 * (cap + 2) * sizeof(int2);
@@ -345,21 +368,26 @@ bool launch_spmm_hyb(const sp_weight_s *w, int orient, int64_t B, const float *i
         cudaMalloc(&stats, 2 * sizeof(unsigned long long));
         cudaMemset(stats, 0, 2 * sizeof(unsigned long long));
     }
-    HybArgs a{t.rows, B, t.KC, t.nkb, cap, t.seg, t.ent, out, gate, t.rowmap, stats};
+    HybArgs a{t.rows, B, t.KC, t.nkb, cap, t.seg, t.tmsplit, t.ent, out, gate, t.rowmap, stats};
     dim3 grid((unsigned)t.nrb, (unsigned)((B + HY_BT - 1) / HY_BT));
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         count_launches(1);
         kern<<<grid, HY_NW * 32, smem, st>>>(a, tmap);
     };
-    if (epi == EPI_RELU) launch(spmm_hyb_kernel<EPI_RELU>);
-    else if (epi == EPI_GATE) launch(spmm_hyb_kernel<EPI_GATE>);
-    else launch(spmm_hyb_kernel<EPI_NONE>);
+    if (stats)
+        launch(spmm_hyb_kernel<EPI_NONE, true>);  // entry counts only (measurement)
+    else if (epi == EPI_RELU)
+        launch(spmm_hyb_kernel<EPI_RELU, false>);
+    else if (epi == EPI_GATE)
+        launch(spmm_hyb_kernel<EPI_GATE, false>);
+    else
+        launch(spmm_hyb_kernel<EPI_NONE, false>);
     if (stats) {
         unsigned long long h[2];
         cudaStreamSynchronize(st);
         cudaMemcpy(h, stats, sizeof(h), cudaMemcpyDeviceToHost);
-        fprintf(stderr, "spmm_hyb: %llu of %llu entry groups gathered from TMEM (cumulative)\n", h[0], h[1]);
+        fprintf(stderr, "spmm_hyb: %llu of %llu entries gathered from TMEM (cumulative)\n", h[0], h[1]);
     }
     return true;
 }
