@@ -11,6 +11,8 @@
 // as the tiled kernels' definition (entries ascending), no atomics.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <climits>
 
@@ -136,6 +138,11 @@ __global__ void __launch_bounds__(256)
 // Gather path wins when staging would move more bytes than gathering:
 // nrb * inner (tile rows streamed per batch column) > nnz (rows gathered).
 bool gather_preferred(const sp_weight_s *w, int orient, int64_t B, bool chunked) {
+    static const int force = [] {  // SP_GATHER=1 / 0: force / forbid the gather kernels (A/B)
+        const char *e = getenv("SP_GATHER");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    if (force >= 0) return force == 1;
     // the gather SpMM walks a whole row per warp: skewed rows (Zipf) would
     // serialise the tail, so only balanced structures take it (the SDDMM's
     // 32-nonzero chunks are balanced by construction)

@@ -74,6 +74,8 @@ SWITCHES = {
     "fused_no_sk": dict(SP_FUSED_SK="0"),
     "fused_no_tmem": dict(SP_FUSED_TMEM="0"),
     "conv_no_sk": dict(SP_CONV_SK="0"),
+    "gather_on": dict(SP_GATHER="1"),
+    "gather_off": dict(SP_GATHER="0"),
 }
 
 
