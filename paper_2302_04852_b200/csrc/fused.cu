@@ -1093,6 +1093,16 @@ bool sk_disabled() {
 
 }  // namespace
 
+// SP_FUSED_KC128=1: the half-warp fused backward on 128-column tiles with
+// three shared-memory stages (two tiles of drift between warps; A/B)
+bool fused_kc128() {
+    static const int v = [] {
+        const char *e = getenv("SP_FUSED_KC128");
+        return (e && e[0] == '1') ? 1 : 0;
+    }();
+    return v != 0;
+}
+
 // SP_FUSED_NW=24|16|28: the stream-K kernel with fewer warps x 4 rows (A/B)
 int fused_nw() {
     static const int v = [] {
@@ -1106,7 +1116,7 @@ int fused_nw() {
 // Stream-K launch of the TMEM kernel (fused backward, or dW alone when dX is
 // null).  Returns false when it does not apply (ragged B, staged entries do
 // not fit, too many entry groups per warp for the TMEM columns).
-template <int TRPW, int TNW = 32, bool HALF = false>
+template <int TRPW, int TNW = 32, bool HALF = false, int NB = 2>
 static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float *X, const float *dY, const float *H,
                           float *dX, float *dW, int64_t B, cudaStream_t st) {
     constexpr int BT = 128, RBT = TRPW * TNW;
@@ -1118,7 +1128,7 @@ static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float 
     const int64_t G = std::min<int64_t>(kNumSMs, T);
     // HALF reads entry pairs up to 6 entries past a segment (masked): slack in the staging
     const int cap = (t.max_tile + (HALF ? 8 : 2) + 3) & ~3;
-    const size_t smem = 2 * ((size_t)(t.KC + 1) * BT * sizeof(float) + (size_t)(cap + 2) * sizeof(int2));
+    const size_t smem = NB * ((size_t)(t.KC + 1) * BT * sizeof(float) + (size_t)(cap + 2) * sizeof(int2));
     if (smem > (size_t)(226 * 1024)) return false;
     CUtensorMap tmap{};
     if (!make_tmap_2d(&tmap, dY, t.inner, B, BT, t.KC)) return false;
@@ -1145,9 +1155,9 @@ static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float 
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<(unsigned)G, TNW * 32, smem, st>>>(a, tmap);
     };
-    if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, 2, false, HALF>);
-    else if (H) go(bwd_fused_sk_kernel<TRPW, TNW, true, false, 2, false, HALF>);
-    else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 2, false, HALF>);
+    if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, NB, false, HALF>);
+    else if (H) go(bwd_fused_sk_kernel<TRPW, TNW, true, false, NB, false, HALF>);
+    else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, NB, false, HALF>);
     JobReduceArgs ja{t.npad, slices, G, t.nrb, t.nkb, RBT, 1, t.seg, t.vidx, nullptr, {}, part, dW};
     job_reduce_kernel<<<dim3((unsigned)(t.nrb * t.nkb), (unsigned)((t.max_tile + 255) / 256)), 256, 0, st>>>(ja);
     count_launches(3);  // refresh, kernel, reduce
@@ -1171,6 +1181,9 @@ static bool launch_sk(const sp_weight_s *w, const float *X, const float *dY, con
     auto fits = [&](const sp_tiling &t, int64_t cols) { return t.seg != nullptr && t.max_warp_groups <= cols * 8; };
     auto fits8 = [&](const sp_tiling &t, int64_t cols) { return t.seg != nullptr && t.max_warp_groups8 <= cols * 4; };
     if (fused_half()) {
+        if (!dw && fused_kc128() && fits8(w->til_f128, sk_dwcols<2, false, 32, true>()) &&
+            launch_sk_rpw<2, 32, true, 3>(w, w->til_f128, X, dY, H, dX, dW, B, st))
+            return true;
         if (dw && fits8(w->til[1][0], sk_dwcols<4, true, 32, true>()) && w->til[1][0].RB == 128 &&
             launch_sk_rpw<4, 32, true>(w, w->til[1][0], X, dY, H, dX, dW, B, st))
             return true;

@@ -76,6 +76,8 @@ struct sp_weight_s {
     // tilings of the TMEM-gather SpMM (spmm_tm.cu): [orientation][variant], KC = kTmKC,
     // RB = 112 (28 compute warps x 4 rows) / 96 (24 x 4) / 128 (16 x 8) / 256 (16 x 16)
     sp_tiling til_t[2][4];
+    // CSC tiling with 128-column tiles for the 3-stage fused backward (SP_FUSED_KC128=1)
+    sp_tiling til_f128;
     // conv handles (sp_weight_create_conv): filter taps and, per tap (x, y),
     // tilings of the OC x IC tap matrix W_xy -- [0]: rows oc / inner ic,
     // [1]: rows ic / inner oc -- whose vidx are slots of THIS handle's CSR.
@@ -155,6 +157,7 @@ bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const floa
 
 // ---- fused.cu: warps per CTA of the fused backward (SP_FUSED_NW A/B switch, default 32)
 int fused_nw();
+bool fused_kc128();
 
 // ---- spmm_tm.cu: TMEM-gather SpMM (B % 4 == 0); false if it does not apply
 int spmm_tm_mode();

@@ -72,6 +72,7 @@ SWITCHES = {
     "fused_nw24": dict(SP_FUSED_NW="24"),
     "fused_nw28": dict(SP_FUSED_NW="28"),
     "fused_no_sk": dict(SP_FUSED_SK="0"),
+    "fused_kc128": dict(SP_FUSED_KC128="1"),
     "fused_no_tmem": dict(SP_FUSED_TMEM="0"),
     "conv_no_sk": dict(SP_CONV_SK="0"),
     "gather_on": dict(SP_GATHER="1"),
