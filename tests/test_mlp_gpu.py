@@ -111,3 +111,29 @@ def test_mlp_full_size_sampled():
         dW1, dW2 = m.dW[l]
         _ok(f"dW2[{l}] full batch", _np(dW2), oracle.linear_bwd_weight(S2, _np(m.H[l]), _np(dY_in), NT))
         _ok(f"dW1[{l}] full batch", _np(dW1), oracle.linear_bwd_weight(S1, _np(m.X[l]), _np(dZ), NT))
+
+
+def test_mlp_sharded_step_matches_full_batch():
+    """The data-parallel algebra on the GPU path without a collective (SURVEY
+    §4 "simulated ranks"): G token shards run one after another on one GPU;
+    their forward outputs are the full-batch outputs of their columns and the
+    sum of their dW is the full-batch dW (what all_reduce(SUM) computes)."""
+    from paper_2302_04852_b200.dp import SparseMLP
+    T, G = 4096, 4
+    c = synth.mlp_case(blocks=2, d_model=768, d_ff=3072, T=T, density=0.05, seed=8)
+    full = SparseMLP(c["layers"], T, "cuda")
+    full.set_batch(torch.from_numpy(c["X0"]), torch.from_numpy(c["target"]), non_blocking=False)
+    full.forward()
+    full.backward(allreduce=False)
+    dW_sum = torch.zeros_like(full.dW_flat)
+    for g in range(G):
+        lo, hi = synth.token_shard(T, G, g)
+        m = SparseMLP(c["layers"], hi - lo, "cuda")
+        m.set_batch(torch.from_numpy(np.ascontiguousarray(c["X0"][:, lo:hi])),
+                    torch.from_numpy(np.ascontiguousarray(c["target"][:, lo:hi])), non_blocking=False)
+        m.forward()
+        m.backward(allreduce=False)
+        _ok(f"shard {g} output", _np(m.X[2]), _np(full.X[2])[:, lo:hi])
+        dW_sum += m.dW_flat
+    torch.cuda.synchronize()
+    _ok("sum of shard dW", _np(dW_sum), _np(full.dW_flat))

@@ -308,3 +308,31 @@ def test_fused_backward(sp, R, C, B, d, gate):
     if B >= 128 and B % 4 == 0:
         a, b = _np(dX), _np(dX2)
         assert np.max(np.abs(a - b)) <= 1e-5 * max(float(np.max(np.abs(b))), 1e-30)
+
+
+def test_random_small_shape_sweep(sp):
+    """SPEC acceptance sweep (S620-S630): 200 seeded instances with
+    (R, C, B) uniform in [1, 128]^3 at sparsity 0, 0.5, 0.9, 0.99 and
+    all-but-one (a single kept weight); fwd, dX, dW and the fused backward
+    against the oracle (B not a multiple of 4 takes the ragged paths)."""
+    g = synth.rng(2302)
+    kinds = [0.0, 0.5, 0.9, 0.99, "one"]
+    for i in range(200):
+        R, C, B = (int(v) for v in g.integers(1, 129, size=3))
+        k = kinds[i % len(kinds)]
+        if k == "one":
+            mask = np.zeros((R, C), np.uint8)
+            mask[int(g.integers(R)), int(g.integers(C))] = 1
+        else:
+            mask = (g.random((R, C)) >= k).astype(np.uint8)
+        W = synth.normal(g, (R, C), 1.0 / C)
+        X = synth.normal(g, (C, B), 1.0)
+        dY = synth.normal(g, (R, B), 1.0)
+        tag = f"sweep {i}: {R}x{C} B={B} {k}"
+        check_linear(sp, W, mask, X, dY, tag)
+        S = oracle.csr_from_mask(W, mask)
+        Wg = sp.sp_weight_create(_dev(W), _dev(mask))
+        fdX, fdW = sp.sp_linear_bwd(Wg, _dev(X), _dev(dY))
+        torch.cuda.synchronize()
+        _assert_tol(f"{tag} fused dX", _np(fdX), oracle.linear_bwd_input(S, dY, NT))
+        _assert_tol(f"{tag} fused dW", _np(fdW), oracle.linear_bwd_weight(S, X, dY, NT))
