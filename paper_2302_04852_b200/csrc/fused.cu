@@ -811,8 +811,11 @@ __global__ void __launch_bounds__(NW * 32, 1)
             // half-warp h takes entries h, 2+h, 4+h, 6+h of each group of 8 (segments
             // have even length, so a group's valid entries are warp-uniform); lane
             // 16h + j covers batch columns 4j.. and 64 + 4j.. (two 16-byte loads per entry)
-            const char *tbh = reinterpret_cast<const char *>(smem + buf * buf_sz + BT + (lane & 15) * VEC);
-            const int2 *esh = es + (lane >> 4);
+            // 32-bit shared-window bases, pinned in registers (an opaque mov: the
+            // compiler would otherwise rematerialize them from %tid in every group)
+            uint32_t tbs, ess;
+            asm volatile("mov.u32 %0, %1;" : "=r"(tbs) : "r"(smem_u32(smem + buf * buf_sz + BT + (lane & 15) * VEC)));
+            asm volatile("mov.u32 %0, %1;" : "=r"(ess) : "r"(smem_u32(ents + buf * ebuf) + (uint32_t)((lane >> 4) - ea) * 8u));
 #pragma unroll 1
             for (int m = 0; m < RPW; ++m) {
                 const int g0 = __shfl_sync(kFull, sg, m), g1 = __shfl_sync(kFull, sg, m + 1);
@@ -825,12 +828,15 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 for (int e = g0; e < g1; e += 8) {
                     float p[4] = {0.f, 0.f, 0.f, 0.f};
                     auto entry = [&](int u) {
-                        const int2 q = esh[e + 2 * u];
+                        int qx, qy;
+                        asm("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(qx), "=r"(qy) : "r"(ess + (uint32_t)(e + 2 * u) * 8u));
+                        const int2 q = make_int2(qx, qy);
                         float x[8];
-                        const float4 lo = *reinterpret_cast<const float4 *>(tbh + q.x);
-                        const float4 hi = *reinterpret_cast<const float4 *>(tbh + q.x + 64 * sizeof(float));
-                        x[0] = lo.x, x[1] = lo.y, x[2] = lo.z, x[3] = lo.w;
-                        x[4] = hi.x, x[5] = hi.y, x[6] = hi.z, x[7] = hi.w;
+                        const uint32_t ta = tbs + (uint32_t)q.x;
+                        asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%8];\n"
+                            "ld.shared.v4.f32 {%4, %5, %6, %7}, [%8+256];"
+                            : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]), "=f"(x[6]), "=f"(x[7])
+                            : "r"(ta));
                         if constexpr (!DWONLY) fma_bcast<8>(dx, __int_as_float(q.y), x);  // dX  (Eq. 1 / Eq. 4)
                         p[u] = dot_vec<8>(rv, x);  // dW partial (Eq. 2 / Eq. 5)
                     };
