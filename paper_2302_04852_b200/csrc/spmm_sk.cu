@@ -176,26 +176,27 @@ __global__ void __launch_bounds__(NW * 32, 1)
         mbar_wait(&full[buf], (q >> 1) & 1);
         int ea, e1t;
         entry_range(id, ea, e1t);
-        const char *tb = reinterpret_cast<const char *>(smem + buf * tile_sz + lane * VEC);
-        const int2 *es = ents + buf * ebuf - ea;
+        // 32-bit shared-window bases pinned in registers (see pin_u32)
+        const uint32_t tbs = pin_u32(smem_u32(smem + buf * tile_sz + lane * VEC));
+        const uint32_t ess = pin_u32(smem_u32(ents + buf * ebuf) - (uint32_t)ea * 8u);
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
             const int s0 = __shfl_sync(kFull, sg, i), s1 = __shfl_sync(kFull, sg, i + 1);
             for (int e = s0; e < s1; e += 4) {
-                const int4 p01 = ld_entry_pair(es + e, true);
-                const int4 p23 = ld_entry_pair(es + e + 2, true);
+                const int4 p01 = lds_entry_pair_s(ess + (uint32_t)e * 8u);
+                const int4 p23 = lds_entry_pair_s(ess + (uint32_t)(e + 2) * 8u);
                 const int off[4] = {p01.x, p01.z, p23.x, p23.z};
                 const float w[4] = {__int_as_float(p01.y), __int_as_float(p01.w), __int_as_float(p23.y),
                                     __int_as_float(p23.w)};
                 float x[4][VEC];
                 if (e + 2 < s1) {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) lds_row_or_zero<VEC, 0>(tb, off[u], x[u]);
+                    for (int u = 0; u < 4; ++u) lds_row_or_zero_s<VEC>(tbs, off[u], x[u]);
 #pragma unroll
                     for (int u = 0; u < 4; ++u) fma_bcast<VEC>(acc[i], w[u], x[u]);
                 } else {  // last pair of the segment
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) lds_row_or_zero<VEC, 0>(tb, off[u], x[u]);
+                    for (int u = 0; u < 2; ++u) lds_row_or_zero_s<VEC>(tbs, off[u], x[u]);
 #pragma unroll
                     for (int u = 0; u < 2; ++u) fma_bcast<VEC>(acc[i], w[u], x[u]);
                 }

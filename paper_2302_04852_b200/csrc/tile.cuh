@@ -94,6 +94,31 @@ __device__ __forceinline__ void lds_row_or_zero(const char *tb, int off, float (
     }
 }
 
+// The same with a 32-bit shared-window base (callers pin it in a register
+// with an opaque mov, so the compiler does not rematerialize it from %tid).
+__device__ __forceinline__ uint32_t pin_u32(uint32_t v) {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
+__device__ __forceinline__ int4 lds_entry_pair_s(uint32_t a) {
+    int4 q;
+    asm("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "r"(a));
+    return q;
+}
+template <int VEC>
+__device__ __forceinline__ void lds_row_or_zero_s(uint32_t tbs, int off, float (&v)[VEC]) {
+    static_assert(VEC == 4, "32-bit-address variant: 16-byte rows only");
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+    asm("{\n.reg .pred q;\nsetp.ge.s32 q, %4, 0;\n@q ld.shared.v4.f32 {%0, %1, %2, %3}, [%5];\n}\n"
+        : "+f"(t.x), "+f"(t.y), "+f"(t.z), "+f"(t.w)
+        : "r"(off), "r"(tbs + (uint32_t)(off >= 0 ? off : 0)));
+    v[0] = t.x;
+    v[1] = t.y;
+    v[2] = t.z;
+    v[3] = t.w;
+}
+
 // Stage rows [k0, k0+nk) x batch columns [b0, b0+BT) of a row-major
 // [nrows x B] fp32 activation into smem tile[nk][BT] (row stride BT),
 // zero-filling batch columns >= B.  16-byte vector path when B % 4 == 0.
