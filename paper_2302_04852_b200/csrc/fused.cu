@@ -857,6 +857,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 if constexpr (!DWONLY) tm_st8(tcol + DX0 + 8 * m, dx);
             }
         } else {
+        const uint32_t tbs = pin_u32(smem_u32(tb));  // 32-bit shared-window base, pinned (see pin_u32)
 #pragma unroll 1
         for (int m = 0; m < RPW; ++m) {
             const int g0 = __shfl_sync(kFull, sg, m), g1 = __shfl_sync(kFull, sg, m + 1);
@@ -877,7 +878,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 // past the segment (length 2 mod 4) is skipped
                 auto entry = [&](int u) {
                     float x[VEC];
-                    lds_vec<VEC>(reinterpret_cast<const float *>(tb + off[u]), x);
+                    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                        : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3])
+                        : "r"(tbs + (uint32_t)off[u]));
                     if constexpr (!DWONLY) fma_bcast<VEC>(dx, w[u], x);   // dX  (Eq. 1 / Eq. 4)
                     p[u] = dot_vec<VEC>(rv, x);    // dW partial (Eq. 2 / Eq. 5)
                 };
