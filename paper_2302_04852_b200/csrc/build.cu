@@ -423,7 +423,9 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
                           {1, 128, kTmKC, 16, 8, &w->til_t[1][2], tm},
                           {0, 256, kTmKC, 16, 16, &w->til_t[0][3], tm},
                           {1, 256, kTmKC, 16, 16, &w->til_t[1][3], tm},
-                          {1, 64, 128, 32, 2, &w->til_f128, fused_kc128()}};
+                          {1, 64, 128, 32, 2, &w->til_f128, fused_kc128()},
+                          {0, 256, 160, 32, 8, &w->til_r256[0], spmm_rb256()},
+                          {1, 256, 160, 32, 8, &w->til_r256[1], spmm_rb256()}};
     constexpr int NS = sizeof(specs) / sizeof(specs[0]);
     int64_t *info = nullptr, *mx = nullptr;
     if (cudaMallocAsync((void **)&info, 2 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
@@ -526,6 +528,7 @@ void free_tilings(sp_weight_s *w) {
     for (auto &o : w->til_t)
         for (auto &t : o) fr(t);
     fr(w->til_f128);
+    for (auto &t : w->til_r256) fr(t);
     if (w->tapdev) cudaFree(w->tapdev);
     w->tapdev = nullptr;
 }

@@ -78,6 +78,8 @@ struct sp_weight_s {
     sp_tiling til_t[2][4];
     // CSC tiling with 128-column tiles for the 3-stage fused backward (SP_FUSED_KC128=1)
     sp_tiling til_f128;
+    // 256-row blocks with 160-column tiles for the SpMM A/B (SP_SPMM_RB256=1): [orientation]
+    sp_tiling til_r256[2];
     // conv handles (sp_weight_create_conv): filter taps and, per tap (x, y),
     // tilings of the OC x IC tap matrix W_xy -- [0]: rows oc / inner ic,
     // [1]: rows ic / inner oc -- whose vidx are slots of THIS handle's CSR.
@@ -157,6 +159,7 @@ bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const floa
 
 // ---- fused.cu: warps per CTA of the fused backward (SP_FUSED_NW A/B switch, default 32)
 int fused_nw();
+bool spmm_rb256();
 bool fused_kc128();
 
 // ---- spmm_tm.cu: TMEM-gather SpMM (B % 4 == 0); false if it does not apply

@@ -367,6 +367,16 @@ bool conv_spmm_vec(const sp_weight_s *w, int orient, int64_t B, const float *in,
 
 }  // namespace
 
+// SP_SPMM_RB256=1: 256-row blocks (32 warps x 8 rows, KC = 160): half the tile
+// fill per entry, more accumulator registers (A/B measurements)
+bool spmm_rb256() {
+    static const int v = [] {
+        const char *e = getenv("SP_SPMM_RB256");
+        return (e && e[0] == '1') ? 1 : 0;
+    }();
+    return v != 0;
+}
+
 // Conv products as tap-tiled SpMM (see conv.cu): in = padded activation
 // [inner x Lp], taps[t] tilings of orientation `orient`, shift sh[t] columns;
 // virtual output columns Nv = OHv * Wv * B stored compactly.  Narrower batch
@@ -398,6 +408,12 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
         const int mode = spmm_sk_mode();
         const bool sk = mode == 1 || (mode < 0 && items < 2 * kNumSMs && t0.nkb >= 8);
         if (sk && launch_spmm_sk(w, orient, B, in, out, gate, epi, st)) return;
+    }
+    if (spmm_rb256() && (B & 3) == 0 && w->til_r256[orient].seg) {  // A/B: 256-row blocks, 32 warps x 8 rows
+        const sp_tiling &t = w->til_r256[orient];
+        launch_refresh(t, w->vals, w->nnz, st);
+        launch_cfg<4, 8, 32>(t, B, in, out, gate, epi, st);
+        return;
     }
     // Choose the largest row block and batch vector that still fill the GPU.
     int vec = B <= 32 ? 1 : (B <= 64 || (B & 3)) ? 2 : 4;

@@ -62,6 +62,7 @@ SWITCHES = {
     "spmm_sk0": dict(SP_SPMM_SK="0"),
     "spmm_sk1": dict(SP_SPMM_SK="1"),
     "spmm_nw16": dict(SP_SPMM_NW32="0"),
+    "spmm_rb256": dict(SP_SPMM_RB256="1"),
     "hyb": dict(SP_SPMM_HYB="1"),
     "tm0": dict(SP_SPMM_TM="1", SP_SPMM_TM_VAR="0"),
     "tm1": dict(SP_SPMM_TM="1", SP_SPMM_TM_VAR="1"),
