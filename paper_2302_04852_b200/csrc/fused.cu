@@ -814,6 +814,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
             // 32-bit shared-window bases, pinned in registers (an opaque mov: the
             // compiler would otherwise rematerialize them from %tid in every group)
             uint32_t tbs, ess;
+            const int lane_p = (int)pin_u32((uint32_t)lane);  // lane bits for the reduction, pinned
             asm volatile("mov.u32 %0, %1;" : "=r"(tbs) : "r"(smem_u32(smem + buf * buf_sz + BT + (lane & 15) * VEC)));
             asm volatile("mov.u32 %0, %1;" : "=r"(ess) : "r"(smem_u32(ents + buf * ebuf) + (uint32_t)((lane >> 4) - ea) * 8u));
 #pragma unroll 1
@@ -849,8 +850,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
                         if (rem > 2) entry(1);
                         if (rem > 4) entry(2);
                     }
-                    const float v = reduce4h(p, lane);
-                    if ((lane & GM) == (cnt & GM)) keep = v;
+                    const float v = reduce4h(p, lane_p);
+                    if ((lane_p & GM) == (cnt & GM)) keep = v;
                     ++cnt;
                     if ((cnt & GM) == 0) flush((cnt >> GSH) - 1);
                 }
