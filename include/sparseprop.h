@@ -220,6 +220,23 @@ sp_status sp_mse_grad(const float *Y, const float *T, float *dY, float *loss_out
 /* Plain SGD on the kept weights only: vals[j] -= lr * dW[j]. */
 sp_status sp_sgd(float *vals, const float *dW, int64_t nnz, float lr, sp_stream_t stream);
 
+/* Managed weights (a launch-count optimisation for training loops; SURVEY
+ * C23 "vals is the one mutable copy" still holds).  Every product first
+ * copies the current `vals` into the handle's tiled index copies (one small
+ * kernel per launch), because the caller may have written `vals` in place.
+ * A caller that updates `vals` ONLY through sp_weight_sgd can declare so:
+ * sp_weight_set_managed(W, 1); products then skip that copy while the tiled
+ * weights are current.  Writing `vals` any other way while managed gives
+ * stale results until sp_weight_set_managed is called again (it marks every
+ * tiling stale).  Host-side flag only: no device work, no synchronisation. */
+sp_status sp_weight_set_managed(sp_weight_t W, int managed);
+
+/* Plain SGD on the kept weights of a handle, vals[j] -= lr * dW[j] (the same
+ * rounding as sp_sgd), also writing each new value into the handle's tiled
+ * copies (one kernel).  dW: device [nnz] in CSR slot order.  Enqueued on
+ * `stream`; the caller keeps dW alive until it completes. */
+sp_status sp_weight_sgd(sp_weight_t W, const float *dW, float lr, sp_stream_t stream);
+
 /* Thread-local message for the last non-OK status on this thread. */
 const char *sp_last_error(void);
 

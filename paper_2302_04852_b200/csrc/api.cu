@@ -333,4 +333,18 @@ sp_status sp_sgd(float *vals, const float *dW, int64_t nnz, float lr, sp_stream_
     return check_launch("sp_sgd");
 }
 
+sp_status sp_weight_set_managed(sp_weight_t w, int managed) {
+    SP_CHECK_HANDLE(w, "sp_weight_set_managed");
+    w->managed = managed ? 1 : 0;
+    ++w->version;  // whatever vals hold now: every tiling refreshes at its next use
+    return SP_OK;
+}
+
+sp_status sp_weight_sgd(sp_weight_t w, const float *dW, float lr, sp_stream_t stream) {
+    SP_CHECK_HANDLE(w, "sp_weight_sgd");
+    if (!dW && w->nnz > 0) return fail(SP_ERR_NULL, "sp_weight_sgd: NULL dW");
+    launch_weight_sgd(w, dW, lr, S(stream));
+    return check_launch("sp_weight_sgd");
+}
+
 }  // extern "C"

@@ -214,6 +214,25 @@ __global__ void til_split_kernel(int64_t nseg, int KC, const int32_t *__restrict
     split[s] = sp < s1 ? sp : s1;
 }
 
+// inv[vidx[e]] = e over a tiling's (padded) entries: slot -> entry position
+__global__ void til_inv_kernel(int64_t cap, const int32_t *__restrict__ vidx, int32_t *__restrict__ inv) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < cap) {
+        const int32_t v = vidx[e];
+        if (v >= 0) inv[v] = (int32_t)e;
+    }
+}
+
+// managed SGD: thread per CSR slot, new value to vals and to every tiling
+__global__ void weight_sgd_kernel(int64_t nnz, float *__restrict__ vals, const float *__restrict__ dW, float lr,
+                                  const SgdRef *__restrict__ tab, int ntab) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nnz) return;
+    const float v = fmaf(-lr, dW[j], vals[j]);  // the same rounding as sp_sgd
+    vals[j] = v;
+    for (int k = 0; k < ntab; ++k) tab[k].ent[tab[k].inv[j]].y = __float_as_int(v);
+}
+
 // max over tiles of the tile's entry count (single block, fixed order)
 __global__ void til_max_kernel(int64_t ntiles, int RB, const int32_t *__restrict__ seg, int64_t *__restrict__ out) {
     __shared__ int32_t sh[256];
@@ -478,6 +497,11 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
                                                                          slotmap, t.rowpos, t.seg, w->vals, t.ent,
                                                                          t.vidx);
             til_max_kernel<<<1, 256, 0, st>>>((int64_t)t.nrb * t.nkb, t.RB, t.seg, mx + si);
+            if (w->nnz > 0) {
+                if (dmalloc(&t.inv, w->nnz) != cudaSuccess) return SP_ERR_ALLOC;
+                til_inv_kernel<<<(unsigned)((cap + 255) / 256), 256, 0, st>>>(cap, t.vidx, t.inv);
+            }
+            t.fresh = 1;  // built from vals: the handle's first version
             if (si == 0 || si == 2) {  // the big tilings (RB = 128, KC = 192): split-source SpMM
                 if (dmalloc(&t.tmsplit, nseg + 8) != cudaSuccess) return SP_ERR_ALLOC;
                 til_split_kernel<<<(unsigned)((nseg + 255) / 256), 256, 0, st>>>(nseg, t.KC, t.seg, t.ent, t.tmsplit);
@@ -501,6 +525,16 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
     }
     cudaFreeAsync(info, st);
     cudaFreeAsync(mx, st);
+    // the managed-SGD table: every built tiling
+    std::vector<SgdRef> tab;
+    for (int si = 0; si < NS; ++si)
+        if (specs[si].need && specs[si].t->inv) tab.push_back({specs[si].t->ent, specs[si].t->inv});
+    w->version = 1;
+    w->nsgd = (int)tab.size();
+    if (!tab.empty()) {
+        if (cudaMalloc((void **)&w->sgdtab, tab.size() * sizeof(SgdRef)) != cudaSuccess) return SP_ERR_ALLOC;
+        cudaMemcpy(w->sgdtab, tab.data(), tab.size() * sizeof(SgdRef), cudaMemcpyHostToDevice);
+    }
     return (e == cudaSuccess && cudaGetLastError() == cudaSuccess) ? SP_OK : SP_ERR_CUDA;
 }
 
@@ -513,6 +547,8 @@ void free_tilings(sp_weight_s *w) {
         cudaFree(t.rowmap);
         cudaFree(t.tmsplit);
         t.tmsplit = nullptr;
+        cudaFree(t.inv);
+        t.inv = nullptr;
         t.seg = nullptr;
         t.ent = nullptr;
         t.vidx = nullptr;
@@ -531,6 +567,34 @@ void free_tilings(sp_weight_s *w) {
     for (auto &t : w->til_r256) fr(t);
     if (w->tapdev) cudaFree(w->tapdev);
     w->tapdev = nullptr;
+    if (w->sgdtab) cudaFree(w->sgdtab);
+    w->sgdtab = nullptr;
+    w->nsgd = 0;
+}
+
+void refresh_if_stale(const sp_weight_s *w, const sp_tiling &t, cudaStream_t st) {
+    if (w->managed && t.fresh == w->version) return;
+    launch_refresh(t, w->vals, w->nnz, st);
+    t.fresh = w->version;
+}
+
+void launch_weight_sgd(sp_weight_s *w, const float *dW, float lr, cudaStream_t st) {
+    if (w->nnz > 0) {
+        count_launches(1);
+        weight_sgd_kernel<<<(unsigned)((w->nnz + 255) / 256), 256, 0, st>>>(w->nnz, w->vals, dW, lr, w->sgdtab,
+                                                                            w->nsgd);
+    }
+    ++w->version;  // vals changed; the tilings in the table hold the new values
+    auto mark = [&](sp_tiling &t) {
+        if (t.inv) t.fresh = w->version;
+    };
+    for (auto &o : w->til)
+        for (auto &t : o) mark(t);
+    for (auto &t : w->til_f) mark(t);
+    for (auto &o : w->til_t)
+        for (auto &t : o) mark(t);
+    mark(w->til_f128);
+    for (auto &t : w->til_r256) mark(t);
 }
 
 void launch_refresh(const sp_tiling &t, const float *vals, int64_t nnz, cudaStream_t st) {

@@ -1158,7 +1158,7 @@ static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float 
         return false;
     }
     if (!dwonly) cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
-    launch_refresh(t, w->vals, w->nnz, st);  // CSC-tiled weights from vals (through perm)
+    refresh_if_stale(w, t, st);  // CSC-tiled weights from vals (through perm)
     FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, 0, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
                 0, t.rowmap, slices, t.nrb, dxpart, tickets, B, 1, nullptr, {}, {}, B, 0, 0, 0};
     auto go = [&](auto kern) {
@@ -1358,7 +1358,7 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
             return SP_ERR_ALLOC;
         }
     }
-    launch_refresh(t, w->vals, w->nnz, st);  // CSC-tiled weights from vals (through perm)
+    refresh_if_stale(w, t, st);  // CSC-tiled weights from vals (through perm)
     FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, (int)spl, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
                 direct ? 1 : 0, t.rowmap, slices, t.nrb, nullptr, nullptr, B, 1, nullptr, {}, {}, B, 0, 0, 0};
     auto pick = [&](auto kern) {

@@ -51,6 +51,16 @@ struct sp_tiling {
     // entry index from which segment s holds only columns >= KC - kHybTC of its
     // column block (those tile rows are mirrored in TMEM), or the segment end
     int32_t *tmsplit;  // [nrb*nkb*RB] (nullptr: not built)
+    // managed weights (sp_weight_sgd): inv[slot] = the entry position of a CSR
+    // slot in this tiling; `fresh` = the handle version whose values ent holds
+    int32_t *inv;      // [nnz]
+    mutable uint64_t fresh;
+};
+
+// One tiling's entries as seen by the managed SGD kernel.
+struct SgdRef {
+    int2 *ent;
+    const int32_t *inv;
 };
 
 struct sp_weight_s {
@@ -91,6 +101,13 @@ struct sp_weight_s {
     sp_tiling tapf[kMaxTaps];
     int64_t tapf_groups;
     struct TapDev *tapdev;  // device copy of the tap tilings' pointers [3][kMaxTaps]: orient 0, 1, fused
+    // managed mode (sp_weight_set_managed): vals change only through
+    // sp_weight_sgd, which rewrites the tilings' weights too, so products skip
+    // the per-launch refresh while a tiling is at the handle's version
+    int managed;
+    uint64_t version;
+    int nsgd;
+    SgdRef *sgdtab;  // device [nsgd]: every built (non-tap) tiling
 };
 
 // Tiling variants (RB rows per CTA, KC inner columns per shared-memory tile).
@@ -142,6 +159,10 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st);
 void free_tilings(sp_weight_s *w);
 // ent[e].y = bits(vals[vidx[e]]) for one tiling (before an SpMM launch)
 void launch_refresh(const sp_tiling &t, const float *vals, int64_t nnz, cudaStream_t st);
+// the same unless the handle is managed and the tiling already holds its version
+void refresh_if_stale(const sp_weight_s *w, const sp_tiling &t, cudaStream_t st);
+// managed SGD: vals[j] -= lr dW[j] and the new value written into every tiling
+void launch_weight_sgd(sp_weight_s *w, const float *dW, float lr, cudaStream_t st);
 
 // ---- spmm.cu ----
 // Epilogue codes for the SpMM kernels.

@@ -411,7 +411,7 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
     }
     if (spmm_rb256() && (B & 3) == 0 && w->til_r256[orient].seg) {  // A/B: 256-row blocks, 32 warps x 8 rows
         const sp_tiling &t = w->til_r256[orient];
-        launch_refresh(t, w->vals, w->nnz, st);
+        refresh_if_stale(w, t, st);
         launch_cfg<4, 8, 32>(t, B, in, out, gate, epi, st);
         return;
     }
@@ -424,7 +424,7 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
     if (ctas(0, vec) < 2 * kNumSMs) var = 1;
     while (var == 1 && vec > 1 && ctas(1, vec) < 2 * kNumSMs) vec >>= 1;
     const sp_tiling &t = w->til[orient][var];
-    launch_refresh(t, w->vals, w->nnz, st);
+    refresh_if_stale(w, t, st);
     if (vec == 4) launch_variant<4>(t, var, B, in, out, gate, epi, st);
     else if (vec == 2) launch_variant<2>(t, var, B, in, out, gate, epi, st);
     else launch_variant<1>(t, var, B, in, out, gate, epi, st);

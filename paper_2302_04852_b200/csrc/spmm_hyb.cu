@@ -361,7 +361,7 @@ bool launch_spmm_hyb(const sp_weight_s *w, int orient, int64_t B, const float *i
     if (smem > (size_t)kSmemHyb) return false;
     CUtensorMap tmap{};
     if (!make_tmap_2d(&tmap, in, t.inner, B, HY_BT, t.KC)) return false;
-    launch_refresh(t, w->vals, w->nnz, st);
+    refresh_if_stale(w, t, st);
     static unsigned long long *stats = nullptr;
     static const bool want_stats = getenv("SP_SPMM_HYB_STATS") != nullptr;
     if (want_stats && !stats) {

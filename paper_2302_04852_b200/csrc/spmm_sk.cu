@@ -286,7 +286,7 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
         cudaMallocAsync((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)
         return false;
     cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
-    launch_refresh(t, w->vals, w->nnz, st);
+    refresh_if_stale(w, t, st);
     SkArgs a{t.rows, B, nslice, t.KC, t.nkb, t.nrb, cap, t.seg, t.ent, out, gate, t.rowmap, part, tickets,
              0, nullptr, {}, 0, 0, 0};
     auto go = [&](auto kern) {

@@ -392,7 +392,7 @@ bool launch_spmm_tm(const sp_weight_s *w, int orient, int64_t B, const float *in
     if (nitems > INT32_MAX / 2 || nitems * t.nkb > INT32_MAX / 2) return false;
     CUtensorMap tmap{};
     if (!make_tmap_2d(&tmap, in, t.inner, B, TM_BT, TM_KC)) return false;
-    launch_refresh(t, w->vals, w->nnz, st);
+    refresh_if_stale(w, t, st);
     static const int dbg = [] {
         const char *e = getenv("SP_SPMM_TM_DBG");
         return e ? atoi(e) : 0;

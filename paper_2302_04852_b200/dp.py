@@ -29,7 +29,11 @@ class CudaOps:
         sp.lib()
 
     def create(self, dense, mask):
-        return self.sp.sp_weight_create(dense, mask)
+        # the model updates vals only through sp_weight_sgd: products skip the
+        # per-launch refresh of the tiled weights (managed handles)
+        W = self.sp.sp_weight_create(dense, mask)
+        self.sp.sp_weight_set_managed(W, True)
+        return W
 
     def vals(self, W):
         return W.vals
@@ -55,6 +59,10 @@ class CudaOps:
 
     def sgd(self, vals, dW, lr):
         self.sp.sp_sgd(vals, dW, lr)
+
+    def sgd_weight(self, W, dW, lr):
+        """SGD of a managed handle: vals and its tiled copies in one kernel."""
+        self.sp.sp_weight_sgd(W, dW, lr)
 
 
 class SparseMLP:
@@ -208,8 +216,12 @@ class SparseMLP:
 
     def sgd(self, lr: float):
         for (W1, W2), (d1, d2) in zip(self.W, self.dW):
-            self.ops.sgd(self.ops.vals(W1), d1, lr)
-            self.ops.sgd(self.ops.vals(W2), d2, lr)
+            if hasattr(self.ops, "sgd_weight"):
+                self.ops.sgd_weight(W1, d1, lr)
+                self.ops.sgd_weight(W2, d2, lr)
+            else:
+                self.ops.sgd(self.ops.vals(W1), d1, lr)
+                self.ops.sgd(self.ops.vals(W2), d2, lr)
 
     def step(self, lr: float, allreduce: bool = True):
         """forward -> loss -> backward (+ bucketed all_reduce of dW) -> SGD.

@@ -29,6 +29,7 @@ EXPORTS = [
     "sp_linear_bwd_input_relu", "sp_conv2d_fwd", "sp_conv2d_bwd_input", "sp_conv2d_bwd_weight",
     "sp_mse_scratch_floats", "sp_mse_grad", "sp_sgd", "sp_last_error", "sp_version",
     "sp_launch_count", "sp_linear_bwd", "sp_linear_bwd_relu", "sp_weight_create_conv", "sp_weight_gather",
+    "sp_weight_set_managed", "sp_weight_sgd",
     "sp_conv2d_bwd",
 ]
 
@@ -81,6 +82,8 @@ def lib() -> ct.CDLL:
             "sp_linear_bwd": (st, [vp, vp, vp, vp, vp, i64, vp]),
             "sp_weight_create_conv": (st, [ct.c_int32] * 4 + [vp, vp, vp, ct.POINTER(vp)]),
             "sp_linear_bwd_relu": (st, [vp, vp, vp, vp, vp, vp, i64, vp]),
+            "sp_weight_set_managed": (st, [vp, ct.c_int]),
+            "sp_weight_sgd": (st, [vp, vp, ct.c_float, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -382,6 +385,19 @@ def sp_mse_grad(Y: torch.Tensor, T: torch.Tensor, dY: torch.Tensor, loss: torch.
     _check(lib().sp_mse_grad(_dev(Y, torch.float32, "Y"), _dev(T, torch.float32, "T"),
                              _dev(dY, torch.float32, "dY"), _dev(loss, torch.float32, "loss"),
                              _dev(scratch, torch.float32, "scratch"), n, _stream(stream)))
+
+
+def sp_weight_set_managed(W: SparseWeight, managed: bool = True):
+    """Declare that W.vals changes only through sp_weight_sgd (products then
+    skip the per-launch refresh of the tiled weights); see the C header."""
+    _check(lib().sp_weight_set_managed(W.handle, 1 if managed else 0))
+
+
+def sp_weight_sgd(W: SparseWeight, dW: torch.Tensor, lr: float, stream=None):
+    """W.vals -= lr * dW, tiled copies included (one kernel)."""
+    n = W.nnz
+    _check(lib().sp_weight_sgd(W.handle, _dev(dW, torch.float32, "dW") if n else None, ct.c_float(lr),
+                               _stream(stream)))
 
 
 def sp_sgd(vals: torch.Tensor, dW: torch.Tensor, lr: float, stream=None):

@@ -137,3 +137,56 @@ def test_mlp_sharded_step_matches_full_batch():
         dW_sum += m.dW_flat
     torch.cuda.synchronize()
     _ok("sum of shard dW", _np(dW_sum), _np(full.dW_flat))
+
+
+def test_managed_weights_stay_in_sync():
+    """sp_weight_sgd on a managed handle (products skip the per-launch refresh
+    of the tiled weights) gives bitwise the results of sp_sgd + refreshing
+    products on an unmanaged handle, over several steps and every kernel that
+    reads tiled weights; sp_weight_set_managed after an external vals write
+    makes the next products pick it up."""
+    from paper_2302_04852_b200 import sparseprop as sp
+    c = synth.linear_case(3072, 768, 2048, 0.05, 1.0 / 768, 91)
+    dev = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+    Wm = sp.sp_weight_create(dev(c["W"]), dev(c["mask"]))
+    Wu = sp.sp_weight_create(dev(c["W"]), dev(c["mask"]))
+    sp.sp_weight_set_managed(Wm, True)
+    X, dY = dev(c["X"]), dev(c["dY"])
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for step in range(3):
+        dW = torch.randn(Wm.nnz, device="cuda", generator=g)
+        sp.sp_weight_sgd(Wm, dW, 1e-2)
+        sp.sp_sgd(Wu.vals, dW, 1e-2)
+        for f in (lambda W: sp.sp_linear_fwd(W, X), lambda W: sp.sp_linear_fwd(W, X, relu=True),
+                  lambda W: sp.sp_linear_bwd_input(W, dY), lambda W: sp.sp_linear_bwd(W, X, dY)[0]):
+            assert torch.equal(f(Wm), f(Wu)), step
+    assert torch.equal(Wm.vals, Wu.vals)
+    # an external write while managed is picked up after sp_weight_set_managed
+    Wm.vals.mul_(0.5)
+    Wu.vals.mul_(0.5)
+    sp.sp_weight_set_managed(Wm, True)
+    assert torch.equal(sp.sp_linear_fwd(Wm, X), sp.sp_linear_fwd(Wu, X))
+    torch.cuda.synchronize()
+    S = oracle.csr_from_mask(c["W"], c["mask"]).with_vals(_np(Wm.vals))
+    _ok("managed fwd vs oracle", _np(sp.sp_linear_fwd(Wm, X)), oracle.linear_fwd(S, c["X"], NT))
+
+
+def test_mlp_two_steps_then_forward_matches_oracle():
+    """Training state stays coherent across steps (managed handles): after two
+    SGD steps the next forward is layer-local equal to the oracle's with the
+    updated weights."""
+    from paper_2302_04852_b200.dp import SparseMLP
+    T = 512
+    c = synth.mlp_case(blocks=2, d_model=768, d_ff=3072, T=T, density=0.05, seed=12)
+    m = SparseMLP(c["layers"], T, "cuda")
+    m.set_batch(torch.from_numpy(c["X0"]), torch.from_numpy(c["target"]), non_blocking=False)
+    m.step(1e-3)
+    m.step(1e-3)
+    m.forward()
+    torch.cuda.synchronize()
+    for l, ((w1, m1, w2, m2), (W1, W2)) in enumerate(zip(c["layers"], m.W)):
+        S1 = oracle.csr_from_mask(w1, m1).with_vals(_np(W1.vals))
+        S2 = oracle.csr_from_mask(w2, m2).with_vals(_np(W2.vals))
+        X, H = _np(m.X[l]), _np(m.H[l])
+        _ok(f"H[{l}] after 2 steps", H, np.maximum(oracle.linear_fwd(S1, X, NT), 0.0))
+        _ok(f"X[{l + 1}] after 2 steps", _np(m.X[l + 1]), oracle.linear_fwd(S2, H, NT))
