@@ -423,6 +423,12 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
     };
     if (ctas(0, vec) < 2 * kNumSMs) var = 1;
     while (var == 1 && vec > 1 && ctas(1, vec) < 2 * kNumSMs) vec >>= 1;
+    // the 32-warp layout takes the split-source kernel by default: the same
+    // entries in the same order (bitwise the same result), a third of the
+    // gathers from TMEM (SP_SPMM_HYB=0 keeps the shared-memory-only kernel)
+    if (var == 0 && vec == 4 && spmm_nw32() && spmm_hyb_mode() != 0 &&
+        launch_spmm_hyb(w, orient, B, in, out, gate, epi, st))
+        return;
     const sp_tiling &t = w->til[orient][var];
     refresh_if_stale(w, t, st);
     if (vec == 4) launch_variant<4>(t, var, B, in, out, gate, epi, st);

@@ -217,7 +217,6 @@ __global__ void __launch_bounds__(HY_NW * 32, 1) spmm_hyb_kernel(const HybArgs a
         const int2 *es = ents + buf * ebuf - ea;
         // TMEM column of an entry in the mirrored rows (padding -> the zero columns)
         const uint32_t tcol = tq + (uint32_t)(buf * 256);
-        auto tc = [&](int off) -> uint32_t { return tcol + (uint32_t)max((off >> 7) + 4 - 4 * c0, 0); };
         bool tm_ok = false;
         unsigned n_tm = 0, n_all = 0;
         // groups of 4 entries (a last lone pair) of [e0, e1) from shared memory / TMEM
@@ -243,19 +242,23 @@ __global__ void __launch_bounds__(HY_NW * 32, 1) spmm_hyb_kernel(const HybArgs a
                 }
             }
         };
+        // column = tb0 + (off >> 7) for mirrored rows; a segment's padding entry
+        // (offset < 0) can only be its last slot, which selects the zero columns
+        const uint32_t tb0 = pin_u32(tcol + (uint32_t)(4 - 4 * c0));
         auto tm_part = [&](float (&ac)[4], int e0, int e1) {
             for (int e = e0; e < e1; e += 4) {
                 const int4 p01 = ld_entry_pair(es + e, true);
                 float x[4][4];
                 if (e + 2 < e1) {
                     const int4 p23 = ld_entry_pair(es + e + 2, true);
-                    hy_gather4(tc(p01.x), tc(p01.z), tc(p23.x), tc(p23.z), x);
+                    hy_gather4(tb0 + (uint32_t)(p01.x >> 7), tb0 + (uint32_t)(p01.z >> 7), tb0 + (uint32_t)(p23.x >> 7),
+                               p23.z >= 0 ? tb0 + (uint32_t)(p23.z >> 7) : tcol, x);
                     fma_bcast<4>(ac, __int_as_float(p01.y), x[0]);
                     fma_bcast<4>(ac, __int_as_float(p01.w), x[1]);
                     fma_bcast<4>(ac, __int_as_float(p23.y), x[2]);
                     fma_bcast<4>(ac, __int_as_float(p23.w), x[3]);
                 } else {
-                    hy_gather2(tc(p01.x), tc(p01.z), x);
+                    hy_gather2(tb0 + (uint32_t)(p01.x >> 7), p01.z >= 0 ? tb0 + (uint32_t)(p01.z >> 7) : tcol, x);
                     fma_bcast<4>(ac, __int_as_float(p01.y), x[0]);
                     fma_bcast<4>(ac, __int_as_float(p01.w), x[1]);
                 }
@@ -338,7 +341,8 @@ constexpr int kSmemHyb = 226 * 1024;
 
 }  // namespace
 
-// SP_SPMM_HYB=1 forces the split-source SpMM where it applies, =0 disables it.
+// SP_SPMM_HYB=1 forces the split-source SpMM wherever it applies, =0 disables
+// it; default: for the per-item 32-warp layout (launch_spmm).
 int spmm_hyb_mode() {
     static const int v = [] {
         const char *e = getenv("SP_SPMM_HYB");

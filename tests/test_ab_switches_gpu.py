@@ -64,6 +64,7 @@ SWITCHES = {
     "spmm_nw16": dict(SP_SPMM_NW32="0"),
     "spmm_rb256": dict(SP_SPMM_RB256="1"),
     "hyb": dict(SP_SPMM_HYB="1"),
+    "hyb_off": dict(SP_SPMM_HYB="0"),
     "tm0": dict(SP_SPMM_TM="1", SP_SPMM_TM_VAR="0"),
     "tm1": dict(SP_SPMM_TM="1", SP_SPMM_TM_VAR="1"),
     "tm2": dict(SP_SPMM_TM="1", SP_SPMM_TM_VAR="2"),

@@ -1,7 +1,7 @@
 #!/bin/bash
 # split-source SpMM: parity (subprocess test) + cfg5 layer timings with and without
 cd "$(dirname "$0")/.."
-timeout 600 python -m pytest tests/test_spmm_tm_gpu.py -x -q -k hyb > gpurun_out/hyb_tests.log 2>&1
+timeout 600 python -m pytest tests/test_ab_switches_gpu.py -x -q -k hyb > gpurun_out/hyb_tests.log 2>&1
 echo "rc=$?" >> gpurun_out/hyb_tests.log
 for m in 0 1; do
   echo "== SP_SPMM_HYB=$m" >> gpurun_out/hyb_layer.log
