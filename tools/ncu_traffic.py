@@ -22,7 +22,7 @@ def val(r, name):
 # bwd_fused_sk_kernel<RPW, NW, GATE, DWONLY>: DWONLY=1 is sp_linear_bwd_weight alone
 classes = {"bwd_fused": r"bwd_fused(_sk_kernel<\d+, \d+, \d, 0[,>]|_kernel)",
            "sddmm_dw_only": r"bwd_fused_sk_kernel<\d+, \d+, \d, 1[,>]",
-           "fwd_spmm": r"spmm_tiled"}
+           "fwd_spmm": r"spmm_tiled|spmm_hyb"}
 res = {"source": sys.argv[3], "kernels": {}}
 for r in rows[2:]:
     name = re.sub(r"\(.*", "", r[ix["Kernel Name"]])
