@@ -92,6 +92,7 @@ sp_status build_conv_taps(sp_weight_s *w, int OC, int IC, int KH, int KW, cudaSt
     std::vector<TapDev> td(3 * kMaxTaps);
     constexpr int kFusedRB = 64, kFusedRPW = 2;  // fused conv backward: 32 warps x 2 rows
     std::vector<int64_t> wgroups((IC + kFusedRB - 1) / kFusedRB * (kFusedRB / kFusedRPW), 0);
+    std::vector<int64_t> wgroups8(wgroups.size(), 0);
     for (int tp = 0; tp < KK; ++tp) {
         // rows oc, inner ic  (entries in (oc, ic) order: col_idx ascending)
         std::vector<int32_t> p0(OC + 1, 0), i0, s0;
@@ -131,11 +132,16 @@ sp_status build_conv_taps(sp_weight_s *w, int OC, int IC, int KH, int KW, cudaSt
             std::vector<int32_t> cnt(tf.nkb, 0);
             for (int32_t k = p1[ic]; k < p1[ic + 1]; ++k) cnt[i1[k] / KCf]++;
             for (int kb = 0; kb < tf.nkb; ++kb)
-                wgroups[(ic / kFusedRB) * (kFusedRB / kFusedRPW) + (ic % kFusedRB) / kFusedRPW] +=
-                    (((cnt[kb] + kTapPad - 1) & ~(kTapPad - 1)) + 3) / 4;
+            {
+                const int64_t wi = (ic / kFusedRB) * (kFusedRB / kFusedRPW) + (ic % kFusedRB) / kFusedRPW;
+                const int32_t n = (cnt[kb] + kTapPad - 1) & ~(kTapPad - 1);
+                wgroups[wi] += (n + 3) / 4;
+                wgroups8[wi] += (n + 7) / 8;  // half-warp fused backward: groups of 8
+            }
         }
     }
     w->tapf_groups = wgroups.empty() ? 0 : *std::max_element(wgroups.begin(), wgroups.end());
+    w->tapf_groups8 = wgroups8.empty() ? 0 : *std::max_element(wgroups8.begin(), wgroups8.end());
     if (cudaMalloc((void **)&w->tapdev, td.size() * sizeof(TapDev)) != cudaSuccess) return SP_ERR_ALLOC;
     cudaMemcpy(w->tapdev, td.data(), td.size() * sizeof(TapDev), cudaMemcpyHostToDevice);
     return SP_OK;

@@ -1252,8 +1252,10 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const float *Dp, int64_t Lq, const
     const sp_tiling &t0 = w->tapf[0];
     if (t0.RB != RBF || t0.seg == nullptr) return false;
     const bool dwonly = dX == nullptr;
+    // half-warp entries (8 batch columns per lane) when the groups of 8 fit the TMEM dW columns
+    const bool half = fused_half() && !dwonly && w->tapf_groups8 <= (int64_t)sk_dwcols<TRPW, false, TNW, true>() * 4;
     const int64_t groups_cap = (int64_t)(dwonly ? sk_dwcols<TRPW, true>() : sk_dwcols<TRPW, false>()) * 8;
-    if (w->tapf_groups > groups_cap) return false;
+    if (!half && w->tapf_groups > groups_cap) return false;
     const int64_t slices = (Nv + BT - 1) / BT;
     const int64_t T = (int64_t)t0.nrb * slices * ntap * t0.nkb;
     if (T >= (1LL << 31)) return false;
@@ -1265,7 +1267,7 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const float *Dp, int64_t Lq, const
         tapbase[t] = tot;
         tot += w->tapf[t].npad;
     }
-    const int cap = (mx + 2 + 3) & ~3;
+    const int cap = (mx + (half ? 8 : 2) + 3) & ~3;  // HALF reads entry pairs past a segment (masked)
     const size_t stage = (size_t)(t0.KC + 1) * BT * sizeof(float) + (size_t)(cap + 2) * sizeof(int2);
     const int nbuf = 3 * stage <= (size_t)(226 * 1024) ? 3 : 2;
     if (nbuf * stage > (size_t)(226 * 1024)) return false;
@@ -1297,7 +1299,10 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const float *Dp, int64_t Lq, const
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(nbuf * stage));
         kern<<<(unsigned)G, TNW * 32, nbuf * stage, st>>>(a, tmap);
     };
-    if (nbuf == 3) {
+    if (half) {
+        if (nbuf == 3) go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 3, true, true>);
+        else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 2, true, true>);
+    } else if (nbuf == 3) {
         if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, 3, true>);
         else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 3, true>);
     } else {

@@ -100,6 +100,7 @@ struct sp_weight_s {
     // of one warp's 2 rows over all taps and column blocks
     sp_tiling tapf[kMaxTaps];
     int64_t tapf_groups;
+    int64_t tapf_groups8;  // the same in groups of 8 (half-warp fused conv backward)
     struct TapDev *tapdev;  // device copy of the tap tilings' pointers [3][kMaxTaps]: orient 0, 1, fused
     // managed mode (sp_weight_set_managed): vals change only through
     // sp_weight_sgd, which rewrites the tilings' weights too, so products skip
