@@ -63,6 +63,23 @@ sp_status tiling_from_host(int64_t rows, int64_t inner, int RB, int KC, const st
             vid[e] = slot[k];
         }
     }
+    // tmsplit (TMEM-mirrored SpMM, spmm_sk.cu): the even entry index from which a
+    // segment holds only columns >= KC - kHybTC of its block (padding comes last)
+    std::vector<int32_t> split;
+    if (KC > kHybTC) {
+        split.assign(nseg + 8, 0);
+        const int off0 = (KC - kHybTC) * kTilRowBytes;
+        for (int64_t i = 0; i < nseg; ++i) {
+            int32_t sp = seg[i + 1];
+            for (int32_t e = seg[i]; e < seg[i + 1]; ++e)
+                if (ent[e].x >= off0) {
+                    sp = e;
+                    break;
+                }
+            sp = seg[i] + ((sp - seg[i] + 1) & ~1);
+            split[i] = std::min(sp, seg[i + 1]);
+        }
+    }
     int32_t mx = 0;
     for (int64_t ti = 0; ti < (int64_t)t.nrb * t.nkb; ++ti) mx = std::max(mx, seg[(ti + 1) * RB] - seg[ti * RB]);
     t.max_tile = mx;
@@ -75,6 +92,10 @@ sp_status tiling_from_host(int64_t rows, int64_t inner, int RB, int KC, const st
     cudaMemcpy(t.seg, seg.data(), (nseg + 1) * sizeof(int32_t), cudaMemcpyHostToDevice);
     cudaMemcpy(t.ent, ent.data(), (npad + 8) * sizeof(int2), cudaMemcpyHostToDevice);
     cudaMemcpy(t.vidx, vid.data(), (npad + 8) * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (!split.empty()) {
+        if (cudaMalloc((void **)&t.tmsplit, split.size() * sizeof(int32_t)) != cudaSuccess) return SP_ERR_ALLOC;
+        cudaMemcpy(t.tmsplit, split.data(), split.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    }
     return SP_OK;
 }
 
@@ -122,10 +143,10 @@ sp_status build_conv_taps(sp_weight_s *w, int OC, int IC, int KH, int KW, cudaSt
         if (s != SP_OK) return s;
         for (int o = 0; o < 2; ++o) {
             const sp_tiling &t = w->tap[tp][o];
-            td[o * kMaxTaps + tp] = TapDev{t.seg, t.ent, t.vidx, t.npad};
+            td[o * kMaxTaps + tp] = TapDev{t.seg, t.ent, t.vidx, t.npad, t.tmsplit};
         }
         const sp_tiling &tf = w->tapf[tp];
-        td[2 * kMaxTaps + tp] = TapDev{tf.seg, tf.ent, tf.vidx, tf.npad};
+        td[2 * kMaxTaps + tp] = TapDev{tf.seg, tf.ent, tf.vidx, tf.npad, tf.tmsplit};
         // entry groups (4 entries, a tail may hold 2) per warp of 2 rows, summed over taps
         const int KCf = tf.KC;
         for (int ic = 0; ic < IC; ++ic) {

@@ -22,6 +22,7 @@ struct TapDev {
     const int2 *ent;
     const int32_t *vidx;
     int64_t npad;
+    const int32_t *split;  // tmsplit of the tap tiling (nullptr: none)
 };
 
 // A tiled copy of one orientation's index structure (built once per handle,

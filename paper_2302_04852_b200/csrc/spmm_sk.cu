@@ -39,6 +39,7 @@ struct SkArgs {
     float *out;
     const float *gate;
     const int32_t *rowmap;
+    const int32_t *split;  // TMM: tmsplit of the (linear) tiling
     float *part;    // [G][2][RB][BT] raw sums of cut items (slot 0: the CTA's first item, 1: its last)
     int *tickets;   // [nrb * nslice], zero on entry, reset by the finishing CTA
     // conv (CONV = true): an item's tiles run over (tap t, column block); tap t uses
@@ -50,16 +51,21 @@ struct SkArgs {
     int64_t Wv, OHv, OWv;
 };
 
-template <int RPW, int NW, int EPI, bool CONV>
+// TMM: the last kHybTC rows of every tile are mirrored in tensor memory and a
+// segment's tail (from its tmsplit index) is gathered from there once the copy
+// is complete -- the split-source scheme of spmm_hyb.cu (same entries, same
+// order: bitwise the same result)
+template <int RPW, int NW, int EPI, bool CONV, bool TMM = false>
 __global__ void __launch_bounds__(NW * 32, 1)
     spmm_sk_kernel(const SkArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr int VEC = 4;
     constexpr int BT = 32 * VEC;
     constexpr int RB = NW * RPW;
     extern __shared__ __align__(128) float smem[];  // [2][KC][BT] floats, [2][cap+2] int2
-    __shared__ uint64_t full[2];
-    __shared__ int released[2];
+    __shared__ uint64_t full[2], tfull[2];
+    __shared__ int released[2], ticket[2];
     __shared__ int last_flag;
+    __shared__ uint32_t tmem_base;
     int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * a.KC * BT);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -73,14 +79,42 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const int ebuf = a.cap + 2;
     const int first_item = t0 / tpi;
 
+    constexpr int kIssue = 8;  // warps issuing a tile's TMEM copies (TMM)
+    const int c0 = a.KC - kHybTC;  // first mirrored tile row (TMM)
+    if (TMM && warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
     if (threadIdx.x == 0) {
         mbar_init(&full[0], 1);
         mbar_init(&full[1], 1);
         released[0] = 0;
         released[1] = 0;
+        if (TMM) {
+            mbar_init(&tfull[0], kIssue);
+            mbar_init(&tfull[1], kIssue);
+            ticket[0] = 0;
+            ticket[1] = 0;
+        }
         fence_mbar_init();
     }
+    uint32_t tq = 0;
+    if constexpr (TMM) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        tq = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16);
+        if (warp < 4) {  // zero columns in front of each TMEM buffer (padding entries read them)
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %1, %1, %1};" ::"r"(tq), "r"(0u) : "memory");
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %1, %1, %1};" ::"r"(tq + 256), "r"(0u)
+                         : "memory");
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
     __syncthreads();
+    if constexpr (TMM) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
     struct Tile {
         int rb, sl, r;  // r: tile within the item (tap * nkb + kb for conv)
@@ -127,9 +161,14 @@ __global__ void __launch_bounds__(NW * 32, 1)
         if (ntile > 0) issue(0, 0);
         if (ntile > 1) issue(1, 1);
     }
+    // lane l <= RPW: the l-th segment bound of this warp's rows; TMM: lanes 8 + i
+    // hold row i's tmsplit
+    auto split_of = [&](const Tile &id) -> const int32_t * { return CONV ? a.taps[tap_of(id)].split : a.split; };
     auto seg_bounds = [&](const Tile &id) -> int {
-        const int32_t *segw = seg_of(id) + ((int64_t)id.rb * a.nkb + kb_of(id)) * RB + warp * RPW;
-        return lane <= RPW ? __ldg(segw + lane) : 0;
+        const int64_t sb = ((int64_t)id.rb * a.nkb + kb_of(id)) * RB + warp * RPW;
+        if (lane <= RPW) return __ldg(seg_of(id) + sb + lane);
+        if (TMM && lane >= 8 && lane < 8 + RPW) return __ldg(split_of(id) + sb + lane - 8);
+        return 0;
     };
     // epilogue of rows (rb, lr = warp*RPW + i) for batch columns bl..bl+3
     auto store = [&](int rb, int i, int64_t bl, const float (&v)[VEC]) {
@@ -173,34 +212,132 @@ __global__ void __launch_bounds__(NW * 32, 1)
         const int sg = sgn;
         nid = next_tile(id);
         if (q + 1 < ntile) sgn = seg_bounds(nid);
-        mbar_wait(&full[buf], (q >> 1) & 1);
+        const unsigned par = (unsigned)(q >> 1) & 1u;
+        mbar_wait(&full[buf], par);
+        if constexpr (TMM) {  // the first kIssue warps to start the tile copy its last rows into TMEM
+            if (lane == 0) {
+                const int tk = atomicAdd(&ticket[buf], 1);
+                if (tk == NW - 1) ticket[buf] = 0;
+                if (tk < kIssue) {
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t dst = tmem_base + (uint32_t)(buf * 256 + 4);
+                    const float *src = smem + buf * tile_sz + (size_t)c0 * BT;
+                    for (int c = tk; c < kHybTC; c += kIssue) {
+                        const uint64_t d = (uint64_t)((smem_u32(src + c * BT) >> 4) & 0x3FFF) |
+                                           ((uint64_t)(128 >> 4) << 32) | ((uint64_t)1 << 46);
+                        asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(dst + 4 * c), "l"(d)
+                                     : "memory");
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     smem_u32(&tfull[buf]))
+                                 : "memory");
+                }
+            }
+            __syncwarp();
+        }
         int ea, e1t;
         entry_range(id, ea, e1t);
         // 32-bit shared-window bases pinned in registers (see pin_u32)
         const uint32_t tbs = pin_u32(smem_u32(smem + buf * tile_sz + lane * VEC));
         const uint32_t ess = pin_u32(smem_u32(ents + buf * ebuf) - (uint32_t)ea * 8u);
-#pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-            const int s0 = __shfl_sync(kFull, sg, i), s1 = __shfl_sync(kFull, sg, i + 1);
-            for (int e = s0; e < s1; e += 4) {
+        // groups of 4 entries (a last lone pair) of [e0, e1) from shared memory
+        auto lds_part = [&](float (&ac)[VEC], int e0, int e1) {
+            for (int e = e0; e < e1; e += 4) {
                 const int4 p01 = lds_entry_pair_s(ess + (uint32_t)e * 8u);
                 const int4 p23 = lds_entry_pair_s(ess + (uint32_t)(e + 2) * 8u);
                 const int off[4] = {p01.x, p01.z, p23.x, p23.z};
                 const float w[4] = {__int_as_float(p01.y), __int_as_float(p01.w), __int_as_float(p23.y),
                                     __int_as_float(p23.w)};
                 float x[4][VEC];
-                if (e + 2 < s1) {
+                if (e + 2 < e1) {
 #pragma unroll
                     for (int u = 0; u < 4; ++u) lds_row_or_zero_s<VEC>(tbs, off[u], x[u]);
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) fma_bcast<VEC>(acc[i], w[u], x[u]);
+                    for (int u = 0; u < 4; ++u) fma_bcast<VEC>(ac, w[u], x[u]);
                 } else {  // last pair of the segment
 #pragma unroll
                     for (int u = 0; u < 2; ++u) lds_row_or_zero_s<VEC>(tbs, off[u], x[u]);
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) fma_bcast<VEC>(acc[i], w[u], x[u]);
+                    for (int u = 0; u < 2; ++u) fma_bcast<VEC>(ac, w[u], x[u]);
                 }
             }
+        };
+        if constexpr (!TMM) {
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                const int s0 = __shfl_sync(kFull, sg, i), s1 = __shfl_sync(kFull, sg, i + 1);
+                lds_part(acc[i], s0, s1);
+            }
+        } else {
+            // TMEM column = tb0 + (offset >> 7) in the mirrored rows; padding entries
+            // (offset < 0, at a segment's end) select the zero columns
+            const uint32_t tcol = tq + (uint32_t)(buf * 256);
+            const uint32_t tb0 = pin_u32(tcol + (uint32_t)(4 - 4 * c0));
+            auto tcolumn = [&](int off) -> uint32_t { return off >= 0 ? tb0 + (uint32_t)(off >> 7) : tcol; };
+            bool tm_ok = false;
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                const int s0 = __shfl_sync(kFull, sg, i), s1 = __shfl_sync(kFull, sg, i + 1);
+                const int sp = __shfl_sync(kFull, sg, 8 + i);
+                lds_part(acc[i], s0, sp);
+                if (sp < s1 && !tm_ok) {  // is the TMEM copy of this tile complete yet? (non-blocking)
+                    unsigned ok;
+                    asm volatile(
+                        "{\n.reg .pred P;\nmbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\nselp.u32 %0, 1, 0, P;\n}\n"
+                        : "=r"(ok)
+                        : "r"(smem_u32(&tfull[buf])), "r"(par)
+                        : "memory");
+                    tm_ok = __shfl_sync(kFull, (int)ok, 0) != 0;
+                    if (tm_ok) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                }
+                if (!tm_ok) {
+                    lds_part(acc[i], sp, s1);
+                    continue;
+                }
+                for (int e = sp; e < s1; e += 4) {
+                    const int4 p01 = lds_entry_pair_s(ess + (uint32_t)e * 8u);
+                    const int4 p23 = lds_entry_pair_s(ess + (uint32_t)(e + 2) * 8u);
+                    uint32_t r[16];
+                    if (e + 2 < s1) {
+                        asm volatile(
+                            "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%16];\n"
+                            "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4, %5, %6, %7}, [%17];\n"
+                            "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%8, %9, %10, %11}, [%18];\n"
+                            "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%12, %13, %14, %15}, [%19];\n"
+                            "tcgen05.wait::ld.sync.aligned;"
+                            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+                              "=r"(r[14]), "=r"(r[15])
+                            : "r"(tcolumn(p01.x)), "r"(tcolumn(p01.z)), "r"(tcolumn(p23.x)), "r"(tcolumn(p23.z))
+                            : "memory");
+                        const float w[4] = {__int_as_float(p01.y), __int_as_float(p01.w), __int_as_float(p23.y),
+                                            __int_as_float(p23.w)};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const float x[VEC] = {__uint_as_float(r[4 * u]), __uint_as_float(r[4 * u + 1]),
+                                                  __uint_as_float(r[4 * u + 2]), __uint_as_float(r[4 * u + 3])};
+                            fma_bcast<VEC>(acc[i], w[u], x);
+                        }
+                    } else {
+                        asm volatile(
+                            "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%8];\n"
+                            "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4, %5, %6, %7}, [%9];\n"
+                            "tcgen05.wait::ld.sync.aligned;"
+                            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                              "=r"(r[7])
+                            : "r"(tcolumn(p01.x)), "r"(tcolumn(p01.z))
+                            : "memory");
+                        const float w[2] = {__int_as_float(p01.y), __int_as_float(p01.w)};
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const float x[VEC] = {__uint_as_float(r[4 * u]), __uint_as_float(r[4 * u + 1]),
+                                                  __uint_as_float(r[4 * u + 2]), __uint_as_float(r[4 * u + 3])};
+                            fma_bcast<VEC>(acc[i], w[u], x);
+                        }
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         }
         // release the buffer; the last warp to finish tile q refills it with tile q+2
         __syncwarp();
@@ -209,7 +346,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
             if (atomicAdd(&released[buf], 1) == NW - 1) {
                 released[buf] = 0;
                 __threadfence_block();
-                if (q + 2 < ntile) issue(q + 2, buf);
+                if (q + 2 < ntile) {
+                    if constexpr (TMM) mbar_wait(&tfull[buf], (unsigned)(q >> 1) & 1u);  // the copies read the buffer
+                    issue(q + 2, buf);
+                }
             }
         }
         if (id.r != tpi - 1 && q != ntile - 1) continue;
@@ -259,6 +399,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
         for (int i = 0; i < RPW; ++i) store(id.rb, i, bl, sum[i]);
     }
+    if constexpr (TMM) {  // the copies of the last tiles complete before TMEM is released
+        if (threadIdx.x == 0)
+            for (int q = ntile > 2 ? ntile - 2 : 0; q < ntile; ++q) mbar_wait(&tfull[q & 1], (unsigned)(q >> 1) & 1u);
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+    }
 }
 
 }  // namespace
@@ -287,13 +434,21 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
         return false;
     cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
     refresh_if_stale(w, t, st);
-    SkArgs a{t.rows, B, nslice, t.KC, t.nkb, t.nrb, cap, t.seg, t.ent, out, gate, t.rowmap, part, tickets,
-             0, nullptr, {}, 0, 0, 0};
+    SkArgs a{t.rows, B, nslice, t.KC, t.nkb, t.nrb, cap, t.seg, t.ent, out, gate, t.rowmap, t.tmsplit, part,
+             tickets, 0, nullptr, {}, 0, 0, 0};
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<(unsigned)G, NW * 32, smem, st>>>(a, tmap);
     };
-    if (epi == EPI_RELU) go(spmm_sk_kernel<RPW, NW, EPI_RELU, false>);
+    // the TMEM mirror of the tiles' last rows only when forced (SP_SPMM_HYB=1): on
+    // the linear stream-K shapes it measured slower (768-row layer, B = 2048 /
+    // 4096: 83 -> 87 / 131 -> 143 us; the copies cover a third of a 192-row tile)
+    const bool tmm = spmm_hyb_mode() == 1 && t.tmsplit != nullptr && t.KC > kHybTC;
+    if (tmm) {
+        if (epi == EPI_RELU) go(spmm_sk_kernel<RPW, NW, EPI_RELU, false, true>);
+        else if (epi == EPI_GATE) go(spmm_sk_kernel<RPW, NW, EPI_GATE, false, true>);
+        else go(spmm_sk_kernel<RPW, NW, EPI_NONE, false, true>);
+    } else if (epi == EPI_RELU) go(spmm_sk_kernel<RPW, NW, EPI_RELU, false>);
     else if (epi == EPI_GATE) go(spmm_sk_kernel<RPW, NW, EPI_GATE, false>);
     else go(spmm_sk_kernel<RPW, NW, EPI_NONE, false>);
     count_launches(1);
@@ -329,12 +484,19 @@ bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const floa
         cudaMallocAsync((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)
         return false;
     cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
-    SkArgs a{t0.rows, B, nslice, t0.KC, t0.nkb, t0.nrb, cap, nullptr, nullptr, out, nullptr, nullptr, part, tickets,
-             ntap, w->tapdev + orient * kMaxTaps, {}, Wv, OHv, OWv};
+    SkArgs a{t0.rows, B, nslice, t0.KC, t0.nkb, t0.nrb, cap, nullptr, nullptr, out, nullptr, nullptr, nullptr,
+             part, tickets, ntap, w->tapdev + orient * kMaxTaps, {}, Wv, OHv, OWv};
     for (int t = 0; t < ntap; ++t) a.sh[t] = sh[t];
-    auto kern = spmm_sk_kernel<RPW, NW, EPI_NONE, true>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)G, NW * 32, smem, st>>>(a, tmap);
+    // conv tap tiles have 128 rows: the TMEM mirror covers half of them (cfg3
+    // fwd / dX 206 -> 202 / 201 us); SP_SPMM_HYB=0 turns it off
+    bool tmm = spmm_hyb_mode() != 0 && t0.KC > kHybTC;
+    for (int t = 0; t < ntap; ++t) tmm = tmm && w->tap[t][orient].tmsplit != nullptr && w->tap[t][orient].KC == t0.KC;
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<(unsigned)G, NW * 32, smem, st>>>(a, tmap);
+    };
+    if (tmm) go(spmm_sk_kernel<RPW, NW, EPI_NONE, true, true>);
+    else go(spmm_sk_kernel<RPW, NW, EPI_NONE, true>);
     count_launches(1);
     cudaFreeAsync(part, st);
     cudaFreeAsync(tickets, st);
