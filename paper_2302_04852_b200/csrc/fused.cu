@@ -932,14 +932,31 @@ __global__ void __launch_bounds__(NW * 32, 1)
                     *reinterpret_cast<float4 *>(dst) = make_float4(o[0], o[1], o[2], o[3]);
                     return;
                 }
+                // gate H == X (the DP step's ReLU'): the row's X slice is already in
+                // TMEM -- lane 16h + j holds columns 4j.. (h = 0) and 64 + 4j.. (h = 1),
+                // exactly the 4 columns this lane stores (loaded before any divergence)
+                float hx[4] = {0.f, 0.f, 0.f, 0.f};
+                const bool gate_tm = HALF && GATE && a.H == a.X;
+                if constexpr (HALF && GATE) {
+                    if (gate_tm) {
+                        float rv8[8];
+                        tm_ld8(tcol + RV0 + 8 * i, rv8);
+                        const bool h = (lane & 16) != 0;
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) hx[v] = h ? rv8[4 + v] : rv8[v];
+                    }
+                }
                 const int64_t r = __ldg(a.rowmap + r_base + i);
                 if (r < 0 || r >= a.nrow || bl >= a.B) return;
                 if (GATE) {
-                    const float4 hv = __ldg(reinterpret_cast<const float4 *>(a.H + r * a.B + bl));
-                    o[0] = hv.x > 0.f ? o[0] : 0.f;
-                    o[1] = hv.y > 0.f ? o[1] : 0.f;
-                    o[2] = hv.z > 0.f ? o[2] : 0.f;
-                    o[3] = hv.w > 0.f ? o[3] : 0.f;
+                    if (!gate_tm) {
+                        const float4 hv = __ldg(reinterpret_cast<const float4 *>(a.H + r * a.B + bl));
+                        hx[0] = hv.x, hx[1] = hv.y, hx[2] = hv.z, hx[3] = hv.w;
+                    }
+                    o[0] = hx[0] > 0.f ? o[0] : 0.f;
+                    o[1] = hx[1] > 0.f ? o[1] : 0.f;
+                    o[2] = hx[2] > 0.f ? o[2] : 0.f;
+                    o[3] = hx[3] > 0.f ? o[3] : 0.f;
                 }
                 *reinterpret_cast<float4 *>(a.dX + r * a.B + bl) = make_float4(o[0], o[1], o[2], o[3]);
             };

@@ -336,3 +336,18 @@ def test_random_small_shape_sweep(sp):
         torch.cuda.synchronize()
         _assert_tol(f"{tag} fused dX", _np(fdX), oracle.linear_bwd_input(S, dY, NT))
         _assert_tol(f"{tag} fused dW", _np(fdW), oracle.linear_bwd_weight(S, X, dY, NT))
+
+
+@pytest.mark.parametrize("R,C,B", [(768, 3072, 2048), (3072, 768, 16384), (500, 300, 200)])
+def test_fused_backward_gate_is_x(sp, R, C, B):
+    """The DP step's ReLU' gate is the layer input itself (H == X): the fused
+    backward then reads the gate from the X rows it already holds in TMEM."""
+    c = synth.linear_case(R, C, B, 0.05, 1.0 / C, R + 7 * B)
+    X = np.maximum(c["X"], 0.0).astype(np.float32)   # a post-ReLU input (exact zeros)
+    S = oracle.csr_from_mask(c["W"], c["mask"])
+    Wg = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))
+    Xg = _dev(X)
+    dX, dW = sp.sp_linear_bwd(Wg, Xg, _dev(c["dY"]), H=Xg)
+    torch.cuda.synchronize()
+    _assert_tol("fused dX (gate = X)", _np(dX), oracle.linear_bwd_input(S, c["dY"], NT) * (X > 0))
+    _assert_tol("fused dW (gate = X)", _np(dW), oracle.linear_bwd_weight(S, X, c["dY"], NT))
