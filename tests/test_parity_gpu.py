@@ -351,3 +351,13 @@ def test_fused_backward_gate_is_x(sp, R, C, B):
     torch.cuda.synchronize()
     _assert_tol("fused dX (gate = X)", _np(dX), oracle.linear_bwd_input(S, c["dY"], NT) * (X > 0))
     _assert_tol("fused dW (gate = X)", _np(dW), oracle.linear_bwd_weight(S, X, c["dY"], NT))
+
+
+@pytest.mark.parametrize("R,C,B,kind", [(3072, 768, 2052, "uniform"), (2048, 1536, 2308, "zipf"),
+                                        (3000, 1000, 2560, "uniform")])
+def test_split_source_spmm_shapes(sp, R, C, B, kind):
+    """Shapes that take the default split-source SpMM (32-warp per-item grid,
+    TMEM-mirrored tile rows) with a partial last batch slice, ragged row / column
+    blocks (R, C not multiples of 128 / 192) and skewed rows."""
+    c = synth.linear_case(R, C, B, 0.05, 1.0 / C, R + B, kind)
+    check_linear(sp, c["W"], c["mask"], c["X"], c["dY"], f"split-source {R}x{C} B={B} {kind}")
