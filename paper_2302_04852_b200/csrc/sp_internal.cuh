@@ -124,14 +124,14 @@ constexpr int kTilNW[2] = {16, 8};  // warps per CTA of the kernels using each v
 // all-zero row kernels keep just before a tile (or is skipped by a predicated
 // load).  Entry columns are stored as byte offsets of a 128-float tile row
 // (kTilRowBytes); kernels with narrower tiles shift them down.  Conv tap
-// tilings keep groups of 4 (kTapPad).
+// tilings are padded the same way (kTapPad).
 constexpr int kTilPad = 2;
 // inner columns per tile of the TMEM-gather SpMM tilings (til_t): 4 zero + 63 x 4
 // tile columns fill one 256-column TMEM buffer
 constexpr int kTmKC = 63;
 // tile rows the split-source SpMM mirrors in TMEM (the last kHybTC of a tile)
 constexpr int kHybTC = 63;
-constexpr int kTapPad = 4;
+constexpr int kTapPad = 2;  // (was 4: groups of 4 without tails; even padding wastes fewer slots)
 constexpr int kTilRowBytes = 512;
 
 namespace sp {
