@@ -273,7 +273,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
             // (offset < 0, at a segment's end) select the zero columns
             const uint32_t tcol = tq + (uint32_t)(buf * 256);
             const uint32_t tb0 = pin_u32(tcol + (uint32_t)(4 - 4 * c0));
+            // segments (linear and conv tap tilings) are padded to even lengths, so
+            // only a segment's last slot can be padding
             auto tcolumn = [&](int off) -> uint32_t { return off >= 0 ? tb0 + (uint32_t)(off >> 7) : tcol; };
+            auto tcol_real = [&](int off) -> uint32_t { return tb0 + (uint32_t)(off >> 7); };
             bool tm_ok = false;
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
                             : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
                               "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
                               "=r"(r[14]), "=r"(r[15])
-                            : "r"(tcolumn(p01.x)), "r"(tcolumn(p01.z)), "r"(tcolumn(p23.x)), "r"(tcolumn(p23.z))
+                            : "r"(tcol_real(p01.x)), "r"(tcol_real(p01.z)), "r"(tcol_real(p23.x)), "r"(tcolumn(p23.z))
                             : "memory");
                         const float w[4] = {__int_as_float(p01.y), __int_as_float(p01.w), __int_as_float(p23.y),
                                             __int_as_float(p23.w)};
@@ -325,7 +328,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
                             "tcgen05.wait::ld.sync.aligned;"
                             : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
                               "=r"(r[7])
-                            : "r"(tcolumn(p01.x)), "r"(tcolumn(p01.z))
+                            : "r"(tcol_real(p01.x)), "r"(tcolumn(p01.z))
                             : "memory");
                         const float w[2] = {__int_as_float(p01.y), __int_as_float(p01.w)};
 #pragma unroll
