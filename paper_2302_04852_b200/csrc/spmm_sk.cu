@@ -251,12 +251,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 float x[4][VEC];
                 if (e + 2 < e1) {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) lds_row_or_zero_s<VEC>(tbs, off[u], x[u]);
+                    for (int u = 0; u < 3; ++u) lds_row_s<VEC>(tbs, off[u], x[u]);  // even padding: only the
+                    lds_row_or_zero_s<VEC>(tbs, off[3], x[3]);                        // last slot can be padding
 #pragma unroll
                     for (int u = 0; u < 4; ++u) fma_bcast<VEC>(ac, w[u], x[u]);
                 } else {  // last pair of the segment
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) lds_row_or_zero_s<VEC>(tbs, off[u], x[u]);
+                    lds_row_s<VEC>(tbs, off[0], x[0]);
+                    lds_row_or_zero_s<VEC>(tbs, off[1], x[1]);
 #pragma unroll
                     for (int u = 0; u < 2; ++u) fma_bcast<VEC>(ac, w[u], x[u]);
                 }

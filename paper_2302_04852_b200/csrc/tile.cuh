@@ -106,6 +106,12 @@ __device__ __forceinline__ int4 lds_entry_pair_s(uint32_t a) {
     asm("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "r"(a));
     return q;
 }
+// an entry that cannot be padding (not a segment's last slot): plain load
+template <int VEC>
+__device__ __forceinline__ void lds_row_s(uint32_t tbs, int off, float (&v)[VEC]) {
+    static_assert(VEC == 4, "32-bit-address variant: 16-byte rows only");
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "r"(tbs + (uint32_t)off));
+}
 template <int VEC>
 __device__ __forceinline__ void lds_row_or_zero_s(uint32_t tbs, int off, float (&v)[VEC]) {
     static_assert(VEC == 4, "32-bit-address variant: 16-byte rows only");
