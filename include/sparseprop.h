@@ -23,7 +23,12 @@
  *    sp_weight_create / sp_weight_create_conv synchronise `stream` several
  *    times (to read nnz, the per-block row counts and the tile maxima of
  *    the cached schedule); compute calls never do.
- *  - No atomics anywhere: results are bitwise run-to-run reproducible.
+ *  - No output is accumulated with atomics: every output element (Y, dX,
+ *    dW) is produced by one thread in a fixed order, or, where a stream-K
+ *    schedule cuts a block between CTAs, as raw parts summed in CTA order by
+ *    the last CTA to arrive.  Integer atomics are used only for those
+ *    arrival tickets and for shared-memory buffer release counters.  Results
+ *    are bitwise run-to-run reproducible on a given device and SM budget.
  *  - Errors: every call returns sp_status; no C++ exception crosses the
  *    ABI.  Arguments are validated before any launch; launch failures are
  *    reported as SP_ERR_CUDA.  sp_last_error() gives a thread-local message.
@@ -243,6 +248,15 @@ const char *sp_last_error(void);
 /* Number of kernels this library has launched in the process so far
  * (provenance: bench.py reports the delta over its timed region). */
 uint64_t sp_launch_count(void);
+
+/* SMs the one-wave (stream-K) kernels leave free: their grid is sized to
+ * multiProcessorCount - n SMs of the current device (at least 1) for every
+ * launch that follows, so that a collective running concurrently on another
+ * stream (the data-parallel dW all_reduce) does not push part
+ * of the wave into a second one.  Default 0.  Process-wide host setting (no
+ * device work).  The stream-K kernels' fp32 summation grouping depends on
+ * the grid, so results may change by rounding when n changes. */
+sp_status sp_set_sm_reserve(int32_t n);
 
 /* Library build string (arch, version) for provenance in bench records. */
 const char *sp_version(void);

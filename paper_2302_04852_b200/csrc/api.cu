@@ -3,6 +3,7 @@
 // exception crosses the ABI; every entry point returns sp_status.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <cstdio>
@@ -19,6 +20,63 @@ static std::atomic<unsigned long long> g_launches{0};
 void count_launches(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
 
 void set_error(const std::string &msg) { g_err = msg; }
+
+namespace {
+constexpr int kMaxDev = 64;
+std::mutex g_dev_mu;
+int g_sms[kMaxDev] = {};
+cudaMemPool_t g_pool[kMaxDev] = {};
+bool g_pool_done[kMaxDev] = {};
+
+int cur_dev() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+}  // namespace
+
+std::atomic<int> g_sm_reserve{0};
+
+int num_sms() {
+    const int d = cur_dev();
+    int n = 148;
+    if (d >= 0 && d < kMaxDev) {
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        if (g_sms[d] == 0) {
+            int v = 0;
+            g_sms[d] = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) == cudaSuccess && v > 0 ? v : 148;
+        }
+        n = g_sms[d];
+    }
+    return std::max(1, n - g_sm_reserve.load());
+}
+
+cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t st) {
+    const int d = cur_dev();
+    cudaMemPool_t pool = nullptr;
+    if (d >= 0 && d < kMaxDev) {
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        if (!g_pool_done[d]) {
+            g_pool_done[d] = true;
+            cudaMemPoolProps pp{};
+            pp.allocType = cudaMemAllocationTypePinned;
+            pp.location.type = cudaMemLocationTypeDevice;
+            pp.location.id = d;
+            if (cudaMemPoolCreate(&g_pool[d], &pp) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(g_pool[d], cudaMemPoolAttrReleaseThreshold, &thr);
+            } else {
+                g_pool[d] = nullptr;
+                cudaGetLastError();
+            }
+        }
+        pool = g_pool[d];
+    }
+    if (pool) return cudaMallocFromPoolAsync(p, bytes, pool, st);
+    return cudaMallocAsync(p, bytes, st);
+}
+
+cudaError_t scratch_free(void *p, cudaStream_t st) { return cudaFreeAsync(p, st); }
 
 sp_status check_launch(const char *what) {
     const cudaError_t e = cudaGetLastError();
@@ -79,6 +137,12 @@ const char *sp_last_error(void) { return g_err.c_str(); }
 
 uint64_t sp_launch_count(void) { return g_launches.load(); }
 
+sp_status sp_set_sm_reserve(int32_t n) {
+    if (n < 0) return fail(SP_ERR_SHAPE, "sp_set_sm_reserve: n must be >= 0");
+    sp::g_sm_reserve.store(n);
+    return SP_OK;
+}
+
 const char *sp_version(void) { return "libsparseprop 0.2 sm_100a fp32 (CUDA cores, TMEM state, deterministic: no atomic output accumulation)"; }
 
 sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8_t *mask,
@@ -89,25 +153,6 @@ sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8
     if (R < 1 || C < 1) return fail(SP_ERR_SHAPE, "sp_weight_create: R and C must be >= 1");
     if (R > kI32Max || C > kI32Max || R * C > kI32Max)
         return fail(SP_ERR_OVERFLOW, "sp_weight_create: R*C must fit int32");
-    {
-        // Scratch buffers (SDDMM split partials) come from the stream-ordered
-        // default pool; keep freed memory cached instead of returning it to
-        // the OS at every synchronisation (which made launches pay page
-        // mapping costs).  Once per device.
-        static std::mutex mu;
-        static bool done[64] = {};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        std::lock_guard<std::mutex> lk(mu);
-        if (dev >= 0 && dev < 64 && !done[dev]) {
-            cudaMemPool_t pool;
-            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-                uint64_t thr = UINT64_MAX;
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-            }
-            done[dev] = true;
-        }
-    }
     sp_weight_s *w = new (std::nothrow) sp_weight_s();
     if (!w) return fail(SP_ERR_ALLOC, "sp_weight_create: host allocation failed");
     w->magic = SP_MAGIC;

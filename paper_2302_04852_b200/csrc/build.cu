@@ -302,9 +302,9 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
         e = (x);                                    \
         if (e != cudaSuccess) goto fail;            \
     } while (0)
-    SP_TRY(cudaMallocAsync((void **)&rcnt, (size_t)R * sizeof(int32_t), st));
-    SP_TRY(cudaMallocAsync((void **)&ccnt, (size_t)C * sizeof(int32_t), st));
-    SP_TRY(cudaMallocAsync((void **)&info, 4 * sizeof(int64_t), st));
+    SP_TRY(scratch_alloc((void **)&rcnt, (size_t)R * sizeof(int32_t), st));
+    SP_TRY(scratch_alloc((void **)&ccnt, (size_t)C * sizeof(int32_t), st));
+    SP_TRY(scratch_alloc((void **)&info, 4 * sizeof(int64_t), st));
     SP_TRY(dmalloc(&w->row_ptr, R + 1));
     SP_TRY(dmalloc(&w->col_ptr, C + 1));
     {
@@ -322,9 +322,9 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
             goto fail;
         }
         if (h[0] > INT32_MAX - 1) {
-            cudaFreeAsync(rcnt, st);
-            cudaFreeAsync(ccnt, st);
-            cudaFreeAsync(info, st);
+            scratch_free(rcnt, st);
+            scratch_free(ccnt, st);
+            scratch_free(info, st);
             set_error("nnz does not fit int32");
             return SP_ERR_OVERFLOW;
         }
@@ -337,7 +337,7 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
     SP_TRY(dmalloc(&w->row_of, w->nnz));
     SP_TRY(dmalloc(&w->row_idx, w->nnz));
     SP_TRY(dmalloc(&w->perm, w->nnz));
-    SP_TRY(cudaMallocAsync((void **)&slot, (size_t)(R * C) * sizeof(int32_t), st));
+    SP_TRY(scratch_alloc((void **)&slot, (size_t)(R * C) * sizeof(int32_t), st));
     csr_compact_kernel<<<(unsigned)((R + 7) / 8), 256, 0, st>>>(R, C, mask, dense, w->row_ptr,
                                                               w->col_idx, w->vals, w->row_of,
                                                               slot);
@@ -352,24 +352,24 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
         const sp_status ts = build_tilings(w, st);
         if (ts != SP_OK) {
             set_error("sp_weight_create: tiling build failed");
-            cudaFreeAsync(slot, st);
-            cudaFreeAsync(rcnt, st);
-            cudaFreeAsync(ccnt, st);
-            cudaFreeAsync(info, st);
+            scratch_free(slot, st);
+            scratch_free(rcnt, st);
+            scratch_free(ccnt, st);
+            scratch_free(info, st);
             return ts;
         }
     }
     // Temporaries are freed in stream order (no second host sync).
-    cudaFreeAsync(slot, st);
-    cudaFreeAsync(rcnt, st);
-    cudaFreeAsync(ccnt, st);
-    cudaFreeAsync(info, st);
+    scratch_free(slot, st);
+    scratch_free(rcnt, st);
+    scratch_free(ccnt, st);
+    scratch_free(info, st);
     return SP_OK;
 fail:
-    if (slot) cudaFreeAsync(slot, st);
-    if (rcnt) cudaFreeAsync(rcnt, st);
-    if (ccnt) cudaFreeAsync(ccnt, st);
-    if (info) cudaFreeAsync(info, st);
+    if (slot) scratch_free(slot, st);
+    if (rcnt) scratch_free(rcnt, st);
+    if (ccnt) scratch_free(ccnt, st);
+    if (info) scratch_free(info, st);
     set_error(std::string("sp_weight_create: ") + cudaGetErrorString(e));
     return e == cudaErrorMemoryAllocation ? SP_ERR_ALLOC : SP_ERR_CUDA;
 #undef SP_TRY
@@ -447,8 +447,8 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
                           {1, 256, 160, 32, 8, &w->til_r256[1], spmm_rb256()}};
     constexpr int NS = sizeof(specs) / sizeof(specs[0]);
     int64_t *info = nullptr, *mx = nullptr;
-    if (cudaMallocAsync((void **)&info, 2 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
-    if (cudaMallocAsync((void **)&mx, 3 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
+    if (scratch_alloc((void **)&info, 2 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
+    if (scratch_alloc((void **)&mx, 3 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
     for (int si = 0; si < NS; ++si) {
         const Spec &sp_ = specs[si];
         if (!sp_.need) continue;  // stays zeroed (seg == nullptr: launchers skip it)
@@ -472,9 +472,9 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
             int32_t *cnt = nullptr;
             if (dmalloc(&t.seg, nseg + 8) != cudaSuccess || dmalloc(&t.ent, cap) != cudaSuccess ||
                 dmalloc(&t.vidx, cap) != cudaSuccess ||
-                cudaMallocAsync((void **)&cnt, (size_t)nseg * sizeof(int32_t), st) != cudaSuccess) {
-                cudaFreeAsync(info, st);
-                cudaFreeAsync(mx, st);
+                scratch_alloc((void **)&cnt, (size_t)nseg * sizeof(int32_t), st) != cudaSuccess) {
+                scratch_free(info, st);
+                scratch_free(mx, st);
                 return SP_ERR_ALLOC;
             }
             {
@@ -508,7 +508,7 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
             }
             til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp, 2, t.seg, mx + NS + si);
             til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp, 3, t.seg, mx + 2 * NS + si);
-            cudaFreeAsync(cnt, st);
+            scratch_free(cnt, st);
         }
     }
     std::vector<int64_t> h(3 * NS), hi(2 * NS);
@@ -523,8 +523,8 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
         t.max_warp_groups8 = h[2 * NS + si];
         t.npad = hi[2 * si];  // padded entry total
     }
-    cudaFreeAsync(info, st);
-    cudaFreeAsync(mx, st);
+    scratch_free(info, st);
+    scratch_free(mx, st);
     // the managed-SGD table: every built tiling
     std::vector<SgdRef> tab;
     for (int si = 0; si < NS; ++si)

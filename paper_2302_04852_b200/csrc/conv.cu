@@ -304,14 +304,14 @@ void launch_conv_fwd(const sp_weight_s *w, const sp_conv_geom &cg, const float *
         const int Hp = g.H + 2 * g.pad, Wp = g.W + 2 * g.pad;
         const int64_t Lp = (int64_t)Hp * Wp * g.B;
         float *Xp = nullptr;
-        if (cudaMallocAsync((void **)&Xp, (size_t)(g.IC * Lp) * sizeof(float), st) == cudaSuccess) {
+        if (scratch_alloc((void **)&Xp, (size_t)(g.IC * Lp) * sizeof(float), st) == cudaSuccess) {
             launch_pad(g.IC, g.H, g.W, Hp, Wp, g.pad, g.pad, g.B, X, Xp, st);
             int sh[kMaxTaps];
             for (int x = 0; x < g.KH; ++x)
                 for (int y = 0; y < g.KW; ++y) sh[x * g.KW + y] = (x * Wp + y) * g.B;
             launch_refresh_taps(w, 0, g.KH * g.KW, st);
             const bool ok = launch_conv_spmm(w, 0, g.B, Xp, Lp, Y, sh, g.KH * g.KW, Wp, g.OH, g.OW, st);
-            cudaFreeAsync(Xp, st);
+            scratch_free(Xp, st);
             if (ok) return;
         }
     }
@@ -336,14 +336,14 @@ void launch_conv_bwd_input(const sp_weight_s *w, const sp_conv_geom &cg, const f
         const int Hq = g.OH + 2 * ph, Wq = g.OW + 2 * pw;
         const int64_t Lq = (int64_t)Hq * Wq * g.B;
         float *Dp = nullptr;
-        if (cudaMallocAsync((void **)&Dp, (size_t)(g.OC * Lq) * sizeof(float), st) == cudaSuccess) {
+        if (scratch_alloc((void **)&Dp, (size_t)(g.OC * Lq) * sizeof(float), st) == cudaSuccess) {
             launch_pad(g.OC, g.OH, g.OW, Hq, Wq, ph, pw, g.B, dY, Dp, st);
             int sh[kMaxTaps];
             for (int x = 0; x < g.KH; ++x)
                 for (int y = 0; y < g.KW; ++y) sh[x * g.KW + y] = ((g.KH - 1 - x) * Wq + (g.KW - 1 - y)) * g.B;
             launch_refresh_taps(w, 1, g.KH * g.KW, st);
             const bool ok = launch_conv_spmm(w, 1, g.B, Dp, Lq, dX, sh, g.KH * g.KW, Wq, g.H, g.W, st);
-            cudaFreeAsync(Dp, st);
+            scratch_free(Dp, st);
             if (ok) return;
         }
     }
@@ -370,9 +370,9 @@ static bool conv_bwd_sk(const sp_weight_s *w, const Geo &g, const float *X, cons
     const int Hq = g.OH + 2 * ph, Wq = g.OW + 2 * pw;
     const int64_t Lq = (int64_t)Hq * Wq * g.B, Nv = (int64_t)g.H * Wq * g.B;
     float *Dp = nullptr, *Xv = nullptr;
-    if (cudaMallocAsync((void **)&Dp, (size_t)(g.OC * Lq) * sizeof(float), st) != cudaSuccess) return false;
-    if (cudaMallocAsync((void **)&Xv, (size_t)(g.IC * Nv) * sizeof(float), st) != cudaSuccess) {
-        cudaFreeAsync(Dp, st);
+    if (scratch_alloc((void **)&Dp, (size_t)(g.OC * Lq) * sizeof(float), st) != cudaSuccess) return false;
+    if (scratch_alloc((void **)&Xv, (size_t)(g.IC * Nv) * sizeof(float), st) != cudaSuccess) {
+        scratch_free(Dp, st);
         return false;
     }
     launch_pad(g.OC, g.OH, g.OW, Hq, Wq, ph, pw, g.B, dY, Dp, st);
@@ -381,8 +381,8 @@ static bool conv_bwd_sk(const sp_weight_s *w, const Geo &g, const float *X, cons
     for (int x = 0; x < g.KH; ++x)
         for (int y = 0; y < g.KW; ++y) sh[x * g.KW + y] = ((g.KH - 1 - x) * Wq + (g.KW - 1 - y)) * g.B;
     const bool ok = launch_conv_bwd_sk(w, Dp, Lq, Xv, Nv, dX, dW, sh, g.KH * g.KW, g.B, Wq, g.H, g.W, st);
-    cudaFreeAsync(Dp, st);
-    cudaFreeAsync(Xv, st);
+    scratch_free(Dp, st);
+    scratch_free(Xv, st);
     return ok;
 }
 
@@ -404,19 +404,19 @@ sp_status launch_conv_bwd_weight(const sp_weight_s *w, const sp_conv_geom &cg, c
         const int Hp = g.H + 2 * g.pad, Wp = g.W + 2 * g.pad;
         const int64_t Lp = (int64_t)Hp * Wp * g.B, Lv = (int64_t)g.OH * Wp * g.B;
         float *Xp = nullptr, *Dv = nullptr;
-        if (cudaMallocAsync((void **)&Xp, (size_t)(g.IC * Lp) * sizeof(float), st) == cudaSuccess &&
-            cudaMallocAsync((void **)&Dv, (size_t)(g.OC * Lv) * sizeof(float), st) == cudaSuccess) {
+        if (scratch_alloc((void **)&Xp, (size_t)(g.IC * Lp) * sizeof(float), st) == cudaSuccess &&
+            scratch_alloc((void **)&Dv, (size_t)(g.OC * Lv) * sizeof(float), st) == cudaSuccess) {
             launch_pad(g.IC, g.H, g.W, Hp, Wp, g.pad, g.pad, g.B, X, Xp, st);
             launch_pad(g.OC, g.OH, g.OW, g.OH, Wp, 0, 0, g.B, dY, Dv, st);
             int sh[kMaxTaps];
             for (int x = 0; x < g.KH; ++x)
                 for (int y = 0; y < g.KW; ++y) sh[x * g.KW + y] = (x * Wp + y) * g.B;
             const bool ok = launch_conv_sddmm(w, g.B, Dv, Xp, Lv, Lp, sh, g.KH * g.KW, dW, st);
-            cudaFreeAsync(Xp, st);
-            cudaFreeAsync(Dv, st);
+            scratch_free(Xp, st);
+            scratch_free(Dv, st);
             if (ok) return SP_OK;
         } else {
-            if (Xp) cudaFreeAsync(Xp, st);
+            if (Xp) scratch_free(Xp, st);
         }
     }
     const int gpr = (w->max_row_nnz + 31) / 32;

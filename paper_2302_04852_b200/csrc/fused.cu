@@ -1088,7 +1088,6 @@ __global__ void __launch_bounds__(256) job_reduce_kernel(const JobReduceArgs a) 
     a.dW[v] = s;
 }
 
-constexpr int kNumSMs = 148;
 
 // SP_FUSED_TMEM=0 selects the register-slot variant (A/B measurements).
 bool tm_disabled() {
@@ -1152,7 +1151,7 @@ static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float 
     const int64_t T = (int64_t)t.nrb * slices * t.nkb;
     // tiny problems (a few tiles) go to the separate kernels: the reduce pass would dominate
     if (T >= (1LL << 31) || T < 32) return false;
-    const int64_t G = std::min<int64_t>(kNumSMs, T);
+    const int64_t G = std::min<int64_t>(num_sms(), T);
     // HALF reads entry pairs up to 6 entries past a segment (masked): slack in the staging
     const int cap = (t.max_tile + (HALF ? 8 : 2) + 3) & ~3;
     const size_t smem = NB * ((size_t)(t.KC + 1) * BT * sizeof(float) + (size_t)(cap + 2) * sizeof(int2));
@@ -1168,10 +1167,10 @@ static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float 
     float *part = nullptr, *dxpart = nullptr;
     int *tickets = nullptr;
     const int64_t nitems = (int64_t)t.nrb * slices;
-    if (cudaMallocAsync((void **)&part, (size_t)(maxjobs * t.npad) * sizeof(float), st) != cudaSuccess) return false;
-    if (!dwonly && (cudaMallocAsync((void **)&dxpart, (size_t)G * 2 * RBT * BT * sizeof(float), st) != cudaSuccess ||
-                    cudaMallocAsync((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)) {
-        cudaFreeAsync(part, st);
+    if (scratch_alloc((void **)&part, (size_t)(maxjobs * t.npad) * sizeof(float), st) != cudaSuccess) return false;
+    if (!dwonly && (scratch_alloc((void **)&dxpart, (size_t)G * 2 * RBT * BT * sizeof(float), st) != cudaSuccess ||
+                    scratch_alloc((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)) {
+        scratch_free(part, st);
         return false;
     }
     if (!dwonly) cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
@@ -1188,10 +1187,10 @@ static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float 
     JobReduceArgs ja{t.npad, slices, G, t.nrb, t.nkb, RBT, 1, t.seg, t.vidx, nullptr, {}, part, dW};
     job_reduce_kernel<<<dim3((unsigned)(t.nrb * t.nkb), (unsigned)((t.max_tile + 255) / 256)), 256, 0, st>>>(ja);
     count_launches(3);  // refresh, kernel, reduce
-    cudaFreeAsync(part, st);
+    scratch_free(part, st);
     if (!dwonly) {
-        cudaFreeAsync(dxpart, st);
-        cudaFreeAsync(tickets, st);
+        scratch_free(dxpart, st);
+        scratch_free(tickets, st);
     }
     return true;
 }
@@ -1276,7 +1275,7 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const float *Dp, int64_t Lq, const
     const int64_t slices = (Nv + BT - 1) / BT;
     const int64_t T = (int64_t)t0.nrb * slices * ntap * t0.nkb;
     if (T >= (1LL << 31)) return false;
-    const int64_t G = std::min<int64_t>(kNumSMs, T);
+    const int64_t G = std::min<int64_t>(num_sms(), T);
     int mx = 0;
     int64_t tapbase[kMaxTaps] = {}, tot = 0;
     for (int t = 0; t < ntap; ++t) {
@@ -1297,10 +1296,10 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const float *Dp, int64_t Lq, const
     float *part = nullptr, *dxpart = nullptr;
     int *tickets = nullptr;
     const int64_t nitems = (int64_t)t0.nrb * slices;
-    if (cudaMallocAsync((void **)&part, (size_t)(maxjobs * tot) * sizeof(float), st) != cudaSuccess) return false;
-    if (!dwonly && (cudaMallocAsync((void **)&dxpart, (size_t)G * 2 * RBF * BT * sizeof(float), st) != cudaSuccess ||
-                    cudaMallocAsync((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)) {
-        cudaFreeAsync(part, st);
+    if (scratch_alloc((void **)&part, (size_t)(maxjobs * tot) * sizeof(float), st) != cudaSuccess) return false;
+    if (!dwonly && (scratch_alloc((void **)&dxpart, (size_t)G * 2 * RBF * BT * sizeof(float), st) != cudaSuccess ||
+                    scratch_alloc((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)) {
+        scratch_free(part, st);
         return false;
     }
     if (!dwonly) cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
@@ -1330,10 +1329,10 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const float *Dp, int64_t Lq, const
     for (int t = 0; t < ntap; ++t) ja.tapbase[t] = tapbase[t];
     job_reduce_kernel<<<dim3((unsigned)(ntap * t0.nrb * t0.nkb), (unsigned)((mx + 255) / 256)), 256, 0, st>>>(ja);
     count_launches(3);  // refresh, kernel, reduce
-    cudaFreeAsync(part, st);
+    scratch_free(part, st);
     if (!dwonly) {
-        cudaFreeAsync(dxpart, st);
-        cudaFreeAsync(tickets, st);
+        scratch_free(dxpart, st);
+        scratch_free(tickets, st);
     }
     return true;
 }
@@ -1356,18 +1355,18 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
     // TMEM variant: staged entries and at most kTmCols*32 padded entries per warp
     const bool tm = sent && !tm_disabled() && t.max_warp_groups <= (int64_t)tm_cols<TNW>() * 8;  // 8 groups per TMEM column
-    if ((int64_t)t.nrb * slices < kNumSMs) return SP_ERR_SHAPE;  // too little parallelism: use the separate kernels
+    if ((int64_t)t.nrb * slices < num_sms()) return SP_ERR_SHAPE;  // too little parallelism: use the separate kernels
     int64_t nsplit, spl;
     if (tm) {
         // one wave: the largest per-CTA slice count that keeps nrb * nsplit <= #SMs
-        spl = std::max<int64_t>(1, (slices * t.nrb + kNumSMs - 1) / kNumSMs);
+        spl = std::max<int64_t>(1, (slices * t.nrb + num_sms() - 1) / num_sms());
         nsplit = (slices + spl - 1) / spl;
-        while (nsplit * t.nrb > kNumSMs) {
+        while (nsplit * t.nrb > num_sms()) {
             ++spl;
             nsplit = (slices + spl - 1) / spl;
         }
     } else {
-        const int64_t want = 2LL * kNumSMs * 4;
+        const int64_t want = 2LL * num_sms() * 4;
         nsplit = std::max<int64_t>(1, std::min<int64_t>(slices, (want + t.nrb - 1) / t.nrb));
         spl = (slices + nsplit - 1) / nsplit;
         nsplit = (slices + spl - 1) / spl;
@@ -1375,7 +1374,7 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     const bool direct = nsplit == 1;
     float *part = dW;
     if (!direct) {
-        if (cudaMallocAsync((void **)&part, (size_t)(nsplit * t.npad) * sizeof(float), st) != cudaSuccess) {
+        if (scratch_alloc((void **)&part, (size_t)(nsplit * t.npad) * sizeof(float), st) != cudaSuccess) {
             set_error("sp_linear_bwd: scratch allocation failed");
             return SP_ERR_ALLOC;
         }
@@ -1400,7 +1399,7 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     }
     if (!direct) {
         launch_split_reduce(t.npad, (int)nsplit, part, t.vidx, dW, st);
-        cudaFreeAsync(part, st);
+        scratch_free(part, st);
     }
     return SP_OK;
 }

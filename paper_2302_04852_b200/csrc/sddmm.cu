@@ -255,7 +255,6 @@ __global__ void split_reduce_kernel(int64_t nnz, int nsplit, const float *__rest
     dW[v] = s;
 }
 
-constexpr int kNumSMs = 148;
 
 template <int VEC, int RPW, int NW>
 sp_status launch_cfg(const sp_weight_s *w, const sp_tiling &t, const float *regop, const float *smemop,
@@ -263,7 +262,7 @@ sp_status launch_cfg(const sp_weight_s *w, const sp_tiling &t, const float *rego
     constexpr int BT = 32 * VEC;
     const int64_t nnz = t.npad;  // partials are kept per (padded) entry
     const int64_t slices = (B + BT - 1) / BT;
-    const int64_t want = (int64_t)ctas_per_sm * kNumSMs * 4;  // >= 4 waves: small tail
+    const int64_t want = (int64_t)ctas_per_sm * num_sms() * 4;  // >= 4 waves: small tail
     int64_t nsplit = std::max<int64_t>(1, std::min<int64_t>(slices, (want + t.nrb - 1) / t.nrb));
     const int64_t spl = (slices + nsplit - 1) / nsplit;
     nsplit = (slices + spl - 1) / spl;
@@ -274,7 +273,7 @@ sp_status launch_cfg(const sp_weight_s *w, const sp_tiling &t, const float *rego
     const bool direct = nsplit == 1;
     float *part = dW;
     if (!direct) {
-        if (cudaMallocAsync((void **)&part, (size_t)(nsplit * nnz) * sizeof(float), st) != cudaSuccess) {
+        if (scratch_alloc((void **)&part, (size_t)(nsplit * nnz) * sizeof(float), st) != cudaSuccess) {
             set_error("sp_linear_bwd_weight: scratch allocation failed");
             return SP_ERR_ALLOC;
         }
@@ -291,7 +290,7 @@ sp_status launch_cfg(const sp_weight_s *w, const sp_tiling &t, const float *rego
     }
     if (!direct) {
         split_reduce_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, st>>>(nnz, (int)nsplit, part, t.vidx, dW);
-        cudaFreeAsync(part, st);
+        scratch_free(part, st);
     }
     return SP_OK;
 }
@@ -339,7 +338,7 @@ bool launch_conv_sddmm(const sp_weight_s *w, int64_t B, const float *dYv, const 
         mx = std::max(mx, w->tap[t][0].max_tile);
     }
     const int64_t slices = (Lv + BT - 1) / BT;
-    const int64_t want = 2LL * kNumSMs * 4;
+    const int64_t want = 2LL * num_sms() * 4;
     const int64_t units = (int64_t)t0.nrb * ntap;
     int64_t nsplit = std::max<int64_t>(1, std::min<int64_t>(slices, (want + units - 1) / units));
     const int64_t spl = (slices + nsplit - 1) / nsplit;
@@ -349,7 +348,7 @@ bool launch_conv_sddmm(const sp_weight_s *w, int64_t B, const float *dYv, const 
     const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)(226 * 1024);
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
     float *part = nullptr;
-    if (cudaMallocAsync((void **)&part, (size_t)(nsplit * tot) * sizeof(float), st) != cudaSuccess) return false;
+    if (scratch_alloc((void **)&part, (size_t)(nsplit * tot) * sizeof(float), st) != cudaSuccess) return false;
     TapBase tbv;
     for (int t = 0; t < kMaxTaps; ++t) tbv.v[t] = tapbase[t];
     SddmmArgs a{t0.rows, t0.inner, Lv, t0.KC, t0.nkb, (int)spl, cap, 1, nullptr, nullptr, nullptr, dYv, Xp,
@@ -363,7 +362,7 @@ bool launch_conv_sddmm(const sp_weight_s *w, int64_t B, const float *dYv, const 
     count_launches(2);
     kern<<<dim3((unsigned)t0.nrb, (unsigned)nsplit, (unsigned)ntap), NW * 32, smem, st>>>(a, tmap);
     conv_split_reduce_kernel<<<dim3(64, ntap), 256, 0, st>>>(w->tapdev, tbv, tot, (int)nsplit, part, dW);
-    cudaFreeAsync(part, st);
+    scratch_free(part, st);
     return true;
 }
 
@@ -386,7 +385,7 @@ sp_status launch_sddmm(const sp_weight_s *w, const float *X, const float *dY, fl
     const float *smemop = orient ? dY : X;
     const int vec = B <= 32 ? 1 : (B <= 64 || (B & 3)) ? 2 : 4;
     // small problems (few row blocks and slices) use the small tiling
-    const int var = (int64_t)w->til[orient][0].nrb * ((B + 32 * vec - 1) / (32 * vec)) < kNumSMs ? 1 : 0;
+    const int var = (int64_t)w->til[orient][0].nrb * ((B + 32 * vec - 1) / (32 * vec)) < num_sms() ? 1 : 0;
     const sp_tiling &t = w->til[orient][var];
     if (vec == 4) return launch_vec<4>(w, t, var, regop, smemop, dW, B, st);
     if (vec == 2) return launch_vec<2>(w, t, var, regop, smemop, dW, B, st);

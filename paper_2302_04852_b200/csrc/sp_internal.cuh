@@ -144,6 +144,17 @@ void count_launches(int n);
 // Launch-error check after an asynchronous launch.
 sp_status check_launch(const char *what);
 
+// SMs a one-wave (stream-K) grid is sized to on the current device: the
+// device's multiProcessorCount, less the reserve set by sp_set_sm_reserve
+// (SMs left free for a concurrent collective), at least 1.
+int num_sms();
+
+// Stream-ordered scratch from a library-owned memory pool per device (its
+// release threshold is raised so freed blocks stay cached; the caller's
+// default pool is left alone).  Same contract as cudaMallocAsync / FreeAsync.
+cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t st);
+cudaError_t scratch_free(void *p, cudaStream_t st);
+
 inline cudaStream_t S(sp_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // ---- tmap.cu ----

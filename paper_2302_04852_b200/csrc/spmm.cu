@@ -267,7 +267,6 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
     }
 }
 
-constexpr int kNumSMs = 148;
 // variant 0 runs as 32 warps x 4 rows (SP_SPMM_NW32=0: 16 warps x 8 rows, for A/B measurements)
 bool spmm_nw32() {
     static const int v = [] {
@@ -385,7 +384,7 @@ bool launch_conv_spmm(const sp_weight_s *w, int orient, int64_t B, const float *
                       const int *sh, int ntap, int64_t Wv, int64_t OHv, int64_t OWv, cudaStream_t st) {
     if (!conv_sk_disabled() && launch_conv_spmm_sk(w, orient, B, in, Lp, out, sh, ntap, Wv, OHv, OWv, st)) return true;
     const int64_t Nv = OHv * Wv * B;
-    if ((int64_t)w->tap[0][orient].nrb * ((Nv + 127) / 128) >= 2 * kNumSMs)
+    if ((int64_t)w->tap[0][orient].nrb * ((Nv + 127) / 128) >= 2 * num_sms())
         return conv_spmm_vec<4>(w, orient, B, in, Lp, out, sh, ntap, Wv, OHv, OWv, st);
     return conv_spmm_vec<2>(w, orient, B, in, Lp, out, sh, ntap, Wv, OHv, OWv, st);
 }
@@ -406,7 +405,7 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
         const sp_tiling &t0 = w->til[orient][0];
         const int64_t items = (int64_t)t0.nrb * ((B + 127) / 128);
         const int mode = spmm_sk_mode();
-        const bool sk = mode == 1 || (mode < 0 && items < 2 * kNumSMs && t0.nkb >= 8);
+        const bool sk = mode == 1 || (mode < 0 && items < 2 * num_sms() && t0.nkb >= 8);
         if (sk && launch_spmm_sk(w, orient, B, in, out, gate, epi, st)) return;
     }
     if (spmm_rb256() && (B & 3) == 0 && w->til_r256[orient].seg) {  // A/B: 256-row blocks, 32 warps x 8 rows
@@ -421,8 +420,8 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
     auto ctas = [&](int v, int vv) {
         return (int64_t)w->til[orient][v].nrb * ((B + 32 * vv - 1) / (32 * vv));
     };
-    if (ctas(0, vec) < 2 * kNumSMs) var = 1;
-    while (var == 1 && vec > 1 && ctas(1, vec) < 2 * kNumSMs) vec >>= 1;
+    if (ctas(0, vec) < 2 * num_sms()) var = 1;
+    while (var == 1 && vec > 1 && ctas(1, vec) < 2 * num_sms()) vec >>= 1;
     // the 32-warp layout takes the split-source kernel by default: the same
     // entries in the same order (bitwise the same result), a third of the
     // gathers from TMEM (SP_SPMM_HYB=0 keeps the shared-memory-only kernel)

@@ -37,6 +37,9 @@
 namespace sp {
 namespace {
 
+// Unpredicated gathers of all but a segment's last slot rely on even padding.
+static_assert(kTilPad == 2 && kTapPad == 2, "only a segment's last slot may be padding");
+
 constexpr int HY_NW = 32, HY_RPW = 4, HY_RB = HY_NW * HY_RPW, HY_BT = 128;
 constexpr int HY_TC = kHybTC;  // tile rows mirrored in TMEM (the last TC of the KC)
 constexpr int HY_ISSUE = 8;    // warps issuing a tile's copies

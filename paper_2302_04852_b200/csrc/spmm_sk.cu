@@ -21,7 +21,11 @@
 namespace sp {
 namespace {
 
-constexpr int kNumSMs = 148;
+// The gathers below load slots 0..2 of an entry group (0 of a last pair)
+// unpredicated: that is only safe while every segment is padded to an EVEN
+// length, so that a segment's last slot is the only one that can be padding.
+static_assert(kTilPad == 2 && kTapPad == 2, "only a segment's last slot may be padding");
+
 
 __host__ __device__ __forceinline__ int64_t lo_of(int64_t c, int64_t T, int64_t G) { return c * T / G; }
 __host__ __device__ __forceinline__ int64_t cta_of(int64_t t, int64_t T, int64_t G) {
@@ -423,7 +427,7 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
     const int64_t nslice = (B + BT - 1) / BT;
     const int64_t T = (int64_t)t.nrb * nslice * t.nkb;
     if (T >= (1LL << 31)) return false;
-    const int64_t G = std::min<int64_t>(kNumSMs, T);
+    const int64_t G = std::min<int64_t>(num_sms(), T);
     const size_t tiles = (size_t)2 * t.KC * BT * sizeof(float);
     const int cap = (t.max_tile + 2 + 3) & ~3;
     const size_t smem = tiles + (size_t)2 * (cap + 2) * sizeof(int2);
@@ -433,8 +437,8 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
     const int64_t nitems = (int64_t)t.nrb * nslice;
     float *part = nullptr;
     int *tickets = nullptr;
-    if (cudaMallocAsync((void **)&part, (size_t)G * 2 * 128 * BT * sizeof(float), st) != cudaSuccess ||
-        cudaMallocAsync((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)
+    if (scratch_alloc((void **)&part, (size_t)G * 2 * 128 * BT * sizeof(float), st) != cudaSuccess ||
+        scratch_alloc((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)
         return false;
     cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
     refresh_if_stale(w, t, st);
@@ -456,8 +460,8 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
     else if (epi == EPI_GATE) go(spmm_sk_kernel<RPW, NW, EPI_GATE, false>);
     else go(spmm_sk_kernel<RPW, NW, EPI_NONE, false>);
     count_launches(1);
-    cudaFreeAsync(part, st);
-    cudaFreeAsync(tickets, st);
+    scratch_free(part, st);
+    scratch_free(tickets, st);
     return true;
 }
 
@@ -473,7 +477,7 @@ bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const floa
     const int64_t nslice = (Nv + BT - 1) / BT;
     const int64_t T = (int64_t)t0.nrb * nslice * ntap * t0.nkb;
     if (T >= (1LL << 31)) return false;
-    const int64_t G = std::min<int64_t>(kNumSMs, T);
+    const int64_t G = std::min<int64_t>(num_sms(), T);
     int mx = 0;
     for (int t = 0; t < ntap; ++t) mx = std::max(mx, w->tap[t][orient].max_tile);
     const int cap = (mx + 2 + 3) & ~3;
@@ -484,8 +488,8 @@ bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const floa
     const int64_t nitems = (int64_t)t0.nrb * nslice;
     float *part = nullptr;
     int *tickets = nullptr;
-    if (cudaMallocAsync((void **)&part, (size_t)G * 2 * 128 * BT * sizeof(float), st) != cudaSuccess ||
-        cudaMallocAsync((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)
+    if (scratch_alloc((void **)&part, (size_t)G * 2 * 128 * BT * sizeof(float), st) != cudaSuccess ||
+        scratch_alloc((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)
         return false;
     cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
     SkArgs a{t0.rows, B, nslice, t0.KC, t0.nkb, t0.nrb, cap, nullptr, nullptr, out, nullptr, nullptr, nullptr,
@@ -502,8 +506,8 @@ bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const floa
     if (tmm) go(spmm_sk_kernel<RPW, NW, EPI_NONE, true, true>);
     else go(spmm_sk_kernel<RPW, NW, EPI_NONE, true>);
     count_launches(1);
-    cudaFreeAsync(part, st);
-    cudaFreeAsync(tickets, st);
+    scratch_free(part, st);
+    scratch_free(tickets, st);
     return true;
 }
 

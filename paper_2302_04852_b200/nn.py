@@ -132,6 +132,22 @@ class _Dispatching(torch.nn.Module):
         self.impl = None  # decided lazily on the first batch, reset by set_mask
         self.probe_ms = None
 
+    def _rebuild(self, weight: torch.Tensor, mask: torch.Tensor):
+        """New handle for (weight, mask).  The `vals` Parameter OBJECT is kept
+        across mask changes (its .data is re-pointed at the new handle's vals,
+        whose storage keeps that handle alive), so an optimizer built before a
+        GMP update keeps stepping the live weights.  Its size changes with
+        nnz: per-parameter optimizer state (momentum, Adam moments) must be
+        dropped by the caller -- `prune.prune_modules(..., optimizer=opt)`
+        does it."""
+        self.W = sp.sp_weight_create(weight.detach().float().contiguous(), mask.to(torch.uint8).contiguous())
+        if getattr(self, "vals", None) is None:
+            self.vals = torch.nn.Parameter(self.W.vals, requires_grad=True)
+        else:
+            self.vals.data = self.W.vals
+            self.vals.grad = None
+        self.impl = None
+
     @property
     def sparsity(self) -> float:
         return 1.0 - self.W.nnz / float(self.W.R * self.W.C)
@@ -140,9 +156,12 @@ class _Dispatching(torch.nn.Module):
         if self.impl is None:
             def run(fn):
                 def go():
-                    xx = x.detach().requires_grad_(x.requires_grad)
-                    out = fn(xx)
-                    out.backward(torch.ones_like(out))
+                    # the probe is a forward+backward even when the first call
+                    # comes under no_grad / inference_mode (e.g. eval first)
+                    with torch.inference_mode(False), torch.enable_grad():
+                        xx = x.detach().clone().requires_grad_(x.requires_grad)
+                        out = fn(xx)
+                        out.backward(torch.ones_like(out))
                 return lambda: self.timer(go)
             self.probe_ms = {}
 
@@ -170,9 +189,7 @@ class SparseLinear(_Dispatching):
 
     def set_mask(self, weight: torch.Tensor, mask: torch.Tensor):
         """(Re)build the sparse structure (masks change "only a few times", P428)."""
-        self.W = sp.sp_weight_create(weight.detach().float().contiguous(), mask.to(torch.uint8).contiguous())
-        self.vals = torch.nn.Parameter(self.W.vals, requires_grad=True)
-        self.impl = None
+        self._rebuild(weight, mask)
 
     def _run(self, x, impl):
         xt = x if self.feature_major else x.t()
@@ -196,9 +213,7 @@ class SparseConv2d(_Dispatching):
         self.set_mask(weight, mask)
 
     def set_mask(self, weight: torch.Tensor, mask: torch.Tensor):
-        self.W = sp.sp_weight_create(weight.detach().float().contiguous(), mask.to(torch.uint8).contiguous())
-        self.vals = torch.nn.Parameter(self.W.vals, requires_grad=True)
-        self.impl = None
+        self._rebuild(weight, mask)
 
     def _run(self, x, impl):
         xc = x if self.batch_last else x.permute(1, 2, 3, 0)

@@ -79,11 +79,13 @@ def global_magnitude_masks(weights: list[torch.Tensor], sparsity: float,
     return out
 
 
-def prune_modules(modules, sparsity: float, scope: str = "uniform") -> dict:
+def prune_modules(modules, sparsity: float, scope: str = "uniform", optimizer=None) -> dict:
     """Prune SparseLinear / SparseConv2d modules to `sparsity` by magnitude of
-    their current kept weights and rebuild their sparse structure.  Returns
-    the achieved sparsities and the time spent rebuilding (the
-    sp_weight_create cost this mask update pays)."""
+    their current kept weights and rebuild their sparse structure.  Each
+    module keeps its `vals` Parameter object (re-pointed at the new handle),
+    so `optimizer` keeps stepping it; its per-parameter state, whose size
+    was the old nnz, is dropped.  Returns the achieved sparsities and the
+    time spent rebuilding (the sp_weight_create cost this mask update pays)."""
     dense, cur = [], []
     for m in modules:
         shape = m.W.filter_shape or (m.W.R, m.W.C)
@@ -101,5 +103,8 @@ def prune_modules(modules, sparsity: float, scope: str = "uniform") -> dict:
         m.set_mask(d * k, k.to(torch.uint8))
     torch.cuda.synchronize()
     rebuild_s = time.perf_counter() - t0
+    if optimizer is not None:
+        for m in modules:
+            optimizer.state.pop(m.vals, None)
     achieved = [1.0 - m.W.nnz / float(m.W.R * m.W.C) for m in modules]
     return {"sparsity": achieved, "rebuild_s": rebuild_s}

@@ -30,7 +30,7 @@ EXPORTS = [
     "sp_mse_scratch_floats", "sp_mse_grad", "sp_sgd", "sp_last_error", "sp_version",
     "sp_launch_count", "sp_linear_bwd", "sp_linear_bwd_relu", "sp_weight_create_conv", "sp_weight_gather",
     "sp_weight_set_managed", "sp_weight_sgd",
-    "sp_conv2d_bwd",
+    "sp_conv2d_bwd", "sp_set_sm_reserve",
 ]
 
 
@@ -84,6 +84,7 @@ def lib() -> ct.CDLL:
             "sp_linear_bwd_relu": (st, [vp, vp, vp, vp, vp, vp, i64, vp]),
             "sp_weight_set_managed": (st, [vp, ct.c_int]),
             "sp_weight_sgd": (st, [vp, vp, ct.c_float, vp]),
+            "sp_set_sm_reserve": (st, [ct.c_int32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -138,15 +139,19 @@ class SparseWeight:
             raise ValueError("dense and mask must be R x C (or matching 4-D conv filters)")
         R, C = dense.shape
         h = ct.c_void_p()
+        # the contiguous copies stay bound to locals until the C call returns: a
+        # temporary freed inside _dev could be handed to the next copy by the
+        # caching allocator and overwritten before the library reads it
+        d = dense.contiguous()
+        m = mask.contiguous()
         if self.filter_shape is not None:
             OC, IC, KH, KW = self.filter_shape
-            _check(lib().sp_weight_create_conv(OC, IC, KH, KW, _dev(dense.contiguous(), torch.float32, "dense"),
-                                               _dev(mask.contiguous(), torch.uint8, "mask"), _stream(stream),
-                                               ct.byref(h)))
+            _check(lib().sp_weight_create_conv(OC, IC, KH, KW, _dev(d, torch.float32, "dense"),
+                                               _dev(m, torch.uint8, "mask"), _stream(stream), ct.byref(h)))
         else:
-            _check(lib().sp_weight_create(R, C, _dev(dense.contiguous(), torch.float32, "dense"),
-                                          _dev(mask.contiguous(), torch.uint8, "mask"), _stream(stream),
-                                          ct.byref(h)))
+            _check(lib().sp_weight_create(R, C, _dev(d, torch.float32, "dense"), _dev(m, torch.uint8, "mask"),
+                                          _stream(stream), ct.byref(h)))
+        del d, m
         self.handle = h
         self.R, self.C = int(R), int(C)
         self.nnz = int(lib().sp_weight_nnz(h))
@@ -157,23 +162,27 @@ class SparseWeight:
 
     # -- zero-copy views of the handle-owned device buffers ------------------
     def _view(self, ptr: int, n: int, dtype) -> torch.Tensor:
+        """A tensor over handle-owned device memory.  torch keeps the
+        __cuda_array_interface__ object alive for the storage's lifetime, and
+        that object holds this SparseWeight: every tensor sharing the storage
+        (views, nn.Parameter aliases, optimizer references) keeps the handle
+        alive, and the handle is destroyed only after the last of them dies.
+        No reference runs back from the handle to its views (no cycle)."""
         if n == 0:
             return torch.empty(0, dtype=dtype, device=self.device)
         typestr = {torch.float32: "<f4", torch.int32: "<i4"}[dtype]
 
         class _CAI:
-            __cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
-                                        "version": 3, "strides": None, "stream": None}
-        t = torch.as_tensor(_CAI(), device=self.device)
-        t._sp_owner = self  # keep the handle alive while the view lives
-        return t
+            def __init__(self, owner):
+                self.owner = owner
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                                 "version": 3, "strides": None, "stream": None}
+        return torch.as_tensor(_CAI(self), device=self.device)
 
     @property
     def vals(self) -> torch.Tensor:
-        """Mutable fp32 view of vals[nnz] (CSR order), zero-copy."""
-        if getattr(self, "_vals_t", None) is None:
-            self._vals_t = self._view(self._vals_ptr, self.nnz, torch.float32)
-        return self._vals_t
+        """Mutable fp32 view of vals[nnz] (CSR order), zero-copy; keeps the handle alive."""
+        return self._view(self._vals_ptr, self.nnz, torch.float32)
 
     def indices(self) -> dict:
         ps = [ct.c_void_p() for _ in range(5)]
@@ -219,8 +228,13 @@ def sp_weight_gather(W: SparseWeight, dense: torch.Tensor, nz: torch.Tensor | No
         nz = torch.empty(W.nnz, dtype=torch.float32, device=dense.device)
     if tuple(dense.shape[-2:]) != (W.R, W.C) and dense.numel() != W.R * W.C:
         raise ValueError("dense must hold R x C values")
-    _check(lib().sp_weight_gather(W.handle, _dev(dense.contiguous(), torch.float32, "dense"),
+    d = dense.contiguous()  # bound until the (stream-ordered) call is enqueued
+    if nz.numel() != W.nnz:
+        raise ValueError("nz must have nnz elements")
+    _check(lib().sp_weight_gather(W.handle, _dev(d, torch.float32, "dense"),
                                   _dev(nz, torch.float32, "nz") if W.nnz else None, _stream(stream)))
+    if stream is not None and d is not dense:  # the copy must outlive the enqueued kernel
+        d.record_stream(stream if isinstance(stream, torch.cuda.Stream) else torch.cuda.ExternalStream(int(stream)))
     return nz
 
 
@@ -322,13 +336,23 @@ def _geo_out(g: sp_conv_geom):
     return g.H + 2 * g.pad - g.KH + 1, g.W + 2 * g.pad - g.KW + 1
 
 
+def _chk_shape(t: torch.Tensor, shape, name: str):
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+
+
+def _chk_nnz(W: SparseWeight, dW: torch.Tensor, name: str = "dW"):
+    if dW.numel() != W.nnz:
+        raise ValueError(f"{name} must have nnz = {W.nnz} elements, got {dW.numel()}")
+
+
 def sp_conv2d_fwd(W: SparseWeight, g: sp_conv_geom, X: torch.Tensor, Y: torch.Tensor | None = None,
                   stream=None) -> torch.Tensor:
     OH, OW = _geo_out(g)
-    if tuple(X.shape) != (g.C_in, g.H, g.W, g.B):
-        raise ValueError("X must be CHWN [C_in][H][W][B]")
+    _chk_shape(X, (g.C_in, g.H, g.W, g.B), "X (CHWN [C_in][H][W][B])")
     if Y is None:
         Y = torch.empty(g.C_out, OH, OW, g.B, dtype=torch.float32, device=X.device)
+    _chk_shape(Y, (g.C_out, OH, OW, g.B), "Y (CHWN [C_out][OH][OW][B])")
     _check(lib().sp_conv2d_fwd(W.handle, ct.byref(g), _dev(X, torch.float32, "X"),
                                _dev(Y, torch.float32, "Y"), _stream(stream)))
     return Y
@@ -337,10 +361,10 @@ def sp_conv2d_fwd(W: SparseWeight, g: sp_conv_geom, X: torch.Tensor, Y: torch.Te
 def sp_conv2d_bwd_input(W: SparseWeight, g: sp_conv_geom, dY: torch.Tensor,
                         dX: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     OH, OW = _geo_out(g)
-    if tuple(dY.shape) != (g.C_out, OH, OW, g.B):
-        raise ValueError("dY must be CHWN [C_out][OH][OW][B]")
+    _chk_shape(dY, (g.C_out, OH, OW, g.B), "dY (CHWN [C_out][OH][OW][B])")
     if dX is None:
         dX = torch.empty(g.C_in, g.H, g.W, g.B, dtype=torch.float32, device=dY.device)
+    _chk_shape(dX, (g.C_in, g.H, g.W, g.B), "dX (CHWN [C_in][H][W][B])")
     _check(lib().sp_conv2d_bwd_input(W.handle, ct.byref(g), _dev(dY, torch.float32, "dY"),
                                      _dev(dX, torch.float32, "dX"), _stream(stream)))
     return dX
@@ -350,12 +374,14 @@ def sp_conv2d_bwd(W: SparseWeight, g: sp_conv_geom, X: torch.Tensor, dY: torch.T
                   dX: torch.Tensor | None = None, dW: torch.Tensor | None = None, stream=None):
     """Both conv backward products in one pass (Alg. 2 single pass): (dX, dW)."""
     OH, OW = _geo_out(g)
-    if tuple(dY.shape) != (g.C_out, OH, OW, g.B):
-        raise ValueError("dY must be CHWN [C_out][OH][OW][B]")
+    _chk_shape(X, (g.C_in, g.H, g.W, g.B), "X (CHWN [C_in][H][W][B])")
+    _chk_shape(dY, (g.C_out, OH, OW, g.B), "dY (CHWN [C_out][OH][OW][B])")
     if dX is None:
         dX = torch.empty(g.C_in, g.H, g.W, g.B, dtype=torch.float32, device=dY.device)
+    _chk_shape(dX, (g.C_in, g.H, g.W, g.B), "dX (CHWN [C_in][H][W][B])")
     if dW is None:
         dW = torch.empty(W.nnz, dtype=torch.float32, device=X.device)
+    _chk_nnz(W, dW)
     _check(lib().sp_conv2d_bwd(W.handle, ct.byref(g), _dev(X, torch.float32, "X"), _dev(dY, torch.float32, "dY"),
                                _dev(dX, torch.float32, "dX"), _dev(dW, torch.float32, "dW") if W.nnz else None,
                                _stream(stream)))
@@ -364,8 +390,12 @@ def sp_conv2d_bwd(W: SparseWeight, g: sp_conv_geom, X: torch.Tensor, dY: torch.T
 
 def sp_conv2d_bwd_weight(W: SparseWeight, g: sp_conv_geom, X: torch.Tensor, dY: torch.Tensor,
                          dW: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    OH, OW = _geo_out(g)
+    _chk_shape(X, (g.C_in, g.H, g.W, g.B), "X (CHWN [C_in][H][W][B])")
+    _chk_shape(dY, (g.C_out, OH, OW, g.B), "dY (CHWN [C_out][OH][OW][B])")
     if dW is None:
         dW = torch.empty(W.nnz, dtype=torch.float32, device=X.device)
+    _chk_nnz(W, dW)
     _check(lib().sp_conv2d_bwd_weight(W.handle, ct.byref(g), _dev(X, torch.float32, "X"),
                                       _dev(dY, torch.float32, "dY"),
                                       _dev(dW, torch.float32, "dW") if W.nnz else None,
@@ -387,6 +417,11 @@ def sp_mse_grad(Y: torch.Tensor, T: torch.Tensor, dY: torch.Tensor, loss: torch.
                              _dev(scratch, torch.float32, "scratch"), n, _stream(stream)))
 
 
+def sp_set_sm_reserve(n: int):
+    """Leave n SMs free in the one-wave kernels' grids (for a concurrent collective)."""
+    _check(lib().sp_set_sm_reserve(int(n)))
+
+
 def sp_weight_set_managed(W: SparseWeight, managed: bool = True):
     """Declare that W.vals changes only through sp_weight_sgd (products then
     skip the per-launch refresh of the tiled weights); see the C header."""
@@ -396,6 +431,7 @@ def sp_weight_set_managed(W: SparseWeight, managed: bool = True):
 def sp_weight_sgd(W: SparseWeight, dW: torch.Tensor, lr: float, stream=None):
     """W.vals -= lr * dW, tiled copies included (one kernel)."""
     n = W.nnz
+    _chk_nnz(W, dW)
     _check(lib().sp_weight_sgd(W.handle, _dev(dW, torch.float32, "dW") if n else None, ct.c_float(lr),
                                _stream(stream)))
 
