@@ -182,6 +182,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--lr", type=float, default=1e-5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config single-layer sweep (BASELINE configs 0-3) added at N=1")
     ap.add_argument("--tokens", type=int, default=CFG["T"], help="global batch (default 16384)")
     args = ap.parse_args()
 
@@ -209,16 +211,18 @@ def main():
     c = synth.mlp_case(blocks=CFG["blocks"], d_model=CFG["d_model"], d_ff=CFG["d_ff"], T=T,
                        density=CFG["density"], seed=CFG["seed"])
     model = SparseMLP(c["layers"], hi - lo, dev)
-    # every rank must hold identical masks (allgather of a structure hash)
+    # every rank must hold identical masks: allgather of a 64-bit hash of every
+    # layer's (row_ptr, col_idx)
     if world > 1:
-        h = 0
+        import hashlib
+        hh = hashlib.blake2b(digest_size=8)
         for W1, W2 in model.W:
             for Wh in (W1, W2):
                 idx = Wh.indices()
-                h = (h * 1000003 + int(idx["col_idx"].to(torch.int64).sum()) * 7
-                     + int(idx["row_ptr"][-1])) % (1 << 61)
+                hh.update(idx["row_ptr"].cpu().numpy().tobytes())
+                hh.update(idx["col_idx"].cpu().numpy().tobytes())
         hs = [None] * world
-        dist.all_gather_object(hs, h)
+        dist.all_gather_object(hs, hh.hexdigest())
         assert len(set(hs)) == 1, "mask mismatch across ranks"
 
     X0_host = torch.from_numpy(np.ascontiguousarray(c["X0"][:, lo:hi])).pin_memory()
@@ -363,6 +367,12 @@ def main():
             "clocks": clk,
             "library": sp.version(),
         }
+        if world == 1 and not args.no_configs:
+            # driver-observed numbers for every single-layer BASELINE config
+            # (cfg1, cfg2a/b, cfg3, the ten cfg4 instances) beside the cfg5 headline
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            import config_sweep
+            line["per_config"] = config_sweep.sweep(fp32_peak * 1e12, float(peaks.get("hbm_gbs", 6550.1)) * 1e9)
         if world == 1 and not args.no_cpu_baseline:
             g, nt, sample, _ = run_oracle_sample(15.0)
             line["cpu_baseline"] = {"value": g, "unit": "GFLOP/s", "cores": nt, "kind": "oracle",

@@ -258,6 +258,12 @@ uint64_t sp_launch_count(void);
  * the grid, so results may change by rounding when n changes. */
 sp_status sp_set_sm_reserve(int32_t n);
 
+/* Provenance: the kernel families the last compute call (sp_linear_*,
+ * sp_conv2d_*) on this thread launched, "+"-separated in launch order (e.g.
+ * "spmm_hyb", "bwd_fused_sk_half").  Thread-local; valid until the next
+ * compute call on this thread. */
+const char *sp_last_path(void);
+
 /* Library build string (arch, version) for provenance in bench records. */
 const char *sp_version(void);
 

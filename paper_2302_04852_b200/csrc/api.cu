@@ -15,6 +15,13 @@
 namespace sp {
 
 static thread_local std::string g_err;
+static thread_local std::string g_path;
+
+void begin_path() { g_path.clear(); }
+void note_path(const char *name) {
+    if (!g_path.empty()) g_path += '+';
+    g_path += name;
+}
 static std::atomic<unsigned long long> g_launches{0};
 
 void count_launches(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
@@ -135,6 +142,8 @@ extern "C" {
 
 const char *sp_last_error(void) { return g_err.c_str(); }
 
+const char *sp_last_path(void) { return g_path.c_str(); }
+
 uint64_t sp_launch_count(void) { return g_launches.load(); }
 
 sp_status sp_set_sm_reserve(int32_t n) {
@@ -246,6 +255,7 @@ sp_status sp_weight_gather(sp_weight_t w, const float *dense, float *nz_out, sp_
 static sp_status linear_fwd_impl(sp_weight_t w, const float *X, float *Y, int64_t B, int epi,
                                  sp_stream_t stream, const char *fn) {
     SP_CHECK_HANDLE(w, fn);
+    begin_path();
     if (!X || !Y) return fail(SP_ERR_NULL, std::string(fn) + ": NULL tensor");
     sp_status s = check_B(B, w->R, w->C, fn);
     if (s != SP_OK) return s;
@@ -264,6 +274,7 @@ sp_status sp_linear_fwd_relu(sp_weight_t w, const float *X, float *Y, int64_t B,
 static sp_status linear_dx_impl(sp_weight_t w, const float *dY, const float *H, float *dX, int64_t B,
                                 int epi, sp_stream_t stream, const char *fn) {
     SP_CHECK_HANDLE(w, fn);
+    begin_path();
     if (!dY || !dX || (epi == EPI_GATE && !H)) return fail(SP_ERR_NULL, std::string(fn) + ": NULL tensor");
     sp_status s = check_B(B, w->R, w->C, fn);
     if (s != SP_OK) return s;
@@ -283,6 +294,7 @@ sp_status sp_linear_bwd_input_relu(sp_weight_t w, const float *dY, const float *
 sp_status sp_linear_bwd_weight(sp_weight_t w, const float *X, const float *dY, float *dW, int64_t B,
                                sp_stream_t stream) {
     SP_CHECK_HANDLE(w, "sp_linear_bwd_weight");
+    begin_path();
     if (!X || !dY || (!dW && w->nnz > 0)) return fail(SP_ERR_NULL, "sp_linear_bwd_weight: NULL tensor");
     sp_status s = check_B(B, w->R, w->C, "sp_linear_bwd_weight");
     if (s != SP_OK) return s;
@@ -294,6 +306,7 @@ sp_status sp_linear_bwd_weight(sp_weight_t w, const float *X, const float *dY, f
 static sp_status linear_bwd_impl(sp_weight_t w, const float *X, const float *dY, const float *H, float *dX,
                                  float *dW, int64_t B, sp_stream_t stream, const char *fn) {
     SP_CHECK_HANDLE(w, fn);
+    begin_path();
     if (!X || !dY || !dX || (!dW && w->nnz > 0)) return fail(SP_ERR_NULL, std::string(fn) + ": NULL tensor");
     sp_status s = check_B(B, w->R, w->C, fn);
     if (s != SP_OK) return s;
@@ -321,6 +334,7 @@ sp_status sp_linear_bwd_relu(sp_weight_t w, const float *X, const float *dY, con
 
 sp_status sp_conv2d_fwd(sp_weight_t w, const sp_conv_geom *g, const float *X, float *Y, sp_stream_t stream) {
     SP_CHECK_HANDLE(w, "sp_conv2d_fwd");
+    begin_path();
     sp_status s = check_geom(w, g, "sp_conv2d_fwd");
     if (s != SP_OK) return s;
     if (!X || !Y) return fail(SP_ERR_NULL, "sp_conv2d_fwd: NULL tensor");
@@ -331,6 +345,7 @@ sp_status sp_conv2d_fwd(sp_weight_t w, const sp_conv_geom *g, const float *X, fl
 sp_status sp_conv2d_bwd_input(sp_weight_t w, const sp_conv_geom *g, const float *dY, float *dX,
                               sp_stream_t stream) {
     SP_CHECK_HANDLE(w, "sp_conv2d_bwd_input");
+    begin_path();
     sp_status s = check_geom(w, g, "sp_conv2d_bwd_input");
     if (s != SP_OK) return s;
     if (!dY || !dX) return fail(SP_ERR_NULL, "sp_conv2d_bwd_input: NULL tensor");
@@ -341,6 +356,7 @@ sp_status sp_conv2d_bwd_input(sp_weight_t w, const sp_conv_geom *g, const float 
 sp_status sp_conv2d_bwd_weight(sp_weight_t w, const sp_conv_geom *g, const float *X, const float *dY,
                                float *dW, sp_stream_t stream) {
     SP_CHECK_HANDLE(w, "sp_conv2d_bwd_weight");
+    begin_path();
     sp_status s = check_geom(w, g, "sp_conv2d_bwd_weight");
     if (s != SP_OK) return s;
     if (!X || !dY || (!dW && w->nnz > 0)) return fail(SP_ERR_NULL, "sp_conv2d_bwd_weight: NULL tensor");
@@ -352,6 +368,7 @@ sp_status sp_conv2d_bwd_weight(sp_weight_t w, const sp_conv_geom *g, const float
 sp_status sp_conv2d_bwd(sp_weight_t w, const sp_conv_geom *g, const float *X, const float *dY, float *dX,
                         float *dW, sp_stream_t stream) {
     SP_CHECK_HANDLE(w, "sp_conv2d_bwd");
+    begin_path();
     sp_status s = check_geom(w, g, "sp_conv2d_bwd");
     if (s != SP_OK) return s;
     if (!X || !dY || !dX || (!dW && w->nnz > 0)) return fail(SP_ERR_NULL, "sp_conv2d_bwd: NULL tensor");

@@ -320,6 +320,7 @@ void launch_conv_fwd(const sp_weight_s *w, const sp_conv_geom &cg, const float *
         const int64_t nbc = (g.B + 32 * vec - 1) / (32 * vec);
         const int64_t warps = (int64_t)g.OC * g.OH * nqc * nbc;
         count_launches(1);
+        note_path("conv_fwd_direct");
         kern<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(g, nqc, w->row_ptr, w->col_idx, w->vals, X, Y);
     };
     if (g.B <= 32) go(conv_fwd_kernel<1, QC>, 1);
@@ -352,6 +353,7 @@ void launch_conv_bwd_input(const sp_weight_s *w, const sp_conv_geom &cg, const f
         const int64_t nbc = (g.B + 32 * vec - 1) / (32 * vec);
         const int64_t warps = (int64_t)g.IC * g.H * nqc * nbc;
         count_launches(1);
+        note_path("conv_dx_direct");
         kern<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(g, nqc, w->col_ptr, w->row_idx, w->perm,
                                                           w->vals, dY, dX);
     };
@@ -423,6 +425,7 @@ sp_status launch_conv_bwd_weight(const sp_weight_s *w, const sp_conv_geom &cg, c
     const int64_t warps = (int64_t)g.OC * gpr;
     auto go = [&](auto kern) {
         count_launches(1);
+        note_path("conv_dw_direct");
         kern<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(g, gpr, w->row_ptr, w->col_idx, X, dY, dW);
     };
     if (g.B <= 32) go(conv_dw_kernel<1>);

@@ -1179,6 +1179,7 @@ static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float 
                 0, t.rowmap, slices, t.nrb, dxpart, tickets, B, 1, nullptr, {}, {}, B, 0, 0, 0};
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        note_path(dwonly ? "sddmm_sk" : HALF ? "bwd_fused_sk_half" : "bwd_fused_sk");
         kern<<<(unsigned)G, TNW * 32, smem, st>>>(a, tmap);
     };
     if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, NB, false, HALF>);
@@ -1313,6 +1314,7 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const float *Dp, int64_t Lq, const
     }
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(nbuf * stage));
+        note_path(dwonly ? "conv_sddmm_sk" : "conv_bwd_fused_sk");
         kern<<<(unsigned)G, TNW * 32, nbuf * stage, st>>>(a, tmap);
     };
     if (half) {
@@ -1384,6 +1386,7 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
                 direct ? 1 : 0, t.rowmap, slices, t.nrb, nullptr, nullptr, B, 1, nullptr, {}, {}, B, 0, 0, 0};
     auto pick = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        note_path(tm ? "bwd_fused_tm_split" : "bwd_fused_split");
         kern<<<dim3((unsigned)t.nrb, (unsigned)nsplit), (tm ? TNW : NW) * 32, smem, st>>>(a, tmap);
     };
     count_launches(direct ? 1 : 2);

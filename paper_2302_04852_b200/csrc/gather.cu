@@ -169,6 +169,7 @@ void launch_spmm_gather(const sp_weight_s *w, int orient, int64_t B, const float
         const int64_t nsl = (B + 32 * vec - 1) / (32 * vec);
         const int64_t warps = rows * nsl;
         count_launches(1);
+        note_path("spmm_gather");
         kern<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(rows, B, ptr, idx, perm, w->vals, in, out, gate);
     };
     const int vec = B >= 128 ? 4 : B >= 64 ? 2 : 1;
@@ -192,6 +193,7 @@ void launch_sddmm_gather(const sp_weight_s *w, const float *X, const float *dY, 
     const int64_t warps = w->nnz / 32 + w->R;  // >= number of chunks
     auto go = [&](auto kern) {
         count_launches(1);
+        note_path("sddmm_gather");
         kern<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(w->R, B, w->chunk_ptr, w->row_ptr, w->col_idx, X, dY, dW);
     };
     if (B >= 128) go(sddmm_gather_kernel<4>);

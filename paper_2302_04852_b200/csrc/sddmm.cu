@@ -286,6 +286,7 @@ sp_status launch_cfg(const sp_weight_s *w, const sp_tiling &t, const float *rego
     {
         auto kern = sent ? sddmm_tiled_kernel<VEC, RPW, NW, true, false> : sddmm_tiled_kernel<VEC, RPW, NW, false, false>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        note_path("sddmm_tiled");
         kern<<<dim3((unsigned)t.nrb, (unsigned)nsplit), NW * 32, smem, st>>>(a, tmap);
     }
     if (!direct) {
@@ -360,6 +361,7 @@ bool launch_conv_sddmm(const sp_weight_s *w, int64_t B, const float *dYv, const 
     auto kern = sent ? sddmm_tiled_kernel<VEC, RPW, NW, true, true> : sddmm_tiled_kernel<VEC, RPW, NW, false, true>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     count_launches(2);
+    note_path("conv_sddmm_tiled");
     kern<<<dim3((unsigned)t0.nrb, (unsigned)nsplit, (unsigned)ntap), NW * 32, smem, st>>>(a, tmap);
     conv_split_reduce_kernel<<<dim3(64, ntap), 256, 0, st>>>(w->tapdev, tbv, tot, (int)nsplit, part, dW);
     scratch_free(part, st);

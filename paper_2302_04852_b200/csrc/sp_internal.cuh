@@ -141,6 +141,12 @@ void set_error(const std::string &msg);
 // Count of kernel launches issued by the library (provenance for bench.py).
 void count_launches(int n);
 
+// Provenance of the kernel path a public compute call took (sp_last_path):
+// begin_path() at the entry point clears it, note_path() appends a kernel
+// family name ("+"-separated) at each launch site of a hot-path kernel.
+void begin_path();
+void note_path(const char *name);
+
 // Launch-error check after an asynchronous launch.
 sp_status check_launch(const char *what);
 

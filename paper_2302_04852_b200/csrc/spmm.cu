@@ -314,6 +314,7 @@ void launch_cfg(const sp_tiling &t, int64_t B, const float *in, float *out, cons
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         count_launches(1);
+        note_path("spmm_tiled");
         kern<<<grid, NW * 32, smem, st>>>(a, tmap);
     };
     if (sent) {
@@ -357,6 +358,7 @@ bool conv_spmm_vec(const sp_weight_s *w, int orient, int64_t B, const float *in,
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         count_launches(1);
+        note_path("conv_spmm_tiled");
         kern<<<grid, NW * 32, smem, st>>>(a, tmap);
     };
     if (sent) launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_NONE, true, true>);

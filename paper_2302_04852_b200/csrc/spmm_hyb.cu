@@ -380,6 +380,7 @@ bool launch_spmm_hyb(const sp_weight_s *w, int orient, int64_t B, const float *i
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         count_launches(1);
+        note_path("spmm_hyb");
         kern<<<grid, HY_NW * 32, smem, st>>>(a, tmap);
     };
     if (stats)

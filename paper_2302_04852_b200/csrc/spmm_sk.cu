@@ -446,6 +446,7 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
              tickets, 0, nullptr, {}, 0, 0, 0};
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        note_path("spmm_sk");
         kern<<<(unsigned)G, NW * 32, smem, st>>>(a, tmap);
     };
     // the TMEM mirror of the tiles' last rows only when forced (SP_SPMM_HYB=1): on
@@ -501,6 +502,7 @@ bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const floa
     for (int t = 0; t < ntap; ++t) tmm = tmm && w->tap[t][orient].tmsplit != nullptr && w->tap[t][orient].KC == t0.KC;
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        note_path("conv_spmm_sk");
         kern<<<(unsigned)G, NW * 32, smem, st>>>(a, tmap);
     };
     if (tmm) go(spmm_sk_kernel<RPW, NW, EPI_NONE, true, true>);

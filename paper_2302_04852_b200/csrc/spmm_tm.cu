@@ -414,6 +414,7 @@ bool launch_spmm_tm(const sp_weight_s *w, int orient, int64_t B, const float *in
     auto launch = [&](auto kern, int nthr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         count_launches(1);
+        note_path("spmm_tm");
         kern<<<grid, nthr, smem, st>>>(a, tmap);
     };
 #define SP_TM_LAUNCH(NC, NP, RPW)                                                       \

@@ -30,7 +30,7 @@ EXPORTS = [
     "sp_mse_scratch_floats", "sp_mse_grad", "sp_sgd", "sp_last_error", "sp_version",
     "sp_launch_count", "sp_linear_bwd", "sp_linear_bwd_relu", "sp_weight_create_conv", "sp_weight_gather",
     "sp_weight_set_managed", "sp_weight_sgd",
-    "sp_conv2d_bwd", "sp_set_sm_reserve",
+    "sp_conv2d_bwd", "sp_set_sm_reserve", "sp_last_path",
 ]
 
 
@@ -85,6 +85,7 @@ def lib() -> ct.CDLL:
             "sp_weight_set_managed": (st, [vp, ct.c_int]),
             "sp_weight_sgd": (st, [vp, vp, ct.c_float, vp]),
             "sp_set_sm_reserve": (st, [ct.c_int32]),
+            "sp_last_path": (ct.c_char_p, []),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -118,6 +119,11 @@ def _dev(t: torch.Tensor, dtype, name: str) -> int:
 
 def version() -> str:
     return lib().sp_version().decode()
+
+
+def last_path() -> str:
+    """Kernel families the last compute call on this thread launched (provenance)."""
+    return lib().sp_last_path().decode()
 
 
 def launch_count() -> int:

@@ -91,3 +91,54 @@ def test_gmp_mask_update_rebuilds_and_stays_exact():
     x = torch.from_numpy(c["X"].T.copy()).cuda()
     y = m(x)
     _ok("y after pruning", y, x.cpu().double() @ Wd.t())
+
+
+def test_optimizer_built_before_pruning_keeps_stepping():
+    """an optimizer built before a GMP update must keep training the
+    kept weights (the Parameter object survives set_mask), and the handle whose
+    vals the Parameter views stays alive while the Parameter does."""
+    import gc
+    import weakref
+    from paper_2302_04852_b200.nn import SparseLinear
+    from paper_2302_04852_b200.prune import prune_modules
+    c = synth.linear_case(256, 192, 128, 0.3, 1.0 / 192, 35)
+    m = SparseLinear(torch.from_numpy(c["W"]).cuda(), torch.from_numpy(c["mask"]).cuda(), mode="sparse")
+    p_before = m.vals
+    opt = torch.optim.SGD(m.parameters(), lr=0.1, momentum=0.9)
+    x = torch.from_numpy(c["X"].T.copy()).cuda()
+    m(x).square().sum().backward()
+    opt.step()
+    prune_modules([m], 0.9, optimizer=opt)
+    assert m.vals is p_before and m.vals.numel() == m.W.nnz
+    before = m.W.vals.clone()
+    opt.zero_grad()
+    m(x).square().sum().backward()
+    opt.step()
+    torch.cuda.synchronize()
+    assert not torch.equal(before, m.W.vals), "the live weights did not move after pruning"
+    # the Parameter keeps its handle alive even after the module lets go of it
+    ref = weakref.ref(m.W)
+    p = m.vals
+    del m
+    gc.collect()
+    assert ref() is not None, "handle freed while its vals Parameter is alive"
+    assert torch.isfinite(p.detach().sum())
+    del p, opt
+    gc.collect()
+    assert ref() is None, "handle leaked after the last view died"
+
+
+def test_first_call_under_no_grad_runs_the_probe():
+    """the auto dispatcher's first call may come under no_grad."""
+    from paper_2302_04852_b200.nn import SparseLinear
+    c = synth.linear_case(256, 256, 64, 0.1, 1.0 / 256, 36)
+    m = SparseLinear(torch.from_numpy(c["W"]).cuda(), torch.from_numpy(c["mask"]).cuda(), mode="auto")
+    x = torch.from_numpy(c["X"].T.copy()).cuda()
+    with torch.no_grad():
+        y = m(x)
+    assert m.impl in ("sparse", "dense") and set(m.probe_ms) == {"dense", "sparse"}
+    assert m.vals.grad is None
+    with torch.inference_mode():
+        y2 = m(x)
+    torch.cuda.synchronize()
+    assert torch.allclose(y, y2)

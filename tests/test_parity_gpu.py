@@ -89,6 +89,48 @@ def test_cfg4(sp, sparsity, kind):
     check_linear(sp, c["W"], c["mask"], c["X"], c["dY"], f"cfg4 {kind} {sparsity}")
 
 
+def _fused_vs_oracle(sp, c, tag, gate_seed=None):
+    """sp_linear_bwd[_relu] (the fused backward the DP step and modules ship)
+    against the oracle; returns the kernel path it took (sp_last_path)."""
+    S = oracle.csr_from_mask(c["W"], c["mask"])
+    Wg = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))
+    H = None
+    if gate_seed is not None:
+        H = synth.normal(synth.rng(gate_seed), c["X"].shape, 1.0)
+        H[H < 0] = 0.0
+    dX, dW = sp.sp_linear_bwd(Wg, _dev(c["X"]), _dev(c["dY"]), H=None if H is None else _dev(H))
+    path = sp.last_path()
+    torch.cuda.synchronize()
+    refx = oracle.linear_bwd_input(S, c["dY"], NT)
+    if H is not None:
+        refx = refx * (H > 0)
+    _assert_tol(f"{tag} fused dX [{path}]", _np(dX), refx)
+    _assert_tol(f"{tag} fused dW [{path}]", _np(dW), oracle.linear_bwd_weight(S, c["X"], c["dY"], NT))
+    return path
+
+
+@pytest.mark.parametrize("kind", ["uniform", "zipf"])
+@pytest.mark.parametrize("sparsity", synth.CFG4_SPARSITIES)
+def test_cfg4_fused_backward(sp, sparsity, kind):
+    """the fused backward on every cfg4 mask (the exact
+    synth.cfg4 seeds), gated and ungated, with the kernel path recorded."""
+    cfg = synth.cfg4(sparsity, kind)
+    c = synth.linear_case(cfg["R"], cfg["C"], cfg["B"], cfg["density"], cfg["wvar"], cfg["seed"], kind)
+    p0 = _fused_vs_oracle(sp, c, f"cfg4 {kind} {sparsity}")
+    p1 = _fused_vs_oracle(sp, c, f"cfg4 {kind} {sparsity} gated", gate_seed=cfg["seed"] + 1)
+    assert p0 and p1, "no kernel path recorded"
+    print(f"cfg4 {kind} {sparsity}: {p0} / gated {p1}")
+
+
+@pytest.mark.parametrize("name", ["cfg2a", "cfg2b"])
+def test_cfg2_fused_backward(sp, name):
+    c = synth.linear_case(**synth.CFG[name])
+    p0 = _fused_vs_oracle(sp, c, name)
+    p1 = _fused_vs_oracle(sp, c, f"{name} gated", gate_seed=77)
+    assert p0 and p1
+    print(f"{name}: {p0} / gated {p1}")
+
+
 def test_paper_shape_B902(sp):
     # P366: (M,N) = (768, 3072), (B,M) = (902, 768); B not a multiple of 4 (S75)
     c = synth.linear_case(3072, 768, 902, 0.1, 1.0 / 768, 990)
