@@ -16,7 +16,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("SPARSEPROP_LIB", os.path.join(_HERE, "libsparseprop.so"))  # override for A/B builds
+LIB_PATH = os.environ.get("SPARSEPROP_LIB") or os.path.join(_HERE, "libsparseprop.so")  # override: A/B builds
 
 SP_STATUS = {0: "SP_OK", 1: "SP_ERR_NULL", 2: "SP_ERR_SHAPE", 3: "SP_ERR_OVERFLOW",
              4: "SP_ERR_ALLOC", 5: "SP_ERR_CUDA", 6: "SP_ERR_BAD_HANDLE"}

@@ -123,7 +123,7 @@ def test_optimizer_built_before_pruning_keeps_stepping():
     gc.collect()
     assert ref() is not None, "handle freed while its vals Parameter is alive"
     assert torch.isfinite(p.detach().sum())
-    del p, opt
+    del p, p_before, opt
     gc.collect()
     assert ref() is None, "handle leaked after the last view died"
 
