@@ -294,13 +294,56 @@ Geo mk(const sp_conv_geom &c) {
 
 constexpr int QC = 8;
 
+// tap offsets of the exact-column path: fwd reads X at (p + x - pad, q + y - pad),
+// dX (transposed conv, Eq. 4) reads dY at (m + pad - x, n + pad - y)
+void conv_taps_offsets(const Geo &g, bool transposed, ConvCols &cc) {
+    for (int x = 0; x < g.KH; ++x)
+        for (int y = 0; y < g.KW; ++y) {
+            const int t = x * g.KW + y;
+            cc.dp[t] = (int8_t)(transposed ? g.pad - x : x - g.pad);
+            cc.dq[t] = (int8_t)(transposed ? g.pad - y : y - g.pad);
+        }
+}
+
 }  // namespace
+
+bool conv_cols(int64_t B, int Po, int Qo, ConvCols *cc) {
+    if ((B & 3) != 0 || B < 4) return false;
+    ConvCols c{};
+    if (B <= 128) {
+        if (128 % B != 0) return false;
+        c.bsh = __builtin_ctzll((unsigned long long)B);
+        c.nq = (int)(128 / B);
+        c.bpr = 1;
+        c.spr = (Qo + c.nq - 1) / c.nq;
+    } else {
+        if (B % 128 != 0) return false;
+        c.bsh = 7;
+        c.nq = 1;
+        c.bpr = (int)(B / 128);
+        c.spr = Qo * c.bpr;
+    }
+    c.Po = Po;
+    c.Qo = Qo;
+    c.B = B;
+    *cc = c;
+    return true;
+}
 
 void launch_conv_fwd(const sp_weight_s *w, const sp_conv_geom &cg, const float *X, float *Y,
                      cudaStream_t st) {
     const Geo g = mk(cg);
+    ConvCols cc;
+    if (tap_path(w, g) && conv_cols(g.B, g.OH, g.OW, &cc)) {
+        // Y[oc][p][q] = sum_taps W_xy . X[p + x - pad][q + y - pad]  (Eq. 3 by taps;
+        // exact output positions, the halo zero-filled by the tensor map)
+        conv_taps_offsets(g, false, cc);
+        launch_refresh_taps(w, 0, g.KH * g.KW, st);
+        if (launch_conv_spmm_sk(w, 0, cc, X, g.H, g.W, Y, g.KH * g.KW, st)) return;
+    }
     if (tap_path(w, g)) {
-        // Y[oc] = sum_taps W_xy . shift_{(x*Wp + y)*B}(X_pad)  (Eq. 3 by taps)
+        // fallback (batch sizes the exact slicing cannot cut): padded copy and
+        // virtual columns, Y[oc] = sum_taps W_xy . shift_{(x*Wp + y)*B}(X_pad)
         const int Hp = g.H + 2 * g.pad, Wp = g.W + 2 * g.pad;
         const int64_t Lp = (int64_t)Hp * Wp * g.B;
         float *Xp = nullptr;
@@ -331,8 +374,15 @@ void launch_conv_fwd(const sp_weight_s *w, const sp_conv_geom &cg, const float *
 void launch_conv_bwd_input(const sp_weight_s *w, const sp_conv_geom &cg, const float *dY, float *dX,
                            cudaStream_t st) {
     const Geo g = mk(cg);
+    ConvCols cc;
+    if (tap_path(w, g) && conv_cols(g.B, g.H, g.W, &cc)) {
+        // transposed conv by taps (Eq. 4): dX[ic][m][n] = sum_taps W_xy^T . dY[m + pad - x][n + pad - y]
+        conv_taps_offsets(g, true, cc);
+        launch_refresh_taps(w, 1, g.KH * g.KW, st);
+        if (launch_conv_spmm_sk(w, 1, cc, dY, g.OH, g.OW, dX, g.KH * g.KW, st)) return;
+    }
     if (tap_path(w, g)) {
-        // transposed conv by taps (Eq. 4): dY padded by K-1-pad, shifts (K-1-x, K-1-y)
+        // fallback: transposed conv by taps on dY padded by K-1-pad, shifts (K-1-x, K-1-y)
         const int ph = g.KH - 1 - g.pad, pw = g.KW - 1 - g.pad;
         const int Hq = g.OH + 2 * ph, Wq = g.OW + 2 * pw;
         const int64_t Lq = (int64_t)Hq * Wq * g.B;
@@ -362,30 +412,15 @@ void launch_conv_bwd_input(const sp_weight_s *w, const sp_conv_geom &cg, const f
     else go(conv_dx_kernel<4, QC>, 4);
 }
 
-// Both conv backward products in one pass (Alg. 2's single pass by taps):
-// dY padded for the transposed conv, X laid out in dX's virtual columns (row
-// width Wq, zeros beyond W).  Falls back to the separate products.
+// Both conv backward products in one pass (Alg. 2's single pass by taps) on
+// the exact dX positions; false when it does not apply (the caller falls back
+// to the separate products).
 static bool conv_bwd_sk(const sp_weight_s *w, const Geo &g, const float *X, const float *dY, float *dX, float *dW,
                         cudaStream_t st) {
-    if (!tap_path(w, g)) return false;
-    const int ph = g.KH - 1 - g.pad, pw = g.KW - 1 - g.pad;
-    const int Hq = g.OH + 2 * ph, Wq = g.OW + 2 * pw;
-    const int64_t Lq = (int64_t)Hq * Wq * g.B, Nv = (int64_t)g.H * Wq * g.B;
-    float *Dp = nullptr, *Xv = nullptr;
-    if (scratch_alloc((void **)&Dp, (size_t)(g.OC * Lq) * sizeof(float), st) != cudaSuccess) return false;
-    if (scratch_alloc((void **)&Xv, (size_t)(g.IC * Nv) * sizeof(float), st) != cudaSuccess) {
-        scratch_free(Dp, st);
-        return false;
-    }
-    launch_pad(g.OC, g.OH, g.OW, Hq, Wq, ph, pw, g.B, dY, Dp, st);
-    launch_pad(g.IC, g.H, g.W, g.H, Wq, 0, 0, g.B, X, Xv, st);
-    int sh[kMaxTaps];
-    for (int x = 0; x < g.KH; ++x)
-        for (int y = 0; y < g.KW; ++y) sh[x * g.KW + y] = ((g.KH - 1 - x) * Wq + (g.KW - 1 - y)) * g.B;
-    const bool ok = launch_conv_bwd_sk(w, Dp, Lq, Xv, Nv, dX, dW, sh, g.KH * g.KW, g.B, Wq, g.H, g.W, st);
-    scratch_free(Dp, st);
-    scratch_free(Xv, st);
-    return ok;
+    ConvCols cc;
+    if (!tap_path(w, g) || !conv_cols(g.B, g.H, g.W, &cc)) return false;
+    conv_taps_offsets(g, true, cc);
+    return launch_conv_bwd_sk(w, cc, dY, g.OH, g.OW, X, dX, dW, g.KH * g.KW, st);
 }
 
 sp_status launch_conv_bwd(const sp_weight_s *w, const sp_conv_geom &cg, const float *X, const float *dY, float *dX,

@@ -48,17 +48,16 @@ struct FusedArgs {
     int nrow_blocks;        // stream-K kernel: row blocks of the tiling
     float *dxpart;          // stream-K kernel: [G][2][RB][BT] raw dX parts of cut items
     int *tickets;           // stream-K kernel: [nrow_blocks * nslice], zero on entry
-    // stream-K kernel, conv (CONV = true): the register operand X is the layer input in
-    // dX's virtual column layout (row stride xstride = Nv); an item's tiles run over
-    // (tap t, column block) with taps[t]'s tiling and the staged operand shifted by sh[t]
-    // columns; dW partial index tapbase[t] + entry; dX column n = (p*Wv + q)*Bc + b is
-    // stored compactly to dX[r][p][q][b] when p < OHv, q < OWv
+    // stream-K kernel, conv (CONV = true): slices are exact dX positions (cc: rows
+    // ic, output H x W); the register operand X [IC][H][W][B] is read at the same
+    // positions (row stride xstride = H*W*B); an item's tiles run over (tap t,
+    // column block) with taps[t]'s tiling and a 4-D TMA box of dY [OC][OH][OW][B]
+    // offset by (dp[t], dq[t]) (halo zero-filled); dW partial index tapbase[t] + entry
     int64_t xstride;
     int ntap;
     const TapDev *taps;
-    int sh[kMaxTaps];
     int64_t tapbase[kMaxTaps];
-    int64_t Bc, Wv, OHv, OWv;
+    ConvCols cc;
 };
 
 template <int RPW, int NW, bool GATE, bool SENT>
@@ -690,8 +689,15 @@ __global__ void __launch_bounds__(NW * 32, 1)
         const unsigned eb = (unsigned)(((e1 - e0) * 8 + 15) & ~15);
         const int2 *ent = CONV ? a.taps[tap_of(id.r)].ent : a.ent;
         mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
-        tma_load_2d(smem + buf * buf_sz + BT, &tmap, id.sl * BT + (CONV ? a.sh[tap_of(id.r)] : 0),
-                    kb_of(id.r) * a.KC, &full[buf]);
+        if constexpr (CONV) {
+            int p, q0, b0;
+            cc_origin(a.cc, id.sl, p, q0, b0);
+            const int t = tap_of(id.r);
+            tma_load_4d(smem + buf * buf_sz + BT, &tmap, b0, q0 + a.cc.dq[t], p + a.cc.dp[t], kb_of(id.r) * a.KC,
+                        &full[buf]);
+        } else {
+            tma_load_2d(smem + buf * buf_sz + BT, &tmap, id.sl * BT, kb_of(id.r) * a.KC, &full[buf]);
+        }
         if (eb) tma_load_1d(ents + buf * ebuf, ent + e0, eb, &full[buf]);
     };
     if (threadIdx.x == 0)
@@ -775,8 +781,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
                 for (int hh = 0; hh < (HALF ? 2 : 1); ++hh) {
                     const int64_t bc = bx + hh * 64;
-                    const float4 t = (r >= 0 && r < a.nrow && bc + 4 <= a.xstride)
-                                         ? __ldg(reinterpret_cast<const float4 *>(a.X + r * a.xstride + bc))
+                    // conv: the slice's exact positions (-1 past the row: zero)
+                    const int64_t xo = CONV ? cc_off(a.cc, id.sl, (int)(bc - (int64_t)id.sl * BT)) : bc;
+                    const float4 t = (r >= 0 && r < a.nrow && xo >= 0 && (CONV || bc + 4 <= a.xstride))
+                                         ? __ldg(reinterpret_cast<const float4 *>(a.X + r * a.xstride + xo))
                                          : make_float4(0.f, 0.f, 0.f, 0.f);
                     const float tv[4] = {t.x, t.y, t.z, t.w};
                     tm_st4(tcol + RV0 + SW * i + 4 * hh, tv);
@@ -922,14 +930,12 @@ __global__ void __launch_bounds__(NW * 32, 1)
             };
             // (ReLU' gate and) store of dX rows (rb, warp*RPW + i), columns bl..bl+3
             auto store = [&](int i, float (&o)[VEC]) {
-                if constexpr (CONV) {  // compact store of the valid positions (tap tilings: identity rows)
+                if constexpr (CONV) {  // exact positions (tap tilings: identity rows)
                     const int64_t r = r_base + i;
-                    if (r >= a.nrow || bl >= a.xstride) return;
-                    const int64_t pq = bl / a.Bc, b = bl - pq * a.Bc;
-                    const int64_t qq = pq % a.Wv, pp = pq / a.Wv;
-                    if (pp >= a.OHv || qq >= a.OWv) return;
-                    float *dst = a.dX + r * (a.OHv * a.OWv * a.Bc) + (pp * a.OWv + qq) * a.Bc + b;
-                    *reinterpret_cast<float4 *>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+                    if (r >= a.nrow) return;
+                    const int64_t off = cc_off(a.cc, (int)(bl / BT), (int)(bl % BT));
+                    if (off < 0) return;
+                    *reinterpret_cast<float4 *>(a.dX + r * a.xstride + off) = make_float4(o[0], o[1], o[2], o[3]);
                     return;
                 }
                 // gate H == X (the DP step's ReLU'): the row's X slice is already in
@@ -1176,7 +1182,7 @@ static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float 
     if (!dwonly) cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
     refresh_if_stale(w, t, st);  // CSC-tiled weights from vals (through perm)
     FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, 0, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
-                0, t.rowmap, slices, t.nrb, dxpart, tickets, B, 1, nullptr, {}, {}, B, 0, 0, 0};
+                0, t.rowmap, slices, t.nrb, dxpart, tickets, B, 1, nullptr, {}, {}};
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         note_path(dwonly ? "sddmm_sk" : HALF ? "bwd_fused_sk_half" : "bwd_fused_sk");
@@ -1258,14 +1264,16 @@ bool launch_sddmm_sk(const sp_weight_s *w, const float *X, const float *dY, floa
 
 // Conv backward by taps through the stream-K TMEM kernel (the paper's Alg. 2
 // single pass, P297-P347, made atomic-free by the CSC-of-taps drive): rows ic
-// of the 64-row tap tilings (tapf), inner oc; Dp = dY padded for the transposed
-// conv [OC x Lq], Xv = X in dX's virtual layout [IC x Nv] (zero beyond column W);
-// dX (compact CHWN, or null for dW alone) and dW at the conv handle's CSR slots.
-bool launch_conv_bwd_sk(const sp_weight_s *w, const float *Dp, int64_t Lq, const float *Xv, int64_t Nv, float *dX,
-                        float *dW, const int *sh, int ntap, int64_t Bc, int64_t Wv, int64_t OHv, int64_t OWv,
-                        cudaStream_t st) {
+// of the 64-row tap tilings (tapf), inner oc; slices are the exact dX positions
+// cc (H x W x B per channel); tap t = (x, y) reads dY [OC][OH][OW][B] through a
+// 4-D tensor map at (m + pad - x, n + pad - y) (cc.dp / cc.dq; out-of-range rows
+// and columns zero-filled: Eq. 4 with its bounds clipped, C6); X [IC][H][W][B] is
+// read at the slice's positions.  dX (CHWN, or null for dW alone) and dW at the
+// conv handle's CSR slots.
+bool launch_conv_bwd_sk(const sp_weight_s *w, const ConvCols &cc, const float *dY, int64_t OH, int64_t OW,
+                        const float *X, float *dX, float *dW, int ntap, cudaStream_t st) {
     constexpr int TRPW = 2, TNW = 32, BT = 128, RBF = TRPW * TNW;
-    if (sk_disabled() || (Bc & 3) != 0 || w->nnz == 0 || ntap > kMaxTaps) return false;
+    if (sk_disabled() || w->nnz == 0 || ntap > kMaxTaps) return false;
     const sp_tiling &t0 = w->tapf[0];
     if (t0.RB != RBF || t0.seg == nullptr) return false;
     const bool dwonly = dX == nullptr;
@@ -1273,7 +1281,8 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const float *Dp, int64_t Lq, const
     const bool half = fused_half() && !dwonly && w->tapf_groups8 <= (int64_t)sk_dwcols<TRPW, false, TNW, true>() * 4;
     const int64_t groups_cap = (int64_t)(dwonly ? sk_dwcols<TRPW, true>() : sk_dwcols<TRPW, false>()) * 8;
     if (!half && w->tapf_groups > groups_cap) return false;
-    const int64_t slices = (Nv + BT - 1) / BT;
+    const int64_t slices = (int64_t)cc.Po * cc.spr;
+    const int64_t xrow = (int64_t)cc.Po * cc.Qo * cc.B;  // floats per channel of X / dX
     const int64_t T = (int64_t)t0.nrb * slices * ntap * t0.nkb;
     if (T >= (1LL << 31)) return false;
     const int64_t G = std::min<int64_t>(num_sms(), T);
@@ -1289,7 +1298,7 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const float *Dp, int64_t Lq, const
     const int nbuf = 3 * stage <= (size_t)(226 * 1024) ? 3 : 2;
     if (nbuf * stage > (size_t)(226 * 1024)) return false;
     CUtensorMap tmap{};
-    if (!make_tmap_2d(&tmap, Dp, t0.inner, Lq, BT, t0.KC)) return false;
+    if (!make_tmap_conv(&tmap, dY, t0.inner, OH, OW, cc.B, 1 << cc.bsh, cc.nq, t0.KC)) return false;
     int64_t maxjobs = 1;
     const int64_t per_rb = slices * ntap * t0.nkb;
     for (int64_t rb = 0; rb < t0.nrb; ++rb)
@@ -1305,13 +1314,9 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const float *Dp, int64_t Lq, const
     }
     if (!dwonly) cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
     launch_refresh_taps(w, 2, ntap, st);  // fused tap tilings' weights from vals
-    FusedArgs a{t0.rows, t0.inner, Nv, t0.KC, t0.nkb, 0, cap, nullptr, nullptr, nullptr, Xv, Dp, nullptr, dX, part,
-                tot, 0, nullptr, slices, t0.nrb, dxpart, tickets, Nv, ntap, w->tapdev + 2 * kMaxTaps, {}, {},
-                Bc, Wv, OHv, OWv};
-    for (int t = 0; t < ntap; ++t) {
-        a.sh[t] = sh[t];
-        a.tapbase[t] = tapbase[t];
-    }
+    FusedArgs a{t0.rows, t0.inner, cc.B, t0.KC, t0.nkb, 0, cap, nullptr, nullptr, nullptr, X, dY, nullptr, dX, part,
+                tot, 0, nullptr, slices, t0.nrb, dxpart, tickets, xrow, ntap, w->tapdev + 2 * kMaxTaps, {}, cc};
+    for (int t = 0; t < ntap; ++t) a.tapbase[t] = tapbase[t];
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(nbuf * stage));
         note_path(dwonly ? "conv_sddmm_sk" : "conv_bwd_fused_sk");
@@ -1383,7 +1388,7 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     }
     refresh_if_stale(w, t, st);  // CSC-tiled weights from vals (through perm)
     FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, (int)spl, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
-                direct ? 1 : 0, t.rowmap, slices, t.nrb, nullptr, nullptr, B, 1, nullptr, {}, {}, B, 0, 0, 0};
+                direct ? 1 : 0, t.rowmap, slices, t.nrb, nullptr, nullptr, B, 1, nullptr, {}, {}};
     auto pick = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         note_path(tm ? "bwd_fused_tm_split" : "bwd_fused_split");

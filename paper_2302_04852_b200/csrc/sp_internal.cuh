@@ -16,6 +16,20 @@
 
 constexpr int kMaxTaps = 25;  // conv filters up to 5x5 use the tap-tiled kernels
 
+// Exact output columns of the conv kernels (4-D TMA path): a
+// batch slice of 128 columns is nq output columns q x bs batch elements of one
+// output row p (B <= 128: bs = B, nq = 128 / B; B > 128: bs = 128, nq = 1 and
+// bpr = B / 128 slices per q).  Slice sl -> p = sl / spr.  Tap t reads the input
+// at (p + dp[t], q + dq[t]) through a CHWN tensor map whose out-of-bounds
+// zero fill is the halo: no padded copy, no virtual columns.
+struct ConvCols {
+    int32_t bsh;  // log2 bs
+    int32_t nq, spr, bpr;
+    int32_t Po, Qo;  // output rows / columns of the product
+    int64_t B;
+    int8_t dp[25], dq[25];  // per-tap input offsets (kMaxTaps)
+};
+
 // Device view of one tap tiling (conv kernels index these by tap).
 struct TapDev {
     const int32_t *seg;
@@ -168,6 +182,12 @@ inline cudaStream_t S(sp_stream_t s) { return reinterpret_cast<cudaStream_t>(s);
 // box of `box_rows` rows x `box_cols` batch columns, no swizzle, zero OOB
 // fill.  Returns false if the driver entry point is unavailable.
 bool make_tmap_2d(CUtensorMap *map, const float *base, int64_t rows, int64_t B, int box_cols, int box_rows);
+// 4-D CHWN map with a (bs, nq, 1, kc) box (conv tap tiles; ConvCols)
+bool make_tmap_conv(CUtensorMap *map, const float *base, int64_t C, int64_t H, int64_t W, int64_t B, int bs, int nq,
+                    int kc);
+// ConvCols for output (Po x Qo) and batch B; false if B fits no exact slicing
+// (B % 4 != 0, or neither 128 % B == 0 nor B % 128 == 0)
+bool conv_cols(int64_t B, int Po, int Qo, ConvCols *cc);
 
 // ---- build.cu ----
 sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *mask,
@@ -194,8 +214,8 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
 // ---- spmm_sk.cu: stream-K SpMM (B % 4 == 0, big tiling); false if it does not apply
 bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,
                     int epi, cudaStream_t st);
-bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in, int64_t Lp, float *out,
-                         const int *sh, int ntap, int64_t Wv, int64_t OHv, int64_t OWv, cudaStream_t st);
+bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, const ConvCols &cc, const float *in, int64_t Hi,
+                         int64_t Wi, float *out, int ntap, cudaStream_t st);
 
 // ---- fused.cu: warps per CTA of the fused backward (SP_FUSED_NW A/B switch, default 32)
 int fused_nw();
@@ -236,9 +256,8 @@ void launch_split_reduce(int64_t npad, int nsplit, const float *part, const int3
 sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY, const float *H, float *dX,
                            float *dW, int64_t B, cudaStream_t st);
 // conv backward by taps through the stream-K TMEM kernel (dX null: dW alone); false if it does not apply
-bool launch_conv_bwd_sk(const sp_weight_s *w, const float *Dp, int64_t Lq, const float *Xv, int64_t Nv, float *dX,
-                        float *dW, const int *sh, int ntap, int64_t Bc, int64_t Wv, int64_t OHv, int64_t OWv,
-                        cudaStream_t st);
+bool launch_conv_bwd_sk(const sp_weight_s *w, const ConvCols &cc, const float *dY, int64_t OH, int64_t OW,
+                        const float *X, float *dX, float *dW, int ntap, cudaStream_t st);
 // fused conv backward (dX and dW); falls back to the separate products
 sp_status launch_conv_bwd(const sp_weight_s *w, const sp_conv_geom &g, const float *X, const float *dY, float *dX,
                           float *dW, cudaStream_t st);

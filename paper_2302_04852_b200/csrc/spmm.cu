@@ -287,14 +287,6 @@ int spmm_sk_mode() {
     }();
     return v;
 }
-// SP_CONV_SK=0 keeps the per-item conv grids (A/B measurements)
-bool conv_sk_disabled() {
-    static const int v = [] {
-        const char *e = getenv("SP_CONV_SK");
-        return (e && e[0] == '0') ? 1 : 0;
-    }();
-    return v != 0;
-}
 constexpr int kSmemLimit = 226 * 1024;  // per SM, usable by CTAs (minus static mbarriers)
 
 template <int VEC, int RPW, int NW>
@@ -378,13 +370,13 @@ bool spmm_rb256() {
     return v != 0;
 }
 
-// Conv products as tap-tiled SpMM (see conv.cu): in = padded activation
+// Conv products as tap-tiled SpMM on a padded copy (see conv.cu; the fallback
+// of the exact-column stream-K path for batch sizes it cannot slice): in = padded activation
 // [inner x Lp], taps[t] tilings of orientation `orient`, shift sh[t] columns;
 // virtual output columns Nv = OHv * Wv * B stored compactly.  Narrower batch
 // slices when the grid would not fill two waves.
 bool launch_conv_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, int64_t Lp, float *out,
                       const int *sh, int ntap, int64_t Wv, int64_t OHv, int64_t OWv, cudaStream_t st) {
-    if (!conv_sk_disabled() && launch_conv_spmm_sk(w, orient, B, in, Lp, out, sh, ntap, Wv, OHv, OWv, st)) return true;
     const int64_t Nv = OHv * Wv * B;
     if ((int64_t)w->tap[0][orient].nrb * ((Nv + 127) / 128) >= 2 * num_sms())
         return conv_spmm_vec<4>(w, orient, B, in, Lp, out, sh, ntap, Wv, OHv, OWv, st);

@@ -47,12 +47,12 @@ struct SkArgs {
     float *part;    // [G][2][RB][BT] raw sums of cut items (slot 0: the CTA's first item, 1: its last)
     int *tickets;   // [nrb * nslice], zero on entry, reset by the finishing CTA
     // conv (CONV = true): an item's tiles run over (tap t, column block); tap t uses
-    // taps[t]'s tiling and reads the padded input shifted by sh[t] columns; output
-    // column n = (p*Wv + q)*B + b is stored compactly to out[r][p][q][b] when p < OHv, q < OWv
+    // taps[t]'s tiling and a 4-D TMA box of the CHWN input at the slice's exact
+    // output positions offset by (dp[t], dq[t]) (halo zero-filled by the hardware);
+    // column c of slice sl is out[r][p][q][b] (ConvCols)
     int ntap;
     const TapDev *taps;
-    int sh[kMaxTaps];
-    int64_t Wv, OHv, OWv;
+    ConvCols cc;
 };
 
 // TMM: the last kHybTC rows of every tile are mirrored in tensor memory and a
@@ -157,8 +157,14 @@ __global__ void __launch_bounds__(NW * 32, 1)
         entry_range(id, e0, e1);
         const unsigned eb = (unsigned)(((e1 - e0) * 8 + 15) & ~15);
         mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
-        tma_load_2d(smem + buf * tile_sz, &tmap, id.sl * BT + (CONV ? a.sh[tap_of(id)] : 0), kb_of(id) * a.KC,
-                    &full[buf]);
+        if constexpr (CONV) {
+            int p, q0, b0;
+            cc_origin(a.cc, id.sl, p, q0, b0);
+            const int t = tap_of(id);
+            tma_load_4d(smem + buf * tile_sz, &tmap, b0, q0 + a.cc.dq[t], p + a.cc.dp[t], kb_of(id) * a.KC, &full[buf]);
+        } else {
+            tma_load_2d(smem + buf * tile_sz, &tmap, id.sl * BT, kb_of(id) * a.KC, &full[buf]);
+        }
         if (eb) tma_load_1d(ents + buf * ebuf, ent_of(id) + e0, eb, &full[buf]);
     };
     if (threadIdx.x == 0) {
@@ -177,12 +183,11 @@ __global__ void __launch_bounds__(NW * 32, 1)
     // epilogue of rows (rb, lr = warp*RPW + i) for batch columns bl..bl+3
     auto store = [&](int rb, int i, int64_t bl, const float (&v)[VEC]) {
         const int64_t tpos = (int64_t)rb * RB + warp * RPW + i;
-        if constexpr (CONV) {  // compact store of the valid output columns (tap tilings: identity rows)
+        if constexpr (CONV) {  // exact output positions (tap tilings: identity rows)
             if (tpos >= a.rows) return;
-            const int64_t pq = bl / B, b = bl - pq * B;
-            const int64_t qq = pq % a.Wv, pp = pq / a.Wv;
-            if (pp >= a.OHv || qq >= a.OWv) return;
-            float *dst = a.out + tpos * (a.OHv * a.OWv * B) + (pp * a.OWv + qq) * B + b;
+            const int64_t off = cc_off(a.cc, (int)(bl / BT), (int)(bl % BT));
+            if (off < 0) return;
+            float *dst = a.out + tpos * ((int64_t)a.cc.Po * a.cc.Qo * B) + off;
             *reinterpret_cast<float4 *>(dst) = make_float4(v[0], v[1], v[2], v[3]);
             return;
         }
@@ -443,7 +448,7 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
     cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
     refresh_if_stale(w, t, st);
     SkArgs a{t.rows, B, nslice, t.KC, t.nkb, t.nrb, cap, t.seg, t.ent, out, gate, t.rowmap, t.tmsplit, part,
-             tickets, 0, nullptr, {}, 0, 0, 0};
+             tickets, 0, nullptr, {}};
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         note_path("spmm_sk");
@@ -466,16 +471,15 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
     return true;
 }
 
-// Conv products (see conv.cu) through the stream-K schedule: in = padded
-// activation [inner x Lp], taps[t] tilings of orientation `orient`, shift sh[t]
-// columns; virtual output columns Nv = OHv * Wv * B stored compactly.
-bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in, int64_t Lp, float *out,
-                         const int *sh, int ntap, int64_t Wv, int64_t OHv, int64_t OWv, cudaStream_t st) {
+// Conv products (see conv.cu) through the stream-K schedule: `in` is the CHWN
+// input [inner][Hi][Wi][B] of the product (fwd: X, dX: dY), taps[t] tilings of
+// orientation `orient`, exact output columns cc (Po x Qo x B per row).
+bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, const ConvCols &cc, const float *in, int64_t Hi,
+                         int64_t Wi, float *out, int ntap, cudaStream_t st) {
     constexpr int RPW = 4, NW = 32, BT = 128;
     const sp_tiling &t0 = w->tap[0][orient];
-    if ((B & 3) != 0 || w->nnz == 0 || t0.RB != RPW * NW) return false;
-    const int64_t Nv = OHv * Wv * B;
-    const int64_t nslice = (Nv + BT - 1) / BT;
+    if (w->nnz == 0 || t0.RB != RPW * NW) return false;
+    const int64_t nslice = (int64_t)cc.Po * cc.spr;
     const int64_t T = (int64_t)t0.nrb * nslice * ntap * t0.nkb;
     if (T >= (1LL << 31)) return false;
     const int64_t G = std::min<int64_t>(num_sms(), T);
@@ -485,7 +489,7 @@ bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const floa
     const size_t smem = (size_t)2 * t0.KC * BT * sizeof(float) + (size_t)2 * (cap + 2) * sizeof(int2);
     if (smem > (size_t)(226 * 1024)) return false;
     CUtensorMap tmap{};
-    if (!make_tmap_2d(&tmap, in, t0.inner, Lp, BT, t0.KC)) return false;
+    if (!make_tmap_conv(&tmap, in, t0.inner, Hi, Wi, cc.B, 1 << cc.bsh, cc.nq, t0.KC)) return false;
     const int64_t nitems = (int64_t)t0.nrb * nslice;
     float *part = nullptr;
     int *tickets = nullptr;
@@ -493,12 +497,11 @@ bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const floa
         scratch_alloc((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)
         return false;
     cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
-    SkArgs a{t0.rows, B, nslice, t0.KC, t0.nkb, t0.nrb, cap, nullptr, nullptr, out, nullptr, nullptr, nullptr,
-             part, tickets, ntap, w->tapdev + orient * kMaxTaps, {}, Wv, OHv, OWv};
-    for (int t = 0; t < ntap; ++t) a.sh[t] = sh[t];
+    SkArgs a{t0.rows, cc.B, nslice, t0.KC, t0.nkb, t0.nrb, cap, nullptr, nullptr, out, nullptr, nullptr, nullptr,
+             part, tickets, ntap, w->tapdev + orient * kMaxTaps, cc};
     // conv tap tiles have 128 rows: the TMEM mirror covers half of them (cfg3
-    // fwd / dX 206 -> 202 / 201 us); SP_SPMM_HYB=0 turns it off
-    bool tmm = spmm_hyb_mode() != 0 && t0.KC > kHybTC;
+    // fwd / dX 206 -> 202 / 201 us)
+    bool tmm = t0.KC > kHybTC;
     for (int t = 0; t < ntap; ++t) tmm = tmm && w->tap[t][orient].tmsplit != nullptr && w->tap[t][orient].KC == t0.KC;
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

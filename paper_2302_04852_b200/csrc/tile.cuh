@@ -241,6 +241,40 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
         : "memory");
 }
 
+// 4-D tensor TMA: box at (b, q, p, channel) of a CHWN map (make_tmap_conv);
+// coordinates outside the tensor (the conv halo) are zero-filled.
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// ConvCols (sp_internal.cuh): slice sl -> origin (output row p, first output
+// column q0, first batch element b0) of its exact output positions
+__device__ __forceinline__ void cc_origin(const ConvCols &g, int sl, int &p, int &q0, int &b0) {
+    p = sl / g.spr;
+    const int r = sl - p * g.spr;
+    if (g.bpr == 1) {
+        q0 = r * g.nq;
+        b0 = 0;
+    } else {
+        q0 = r / g.bpr;
+        b0 = (r - q0 * g.bpr) * 128;
+    }
+}
+// column c (0..127) of slice sl -> float offset (p*Qo + q)*B + b of its output
+// position within a channel, or -1 when q lies past the row (a partial last slice)
+__device__ __forceinline__ int64_t cc_off(const ConvCols &g, int sl, int c) {
+    int p, q0, b0;
+    cc_origin(g, sl, p, q0, b0);
+    const int q = q0 + (c >> g.bsh);
+    if (q >= g.Qo) return -1;
+    return ((int64_t)p * g.Qo + q) * g.B + b0 + (c & ((1 << g.bsh) - 1));
+}
+
 // Issue (from one warp) the TMA copies of rows [k0, k0+nk) x batch columns
 // [b0, b0 + min(BT, B-b0)) of a [rows x B] activation (B % 4 == 0) into
 // tile[nk][BT], plus optionally `ebytes` of entries, all on `bar`.

@@ -307,7 +307,13 @@ def test_conv_handle_matches_linear_handle_and_is_deterministic(sp):
     (4, 300, 140, 5, 6, 3, 1, 0.05),  # several row / column blocks on the tap path
     (3, 6, 5, 9, 9, 3, 1, 0.1), (8, 128 // 8, 256 // 8, 7, 7, 3, 1, 0.05), (2, 4, 3, 6, 5, 3, 0, 0.4),
     (1, 2, 2, 5, 5, 5, 2, 0.6), (5, 3, 2, 4, 6, 1, 0, 0.7), (33, 8, 16, 10, 10, 3, 1, 0.2),
-    (64, 16, 16, 17, 19, 3, 1, 0.1), (130, 4, 4, 3, 3, 3, 1, 0.5)])
+    (64, 16, 16, 17, 19, 3, 1, 0.1), (130, 4, 4, 3, 3, 3, 1, 0.5),
+    # exact-column 4-D TMA path: B > 128 (two batch slices per q), B = 128 (one q per
+    # slice), partial last slices of a row (W % (128 / B) != 0), pad = K - 1, K = 5
+    (256, 8, 16, 5, 6, 3, 1, 0.2), (128, 16, 8, 6, 7, 3, 2, 0.2), (32, 8, 8, 7, 7, 3, 1, 0.3),
+    (16, 8, 8, 9, 7, 5, 2, 0.2), (4, 6, 6, 5, 5, 3, 0, 0.5), (64, 256, 64, 14, 14, 3, 1, 0.1),
+    (12, 6, 6, 6, 6, 3, 1, 0.3),      # B does not divide 128: padded-copy fallback
+])
 def test_conv_shapes(sp, B, IC, OC, H, W, K, pad, d):
     c = synth.conv_case(OC=OC, IC=IC, H=H, W=W, KH=K, KW=K, pad=pad, B=B, density=d,
                         wvar=1.0 / (IC * K * K), seed=B * 7 + IC + OC + H)
