@@ -274,6 +274,24 @@ __global__ void til_warp_max_kernel(int nrb, int nkb, int RB, int RPW, int GL, c
     if (threadIdx.x == 0) *out = sh[0];
 }
 
+// gpre (see sp_tiling): thread per (row block, warp); prefix of the warp's
+// groups of 2^GL entries over the column blocks.
+__global__ void til_gpre_kernel(int nrb, int nkb, int RB, int RPW, int GL, const int32_t *__restrict__ seg,
+                                int32_t *__restrict__ out) {
+    const int nw = RB / RPW;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nrb * nw) return;
+    const int rb = i / nw, wi = i - rb * nw;
+    int32_t s = 0;
+    int32_t *o = out + (int64_t)i * (nkb + 1);
+    for (int kb = 0; kb < nkb; ++kb) {
+        o[kb] = s;
+        const int64_t t = ((int64_t)rb * nkb + kb) * RB + (int64_t)wi * RPW;
+        for (int r = 0; r < RPW; ++r) s += (seg[t + r + 1] - seg[t + r] + (1 << GL) - 1) >> GL;
+    }
+    o[nkb] = s;
+}
+
 __global__ void til_refresh_kernel(int64_t nnz, const int32_t *__restrict__ vidx, const float *__restrict__ vals,
                                    int2 *__restrict__ ent) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -506,6 +524,16 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
                 if (dmalloc(&t.tmsplit, nseg + 8) != cudaSuccess) return SP_ERR_ALLOC;
                 til_split_kernel<<<(unsigned)((nseg + 255) / 256), 256, 0, st>>>(nseg, t.KC, t.seg, t.ent, t.tmsplit);
             }
+            if (o == 1) {  // group prefix tables of the fused backward (groups of 4 and of 8)
+                const int nwg = t.RB / sp_.RPWgrp;
+                t.RPWg = sp_.RPWgrp;
+                for (int g = 0; g < 2; ++g) {
+                    if (dmalloc(&t.gpre[g], (int64_t)t.nrb * nwg * (t.nkb + 1)) != cudaSuccess) return SP_ERR_ALLOC;
+                    til_gpre_kernel<<<(unsigned)((t.nrb * nwg + 127) / 128), 128, 0, st>>>(t.nrb, t.nkb, t.RB,
+                                                                                             sp_.RPWgrp, 2 + g, t.seg,
+                                                                                             t.gpre[g]);
+                }
+            }
             til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp, 2, t.seg, mx + NS + si);
             til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp, 3, t.seg, mx + 2 * NS + si);
             scratch_free(cnt, st);
@@ -549,6 +577,10 @@ void free_tilings(sp_weight_s *w) {
         t.tmsplit = nullptr;
         cudaFree(t.inv);
         t.inv = nullptr;
+        for (auto &g : t.gpre) {
+            cudaFree(g);
+            g = nullptr;
+        }
         t.seg = nullptr;
         t.ent = nullptr;
         t.vidx = nullptr;

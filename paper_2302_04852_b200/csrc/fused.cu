@@ -58,6 +58,9 @@ struct FusedArgs {
     const TapDev *taps;
     int64_t tapbase[kMaxTaps];
     ConvCols cc;
+    // stream-K kernel: the tiling's group prefix table for this kernel's group
+    // size (sp_tiling::gpre), nullptr: walk the earlier tiles' segment bounds
+    const int32_t *gpre;
 };
 
 template <int RPW, int NW, bool GATE, bool SENT>
@@ -729,17 +732,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
             if (my_e >= 0) P[my_e] = val;
             my_e = -1;
         };
-        for (int r = 0; r < tpi; ++r) {
+        // the groups of touched tile r (c2 = its first group's index in the item)
+        auto walk = [&](int r) {
             const int sg = lane <= RPW ? __ldg(segw_of(rb, r) + lane) : 0;
-            if (!touched(r, ra, len)) {  // advance the slot sequence past this tile
-                int gs = 0;
-#pragma unroll
-                for (int m = 0; m < RPW; ++m)
-                    gs += (__shfl_sync(kFull, sg, m + 1) - __shfl_sync(kFull, sg, m) + GE - 1) >> GL;
-                if ((c2 & GM) != 0 && ((c2 + gs) >> GSH) != (c2 >> GSH)) out(c2 >> GSH);
-                c2 += gs;
-                continue;
-            }
             const int64_t base = CONV ? a.tapbase[tap_of(r)] : 0;
             for (int m = 0; m < RPW; ++m) {
                 const int g0 = __shfl_sync(kFull, sg, m), g1 = __shfl_sync(kFull, sg, m + 1);
@@ -751,6 +746,34 @@ __global__ void __launch_bounds__(NW * 32, 1)
                     if ((c2 & GM) == 0) out((c2 >> GSH) - 1);
                 }
             }
+        };
+        if (a.gpre != nullptr) {
+            // only the touched tiles: one or two (cyclic) runs of consecutive tiles,
+            // each starting at its first group's column from the prefix table
+            const int32_t *gp = a.gpre + ((int64_t)rb * NW + warp) * (tpi + 1);
+            const int n1 = len >= tpi ? tpi - ra : min(len, tpi - ra);
+            const int n2 = len >= tpi ? ra : len - n1;
+            c2 = __ldg(gp + ra);
+            for (int r = ra; r < ra + n1; ++r) walk(r);
+            if (c2 & GM) out(c2 >> GSH);
+            if (n2 > 0) {
+                c2 = __ldg(gp);
+                for (int r = 0; r < n2; ++r) walk(r);
+            }
+        } else {
+        for (int r = 0; r < tpi; ++r) {
+            if (!touched(r, ra, len)) {  // advance the slot sequence past this tile
+                const int sg = lane <= RPW ? __ldg(segw_of(rb, r) + lane) : 0;
+                int gs = 0;
+#pragma unroll
+                for (int m = 0; m < RPW; ++m)
+                    gs += (__shfl_sync(kFull, sg, m + 1) - __shfl_sync(kFull, sg, m) + GE - 1) >> GL;
+                if ((c2 & GM) != 0 && ((c2 + gs) >> GSH) != (c2 >> GSH)) out(c2 >> GSH);
+                c2 += gs;
+                continue;
+            }
+            walk(r);
+        }
         }
         if (c2 & GM) out(c2 >> GSH);
     };
@@ -794,6 +817,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
             whole = id.r == 0;
             // group index of this tile's first group in the slice sequence
             cnt = 0;
+            if (a.gpre != nullptr)
+                cnt = __ldg(a.gpre + ((int64_t)id.rb * NW + warp) * (tpi + 1) + id.r);
+            else
             for (int k = 0; k < id.r; ++k) {  // groups of 4 per row segment (a last group may hold 2)
                 const int32_t *sw = segw_of(id.rb, k);
 #pragma unroll
@@ -1182,7 +1208,8 @@ static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float 
     if (!dwonly) cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
     refresh_if_stale(w, t, st);  // CSC-tiled weights from vals (through perm)
     FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, 0, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
-                0, t.rowmap, slices, t.nrb, dxpart, tickets, B, 1, nullptr, {}, {}};
+                0, t.rowmap, slices, t.nrb, dxpart, tickets, B, 1, nullptr, {}, {},
+                (t.RPWg == TRPW && t.RB == TRPW * TNW) ? t.gpre[HALF ? 1 : 0] : nullptr};
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         note_path(dwonly ? "sddmm_sk" : HALF ? "bwd_fused_sk_half" : "bwd_fused_sk");
@@ -1315,7 +1342,7 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const ConvCols &cc, const float *d
     if (!dwonly) cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
     launch_refresh_taps(w, 2, ntap, st);  // fused tap tilings' weights from vals
     FusedArgs a{t0.rows, t0.inner, cc.B, t0.KC, t0.nkb, 0, cap, nullptr, nullptr, nullptr, X, dY, nullptr, dX, part,
-                tot, 0, nullptr, slices, t0.nrb, dxpart, tickets, xrow, ntap, w->tapdev + 2 * kMaxTaps, {}, cc};
+                tot, 0, nullptr, slices, t0.nrb, dxpart, tickets, xrow, ntap, w->tapdev + 2 * kMaxTaps, {}, cc, nullptr};
     for (int t = 0; t < ntap; ++t) a.tapbase[t] = tapbase[t];
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(nbuf * stage));
@@ -1388,7 +1415,7 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     }
     refresh_if_stale(w, t, st);  // CSC-tiled weights from vals (through perm)
     FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, (int)spl, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
-                direct ? 1 : 0, t.rowmap, slices, t.nrb, nullptr, nullptr, B, 1, nullptr, {}, {}};
+                direct ? 1 : 0, t.rowmap, slices, t.nrb, nullptr, nullptr, B, 1, nullptr, {}, {}, nullptr};
     auto pick = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         note_path(tm ? "bwd_fused_tm_split" : "bwd_fused_split");

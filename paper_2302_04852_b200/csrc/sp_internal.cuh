@@ -70,6 +70,12 @@ struct sp_tiling {
     // slot in this tiling; `fresh` = the handle version whose values ent holds
     int32_t *inv;      // [nnz]
     mutable uint64_t fresh;
+    // CSC tilings (fused backward): per (row block, warp of RPWg rows), the prefix
+    // over column blocks of the warp's entry groups, gpre[g][(rb*NWg + w)*(nkb+1) + k]
+    // = sum over column blocks < k of ceil(segment length / (4 << g)) -- the TMEM
+    // dW column of a tile's first group without walking the earlier tiles
+    int32_t *gpre[2];
+    int RPWg;
 };
 
 // One tiling's entries as seen by the managed SGD kernel.
