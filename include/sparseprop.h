@@ -78,7 +78,8 @@ typedef struct {
  * plus the tiled copies of both orientations the kernels stream (row blocks x
  * column blocks), deterministically on the device; it
  * synchronises `stream` (to read nnz, block row counts and tile maxima).
- * R, C >= 1; R*C and nnz must fit int32 (else SP_ERR_OVERFLOW).
+ * R, C >= 1; R, C and nnz must fit int32 (else SP_ERR_OVERFLOW); R*C may
+ * exceed it (no R x C scratch is used).
  * The handle owns all its device buffers. */
 sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8_t *mask,
                            sp_stream_t stream, sp_weight_t *out);

@@ -160,8 +160,8 @@ sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8
     *out = nullptr;
     if (!dense || !mask) return fail(SP_ERR_NULL, "sp_weight_create: dense or mask is NULL");
     if (R < 1 || C < 1) return fail(SP_ERR_SHAPE, "sp_weight_create: R and C must be >= 1");
-    if (R > kI32Max || C > kI32Max || R * C > kI32Max)
-        return fail(SP_ERR_OVERFLOW, "sp_weight_create: R*C must fit int32");
+    if (R > kI32Max || C > kI32Max)
+        return fail(SP_ERR_OVERFLOW, "sp_weight_create: R and C must fit int32");
     sp_weight_s *w = new (std::nothrow) sp_weight_s();
     if (!w) return fail(SP_ERR_ALLOC, "sp_weight_create: host allocation failed");
     w->magic = SP_MAGIC;

@@ -32,15 +32,32 @@ __global__ void row_count_kernel(int64_t R, int64_t C, const uint8_t *__restrict
     if (lane == 0) cnt[r] = n;
 }
 
-// Thread per column: count kept entries down the column (coalesced across
-// threads: adjacent threads read adjacent bytes of each mask row).
-__global__ void col_count_kernel(int64_t R, int64_t C, const uint8_t *__restrict__ mask,
-                                 int32_t *__restrict__ cnt) {
+// Column counts by row blocks: thread (b, c) counts the kept entries of column
+// c in rows [b*rbk, (b+1)*rbk) (coalesced: adjacent threads read adjacent bytes
+// of each mask row).  blk[b*C + c] = that count.
+__global__ void colblk_count_kernel(int64_t R, int64_t C, int64_t nb, int64_t rbk, const uint8_t *__restrict__ mask,
+                                    int32_t *__restrict__ blk) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nb * C) return;
+    const int64_t b = i / C, c = i - b * C;
+    const int64_t r1 = min(R, (b + 1) * rbk);
+    int n = 0;
+    for (int64_t r = b * rbk; r < r1; ++r) n += mask[r * C + c] != 0;
+    blk[i] = n;
+}
+
+// Thread per column: blk[.][c] -> exclusive prefix over the row blocks (fixed
+// order), cnt[c] = the column's total.
+__global__ void colblk_scan_kernel(int64_t C, int64_t nb, int32_t *__restrict__ blk, int32_t *__restrict__ cnt) {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= C) return;
-    int n = 0;
-    for (int64_t r = 0; r < R; ++r) n += mask[r * C + c] != 0;
-    cnt[c] = n;
+    int32_t run = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        const int32_t v = blk[b * C + c];
+        blk[b * C + c] = run;
+        run += v;
+    }
+    cnt[c] = run;
 }
 
 // Single-block exclusive scan of n int32 counts into out[0..n] (out[n] = total)
@@ -83,13 +100,12 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(int64_t n, const int
     if (t == kScanThreads - 1) out[n] = (int32_t)run;
 }
 
-// Warp per row: stable compaction with ballots.  Writes col_idx, vals,
-// row_of, and the CSR slot of every kept (r, c) into slot[r*C + c].
+// Warp per row: stable compaction with ballots.  Writes col_idx, vals, row_of.
 __global__ void csr_compact_kernel(int64_t R, int64_t C, const uint8_t *__restrict__ mask,
                                    const float *__restrict__ dense,
                                    const int32_t *__restrict__ row_ptr,
                                    int32_t *__restrict__ col_idx, float *__restrict__ vals,
-                                   int32_t *__restrict__ row_of, int32_t *__restrict__ slot) {
+                                   int32_t *__restrict__ row_of) {
     const int lane = threadIdx.x & 31;
     const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (r >= R) return;
@@ -104,24 +120,34 @@ __global__ void csr_compact_kernel(int64_t R, int64_t C, const uint8_t *__restri
             col_idx[j] = (int32_t)c;
             vals[j] = dense[r * C + c];
             row_of[j] = (int32_t)r;
-            slot[r * C + c] = j;
         }
         pos += __popc(bal);
     }
 }
 
-// Thread per column: rows ascending, perm = CSR slot of (r, c).
-__global__ void csc_compact_kernel(int64_t R, int64_t C, const uint8_t *__restrict__ mask,
-                                   const int32_t *__restrict__ slot,
-                                   const int32_t *__restrict__ col_ptr,
+// CSC compaction by row blocks: thread (b, c) writes column c's kept rows of
+// block b (ascending) from position col_ptr[c] + blk[b][c]; perm = the CSR slot
+// of (r, c), found by binary search of c in row r's (ascending) col_idx.  No
+// R x C scratch: works for any R * C.
+__global__ void csc_compact_kernel(int64_t R, int64_t C, int64_t nb, int64_t rbk, const uint8_t *__restrict__ mask,
+                                   const int32_t *__restrict__ blk, const int32_t *__restrict__ col_ptr,
+                                   const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col_idx,
                                    int32_t *__restrict__ row_idx, int32_t *__restrict__ perm) {
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= C) return;
-    int32_t k = col_ptr[c];
-    for (int64_t r = 0; r < R; ++r) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nb * C) return;
+    const int64_t b = i / C, c = i - b * C;
+    const int64_t r1 = min(R, (b + 1) * rbk);
+    int32_t k = col_ptr[c] + blk[i];
+    for (int64_t r = b * rbk; r < r1; ++r) {
         if (mask[r * C + c]) {
+            int32_t lo = row_ptr[r], hi = row_ptr[r + 1] - 1;  // c is in [lo, hi]
+            while (lo < hi) {
+                const int32_t mid = (lo + hi) >> 1;
+                if (col_idx[mid] < (int32_t)c) lo = mid + 1;
+                else hi = mid;
+            }
             row_idx[k] = (int32_t)r;
-            perm[k] = slot[r * C + c];
+            perm[k] = lo;
             ++k;
         }
     }
@@ -312,7 +338,10 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
                        cudaStream_t st, sp_weight_s *w) {
     w->R = R;
     w->C = C;
-    int32_t *rcnt = nullptr, *ccnt = nullptr, *slot = nullptr;
+    int32_t *rcnt = nullptr, *ccnt = nullptr, *blk = nullptr;
+    // column counts / CSC compaction by row blocks: about 256k (block, column) threads
+    const int64_t nb = std::max<int64_t>(1, std::min<int64_t>(R, (262144 + C - 1) / C));
+    const int64_t rbk = (R + nb - 1) / nb;
     int64_t *info = nullptr;
     cudaError_t e = cudaSuccess;
 #define SP_TRY(x)                                   \
@@ -323,11 +352,13 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
     SP_TRY(scratch_alloc((void **)&rcnt, (size_t)R * sizeof(int32_t), st));
     SP_TRY(scratch_alloc((void **)&ccnt, (size_t)C * sizeof(int32_t), st));
     SP_TRY(scratch_alloc((void **)&info, 4 * sizeof(int64_t), st));
+    SP_TRY(scratch_alloc((void **)&blk, (size_t)(nb * C) * sizeof(int32_t), st));
     SP_TRY(dmalloc(&w->row_ptr, R + 1));
     SP_TRY(dmalloc(&w->col_ptr, C + 1));
     {
         row_count_kernel<<<(unsigned)((R + 7) / 8), 256, 0, st>>>(R, C, mask, rcnt);
-        col_count_kernel<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(R, C, mask, ccnt);
+        colblk_count_kernel<<<(unsigned)((nb * C + 255) / 256), 256, 0, st>>>(R, C, nb, rbk, mask, blk);
+        colblk_scan_kernel<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(C, nb, blk, ccnt);
         scan_kernel<<<1, kScanThreads, 0, st>>>(R, rcnt, w->row_ptr, info);
         scan_kernel<<<1, kScanThreads, 0, st>>>(C, ccnt, w->col_ptr, info + 2);
         SP_TRY(cudaGetLastError());
@@ -343,6 +374,7 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
             scratch_free(rcnt, st);
             scratch_free(ccnt, st);
             scratch_free(info, st);
+            scratch_free(blk, st);
             set_error("nnz does not fit int32");
             return SP_ERR_OVERFLOW;
         }
@@ -355,12 +387,11 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
     SP_TRY(dmalloc(&w->row_of, w->nnz));
     SP_TRY(dmalloc(&w->row_idx, w->nnz));
     SP_TRY(dmalloc(&w->perm, w->nnz));
-    SP_TRY(scratch_alloc((void **)&slot, (size_t)(R * C) * sizeof(int32_t), st));
     csr_compact_kernel<<<(unsigned)((R + 7) / 8), 256, 0, st>>>(R, C, mask, dense, w->row_ptr,
-                                                              w->col_idx, w->vals, w->row_of,
-                                                              slot);
-    csc_compact_kernel<<<(unsigned)((C + 127) / 128), 128, 0, st>>>(R, C, mask, slot, w->col_ptr,
-                                                                   w->row_idx, w->perm);
+                                                              w->col_idx, w->vals, w->row_of);
+    csc_compact_kernel<<<(unsigned)((nb * C + 255) / 256), 256, 0, st>>>(R, C, nb, rbk, mask, blk, w->col_ptr,
+                                                                       w->row_ptr, w->col_idx, w->row_idx,
+                                                                       w->perm);
     SP_TRY(cudaGetLastError());
     // gather-SDDMM work list: chunks of <= 32 consecutive nonzeros of one row
     SP_TRY(dmalloc(&w->chunk_ptr, R + 1));
@@ -370,7 +401,7 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
         const sp_status ts = build_tilings(w, st);
         if (ts != SP_OK) {
             set_error("sp_weight_create: tiling build failed");
-            scratch_free(slot, st);
+            scratch_free(blk, st);
             scratch_free(rcnt, st);
             scratch_free(ccnt, st);
             scratch_free(info, st);
@@ -378,13 +409,13 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
         }
     }
     // Temporaries are freed in stream order (no second host sync).
-    scratch_free(slot, st);
+    scratch_free(blk, st);
     scratch_free(rcnt, st);
     scratch_free(ccnt, st);
     scratch_free(info, st);
     return SP_OK;
 fail:
-    if (slot) scratch_free(slot, st);
+    if (blk) scratch_free(blk, st);
     if (rcnt) scratch_free(rcnt, st);
     if (ccnt) scratch_free(ccnt, st);
     if (info) scratch_free(info, st);
@@ -439,30 +470,13 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
         sp_tiling *t;
         bool need;  // tilings of A/B variants are built only when their switch is set
     };
-    const int fnw = fused_nw();
-    const bool tm = spmm_tm_mode() == 1;
     const Spec specs[] = {{0, kTilRB[0], kTilKC[0], kTilNW[0], 4, &w->til[0][0], true},
                           {0, kTilRB[1], kTilKC[1], kTilNW[1], kTilRB[1] / kTilNW[1], &w->til[0][1], true},
                           {1, kTilRB[0], kTilKC[0], kTilNW[0], 4, &w->til[1][0], true},
                           {1, kTilRB[1], kTilKC[1], kTilNW[1], kTilRB[1] / kTilNW[1], &w->til[1][1], true},
                           {1, 64, kTilKC[0], 32, 2, &w->til_f[0], true},
                           {1, 32, kTilKC[0], 32, 1, &w->til_f[1], true},
-                          {1, 96, kTilKC[0], 24, 4, &w->til_f[2], fnw == 24},
-                          {1, 64, kTilKC[0], 16, 4, &w->til_f[3], true},
-                          {1, 112, kTilKC[0], 28, 4, &w->til_f[4], fnw == 28},
-                          {1, 56, kTilKC[0], 28, 2, &w->til_f[5], fnw == 28},
-                          {1, 48, kTilKC[0], 24, 2, &w->til_f[6], fnw == 24},
-                          {0, 112, kTmKC, 28, 4, &w->til_t[0][0], tm},
-                          {1, 112, kTmKC, 28, 4, &w->til_t[1][0], tm},
-                          {0, 96, kTmKC, 24, 4, &w->til_t[0][1], tm},
-                          {1, 96, kTmKC, 24, 4, &w->til_t[1][1], tm},
-                          {0, 128, kTmKC, 16, 8, &w->til_t[0][2], tm},
-                          {1, 128, kTmKC, 16, 8, &w->til_t[1][2], tm},
-                          {0, 256, kTmKC, 16, 16, &w->til_t[0][3], tm},
-                          {1, 256, kTmKC, 16, 16, &w->til_t[1][3], tm},
-                          {1, 64, 128, 32, 2, &w->til_f128, fused_kc128()},
-                          {0, 256, 160, 32, 8, &w->til_r256[0], spmm_rb256()},
-                          {1, 256, 160, 32, 8, &w->til_r256[1], spmm_rb256()}};
+                          {1, 64, kTilKC[0], 16, 4, &w->til_f[2], true}};
     constexpr int NS = sizeof(specs) / sizeof(specs[0]);
     int64_t *info = nullptr, *mx = nullptr;
     if (scratch_alloc((void **)&info, 2 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
@@ -593,10 +607,7 @@ void free_tilings(sp_weight_s *w) {
         for (auto &t : o) fr(t);
     for (auto &t : w->tapf) fr(t);
     for (auto &t : w->til_f) fr(t);
-    for (auto &o : w->til_t)
-        for (auto &t : o) fr(t);
-    fr(w->til_f128);
-    for (auto &t : w->til_r256) fr(t);
+
     if (w->tapdev) cudaFree(w->tapdev);
     w->tapdev = nullptr;
     if (w->sgdtab) cudaFree(w->sgdtab);
@@ -623,10 +634,7 @@ void launch_weight_sgd(sp_weight_s *w, const float *dW, float lr, cudaStream_t s
     for (auto &o : w->til)
         for (auto &t : o) mark(t);
     for (auto &t : w->til_f) mark(t);
-    for (auto &o : w->til_t)
-        for (auto &t : o) mark(t);
-    mark(w->til_f128);
-    for (auto &t : w->til_r256) mark(t);
+
 }
 
 void launch_refresh(const sp_tiling &t, const float *vals, int64_t nnz, cudaStream_t st) {

@@ -1121,55 +1121,7 @@ __global__ void __launch_bounds__(256) job_reduce_kernel(const JobReduceArgs a) 
 }
 
 
-// SP_FUSED_TMEM=0 selects the register-slot variant (A/B measurements).
-bool tm_disabled() {
-    static const int v = [] {
-        const char *e = getenv("SP_FUSED_TMEM");
-        return (e && e[0] == '0') ? 1 : 0;
-    }();
-    return v != 0;
-}
-
-// Half-warp entries (8 batch columns per lane, 16-lane dW reductions) unless
-// SP_FUSED_HALF=0 (A/B)
-bool fused_half() {
-    static const int v = [] {
-        const char *e = getenv("SP_FUSED_HALF");
-        return (e && e[0] == '0') ? 0 : 1;
-    }();
-    return v != 0;
-}
-
-// SP_FUSED_SK=0 keeps the slice-split grid for the TMEM variant (A/B measurements).
-bool sk_disabled() {
-    static const int v = [] {
-        const char *e = getenv("SP_FUSED_SK");
-        return (e && e[0] == '0') ? 1 : 0;
-    }();
-    return v != 0;
-}
-
 }  // namespace
-
-// SP_FUSED_KC128=1: the half-warp fused backward on 128-column tiles with
-// three shared-memory stages (two tiles of drift between warps; A/B)
-bool fused_kc128() {
-    static const int v = [] {
-        const char *e = getenv("SP_FUSED_KC128");
-        return (e && e[0] == '1') ? 1 : 0;
-    }();
-    return v != 0;
-}
-
-// SP_FUSED_NW=24|16|28: the stream-K kernel with fewer warps x 4 rows (A/B)
-int fused_nw() {
-    static const int v = [] {
-        const char *e = getenv("SP_FUSED_NW");
-        return e ? atoi(e) : 32;
-    }();
-    return v;
-}
-
 
 // Stream-K launch of the TMEM kernel (fused backward, or dW alone when dX is
 // null).  Returns false when it does not apply (ragged B, staged entries do
@@ -1240,38 +1192,18 @@ static bool launch_sk(const sp_weight_s *w, const float *X, const float *dY, con
     const bool dw = dX == nullptr;
     auto fits = [&](const sp_tiling &t, int64_t cols) { return t.seg != nullptr && t.max_warp_groups <= cols * 8; };
     auto fits8 = [&](const sp_tiling &t, int64_t cols) { return t.seg != nullptr && t.max_warp_groups8 <= cols * 4; };
-    if (fused_half()) {
-        if (!dw && fused_kc128() && fits8(w->til_f128, sk_dwcols<2, false, 32, true>()) &&
-            launch_sk_rpw<2, 32, true, 3>(w, w->til_f128, X, dY, H, dX, dW, B, st))
-            return true;
-        if (dw && fits8(w->til[1][0], sk_dwcols<4, true, 32, true>()) && w->til[1][0].RB == 128 &&
-            launch_sk_rpw<4, 32, true>(w, w->til[1][0], X, dY, H, dX, dW, B, st))
-            return true;
-        if (!dw && fused_nw() == 28 && fits8(w->til_f[5], sk_dwcols<2, false, 28, true>()) &&
-            launch_sk_rpw<2, 28, true>(w, w->til_f[5], X, dY, H, dX, dW, B, st))
-            return true;
-        if (!dw && fused_nw() == 24 && fits8(w->til_f[6], sk_dwcols<2, false, 24, true>()) &&
-            launch_sk_rpw<2, 24, true>(w, w->til_f[6], X, dY, H, dX, dW, B, st))
-            return true;
-        if (!dw && fused_nw() == 16 && fits8(w->til_f[3], sk_dwcols<4, false, 16, true>()) &&
-            launch_sk_rpw<4, 16, true>(w, w->til_f[3], X, dY, H, dX, dW, B, st))
-            return true;
-        if (!dw && fits8(w->til_f[0], sk_dwcols<2, false, 32, true>()) &&
-            launch_sk_rpw<2, 32, true>(w, w->til_f[0], X, dY, H, dX, dW, B, st))
-            return true;
-        if (!dw && fits8(w->til_f[3], sk_dwcols<4, false, 16, true>()) &&
-            launch_sk_rpw<4, 16, true>(w, w->til_f[3], X, dY, H, dX, dW, B, st))
-            return true;
-    }
-    if (fused_nw() == 24 && fits(w->til_f[2], dw ? sk_dwcols<4, true, 24>() : sk_dwcols<4, false, 24>()) &&
-        launch_sk_rpw<4, 24>(w, w->til_f[2], X, dY, H, dX, dW, B, st))
+    // half-warp entries (8 batch columns per lane): dW alone on 128-row blocks, the
+    // fused backward on 64-row blocks (32 warps x 2 rows, else 16 warps x 4 rows)
+    if (dw && fits8(w->til[1][0], sk_dwcols<4, true, 32, true>()) && w->til[1][0].RB == 128 &&
+        launch_sk_rpw<4, 32, true>(w, w->til[1][0], X, dY, H, dX, dW, B, st))
         return true;
-    if (fused_nw() == 16 && fits(w->til_f[3], dw ? sk_dwcols<4, true, 16>() : sk_dwcols<4, false, 16>()) &&
-        launch_sk_rpw<4, 16>(w, w->til_f[3], X, dY, H, dX, dW, B, st))
+    if (!dw && fits8(w->til_f[0], sk_dwcols<2, false, 32, true>()) &&
+        launch_sk_rpw<2, 32, true>(w, w->til_f[0], X, dY, H, dX, dW, B, st))
         return true;
-    if (fused_nw() == 28 && fits(w->til_f[4], dw ? sk_dwcols<4, true, 28>() : sk_dwcols<4, false, 28>()) &&
-        launch_sk_rpw<4, 28>(w, w->til_f[4], X, dY, H, dX, dW, B, st))
+    if (!dw && fits8(w->til_f[2], sk_dwcols<4, false, 16, true>()) &&
+        launch_sk_rpw<4, 16, true>(w, w->til_f[2], X, dY, H, dX, dW, B, st))
         return true;
+    // whole-warp entries (more dW columns per warp): long rows (e.g. Zipf head rows)
     if (fits(w->til[1][0], dw ? sk_dwcols<4, true>() : sk_dwcols<4, false>()) && w->til[1][0].RB == 128 &&
         launch_sk_rpw<4>(w, w->til[1][0], X, dY, H, dX, dW, B, st))
         return true;
@@ -1286,7 +1218,7 @@ static bool launch_sk(const sp_weight_s *w, const float *X, const float *dY, con
 }
 
 bool launch_sddmm_sk(const sp_weight_s *w, const float *X, const float *dY, float *dW, int64_t B, cudaStream_t st) {
-    return !sk_disabled() && launch_sk(w, X, dY, nullptr, nullptr, dW, B, st);
+    return launch_sk(w, X, dY, nullptr, nullptr, dW, B, st);
 }
 
 // Conv backward by taps through the stream-K TMEM kernel (the paper's Alg. 2
@@ -1300,12 +1232,12 @@ bool launch_sddmm_sk(const sp_weight_s *w, const float *X, const float *dY, floa
 bool launch_conv_bwd_sk(const sp_weight_s *w, const ConvCols &cc, const float *dY, int64_t OH, int64_t OW,
                         const float *X, float *dX, float *dW, int ntap, cudaStream_t st) {
     constexpr int TRPW = 2, TNW = 32, BT = 128, RBF = TRPW * TNW;
-    if (sk_disabled() || w->nnz == 0 || ntap > kMaxTaps) return false;
+    if (w->nnz == 0 || ntap > kMaxTaps) return false;
     const sp_tiling &t0 = w->tapf[0];
     if (t0.RB != RBF || t0.seg == nullptr) return false;
     const bool dwonly = dX == nullptr;
     // half-warp entries (8 batch columns per lane) when the groups of 8 fit the TMEM dW columns
-    const bool half = fused_half() && !dwonly && w->tapf_groups8 <= (int64_t)sk_dwcols<TRPW, false, TNW, true>() * 4;
+    const bool half = !dwonly && w->tapf_groups8 <= (int64_t)sk_dwcols<TRPW, false, TNW, true>() * 4;
     const int64_t groups_cap = (int64_t)(dwonly ? sk_dwcols<TRPW, true>() : sk_dwcols<TRPW, false>()) * 8;
     if (!half && w->tapf_groups > groups_cap) return false;
     const int64_t slices = (int64_t)cc.Po * cc.spr;
@@ -1374,7 +1306,7 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const ConvCols &cc, const float *d
 sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY, const float *H, float *dX,
                            float *dW, int64_t B, cudaStream_t st) {
     // stream-K TMEM kernel (any B % 4 == 0) when the rows fit its TMEM columns
-    if (!tm_disabled() && !sk_disabled() && launch_sk(w, X, dY, H, dX, dW, B, st)) return SP_OK;
+    if (launch_sk(w, X, dY, H, dX, dW, B, st)) return SP_OK;
     // slice-split grids: B % 4 == 0, at least one full slice, the big CSC tiling
     if ((B & 3) != 0 || B < 128 || w->nnz == 0) return SP_ERR_SHAPE;
     constexpr int RPW = 8, NW = 16, BT = 128;
@@ -1388,7 +1320,7 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
     const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)(226 * 1024);
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
     // TMEM variant: staged entries and at most kTmCols*32 padded entries per warp
-    const bool tm = sent && !tm_disabled() && t.max_warp_groups <= (int64_t)tm_cols<TNW>() * 8;  // 8 groups per TMEM column
+    const bool tm = sent && t.max_warp_groups <= (int64_t)tm_cols<TNW>() * 8;  // 8 groups per TMEM column
     if ((int64_t)t.nrb * slices < num_sms()) return SP_ERR_SHAPE;  // too little parallelism: use the separate kernels
     int64_t nsplit, spl;
     if (tm) {

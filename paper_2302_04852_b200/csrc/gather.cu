@@ -138,11 +138,6 @@ __global__ void __launch_bounds__(256)
 // Gather path wins when staging would move more bytes than gathering:
 // nrb * inner (tile rows streamed per batch column) > nnz (rows gathered).
 bool gather_preferred(const sp_weight_s *w, int orient, int64_t B, bool chunked) {
-    static const int force = [] {  // SP_GATHER=1 / 0: force / forbid the gather kernels (A/B)
-        const char *e = getenv("SP_GATHER");
-        return e ? (e[0] == '1' ? 1 : 0) : -1;
-    }();
-    if (force >= 0) return force == 1;
     // the gather SpMM walks a whole row per warp: skewed rows (Zipf) would
     // serialise the tail, so only balanced structures take it (the SDDMM's
     // 32-nonzero chunks are balanced by construction)
@@ -155,7 +150,7 @@ bool gather_preferred(const sp_weight_s *w, int orient, int64_t B, bool chunked)
     const sp_tiling &t = w->til[orient][1];  // the smallest tiling the tiled path would fall back to
     const sp_tiling &t0 = w->til[orient][0];
     const int64_t slices = (B + 127) / 128;
-    const sp_tiling &tt = (int64_t)t0.nrb * slices >= 2 * 148 ? t0 : t;
+    const sp_tiling &tt = (int64_t)t0.nrb * slices >= 2 * num_sms() ? t0 : t;
     return (double)tt.nrb * (double)tt.inner > 1.25 * (double)w->nnz;
 }
 

@@ -101,16 +101,10 @@ struct sp_weight_s {
     int32_t *chunk_ptr;  // [R+1] exclusive scan of ceil(row nnz / 32) (gather SDDMM work list)
     // tilings: [orientation 0 = CSR rows, 1 = CSC columns][variant 0 = big, 1 = small]
     sp_tiling til[2][2];
-    // CSC tilings of the fused backward for dense-ish rows (KC = 192): [0] 64-row
-    // blocks (32 warps x 2 rows), [1] 32-row blocks (32 warps x 1 row)
-    sp_tiling til_f[7];  // [2..4]: 96/64/112-row blocks (24/16/28 warps x 4 rows, experimental)
-    // tilings of the TMEM-gather SpMM (spmm_tm.cu): [orientation][variant], KC = kTmKC,
-    // RB = 112 (28 compute warps x 4 rows) / 96 (24 x 4) / 128 (16 x 8) / 256 (16 x 16)
-    sp_tiling til_t[2][4];
-    // CSC tiling with 128-column tiles for the 3-stage fused backward (SP_FUSED_KC128=1)
-    sp_tiling til_f128;
-    // 256-row blocks with 160-column tiles for the SpMM A/B (SP_SPMM_RB256=1): [orientation]
-    sp_tiling til_r256[2];
+    // CSC tilings of the fused backward (KC = 192): [0] 64-row blocks (32 warps x 2
+    // rows), [1] 32-row blocks (32 warps x 1 row, long rows), [2] 64-row blocks
+    // as 16 warps x 4 rows (half-warp entries when [0]'s dW columns overflow)
+    sp_tiling til_f[3];
     // conv handles (sp_weight_create_conv): filter taps and, per tap (x, y),
     // tilings of the OC x IC tap matrix W_xy -- [0]: rows oc / inner ic,
     // [1]: rows ic / inner oc -- whose vidx are slots of THIS handle's CSR.
@@ -146,9 +140,6 @@ constexpr int kTilNW[2] = {16, 8};  // warps per CTA of the kernels using each v
 // (kTilRowBytes); kernels with narrower tiles shift them down.  Conv tap
 // tilings are padded the same way (kTapPad).
 constexpr int kTilPad = 2;
-// inner columns per tile of the TMEM-gather SpMM tilings (til_t): 4 zero + 63 x 4
-// tile columns fill one 256-column TMEM buffer
-constexpr int kTmKC = 63;
 // tile rows the split-source SpMM mirrors in TMEM (the last kHybTC of a tile)
 constexpr int kHybTC = 63;
 constexpr int kTapPad = 2;  // (was 4: groups of 4 without tails; even padding wastes fewer slots)
@@ -223,18 +214,7 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
 bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, const ConvCols &cc, const float *in, int64_t Hi,
                          int64_t Wi, float *out, int ntap, cudaStream_t st);
 
-// ---- fused.cu: warps per CTA of the fused backward (SP_FUSED_NW A/B switch, default 32)
-int fused_nw();
-bool spmm_rb256();
-bool fused_kc128();
-
-// ---- spmm_tm.cu: TMEM-gather SpMM (B % 4 == 0); false if it does not apply
-int spmm_tm_mode();
-bool launch_spmm_tm(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,
-                    int epi, cudaStream_t st);
-
 // ---- spmm_hyb.cu: the 32-warp SpMM with the tiles' last rows mirrored in TMEM
-int spmm_hyb_mode();
 bool launch_spmm_hyb(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,
                      int epi, cudaStream_t st);
 

@@ -267,26 +267,11 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
     }
 }
 
-// variant 0 runs as 32 warps x 4 rows (SP_SPMM_NW32=0: 16 warps x 8 rows, for A/B measurements)
-bool spmm_nw32() {
-    static const int v = [] {
-        const char *e = getenv("SP_SPMM_NW32");
-        return (e && e[0] == '0') ? 0 : 1;
-    }();
-    return v != 0;
-}
-// The stream-K SpMM (spmm_sk.cu): SP_SPMM_SK=1 forces it, =0 disables it; by
-// default it runs when the per-item grid is short (< 2 waves of 128-row items)
-// and the items are long (>= 8 column blocks) -- e.g. the 768-row cfg5 layer at
-// a per-rank batch of 2048-4096: +10-17%.  Elsewhere the per-item grid wins
-// (measured) and keeps every output element's order independent of B.
-int spmm_sk_mode() {
-    static const int v = [] {
-        const char *e = getenv("SP_SPMM_SK");
-        return e ? (e[0] == '1' ? 1 : 0) : -1;
-    }();
-    return v;
-}
+// The stream-K SpMM (spmm_sk.cu) runs when the per-item grid is short (< 2
+// waves of 128-row items) and the items are long (>= 8 column blocks) -- e.g.
+// the 768-row cfg5 layer at a per-rank batch of 2048-4096: +10-17%.  Elsewhere
+// the per-item grid wins (measured) and keeps every output element's order
+// independent of B.
 constexpr int kSmemLimit = 226 * 1024;  // per SM, usable by CTAs (minus static mbarriers)
 
 template <int VEC, int RPW, int NW>
@@ -325,7 +310,7 @@ void launch_cfg(const sp_tiling &t, int64_t B, const float *in, float *out, cons
 template <int VEC>
 void launch_variant(const sp_tiling &t, int v, int64_t B, const float *in, float *out, const float *gate,
                     int epi, cudaStream_t st) {
-    if (v == 0) { if (spmm_nw32()) launch_cfg<VEC, 4, 32>(t, B, in, out, gate, epi, st); else launch_cfg<VEC, 8, 16>(t, B, in, out, gate, epi, st); }
+    if (v == 0) launch_cfg<VEC, 4, 32>(t, B, in, out, gate, epi, st);
     else launch_cfg<VEC, 4, 8>(t, B, in, out, gate, epi, st);
 }
 
@@ -360,16 +345,6 @@ bool conv_spmm_vec(const sp_weight_s *w, int orient, int64_t B, const float *in,
 
 }  // namespace
 
-// SP_SPMM_RB256=1: 256-row blocks (32 warps x 8 rows, KC = 160): half the tile
-// fill per entry, more accumulator registers (A/B measurements)
-bool spmm_rb256() {
-    static const int v = [] {
-        const char *e = getenv("SP_SPMM_RB256");
-        return (e && e[0] == '1') ? 1 : 0;
-    }();
-    return v != 0;
-}
-
 // Conv products as tap-tiled SpMM on a padded copy (see conv.cu; the fallback
 // of the exact-column stream-K path for batch sizes it cannot slice): in = padded activation
 // [inner x Lp], taps[t] tilings of orientation `orient`, shift sh[t] columns;
@@ -393,20 +368,10 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
         launch_spmm_gather(w, orient, B, in, out, gate, epi, st);
         return;
     }
-    if (spmm_tm_mode() == 1 && launch_spmm_tm(w, orient, B, in, out, gate, epi, st)) return;
-    if (spmm_hyb_mode() == 1 && launch_spmm_hyb(w, orient, B, in, out, gate, epi, st)) return;
     {
         const sp_tiling &t0 = w->til[orient][0];
         const int64_t items = (int64_t)t0.nrb * ((B + 127) / 128);
-        const int mode = spmm_sk_mode();
-        const bool sk = mode == 1 || (mode < 0 && items < 2 * num_sms() && t0.nkb >= 8);
-        if (sk && launch_spmm_sk(w, orient, B, in, out, gate, epi, st)) return;
-    }
-    if (spmm_rb256() && (B & 3) == 0 && w->til_r256[orient].seg) {  // A/B: 256-row blocks, 32 warps x 8 rows
-        const sp_tiling &t = w->til_r256[orient];
-        refresh_if_stale(w, t, st);
-        launch_cfg<4, 8, 32>(t, B, in, out, gate, epi, st);
-        return;
+        if (items < 2 * num_sms() && t0.nkb >= 8 && launch_spmm_sk(w, orient, B, in, out, gate, epi, st)) return;
     }
     // Choose the largest row block and batch vector that still fill the GPU.
     int vec = B <= 32 ? 1 : (B <= 64 || (B & 3)) ? 2 : 4;
@@ -416,12 +381,10 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
     };
     if (ctas(0, vec) < 2 * num_sms()) var = 1;
     while (var == 1 && vec > 1 && ctas(1, vec) < 2 * num_sms()) vec >>= 1;
-    // the 32-warp layout takes the split-source kernel by default: the same
-    // entries in the same order (bitwise the same result), a third of the
-    // gathers from TMEM (SP_SPMM_HYB=0 keeps the shared-memory-only kernel)
-    if (var == 0 && vec == 4 && spmm_nw32() && spmm_hyb_mode() != 0 &&
-        launch_spmm_hyb(w, orient, B, in, out, gate, epi, st))
-        return;
+    // the 32-warp layout takes the split-source kernel: the same entries in the
+    // same order (bitwise the shared-memory kernel's result), a third of the
+    // gathers from TMEM
+    if (var == 0 && vec == 4 && launch_spmm_hyb(w, orient, B, in, out, gate, epi, st)) return;
     const sp_tiling &t = w->til[orient][var];
     refresh_if_stale(w, t, st);
     if (vec == 4) launch_variant<4>(t, var, B, in, out, gate, epi, st);

@@ -344,16 +344,6 @@ constexpr int kSmemHyb = 226 * 1024;
 
 }  // namespace
 
-// SP_SPMM_HYB=1 forces the split-source SpMM wherever it applies, =0 disables
-// it; default: for the per-item 32-warp layout (launch_spmm).
-int spmm_hyb_mode() {
-    static const int v = [] {
-        const char *e = getenv("SP_SPMM_HYB");
-        return e ? (e[0] == '1' ? 1 : 0) : -1;
-    }();
-    return v;
-}
-
 // The 32-warp big-tiling SpMM with the TMEM mirror; false when it does not
 // apply (ragged B, a tiling other than RB = 128 / KC = 192, staged entries
 // that do not fit).
@@ -369,12 +359,7 @@ bool launch_spmm_hyb(const sp_weight_s *w, int orient, int64_t B, const float *i
     CUtensorMap tmap{};
     if (!make_tmap_2d(&tmap, in, t.inner, B, HY_BT, t.KC)) return false;
     refresh_if_stale(w, t, st);
-    static unsigned long long *stats = nullptr;
-    static const bool want_stats = getenv("SP_SPMM_HYB_STATS") != nullptr;
-    if (want_stats && !stats) {
-        cudaMalloc(&stats, 2 * sizeof(unsigned long long));
-        cudaMemset(stats, 0, 2 * sizeof(unsigned long long));
-    }
+    unsigned long long *stats = nullptr;  // entry counters of a measurement build (none in the product)
     HybArgs a{t.rows, B, t.KC, t.nkb, cap, t.seg, t.tmsplit, t.ent, out, gate, t.rowmap, stats};
     dim3 grid((unsigned)t.nrb, (unsigned)((B + HY_BT - 1) / HY_BT));
     auto launch = [&](auto kern) {
@@ -383,20 +368,12 @@ bool launch_spmm_hyb(const sp_weight_s *w, int orient, int64_t B, const float *i
         note_path("spmm_hyb");
         kern<<<grid, HY_NW * 32, smem, st>>>(a, tmap);
     };
-    if (stats)
-        launch(spmm_hyb_kernel<EPI_NONE, true>);  // entry counts only (measurement)
-    else if (epi == EPI_RELU)
+    if (epi == EPI_RELU)
         launch(spmm_hyb_kernel<EPI_RELU, false>);
     else if (epi == EPI_GATE)
         launch(spmm_hyb_kernel<EPI_GATE, false>);
     else
         launch(spmm_hyb_kernel<EPI_NONE, false>);
-    if (stats) {
-        unsigned long long h[2];
-        cudaStreamSynchronize(st);
-        cudaMemcpy(h, stats, sizeof(h), cudaMemcpyDeviceToHost);
-        fprintf(stderr, "spmm_hyb: %llu of %llu entries gathered from TMEM (cumulative)\n", h[0], h[1]);
-    }
     return true;
 }
 

@@ -454,15 +454,9 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
         note_path("spmm_sk");
         kern<<<(unsigned)G, NW * 32, smem, st>>>(a, tmap);
     };
-    // the TMEM mirror of the tiles' last rows only when forced (SP_SPMM_HYB=1): on
-    // the linear stream-K shapes it measured slower (768-row layer, B = 2048 /
-    // 4096: 83 -> 87 / 131 -> 143 us; the copies cover a third of a 192-row tile)
-    const bool tmm = spmm_hyb_mode() == 1 && t.tmsplit != nullptr && t.KC > kHybTC;
-    if (tmm) {
-        if (epi == EPI_RELU) go(spmm_sk_kernel<RPW, NW, EPI_RELU, false, true>);
-        else if (epi == EPI_GATE) go(spmm_sk_kernel<RPW, NW, EPI_GATE, false, true>);
-        else go(spmm_sk_kernel<RPW, NW, EPI_NONE, false, true>);
-    } else if (epi == EPI_RELU) go(spmm_sk_kernel<RPW, NW, EPI_RELU, false>);
+    // (the TMEM mirror of the tiles' last rows measured slower on the linear
+    // stream-K shapes: 768-row layer, B = 2048 / 4096: 83 -> 87 / 131 -> 143 us)
+    if (epi == EPI_RELU) go(spmm_sk_kernel<RPW, NW, EPI_RELU, false>);
     else if (epi == EPI_GATE) go(spmm_sk_kernel<RPW, NW, EPI_GATE, false>);
     else go(spmm_sk_kernel<RPW, NW, EPI_NONE, false>);
     count_launches(1);

@@ -54,7 +54,8 @@ def test_argument_validation_without_gpu(L):
     assert L.sp_weight_create(4, 4, None, None, None, ct.byref(h)) == 1          # SP_ERR_NULL
     assert "NULL" in L.sp_last_error().decode()
     assert L.sp_weight_create(0, 4, 1, 1, None, ct.byref(h)) == 2                # SP_ERR_SHAPE
-    assert L.sp_weight_create(1 << 20, 1 << 20, 1, 1, None, ct.byref(h)) == 3    # SP_ERR_OVERFLOW
+    assert L.sp_weight_create(1 << 31, 4, 1, 1, None, ct.byref(h)) == 3         # SP_ERR_OVERFLOW: R > int32
+    assert L.sp_weight_create(4, 1 << 31, 1, 1, None, ct.byref(h)) == 3         # C > int32
     assert L.sp_weight_create(4, 4, 1, 1, None, None) == 1
     assert L.sp_linear_fwd(None, 1, 1, 8, None) == 6                              # SP_ERR_BAD_HANDLE
     assert L.sp_linear_bwd_input(None, 1, 1, 8, None) == 6

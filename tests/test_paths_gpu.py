@@ -1,0 +1,118 @@
+"""Every kernel family the library dispatches to by default, reached through a
+shape that selects it (sp_last_path names what ran), checked against the fp64
+oracle at the north-star tolerance.  Replaces round 1's environment-switch
+matrix: the measured-slower variants those switches selected are gone, and
+each family that remains is a default choice for some shape."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from conftest import tol_ok
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+NT = min(8, oracle.threads_available())
+
+
+@pytest.fixture(scope="module")
+def sp():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    from paper_2302_04852_b200 import _build, sparseprop
+    _build.build()
+    return sparseprop
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _ok(name, got, ref):
+    ok, err, bound = tol_ok(got.detach().cpu().numpy(), ref)
+    assert ok, f"{name}: max|err| {err:.3e} > {bound:.3e}"
+
+
+# (R, C, B, density, op, expected kernel family in sp_last_path)
+LINEAR = [
+    (3072, 768, 2048, 0.05, "fwd", "spmm_hyb"),        # per-item grid, 32 warps, TMEM-mirrored tiles
+    (768, 3072, 2048, 0.05, "fwd", "spmm_sk"),         # short per-item grid, long items: stream-K
+    (3072, 768, 512, 0.05, "fwd", "spmm_tiled"),       # small row blocks (8 warps)
+    (256, 256, 32, 0.1, "fwd", "spmm_gather"),         # tiny product: straight from L2
+    (768, 3072, 2048, 0.05, "dx", "spmm_hyb"),         # CSC-driven dX (gather form)
+    (3072, 768, 2048, 0.05, "dw", "sddmm_sk"),         # dW alone through the stream-K TMEM kernel
+    (256, 256, 32, 0.1, "dw", "sddmm_gather"),         # tiny SDDMM
+    (300, 200, 902, 0.1, "dw", "sddmm_tiled"),         # B % 4 != 0: the tiled SDDMM
+    (3072, 768, 2048, 0.05, "bwd", "bwd_fused_sk_half"),  # fused backward, half-warp entries
+    (4096, 4096, 256, 0.2, "bwd", "bwd_fused_sk"),     # long CSC rows: whole-warp entries
+    (4096, 1024, 2560, 0.5, "bwd", "bwd_fused_split|bwd_fused_tm_split"),  # rows too long for the
+                                                       # stream-K TMEM columns: slice-split grid
+    (2048, 256, 256, 0.5, "bwd", "spmm_tiled"),        # ... and too few row blocks for it: separate kernels
+]
+
+
+@pytest.mark.parametrize("R,C,B,d,op,family", LINEAR)
+def test_linear_path(sp, R, C, B, d, op, family):
+    c = synth.linear_case(R, C, B, d, 1.0 / C, R + 7 * C + B)
+    S = oracle.csr_from_mask(c["W"], c["mask"])
+    W = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))
+    X, dY = _dev(c["X"]), _dev(c["dY"])
+    if op == "fwd":
+        out = [sp.sp_linear_fwd(W, X)]
+        refs = [oracle.linear_fwd(S, c["X"], NT)]
+    elif op == "dx":
+        out = [sp.sp_linear_bwd_input(W, dY)]
+        refs = [oracle.linear_bwd_input(S, c["dY"], NT)]
+    elif op == "dw":
+        out = [sp.sp_linear_bwd_weight(W, X, dY)]
+        refs = [oracle.linear_bwd_weight(S, c["X"], c["dY"], NT)]
+    else:
+        out = list(sp.sp_linear_bwd(W, X, dY))
+        refs = [oracle.linear_bwd_input(S, c["dY"], NT), oracle.linear_bwd_weight(S, c["X"], c["dY"], NT)]
+    path = sp.last_path()
+    torch.cuda.synchronize()
+    assert set(family.split("|")) & set(path.split("+")), f"expected {family}, ran {path}"
+    for o, r in zip(out, refs):
+        _ok(f"{op} [{path}]", o, r)
+
+
+# (B, IC, OC, H, W, K, pad, op, expected family)
+CONV = [
+    (64, 32, 32, 14, 14, 3, 1, "fwd", "conv_spmm_sk"),            # exact positions, 4-D TMA halo
+    (64, 32, 32, 14, 14, 3, 1, "dx", "conv_spmm_sk"),
+    (64, 32, 32, 14, 14, 3, 1, "bwd", "conv_bwd_fused_sk"),       # Alg. 2 single pass by taps
+    (64, 32, 32, 14, 14, 3, 1, "dw", "conv_sddmm_tiled"),         # dW alone: tap-parallel SDDMM
+    (12, 16, 16, 6, 6, 3, 1, "fwd", "conv_spmm_tiled"),           # B not slicing 128: padded fallback
+    (8, 4, 6, 9, 9, 7, 3, "fwd", "conv_fwd_direct"),              # 49 taps > tap-path limit
+    (8, 4, 6, 9, 9, 7, 3, "dx", "conv_dx_direct"),
+    (8, 4, 6, 9, 9, 7, 3, "dw", "conv_dw_direct"),
+]
+
+
+@pytest.mark.parametrize("B,IC,OC,H,W,K,pad,op,family", CONV)
+def test_conv_path(sp, B, IC, OC, H, W, K, pad, op, family):
+    c = synth.conv_case(OC=OC, IC=IC, H=H, W=W, KH=K, KW=K, pad=pad, B=B, density=0.2,
+                        wvar=1.0 / (IC * K * K), seed=B + IC + OC + K)
+    Wg = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))
+    g = sp.conv_geom(Wg, B, H, W, pad)
+    X, dY = _dev(c["X"]), _dev(c["dY"])
+    F = oracle.conv_format(c["W"], c["mask"])
+    Xn, dOn = oracle.chwn_to_nchw(c["X"]), oracle.chwn_to_nchw(c["dY"])
+    if op == "fwd":
+        out = [sp.sp_conv2d_fwd(Wg, g, X)]
+        path = sp.last_path()
+        refs = [oracle.nchw_to_chwn(oracle.conv2d_fwd(F, Xn, pad, NT))]
+    else:
+        rdX, rdW = oracle.conv2d_bwd(F, Xn, dOn, pad)
+        if op == "dx":
+            out, refs = [sp.sp_conv2d_bwd_input(Wg, g, dY)], [oracle.nchw_to_chwn(rdX)]
+        elif op == "dw":
+            out, refs = [sp.sp_conv2d_bwd_weight(Wg, g, X, dY)], [rdW]
+        else:
+            out, refs = list(sp.sp_conv2d_bwd(Wg, g, X, dY)), [oracle.nchw_to_chwn(rdX), rdW]
+        path = sp.last_path()
+    torch.cuda.synchronize()
+    assert family in path.split("+"), f"expected {family}, ran {path}"
+    for o, r in zip(out, refs):
+        _ok(f"conv {op} [{path}]", o, r)
