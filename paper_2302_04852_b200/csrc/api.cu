@@ -59,6 +59,11 @@ int num_sms() {
 }
 
 cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t st) {
+    // under stream capture the allocation becomes a graph memory node (the
+    // graph owns it; the library pool is only for eager launches)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+        return cudaMallocAsync(p, bytes, st);
     const int d = cur_dev();
     cudaMemPool_t pool = nullptr;
     if (d >= 0 && d < kMaxDev) {
@@ -167,15 +172,7 @@ sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8
     w->magic = SP_MAGIC;
     const sp_status s = build_weight(R, C, dense, mask, S(stream), w);
     if (s != SP_OK) {
-        cudaFree(w->row_ptr);
-        cudaFree(w->col_idx);
-        cudaFree(w->vals);
-        cudaFree(w->col_ptr);
-        cudaFree(w->row_idx);
-        cudaFree(w->perm);
-        cudaFree(w->row_of);
-        cudaFree(w->chunk_ptr);
-        free_tilings(w);
+        free_weight(w);
         w->magic = 0;
         delete w;
         return s;
@@ -202,15 +199,7 @@ sp_status sp_weight_create_conv(int32_t C_out, int32_t C_in, int32_t KH, int32_t
 sp_status sp_weight_destroy(sp_weight_t w, sp_stream_t stream) {
     SP_CHECK_HANDLE(w, "sp_weight_destroy");
     cudaStreamSynchronize(S(stream));
-    cudaFree(w->row_ptr);
-    cudaFree(w->col_idx);
-    cudaFree(w->vals);
-    cudaFree(w->col_ptr);
-    cudaFree(w->row_idx);
-    cudaFree(w->perm);
-    cudaFree(w->row_of);
-    cudaFree(w->chunk_ptr);
-    free_tilings(w);
+    free_weight(w);
     w->magic = 0;
     delete w;
     return SP_OK;

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "sp_internal.cuh"
@@ -327,12 +328,35 @@ __global__ void til_refresh_kernel(int64_t nnz, const int32_t *__restrict__ vidx
     }
 }
 
+
+// Bump allocator over one device allocation (256-byte aligned pieces).
+struct Arena {
+    char *base = nullptr;
+    size_t off = 0, cap = 0;
+    static size_t al(size_t n) { return (n + 255) & ~(size_t)255; }
+    template <typename T>
+    T *take(int64_t n) {
+        T *p = reinterpret_cast<T *>(base + off);
+        off += al((size_t)(n > 0 ? n : 1) * sizeof(T));
+        return p;
+    }
+};
 template <typename T>
-cudaError_t dmalloc(T **p, int64_t n) {
-    return cudaMalloc((void **)p, (size_t)(n > 0 ? n : 1) * sizeof(T));
+size_t asize(int64_t n) {
+    return Arena::al((size_t)(n > 0 ? n : 1) * sizeof(T));
 }
 
 }  // namespace
+
+void free_weight(sp_weight_s *w) {
+    for (auto &a : w->arena) {
+        cudaFree(a);
+        a = nullptr;
+    }
+    w->row_ptr = w->col_ptr = w->col_idx = w->row_of = w->row_idx = w->perm = w->chunk_ptr = nullptr;
+    w->vals = nullptr;
+    free_tilings(w);
+}
 
 sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *mask,
                        cudaStream_t st, sp_weight_s *w) {
@@ -353,8 +377,13 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
     SP_TRY(scratch_alloc((void **)&ccnt, (size_t)C * sizeof(int32_t), st));
     SP_TRY(scratch_alloc((void **)&info, 4 * sizeof(int64_t), st));
     SP_TRY(scratch_alloc((void **)&blk, (size_t)(nb * C) * sizeof(int32_t), st));
-    SP_TRY(dmalloc(&w->row_ptr, R + 1));
-    SP_TRY(dmalloc(&w->col_ptr, C + 1));
+    {
+        Arena a;
+        SP_TRY(cudaMalloc((void **)&a.base, asize<int32_t>(R + 1) + asize<int32_t>(C + 1)));
+        w->arena[0] = a.base;
+        w->row_ptr = a.take<int32_t>(R + 1);
+        w->col_ptr = a.take<int32_t>(C + 1);
+    }
     {
         row_count_kernel<<<(unsigned)((R + 7) / 8), 256, 0, st>>>(R, C, mask, rcnt);
         colblk_count_kernel<<<(unsigned)((nb * C + 255) / 256), 256, 0, st>>>(R, C, nb, rbk, mask, blk);
@@ -382,11 +411,17 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
         w->max_row_nnz = (int32_t)h[1];
         w->max_col_nnz = (int32_t)h[3];
     }
-    SP_TRY(dmalloc(&w->col_idx, w->nnz));
-    SP_TRY(dmalloc(&w->vals, w->nnz));
-    SP_TRY(dmalloc(&w->row_of, w->nnz));
-    SP_TRY(dmalloc(&w->row_idx, w->nnz));
-    SP_TRY(dmalloc(&w->perm, w->nnz));
+    {
+        Arena a;
+        SP_TRY(cudaMalloc((void **)&a.base, 5 * asize<int32_t>(w->nnz) + asize<int32_t>(R + 1)));
+        w->arena[1] = a.base;
+        w->col_idx = a.take<int32_t>(w->nnz);
+        w->vals = a.take<float>(w->nnz);
+        w->row_of = a.take<int32_t>(w->nnz);
+        w->row_idx = a.take<int32_t>(w->nnz);
+        w->perm = a.take<int32_t>(w->nnz);
+        w->chunk_ptr = a.take<int32_t>(R + 1);
+    }
     csr_compact_kernel<<<(unsigned)((R + 7) / 8), 256, 0, st>>>(R, C, mask, dense, w->row_ptr,
                                                               w->col_idx, w->vals, w->row_of);
     csc_compact_kernel<<<(unsigned)((nb * C + 255) / 256), 256, 0, st>>>(R, C, nb, rbk, mask, blk, w->col_ptr,
@@ -394,7 +429,6 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
                                                                        w->perm);
     SP_TRY(cudaGetLastError());
     // gather-SDDMM work list: chunks of <= 32 consecutive nonzeros of one row
-    SP_TRY(dmalloc(&w->chunk_ptr, R + 1));
     chunk_count_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(R, w->row_ptr, rcnt);
     scan_kernel<<<1, kScanThreads, 0, st>>>(R, rcnt, w->chunk_ptr, info);
     {
@@ -468,97 +502,135 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
     struct Spec {
         int o, RB, KC, NWbal, RPWgrp;
         sp_tiling *t;
-        bool need;  // tilings of A/B variants are built only when their switch is set
     };
-    const Spec specs[] = {{0, kTilRB[0], kTilKC[0], kTilNW[0], 4, &w->til[0][0], true},
-                          {0, kTilRB[1], kTilKC[1], kTilNW[1], kTilRB[1] / kTilNW[1], &w->til[0][1], true},
-                          {1, kTilRB[0], kTilKC[0], kTilNW[0], 4, &w->til[1][0], true},
-                          {1, kTilRB[1], kTilKC[1], kTilNW[1], kTilRB[1] / kTilNW[1], &w->til[1][1], true},
-                          {1, 64, kTilKC[0], 32, 2, &w->til_f[0], true},
-                          {1, 32, kTilKC[0], 32, 1, &w->til_f[1], true},
-                          {1, 64, kTilKC[0], 16, 4, &w->til_f[2], true}};
+    const Spec specs[] = {{0, kTilRB[0], kTilKC[0], kTilNW[0], 4, &w->til[0][0]},
+                          {0, kTilRB[1], kTilKC[1], kTilNW[1], kTilRB[1] / kTilNW[1], &w->til[0][1]},
+                          {1, kTilRB[0], kTilKC[0], kTilNW[0], 4, &w->til[1][0]},
+                          {1, kTilRB[1], kTilKC[1], kTilNW[1], kTilRB[1] / kTilNW[1], &w->til[1][1]},
+                          {1, 64, kTilKC[0], 32, 2, &w->til_f[0]},
+                          {1, 32, kTilKC[0], 32, 1, &w->til_f[1]},
+                          {1, 64, kTilKC[0], 16, 4, &w->til_f[2]}};
     constexpr int NS = sizeof(specs) / sizeof(specs[0]);
+    // ---- plan: every tiling's geometry and buffer sizes, then ONE device
+    // allocation (the tiling arena) and ONE host -> device copy of the host-built
+    // row placements and the managed-SGD table
+    struct Plan {
+        int64_t rows, inner, nseg, cap, nwg;
+    } pl[NS];
+    size_t bytes = 0, hbytes = 0;  // arena total; the host-filled region
+    for (int si = 0; si < NS; ++si) {
+        const Spec &sp_ = specs[si];
+        sp_tiling &t = *sp_.t;
+        const int o = sp_.o;
+        Plan &P = pl[si];
+        P.rows = o == 0 ? w->R : w->C;
+        P.inner = o == 0 ? w->C : w->R;
+        t.RB = sp_.RB;
+        t.KC = sp_.KC;
+        t.rows = P.rows;
+        t.inner = P.inner;
+        t.nrb = (int)((P.rows + t.RB - 1) / t.RB);
+        t.nkb = (int)((P.inner + t.KC - 1) / t.KC);
+        P.nseg = (int64_t)t.nrb * t.nkb * t.RB;
+        // upper bound on the padded entry count (each segment pads < kTilPad)
+        P.cap = w->nnz + (kTilPad - 1) * std::min<int64_t>(P.nseg, w->nnz) + 8;
+        P.nwg = t.RB / sp_.RPWgrp;
+        hbytes += asize<int32_t>(P.rows) + asize<int32_t>((int64_t)t.nrb * t.RB);
+        bytes += asize<int32_t>(P.nseg + 8) + asize<int2>(P.cap) + asize<int32_t>(P.cap);
+        if (w->nnz > 0) bytes += asize<int32_t>(w->nnz);
+        if (si == 0 || si == 2) bytes += asize<int32_t>(P.nseg + 8);
+        if (o == 1) bytes += 2 * asize<int32_t>((int64_t)t.nrb * P.nwg * (t.nkb + 1));
+    }
+    hbytes += asize<SgdRef>(NS);
+    Arena ar;
+    if (cudaMalloc((void **)&ar.base, bytes + hbytes) != cudaSuccess) return SP_ERR_ALLOC;
+    w->arena[2] = ar.base;
+    // host-filled region first (rowpos / rowmap of every tiling, the SGD table)
+    std::vector<char> hreg(hbytes, 0);
+    for (int si = 0; si < NS; ++si) {
+        sp_tiling &t = *specs[si].t;
+        t.in_arena = true;
+        const size_t o1 = ar.off;
+        t.rowpos = ar.take<int32_t>(pl[si].rows);
+        const size_t o2 = ar.off;
+        t.rowmap = ar.take<int32_t>((int64_t)t.nrb * t.RB);
+        std::vector<int32_t> rowpos, rowmap;
+        balanced_rows(hptr[specs[si].o], pl[si].rows, t.RB, specs[si].NWbal, rowpos, rowmap);
+        memcpy(hreg.data() + o1, rowpos.data(), rowpos.size() * sizeof(int32_t));
+        memcpy(hreg.data() + o2, rowmap.data(), rowmap.size() * sizeof(int32_t));
+    }
+    const size_t otab = ar.off;
+    w->sgdtab = ar.take<SgdRef>(NS);
+    for (int si = 0; si < NS; ++si) {
+        sp_tiling &t = *specs[si].t;
+        const Plan &P = pl[si];
+        t.seg = ar.take<int32_t>(P.nseg + 8);
+        t.ent = ar.take<int2>(P.cap);
+        t.vidx = ar.take<int32_t>(P.cap);
+        t.cap_ent = P.cap;
+        if (w->nnz > 0) t.inv = ar.take<int32_t>(w->nnz);
+        if (si == 0 || si == 2) t.tmsplit = ar.take<int32_t>(P.nseg + 8);
+        if (specs[si].o == 1)
+            for (int g = 0; g < 2; ++g) t.gpre[g] = ar.take<int32_t>((int64_t)t.nrb * P.nwg * (t.nkb + 1));
+    }
+    {
+        std::vector<SgdRef> tab;
+        for (int si = 0; si < NS; ++si)
+            if (specs[si].t->inv) tab.push_back({specs[si].t->ent, specs[si].t->inv});
+        w->nsgd = (int)tab.size();
+        memcpy(hreg.data() + otab, tab.data(), tab.size() * sizeof(SgdRef));
+    }
+    cudaMemcpyAsync(ar.base, hreg.data(), hbytes, cudaMemcpyHostToDevice, st);
+
     int64_t *info = nullptr, *mx = nullptr;
     if (scratch_alloc((void **)&info, 2 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
     if (scratch_alloc((void **)&mx, 3 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
     for (int si = 0; si < NS; ++si) {
         const Spec &sp_ = specs[si];
-        if (!sp_.need) continue;  // stays zeroed (seg == nullptr: launchers skip it)
         const int o = sp_.o;
-        const int64_t rows = o == 0 ? w->R : w->C, inner = o == 0 ? w->C : w->R;
+        const int64_t rows = pl[si].rows;
         const int32_t *ptr = o == 0 ? w->row_ptr : w->col_ptr;
         const int32_t *idx = o == 0 ? w->col_idx : w->row_idx;
         const int32_t *slotmap = o == 0 ? nullptr : w->perm;
-        {
-            sp_tiling &t = *sp_.t;
-            t.RB = sp_.RB;
-            t.KC = sp_.KC;
-            t.rows = rows;
-            t.inner = inner;
-            t.nrb = (int)((rows + t.RB - 1) / t.RB);
-            t.nkb = (int)((inner + t.KC - 1) / t.KC);
-            const int64_t nseg = (int64_t)t.nrb * t.nkb * t.RB;
-            // upper bound on the padded entry count (each segment pads < kTilPad)
-            const int64_t cap = w->nnz + (kTilPad - 1) * std::min<int64_t>(nseg, w->nnz) + 8;
-            t.cap_ent = cap;
-            int32_t *cnt = nullptr;
-            if (dmalloc(&t.seg, nseg + 8) != cudaSuccess || dmalloc(&t.ent, cap) != cudaSuccess ||
-                dmalloc(&t.vidx, cap) != cudaSuccess ||
-                scratch_alloc((void **)&cnt, (size_t)nseg * sizeof(int32_t), st) != cudaSuccess) {
-                scratch_free(info, st);
-                scratch_free(mx, st);
-                return SP_ERR_ALLOC;
-            }
-            {
-                std::vector<int32_t> rowpos, rowmap;
-                balanced_rows(hptr[o], rows, t.RB, sp_.NWbal, rowpos, rowmap);
-                if (dmalloc(&t.rowpos, rows) != cudaSuccess || dmalloc(&t.rowmap, (int64_t)t.nrb * t.RB) != cudaSuccess)
-                    return SP_ERR_ALLOC;
-                cudaMemcpy(t.rowpos, rowpos.data(), rows * sizeof(int32_t), cudaMemcpyHostToDevice);
-                cudaMemcpy(t.rowmap, rowmap.data(), (size_t)t.nrb * t.RB * sizeof(int32_t), cudaMemcpyHostToDevice);
-            }
-            cudaMemsetAsync(cnt, 0, (size_t)nseg * sizeof(int32_t), st);
-            cudaMemsetAsync(t.seg + nseg + 1, 0, 7 * sizeof(int32_t), st);  // slack for 16-byte bulk copies of bounds
-            cudaMemsetAsync(t.ent, 0, (size_t)cap * sizeof(int2), st);
-            cudaMemsetAsync(t.vidx, 0xff, (size_t)cap * sizeof(int32_t), st);  // -1: no slot
-            const int64_t nt = rows * t.nkb;
-            til_count_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, t.nkb, t.KC, t.RB, ptr, idx,
-                                                                          t.rowpos, cnt);
-            scan_kernel<<<1, kScanThreads, 0, st>>>(nseg, cnt, t.seg, info + 2 * si);
-            til_fill_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, t.nkb, t.KC, t.RB, ptr, idx,
-                                                                         slotmap, t.rowpos, t.seg, w->vals, t.ent,
-                                                                         t.vidx);
-            til_max_kernel<<<1, 256, 0, st>>>((int64_t)t.nrb * t.nkb, t.RB, t.seg, mx + si);
-            if (w->nnz > 0) {
-                if (dmalloc(&t.inv, w->nnz) != cudaSuccess) return SP_ERR_ALLOC;
-                til_inv_kernel<<<(unsigned)((cap + 255) / 256), 256, 0, st>>>(cap, t.vidx, t.inv);
-            }
-            t.fresh = 1;  // built from vals: the handle's first version
-            if (si == 0 || si == 2) {  // the big tilings (RB = 128, KC = 192): split-source SpMM
-                if (dmalloc(&t.tmsplit, nseg + 8) != cudaSuccess) return SP_ERR_ALLOC;
-                til_split_kernel<<<(unsigned)((nseg + 255) / 256), 256, 0, st>>>(nseg, t.KC, t.seg, t.ent, t.tmsplit);
-            }
-            if (o == 1) {  // group prefix tables of the fused backward (groups of 4 and of 8)
-                const int nwg = t.RB / sp_.RPWgrp;
-                t.RPWg = sp_.RPWgrp;
-                for (int g = 0; g < 2; ++g) {
-                    if (dmalloc(&t.gpre[g], (int64_t)t.nrb * nwg * (t.nkb + 1)) != cudaSuccess) return SP_ERR_ALLOC;
-                    til_gpre_kernel<<<(unsigned)((t.nrb * nwg + 127) / 128), 128, 0, st>>>(t.nrb, t.nkb, t.RB,
-                                                                                             sp_.RPWgrp, 2 + g, t.seg,
-                                                                                             t.gpre[g]);
-                }
-            }
-            til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp, 2, t.seg, mx + NS + si);
-            til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp, 3, t.seg, mx + 2 * NS + si);
-            scratch_free(cnt, st);
+        sp_tiling &t = *sp_.t;
+        const int64_t nseg = pl[si].nseg, cap = pl[si].cap;
+        int32_t *cnt = nullptr;
+        if (scratch_alloc((void **)&cnt, (size_t)nseg * sizeof(int32_t), st) != cudaSuccess) {
+            scratch_free(info, st);
+            scratch_free(mx, st);
+            return SP_ERR_ALLOC;
         }
+        cudaMemsetAsync(cnt, 0, (size_t)nseg * sizeof(int32_t), st);
+        cudaMemsetAsync(t.seg + nseg + 1, 0, 7 * sizeof(int32_t), st);  // slack for 16-byte bulk copies of bounds
+        cudaMemsetAsync(t.ent, 0, (size_t)cap * sizeof(int2), st);
+        cudaMemsetAsync(t.vidx, 0xff, (size_t)cap * sizeof(int32_t), st);  // -1: no slot
+        const int64_t nt = rows * t.nkb;
+        til_count_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, t.nkb, t.KC, t.RB, ptr, idx, t.rowpos,
+                                                                      cnt);
+        scan_kernel<<<1, kScanThreads, 0, st>>>(nseg, cnt, t.seg, info + 2 * si);
+        til_fill_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, t.nkb, t.KC, t.RB, ptr, idx, slotmap,
+                                                                     t.rowpos, t.seg, w->vals, t.ent, t.vidx);
+        til_max_kernel<<<1, 256, 0, st>>>((int64_t)t.nrb * t.nkb, t.RB, t.seg, mx + si);
+        if (w->nnz > 0) til_inv_kernel<<<(unsigned)((cap + 255) / 256), 256, 0, st>>>(cap, t.vidx, t.inv);
+        t.fresh = 1;  // built from vals: the handle's first version
+        if (t.tmsplit)  // the big tilings (RB = 128, KC = 192): split-source SpMM
+            til_split_kernel<<<(unsigned)((nseg + 255) / 256), 256, 0, st>>>(nseg, t.KC, t.seg, t.ent, t.tmsplit);
+        if (o == 1) {  // group prefix tables of the fused backward (groups of 4 and of 8)
+            const int nwg = (int)pl[si].nwg;
+            t.RPWg = sp_.RPWgrp;
+            for (int g = 0; g < 2; ++g)
+                til_gpre_kernel<<<(unsigned)((t.nrb * nwg + 127) / 128), 128, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp,
+                                                                                         2 + g, t.seg, t.gpre[g]);
+        }
+        til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp, 2, t.seg, mx + NS + si);
+        til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp, 3, t.seg, mx + 2 * NS + si);
+        scratch_free(cnt, st);
     }
     std::vector<int64_t> h(3 * NS), hi(2 * NS);
     cudaMemcpyAsync(h.data(), mx, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(hi.data(), info, hi.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-    const cudaError_t e = cudaStreamSynchronize(st);  // second (last) host sync of sp_weight_create
+    const cudaError_t e = cudaStreamSynchronize(st);  // last host sync of sp_weight_create
     for (int si = 0; si < NS; ++si) {
-        if (!specs[si].need) continue;
         sp_tiling &t = *specs[si].t;
         t.max_tile = (int32_t)h[si];
         t.max_warp_groups = h[NS + si];
@@ -567,21 +639,16 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
     }
     scratch_free(info, st);
     scratch_free(mx, st);
-    // the managed-SGD table: every built tiling
-    std::vector<SgdRef> tab;
-    for (int si = 0; si < NS; ++si)
-        if (specs[si].need && specs[si].t->inv) tab.push_back({specs[si].t->ent, specs[si].t->inv});
     w->version = 1;
-    w->nsgd = (int)tab.size();
-    if (!tab.empty()) {
-        if (cudaMalloc((void **)&w->sgdtab, tab.size() * sizeof(SgdRef)) != cudaSuccess) return SP_ERR_ALLOC;
-        cudaMemcpy(w->sgdtab, tab.data(), tab.size() * sizeof(SgdRef), cudaMemcpyHostToDevice);
-    }
     return (e == cudaSuccess && cudaGetLastError() == cudaSuccess) ? SP_OK : SP_ERR_CUDA;
 }
 
 void free_tilings(sp_weight_s *w) {
     auto fr = [](sp_tiling &t) {
+        if (t.in_arena) {  // the buffers belong to the tiling arena (freed by free_weight)
+            t = sp_tiling{};
+            return;
+        }
         cudaFree(t.seg);
         cudaFree(t.ent);
         cudaFree(t.vidx);
@@ -610,8 +677,7 @@ void free_tilings(sp_weight_s *w) {
 
     if (w->tapdev) cudaFree(w->tapdev);
     w->tapdev = nullptr;
-    if (w->sgdtab) cudaFree(w->sgdtab);
-    w->sgdtab = nullptr;
+    w->sgdtab = nullptr;  // lives in the tiling arena
     w->nsgd = 0;
 }
 

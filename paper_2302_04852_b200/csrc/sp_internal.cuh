@@ -76,6 +76,7 @@ struct sp_tiling {
     // dW column of a tile's first group without walking the earlier tiles
     int32_t *gpre[2];
     int RPWg;
+    bool in_arena;  // buffers carved from the handle's tiling arena (freed with it)
 };
 
 // One tiling's entries as seen by the managed SGD kernel.
@@ -86,6 +87,10 @@ struct SgdRef {
 
 struct sp_weight_s {
     uint32_t magic;
+    // device arenas (one cudaMalloc each, sp_weight_create's allocation cost):
+    // [0] row_ptr + col_ptr, [1] the nnz-sized index arrays + chunk_ptr,
+    // [2] every linear tiling + the managed-SGD table
+    void *arena[3];
     int64_t R, C, nnz;
     // CSR (P153-P154): row_ptr[R+1], col_idx[nnz], vals[nnz]
     int32_t *row_ptr;
@@ -193,6 +198,8 @@ void launch_to_dense(const sp_weight_s *w, const float *nz, float *dense, cudaSt
 void launch_gather_dense(const sp_weight_s *w, const float *dense, float *nz, cudaStream_t st);
 sp_status build_tilings(sp_weight_s *w, cudaStream_t st);
 void free_tilings(sp_weight_s *w);
+// every device buffer of a handle (arenas, conv tap tilings)
+void free_weight(sp_weight_s *w);
 // ent[e].y = bits(vals[vidx[e]]) for one tiling (before an SpMM launch)
 void launch_refresh(const sp_tiling &t, const float *vals, int64_t nnz, cudaStream_t st);
 // the same unless the handle is managed and the tiling already holds its version

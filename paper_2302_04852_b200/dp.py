@@ -231,6 +231,27 @@ class SparseMLP:
         self.sgd(lr)
         return loss
 
+    # ---- whole-step CUDA graph: the step's ~100 launches
+    # (and, at N > 1, its NCCL all_reduces on the comm stream) replayed as one
+    # graph.  Capture-safe: scratch is stream-ordered (graph memory nodes under
+    # capture), the tensor maps are kernel parameters, and managed handles launch
+    # no per-product refresh.  Buffers are fixed at capture: one graph per
+    # input-buffer parity when the e2e loop double-buffers its inputs.
+    def capture(self, lr: float, allreduce: bool = True):
+        """Capture one step (forward, loss, backward + all_reduce, SGD) with the
+        current X[0] / target buffers; returns the graph (replay() runs a step)."""
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            self.step(lr, allreduce=allreduce)  # warm: lazy state outside the capture
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        torch.cuda.synchronize(self.device)
+        with torch.cuda.graph(g, stream=s):
+            self.step(lr, allreduce=allreduce)
+        torch.cuda.synchronize(self.device)
+        return g
+
     def step_flops(self) -> int:
         """Effective FLOPs of one step on this rank: 2*nnz*B per product
         (BASELINE metric): 3 products per layer (fwd, dX, dW),

@@ -84,8 +84,11 @@ def prune_modules(modules, sparsity: float, scope: str = "uniform", optimizer=No
     their current kept weights and rebuild their sparse structure.  Each
     module keeps its `vals` Parameter object (re-pointed at the new handle),
     so `optimizer` keeps stepping it; its per-parameter state, whose size
-    was the old nnz, is dropped.  Returns the achieved sparsities and the
-    time spent rebuilding (the sp_weight_create cost this mask update pays)."""
+    was the old nnz, is dropped.  Autograd graphs recorded before the update
+    must have been released (a live loss tensor from the last step still holds
+    the old-size gradient accumulator of `vals`).  Returns the achieved
+    sparsities and the time spent rebuilding (the sp_weight_create cost this
+    mask update pays)."""
     dense, cur = [], []
     for m in modules:
         shape = m.W.filter_shape or (m.W.R, m.W.C)

@@ -190,3 +190,27 @@ def test_mlp_two_steps_then_forward_matches_oracle():
         X, H = _np(m.X[l]), _np(m.H[l])
         _ok(f"H[{l}] after 2 steps", H, np.maximum(oracle.linear_fwd(S1, X, NT), 0.0))
         _ok(f"X[{l + 1}] after 2 steps", _np(m.X[l + 1]), oracle.linear_fwd(S2, H, NT))
+
+
+def test_graph_captured_step_matches_eager():
+    """The whole step captured once in a CUDA graph (bench.py's timed loop) and
+    replayed gives bitwise the eager steps' weights and loss: the same kernels
+    with the same arguments, scratch from graph memory nodes."""
+    from paper_2302_04852_b200.dp import SparseMLP
+    T = 2048
+    c = synth.mlp_case(blocks=3, d_model=768, d_ff=3072, T=T, density=0.05, seed=21)
+    X0, Tg = torch.from_numpy(c["X0"]), torch.from_numpy(c["target"])
+    a = SparseMLP(c["layers"], T, "cuda")
+    b = SparseMLP(c["layers"], T, "cuda")
+    for m in (a, b):
+        m.set_batch(X0, Tg, non_blocking=False)
+    for _ in range(3):
+        la = a.step(1e-6)
+    g = b.capture(1e-6)      # runs one eager (warm) step, then captures one
+    g.replay()               # step 2
+    g.replay()               # step 3
+    torch.cuda.synchronize()
+    assert torch.isfinite(la).all() and torch.equal(la, b.loss)
+    for (A1, A2), (B1, B2) in zip(a.W, b.W):
+        assert torch.equal(A1.vals, B1.vals) and torch.equal(A2.vals, B2.vals)
+    assert torch.equal(a.dW_flat, b.dW_flat)

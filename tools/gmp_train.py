@@ -92,6 +92,7 @@ def main():
     for ep in range(a.epochs):
         target = gmp_target_at(ep, a.final)
         if target > cur + 1e-12:
+            loss = None  # release the last step's autograd graph before vals change size
             rep = prune_modules(mods, target, scope=a.scope, optimizer=opt)
             cur = target
             x0 = torch.randn(a.batch, dm, generator=g, device=dev)
