@@ -185,6 +185,8 @@ def main():
     ap.add_argument("--graph", type=int, default=None,
                     help="replay the whole step as one CUDA graph (default: 1 at N=1, 0 at N>1, where the "
                          "NCCL all_reduce would have to be captured too)")
+    ap.add_argument("--sm-reserve", type=int, default=8,
+                    help="N>1: NCCL channels = SMs the backward's one-wave kernels leave to the all_reduce")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the per-config single-layer sweep (BASELINE configs 0-3) added at N=1")
     ap.add_argument("--tokens", type=int, default=CFG["T"], help="global batch (default 16384)")
@@ -204,6 +206,9 @@ def main():
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
+        # the dW all_reduce overlaps the backward: cap NCCL's CTAs (channels) and
+        # leave that many SMs free in the one-wave kernels (SparseMLP sm_reserve)
+        os.environ.setdefault("NCCL_MAX_NCHANNELS", str(args.sm_reserve))
         dist.init_process_group("nccl", device_id=dev)
 
     from paper_2302_04852_b200 import sparseprop as sp
@@ -213,7 +218,7 @@ def main():
     lo, hi = synth.token_shard(T, world, rank)
     c = synth.mlp_case(blocks=CFG["blocks"], d_model=CFG["d_model"], d_ff=CFG["d_ff"], T=T,
                        density=CFG["density"], seed=CFG["seed"])
-    model = SparseMLP(c["layers"], hi - lo, dev)
+    model = SparseMLP(c["layers"], hi - lo, dev, sm_reserve=args.sm_reserve)
     # every rank must hold identical masks: allgather of a 64-bit hash of every
     # layer's (row_ptr, col_idx)
     if world > 1:

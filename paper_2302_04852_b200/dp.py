@@ -64,13 +64,22 @@ class CudaOps:
         """SGD of a managed handle: vals and its tiled copies in one kernel."""
         self.sp.sp_weight_sgd(W, dW, lr)
 
+    def sm_reserve(self, n):
+        """One-wave kernels leave n SMs to the concurrent all_reduce."""
+        self.sp.sp_set_sm_reserve(n)
+
 
 class SparseMLP:
     """cfg5 model state + one training step on this rank's token shard."""
 
     def __init__(self, layers, T_local: int, device, ops=None, group=None, bucket_blocks: int = 3,
-                 keep_dx0: bool = True, fused: bool = True):
-        """layers: list of (w1, m1, w2, m2) host arrays (synth.mlp_case)."""
+                 keep_dx0: bool = True, fused: bool = True, sm_reserve: int = 8):
+        """layers: list of (w1, m1, w2, m2) host arrays (synth.mlp_case).
+        sm_reserve: at N > 1, SMs the backward's one-wave (stream-K) kernels
+        leave free while the bucketed all_reduce runs on the comm stream, so
+        the collective's CTAs do not push part of a wave into a second one
+        (match it to NCCL's channel count, NCCL_MAX_NCHANNELS)."""
+        self.sm_reserve = sm_reserve
         self.ops = ops if ops is not None else CudaOps()
         self.device = torch.device(device)
         self.group = group
@@ -171,6 +180,8 @@ class SparseMLP:
         bi = 0
         dY, dYn = self.dY, self.dYb
         fused = self.fused and hasattr(ops, "bwd")
+        if comm and self.sm_reserve and hasattr(ops, "sm_reserve"):
+            ops.sm_reserve(self.sm_reserve)
         for l in range(self.blocks - 1, -1, -1):
             W1, W2 = self.W[l]
             dW1, dW2 = self.dW[l]
@@ -195,6 +206,8 @@ class SparseMLP:
                 bi += 1
         if comm:
             self._wait(pending)
+            if self.sm_reserve and hasattr(ops, "sm_reserve"):
+                ops.sm_reserve(0)
 
     def _launch_allreduce(self, buf):
         if self.comm_stream is not None:
