@@ -211,6 +211,26 @@ sp_status sp_conv2d_bwd_weight(sp_weight_t W, const sp_conv_geom *g, const float
 sp_status sp_conv2d_bwd(sp_weight_t W, const sp_conv_geom *g, const float *X, const float *dY,
                         float *dX, float *dW, sp_stream_t stream);
 
+/* NCHW entry points: the paper's second conv kernel, SparseConvOverON
+ * (P293, P397-P400: the natural B x C x H x W layout, vectorised over the
+ * output width, for large spatial inputs).  Same products and readings as the
+ * CHWN calls above, with X / dX [B][C_in][H][W] and Y / dY [B][C_out][OH][OW]:
+ * the tap tiles are np x nq spatial tiles of one image (lanes along the output
+ * rows), read through NCHW tensor maps whose out-of-bounds zero fill is the
+ * halo.  A TMA box's innermost start (here: the width) must be 16-byte
+ * aligned, so this direct path takes filters whose every column shift
+ * (y - pad) is a multiple of 4 -- 1 x 1 convolutions with pad 0 -- with W and
+ * OW multiples of 4 and a handle from sp_weight_create_conv; other shapes run
+ * the CHWN kernels (whose slices span output columns x batch jointly) on
+ * permuted copies (stream-ordered scratch).  dW in the handle's CSR order. */
+sp_status sp_conv2d_fwd_nchw(sp_weight_t W, const sp_conv_geom *g, const float *X, float *Y, sp_stream_t stream);
+sp_status sp_conv2d_bwd_input_nchw(sp_weight_t W, const sp_conv_geom *g, const float *dY, float *dX,
+                                   sp_stream_t stream);
+sp_status sp_conv2d_bwd_weight_nchw(sp_weight_t W, const sp_conv_geom *g, const float *X, const float *dY,
+                                    float *dW, sp_stream_t stream);
+sp_status sp_conv2d_bwd_nchw(sp_weight_t W, const sp_conv_geom *g, const float *X, const float *dY, float *dX,
+                             float *dW, sp_stream_t stream);
+
 /* ---------------------------------------------------------------------- */
 /* Step helpers for the data-parallel sparse MLP (north star cfg5)        */
 /* ---------------------------------------------------------------------- */

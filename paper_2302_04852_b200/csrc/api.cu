@@ -366,6 +366,38 @@ sp_status sp_conv2d_bwd(sp_weight_t w, const sp_conv_geom *g, const float *X, co
     return check_launch("sp_conv2d_bwd");
 }
 
+static sp_status conv_nchw_impl(sp_weight_t w, const sp_conv_geom *g, int op, const float *X, const float *dY,
+                                float *out, float *dW, sp_stream_t stream, const char *fn) {
+    SP_CHECK_HANDLE(w, fn);
+    begin_path();
+    sp_status s = check_geom(w, g, fn);
+    if (s != SP_OK) return s;
+    if ((op != 1 && !X) || (op != 0 && !dY) || (op != 3 && !out) || (op >= 2 && !dW && w->nnz > 0))
+        return fail(SP_ERR_NULL, std::string(fn) + ": NULL tensor");
+    s = launch_conv_nchw(w, *g, op, X, dY, out, dW, S(stream));
+    if (s != SP_OK) return s;
+    return check_launch(fn);
+}
+
+sp_status sp_conv2d_fwd_nchw(sp_weight_t w, const sp_conv_geom *g, const float *X, float *Y, sp_stream_t stream) {
+    return conv_nchw_impl(w, g, 0, X, nullptr, Y, nullptr, stream, "sp_conv2d_fwd_nchw");
+}
+
+sp_status sp_conv2d_bwd_input_nchw(sp_weight_t w, const sp_conv_geom *g, const float *dY, float *dX,
+                                   sp_stream_t stream) {
+    return conv_nchw_impl(w, g, 1, nullptr, dY, dX, nullptr, stream, "sp_conv2d_bwd_input_nchw");
+}
+
+sp_status sp_conv2d_bwd_nchw(sp_weight_t w, const sp_conv_geom *g, const float *X, const float *dY, float *dX,
+                             float *dW, sp_stream_t stream) {
+    return conv_nchw_impl(w, g, 2, X, dY, dX, dW, stream, "sp_conv2d_bwd_nchw");
+}
+
+sp_status sp_conv2d_bwd_weight_nchw(sp_weight_t w, const sp_conv_geom *g, const float *X, const float *dY, float *dW,
+                                    sp_stream_t stream) {
+    return conv_nchw_impl(w, g, 3, X, dY, nullptr, dW, stream, "sp_conv2d_bwd_weight_nchw");
+}
+
 int64_t sp_mse_scratch_floats(int64_t n) { return mse_scratch_floats(n); }
 
 sp_status sp_mse_grad(const float *Y, const float *T, float *dY, float *loss_out, float *scratch, int64_t n,

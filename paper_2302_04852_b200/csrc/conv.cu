@@ -307,7 +307,7 @@ void conv_taps_offsets(const Geo &g, bool transposed, ConvCols &cc) {
 
 }  // namespace
 
-bool conv_cols(int64_t B, int Po, int Qo, ConvCols *cc) {
+bool conv_cols(int64_t B, int Po, int Qo, int64_t R, ConvCols *cc) {
     if ((B & 3) != 0 || B < 4) return false;
     ConvCols c{};
     if (B <= 128) {
@@ -326,6 +326,39 @@ bool conv_cols(int64_t B, int Po, int Qo, ConvCols *cc) {
     c.Po = Po;
     c.Qo = Qo;
     c.B = B;
+    c.rowlen = (int64_t)Po * Qo * B;
+    c.imgstride = 0;
+    c.nslice = (int64_t)Po * c.spr;
+    (void)R;
+    *cc = c;
+    return true;
+}
+
+bool conv_cols_nchw(int64_t B, int Po, int Qo, int64_t R, ConvCols *cc) {
+    if ((Qo & 3) != 0 || B < 1) return false;
+    // np x nq = 128 with nq a power of two >= 4: the tile shape wasting the
+    // fewest lanes on the partial last row / column tiles of the image
+    ConvCols c{};
+    int64_t best = -1;
+    for (int nq = 4; nq <= 128; nq *= 2) {
+        const int np = 128 / nq;
+        const int64_t cols = (int64_t)((Qo + nq - 1) / nq) * nq * ((Po + np - 1) / np) * np;
+        if (best < 0 || cols < best) {
+            best = cols;
+            c.nq = nq;
+            c.np = np;
+        }
+    }
+    c.nchw = 1;
+    c.qsh = __builtin_ctz((unsigned)c.nq);
+    c.nqt = (Qo + c.nq - 1) / c.nq;
+    c.npt = (Po + c.np - 1) / c.np;
+    c.Po = Po;
+    c.Qo = Qo;
+    c.B = B;
+    c.rowlen = (int64_t)Po * Qo;
+    c.imgstride = R * Po * Qo;
+    c.nslice = B * c.nqt * c.npt;
     *cc = c;
     return true;
 }
@@ -334,7 +367,7 @@ void launch_conv_fwd(const sp_weight_s *w, const sp_conv_geom &cg, const float *
                      cudaStream_t st) {
     const Geo g = mk(cg);
     ConvCols cc;
-    if (tap_path(w, g) && conv_cols(g.B, g.OH, g.OW, &cc)) {
+    if (tap_path(w, g) && conv_cols(g.B, g.OH, g.OW, g.OC, &cc)) {
         // Y[oc][p][q] = sum_taps W_xy . X[p + x - pad][q + y - pad]  (Eq. 3 by taps;
         // exact output positions, the halo zero-filled by the tensor map)
         conv_taps_offsets(g, false, cc);
@@ -375,7 +408,7 @@ void launch_conv_bwd_input(const sp_weight_s *w, const sp_conv_geom &cg, const f
                            cudaStream_t st) {
     const Geo g = mk(cg);
     ConvCols cc;
-    if (tap_path(w, g) && conv_cols(g.B, g.H, g.W, &cc)) {
+    if (tap_path(w, g) && conv_cols(g.B, g.H, g.W, g.IC, &cc)) {
         // transposed conv by taps (Eq. 4): dX[ic][m][n] = sum_taps W_xy^T . dY[m + pad - x][n + pad - y]
         conv_taps_offsets(g, true, cc);
         launch_refresh_taps(w, 1, g.KH * g.KW, st);
@@ -418,7 +451,7 @@ void launch_conv_bwd_input(const sp_weight_s *w, const sp_conv_geom &cg, const f
 static bool conv_bwd_sk(const sp_weight_s *w, const Geo &g, const float *X, const float *dY, float *dX, float *dW,
                         cudaStream_t st) {
     ConvCols cc;
-    if (!tap_path(w, g) || !conv_cols(g.B, g.H, g.W, &cc)) return false;
+    if (!tap_path(w, g) || !conv_cols(g.B, g.H, g.W, g.IC, &cc)) return false;
     conv_taps_offsets(g, true, cc);
     return launch_conv_bwd_sk(w, cc, dY, g.OH, g.OW, X, dX, dW, g.KH * g.KW, st);
 }
@@ -467,6 +500,96 @@ sp_status launch_conv_bwd_weight(const sp_weight_s *w, const sp_conv_geom &cg, c
     else if (g.B <= 64 || (g.B & 3)) go(conv_dw_kernel<2>);
     else go(conv_dw_kernel<4>);
     return SP_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// NCHW products: the paper's SparseConvOverON (natural B x C x H x W layout,
+// vectorised over the output width, P293, P397-P400).  Same tap tilings and
+// stream-K kernels as the CHWN path, with NCHW tensor maps: a slice is an
+// np x nq spatial tile of one image and lanes run along the output rows.
+// A TMA box may start anywhere in its outer dimensions, but its innermost
+// start must be 16-byte aligned: here that is the width, so a tap's column
+// shift dq must be a multiple of 4 -- in practice 1 x 1 filters with pad 0
+// (the ResNet bottleneck convolutions).  Other shapes (wider filters, W or OW
+// not a multiple of 4, direct-kernel filters) run the CHWN kernels -- whose
+// slices already span (q, b) jointly, i.e. are vectorised over the output
+// width when B is small -- on permuted copies.
+namespace {
+
+// dst = src permuted between [B][C][HW] (NCHW) and [C][HW][B] (CHWN)
+__global__ void permute_kernel(int64_t B, int64_t C, int64_t HW, int to_chwn, const float *__restrict__ src,
+                               float *__restrict__ dst) {
+    const int64_t total = B * C * HW;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        if (to_chwn) {  // i = (c*HW + s)*B + b  <-  (b*C + c)*HW + s
+            const int64_t b = i % B, t = i / B, sp = t % HW, c = t / HW;
+            dst[i] = __ldg(src + (b * C + c) * HW + sp);
+        } else {  // i = (b*C + c)*HW + s  <-  (c*HW + s)*B + b
+            const int64_t sp = i % HW, t = i / HW, c = t % C, b = t / C;
+            dst[i] = __ldg(src + (c * HW + sp) * B + b);
+        }
+    }
+}
+
+void launch_permute(int64_t B, int64_t C, int64_t HW, bool to_chwn, const float *src, float *dst, cudaStream_t st) {
+    count_launches(1);
+    note_path(to_chwn ? "permute_nchw_chwn" : "permute_chwn_nchw");
+    permute_kernel<<<(unsigned)(num_sms() * 8), 256, 0, st>>>(B, C, HW, to_chwn ? 1 : 0, src, dst);
+}
+
+}  // namespace
+
+sp_status launch_conv_nchw(const sp_weight_s *w, const sp_conv_geom &cg, int op, const float *X, const float *dY,
+                           float *out, float *dW, cudaStream_t st) {
+    const Geo g = mk(cg);
+    const int ntap = g.KH * g.KW;
+    ConvCols cc;
+    bool aligned = true;  // every tap's width shift a multiple of 4 floats (16 bytes)
+    for (int y = 0; y < g.KW; ++y) aligned = aligned && ((y - g.pad) & 3) == 0 && ((g.pad - y) & 3) == 0;
+    // the tap path without its batch-vector condition (NCHW slices do not split the batch)
+    const bool taps = w->tapdev != nullptr && w->conv_kh == g.KH && w->conv_kw == g.KW && ntap <= kMaxTaps &&
+                      g.pad <= g.KH - 1 && g.pad <= g.KW - 1;
+    if (taps && aligned && (g.W & 3) == 0 && (g.OW & 3) == 0 && w->nnz > 0) {
+        if (op == 0 && conv_cols_nchw(g.B, g.OH, g.OW, g.OC, &cc)) {  // Y = conv(X)
+            conv_taps_offsets(g, false, cc);
+            launch_refresh_taps(w, 0, ntap, st);
+            if (launch_conv_spmm_sk(w, 0, cc, X, g.H, g.W, out, ntap, st)) return SP_OK;
+        } else if (op == 1 && conv_cols_nchw(g.B, g.H, g.W, g.IC, &cc)) {  // dX (Eq. 4)
+            conv_taps_offsets(g, true, cc);
+            launch_refresh_taps(w, 1, ntap, st);
+            if (launch_conv_spmm_sk(w, 1, cc, dY, g.OH, g.OW, out, ntap, st)) return SP_OK;
+        } else if ((op == 2 || op == 3) && conv_cols_nchw(g.B, g.H, g.W, g.IC, &cc)) {  // dX + dW / dW alone
+            conv_taps_offsets(g, true, cc);
+            if (launch_conv_bwd_sk(w, cc, dY, g.OH, g.OW, X, op == 2 ? out : nullptr, dW, ntap, st)) return SP_OK;
+        }
+    }
+    // permuted fallback through the CHWN entry points
+    const int64_t nx = (int64_t)g.B * g.IC * g.H * g.W, ny = (int64_t)g.B * g.OC * g.OH * g.OW;
+    float *xc = nullptr, *yc = nullptr, *oc = nullptr;
+    const bool need_x = op != 1, need_y = op != 0;
+    const int64_t no = op == 0 ? ny : op == 3 ? 0 : nx;
+    if ((need_x && scratch_alloc((void **)&xc, (size_t)nx * sizeof(float), st) != cudaSuccess) ||
+        (need_y && scratch_alloc((void **)&yc, (size_t)ny * sizeof(float), st) != cudaSuccess) ||
+        (no > 0 && scratch_alloc((void **)&oc, (size_t)no * sizeof(float), st) != cudaSuccess)) {
+        if (xc) scratch_free(xc, st);
+        if (yc) scratch_free(yc, st);
+        set_error("sp_conv2d_*_nchw: scratch allocation failed");
+        return SP_ERR_ALLOC;
+    }
+    if (need_x) launch_permute(g.B, g.IC, (int64_t)g.H * g.W, true, X, xc, st);
+    if (need_y) launch_permute(g.B, g.OC, (int64_t)g.OH * g.OW, true, dY, yc, st);
+    sp_status s = SP_OK;
+    if (op == 0) launch_conv_fwd(w, cg, xc, oc, st);
+    else if (op == 1) launch_conv_bwd_input(w, cg, yc, oc, st);
+    else if (op == 2) s = launch_conv_bwd(w, cg, xc, yc, oc, dW, st);
+    else s = launch_conv_bwd_weight(w, cg, xc, yc, dW, st);
+    if (op == 0) launch_permute(g.B, g.OC, (int64_t)g.OH * g.OW, false, oc, out, st);
+    else if (op != 3) launch_permute(g.B, g.IC, (int64_t)g.H * g.W, false, oc, out, st);
+    if (xc) scratch_free(xc, st);
+    if (yc) scratch_free(yc, st);
+    if (oc) scratch_free(oc, st);
+    return s;
 }
 
 }  // namespace sp

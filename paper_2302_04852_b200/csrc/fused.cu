@@ -693,11 +693,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
         const int2 *ent = CONV ? a.taps[tap_of(id.r)].ent : a.ent;
         mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
         if constexpr (CONV) {
-            int p, q0, b0;
-            cc_origin(a.cc, id.sl, p, q0, b0);
-            const int t = tap_of(id.r);
-            tma_load_4d(smem + buf * buf_sz + BT, &tmap, b0, q0 + a.cc.dq[t], p + a.cc.dp[t], kb_of(id.r) * a.KC,
-                        &full[buf]);
+            int c[4];
+            cc_coords(a.cc, id.sl, tap_of(id.r), kb_of(id.r) * a.KC, c);
+            tma_load_4d(smem + buf * buf_sz + BT, &tmap, c[0], c[1], c[2], c[3], &full[buf]);
         } else {
             tma_load_2d(smem + buf * buf_sz + BT, &tmap, id.sl * BT, kb_of(id.r) * a.KC, &full[buf]);
         }
@@ -1240,8 +1238,8 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const ConvCols &cc, const float *d
     const bool half = !dwonly && w->tapf_groups8 <= (int64_t)sk_dwcols<TRPW, false, TNW, true>() * 4;
     const int64_t groups_cap = (int64_t)(dwonly ? sk_dwcols<TRPW, true>() : sk_dwcols<TRPW, false>()) * 8;
     if (!half && w->tapf_groups > groups_cap) return false;
-    const int64_t slices = (int64_t)cc.Po * cc.spr;
-    const int64_t xrow = (int64_t)cc.Po * cc.Qo * cc.B;  // floats per channel of X / dX
+    const int64_t slices = cc.nslice;
+    const int64_t xrow = cc.rowlen;  // floats between channels of X / dX
     const int64_t T = (int64_t)t0.nrb * slices * ntap * t0.nkb;
     if (T >= (1LL << 31)) return false;
     const int64_t G = std::min<int64_t>(num_sms(), T);
@@ -1257,7 +1255,7 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const ConvCols &cc, const float *d
     const int nbuf = 3 * stage <= (size_t)(226 * 1024) ? 3 : 2;
     if (nbuf * stage > (size_t)(226 * 1024)) return false;
     CUtensorMap tmap{};
-    if (!make_tmap_conv(&tmap, dY, t0.inner, OH, OW, cc.B, 1 << cc.bsh, cc.nq, t0.KC)) return false;
+    if (!make_tmap_conv(&tmap, dY, cc, t0.inner, OH, OW, t0.KC)) return false;
     int64_t maxjobs = 1;
     const int64_t per_rb = slices * ntap * t0.nkb;
     for (int64_t rb = 0; rb < t0.nrb; ++rb)

@@ -16,17 +16,26 @@
 
 constexpr int kMaxTaps = 25;  // conv filters up to 5x5 use the tap-tiled kernels
 
-// Exact output columns of the conv kernels (4-D TMA path): a
-// batch slice of 128 columns is nq output columns q x bs batch elements of one
-// output row p (B <= 128: bs = B, nq = 128 / B; B > 128: bs = 128, nq = 1 and
-// bpr = B / 128 slices per q).  Slice sl -> p = sl / spr.  Tap t reads the input
-// at (p + dp[t], q + dq[t]) through a CHWN tensor map whose out-of-bounds
-// zero fill is the halo: no padded copy, no virtual columns.
+// Exact output columns of the conv kernels (4-D TMA path).  A
+// slice of 128 columns is
+//  - CHWN (the paper's batch-last SparseConv layout, P293): nq output columns
+//    q x bs batch elements of one output row p (B <= 128: bs = B, nq = 128 / B;
+//    B > 128: bs = 128, nq = 1, bpr = B / 128 slices per q); slice sl -> p = sl / spr;
+//  - NCHW (the paper's SparseConvOverON, natural layout vectorised over the
+//    output width, P293 / P397): an np x nq spatial tile of one image, nq
+//    consecutive output columns per row (lanes over q).
+// Tap t reads the input at (p + dp[t], q + dq[t]) through a 4-D tensor map
+// whose out-of-bounds zero fill is the halo: no padded copy, no virtual columns.
 struct ConvCols {
-    int32_t bsh;  // log2 bs
-    int32_t nq, spr, bpr;
-    int32_t Po, Qo;  // output rows / columns of the product
+    int32_t nchw;           // 0: CHWN, 1: NCHW
+    int32_t bsh;            // CHWN: log2 bs
+    int32_t nq, spr, bpr;   // CHWN: q per slice, slices per output row, batch slices per q
+    int32_t np, qsh, nqt, npt;  // NCHW: rows per slice, log2 nq, q tiles / p tiles per image
+    int32_t Po, Qo;         // output rows / columns of the product
     int64_t B;
+    int64_t rowlen;         // floats between consecutive channels (rows) of an output / X tensor
+    int64_t imgstride;      // NCHW: floats per image of the output / X tensor
+    int64_t nslice;
     int8_t dp[25], dq[25];  // per-tap input offsets (kMaxTaps)
 };
 
@@ -184,12 +193,16 @@ inline cudaStream_t S(sp_stream_t s) { return reinterpret_cast<cudaStream_t>(s);
 // box of `box_rows` rows x `box_cols` batch columns, no swizzle, zero OOB
 // fill.  Returns false if the driver entry point is unavailable.
 bool make_tmap_2d(CUtensorMap *map, const float *base, int64_t rows, int64_t B, int box_cols, int box_rows);
-// 4-D CHWN map with a (bs, nq, 1, kc) box (conv tap tiles; ConvCols)
-bool make_tmap_conv(CUtensorMap *map, const float *base, int64_t C, int64_t H, int64_t W, int64_t B, int bs, int nq,
+// 4-D map of the input of a conv product ([C][Hi][Wi][B] for CHWN, [B][C][Hi][Wi]
+// for NCHW) with the box of one tap tile of cc (kc channels x 128 positions)
+bool make_tmap_conv(CUtensorMap *map, const float *base, const ConvCols &cc, int64_t C, int64_t Hi, int64_t Wi,
                     int kc);
-// ConvCols for output (Po x Qo) and batch B; false if B fits no exact slicing
-// (B % 4 != 0, or neither 128 % B == 0 nor B % 128 == 0)
-bool conv_cols(int64_t B, int Po, int Qo, ConvCols *cc);
+// ConvCols of a CHWN product with output Po x Qo, batch B and R output
+// channels; false if B fits no exact slicing (B % 4 != 0, or neither
+// 128 % B == 0 nor B % 128 == 0)
+bool conv_cols(int64_t B, int Po, int Qo, int64_t R, ConvCols *cc);
+// ConvCols of an NCHW product (SparseConvOverON); false unless Qo % 4 == 0
+bool conv_cols_nchw(int64_t B, int Po, int Qo, int64_t R, ConvCols *cc);
 
 // ---- build.cu ----
 sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *mask,
@@ -218,6 +231,9 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
 // ---- spmm_sk.cu: stream-K SpMM (B % 4 == 0, big tiling); false if it does not apply
 bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,
                     int epi, cudaStream_t st);
+// the same on the small tiling (32-row blocks, 8 warps, two CTAs per SM)
+bool launch_spmm_sk_small(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out,
+                          const float *gate, int epi, cudaStream_t st);
 bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, const ConvCols &cc, const float *in, int64_t Hi,
                          int64_t Wi, float *out, int ntap, cudaStream_t st);
 
@@ -275,6 +291,10 @@ void launch_conv_bwd_input(const sp_weight_s *w, const sp_conv_geom &g, const fl
                            float *dX, cudaStream_t st);
 sp_status launch_conv_bwd_weight(const sp_weight_s *w, const sp_conv_geom &g, const float *X,
                                  const float *dY, float *dW, cudaStream_t st);
+// NCHW products (SparseConvOverON): op 0 fwd (X -> out = Y), 1 dX (dY -> out = dX),
+// 2 fused backward (X, dY -> out = dX, dW), 3 dW alone
+sp_status launch_conv_nchw(const sp_weight_s *w, const sp_conv_geom &g, int op, const float *X, const float *dY,
+                           float *out, float *dW, cudaStream_t st);
 
 // ---- step.cu ----
 int64_t mse_scratch_floats(int64_t n);

@@ -252,11 +252,20 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, i
         : "memory");
 }
 
-// ConvCols (sp_internal.cuh): slice sl -> origin (output row p, first output
-// column q0, first batch element b0) of its exact output positions
-__device__ __forceinline__ void cc_origin(const ConvCols &g, int sl, int &p, int &q0, int &b0) {
-    p = sl / g.spr;
-    const int r = sl - p * g.spr;
+// ConvCols (sp_internal.cuh): the tensor-map coordinates of tap t's tile of
+// slice sl (channel block starting at kc): CHWN (b0, q0 + dq, p + dp, kc),
+// NCHW (q0 + dq, p0 + dp, kc, b)
+__device__ __forceinline__ void cc_coords(const ConvCols &g, int sl, int t, int kc, int (&c)[4]) {
+    if (g.nchw) {
+        const int per = g.nqt * g.npt, b = sl / per, r = sl - b * per, pt = r / g.nqt;
+        c[0] = (r - pt * g.nqt) * g.nq + g.dq[t];
+        c[1] = pt * g.np + g.dp[t];
+        c[2] = kc;
+        c[3] = b;
+        return;
+    }
+    const int p = sl / g.spr, r = sl - p * g.spr;
+    int q0, b0;
     if (g.bpr == 1) {
         q0 = r * g.nq;
         b0 = 0;
@@ -264,12 +273,30 @@ __device__ __forceinline__ void cc_origin(const ConvCols &g, int sl, int &p, int
         q0 = r / g.bpr;
         b0 = (r - q0 * g.bpr) * 128;
     }
+    c[0] = b0;
+    c[1] = q0 + g.dq[t];
+    c[2] = p + g.dp[t];
+    c[3] = kc;
 }
-// column c (0..127) of slice sl -> float offset (p*Qo + q)*B + b of its output
-// position within a channel, or -1 when q lies past the row (a partial last slice)
+// column c (0..127) of slice sl -> float offset of its output position from the
+// start of its channel row (add r * rowlen), or -1 outside the output (a partial
+// slice at the edge of a row / image)
 __device__ __forceinline__ int64_t cc_off(const ConvCols &g, int sl, int c) {
-    int p, q0, b0;
-    cc_origin(g, sl, p, q0, b0);
+    if (g.nchw) {
+        const int per = g.nqt * g.npt, b = sl / per, r = sl - b * per, pt = r / g.nqt;
+        const int p = pt * g.np + (c >> g.qsh), q = (r - pt * g.nqt) * g.nq + (c & (g.nq - 1));
+        if (p >= g.Po || q >= g.Qo) return -1;
+        return (int64_t)b * g.imgstride + (int64_t)p * g.Qo + q;
+    }
+    const int p = sl / g.spr, r = sl - p * g.spr;
+    int q0, b0;
+    if (g.bpr == 1) {
+        q0 = r * g.nq;
+        b0 = 0;
+    } else {
+        q0 = r / g.bpr;
+        b0 = (r - q0 * g.bpr) * 128;
+    }
     const int q = q0 + (c >> g.bsh);
     if (q >= g.Qo) return -1;
     return ((int64_t)p * g.Qo + q) * g.B + b0 + (c & ((1 << g.bsh) - 1));

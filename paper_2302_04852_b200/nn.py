@@ -79,6 +79,27 @@ class _SparseConvFn(torch.autograd.Function):
         return dX, dW, None, None
 
 
+class _SparseConvNCHWFn(torch.autograd.Function):
+    """The paper's SparseConvOverON (P293, P397): NCHW in and out, no permutes."""
+
+    @staticmethod
+    def forward(ctx, x, vals, W, g):  # x NCHW contiguous
+        ctx.W, ctx.g = W, g
+        ctx.save_for_backward(x)
+        return sp.sp_conv2d_fwd_nchw(W, g, x)
+
+    @staticmethod
+    def backward(ctx, gy):
+        (x,) = ctx.saved_tensors
+        dX, dW = sp.sp_conv2d_bwd_nchw(ctx.W, ctx.g, x, gy.contiguous())
+        return dX, dW, None, None
+
+
+def _fp32_cudnn():
+    """The dense path stays fp32 (P134): no TF32 tensor-core convolutions."""
+    return torch.backends.cudnn.flags(enabled=True, benchmark=False, deterministic=False, allow_tf32=False)
+
+
 class _DenseConvFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, vals, W, g):  # x CHWN
@@ -86,14 +107,16 @@ class _DenseConvFn(torch.autograd.Function):
         xn = x.permute(3, 0, 1, 2)
         ctx.W, ctx.g = W, g
         ctx.save_for_backward(xn, Wd)
-        return F.conv2d(xn, Wd, padding=g.pad).permute(1, 2, 3, 0).contiguous()
+        with _fp32_cudnn():
+            return F.conv2d(xn, Wd, padding=g.pad).permute(1, 2, 3, 0).contiguous()
 
     @staticmethod
     def backward(ctx, gy):
         xn, Wd = ctx.saved_tensors
         gyn = gy.permute(3, 0, 1, 2)
-        dxn = torch.nn.grad.conv2d_input(xn.shape, Wd, gyn, padding=ctx.g.pad)
-        dWd = torch.nn.grad.conv2d_weight(xn, Wd.shape, gyn, padding=ctx.g.pad)
+        with _fp32_cudnn():
+            dxn = torch.nn.grad.conv2d_input(xn.shape, Wd, gyn, padding=ctx.g.pad)
+            dWd = torch.nn.grad.conv2d_weight(xn, Wd.shape, gyn, padding=ctx.g.pad)
         dvals = sp.sp_weight_gather(ctx.W, dWd.reshape(Wd.shape[0], -1))
         return dxn.permute(1, 2, 3, 0).contiguous(), dvals, None, None
 
@@ -118,15 +141,25 @@ def cuda_timer(fn, reps: int = 3) -> float:
     return best
 
 
-def decide(sparsity: float, time_dense, time_sparse, mode: str = "auto") -> str:
+def decide(sparsity: float, time_dense, time_sparse, mode: str = "auto", more_sparse: dict | None = None) -> str:
     """The §4.2 rule: forced modes win; below 80 % sparsity -> dense without
-    probing; otherwise the faster of one timed dense and one timed sparse
-    forward+backward."""
-    if mode in ("dense", "sparse"):
+    probing; otherwise the fastest of one timed forward+backward of each
+    implementation -- dense, sparse, and (convolution: "both sparse
+    implementations are considered", P427) the extra sparse ones in
+    `more_sparse` {name: timer}.  Ties go to the sparse implementations, in
+    order."""
+    names = ["sparse"] + list(more_sparse or {})
+    if mode == "dense" or mode in names:
         return mode
     if sparsity < DENSE_BELOW:
         return "dense"
-    return "sparse" if time_sparse() <= time_dense() else "dense"
+    timers = {"sparse": time_sparse, **(more_sparse or {})}
+    best, best_t = "dense", time_dense()
+    for n in reversed(names):  # ties: the first sparse implementation wins
+        t = timers[n]()
+        if t <= best_t:
+            best, best_t = n, t
+    return best
 
 
 class _Dispatching(torch.nn.Module):
@@ -153,6 +186,10 @@ class _Dispatching(torch.nn.Module):
             self.vals.grad = None
         self.impl = None
 
+    def _extra_impls(self):
+        """Sparse implementations besides "sparse" the dispatcher times."""
+        return []
+
     @property
     def sparsity(self) -> float:
         return 1.0 - self.W.nnz / float(self.W.R * self.W.C)
@@ -177,7 +214,14 @@ class _Dispatching(torch.nn.Module):
             def ts():
                 self.probe_ms["sparse"] = run(lambda xx: self._run(xx, "sparse"))()
                 return self.probe_ms["sparse"]
-            self.impl = decide(self.sparsity, td, ts, self.mode)
+
+            def timer_of(name):
+                def t():
+                    self.probe_ms[name] = run(lambda xx: self._run(xx, name))()
+                    return self.probe_ms[name]
+                return t
+            extra = {n: timer_of(n) for n in self._extra_impls()}
+            self.impl = decide(self.sparsity, td, ts, self.mode, extra)
             if self.vals.grad is not None:  # probes must not leak gradients
                 self.vals.grad = None
         return self.impl
@@ -220,7 +264,17 @@ class SparseConv2d(_Dispatching):
     def set_mask(self, weight: torch.Tensor, mask: torch.Tensor):
         self._rebuild(weight, mask)
 
+    def _extra_impls(self):
+        # NCHW input: the batch-last kernel (on permuted copies) and
+        # SparseConvOverON (natural layout) are both candidates (P427)
+        return [] if self.batch_last else ["sparse_nchw"]
+
     def _run(self, x, impl):
+        if impl == "sparse_nchw":  # SparseConvOverON: NCHW in and out
+            xn = x.contiguous()
+            B, C, H, Wd = xn.shape
+            g = sp.conv_geom(self.W, B, H, Wd, self.padding)
+            return _SparseConvNCHWFn.apply(xn, self.vals, self.W, g)
         xc = x if self.batch_last else x.permute(1, 2, 3, 0)
         xc = xc.contiguous()
         C, H, Wd, B = xc.shape

@@ -31,6 +31,7 @@ EXPORTS = [
     "sp_launch_count", "sp_linear_bwd", "sp_linear_bwd_relu", "sp_weight_create_conv", "sp_weight_gather",
     "sp_weight_set_managed", "sp_weight_sgd",
     "sp_conv2d_bwd", "sp_set_sm_reserve", "sp_last_path",
+    "sp_conv2d_fwd_nchw", "sp_conv2d_bwd_input_nchw", "sp_conv2d_bwd_weight_nchw", "sp_conv2d_bwd_nchw",
 ]
 
 
@@ -86,6 +87,10 @@ def lib() -> ct.CDLL:
             "sp_weight_sgd": (st, [vp, vp, ct.c_float, vp]),
             "sp_set_sm_reserve": (st, [ct.c_int32]),
             "sp_last_path": (ct.c_char_p, []),
+            "sp_conv2d_fwd_nchw": (st, [vp, ct.POINTER(sp_conv_geom), vp, vp, vp]),
+            "sp_conv2d_bwd_input_nchw": (st, [vp, ct.POINTER(sp_conv_geom), vp, vp, vp]),
+            "sp_conv2d_bwd_weight_nchw": (st, [vp, ct.POINTER(sp_conv_geom), vp, vp, vp, vp]),
+            "sp_conv2d_bwd_nchw": (st, [vp, ct.POINTER(sp_conv_geom), vp, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -406,6 +411,63 @@ def sp_conv2d_bwd_weight(W: SparseWeight, g: sp_conv_geom, X: torch.Tensor, dY: 
                                       _dev(dY, torch.float32, "dY"),
                                       _dev(dW, torch.float32, "dW") if W.nnz else None,
                                       _stream(stream)))
+    return dW
+
+
+# ---- NCHW (SparseConvOverON, P293 / P397): X, dX [B][C_in][H][W]; Y, dY [B][C_out][OH][OW]
+def sp_conv2d_fwd_nchw(W: SparseWeight, g: sp_conv_geom, X: torch.Tensor, Y: torch.Tensor | None = None,
+                       stream=None) -> torch.Tensor:
+    OH, OW = _geo_out(g)
+    _chk_shape(X, (g.B, g.C_in, g.H, g.W), "X (NCHW [B][C_in][H][W])")
+    if Y is None:
+        Y = torch.empty(g.B, g.C_out, OH, OW, dtype=torch.float32, device=X.device)
+    _chk_shape(Y, (g.B, g.C_out, OH, OW), "Y (NCHW [B][C_out][OH][OW])")
+    _check(lib().sp_conv2d_fwd_nchw(W.handle, ct.byref(g), _dev(X, torch.float32, "X"),
+                                    _dev(Y, torch.float32, "Y"), _stream(stream)))
+    return Y
+
+
+def sp_conv2d_bwd_input_nchw(W: SparseWeight, g: sp_conv_geom, dY: torch.Tensor, dX: torch.Tensor | None = None,
+                             stream=None) -> torch.Tensor:
+    OH, OW = _geo_out(g)
+    _chk_shape(dY, (g.B, g.C_out, OH, OW), "dY (NCHW [B][C_out][OH][OW])")
+    if dX is None:
+        dX = torch.empty(g.B, g.C_in, g.H, g.W, dtype=torch.float32, device=dY.device)
+    _chk_shape(dX, (g.B, g.C_in, g.H, g.W), "dX (NCHW [B][C_in][H][W])")
+    _check(lib().sp_conv2d_bwd_input_nchw(W.handle, ct.byref(g), _dev(dY, torch.float32, "dY"),
+                                          _dev(dX, torch.float32, "dX"), _stream(stream)))
+    return dX
+
+
+def sp_conv2d_bwd_nchw(W: SparseWeight, g: sp_conv_geom, X: torch.Tensor, dY: torch.Tensor,
+                       dX: torch.Tensor | None = None, dW: torch.Tensor | None = None, stream=None):
+    """Both NCHW conv backward products in one pass: (dX, dW)."""
+    OH, OW = _geo_out(g)
+    _chk_shape(X, (g.B, g.C_in, g.H, g.W), "X (NCHW [B][C_in][H][W])")
+    _chk_shape(dY, (g.B, g.C_out, OH, OW), "dY (NCHW [B][C_out][OH][OW])")
+    if dX is None:
+        dX = torch.empty(g.B, g.C_in, g.H, g.W, dtype=torch.float32, device=dY.device)
+    _chk_shape(dX, (g.B, g.C_in, g.H, g.W), "dX (NCHW [B][C_in][H][W])")
+    if dW is None:
+        dW = torch.empty(W.nnz, dtype=torch.float32, device=X.device)
+    _chk_nnz(W, dW)
+    _check(lib().sp_conv2d_bwd_nchw(W.handle, ct.byref(g), _dev(X, torch.float32, "X"),
+                                    _dev(dY, torch.float32, "dY"), _dev(dX, torch.float32, "dX"),
+                                    _dev(dW, torch.float32, "dW") if W.nnz else None, _stream(stream)))
+    return dX, dW
+
+
+def sp_conv2d_bwd_weight_nchw(W: SparseWeight, g: sp_conv_geom, X: torch.Tensor, dY: torch.Tensor,
+                              dW: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    OH, OW = _geo_out(g)
+    _chk_shape(X, (g.B, g.C_in, g.H, g.W), "X (NCHW [B][C_in][H][W])")
+    _chk_shape(dY, (g.B, g.C_out, OH, OW), "dY (NCHW [B][C_out][OH][OW])")
+    if dW is None:
+        dW = torch.empty(W.nnz, dtype=torch.float32, device=X.device)
+    _chk_nnz(W, dW)
+    _check(lib().sp_conv2d_bwd_weight_nchw(W.handle, ct.byref(g), _dev(X, torch.float32, "X"),
+                                           _dev(dY, torch.float32, "dY"),
+                                           _dev(dW, torch.float32, "dW") if W.nnz else None, _stream(stream)))
     return dW
 
 

@@ -142,3 +142,22 @@ def test_first_call_under_no_grad_runs_the_probe():
         y2 = m(x)
     torch.cuda.synchronize()
     assert torch.allclose(y, y2)
+
+
+def test_conv_module_dispatch_times_both_sparse_kernels():
+    """P427: at >= 80 % sparsity the NCHW conv module times dense, the batch-last
+    sparse kernel and SparseConvOverON, keeps the fastest, and each of the three
+    matches the float64 reference."""
+    from paper_2302_04852_b200.nn import SparseConv2d
+    c = synth.conv_case(OC=64, IC=64, H=28, W=28, KH=1, KW=1, pad=0, B=4, density=0.1, wvar=1.0 / 64, seed=41)
+    Wt, Mt = torch.from_numpy(c["W"]).cuda(), torch.from_numpy(c["mask"]).cuda()
+    x = torch.from_numpy(c["X"]).permute(3, 0, 1, 2).contiguous().cuda()
+    ref = torch.nn.functional.conv2d(x.cpu().double(), (Wt * Mt).cpu().double(), padding=0)
+    m = SparseConv2d(Wt, Mt, padding=0, mode="auto")
+    y = m(x)
+    assert set(m.probe_ms) == {"dense", "sparse", "sparse_nchw"}
+    assert m.impl == min(m.probe_ms, key=m.probe_ms.get) or m.probe_ms[m.impl] <= min(m.probe_ms.values())
+    _ok("auto", y, ref)
+    for impl in ("dense", "sparse", "sparse_nchw"):
+        mm = SparseConv2d(Wt, Mt, padding=0, mode=impl)
+        _ok(impl, mm(x), ref)

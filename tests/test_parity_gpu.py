@@ -409,3 +409,39 @@ def test_split_source_spmm_shapes(sp, R, C, B, kind):
     blocks (R, C not multiples of 128 / 192) and skewed rows."""
     c = synth.linear_case(R, C, B, 0.05, 1.0 / C, R + B, kind)
     check_linear(sp, c["W"], c["mask"], c["X"], c["dY"], f"split-source {R}x{C} B={B} {kind}")
+
+
+# ---------------------------------------------------------------- conv, NCHW (SparseConvOverON)
+@pytest.mark.parametrize("B,IC,OC,H,W,K,pad,d", [
+    (4, 64, 48, 56, 56, 1, 0, 0.1),     # 1 x 1 on a large spatial input: the direct NCHW path (P397)
+    (3, 16, 24, 28, 20, 1, 0, 0.2),     # 1 x 1, partial spatial tiles (nq x np tiles of 28 x 20)
+    (1, 4, 4, 8, 8, 1, 0, 0.5),         # 1 x 1, one image
+    (4, 32, 48, 56, 56, 3, 1, 0.1),     # 3 x 3 (column shifts of one float): permuted CHWN kernels
+    (2, 16, 16, 28, 20, 5, 2, 0.2),     # K = 5
+    (8, 16, 16, 14, 14, 3, 1, 0.2),     # W = 14 (not % 4)
+])
+def test_conv_nchw(sp, B, IC, OC, H, W, K, pad, d):
+    """The NCHW entry points against the oracle's native NCHW conv (Eq. 3-5)."""
+    c = synth.conv_case(OC=OC, IC=IC, H=H, W=W, KH=K, KW=K, pad=pad, B=B, density=d,
+                        wvar=1.0 / (IC * K * K), seed=B * 11 + IC + OC + H + K)
+    Wg = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))
+    g = sp.conv_geom(Wg, B, H, W, pad)
+    Xn, dOn = oracle.chwn_to_nchw(c["X"]), oracle.chwn_to_nchw(c["dY"])
+    X, dY = _dev(Xn), _dev(dOn)
+    Y = sp.sp_conv2d_fwd_nchw(Wg, g, X)
+    pf = sp.last_path()
+    dX = sp.sp_conv2d_bwd_input_nchw(Wg, g, dY)
+    dW = sp.sp_conv2d_bwd_weight_nchw(Wg, g, X, dY)
+    fdX, fdW = sp.sp_conv2d_bwd_nchw(Wg, g, X, dY)
+    pb = sp.last_path()
+    torch.cuda.synchronize()
+    F = oracle.conv_format(c["W"], c["mask"])
+    tag = f"nchw B={B} {IC}->{OC} {H}x{W} K={K} pad={pad} [{pf} / {pb}]"
+    _assert_tol(f"{tag} Y", _np(Y), oracle.conv2d_fwd(F, Xn, pad, NT))
+    rdX, rdW = oracle.conv2d_bwd(F, Xn, dOn, pad)
+    _assert_tol(f"{tag} dX", _np(dX), rdX)
+    _assert_tol(f"{tag} dW", _np(dW), rdW)
+    _assert_tol(f"{tag} fused dX", _np(fdX), rdX)
+    _assert_tol(f"{tag} fused dW", _np(fdW), rdW)
+    if K == 1 and pad == 0 and W % 4 == 0:
+        assert "permute" not in pf and "permute" not in pb, (pf, pb)

@@ -87,6 +87,9 @@ CONV = [
     (8, 4, 6, 9, 9, 7, 3, "fwd", "conv_fwd_direct"),              # 49 taps > tap-path limit
     (8, 4, 6, 9, 9, 7, 3, "dx", "conv_dx_direct"),
     (8, 4, 6, 9, 9, 7, 3, "dw", "conv_dw_direct"),
+    (4, 32, 32, 56, 56, 1, 0, "fwd_nchw", "conv_spmm_sk"),      # SparseConvOverON: 1 x 1, NCHW tensor maps
+    (4, 32, 32, 56, 56, 1, 0, "bwd_nchw", "conv_bwd_fused_sk"),
+    (4, 32, 32, 56, 56, 3, 1, "fwd_nchw", "permute_nchw_chwn"),  # 3 x 3: permuted CHWN kernels
 ]
 
 
@@ -99,7 +102,16 @@ def test_conv_path(sp, B, IC, OC, H, W, K, pad, op, family):
     X, dY = _dev(c["X"]), _dev(c["dY"])
     F = oracle.conv_format(c["W"], c["mask"])
     Xn, dOn = oracle.chwn_to_nchw(c["X"]), oracle.chwn_to_nchw(c["dY"])
-    if op == "fwd":
+    if op == "fwd_nchw":
+        out = [sp.sp_conv2d_fwd_nchw(Wg, g, _dev(Xn))]
+        path = sp.last_path()
+        refs = [oracle.conv2d_fwd(F, Xn, pad, NT)]
+    elif op == "bwd_nchw":
+        out = list(sp.sp_conv2d_bwd_nchw(Wg, g, _dev(Xn), _dev(dOn)))
+        path = sp.last_path()
+        rdX, rdW = oracle.conv2d_bwd(F, Xn, dOn, pad)
+        refs = [rdX, rdW]
+    elif op == "fwd":
         out = [sp.sp_conv2d_fwd(Wg, g, X)]
         path = sp.last_path()
         refs = [oracle.nchw_to_chwn(oracle.conv2d_fwd(F, Xn, pad, NT))]
