@@ -158,10 +158,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
         const unsigned eb = (unsigned)(((e1 - e0) * 8 + 15) & ~15);
         mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
         if constexpr (CONV) {
-            int p, q0, b0;
-            cc_origin(a.cc, id.sl, p, q0, b0);
-            const int t = tap_of(id);
-            tma_load_4d(smem + buf * tile_sz, &tmap, b0, q0 + a.cc.dq[t], p + a.cc.dp[t], kb_of(id) * a.KC, &full[buf]);
+            int c[4];
+            cc_coords(a.cc, id.sl, tap_of(id), kb_of(id) * a.KC, c);
+            tma_load_4d(smem + buf * tile_sz, &tmap, c[0], c[1], c[2], c[3], &full[buf]);
         } else {
             tma_load_2d(smem + buf * tile_sz, &tmap, id.sl * BT, kb_of(id) * a.KC, &full[buf]);
         }
@@ -187,7 +186,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
             if (tpos >= a.rows) return;
             const int64_t off = cc_off(a.cc, (int)(bl / BT), (int)(bl % BT));
             if (off < 0) return;
-            float *dst = a.out + tpos * ((int64_t)a.cc.Po * a.cc.Qo * B) + off;
+            float *dst = a.out + tpos * a.cc.rowlen + off;
             *reinterpret_cast<float4 *>(dst) = make_float4(v[0], v[1], v[2], v[3]);
             return;
         }
@@ -473,7 +472,7 @@ bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, const ConvCols &cc, c
     constexpr int RPW = 4, NW = 32, BT = 128;
     const sp_tiling &t0 = w->tap[0][orient];
     if (w->nnz == 0 || t0.RB != RPW * NW) return false;
-    const int64_t nslice = (int64_t)cc.Po * cc.spr;
+    const int64_t nslice = cc.nslice;
     const int64_t T = (int64_t)t0.nrb * nslice * ntap * t0.nkb;
     if (T >= (1LL << 31)) return false;
     const int64_t G = std::min<int64_t>(num_sms(), T);
@@ -483,7 +482,7 @@ bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, const ConvCols &cc, c
     const size_t smem = (size_t)2 * t0.KC * BT * sizeof(float) + (size_t)2 * (cap + 2) * sizeof(int2);
     if (smem > (size_t)(226 * 1024)) return false;
     CUtensorMap tmap{};
-    if (!make_tmap_conv(&tmap, in, t0.inner, Hi, Wi, cc.B, 1 << cc.bsh, cc.nq, t0.KC)) return false;
+    if (!make_tmap_conv(&tmap, in, cc, t0.inner, Hi, Wi, t0.KC)) return false;
     const int64_t nitems = (int64_t)t0.nrb * nslice;
     float *part = nullptr;
     int *tickets = nullptr;
