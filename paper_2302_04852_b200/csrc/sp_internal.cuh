@@ -231,9 +231,6 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
 // ---- spmm_sk.cu: stream-K SpMM (B % 4 == 0, big tiling); false if it does not apply
 bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,
                     int epi, cudaStream_t st);
-// the same on the small tiling (32-row blocks, 8 warps, two CTAs per SM)
-bool launch_spmm_sk_small(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out,
-                          const float *gate, int epi, cudaStream_t st);
 bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, const ConvCols &cc, const float *in, int64_t Hi,
                          int64_t Wi, float *out, int ntap, cudaStream_t st);
 
