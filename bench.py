@@ -365,7 +365,7 @@ def main():
         achieved = fl / (ktime[dom] * 1e-3) / 1e12
         # DRAM traffic per launch of this kernel from the committed ncu --set full capture
         traffic = None
-        tf = os.path.join(ROOT, "profiles", "r1_kernel_traffic.json")
+        tf = os.path.join(ROOT, "profiles", "r2_kernel_traffic.json")
         if os.path.exists(tf):
             kt_ = json.load(open(tf)).get("kernels", {}).get(dom)
             if kt_:
