@@ -61,44 +61,97 @@ __global__ void colblk_scan_kernel(int64_t C, int64_t nb, int32_t *__restrict__ 
     cnt[c] = run;
 }
 
-// Single-block exclusive scan of n int32 counts into out[0..n] (out[n] = total)
-// plus the max count.  Each thread owns a contiguous segment; fixed order.
-__global__ void __launch_bounds__(kScanThreads) scan_kernel(int64_t n, const int32_t *__restrict__ in,
-                                                            int32_t *__restrict__ out,
-                                                            int64_t *__restrict__ info) {
-    __shared__ int64_t sums[kScanThreads];
-    __shared__ int32_t maxs[kScanThreads];
-    const int t = threadIdx.x;
-    const int64_t seg = (n + kScanThreads - 1) / kScanThreads;
-    const int64_t lo = t * seg, hi = lo + seg < n ? lo + seg : n;
-    int64_t s = 0;
-    int32_t mx = 0;
-    for (int64_t i = lo; i < hi; ++i) {
-        s += in[i];
-        mx = in[i] > mx ? in[i] : mx;
+// Exclusive scan of n int32 counts into out[0..n] (out[n] = total) plus the
+// total and the max count (info[0], info[1]), in three coalesced passes over
+// 4096-element chunks: chunk sums / maxima, a one-block scan of the chunk sums,
+// then each chunk's block scan plus its offset.  Fixed order (deterministic).
+constexpr int kScanChunk = 4 * kScanThreads;
+
+__device__ __forceinline__ void chunk_load(int64_t n, const int32_t *__restrict__ in, int64_t c0, int32_t (&v)[4]) {
+    const int64_t i0 = c0 + 4 * (int64_t)threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = i0 + k < n ? in[i0 + k] : 0;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_chunks_kernel(int64_t n, const int32_t *__restrict__ in,
+                                                                   int64_t *__restrict__ csum,
+                                                                   int32_t *__restrict__ cmax) {
+    __shared__ int64_t ws[32];
+    __shared__ int32_t wm[32];
+    int32_t v[4];
+    chunk_load(n, in, (int64_t)blockIdx.x * kScanChunk, v);
+    int64_t sm = (int64_t)v[0] + v[1] + v[2] + v[3];
+    int32_t mx = max(max(v[0], v[1]), max(v[2], v[3]));
+    for (int o = 16; o; o >>= 1) {
+        sm += __shfl_xor_sync(0xffffffffu, sm, o);
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
-    sums[t] = s;
-    maxs[t] = mx;
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    if (lane == 0) {
+        ws[wp] = sm;
+        wm[wp] = mx;
+    }
     __syncthreads();
-    if (t == 0) {
-        int64_t run = 0;
+    if (threadIdx.x == 0) {
+        int64_t t = 0;
         int32_t m = 0;
-        for (int i = 0; i < kScanThreads; ++i) {
-            int64_t v = sums[i];
-            sums[i] = run;
-            run += v;
-            m = maxs[i] > m ? maxs[i] : m;
+        for (int i = 0; i < kScanThreads / 32; ++i) {
+            t += ws[i];
+            m = max(m, wm[i]);
         }
-        info[0] = run;
-        info[1] = m;
+        csum[blockIdx.x] = t;
+        cmax[blockIdx.x] = m;
+    }
+}
+
+__global__ void scan_top_kernel(int64_t nc, int64_t *__restrict__ csum, const int32_t *__restrict__ cmax,
+                                int64_t *__restrict__ info) {
+    int64_t run = 0;
+    int32_t m = 0;
+    for (int64_t c = 0; c < nc; ++c) {
+        const int64_t v = csum[c];
+        csum[c] = run;
+        run += v;
+        m = max(m, cmax[c]);
+    }
+    info[0] = run;
+    info[1] = m;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(int64_t n, const int32_t *__restrict__ in,
+                                                                  const int64_t *__restrict__ coff,
+                                                                  const int64_t *__restrict__ info,
+                                                                  int32_t *__restrict__ out) {
+    __shared__ int64_t ws[32];
+    int32_t v[4];
+    const int64_t c0 = (int64_t)blockIdx.x * kScanChunk;
+    chunk_load(n, in, c0, v);
+    const int64_t ts = (int64_t)v[0] + v[1] + v[2] + v[3];
+    int64_t inc = ts;  // inclusive warp scan of the thread sums
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) ws[wp] = inc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t run = 0;
+        for (int i = 0; i < kScanThreads / 32; ++i) {
+            const int64_t y = ws[i];
+            ws[i] = run;
+            run += y;
+        }
     }
     __syncthreads();
-    int64_t run = sums[t];
-    for (int64_t i = lo; i < hi; ++i) {
-        out[i] = (int32_t)run;  // total checked < 2^31 on the host before use
-        run += in[i];
+    int64_t run = coff[blockIdx.x] + ws[wp] + inc - ts;  // exclusive prefix of this thread's first element
+    const int64_t i0 = c0 + 4 * (int64_t)threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (i0 + k < n) out[i0 + k] = (int32_t)run;  // total checked < 2^31 on the host before use
+        run += v[k];
     }
-    if (t == kScanThreads - 1) out[n] = (int32_t)run;
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = (int32_t)info[0];
 }
 
 // Warp per row: stable compaction with ballots.  Writes col_idx, vals, row_of.
@@ -261,62 +314,83 @@ __global__ void weight_sgd_kernel(int64_t nnz, float *__restrict__ vals, const f
 }
 
 // max over tiles of the tile's entry count (single block, fixed order)
-__global__ void til_max_kernel(int64_t ntiles, int RB, const int32_t *__restrict__ seg, int64_t *__restrict__ out) {
-    __shared__ int32_t sh[256];
-    int32_t m = 0;
-    for (int64_t t = threadIdx.x; t < ntiles; t += blockDim.x) m = max(m, seg[(t + 1) * RB] - seg[t * RB]);
-    sh[threadIdx.x] = m;
-    __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
-        if ((int)threadIdx.x < o) sh[threadIdx.x] = max(sh[threadIdx.x], sh[threadIdx.x + o]);
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *out = sh[0];
+__global__ void til_max_kernel(int64_t ntiles, int RB, const int32_t *__restrict__ seg,
+                               unsigned long long *__restrict__ out) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int32_t m = t < ntiles ? seg[(t + 1) * RB] - seg[t * RB] : 0;
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(out, (unsigned long long)m);  // integer max: order-free
 }
 
-// max over (row block, warp) of the warp's entry groups (segments walked in
-// groups of 4 entries, a last group may hold 2) summed over all column blocks
-// (rows rb*RB + w*RPW .. +RPW), single block, fixed order.  Bounds the
-// per-warp dW sum columns of the TMEM fused backward (8 groups per column).
-__global__ void til_warp_max_kernel(int nrb, int nkb, int RB, int RPW, int GL, const int32_t *__restrict__ seg,
-                                    int64_t *__restrict__ out) {
-    __shared__ int32_t sh[256];
-    const int nw = RB / RPW;
-    int32_t m = 0;
-    for (int i = threadIdx.x; i < nrb * nw; i += blockDim.x) {
-        const int rb = i / nw, wi = i - rb * nw;
-        int32_t s = 0;
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int64_t t = ((int64_t)rb * nkb + kb) * RB + (int64_t)wi * RPW;
-            for (int r = 0; r < RPW; ++r) s += (seg[t + r + 1] - seg[t + r] + (1 << GL) - 1) >> GL;
-        }
-        m = max(m, s);
-    }
-    sh[threadIdx.x] = m;
-    __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
-        if ((int)threadIdx.x < o) sh[threadIdx.x] = max(sh[threadIdx.x], sh[threadIdx.x + o]);
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *out = sh[0];
-}
-
-// gpre (see sp_tiling): thread per (row block, warp); prefix of the warp's
-// groups of 2^GL entries over the column blocks.
-__global__ void til_gpre_kernel(int nrb, int nkb, int RB, int RPW, int GL, const int32_t *__restrict__ seg,
-                                int32_t *__restrict__ out) {
+// per (row block, warp of RPW rows): its entry groups of 4 and of 8 summed
+// over all column blocks -- the maxima bound the per-warp TMEM dW columns of
+// the fused backward (out[0]: groups of 4, out[1]: groups of 8) -- and, when
+// gpre is given, the prefix tables of both (sp_tiling::gpre).  Thread per
+// (row block, warp); maxima by integer atomicMax (order-free).
+__global__ void til_warp_groups_kernel(int nrb, int nkb, int RB, int RPW, const int32_t *__restrict__ seg,
+                                       unsigned long long *__restrict__ mx4, unsigned long long *__restrict__ mx8,
+                                       int32_t *__restrict__ gpre4, int32_t *__restrict__ gpre8) {
     const int nw = RB / RPW;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nrb * nw) return;
-    const int rb = i / nw, wi = i - rb * nw;
-    int32_t s = 0;
-    int32_t *o = out + (int64_t)i * (nkb + 1);
-    for (int kb = 0; kb < nkb; ++kb) {
-        o[kb] = s;
-        const int64_t t = ((int64_t)rb * nkb + kb) * RB + (int64_t)wi * RPW;
-        for (int r = 0; r < RPW; ++r) s += (seg[t + r + 1] - seg[t + r] + (1 << GL) - 1) >> GL;
+    int32_t s4 = 0, s8 = 0;
+    if (i < nrb * nw) {
+        const int rb = i / nw, wi = i - rb * nw;
+        const int64_t g0 = (int64_t)i * (nkb + 1);
+        for (int kb = 0; kb < nkb; ++kb) {
+            if (gpre4) {
+                gpre4[g0 + kb] = s4;
+                gpre8[g0 + kb] = s8;
+            }
+            const int64_t t = ((int64_t)rb * nkb + kb) * RB + (int64_t)wi * RPW;
+            for (int r = 0; r < RPW; ++r) {
+                const int32_t len = seg[t + r + 1] - seg[t + r];
+                s4 += (len + 3) >> 2;
+                s8 += (len + 7) >> 3;
+            }
+        }
+        if (gpre4) {
+            gpre4[g0 + nkb] = s4;
+            gpre8[g0 + nkb] = s8;
+        }
     }
-    o[nkb] = s;
+    for (int o = 16; o; o >>= 1) {
+        s4 = max(s4, __shfl_xor_sync(0xffffffffu, s4, o));
+        s8 = max(s8, __shfl_xor_sync(0xffffffffu, s8, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (s4 > 0) atomicMax(mx4, (unsigned long long)s4);
+        if (s8 > 0) atomicMax(mx8, (unsigned long long)s8);
+    }
+}
+
+// Virtual CSR of the forward tilings with split rows: CSR slot j = the t-th
+// entry of row r goes to part row vbase[r] + t % kp[r], position t / kp[r] of
+// it (columns stay ascending in every part row).
+__global__ void vcsr_kernel(int64_t nnz, const int32_t *__restrict__ row_of, const int32_t *__restrict__ row_ptr,
+                            const int32_t *__restrict__ kp, const int32_t *__restrict__ vbase,
+                            const int32_t *__restrict__ vptr, const int32_t *__restrict__ col_idx,
+                            int32_t *__restrict__ vcol, int32_t *__restrict__ vslot) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nnz) return;
+    const int r = row_of[j], t = (int)(j - row_ptr[r]), k = kp[r];
+    const int pos = vptr[vbase[r] + t % k] + t / k;
+    vcol[pos] = col_idx[j];
+    vslot[pos] = (int32_t)j;
+}
+
+// out[prow[i]][b] = epi(sum over the part slots of split row i, in slot order)
+__global__ void split_rows_reduce_kernel(int nsplit, int64_t B, const int32_t *__restrict__ prow,
+                                         const int32_t *__restrict__ pptr, const float *__restrict__ vpart,
+                                         float *__restrict__ out, const float *__restrict__ gate, int epi) {
+    const int i = blockIdx.y;
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nsplit || b >= B) return;
+    const int64_t r = prow[i];
+    float s = 0.f;
+    for (int k = pptr[i]; k < pptr[i + 1]; ++k) s += vpart[(int64_t)k * B + b];
+    if (epi == 1) s = fmaxf(s, 0.f);
+    if (epi == 2) s = gate[r * B + b] > 0.f ? s : 0.f;
+    out[r * B + b] = s;
 }
 
 __global__ void til_refresh_kernel(int64_t nnz, const int32_t *__restrict__ vidx, const float *__restrict__ vals,
@@ -346,6 +420,27 @@ size_t asize(int64_t n) {
     return Arena::al((size_t)(n > 0 ? n : 1) * sizeof(T));
 }
 
+// out[0..n] = exclusive scan of in[0..n) with out[n] = total; info[0] = total,
+// info[1] = max (int64).  Stream-ordered scratch.
+cudaError_t launch_scan(int64_t n, const int32_t *in, int32_t *out, int64_t *info, cudaStream_t st) {
+    const int64_t nc = std::max<int64_t>(1, (n + kScanChunk - 1) / kScanChunk);
+    int64_t *csum = nullptr;
+    int32_t *cmax = nullptr;
+    cudaError_t e = scratch_alloc((void **)&csum, (size_t)nc * sizeof(int64_t), st);
+    if (e != cudaSuccess) return e;
+    e = scratch_alloc((void **)&cmax, (size_t)nc * sizeof(int32_t), st);
+    if (e != cudaSuccess) {
+        scratch_free(csum, st);
+        return e;
+    }
+    scan_chunks_kernel<<<(unsigned)nc, kScanThreads, 0, st>>>(n, in, csum, cmax);
+    scan_top_kernel<<<1, 1, 0, st>>>(nc, csum, cmax, info);
+    scan_apply_kernel<<<(unsigned)nc, kScanThreads, 0, st>>>(n, in, csum, info, out);
+    scratch_free(csum, st);
+    scratch_free(cmax, st);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 void free_weight(sp_weight_s *w) {
@@ -363,8 +458,10 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
     w->R = R;
     w->C = C;
     int32_t *rcnt = nullptr, *ccnt = nullptr, *blk = nullptr;
-    // column counts / CSC compaction by row blocks: about 256k (block, column) threads
-    const int64_t nb = std::max<int64_t>(1, std::min<int64_t>(R, (262144 + C - 1) / C));
+    // column counts / CSC compaction by row blocks: about 64k (block, column)
+    // threads -- enough to fill the GPU, few enough blocks that the per-column
+    // scan over them stays short
+    const int64_t nb = std::max<int64_t>(1, std::min<int64_t>(R, (65536 + C - 1) / C));
     const int64_t rbk = (R + nb - 1) / nb;
     int64_t *info = nullptr;
     cudaError_t e = cudaSuccess;
@@ -388,8 +485,8 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
         row_count_kernel<<<(unsigned)((R + 7) / 8), 256, 0, st>>>(R, C, mask, rcnt);
         colblk_count_kernel<<<(unsigned)((nb * C + 255) / 256), 256, 0, st>>>(R, C, nb, rbk, mask, blk);
         colblk_scan_kernel<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(C, nb, blk, ccnt);
-        scan_kernel<<<1, kScanThreads, 0, st>>>(R, rcnt, w->row_ptr, info);
-        scan_kernel<<<1, kScanThreads, 0, st>>>(C, ccnt, w->col_ptr, info + 2);
+        SP_TRY(launch_scan(R, rcnt, w->row_ptr, info, st));
+        SP_TRY(launch_scan(C, ccnt, w->col_ptr, info + 2, st));
         SP_TRY(cudaGetLastError());
         int64_t h[4];
         SP_TRY(cudaMemcpyAsync(h, info, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -430,7 +527,7 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
     SP_TRY(cudaGetLastError());
     // gather-SDDMM work list: chunks of <= 32 consecutive nonzeros of one row
     chunk_count_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(R, w->row_ptr, rcnt);
-    scan_kernel<<<1, kScanThreads, 0, st>>>(R, rcnt, w->chunk_ptr, info);
+    SP_TRY(launch_scan(R, rcnt, w->chunk_ptr, info, st));
     {
         const sp_status ts = build_tilings(w, st);
         if (ts != SP_OK) {
@@ -511,6 +608,53 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
                           {1, 32, kTilKC[0], 32, 1, &w->til_f[1]},
                           {1, 64, kTilKC[0], 16, 4, &w->til_f[2]}};
     constexpr int NS = sizeof(specs) / sizeof(specs[0]);
+    // ---- split rows of the forward (CSR) tilings: a row with more than
+    // L = max(32, 2 * mean) entries (Zipf head rows) becomes k = ceil(n / L)
+    // part rows taking its entries in turn, so every part spans all column
+    // blocks with ~n / k entries and no warp carries a whole dense row
+    const int64_t R = w->R;
+    std::vector<int32_t> kp(R, 1), vbase(R), vptr_h, real_of, slot_of;  // part rows per row, ...
+    int64_t nv = 0, nsplit = 0, nparts = 0;
+    {
+        const int64_t L = std::max<int64_t>(32, 2 * ((w->nnz + R - 1) / std::max<int64_t>(R, 1)));
+        for (int64_t r = 0; r < R; ++r) {
+            const int64_t n = hptr[0][r + 1] - hptr[0][r];
+            if (n > L) kp[r] = (int32_t)((n + L - 1) / L);
+            vbase[r] = (int32_t)nv;
+            nv += kp[r];
+            if (kp[r] > 1) {
+                ++nsplit;
+                nparts += kp[r];
+            }
+        }
+    }
+#ifdef SP_NO_SPLIT_ROWS
+    const bool splitting = false;
+#else
+    const bool splitting = nsplit > 0;
+#endif
+    std::vector<int32_t> vlen_ptr;  // pointer array of the virtual rows (for balanced_rows / the tilings)
+    std::vector<int32_t> prow_h, pptr_h;
+    if (splitting) {
+        vlen_ptr.assign(nv + 1, 0);
+        real_of.resize(nv);
+        slot_of.assign(nv, -1);
+        int32_t slot = 0;
+        for (int64_t r = 0; r < R; ++r) {
+            const int32_t n = hptr[0][r + 1] - hptr[0][r], k = kp[r];
+            if (k > 1) {
+                prow_h.push_back((int32_t)r);
+                pptr_h.push_back(slot);
+            }
+            for (int32_t q = 0; q < k; ++q) {
+                const int64_t v = vbase[r] + q;
+                vlen_ptr[v + 1] = vlen_ptr[v] + (n - q + k - 1) / k;
+                real_of[v] = (int32_t)r;
+                if (k > 1) slot_of[v] = slot++;
+            }
+        }
+        pptr_h.push_back(slot);
+    }
     // ---- plan: every tiling's geometry and buffer sizes, then ONE device
     // allocation (the tiling arena) and ONE host -> device copy of the host-built
     // row placements and the managed-SGD table
@@ -523,11 +667,12 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
         sp_tiling &t = *sp_.t;
         const int o = sp_.o;
         Plan &P = pl[si];
-        P.rows = o == 0 ? w->R : w->C;
+        const bool vs = o == 0 && splitting;  // the tiling places part rows
+        P.rows = o == 0 ? (vs ? nv : w->R) : w->C;  // placed (possibly part) rows
         P.inner = o == 0 ? w->C : w->R;
         t.RB = sp_.RB;
         t.KC = sp_.KC;
-        t.rows = P.rows;
+        t.rows = o == 0 ? w->R : w->C;  // output rows (kernel bounds)
         t.inner = P.inner;
         t.nrb = (int)((P.rows + t.RB - 1) / t.RB);
         t.nkb = (int)((P.inner + t.KC - 1) / t.KC);
@@ -536,6 +681,7 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
         P.cap = w->nnz + (kTilPad - 1) * std::min<int64_t>(P.nseg, w->nnz) + 8;
         P.nwg = t.RB / sp_.RPWgrp;
         hbytes += asize<int32_t>(P.rows) + asize<int32_t>((int64_t)t.nrb * t.RB);
+        if (vs) hbytes += asize<int32_t>((int64_t)t.nrb * t.RB) + asize<int32_t>(nsplit) + asize<int32_t>(nsplit + 1);
         bytes += asize<int32_t>(P.nseg + 8) + asize<int2>(P.cap) + asize<int32_t>(P.cap);
         if (w->nnz > 0) bytes += asize<int32_t>(w->nnz);
         if (si == 0 || si == 2) bytes += asize<int32_t>(P.nseg + 8);
@@ -555,8 +701,28 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
         const size_t o2 = ar.off;
         t.rowmap = ar.take<int32_t>((int64_t)t.nrb * t.RB);
         std::vector<int32_t> rowpos, rowmap;
-        balanced_rows(hptr[specs[si].o], pl[si].rows, t.RB, specs[si].NWbal, rowpos, rowmap);
+        const bool vs = specs[si].o == 0 && splitting;
+        balanced_rows(vs ? vlen_ptr : hptr[specs[si].o], pl[si].rows, t.RB, specs[si].NWbal, rowpos, rowmap);
         memcpy(hreg.data() + o1, rowpos.data(), rowpos.size() * sizeof(int32_t));
+        if (vs) {  // positions hold part rows: rowmap -> the real row, split -> the part slot
+            std::vector<int32_t> sm(rowmap.size(), -1);
+            for (size_t pos = 0; pos < rowmap.size(); ++pos)
+                if (rowmap[pos] >= 0) {
+                    sm[pos] = slot_of[rowmap[pos]];
+                    rowmap[pos] = real_of[rowmap[pos]];
+                }
+            const size_t o3 = ar.off;
+            t.split = ar.take<int32_t>((int64_t)t.nrb * t.RB);
+            memcpy(hreg.data() + o3, sm.data(), sm.size() * sizeof(int32_t));
+            const size_t o4 = ar.off;
+            t.prow = ar.take<int32_t>(nsplit);
+            memcpy(hreg.data() + o4, prow_h.data(), prow_h.size() * sizeof(int32_t));
+            const size_t o5 = ar.off;
+            t.pptr = ar.take<int32_t>(nsplit + 1);
+            memcpy(hreg.data() + o5, pptr_h.data(), pptr_h.size() * sizeof(int32_t));
+            t.nsplit = (int32_t)nsplit;
+            t.nparts = (int32_t)nparts;
+        }
         memcpy(hreg.data() + o2, rowmap.data(), rowmap.size() * sizeof(int32_t));
     }
     const size_t otab = ar.off;
@@ -582,16 +748,33 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
     }
     cudaMemcpyAsync(ar.base, hreg.data(), hbytes, cudaMemcpyHostToDevice, st);
 
+    // the virtual CSR of the part rows (device scratch, freed after the build)
+    int32_t *vptr_d = nullptr, *vcol_d = nullptr, *vslot_d = nullptr, *kp_d = nullptr, *vbase_d = nullptr;
+    if (splitting) {
+        if (scratch_alloc((void **)&vptr_d, (size_t)(nv + 1) * sizeof(int32_t), st) != cudaSuccess ||
+            scratch_alloc((void **)&vcol_d, (size_t)std::max<int64_t>(w->nnz, 1) * sizeof(int32_t), st) != cudaSuccess ||
+            scratch_alloc((void **)&vslot_d, (size_t)std::max<int64_t>(w->nnz, 1) * sizeof(int32_t), st) != cudaSuccess ||
+            scratch_alloc((void **)&kp_d, (size_t)R * sizeof(int32_t), st) != cudaSuccess ||
+            scratch_alloc((void **)&vbase_d, (size_t)R * sizeof(int32_t), st) != cudaSuccess)
+            return SP_ERR_ALLOC;
+        cudaMemcpyAsync(vptr_d, vlen_ptr.data(), (size_t)(nv + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(kp_d, kp.data(), (size_t)R * sizeof(int32_t), cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(vbase_d, vbase.data(), (size_t)R * sizeof(int32_t), cudaMemcpyHostToDevice, st);
+        vcsr_kernel<<<(unsigned)((w->nnz + 255) / 256), 256, 0, st>>>(w->nnz, w->row_of, w->row_ptr, kp_d, vbase_d,
+                                                                      vptr_d, w->col_idx, vcol_d, vslot_d);
+    }
     int64_t *info = nullptr, *mx = nullptr;
     if (scratch_alloc((void **)&info, 2 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
     if (scratch_alloc((void **)&mx, 3 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
+    cudaMemsetAsync(mx, 0, 3 * NS * sizeof(int64_t), st);  // atomicMax targets
     for (int si = 0; si < NS; ++si) {
         const Spec &sp_ = specs[si];
         const int o = sp_.o;
         const int64_t rows = pl[si].rows;
-        const int32_t *ptr = o == 0 ? w->row_ptr : w->col_ptr;
-        const int32_t *idx = o == 0 ? w->col_idx : w->row_idx;
-        const int32_t *slotmap = o == 0 ? nullptr : w->perm;
+        const bool vs = o == 0 && splitting;
+        const int32_t *ptr = o == 0 ? (vs ? vptr_d : w->row_ptr) : w->col_ptr;
+        const int32_t *idx = o == 0 ? (vs ? vcol_d : w->col_idx) : w->row_idx;
+        const int32_t *slotmap = o == 0 ? (vs ? vslot_d : nullptr) : w->perm;
         sp_tiling &t = *sp_.t;
         const int64_t nseg = pl[si].nseg, cap = pl[si].cap;
         int32_t *cnt = nullptr;
@@ -607,23 +790,25 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
         const int64_t nt = rows * t.nkb;
         til_count_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, t.nkb, t.KC, t.RB, ptr, idx, t.rowpos,
                                                                       cnt);
-        scan_kernel<<<1, kScanThreads, 0, st>>>(nseg, cnt, t.seg, info + 2 * si);
+        if (launch_scan(nseg, cnt, t.seg, info + 2 * si, st) != cudaSuccess) return SP_ERR_ALLOC;
         til_fill_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, t.nkb, t.KC, t.RB, ptr, idx, slotmap,
                                                                      t.rowpos, t.seg, w->vals, t.ent, t.vidx);
-        til_max_kernel<<<1, 256, 0, st>>>((int64_t)t.nrb * t.nkb, t.RB, t.seg, mx + si);
+        const int64_t ntl = (int64_t)t.nrb * t.nkb;
+        til_max_kernel<<<(unsigned)((ntl + 255) / 256), 256, 0, st>>>(ntl, t.RB, t.seg,
+                                                                     (unsigned long long *)(mx + si));
         if (w->nnz > 0) til_inv_kernel<<<(unsigned)((cap + 255) / 256), 256, 0, st>>>(cap, t.vidx, t.inv);
         t.fresh = 1;  // built from vals: the handle's first version
         if (t.tmsplit)  // the big tilings (RB = 128, KC = 192): split-source SpMM
             til_split_kernel<<<(unsigned)((nseg + 255) / 256), 256, 0, st>>>(nseg, t.KC, t.seg, t.ent, t.tmsplit);
-        if (o == 1) {  // group prefix tables of the fused backward (groups of 4 and of 8)
+        // per-warp group maxima (and, for the fused backward's CSC tilings, the
+        // group prefix tables of groups of 4 and of 8)
+        {
             const int nwg = (int)pl[si].nwg;
-            t.RPWg = sp_.RPWgrp;
-            for (int g = 0; g < 2; ++g)
-                til_gpre_kernel<<<(unsigned)((t.nrb * nwg + 127) / 128), 128, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp,
-                                                                                         2 + g, t.seg, t.gpre[g]);
+            if (o == 1) t.RPWg = sp_.RPWgrp;
+            til_warp_groups_kernel<<<(unsigned)((t.nrb * nwg + 127) / 128), 128, 0, st>>>(
+                t.nrb, t.nkb, t.RB, sp_.RPWgrp, t.seg, (unsigned long long *)(mx + NS + si),
+                (unsigned long long *)(mx + 2 * NS + si), o == 1 ? t.gpre[0] : nullptr, o == 1 ? t.gpre[1] : nullptr);
         }
-        til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp, 2, t.seg, mx + NS + si);
-        til_warp_max_kernel<<<1, 256, 0, st>>>(t.nrb, t.nkb, t.RB, sp_.RPWgrp, 3, t.seg, mx + 2 * NS + si);
         scratch_free(cnt, st);
     }
     std::vector<int64_t> h(3 * NS), hi(2 * NS);
@@ -639,6 +824,8 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
     }
     scratch_free(info, st);
     scratch_free(mx, st);
+    for (int32_t *p : {vptr_d, vcol_d, vslot_d, kp_d, vbase_d})
+        if (p) scratch_free(p, st);
     w->version = 1;
     return (e == cudaSuccess && cudaGetLastError() == cudaSuccess) ? SP_OK : SP_ERR_CUDA;
 }
@@ -701,6 +888,14 @@ void launch_weight_sgd(sp_weight_s *w, const float *dW, float lr, cudaStream_t s
         for (auto &t : o) mark(t);
     for (auto &t : w->til_f) mark(t);
 
+}
+
+void launch_split_rows_reduce(const sp_tiling &t, const float *vpart, int64_t B, float *out, const float *gate,
+                              int epi, cudaStream_t st) {
+    count_launches(1);
+    note_path("split_rows_reduce");
+    split_rows_reduce_kernel<<<dim3((unsigned)((B + 255) / 256), (unsigned)t.nsplit), 256, 0, st>>>(
+        t.nsplit, B, t.prow, t.pptr, vpart, out, gate, epi);
 }
 
 void launch_refresh(const sp_tiling &t, const float *vals, int64_t nnz, cudaStream_t st) {

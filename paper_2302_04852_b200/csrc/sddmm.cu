@@ -382,7 +382,9 @@ sp_status launch_sddmm(const sp_weight_s *w, const float *X, const float *dY, fl
     }
     // the stream-K TMEM kernel (fused.cu) in its dW-only mode when it applies
     if (launch_sddmm_sk(w, X, dY, dW, B, st)) return SP_OK;
-    const int orient = w->C > w->R ? 1 : 0;  // stage the smaller feature dimension
+    // stage the smaller feature dimension; the CSC tiling when the CSR one has
+    // split (part) rows, which would reload a row's register operand per part
+    const int orient = (w->C > w->R || w->til[0][0].psplit_rows()) ? 1 : 0;
     const float *regop = orient ? X : dY;
     const float *smemop = orient ? dY : X;
     const int vec = B <= 32 ? 1 : (B <= 64 || (B & 3)) ? 2 : 4;

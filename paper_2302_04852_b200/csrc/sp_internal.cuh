@@ -86,6 +86,17 @@ struct sp_tiling {
     int32_t *gpre[2];
     int RPWg;
     bool in_arena;  // buffers carved from the handle's tiling arena (freed with it)
+    // split rows (forward tilings of skewed masks, e.g. Zipf head rows): a row
+    // with many more entries than the mean is dealt, entry by entry in turn, into
+    // `k` part rows placed like any other row, so no warp carries a whole dense
+    // row through every tile.  split[pos] = the part slot of a part row (-1 for a
+    // whole row; rowmap still gives the real row), part rows store raw sums to a
+    // scratch [nparts x B] and split_reduce adds each row's parts in slot order
+    int32_t *split;  // [nrb * RB] (nullptr: no split rows)
+    int32_t nparts, nsplit;
+    int32_t *prow;   // [nsplit] real row of each split row
+    int32_t *pptr;   // [nsplit + 1] its part slots [pptr[i], pptr[i+1])
+    bool psplit_rows() const { return split != nullptr; }
 };
 
 // One tiling's entries as seen by the managed SGD kernel.
@@ -227,6 +238,10 @@ enum Epi { EPI_NONE = 0, EPI_RELU = 1, EPI_GATE = 2 };
 // orient 0: forward (CSR, rows = R, inner = C); 1: dX (CSC, rows = C, inner = R).
 void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out,
                  const float *gate, int epi, cudaStream_t st);
+
+// ---- split rows (build.cu): out[prow[i]][b] = epi(sum of the parts of split row i)
+void launch_split_rows_reduce(const sp_tiling &t, const float *vpart, int64_t B, float *out, const float *gate,
+                              int epi, cudaStream_t st);
 
 // ---- spmm_sk.cu: stream-K SpMM (B % 4 == 0, big tiling); false if it does not apply
 bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,

@@ -40,6 +40,8 @@ struct SpmmArgs {
     float *out;
     const float *gate;
     const int32_t *rowmap;  // tiled position -> output row (nullptr: identity)
+    const int32_t *psplit;  // tiled position -> part slot of a split row (-1 whole; nullptr: none)
+    float *vpart;           // [nparts x B] raw sums of the part rows
     // conv (CONV=true): the tile sequence runs over (tap, column block); tap t
     // uses taps[t]'s tiling and reads the padded input shifted by sh[t]
     // columns; output column n = ((p*Wv) + q)*B + b is stored compactly to
@@ -243,6 +245,15 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
         const int64_t tpos = (int64_t)rb * RB + warp * RPW + i;
         const int64_t r = a.rowmap ? (int64_t)__ldg(a.rowmap + tpos) : tpos;
         if (r < 0 || r >= a.rows) continue;
+        if (a.psplit) {  // a part row: raw sums to its slot (split_reduce applies the epilogue)
+            const int sv = __ldg(a.psplit + tpos);
+            if (sv >= 0) {
+#pragma unroll
+                for (int v = 0; v < VEC; ++v)
+                    if (bl + v < B) a.vpart[(int64_t)sv * B + bl + v] = acc[i][v];
+                continue;
+            }
+        }
         float o[VEC];
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
@@ -285,14 +296,20 @@ void launch_cfg(const sp_tiling &t, int64_t B, const float *in, float *out, cons
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
     CUtensorMap tmap{};
     const bool tma = (B & 3) == 0 && make_tmap_2d(&tmap, in, t.inner, B, BT, t.KC);
+    float *vpart = nullptr;
+    if (t.split && scratch_alloc((void **)&vpart, (size_t)t.nparts * B * sizeof(float), st) != cudaSuccess) return;
     SpmmArgs a{t.rows, t.inner, B, t.KC, t.nkb, cap, tma ? 1 : 0, t.seg, t.ent, in, out, gate, t.rowmap,
-               0, nullptr, {}, 0, 0, 0};
+               t.split, vpart, 0, nullptr, {}, 0, 0, 0};
     dim3 grid((unsigned)t.nrb, (unsigned)((B + BT - 1) / BT));
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         count_launches(1);
         note_path("spmm_tiled");
         kern<<<grid, NW * 32, smem, st>>>(a, tmap);
+        if (vpart) {
+            launch_split_rows_reduce(t, vpart, B, out, gate, epi, st);
+            scratch_free(vpart, st);
+        }
     };
     if (sent) {
         if (epi == EPI_RELU) launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_RELU, true, false>);
@@ -328,7 +345,7 @@ bool conv_spmm_vec(const sp_weight_s *w, int orient, int64_t B, const float *in,
     const bool sent = tiles + (size_t)2 * (cap + 2) * sizeof(int2) <= (size_t)kSmemLimit;
     const size_t smem = tiles + (sent ? (size_t)2 * (cap + 2) * sizeof(int2) : 0);
     SpmmArgs a{t0.rows, t0.inner, B, t0.KC, t0.nkb, cap, 1, nullptr, nullptr, nullptr, out, nullptr, nullptr,
-               ntap, w->tapdev + orient * kMaxTaps, {}, Wv, OHv, OWv};
+               nullptr, nullptr, ntap, w->tapdev + orient * kMaxTaps, {}, Wv, OHv, OWv};
     for (int t = 0; t < ntap; ++t) a.sh[t] = sh[t];
     const int64_t Nv = OHv * Wv * B;
     dim3 grid((unsigned)t0.nrb, (unsigned)((Nv + BT - 1) / BT));

@@ -53,6 +53,8 @@ struct HybArgs {
     float *out;
     const float *gate;
     const int32_t *rowmap;
+    const int32_t *psplit;  // tiled position -> part slot of a split row (-1 whole; nullptr: none)
+    float *vpart;          // [nparts x B] raw sums of the part rows
     unsigned long long *stats;  // SP_SPMM_HYB_STATS=1: [groups from TMEM, all groups] (measurement only)
 };
 
@@ -321,6 +323,14 @@ __global__ void __launch_bounds__(HY_NW * 32, 1) spmm_hyb_kernel(const HybArgs a
             const int64_t tpos = (int64_t)rb * HY_RB + warp * HY_RPW + i;
             const int64_t r = a.rowmap ? (int64_t)__ldg(a.rowmap + tpos) : tpos;
             if (r < 0 || r >= a.rows) continue;
+            if (a.psplit) {  // a part row: raw sums to its slot (split_reduce applies the epilogue)
+                const int sv = __ldg(a.psplit + tpos);
+                if (sv >= 0) {
+                    *reinterpret_cast<float4 *>(a.vpart + (int64_t)sv * a.B + bl) =
+                        make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+                    continue;
+                }
+            }
             float o[4];
             if (EPI == EPI_GATE) {
                 const float4 g = __ldg(reinterpret_cast<const float4 *>(a.gate + r * a.B + bl));
@@ -360,13 +370,20 @@ bool launch_spmm_hyb(const sp_weight_s *w, int orient, int64_t B, const float *i
     if (!make_tmap_2d(&tmap, in, t.inner, B, HY_BT, t.KC)) return false;
     refresh_if_stale(w, t, st);
     unsigned long long *stats = nullptr;  // entry counters of a measurement build (none in the product)
-    HybArgs a{t.rows, B, t.KC, t.nkb, cap, t.seg, t.tmsplit, t.ent, out, gate, t.rowmap, stats};
+    float *vpart = nullptr;
+    if (t.split && scratch_alloc((void **)&vpart, (size_t)t.nparts * B * sizeof(float), st) != cudaSuccess)
+        return false;
+    HybArgs a{t.rows, B, t.KC, t.nkb, cap, t.seg, t.tmsplit, t.ent, out, gate, t.rowmap, t.split, vpart, stats};
     dim3 grid((unsigned)t.nrb, (unsigned)((B + HY_BT - 1) / HY_BT));
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         count_launches(1);
         note_path("spmm_hyb");
         kern<<<grid, HY_NW * 32, smem, st>>>(a, tmap);
+        if (vpart) {
+            launch_split_rows_reduce(t, vpart, B, out, gate, epi, st);
+            scratch_free(vpart, st);
+        }
     };
     if (epi == EPI_RELU)
         launch(spmm_hyb_kernel<EPI_RELU, false>);

@@ -43,6 +43,8 @@ struct SkArgs {
     float *out;
     const float *gate;
     const int32_t *rowmap;
+    const int32_t *psplit;  // tiled position -> part slot of a split row (-1 whole; nullptr: none)
+    float *vpart;          // [nparts x B] raw sums of the part rows
     const int32_t *split;  // TMM: tmsplit of the (linear) tiling
     float *part;    // [G][2][RB][BT] raw sums of cut items (slot 0: the CTA's first item, 1: its last)
     int *tickets;   // [nrb * nslice], zero on entry, reset by the finishing CTA
@@ -192,6 +194,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
         const int64_t r = a.rowmap ? (int64_t)__ldg(a.rowmap + tpos) : tpos;
         if (r < 0 || r >= a.rows || bl >= B) return;
+        if (a.psplit) {  // a part row: raw sums to its slot (split_reduce applies the epilogue)
+            const int sv = __ldg(a.psplit + tpos);
+            if (sv >= 0) {
+                *reinterpret_cast<float4 *>(a.vpart + (int64_t)sv * B + bl) = make_float4(v[0], v[1], v[2], v[3]);
+                return;
+            }
+        }
         float o[VEC];
 #pragma unroll
         for (int u = 0; u < VEC; ++u) {
@@ -446,8 +455,11 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
         return false;
     cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
     refresh_if_stale(w, t, st);
-    SkArgs a{t.rows, B, nslice, t.KC, t.nkb, t.nrb, cap, t.seg, t.ent, out, gate, t.rowmap, t.tmsplit, part,
-             tickets, 0, nullptr, {}};
+    float *vpart = nullptr;
+    if (t.split && scratch_alloc((void **)&vpart, (size_t)t.nparts * B * sizeof(float), st) != cudaSuccess)
+        return false;
+    SkArgs a{t.rows, B, nslice, t.KC, t.nkb, t.nrb, cap, t.seg, t.ent, out, gate, t.rowmap, t.split, vpart,
+             t.tmsplit, part, tickets, 0, nullptr, {}};
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         note_path("spmm_sk");
@@ -459,6 +471,10 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
     else if (epi == EPI_GATE) go(spmm_sk_kernel<RPW, NW, EPI_GATE, false>);
     else go(spmm_sk_kernel<RPW, NW, EPI_NONE, false>);
     count_launches(1);
+    if (vpart) {
+        launch_split_rows_reduce(t, vpart, B, out, gate, epi, st);
+        scratch_free(vpart, st);
+    }
     scratch_free(part, st);
     scratch_free(tickets, st);
     return true;
@@ -491,7 +507,7 @@ bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, const ConvCols &cc, c
         return false;
     cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
     SkArgs a{t0.rows, cc.B, nslice, t0.KC, t0.nkb, t0.nrb, cap, nullptr, nullptr, out, nullptr, nullptr, nullptr,
-             part, tickets, ntap, w->tapdev + orient * kMaxTaps, cc};
+             nullptr, nullptr, part, tickets, ntap, w->tapdev + orient * kMaxTaps, cc};
     // conv tap tiles have 128 rows: the TMEM mirror covers half of them (cfg3
     // fwd / dX 206 -> 202 / 201 us)
     bool tmm = t0.KC > kHybTC;

@@ -445,3 +445,33 @@ def test_conv_nchw(sp, B, IC, OC, H, W, K, pad, d):
     _assert_tol(f"{tag} fused dW", _np(fdW), rdW)
     if K == 1 and pad == 0 and W % 4 == 0:
         assert "permute" not in pf and "permute" not in pb, (pf, pb)
+
+
+@pytest.mark.parametrize("B", [256, 2048, 90])
+def test_split_rows_dense_head(sp, B):
+    """Rows far longer than the mean (Zipf heads) are dealt into part rows in
+    the forward tilings and summed by split_rows_reduce: fwd, fwd+ReLU and
+    every backward product against the oracle, with a few fully dense rows."""
+    R, C = 2048, 1536
+    c = synth.linear_case(R, C, B, 0.03, 1.0 / C, 4321 + B)
+    mask = c["mask"].copy()
+    mask[[3, 700, 701, 2047], :] = 1          # dense head rows
+    mask[1000, : C // 2] = 1                  # a half-dense row
+    S = oracle.csr_from_mask(c["W"], mask)
+    Wg = sp.sp_weight_create(_dev(c["W"]), _dev(mask))
+    X, dY = _dev(c["X"]), _dev(c["dY"])
+    Y = sp.sp_linear_fwd(Wg, X)
+    p0 = sp.last_path()
+    Yr = sp.sp_linear_fwd(Wg, X, relu=True)
+    dX, dW = sp.sp_linear_bwd(Wg, X, dY)
+    dW2 = sp.sp_linear_bwd_weight(Wg, X, dY)
+    torch.cuda.synchronize()
+    ref = oracle.linear_fwd(S, c["X"], NT)
+    _assert_tol(f"split fwd B={B} [{p0}]", _np(Y), ref)
+    _assert_tol(f"split fwd relu B={B}", _np(Yr), np.maximum(ref, 0.0))
+    _assert_tol(f"split dX B={B}", _np(dX), oracle.linear_bwd_input(S, c["dY"], NT))
+    refw = oracle.linear_bwd_weight(S, c["X"], c["dY"], NT)
+    _assert_tol(f"split dW B={B}", _np(dW), refw)
+    _assert_tol(f"split dW alone B={B}", _np(dW2), refw)
+    if B % 4 == 0:
+        assert "split_rows_reduce" in p0.split("+") or "spmm_gather" in p0, p0
