@@ -94,7 +94,9 @@ sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8
 sp_status sp_weight_create_conv(int32_t C_out, int32_t C_in, int32_t KH, int32_t KW, const float *dense,
                                 const uint8_t *mask, sp_stream_t stream, sp_weight_t *out);
 
-/* Frees the handle's buffers (after synchronising `stream`). */
+/* Frees the handle's buffers after synchronising `stream` and the device (work on
+ * other streams may still read it).  The buffers return to the library's
+ * stream-ordered pool (sp_weight_create allocates its three arenas there). */
 sp_status sp_weight_destroy(sp_weight_t W, sp_stream_t stream);
 
 /* nnz, R, C of a handle (-1 on a bad handle). */

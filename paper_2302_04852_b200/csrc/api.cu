@@ -172,6 +172,7 @@ sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8
     w->magic = SP_MAGIC;
     const sp_status s = build_weight(R, C, dense, mask, S(stream), w);
     if (s != SP_OK) {
+        cudaDeviceSynchronize();
         free_weight(w);
         w->magic = 0;
         delete w;
@@ -199,6 +200,7 @@ sp_status sp_weight_create_conv(int32_t C_out, int32_t C_in, int32_t KH, int32_t
 sp_status sp_weight_destroy(sp_weight_t w, sp_stream_t stream) {
     SP_CHECK_HANDLE(w, "sp_weight_destroy");
     cudaStreamSynchronize(S(stream));
+    cudaDeviceSynchronize();  // work on other streams may still read the handle (as cudaFree would wait)
     free_weight(w);
     w->magic = 0;
     delete w;

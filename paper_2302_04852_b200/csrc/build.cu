@@ -444,8 +444,11 @@ cudaError_t launch_scan(int64_t n, const int32_t *in, int32_t *out, int64_t *inf
 }  // namespace
 
 void free_weight(sp_weight_s *w) {
+    // the arenas come from the library's stream-ordered pool (cheap to create,
+    // cached on release); every stream's work is complete here (the callers
+    // synchronise the device first), so the legacy stream orders the frees
     for (auto &a : w->arena) {
-        cudaFree(a);
+        if (a) scratch_free(a, 0);
         a = nullptr;
     }
     w->row_ptr = w->col_ptr = w->col_idx = w->row_of = w->row_idx = w->perm = w->chunk_ptr = nullptr;
@@ -476,7 +479,7 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
     SP_TRY(scratch_alloc((void **)&blk, (size_t)(nb * C) * sizeof(int32_t), st));
     {
         Arena a;
-        SP_TRY(cudaMalloc((void **)&a.base, asize<int32_t>(R + 1) + asize<int32_t>(C + 1)));
+        SP_TRY(scratch_alloc((void **)&a.base, asize<int32_t>(R + 1) + asize<int32_t>(C + 1), st));
         w->arena[0] = a.base;
         w->row_ptr = a.take<int32_t>(R + 1);
         w->col_ptr = a.take<int32_t>(C + 1);
@@ -510,7 +513,7 @@ sp_status build_weight(int64_t R, int64_t C, const float *dense, const uint8_t *
     }
     {
         Arena a;
-        SP_TRY(cudaMalloc((void **)&a.base, 5 * asize<int32_t>(w->nnz) + asize<int32_t>(R + 1)));
+        SP_TRY(scratch_alloc((void **)&a.base, 5 * asize<int32_t>(w->nnz) + asize<int32_t>(R + 1), st));
         w->arena[1] = a.base;
         w->col_idx = a.take<int32_t>(w->nnz);
         w->vals = a.take<float>(w->nnz);
@@ -689,7 +692,7 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
     }
     hbytes += asize<SgdRef>(NS);
     Arena ar;
-    if (cudaMalloc((void **)&ar.base, bytes + hbytes) != cudaSuccess) return SP_ERR_ALLOC;
+    if (scratch_alloc((void **)&ar.base, bytes + hbytes, st) != cudaSuccess) return SP_ERR_ALLOC;
     w->arena[2] = ar.base;
     // host-filled region first (rowpos / rowmap of every tiling, the SGD table)
     std::vector<char> hreg(hbytes, 0);

@@ -67,8 +67,32 @@ __global__ void __launch_bounds__(256)
         const int cl = j < end ? __ldg(idx + j) : 0;
         const float wl = j < end ? __ldg(vals + (perm ? __ldg(perm + j) : j)) : 0.f;
         const int n = min(32, end - j0);
+#ifndef SP_GATHER_U4
+        // GU entries in flight per warp: all their row loads issue before the FMAs
+        // (the L2 latency, not its bandwidth, bounds a per-entry load chain;
+        // cfg4 99 %: 4 -> 8 in flight, fwd 38 -> 31 us)
+#ifndef SP_GATHER_GU
+#define SP_GATHER_GU 8
+#endif
+        constexpr int GU = SP_GATHER_GU;
+        int t = 0;
+        for (; t + GU <= n; t += GU) {
+            float x[GU][VEC];
+            float w[GU];
+#pragma unroll
+            for (int u = 0; u < GU; ++u) {
+                const int c = __shfl_sync(kFull, cl, t + u);
+                w[u] = __shfl_sync(kFull, wl, t + u);
+                ldg_vec4<VEC>(in + (int64_t)c * B + bl, x[u], vec, nvalid);
+            }
+#pragma unroll
+            for (int u = 0; u < GU; ++u) fma_bcast<VEC>(acc, w[u], x[u]);
+        }
+        for (; t < n; ++t) {
+#else
 #pragma unroll 4
         for (int t = 0; t < n; ++t) {
+#endif
             const int c = __shfl_sync(kFull, cl, t);
             const float w = __shfl_sync(kFull, wl, t);
             float x[VEC];

@@ -396,7 +396,10 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
     auto ctas = [&](int v, int vv) {
         return (int64_t)w->til[orient][v].nrb * ((B + 32 * vv - 1) / (32 * vv));
     };
-    if (ctas(0, vec) < 2 * num_sms()) var = 1;
+#ifndef SP_VAR1_BELOW_X10
+#define SP_VAR1_BELOW_X10 20
+#endif
+    if (ctas(0, vec) * 10 < SP_VAR1_BELOW_X10 * num_sms()) var = 1;
     while (var == 1 && vec > 1 && ctas(1, vec) < 2 * num_sms()) vec >>= 1;
     // the 32-warp layout takes the split-source kernel: the same entries in the
     // same order (bitwise the shared-memory kernel's result), a third of the
