@@ -38,7 +38,7 @@ def _ok(name, got, ref):
 LINEAR = [
     (3072, 768, 2048, 0.05, "fwd", "spmm_hyb"),        # per-item grid, 32 warps, TMEM-mirrored tiles
     (768, 3072, 2048, 0.05, "fwd", "spmm_sk"),         # short per-item grid, long items: stream-K
-    (3072, 768, 512, 0.05, "fwd", "spmm_tiled"),       # small row blocks (8 warps)
+    (1024, 768, 512, 0.05, "fwd", "spmm_tiled"),       # small row blocks (8 warps): few 128-row items
     (256, 256, 32, 0.1, "fwd", "spmm_gather"),         # tiny product: straight from L2
     (768, 3072, 2048, 0.05, "dx", "spmm_hyb"),         # CSC-driven dX (gather form)
     (3072, 768, 2048, 0.05, "dw", "sddmm_sk"),         # dW alone through the stream-K TMEM kernel
