@@ -1,7 +1,7 @@
 """Compile libsparseprop.so in-tree for sm_100a (nvcc, no JIT cache).
 
-Used by __graft_entry__.build() and the Makefile.  The .so lands next to this
-file so gpurun snapshots carry it to the GPU box.
+Used by __graft_entry__.build() (and tools/build_variant.py for A/B builds).
+The .so lands next to this file so gpurun snapshots carry it to the GPU box.
 """
 from __future__ import annotations
 

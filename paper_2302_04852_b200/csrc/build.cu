@@ -753,22 +753,30 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
 
     // the virtual CSR of the part rows (device scratch, freed after the build)
     int32_t *vptr_d = nullptr, *vcol_d = nullptr, *vslot_d = nullptr, *kp_d = nullptr, *vbase_d = nullptr;
+    int64_t *info = nullptr, *mx = nullptr;
+    int32_t *cnt = nullptr;
+    // error paths release every scratch buffer (the arena itself belongs to the handle)
+    auto fail_alloc = [&]() -> sp_status {
+        for (void *p : {(void *)vptr_d, (void *)vcol_d, (void *)vslot_d, (void *)kp_d, (void *)vbase_d, (void *)info,
+                        (void *)mx, (void *)cnt})
+            if (p) scratch_free(p, st);
+        return SP_ERR_ALLOC;
+    };
     if (splitting) {
         if (scratch_alloc((void **)&vptr_d, (size_t)(nv + 1) * sizeof(int32_t), st) != cudaSuccess ||
             scratch_alloc((void **)&vcol_d, (size_t)std::max<int64_t>(w->nnz, 1) * sizeof(int32_t), st) != cudaSuccess ||
             scratch_alloc((void **)&vslot_d, (size_t)std::max<int64_t>(w->nnz, 1) * sizeof(int32_t), st) != cudaSuccess ||
             scratch_alloc((void **)&kp_d, (size_t)R * sizeof(int32_t), st) != cudaSuccess ||
             scratch_alloc((void **)&vbase_d, (size_t)R * sizeof(int32_t), st) != cudaSuccess)
-            return SP_ERR_ALLOC;
+            return fail_alloc();
         cudaMemcpyAsync(vptr_d, vlen_ptr.data(), (size_t)(nv + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st);
         cudaMemcpyAsync(kp_d, kp.data(), (size_t)R * sizeof(int32_t), cudaMemcpyHostToDevice, st);
         cudaMemcpyAsync(vbase_d, vbase.data(), (size_t)R * sizeof(int32_t), cudaMemcpyHostToDevice, st);
         vcsr_kernel<<<(unsigned)((w->nnz + 255) / 256), 256, 0, st>>>(w->nnz, w->row_of, w->row_ptr, kp_d, vbase_d,
                                                                       vptr_d, w->col_idx, vcol_d, vslot_d);
     }
-    int64_t *info = nullptr, *mx = nullptr;
-    if (scratch_alloc((void **)&info, 2 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
-    if (scratch_alloc((void **)&mx, 3 * NS * sizeof(int64_t), st) != cudaSuccess) return SP_ERR_ALLOC;
+    if (scratch_alloc((void **)&info, 2 * NS * sizeof(int64_t), st) != cudaSuccess) return fail_alloc();
+    if (scratch_alloc((void **)&mx, 3 * NS * sizeof(int64_t), st) != cudaSuccess) return fail_alloc();
     cudaMemsetAsync(mx, 0, 3 * NS * sizeof(int64_t), st);  // atomicMax targets
     for (int si = 0; si < NS; ++si) {
         const Spec &sp_ = specs[si];
@@ -780,12 +788,8 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
         const int32_t *slotmap = o == 0 ? (vs ? vslot_d : nullptr) : w->perm;
         sp_tiling &t = *sp_.t;
         const int64_t nseg = pl[si].nseg, cap = pl[si].cap;
-        int32_t *cnt = nullptr;
-        if (scratch_alloc((void **)&cnt, (size_t)nseg * sizeof(int32_t), st) != cudaSuccess) {
-            scratch_free(info, st);
-            scratch_free(mx, st);
-            return SP_ERR_ALLOC;
-        }
+        cnt = nullptr;
+        if (scratch_alloc((void **)&cnt, (size_t)nseg * sizeof(int32_t), st) != cudaSuccess) return fail_alloc();
         cudaMemsetAsync(cnt, 0, (size_t)nseg * sizeof(int32_t), st);
         cudaMemsetAsync(t.seg + nseg + 1, 0, 7 * sizeof(int32_t), st);  // slack for 16-byte bulk copies of bounds
         cudaMemsetAsync(t.ent, 0, (size_t)cap * sizeof(int2), st);
@@ -793,7 +797,7 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
         const int64_t nt = rows * t.nkb;
         til_count_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, t.nkb, t.KC, t.RB, ptr, idx, t.rowpos,
                                                                       cnt);
-        if (launch_scan(nseg, cnt, t.seg, info + 2 * si, st) != cudaSuccess) return SP_ERR_ALLOC;
+        if (launch_scan(nseg, cnt, t.seg, info + 2 * si, st) != cudaSuccess) return fail_alloc();
         til_fill_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, t.nkb, t.KC, t.RB, ptr, idx, slotmap,
                                                                      t.rowpos, t.seg, w->vals, t.ent, t.vidx);
         const int64_t ntl = (int64_t)t.nrb * t.nkb;
@@ -813,6 +817,7 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
                 (unsigned long long *)(mx + 2 * NS + si), o == 1 ? t.gpre[0] : nullptr, o == 1 ? t.gpre[1] : nullptr);
         }
         scratch_free(cnt, st);
+        cnt = nullptr;
     }
     std::vector<int64_t> h(3 * NS), hi(2 * NS);
     cudaMemcpyAsync(h.data(), mx, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st);

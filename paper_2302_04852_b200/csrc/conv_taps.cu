@@ -147,7 +147,9 @@ sp_status build_conv_taps(sp_weight_s *w, int OC, int IC, int KH, int KW, cudaSt
         }
         const sp_tiling &tf = w->tapf[tp];
         td[2 * kMaxTaps + tp] = TapDev{tf.seg, tf.ent, tf.vidx, tf.npad, tf.tmsplit};
-        // entry groups (4 entries, a tail may hold 2) per warp of 2 rows, summed over taps
+        // entry groups per warp of 2 rows, summed over taps: groups of 4 (whole-warp
+        // entries; segments have even length, so a last group may hold 2) and of 8
+        // (half-warp entries)
         const int KCf = tf.KC;
         for (int ic = 0; ic < IC; ++ic) {
             std::vector<int32_t> cnt(tf.nkb, 0);

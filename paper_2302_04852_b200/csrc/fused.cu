@@ -487,10 +487,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
 // The work is the tile sequence (row block rb, batch slice sl, column block kb),
 // rb-major, T = nrb * nslice * nkb tiles; CTA c of G runs the contiguous range
 // [c*T/G, (c+1)*T/G), so every SM gets the same number of tiles (+-1) instead
-// of a whole number of slices.  An item (rb, sl) cut by a range boundary is
-// shared by exactly two CTAs (ranges are longer than nkb): both add their
-// gated dX partial into the pre-zeroed item with fp32 atomics -- two addends on
-// zero give a + b in either order, so the result stays deterministic.  A job is
+// of a whole number of slices.  An item (rb, sl) cut by range boundaries is
+// shared by the CTAs whose ranges cover it: each stores its raw dX part, and
+// the last to arrive (an integer ticket per item) adds the parts in CTA order,
+// gates and stores -- a fixed order, so the result is deterministic.  A job is
 // one CTA's run of tiles of one row block: its dW sums (TMEM, as above) go to
 // row (c - first CTA of rb) of the partial buffer, summed per entry in fixed
 // order by job_reduce_kernel.
@@ -1073,6 +1073,7 @@ struct JobReduceArgs {
     int64_t tapbase[kMaxTaps];
     const float *part;
     float *dW;
+    int64_t chunk;  // entries per CTA (grid.y chunks per tile)
 };
 __global__ void __launch_bounds__(256) job_reduce_kernel(const JobReduceArgs a) {
     __shared__ int rows[kMaxJobTab];  // part rows (job indices) that touched this tile, ascending
@@ -1082,7 +1083,10 @@ __global__ void __launch_bounds__(256) job_reduce_kernel(const JobReduceArgs a) 
     const int32_t *seg = a.taps ? a.taps[tap].seg : a.seg;
     const int32_t *vidx = a.taps ? a.taps[tap].vidx : a.vidx;
     const int64_t base_e = a.taps ? a.tapbase[tap] : 0;
-    const int64_t e0 = seg[(int64_t)tile * a.RB] + (int64_t)blockIdx.y * blockDim.x, e1 = seg[(int64_t)(tile + 1) * a.RB];
+    // blockIdx.y: a chunk of the tile's entries (grid.y > 1 only when the tiles
+    // alone would not fill the GPU)
+    const int64_t t0e = seg[(int64_t)tile * a.RB], t1e = seg[(int64_t)(tile + 1) * a.RB];
+    const int64_t e0 = t0e + (int64_t)blockIdx.y * a.chunk, e1 = min(t1e, e0 + a.chunk);
     if (e0 >= e1) return;
     const int tpi = a.ntap * a.nkb, r = tap * a.nkb + kb;
     const int64_t T = (int64_t)a.nrb * a.nslice * tpi, G = a.G;
@@ -1108,16 +1112,28 @@ __global__ void __launch_bounds__(256) job_reduce_kernel(const JobReduceArgs a) 
         if (lane == 0) nrows = n;
     }
     __syncthreads();
-    const int64_t e = e0 + threadIdx.x;
-    if (e >= e1) return;
-    const int v = vidx[e];
-    if (v < 0) return;
+    // the CTA loops over its entries (the job search above is paid once per
+    // CTA: one per tile when the tiles fill the GPU)
     const int n = nrows;
-    float s = 0.f;
-    for (int j = 0; j < n; ++j) s += a.part[(int64_t)rows[j] * a.npad + base_e + e];
-    a.dW[v] = s;
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        const int v = vidx[e];
+        if (v < 0) continue;
+        float s = 0.f;
+#pragma unroll 4
+        for (int j = 0; j < n; ++j) s += a.part[(int64_t)rows[j] * a.npad + base_e + e];
+        a.dW[v] = s;
+    }
 }
 
+
+// entries per job_reduce CTA: whole tiles when the tiles alone give >= 4 CTAs
+// per SM (the per-CTA job search is paid once per tile), else 256-entry chunks
+int64_t jr_chunk(int64_t ntiles, int64_t max_tile) {
+    if (max_tile < 1) return 256;
+    const int64_t ny = std::max<int64_t>(1, (4LL * num_sms() + ntiles - 1) / ntiles);
+    const int64_t c = std::max<int64_t>(256, (max_tile + ny - 1) / ny);
+    return (c + 255) / 256 * 256;
+}
 
 }  // namespace
 
@@ -1168,8 +1184,9 @@ static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float 
     if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, NB, false, HALF>);
     else if (H) go(bwd_fused_sk_kernel<TRPW, TNW, true, false, NB, false, HALF>);
     else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, NB, false, HALF>);
-    JobReduceArgs ja{t.npad, slices, G, t.nrb, t.nkb, RBT, 1, t.seg, t.vidx, nullptr, {}, part, dW};
-    job_reduce_kernel<<<dim3((unsigned)(t.nrb * t.nkb), (unsigned)((t.max_tile + 255) / 256)), 256, 0, st>>>(ja);
+    const int64_t ntl = (int64_t)t.nrb * t.nkb, jch = jr_chunk(ntl, t.max_tile);
+    JobReduceArgs ja{t.npad, slices, G, t.nrb, t.nkb, RBT, 1, t.seg, t.vidx, nullptr, {}, part, dW, jch};
+    job_reduce_kernel<<<dim3((unsigned)ntl, (unsigned)((t.max_tile + jch - 1) / jch)), 256, 0, st>>>(ja);
     count_launches(3);  // refresh, kernel, reduce
     scratch_free(part, st);
     if (!dwonly) {
@@ -1289,9 +1306,11 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const ConvCols &cc, const float *d
         if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, 2, true>);
         else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 2, true>);
     }
-    JobReduceArgs ja{tot, slices, G, t0.nrb, t0.nkb, RBF, ntap, nullptr, nullptr, w->tapdev + 2 * kMaxTaps, {}, part, dW};
+    const int64_t ntl = (int64_t)ntap * t0.nrb * t0.nkb, jch = jr_chunk(ntl, mx);
+    JobReduceArgs ja{tot, slices, G, t0.nrb, t0.nkb, RBF, ntap, nullptr, nullptr, w->tapdev + 2 * kMaxTaps, {}, part, dW,
+                     jch};
     for (int t = 0; t < ntap; ++t) ja.tapbase[t] = tapbase[t];
-    job_reduce_kernel<<<dim3((unsigned)(ntap * t0.nrb * t0.nkb), (unsigned)((mx + 255) / 256)), 256, 0, st>>>(ja);
+    job_reduce_kernel<<<dim3((unsigned)ntl, (unsigned)((mx + jch - 1) / jch)), 256, 0, st>>>(ja);
     count_launches(3);  // refresh, kernel, reduce
     scratch_free(part, st);
     if (!dwonly) {

@@ -11,12 +11,12 @@
 // (row block, column block, row) segment are contiguous and store the
 // block-local column and the value).  A CTA owns one row block and one batch
 // slice of BT = 32*VEC columns.  The `in` tile [KC x BT] of each column block
-// is double-buffered in shared memory with cp.async (LDGSTS), coalesced
-// 16-byte copies along the batch.  Each warp owns RPW consecutive rows and
-// keeps their VEC-wide accumulators in registers across column blocks.  Per
-// entry: one warp-uniform 8-byte load of (column, value) (L1-resident: the
-// next tile's entries are prefetched while the current one computes), one
-// vector LDS of tile[column][lane*VEC..], VEC FFMAs.  Every output element is
+// and the tile's entries arrive by TMA (a 2-D box and a 1-D bulk copy) into
+// one of two buffers; the last warp done with a buffer refills it.  Each warp
+// owns RPW consecutive tiled rows and keeps their VEC-wide accumulators in
+// registers across column blocks.  Per pair of entries: one broadcast 16-byte
+// LDS of (column, value) x 2; per entry one vector LDS of tile[column][lane*VEC..]
+// and VEC FFMAs (FFMA2).  Ragged B (B % 4 != 0) stages synchronously.  Every output element is
 // produced by exactly one lane in a fixed order (entries ascending): no
 // atomics, bitwise reproducible, independent of B and of the grid.
 #include <cuda_runtime.h>
@@ -322,7 +322,7 @@ void launch_cfg(const sp_tiling &t, int64_t B, const float *in, float *out, cons
     }
 }
 
-// variant 0: RB = 128 = 16 warps x 8 rows, KC = 192 (1 CTA / SM);
+// variant 0: RB = 128 = 32 warps x 4 rows, KC = 192 (1 CTA / SM);
 // variant 1: RB = 32 = 8 warps x 4 rows, KC = 96 (2 CTAs / SM).
 template <int VEC>
 void launch_variant(const sp_tiling &t, int v, int64_t B, const float *in, float *out, const float *gate,
