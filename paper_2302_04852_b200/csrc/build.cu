@@ -603,14 +603,21 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
         int o, RB, KC, NWbal, RPWgrp;
         sp_tiling *t;
     };
-    const Spec specs[] = {{0, kTilRB[0], kTilKC[0], kTilNW[0], 4, &w->til[0][0]},
-                          {0, kTilRB[1], kTilKC[1], kTilNW[1], kTilRB[1] / kTilNW[1], &w->til[0][1]},
-                          {1, kTilRB[0], kTilKC[0], kTilNW[0], 4, &w->til[1][0]},
-                          {1, kTilRB[1], kTilKC[1], kTilNW[1], kTilRB[1] / kTilNW[1], &w->til[1][1]},
-                          {1, 64, kTilKC[0], 32, 2, &w->til_f[0]},
-                          {1, 32, kTilKC[0], 32, 1, &w->til_f[1]},
-                          {1, 64, kTilKC[0], 16, 4, &w->til_f[2]}};
-    constexpr int NS = sizeof(specs) / sizeof(specs[0]);
+    std::vector<Spec> specs = {{0, kTilRB[0], kTilKC[0], kTilNW[0], 4, &w->til[0][0]},
+                               {0, kTilRB[1], kTilKC[1], kTilNW[1], kTilRB[1] / kTilNW[1], &w->til[0][1]},
+                               {1, kTilRB[0], kTilKC[0], kTilNW[0], 4, &w->til[1][0]},
+                               {1, kTilRB[1], kTilKC[1], kTilNW[1], kTilRB[1] / kTilNW[1], &w->til[1][1]},
+                               {1, 64, kTilKC[0], 32, 2, &w->til_f[0]},
+                               {1, 32, kTilKC[0], 32, 1, &w->til_f[1]},
+                               {1, 64, kTilKC[0], 16, 4, &w->til_f[2]}};
+    // gather tilings (whole inner dimension in one column block; inner indices
+    // times kTilRowBytes must fit an int32 entry offset)
+    if (w->nnz > 0 && ((double)w->nnz <= kGatherDensity * (double)w->R * (double)w->C || w->nnz <= kGatherNnz) &&
+        std::max(w->R, w->C) < (int64_t)(INT32_MAX / kTilRowBytes)) {
+        specs.push_back({0, kGatherRB, (int)w->C, kGatherRB / kGatherUnit, kGatherUnit, &w->til_g[0]});
+        specs.push_back({1, kGatherRB, (int)w->R, kGatherRB / kGatherUnit, kGatherUnit, &w->til_g[1]});
+    }
+    const int NS = (int)specs.size();
     // ---- split rows of the forward (CSR) tilings: a row with more than
     // L = max(32, 2 * mean) entries (Zipf head rows) becomes k = ceil(n / L)
     // part rows taking its entries in turn, so every part spans all column
@@ -663,7 +670,8 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
     // row placements and the managed-SGD table
     struct Plan {
         int64_t rows, inner, nseg, cap, nwg;
-    } pl[NS];
+    };
+    std::vector<Plan> pl(NS);
     size_t bytes = 0, hbytes = 0;  // arena total; the host-filled region
     for (int si = 0; si < NS; ++si) {
         const Spec &sp_ = specs[si];
@@ -869,6 +877,7 @@ void free_tilings(sp_weight_s *w) {
         for (auto &t : o) fr(t);
     for (auto &t : w->tapf) fr(t);
     for (auto &t : w->til_f) fr(t);
+    for (auto &t : w->til_g) fr(t);
 
     if (w->tapdev) cudaFree(w->tapdev);
     w->tapdev = nullptr;
@@ -895,6 +904,7 @@ void launch_weight_sgd(sp_weight_s *w, const float *dW, float lr, cudaStream_t s
     for (auto &o : w->til)
         for (auto &t : o) mark(t);
     for (auto &t : w->til_f) mark(t);
+    for (auto &t : w->til_g) mark(t);
 
 }
 

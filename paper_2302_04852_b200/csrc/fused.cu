@@ -1322,6 +1322,10 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const ConvCols &cc, const float *d
 
 sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY, const float *H, float *dX,
                            float *dW, int64_t B, cudaStream_t st) {
+    // very sparse: the position-gather kernel (both products from each gathered dY row)
+    if (w->nnz > 0 && gather_preferred(w, 1, B) &&
+        launch_gather_pos(w, 1, 1, B, dY, X, H, H ? EPI_GATE : EPI_NONE, dX, dW, st))
+        return SP_OK;
     // stream-K TMEM kernel (any B % 4 == 0) when the rows fit its TMEM columns
     if (launch_sk(w, X, dY, H, dX, dW, B, st)) return SP_OK;
     // slice-split grids: B % 4 == 0, at least one full slice, the big CSC tiling

@@ -377,7 +377,7 @@ sp_status launch_sddmm(const sp_weight_s *w, const float *X, const float *dY, fl
                        cudaStream_t st) {
     if (w->nnz == 0) return SP_OK;
     if (gather_preferred(w, 0, B, true)) {
-        launch_sddmm_gather(w, X, dY, dW, B, st);
+        if (!launch_gather_pos(w, 0, 2, B, X, dY, nullptr, EPI_NONE, nullptr, dW, st)) launch_sddmm_gather(w, X, dY, dW, B, st);
         return SP_OK;
     }
     // the stream-K TMEM kernel (fused.cu) in its dW-only mode when it applies

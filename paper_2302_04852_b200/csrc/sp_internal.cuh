@@ -130,6 +130,11 @@ struct sp_weight_s {
     // rows), [1] 32-row blocks (32 warps x 1 row, long rows), [2] 64-row blocks
     // as 16 warps x 4 rows (half-warp entries when [0]'s dW columns overflow)
     sp_tiling til_f[3];
+    // gather tilings of the very sparse regime (gather.cu's bulk-gather kernels):
+    // [orientation], one column block spanning the whole inner dimension (ent.x =
+    // inner index * kTilRowBytes), 32-position blocks balanced over 8 units of 4
+    // positions; built only when kGatherDensity / kGatherNnz admit the gather path
+    sp_tiling til_g[2];
     // conv handles (sp_weight_create_conv): filter taps and, per tap (x, y),
     // tilings of the OC x IC tap matrix W_xy -- [0]: rows oc / inner ic,
     // [1]: rows ic / inner oc -- whose vidx are slots of THIS handle's CSR.
@@ -150,6 +155,11 @@ struct sp_weight_s {
     int nsgd;
     SgdRef *sgdtab;  // device [nsgd]: every built (non-tap) tiling
 };
+
+// The gather tilings are built for masks at most this dense, or this small.
+constexpr double kGatherDensity = 0.03;
+constexpr int64_t kGatherNnz = 1 << 17;
+constexpr int kGatherRB = 32, kGatherUnit = 4;  // positions per block / per warp unit
 
 // Tiling variants (RB rows per CTA, KC inner columns per shared-memory tile).
 constexpr int kTilRB[2] = {128, 32};
@@ -255,6 +265,10 @@ bool launch_spmm_hyb(const sp_weight_s *w, int orient, int64_t B, const float *i
 
 // ---- gather.cu (very sparse / small regime: no shared-memory staging) ----
 bool gather_preferred(const sp_weight_s *w, int orient, int64_t B, bool chunked = false);
+// position-gather kernels: mode 0 SpMM (orient 0 fwd / 1 dX), 1 fused backward
+// (orient 1), 2 dW alone (orient 0); false when they do not apply
+bool launch_gather_pos(const sp_weight_s *w, int orient, int mode, int64_t B, const float *gin, const float *rin,
+                    const float *gate, int epi, float *out, float *dW, cudaStream_t st);
 void launch_spmm_gather(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out,
                         const float *gate, int epi, cudaStream_t st);
 void launch_sddmm_gather(const sp_weight_s *w, const float *X, const float *dY, float *dW, int64_t B,

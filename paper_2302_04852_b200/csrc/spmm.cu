@@ -382,7 +382,8 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
             cudaMemsetAsync(out, 0, (size_t)((orient == 0 ? w->R : w->C) * B) * sizeof(float), st);
             return;
         }
-        launch_spmm_gather(w, orient, B, in, out, gate, epi, st);
+        if (!launch_gather_pos(w, orient, 0, B, in, nullptr, gate, epi, out, nullptr, st))
+            launch_spmm_gather(w, orient, B, in, out, gate, epi, st);
         return;
     }
     {

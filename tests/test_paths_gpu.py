@@ -39,7 +39,15 @@ LINEAR = [
     (3072, 768, 2048, 0.05, "fwd", "spmm_hyb"),        # per-item grid, 32 warps, TMEM-mirrored tiles
     (768, 3072, 2048, 0.05, "fwd", "spmm_sk"),         # short per-item grid, long items: stream-K
     (1024, 768, 512, 0.05, "fwd", "spmm_tiled"),       # small row blocks (8 warps): few 128-row items
-    (256, 256, 32, 0.1, "fwd", "spmm_gather"),         # tiny product: straight from L2
+    (256, 256, 32, 0.1, "fwd", "spmm_gather"),         # tiny product: straight from L2, narrow lanes
+    (4096, 4096, 256, 0.01, "fwd", "spmm_gather_pos"), # 99 %: warp per gather-tiling position
+    (2048, 2048, 640, 0.01, "fwd", "spmm_gather_pos"), # ragged last 128-column slice
+    (4096, 4096, 252, 0.01, "fwd", "spmm_gather_pos"), # B % 128 != 0
+    (4096, 4096, 256, 0.01, "dx", "spmm_gather_pos"),  # dX through the CSC gather tiling
+    (4096, 4096, 256, 0.01, "bwd", "bwd_gather_pos"),  # fused backward from the gathered dY rows
+    (2048, 2048, 512, 0.01, "bwd", "bwd_gather_pos"),  # ... 512 columns per lane group
+    (2048, 2048, 128, 0.01, "bwd", "bwd_gather_pos"),  # ... 128
+    (4096, 4096, 256, 0.01, "dw", "sddmm_gather_pos"), # dW alone on the CSR gather tiling
     (768, 3072, 2048, 0.05, "dx", "spmm_hyb"),         # CSC-driven dX (gather form)
     (3072, 768, 2048, 0.05, "dw", "sddmm_sk"),         # dW alone through the stream-K TMEM kernel
     (256, 256, 32, 0.1, "dw", "sddmm_gather"),         # tiny SDDMM
@@ -75,6 +83,24 @@ def test_linear_path(sp, R, C, B, d, op, family):
     assert set(family.split("|")) & set(path.split("+")), f"expected {family}, ran {path}"
     for o, r in zip(out, refs):
         _ok(f"{op} [{path}]", o, r)
+
+
+@pytest.mark.parametrize("op", ["fwd", "dw"])
+def test_gather_pos_split_rows(sp, op):
+    """Zipf-skewed rows at 99 %: the position-gather SpMM walks the head rows as
+    balanced part rows (split_rows_reduce adds them); the SDDMM needs no sum."""
+    c = synth.linear_case(4096, 2048, 256, 0.01, 1.0 / 2048, 99, kind="zipf")
+    S = oracle.csr_from_mask(c["W"], c["mask"])
+    W = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))
+    X, dY = _dev(c["X"]), _dev(c["dY"])
+    if op == "fwd":
+        o, r, fam = sp.sp_linear_fwd(W, X), oracle.linear_fwd(S, c["X"], NT), {"spmm_gather_pos", "split_rows_reduce"}
+    else:
+        o, r, fam = sp.sp_linear_bwd_weight(W, X, dY), oracle.linear_bwd_weight(S, c["X"], c["dY"], NT), {"sddmm_gather_pos"}
+    path = sp.last_path()
+    torch.cuda.synchronize()
+    assert fam <= set(path.split("+")), f"expected {fam}, ran {path}"
+    _ok(f"zipf {op} [{path}]", o, r)
 
 
 # (B, IC, OC, H, W, K, pad, op, expected family)

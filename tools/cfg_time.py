@@ -10,11 +10,15 @@ import synth  # noqa: E402
 
 PEAK, HBM = 148 * 128 * 2 * 1965e6, 6550.1e9
 for name in sys.argv[1:]:
-    if name.startswith("cfg4:"):
-        _, kind, sp_ = name.split(":")
+    if name.startswith("cfg4:"):  # cfg4:kind:sparsity[:B]
+        _, kind, sp_, *rest = name.split(":")
         cf = synth.cfg4(float(sp_), kind)
-        r = cs.linear("cfg4", cf["R"], cf["C"], cf["B"], cf["density"], cf["wvar"], cf["seed"], kind, reps=9,
-                      peak=PEAK, hbm=HBM)
+        B = int(rest[0]) if rest else cf["B"]
+        r = cs.linear("cfg4" + (f"@B{B}" if rest else ""), cf["R"], cf["C"], B, cf["density"], cf["wvar"], cf["seed"],
+                      kind, reps=9, peak=PEAK, hbm=HBM)
+    elif name in ("cfg5w1", "cfg5w2"):  # the bench's layer shapes at the full 16384 tokens
+        R, C = (3072, 768) if name == "cfg5w1" else (768, 3072)
+        r = cs.linear(name, R, C, 16384, 0.05, 1.0 / C, 5, reps=5, peak=PEAK, hbm=HBM)
     elif name == "cfg3":
         r = cs.conv("cfg3", reps=9, peak=PEAK, hbm=HBM, **synth.CFG["cfg3"])
     else:
