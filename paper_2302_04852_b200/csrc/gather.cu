@@ -306,15 +306,15 @@ __global__ void __launch_bounds__(256) gather_pos_kernel(const PgArgs a) {
 }  // namespace
 
 // Position-gather launch (MODE as gather_pos_kernel).  false: no gather tiling,
-// B % 4 != 0 or B < 128 (the plain gather's narrower lanes serve those), or
-// (MODE 1 / 2) more than 512 batch columns.
+// B % 4 != 0, (MODE 0) B < 128 (the plain gather's narrower lanes serve those),
+// or (MODE 1 / 2) more than 512 batch columns.
 bool launch_gather_pos(const sp_weight_s *w, int orient, int mode, int64_t B, const float *gin, const float *rin,
                        const float *gate, int epi, float *out, float *dW, cudaStream_t st) {
 #ifdef SP_NO_GATHER_POS
     return false;
 #endif
     const sp_tiling &t = w->til_g[orient];
-    if (t.ent == nullptr || (B & 3) != 0 || B < 128) return false;
+    if (t.ent == nullptr || (B & 3) != 0 || (mode == 0 && B < 128)) return false;
     const int NS = mode == 0 ? 1 : B <= 128 ? 1 : B <= 256 ? 2 : 4;
     if (mode != 0 && B > 128 * NS) return false;
     const int64_t npos = (int64_t)t.nrb * t.RB;

@@ -50,7 +50,9 @@ LINEAR = [
     (4096, 4096, 256, 0.01, "dw", "sddmm_gather_pos"), # dW alone on the CSR gather tiling
     (768, 3072, 2048, 0.05, "dx", "spmm_hyb"),         # CSC-driven dX (gather form)
     (3072, 768, 2048, 0.05, "dw", "sddmm_sk"),         # dW alone through the stream-K TMEM kernel
-    (256, 256, 32, 0.1, "dw", "sddmm_gather"),         # tiny SDDMM
+    (256, 256, 32, 0.1, "dw", "sddmm_gather_pos"),     # tiny SDDMM (8 active lanes)
+    (256, 256, 30, 0.1, "dw", "sddmm_gather"),         # ... B % 4 != 0: the chunked SDDMM
+    (256, 256, 32, 0.1, "bwd", "bwd_gather_pos"),      # tiny fused backward
     (300, 200, 902, 0.1, "dw", "sddmm_tiled"),         # B % 4 != 0: the tiled SDDMM
     (3072, 768, 2048, 0.05, "bwd", "bwd_fused_sk_half"),  # fused backward, half-warp entries
     (4096, 4096, 256, 0.2, "bwd", "bwd_fused_sk"),     # long CSC rows: whole-warp entries
