@@ -185,8 +185,11 @@ def main():
     ap.add_argument("--graph", type=int, default=None,
                     help="replay the whole step as one CUDA graph (default: 1 at N=1, 0 at N>1, where the "
                          "NCCL all_reduce would have to be captured too)")
-    ap.add_argument("--sm-reserve", type=int, default=8,
-                    help="N>1: NCCL channels = SMs the backward's one-wave kernels leave to the all_reduce")
+    ap.add_argument("--sm-reserve", type=int, default=None,
+                    help="N>1: SMs the backward's one-wave kernels leave to the all_reduce (default: 8 NCCL "
+                         "channels; --comm p2p: the peer-memory kernel's CTAs)")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "p2p"],
+                    help="N>1 dW all_reduce: NCCL, or the library's peer-memory kernel (SURVEY F2)")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the per-config single-layer sweep (BASELINE configs 0-3) added at N=1")
     ap.add_argument("--tokens", type=int, default=CFG["T"], help="global batch (default 16384)")
@@ -205,20 +208,22 @@ def main():
     assert args.warmup >= 3, "timing rules need >= 3 warm-up steps"
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    from paper_2302_04852_b200 import sparseprop as sp
+    from paper_2302_04852_b200.dp import SparseMLP
+
+    if args.sm_reserve is None:
+        args.sm_reserve = sp.comm_ctas() if args.comm == "p2p" else 8
     if world > 1:
         # the dW all_reduce overlaps the backward: cap NCCL's CTAs (channels) and
         # leave that many SMs free in the one-wave kernels (SparseMLP sm_reserve)
         os.environ.setdefault("NCCL_MAX_NCHANNELS", str(args.sm_reserve))
         dist.init_process_group("nccl", device_id=dev)
 
-    from paper_2302_04852_b200 import sparseprop as sp
-    from paper_2302_04852_b200.dp import SparseMLP
-
     T = args.tokens
     lo, hi = synth.token_shard(T, world, rank)
     c = synth.mlp_case(blocks=CFG["blocks"], d_model=CFG["d_model"], d_ff=CFG["d_ff"], T=T,
                        density=CFG["density"], seed=CFG["seed"])
-    model = SparseMLP(c["layers"], hi - lo, dev, sm_reserve=args.sm_reserve)
+    model = SparseMLP(c["layers"], hi - lo, dev, sm_reserve=args.sm_reserve, comm=args.comm)
     # every rank must hold identical masks: allgather of a 64-bit hash of every
     # layer's (row_ptr, col_idx)
     if world > 1:
@@ -379,6 +384,7 @@ def main():
             "config": {"workload": WORKLOAD, "model": "sparse MLP 12x(768-3072-768) 95% sparse",
                        "global_batch": T, "seq_len": None, "parallelism": f"dp{world}",
                        "tokens_per_rank": hi - lo,
+                       "dw_allreduce": (args.comm if world > 1 else "none (N=1)"),
                        "l2": "no flush: per-step working set (activations >= 300 MB per rank) > 126 MB L2",
                        "nnz_total": model.nnz_total},
             "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": fp32_peak,

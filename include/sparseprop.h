@@ -287,6 +287,52 @@ sp_status sp_set_sm_reserve(int32_t n);
  * compute call on this thread. */
 const char *sp_last_path(void);
 
+/* ---------------------------------------------------------------------- */
+/* Data-parallel dW all_reduce over peer memory          */
+/* ---------------------------------------------------------------------- */
+/* The multi-GPU exchange of the DP step is the SUM of every rank's
+ * nnz-length dW buffer (the paper runs one CPU, P367).  This
+ * communicator does it without NCCL: each rank's dW lives in a "symmetric"
+ * buffer (one per rank, the same size, mapped into every peer over
+ * NVLink / NVSwitch with CUDA IPC), and ONE kernel per call does a two-shot
+ * all_reduce on [offset, offset + count) floats: the range is cut into
+ * `world` chunks; rank r reads chunk r from every peer, adds the values in
+ * rank order 0..world-1 (fixed order: every rank ends with bitwise the same
+ * sums) and stores the sums into every peer's chunk r (in place).  Each CTA
+ * synchronises with its peer CTAs through flag words in the peers' signal
+ * buffers (system-scope release / acquire, an epoch counter in device
+ * memory: graph-capturable) before reading and after storing.
+ * Setup (collective: every rank, same world / count):
+ *   sp_comm_create  allocates this rank's buffer (count floats, zeroed) and
+ *                   signal words, writes SP_COMM_HANDLE_BYTES of IPC handles
+ *                   to handle_out (host memory);
+ *   exchange the handles (e.g. torch.distributed.all_gather_object);
+ *   sp_comm_open    maps the peers' buffers (handles: world records in rank
+ *                   order, this rank's own included).
+ * world <= SP_COMM_MAX_WORLD; count >= 1.  The buffer is owned by the
+ * communicator (freed by sp_comm_destroy, which synchronises the device). */
+#define SP_COMM_HANDLE_BYTES 128
+#define SP_COMM_MAX_WORLD 8
+typedef struct sp_comm_s *sp_comm_t;
+sp_status sp_comm_create(int32_t rank, int32_t world, int64_t count, sp_comm_t *out, void *handle_out);
+sp_status sp_comm_open(sp_comm_t c, const void *handles);
+/* This rank's symmetric buffer (device, count floats). */
+float *sp_comm_buffer(sp_comm_t c);
+/* In-place SUM over all ranks of buffer[offset, offset + count), enqueued on
+ * `stream`; every rank must make the same sequence of calls (SP_ERR_SHAPE if
+ * the range leaves the buffer).  The kernel uses sp_comm_ctas() CTAs: leave
+ * that many SMs free with sp_set_sm_reserve when it overlaps one-wave kernels. */
+sp_status sp_comm_allreduce(sp_comm_t c, int64_t offset, int64_t count, sp_stream_t stream);
+int32_t sp_comm_ctas(void);
+sp_status sp_comm_destroy(sp_comm_t c);
+/* Single-process test hooks: `world` virtual ranks' buffers on this device;
+ * sp_comm_allreduce_as runs rank r's share of one call with the flag
+ * synchronisation OFF (the caller runs r = 0..world-1 in order on one stream,
+ * which reproduces the multi-GPU result: rank r reads and writes only chunk r). */
+sp_status sp_comm_create_local(int32_t world, int64_t count, sp_comm_t *out);
+float *sp_comm_local_buffer(sp_comm_t c, int32_t rank);
+sp_status sp_comm_allreduce_as(sp_comm_t c, int32_t rank, int64_t offset, int64_t count, sp_stream_t stream);
+
 /* Library build string (arch, version) for provenance in bench records. */
 const char *sp_version(void);
 

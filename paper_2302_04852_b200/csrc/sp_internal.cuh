@@ -158,7 +158,7 @@ struct sp_weight_s {
 
 // The gather tilings are built for masks at most this dense, or this small.
 constexpr double kGatherDensity = 0.03;
-constexpr int64_t kGatherNnz = 1 << 17;
+constexpr int64_t kGatherNnz = 1 << 15;
 constexpr int kGatherRB = 32, kGatherUnit = 4;  // positions per block / per warp unit
 
 // Tiling variants (RB rows per CTA, KC inner columns per shared-memory tile).

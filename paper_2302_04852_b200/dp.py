@@ -69,17 +69,52 @@ class CudaOps:
         self.sp.sp_set_sm_reserve(n)
 
 
+class P2PAllReduce:
+    """The peer-memory dW all_reduce (sparseprop.PeerComm):
+    every rank creates its symmetric buffer, the IPC handle records are
+    exchanged with all_gather_object over `group` (rank order), and each rank
+    maps its peers.  The model's flat dW buffer IS this rank's symmetric buffer,
+    so the backward writes dW where the peers read it.  comm_factory (tests):
+    (rank, world, count) -> an object with .record, .open(records), .buffer,
+    .allreduce(offset, count, stream)."""
+
+    def __init__(self, group, count: int, device, comm_factory=None):
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if comm_factory is None:
+            from . import sparseprop as sp
+            comm_factory = lambda r, w, n: sp.PeerComm(r, w, n, device)  # noqa: E731
+        self.comm = comm_factory(self.rank, self.world, count)
+        records = [None] * self.world
+        dist.all_gather_object(records, self.comm.record, group=group)
+        self.comm.open(records)
+
+    @property
+    def buffer(self):
+        return self.comm.buffer
+
+    def allreduce(self, lo: int, hi: int, stream=None):
+        self.comm.allreduce(lo, hi - lo, stream)
+
+
 class SparseMLP:
     """cfg5 model state + one training step on this rank's token shard."""
 
     def __init__(self, layers, T_local: int, device, ops=None, group=None, bucket_blocks: int = 3,
-                 keep_dx0: bool = True, fused: bool = True, sm_reserve: int = 8):
+                 keep_dx0: bool = True, fused: bool = True, sm_reserve: int = 8, comm: str = "nccl",
+                 comm_factory=None):
         """layers: list of (w1, m1, w2, m2) host arrays (synth.mlp_case).
         sm_reserve: at N > 1, SMs the backward's one-wave (stream-K) kernels
         leave free while the bucketed all_reduce runs on the comm stream, so
         the collective's CTAs do not push part of a wave into a second one
-        (match it to NCCL's channel count, NCCL_MAX_NCHANNELS)."""
+        (match it to NCCL's channel count, NCCL_MAX_NCHANNELS; "p2p": the
+        peer-memory kernel's CTA count, sparseprop.comm_ctas()).
+        comm: "nccl" (torch.distributed.all_reduce) or "p2p" (P2PAllReduce:
+        the library's peer-memory kernel over NVLink, CUDA only)."""
+        if comm not in ("nccl", "p2p"):
+            raise ValueError("comm must be 'nccl' or 'p2p'")
         self.sm_reserve = sm_reserve
+        self.comm = comm
         self.ops = ops if ops is not None else CudaOps()
         self.device = torch.device(device)
         self.group = group
@@ -99,7 +134,12 @@ class SparseMLP:
         # one flat dW buffer; per-layer views; buckets in reverse block order
         sizes = [(W1.nnz, W2.nnz) for (W1, W2) in self.W]
         self.nnz_total = sum(a + b for a, b in sizes)
-        self.dW_flat = torch.zeros(self.nnz_total, **f32)
+        self.p2p = None
+        if comm == "p2p" and self.world > 1:
+            self.p2p = P2PAllReduce(group, self.nnz_total, self.device, comm_factory)
+            self.dW_flat = self.p2p.buffer[:self.nnz_total]
+        else:
+            self.dW_flat = torch.zeros(self.nnz_total, **f32)
         self.dW = []
         off = 0
         self.block_range = []
@@ -125,6 +165,8 @@ class SparseMLP:
         self.mse_scratch = torch.empty(max(2, self.ops.mse_scratch(self.d_model * T_local)), **f32)
         self.is_cuda = self.device.type == "cuda"
         self.comm_stream = torch.cuda.Stream(device=self.device) if (self.is_cuda and self.world > 1) else None
+        if self.p2p is not None and self.comm_stream is None:
+            raise ValueError("comm='p2p' needs CUDA tensors")
 
     # ------------------------------------------------------------------
     def set_batch(self, X0: torch.Tensor, target: torch.Tensor, non_blocking: bool = True):
@@ -202,18 +244,24 @@ class SparseMLP:
                 dY, dYn = dYn, dY
             if comm and bi < len(self.buckets) and self.buckets[bi][0] == l:
                 lo, hi = self.buckets[bi][2], self.buckets[bi][3]
-                pending.append(self._launch_allreduce(self.dW_flat[lo:hi]))
+                pending.append(self._launch_allreduce(lo, hi))
                 bi += 1
         if comm:
             self._wait(pending)
             if self.sm_reserve and hasattr(ops, "sm_reserve"):
                 ops.sm_reserve(0)
 
-    def _launch_allreduce(self, buf):
+    def _launch_allreduce(self, lo: int, hi: int):
+        """All_reduce(SUM) of dW_flat[lo:hi] on the comm stream once the current
+        stream has produced it (NCCL, or the peer-memory kernel)."""
+        buf = self.dW_flat[lo:hi]
         if self.comm_stream is not None:
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream(self.device))
             self.comm_stream.wait_event(ev)
+            if self.p2p is not None:
+                self.p2p.allreduce(lo, hi, self.comm_stream)
+                return None
             with torch.cuda.stream(self.comm_stream):
                 dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
             return None

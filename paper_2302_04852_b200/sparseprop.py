@@ -32,6 +32,8 @@ EXPORTS = [
     "sp_weight_set_managed", "sp_weight_sgd",
     "sp_conv2d_bwd", "sp_set_sm_reserve", "sp_last_path",
     "sp_conv2d_fwd_nchw", "sp_conv2d_bwd_input_nchw", "sp_conv2d_bwd_weight_nchw", "sp_conv2d_bwd_nchw",
+    "sp_comm_create", "sp_comm_open", "sp_comm_buffer", "sp_comm_allreduce", "sp_comm_ctas", "sp_comm_destroy",
+    "sp_comm_create_local", "sp_comm_local_buffer", "sp_comm_allreduce_as",
 ]
 
 
@@ -91,6 +93,15 @@ def lib() -> ct.CDLL:
             "sp_conv2d_bwd_input_nchw": (st, [vp, ct.POINTER(sp_conv_geom), vp, vp, vp]),
             "sp_conv2d_bwd_weight_nchw": (st, [vp, ct.POINTER(sp_conv_geom), vp, vp, vp, vp]),
             "sp_conv2d_bwd_nchw": (st, [vp, ct.POINTER(sp_conv_geom), vp, vp, vp, vp, vp]),
+            "sp_comm_create": (st, [ct.c_int32, ct.c_int32, i64, ct.POINTER(vp), vp]),
+            "sp_comm_open": (st, [vp, vp]),
+            "sp_comm_buffer": (vp, [vp]),
+            "sp_comm_allreduce": (st, [vp, i64, i64, vp]),
+            "sp_comm_ctas": (ct.c_int32, []),
+            "sp_comm_destroy": (st, [vp]),
+            "sp_comm_create_local": (st, [ct.c_int32, i64, ct.POINTER(vp)]),
+            "sp_comm_local_buffer": (vp, [vp, ct.c_int32]),
+            "sp_comm_allreduce_as": (st, [vp, ct.c_int32, i64, i64, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -511,3 +522,91 @@ def sp_sgd(vals: torch.Tensor, dW: torch.Tensor, lr: float, stream=None):
     _check(lib().sp_sgd(_dev(vals, torch.float32, "vals") if n else None,
                         _dev(dW, torch.float32, "dW") if n else None, n, ct.c_float(lr),
                         _stream(stream)))
+
+
+# ---------------------------------------------------------------------------
+# Peer-memory dW all_reduce (include/sparseprop.h)
+# ---------------------------------------------------------------------------
+COMM_HANDLE_BYTES = 128
+
+
+def _cai_view(owner, ptr: int, n: int, device) -> torch.Tensor:
+    """fp32 [n] tensor over library-owned device memory; keeps `owner` alive."""
+    class _CAI:
+        def __init__(self):
+            self.owner = owner
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False),
+                                             "version": 3, "strides": None, "stream": None}
+    return torch.as_tensor(_CAI(), device=device)
+
+
+class PeerComm:
+    """sp_comm_t owner.  create(): this rank's symmetric buffer + its IPC handle
+    record (bytes); open(records): map the peers' buffers (records in rank order).
+    The rendezvous (exchanging the records) is the caller's -- dp.P2PAllReduce
+    does it with torch.distributed.all_gather_object."""
+
+    def __init__(self, rank: int, world: int, count: int, device=None):
+        self.rank, self.world, self.count = int(rank), int(world), int(count)
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        h = ct.c_void_p()
+        rec = ct.create_string_buffer(COMM_HANDLE_BYTES)
+        _check(lib().sp_comm_create(self.rank, self.world, self.count, ct.byref(h), rec))
+        self.handle = h
+        self.record = rec.raw
+
+    def open(self, records: list):
+        if len(records) != self.world or any(len(r) != COMM_HANDLE_BYTES for r in records):
+            raise ValueError("PeerComm.open: one handle record per rank, in rank order")
+        _check(lib().sp_comm_open(self.handle, b"".join(records)))
+
+    @property
+    def buffer(self) -> torch.Tensor:
+        return _cai_view(self, lib().sp_comm_buffer(self.handle), self.count, self.device)
+
+    def allreduce(self, offset: int, count: int, stream=None):
+        _check(lib().sp_comm_allreduce(self.handle, int(offset), int(count), _stream(stream)))
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            lib().sp_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def comm_ctas() -> int:
+    """CTAs one sp_comm_allreduce kernel occupies (SMs to leave free for it)."""
+    return int(lib().sp_comm_ctas())
+
+
+class LocalPeerComm:
+    """Test hook: `world` virtual ranks' buffers in this process (sp_comm_create_local)."""
+
+    def __init__(self, world: int, count: int):
+        self.world, self.count = int(world), int(count)
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        h = ct.c_void_p()
+        _check(lib().sp_comm_create_local(self.world, self.count, ct.byref(h)))
+        self.handle = h
+
+    def buffer(self, rank: int) -> torch.Tensor:
+        return _cai_view(self, lib().sp_comm_local_buffer(self.handle, int(rank)), self.count, self.device)
+
+    def allreduce_as(self, rank: int, offset: int, count: int, stream=None):
+        _check(lib().sp_comm_allreduce_as(self.handle, int(rank), int(offset), int(count), _stream(stream)))
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            lib().sp_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -64,6 +64,14 @@ def test_argument_validation_without_gpu(L):
     assert L.sp_weight_nnz(None) == -1
     assert L.sp_sgd(None, None, 5, ct.c_float(0.1), None) == 1
     assert L.sp_mse_grad(None, None, None, None, None, 5, None) == 1
+    h2 = ct.c_void_p()
+    rec = ct.create_string_buffer(128)
+    assert L.sp_comm_create(0, 9, 16, ct.byref(h2), rec) == 2                    # world > SP_COMM_MAX_WORLD
+    assert L.sp_comm_create(2, 2, 16, ct.byref(h2), rec) == 2                    # rank >= world
+    assert L.sp_comm_create(0, 2, 16, None, rec) == 1
+    assert L.sp_comm_allreduce(None, 0, 4, None) == 6
+    assert L.sp_comm_open(None, rec) == 6
+    assert L.sp_comm_ctas() >= 1
     assert "sm_100a" in sp.version()
 
 

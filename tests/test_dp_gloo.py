@@ -116,3 +116,47 @@ def test_dp_gloo_matches_full_batch(world, fused):
         # buckets cover the flat buffer exactly once, in reverse block order
         assert [b[0] for b in buckets] == [1, 0] and buckets[0][3] == dW.size and buckets[-1][2] == 0
     assert np.array_equal(res[0][2], res[1][2])                          # identical after all_reduce
+
+
+class _FakeComm:
+    """Stand-in for sparseprop.PeerComm (host logic only): a record naming
+    its rank, a CPU buffer, and a log of the calls."""
+
+    def __init__(self, rank, world, count):
+        self.record = bytes([rank]) * 128
+        self.buffer = torch.zeros(count)
+        self.opened = None
+
+    def open(self, records):
+        self.opened = [r[0] for r in records]
+
+
+def _p2p_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2302_04852_b200.dp import P2PAllReduce
+    made = []
+    ar = P2PAllReduce(None, 37, "cpu", comm_factory=lambda r, w, n: made.append((r, w, n)) or _FakeComm(r, w, n))
+    q.put((rank, made, ar.comm.opened, ar.buffer.numel()))
+    dist.destroy_process_group()
+
+
+def test_p2p_rendezvous_gathers_records_in_rank_order():
+    """SURVEY F2 host logic: each rank creates its communicator once and maps
+    its peers from the records all ranks exchanged, in rank order."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, made, opened, n in res:
+        assert made == [(rank, world, 37)]
+        assert opened == list(range(world))
+        assert n == 37
