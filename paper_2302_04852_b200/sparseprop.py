@@ -104,6 +104,8 @@ def lib() -> ct.CDLL:
             "sp_comm_allreduce_as": (st, [vp, ct.c_int32, i64, i64, vp]),
         }
         for name, (res, args) in sig.items():
+            if os.environ.get("SPARSEPROP_LIB") and not hasattr(L, name):
+                continue  # an A/B library built from older sources (tools/build_at_commit.py)
             f = getattr(L, name)
             f.restype, f.argtypes = res, args
         _lib = L

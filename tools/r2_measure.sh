@@ -16,10 +16,11 @@ summ() {
 }
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/${TAG}_smi.txt
 python bench.py > gpurun_out/${TAG}_bench.log 2>&1 || exit 1
-# launch list (same command twice: plain first, then under ncu)
-python bench.py --steps 2 --warmup 3 --no-configs --no-cpu-baseline > gpurun_out/${TAG}_plain.log 2>&1 &&
+# launch list (same command twice: plain first, then under ncu; eager steps: ncu cannot
+# follow the whole-step graph capture -- the capture launch fails under it)
+python bench.py --steps 2 --warmup 3 --no-configs --no-cpu-baseline --graph 0 > gpurun_out/${TAG}_plain.log 2>&1 &&
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
-    python bench.py --steps 2 --warmup 3 --no-configs --no-cpu-baseline > gpurun_out/${TAG}_ncu_launches.log 2>&1
+    python bench.py --steps 2 --warmup 3 --no-configs --no-cpu-baseline --graph 0 > gpurun_out/${TAG}_ncu_launches.log 2>&1
 # cfg5 layer kernels: fwd (split-source SpMM), fused backward
 python tools/prof_layer.py --iters 1 > gpurun_out/${TAG}_plain2.log 2>&1 &&
 timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:spmm_hyb|bwd_fused' -c 4 \
