@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     extern __shared__ __align__(128) float smem[];  // [2][KC][BT] floats, [2][cap+2] int2
     __shared__ uint64_t full[2], tfull[2];
     __shared__ int released[2], ticket[2];
+    __shared__ int tile_ea[2];  // first staged entry of the tile in each buffer, set by its issuer
     __shared__ int last_flag;
     __shared__ uint32_t tmem_base;
     int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * a.KC * BT);
@@ -158,6 +159,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         int e0, e1;
         entry_range(id, e0, e1);
         const unsigned eb = (unsigned)(((e1 - e0) * 8 + 15) & ~15);
+        tile_ea[buf] = e0;  // published to the consumers by the arrive below (release)
         mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
         if constexpr (CONV) {
             int c[4];
@@ -253,7 +255,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
             __syncwarp();
         }
         int ea, e1t;
+#ifndef SP_SPMM_EA_LDG
+        // (a shared-memory read instead of two dependent global ones: stream-K SpMM
+        // -3 to -5 %; the split-source kernel measured slower with it and keeps the loads)
+        ea = tile_ea[buf];
+#else
         entry_range(id, ea, e1t);
+#endif
         // 32-bit shared-window bases pinned in registers (see pin_u32)
         const uint32_t tbs = pin_u32(smem_u32(smem + buf * tile_sz + lane * VEC));
         const uint32_t ess = pin_u32(smem_u32(ents + buf * ebuf) - (uint32_t)ea * 8u);
