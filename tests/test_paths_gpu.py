@@ -156,3 +156,27 @@ def test_conv_path(sp, B, IC, OC, H, W, K, pad, op, family):
     assert family in path.split("+"), f"expected {family}, ran {path}"
     for o, r in zip(out, refs):
         _ok(f"conv {op} [{path}]", o, r)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "zipf"])
+def test_gather_pos_epilogues(sp, kind):
+    """The position gather's ReLU (forward) and ReLU' gate (dX) epilogues, on
+    whole rows and (Zipf) on split part rows, whose epilogue split_rows_reduce
+    applies after adding the parts."""
+    c = synth.linear_case(4096, 2048, 256, 0.01, 1.0 / 2048, 5 if kind == "uniform" else 6, kind=kind)
+    S = oracle.csr_from_mask(c["W"], c["mask"])
+    W = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))
+    X, dY = _dev(c["X"]), _dev(c["dY"])
+    Y = sp.sp_linear_fwd_relu(W, X)
+    path = sp.last_path()
+    torch.cuda.synchronize()
+    assert "spmm_gather_pos" in path.split("+"), path
+    _ok(f"relu fwd [{path}]", Y, np.maximum(oracle.linear_fwd(S, c["X"], NT), 0.0))
+    g = synth.rng(11)
+    gate = synth.normal(g, (2048, 256), 1.0)
+    gate[g.random((2048, 256)) < 0.3] = 0.0
+    dX = sp.sp_linear_bwd_input_relu(W, dY, _dev(gate))
+    path = sp.last_path()
+    torch.cuda.synchronize()
+    assert "spmm_gather_pos" in path.split("+"), path
+    _ok(f"relu' dX [{path}]", dX, oracle.linear_bwd_input(S, c["dY"], NT) * (gate > 0))
