@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
     extern __shared__ __align__(128) float smem[];  // [2][KC][BT] floats, [2][cap+2] int2
     __shared__ uint64_t full[2];
     __shared__ int released[2];  // TMA path: warps done with each buffer (the last one refills it)
+    __shared__ int tile_ea[2];   // TMA path: first staged entry of the tile in each buffer, set by its issuer
     int2 *ents = reinterpret_cast<int2 *>(smem + (size_t)2 * (a.KC + 1) * BT);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
         int e0 = 0, e1 = 0;
         if constexpr (SENT) entry_range(q, e0, e1);
         const unsigned eb = SENT ? (unsigned)(((e1 - e0) * 8 + 15) & ~15) : 0u;
+        if constexpr (SENT) tile_ea[buf] = e0;  // published to the consumers by the arrive below (release)
         // the box is always KC x BT floats (OOB rows / columns zero-filled)
         mbar_arrive_expect_tx(&full[buf], (unsigned)(tile_sz * sizeof(float)) + eb);
         tma_load_2d(smem + buf * buf_sz + BT, &tmap, (int)(b0 + (CONV ? a.sh[t] : 0)), (int)k0, &full[buf]);
@@ -159,8 +161,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
         if (vec4) {
             mbar_wait(&full[buf], (q >> 1) & 1);
             if constexpr (SENT) {
+#ifndef SP_SPMM_EA_LDG
+                ea = tile_ea[buf];  // (a shared-memory read instead of two dependent global ones)
+#else
                 int e1;
                 entry_range(q, ea, e1);
+#endif
             }
         } else {  // ragged B: synchronous staging of this tile (never CONV)
             const int64_t k0 = (int64_t)kb * a.KC;
