@@ -21,6 +21,11 @@ for name in sys.argv[1:]:
         r = cs.linear(name, R, C, 16384, 0.05, 1.0 / C, 5, reps=5, peak=PEAK, hbm=HBM)
     elif name == "cfg3":
         r = cs.conv("cfg3", reps=9, peak=PEAK, hbm=HBM, **synth.CFG["cfg3"])
+    elif "@" in name:  # cfg2a@B: a cfg2 shape at another batch
+        base, B = name.split("@")
+        cf = dict(synth.CFG[base])
+        cf["B"] = int(B)
+        r = cs.linear(name, **cf, reps=9, peak=PEAK, hbm=HBM)
     else:
         r = cs.linear(name, **synth.CFG[name], reps=9, peak=PEAK, hbm=HBM)
     print(json.dumps({k: r[k] for k in ("config", "t_fwd_us", "t_bwd_us", "t_us", "pct_roofline", "path")
