@@ -566,13 +566,21 @@ fail:
 static void balanced_rows(const std::vector<int32_t> &ptr, int64_t rows, int RB, int NW, std::vector<int32_t> &rowpos,
                           std::vector<int32_t> &rowmap) {
     const int64_t nrb = (rows + RB - 1) / RB;
-    const int RPW = RB / NW;
     std::vector<int32_t> order(rows);
     for (int64_t r = 0; r < rows; ++r) order[r] = (int32_t)r;
     std::stable_sort(order.begin(), order.end(),
                      [&](int32_t a, int32_t b) { return ptr[a + 1] - ptr[a] > ptr[b + 1] - ptr[b]; });
     rowpos.assign(rows, 0);
     rowmap.assign(nrb * RB, -1);
+    if (NW == 0) {  // longest first (the gather tilings: a warp per position, CTAs launched in
+                    // position order -- the long rows start first, a CTA's warps have similar lengths)
+        for (int64_t k = 0; k < rows; ++k) {
+            rowpos[order[k]] = (int32_t)k;
+            rowmap[k] = order[k];
+        }
+        return;
+    }
+    const int RPW = RB / NW;
     std::vector<int32_t> used(nrb, 0);
     int64_t k = 0;
     for (int64_t round = 0; k < rows; ++round) {
@@ -614,8 +622,13 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
     // times kTilRowBytes must fit an int32 entry offset)
     if (w->nnz > 0 && ((double)w->nnz <= kGatherDensity * (double)w->R * (double)w->C || w->nnz <= kGatherNnz) &&
         std::max(w->R, w->C) < (int64_t)(INT32_MAX / kTilRowBytes)) {
+#ifndef SP_GATHER_BALANCED
+        specs.push_back({0, kGatherRB, (int)w->C, 0, kGatherUnit, &w->til_g[0]});
+        specs.push_back({1, kGatherRB, (int)w->R, 0, kGatherUnit, &w->til_g[1]});
+#else
         specs.push_back({0, kGatherRB, (int)w->C, kGatherRB / kGatherUnit, kGatherUnit, &w->til_g[0]});
         specs.push_back({1, kGatherRB, (int)w->R, kGatherRB / kGatherUnit, kGatherUnit, &w->til_g[1]});
+#endif
     }
     const int NS = (int)specs.size();
     // ---- split rows of the forward (CSR) tilings: a row with more than

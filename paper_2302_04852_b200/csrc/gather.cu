@@ -315,16 +315,26 @@ bool launch_gather_pos(const sp_weight_s *w, int orient, int mode, int64_t B, co
 #endif
     const sp_tiling &t = w->til_g[orient];
     if (t.ent == nullptr || (B & 3) != 0 || (mode == 0 && B < 128)) return false;
-    const int NS = mode == 0 ? 1 : B <= 128 ? 1 : B <= 256 ? 2 : 4;
-    if (mode != 0 && B > 128 * NS) return false;
     const int64_t npos = (int64_t)t.nrb * t.RB;
+    // MODE 0: a warp per (position, 128-column slice) while that fits one wave of
+    // 64 warps per SM, else 256 columns per warp (e.g. Zipf part rows at 99 %: 1.2
+    // waves of 128-column warps)
+#ifndef SP_GPOS_NS0_WAVE
+#define SP_GPOS_NS0_WAVE 64
+#endif
+    const int NS = mode == 0 ? ((B > 128 && npos * ((B + 127) / 128) > (int64_t)SP_GPOS_NS0_WAVE * num_sms()) ? 2 : 1)
+                             : B <= 128 ? 1 : B <= 256 ? 2 : 4;
+    if (mode != 0 && B > 128 * NS) return false;
     float *vpart = nullptr;
     const bool parts = mode == 0 && t.psplit_rows();
     if (parts && scratch_alloc((void **)&vpart, (size_t)t.nparts * B * sizeof(float), st) != cudaSuccess) return false;
     refresh_if_stale(w, t, st);
     PgArgs a{B, npos, t.seg, t.ent, t.vidx, t.rowmap, parts ? t.split : nullptr, gin, rin, gate, out, dW, vpart, epi};
-    const dim3 grid((unsigned)((npos + 7) / 8), mode == 0 ? (unsigned)((B + 127) / 128) : 1u);
-    if (mode == 0) gather_pos_kernel<1, 0><<<grid, 256, 0, st>>>(a);
+    const dim3 grid((unsigned)((npos + 7) / 8), mode == 0 ? (unsigned)((B + 128 * NS - 1) / (128 * NS)) : 1u);
+    if (mode == 0) {
+        if (NS == 1) gather_pos_kernel<1, 0><<<grid, 256, 0, st>>>(a);
+        else gather_pos_kernel<2, 0><<<grid, 256, 0, st>>>(a);
+    }
     else if (mode == 1) {
         if (NS == 1) gather_pos_kernel<1, 1><<<grid, 256, 0, st>>>(a);
         else if (NS == 2) gather_pos_kernel<2, 1><<<grid, 256, 0, st>>>(a);
