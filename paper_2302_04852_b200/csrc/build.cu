@@ -386,6 +386,7 @@ __global__ void split_rows_reduce_kernel(int nsplit, int64_t B, const int32_t *_
     const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nsplit || b >= B) return;
     const int64_t r = prow[i];
+    pdl_wait();  // (a programmatic dependent of the part-row SpMM)
     float s = 0.f;
     for (int k = pptr[i]; k < pptr[i + 1]; ++k) s += vpart[(int64_t)k * B + b];
     if (epi == 1) s = fmaxf(s, 0.f);
@@ -925,8 +926,8 @@ void launch_split_rows_reduce(const sp_tiling &t, const float *vpart, int64_t B,
                               int epi, cudaStream_t st) {
     count_launches(1);
     note_path("split_rows_reduce");
-    split_rows_reduce_kernel<<<dim3((unsigned)((B + 255) / 256), (unsigned)t.nsplit), 256, 0, st>>>(
-        t.nsplit, B, t.prow, t.pptr, vpart, out, gate, epi);
+    launch_pdl(split_rows_reduce_kernel, dim3((unsigned)((B + 255) / 256), (unsigned)t.nsplit), dim3(256), 0, st,
+               t.nsplit, B, t.prow, t.pptr, vpart, out, gate, epi);
 }
 
 void launch_refresh(const sp_tiling &t, const float *vals, int64_t nnz, cudaStream_t st) {

@@ -709,6 +709,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
     };
     if (threadIdx.x == 0)
         for (int b = 0; b < NBUF && b < ntile; ++b) issue(b, b);
+    // the job reduction that follows (programmatic dependent launch) may start its
+    // CTAs -- and their job search -- on SMs this one-wave grid frees; it waits for
+    // this grid's completion before reading the partial rows
+    pdl_trigger();
     // this warp's segment bounds of (rb, tile r): lane l <= RPW holds the l-th
     auto segw_of = [&](int rb, int r) -> const int32_t * {
         return seg_of(r) + ((int64_t)rb * a.nkb + kb_of(r)) * RB + warp * RPW;
@@ -1125,6 +1129,9 @@ __global__ void __launch_bounds__(256) job_reduce_kernel(const JobReduceArgs a) 
         if (lane == 0) nrows = n;
     }
     __syncthreads();
+    // launched as a programmatic dependent of the fused kernel: everything above
+    // reads only the tiling; the partial rows are complete once the primary is
+    pdl_wait();
     // the CTA loops over its entries (the job search above is paid once per
     // CTA: one per tile when the tiles fill the GPU)
     const int n = nrows;
@@ -1138,6 +1145,12 @@ __global__ void __launch_bounds__(256) job_reduce_kernel(const JobReduceArgs a) 
     }
 }
 
+
+// job_reduce_kernel as a programmatic dependent of the fused kernel just
+// enqueued on `st` (PDL: its launch and job search overlap the fused grid's tail)
+void launch_job_reduce(dim3 grid, const JobReduceArgs &ja, cudaStream_t st) {
+    launch_pdl(job_reduce_kernel, grid, dim3(256), 0, st, ja);
+}
 
 // entries per job_reduce CTA: whole tiles when the tiles alone give >= 4 CTAs
 // per SM (the per-CTA job search is paid once per tile), else 256-entry chunks
@@ -1199,7 +1212,7 @@ static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float 
     else go(bwd_fused_sk_kernel<TRPW, TNW, false, false, NB, false, HALF>);
     const int64_t ntl = (int64_t)t.nrb * t.nkb, jch = jr_chunk(ntl, t.max_tile);
     JobReduceArgs ja{t.npad, slices, G, t.nrb, t.nkb, RBT, 1, t.seg, t.vidx, nullptr, {}, part, dW, jch};
-    job_reduce_kernel<<<dim3((unsigned)ntl, (unsigned)((t.max_tile + jch - 1) / jch)), 256, 0, st>>>(ja);
+    launch_job_reduce(dim3((unsigned)ntl, (unsigned)((t.max_tile + jch - 1) / jch)), ja, st);
     count_launches(3);  // refresh, kernel, reduce
     scratch_free(part, st);
     if (!dwonly) {
@@ -1323,7 +1336,7 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const ConvCols &cc, const float *d
     JobReduceArgs ja{tot, slices, G, t0.nrb, t0.nkb, RBF, ntap, nullptr, nullptr, w->tapdev + 2 * kMaxTaps, {}, part, dW,
                      jch};
     for (int t = 0; t < ntap; ++t) ja.tapbase[t] = tapbase[t];
-    job_reduce_kernel<<<dim3((unsigned)ntl, (unsigned)((mx + jch - 1) / jch)), 256, 0, st>>>(ja);
+    launch_job_reduce(dim3((unsigned)ntl, (unsigned)((mx + jch - 1) / jch)), ja, st);
     count_launches(3);  // refresh, kernel, reduce
     scratch_free(part, st);
     if (!dwonly) {

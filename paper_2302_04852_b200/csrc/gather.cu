@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(256) gather_pos_kernel(const PgArgs a) {
     constexpr bool DW = MODE != 0, ACC = MODE != 2;
     const int lane = threadIdx.x & 31;
     const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    pdl_trigger();  // (a split-row reduction may follow as a programmatic dependent)
     if (p >= a.npos) return;
     const int r = __ldg(a.rowmap + p);
     if (r < 0) return;  // an unused position (no entries)

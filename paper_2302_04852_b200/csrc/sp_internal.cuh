@@ -182,6 +182,42 @@ constexpr int kTilRowBytes = 512;
 
 namespace sp {
 
+// ---- programmatic dependent launch (PDL) ---------------------------------------
+// A short consumer kernel (a reduction of a previous kernel's parts) is launched
+// as a programmatic dependent: its CTAs may be scheduled on SMs the producer
+// grid frees once every producer CTA has called pdl_trigger() (early in the
+// producer), do their independent prologue, and pdl_wait() for the producer's
+// completion (its memory visible) before reading what it wrote.  Kernels that
+// are not launched this way ignore both instructions.
+__device__ __forceinline__ void pdl_trigger() {
+#ifndef SP_NO_PDL
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_wait() {
+#ifndef SP_NO_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+#ifndef SP_NO_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...) == cudaSuccess) return;
+    cudaGetLastError();  // (clear the failed attempt; launch plainly)
+#endif
+    kern<<<grid, block, smem, st>>>(static_cast<KArgs>(args)...);
+}
+
 void set_error(const std::string &msg);
 
 // Count of kernel launches issued by the library (provenance for bench.py).

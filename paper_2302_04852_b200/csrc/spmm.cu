@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
         issue(0, 0);
         if (ntile > 1) issue(1, 1);
     }
+    pdl_trigger();  // (a split-row reduction may follow as a programmatic dependent)
 
     // lane l <= RPW holds the l-th segment bound of this warp's rows in tile q
     // (rows rb*RB + warp*RPW + i).

@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         if (ntile > 0) issue(0, 0);
         if (ntile > 1) issue(1, 1);
     }
+    pdl_trigger();  // (a split-row reduction may follow as a programmatic dependent)
     // lane l <= RPW: the l-th segment bound of this warp's rows; TMM: lanes 8 + i
     // hold row i's tmsplit
     auto split_of = [&](const Tile &id) -> const int32_t * { return CONV ? a.taps[tap_of(id)].split : a.split; };
