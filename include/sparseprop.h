@@ -76,8 +76,10 @@ typedef struct {
  *   col_ptr[C+1], row_idx[nnz] (ascending per column),
  *   perm[nnz] (CSC slot k -> CSR slot holding the same (r, c)),
  * plus the tiled copies of both orientations the kernels stream (row blocks x
- * column blocks), deterministically on the device; it
- * synchronises `stream` (to read nnz, block row counts and tile maxima).
+ * column blocks; masks at most 3 % dense or with at most 2^15
+ * nonzeros also get the single-column-block gather tilings of the L2-gather
+ * kernels), deterministically on the device; it synchronises `stream` (to
+ * read nnz, block row counts and tile maxima).
  * R, C >= 1; R, C and nnz must fit int32 (else SP_ERR_OVERFLOW); R*C may
  * exceed it (no R x C scratch is used).
  * The handle owns all its device buffers. */
@@ -87,8 +89,9 @@ sp_status sp_weight_create(int64_t R, int64_t C, const float *dense, const uint8
 /* Same as sp_weight_create for a conv filter [C_out][C_in][KH][KW] (dense and
  * mask on the device in that order; R = C_out, C = C_in*KH*KW), plus the
  * per-tap tilings the conv kernels stream: implicit im2col by taps -- each
- * filter tap (x, y) is an OC x IC sparse matrix applied to a shifted view of
- * the spatially padded activation (Eq. 3, P224; pruned taps skipped, P248).
+ * filter tap (x, y) is an OC x IC sparse matrix applied to the activation
+ * shifted by (x - pad, y - pad), out-of-range positions reading zero (Eq. 3,
+ * P224; pruned taps skipped, P248).
  * Synchronises `stream`.  Handles from sp_weight_create also work with the
  * conv entry points (through slower direct kernels). */
 sp_status sp_weight_create_conv(int32_t C_out, int32_t C_in, int32_t KH, int32_t KW, const float *dense,
