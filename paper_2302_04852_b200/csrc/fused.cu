@@ -607,9 +607,24 @@ constexpr int sk_dw0() { return (DWONLY ? 1 : 2) * RPW * (HALF ? 8 : 4); }
 template <int RPW, bool DWONLY, int NW = 32, bool HALF = false>
 constexpr int sk_dwcols() { return sk_cpw<NW>() - sk_dw0<RPW, DWONLY, HALF>(); }
 
+#ifdef SP_FUSED_TS
+// (measurement build only: tools/dbg/fused_ts.py) per-CTA %globaltimer stamps of
+// the last fused launch: [cta][0] entry, [1] first tile ready, [2] main loop done, [3] exit
+__device__ unsigned long long g_fused_ts[1024][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define FUSED_TS(k) \
+    if (threadIdx.x == 0 && blockIdx.x < 1024) g_fused_ts[blockIdx.x][k] = gtimer()
+#else
+#define FUSED_TS(k)
+#endif
 template <int RPW, int NW, bool GATE, bool DWONLY, int NBUF, bool CONV, bool HALF = false>
 __global__ void __launch_bounds__(NW * 32, 1)
     bwd_fused_sk_kernel(const FusedArgs a, const __grid_constant__ CUtensorMap tmap) {
+    FUSED_TS(0);
     constexpr int VEC = 4;
     constexpr int SW = HALF ? 8 : 4;  // TMEM columns per row (X row, dX accumulator)
     constexpr int RV0 = 0, DX0 = SW * RPW, DW0 = sk_dw0<RPW, DWONLY, HALF>(), DWC = sk_dwcols<RPW, DWONLY, NW, HALF>();
@@ -839,6 +854,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         nid = next_tile(id);
         if (q + 1 < ntile) sgn = seg_bounds(nid);
         mbar_wait(&full[buf], (q / NBUF) & 1);
+        if (q == 0) FUSED_TS(1);
         // the tile's first staged entry: from its issuer through shared memory (linear
         // layers: cfg5 fused backward -1.5 %), from the tiling for conv (measured +0.8 %)
         int ea, e1t;
@@ -1071,9 +1087,11 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
     }
     tm_wait_st();
+    FUSED_TS(2);
     if (cur_rb >= 0) dump(cur_rb, job_a, t0 + ntile - job_a - (int)((int64_t)cur_rb * a.nslice * tpi));
     tm_fence_before();
     __syncthreads();
+    FUSED_TS(3);
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
 }
 
@@ -1419,3 +1437,9 @@ sp_status launch_bwd_fused(const sp_weight_s *w, const float *X, const float *dY
 }
 
 }  // namespace sp
+
+#ifdef SP_FUSED_TS
+extern "C" int sp_debug_fused_ts(unsigned long long *out, int n) {
+    return cudaMemcpyFromSymbol(out, sp::g_fused_ts, (size_t)n * 4 * sizeof(unsigned long long)) == cudaSuccess ? 0 : 1;
+}
+#endif
