@@ -180,3 +180,38 @@ def test_gather_pos_epilogues(sp, kind):
     torch.cuda.synchronize()
     assert "spmm_gather_pos" in path.split("+"), path
     _ok(f"relu' dX [{path}]", dX, oracle.linear_bwd_input(S, c["dY"], NT) * (gate > 0))
+
+
+def test_gather_pos_random_sweep(sp):
+    """24 seeded very sparse instances (0.5-2 % dense, uniform and Zipf rows,
+    ragged R / C, B in {4..640} with B % 4 == 0): forward, dX, dW alone and
+    the fused backward (plain and gated) through the position-gather kernels
+    (mode 0 / 1 / 2, one- and two-slice warps, split part rows) against the oracle."""
+    g = synth.rng(98)
+    seen = set()
+    for i in range(24):
+        R, C = (int(v) for v in g.integers(97, 3001, size=2))
+        B = int(g.choice([4, 36, 128, 252, 256, 384, 512, 640]))
+        d = float(g.choice([0.005, 0.01, 0.02]))
+        kind = "zipf" if i % 3 == 2 else "uniform"
+        c = synth.linear_case(R, C, B, d, 1.0 / C, 900 + i, kind=kind)
+        S = oracle.csr_from_mask(c["W"], c["mask"])
+        W = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))
+        X, dY = _dev(c["X"]), _dev(c["dY"])
+        gate = synth.normal(synth.rng(1900 + i), (C, B), 1.0)
+        tag = f"gather sweep {i}: {R}x{C} B={B} d={d} {kind}"
+        outs = [("fwd", sp.sp_linear_fwd(W, X), oracle.linear_fwd(S, c["X"], NT))]
+        seen.add(sp.last_path())
+        outs.append(("dx", sp.sp_linear_bwd_input(W, dY), oracle.linear_bwd_input(S, c["dY"], NT)))
+        seen.add(sp.last_path())
+        outs.append(("dw", sp.sp_linear_bwd_weight(W, X, dY), oracle.linear_bwd_weight(S, c["X"], c["dY"], NT)))
+        seen.add(sp.last_path())
+        fdX, fdW = sp.sp_linear_bwd_relu(W, X, dY, _dev(gate))
+        seen.add(sp.last_path())
+        outs += [("fused dX", fdX, oracle.linear_bwd_input(S, c["dY"], NT) * (gate > 0)),
+                 ("fused dW", fdW, oracle.linear_bwd_weight(S, c["X"], c["dY"], NT))]
+        torch.cuda.synchronize()
+        for name, o, r in outs:
+            _ok(f"{tag} {name}", o, r)
+    fams = set("+".join(seen).split("+"))
+    assert {"spmm_gather_pos", "bwd_gather_pos", "sddmm_gather_pos"} <= fams, fams
