@@ -215,3 +215,33 @@ def test_gather_pos_random_sweep(sp):
             _ok(f"{tag} {name}", o, r)
     fams = set("+".join(seen).split("+"))
     assert {"spmm_gather_pos", "bwd_gather_pos", "sddmm_gather_pos"} <= fams, fams
+
+
+@pytest.mark.parametrize("reserve", [8, 16])
+def test_sm_reserve_grids(sp, reserve):
+    """At N > 1 the DP backward runs with SMs reserved for the concurrent
+    all_reduce (sp_set_sm_reserve: NCCL's 8 channels, or the peer-memory
+    kernel's 16 CTAs): every one-wave (stream-K) kernel then partitions its
+    tiles over fewer CTAs -- different cut items and job tables.  The results
+    must still match the oracle."""
+    cases = [(768, 3072, 2048, "bwd"), (3072, 768, 2048, "bwd"), (768, 3072, 2048, "fwd"), (4096, 4096, 256, "bwd")]
+    try:
+        sp.sp_set_sm_reserve(reserve)
+        for R, C, B, op in cases:
+            c = synth.linear_case(R, C, B, 0.05, 1.0 / C, R + B + reserve)
+            S = oracle.csr_from_mask(c["W"], c["mask"])
+            W = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))
+            X, dY = _dev(c["X"]), _dev(c["dY"])
+            if op == "fwd":
+                out = [sp.sp_linear_fwd(W, X)]
+                refs = [oracle.linear_fwd(S, c["X"], NT)]
+            else:
+                out = list(sp.sp_linear_bwd(W, X, dY))
+                refs = [oracle.linear_bwd_input(S, c["dY"], NT), oracle.linear_bwd_weight(S, c["X"], c["dY"], NT)]
+            path = sp.last_path()
+            torch.cuda.synchronize()
+            assert "_sk" in path, path  # a one-wave kernel ran
+            for o, r in zip(out, refs):
+                _ok(f"reserve {reserve} {R}x{C} B={B} {op} [{path}]", o, r)
+    finally:
+        sp.sp_set_sm_reserve(0)
