@@ -564,13 +564,18 @@ fail:
 // blocks, and within a block round-robin (snake) over the NW warps, so every
 // CTA and every warp gets a similar share of heavy and light rows (Zipf masks).
 // rowpos[r] = tiled position, rowmap[pos] = r (or -1 for unused positions).
-static void balanced_rows(const std::vector<int32_t> &ptr, int64_t rows, int RB, int NW, std::vector<int32_t> &rowpos,
-                          std::vector<int32_t> &rowmap) {
-    const int64_t nrb = (rows + RB - 1) / RB;
+// rows by length, longest first (ties by index): shared by every tiling of one row set
+static std::vector<int32_t> length_order(const std::vector<int32_t> &ptr, int64_t rows) {
     std::vector<int32_t> order(rows);
     for (int64_t r = 0; r < rows; ++r) order[r] = (int32_t)r;
     std::stable_sort(order.begin(), order.end(),
                      [&](int32_t a, int32_t b) { return ptr[a + 1] - ptr[a] > ptr[b + 1] - ptr[b]; });
+    return order;
+}
+
+static void balanced_rows(const std::vector<int32_t> &order, int64_t rows, int RB, int NW, std::vector<int32_t> &rowpos,
+                          std::vector<int32_t> &rowmap) {
+    const int64_t nrb = (rows + RB - 1) / RB;
     rowpos.assign(rows, 0);
     rowmap.assign(nrb * RB, -1);
     if (NW == 0) {  // longest first (the gather tilings: a warp per position, CTAs launched in
@@ -718,6 +723,7 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
     w->arena[2] = ar.base;
     // host-filled region first (rowpos / rowmap of every tiling, the SGD table)
     std::vector<char> hreg(hbytes, 0);
+    std::vector<int32_t> orders[3];  // length orders of the CSR rows, the CSC rows, the CSR part rows
     for (int si = 0; si < NS; ++si) {
         sp_tiling &t = *specs[si].t;
         t.in_arena = true;
@@ -727,7 +733,11 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
         t.rowmap = ar.take<int32_t>((int64_t)t.nrb * t.RB);
         std::vector<int32_t> rowpos, rowmap;
         const bool vs = specs[si].o == 0 && splitting;
-        balanced_rows(vs ? vlen_ptr : hptr[specs[si].o], pl[si].rows, t.RB, specs[si].NWbal, rowpos, rowmap);
+        // the length order of this tiling's row set (computed once per set)
+        const int oset = specs[si].o == 1 ? 1 : vs ? 2 : 0;
+        if (orders[oset].empty() && pl[si].rows > 0)
+            orders[oset] = length_order(oset == 2 ? vlen_ptr : hptr[specs[si].o], pl[si].rows);
+        balanced_rows(orders[oset], pl[si].rows, t.RB, specs[si].NWbal, rowpos, rowmap);
         memcpy(hreg.data() + o1, rowpos.data(), rowpos.size() * sizeof(int32_t));
         if (vs) {  // positions hold part rows: rowmap -> the real row, split -> the part slot
             std::vector<int32_t> sm(rowmap.size(), -1);

@@ -28,7 +28,9 @@ def t_create(W, M, n=5):
 
 recs = []
 for name, (R, C, d) in {"cfg5_W1 3072x768": (3072, 768, 0.05), "cfg5_W2 768x3072": (768, 3072, 0.05),
-                        "cfg4 4096^2 95%": (4096, 4096, 0.05), "cfg4 4096^2 80%": (4096, 4096, 0.2)}.items():
+                        "cfg4 4096^2 95%": (4096, 4096, 0.05), "cfg4 4096^2 80%": (4096, 4096, 0.2),
+                        "cfg4 4096^2 99% (+ gather tilings)": (4096, 4096, 0.01),
+                        "cfg1 256^2 90% (+ gather tilings)": (256, 256, 0.1)}.items():
     c = synth.linear_case(R, C, 4, d, 1.0 / C, 7)
     recs.append({"shape": name, "nnz": int(c["mask"].sum()),
                  "create_ms": round(t_create(torch.from_numpy(c["W"]).cuda(), torch.from_numpy(c["mask"]).cuda()), 3)})
