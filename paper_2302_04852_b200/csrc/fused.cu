@@ -722,6 +722,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
         if (eb) tma_load_1d(ents + buf * ebuf, ent + e0, eb, &full[buf]);
     };
+    pdl_wait();  // (launched as a programmatic dependent: the prologue above overlapped the previous kernel)
     if (threadIdx.x == 0)
         for (int b = 0; b < NBUF && b < ntile; ++b) issue(b, b);
     // the job reduction that follows (programmatic dependent launch) may start its
@@ -1223,7 +1224,7 @@ static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float 
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         note_path(dwonly ? "sddmm_sk" : HALF ? "bwd_fused_sk_half" : "bwd_fused_sk");
-        kern<<<(unsigned)G, TNW * 32, smem, st>>>(a, tmap);
+        launch_pdl(kern, dim3((unsigned)G), dim3(TNW * 32), smem, st, a, tmap);
     };
     if (dwonly) go(bwd_fused_sk_kernel<TRPW, TNW, false, true, NB, false, HALF>);
     else if (H) go(bwd_fused_sk_kernel<TRPW, TNW, true, false, NB, false, HALF>);
@@ -1338,7 +1339,7 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const ConvCols &cc, const float *d
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(nbuf * stage));
         note_path(dwonly ? "conv_sddmm_sk" : "conv_bwd_fused_sk");
-        kern<<<(unsigned)G, TNW * 32, nbuf * stage, st>>>(a, tmap);
+        launch_pdl(kern, dim3((unsigned)G), dim3(TNW * 32), (size_t)(nbuf * stage), st, a, tmap);
     };
     if (half) {
         if (nbuf == 3) go(bwd_fused_sk_kernel<TRPW, TNW, false, false, 3, true, true>);

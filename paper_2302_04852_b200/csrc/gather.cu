@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(256) gather_pos_kernel(const PgArgs a) {
     constexpr bool DW = MODE != 0, ACC = MODE != 2;
     const int lane = threadIdx.x & 31;
     const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    pdl_wait();     // (launched as a programmatic dependent of the previous kernel)
     pdl_trigger();  // (a split-row reduction may follow as a programmatic dependent)
     if (p >= a.npos) return;
     const int r = __ldg(a.rowmap + p);
@@ -333,17 +334,17 @@ bool launch_gather_pos(const sp_weight_s *w, int orient, int mode, int64_t B, co
     PgArgs a{B, npos, t.seg, t.ent, t.vidx, t.rowmap, parts ? t.split : nullptr, gin, rin, gate, out, dW, vpart, epi};
     const dim3 grid((unsigned)((npos + 7) / 8), mode == 0 ? (unsigned)((B + 128 * NS - 1) / (128 * NS)) : 1u);
     if (mode == 0) {
-        if (NS == 1) gather_pos_kernel<1, 0><<<grid, 256, 0, st>>>(a);
-        else gather_pos_kernel<2, 0><<<grid, 256, 0, st>>>(a);
+        if (NS == 1) launch_pdl(gather_pos_kernel<1, 0>, grid, dim3(256), 0, st, a);
+        else launch_pdl(gather_pos_kernel<2, 0>, grid, dim3(256), 0, st, a);
     }
     else if (mode == 1) {
-        if (NS == 1) gather_pos_kernel<1, 1><<<grid, 256, 0, st>>>(a);
-        else if (NS == 2) gather_pos_kernel<2, 1><<<grid, 256, 0, st>>>(a);
-        else gather_pos_kernel<4, 1><<<grid, 256, 0, st>>>(a);
+        if (NS == 1) launch_pdl(gather_pos_kernel<1, 1>, grid, dim3(256), 0, st, a);
+        else if (NS == 2) launch_pdl(gather_pos_kernel<2, 1>, grid, dim3(256), 0, st, a);
+        else launch_pdl(gather_pos_kernel<4, 1>, grid, dim3(256), 0, st, a);
     } else {
-        if (NS == 1) gather_pos_kernel<1, 2><<<grid, 256, 0, st>>>(a);
-        else if (NS == 2) gather_pos_kernel<2, 2><<<grid, 256, 0, st>>>(a);
-        else gather_pos_kernel<4, 2><<<grid, 256, 0, st>>>(a);
+        if (NS == 1) launch_pdl(gather_pos_kernel<1, 2>, grid, dim3(256), 0, st, a);
+        else if (NS == 2) launch_pdl(gather_pos_kernel<2, 2>, grid, dim3(256), 0, st, a);
+        else launch_pdl(gather_pos_kernel<4, 2>, grid, dim3(256), 0, st, a);
     }
     note_path(mode == 0 ? "spmm_gather_pos" : mode == 1 ? "bwd_gather_pos" : "sddmm_gather_pos");
     count_launches(1);

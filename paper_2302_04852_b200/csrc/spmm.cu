@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
         tma_load_2d(smem + buf * buf_sz + BT, &tmap, (int)(b0 + (CONV ? a.sh[t] : 0)), (int)k0, &full[buf]);
         if (eb) tma_load_1d(ents + buf * ebuf, ent_of(t) + e0, eb, &full[buf]);
     };
+    pdl_wait();  // (launched as a programmatic dependent: the prologue above overlapped the previous kernel)
     if (vec4 && threadIdx.x == 0) {
         issue(0, 0);
         if (ntile > 1) issue(1, 1);
@@ -312,7 +313,7 @@ void launch_cfg(const sp_tiling &t, int64_t B, const float *in, float *out, cons
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         count_launches(1);
         note_path("spmm_tiled");
-        kern<<<grid, NW * 32, smem, st>>>(a, tmap);
+        launch_pdl(kern, grid, dim3(NW * 32), smem, st, a, tmap);
         if (vpart) {
             launch_split_rows_reduce(t, vpart, B, out, gate, epi, st);
             scratch_free(vpart, st);
@@ -360,7 +361,7 @@ bool conv_spmm_vec(const sp_weight_s *w, int orient, int64_t B, const float *in,
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         count_launches(1);
         note_path("conv_spmm_tiled");
-        kern<<<grid, NW * 32, smem, st>>>(a, tmap);
+        launch_pdl(kern, grid, dim3(NW * 32), smem, st, a, tmap);
     };
     if (sent) launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_NONE, true, true>);
     else launch(spmm_tiled_kernel<VEC, RPW, NW, EPI_NONE, false, true>);

@@ -173,10 +173,12 @@ __global__ void __launch_bounds__(HY_NW * 32, 1) spmm_hyb_kernel(const HybArgs a
         tma_load_2d(smem + buf * buf_sz + HY_BT, &tmap, (int)b0, q * a.KC, &full[buf]);
         if (eb) tma_load_1d(ents + buf * ebuf, a.ent + e0, eb, &full[buf]);
     };
+    pdl_wait();  // (launched as a programmatic dependent: the prologue above overlapped the previous kernel)
     if (threadIdx.x == 0) {
         issue(0, 0);
         if (ntile > 1) issue(1, 1);
     }
+    pdl_trigger();
     // lane l <= RPW: the l-th segment bound of this warp's rows in tile q;
     // lanes 8 + i: row i's TMEM split (tmsplit)
     auto seg_bounds = [&](int q) -> int {
@@ -379,7 +381,7 @@ bool launch_spmm_hyb(const sp_weight_s *w, int orient, int64_t B, const float *i
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         count_launches(1);
         note_path("spmm_hyb");
-        kern<<<grid, HY_NW * 32, smem, st>>>(a, tmap);
+        launch_pdl(kern, grid, dim3(HY_NW * 32), smem, st, a, tmap);
         if (vpart) {
             launch_split_rows_reduce(t, vpart, B, out, gate, epi, st);
             scratch_free(vpart, st);

@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
         if (eb) tma_load_1d(ents + buf * ebuf, ent_of(id) + e0, eb, &full[buf]);
     };
+    pdl_wait();  // (launched as a programmatic dependent: the prologue above overlapped the previous kernel)
     if (threadIdx.x == 0) {
         if (ntile > 0) issue(0, 0);
         if (ntile > 1) issue(1, 1);
@@ -472,7 +473,7 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         note_path("spmm_sk");
-        kern<<<(unsigned)G, NW * 32, smem, st>>>(a, tmap);
+        launch_pdl(kern, dim3((unsigned)G), dim3(NW * 32), smem, st, a, tmap);
     };
     // (the TMEM mirror of the tiles' last rows measured slower on the linear
     // stream-K shapes: 768-row layer, B = 2048 / 4096: 83 -> 87 / 131 -> 143 us)
@@ -524,7 +525,7 @@ bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, const ConvCols &cc, c
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         note_path("conv_spmm_sk");
-        kern<<<(unsigned)G, NW * 32, smem, st>>>(a, tmap);
+        launch_pdl(kern, dim3((unsigned)G), dim3(NW * 32), smem, st, a, tmap);
     };
     if (tmm) go(spmm_sk_kernel<RPW, NW, EPI_NONE, true, true>);
     else go(spmm_sk_kernel<RPW, NW, EPI_NONE, true>);
