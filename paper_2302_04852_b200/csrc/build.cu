@@ -305,12 +305,13 @@ __global__ void til_inv_kernel(int64_t cap, const int32_t *__restrict__ vidx, in
 
 // managed SGD: thread per CSR slot, new value to vals and to every tiling
 __global__ void weight_sgd_kernel(int64_t nnz, float *__restrict__ vals, const float *__restrict__ dW, float lr,
-                                  const SgdRef *__restrict__ tab, int ntab) {
+                                  const SgdRef *__restrict__ tab, int ntab, uint32_t mask) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= nnz) return;
     const float v = fmaf(-lr, dW[j], vals[j]);  // the same rounding as sp_sgd
     vals[j] = v;
-    for (int k = 0; k < ntab; ++k) tab[k].ent[tab[k].inv[j]].y = __float_as_int(v);
+    for (int k = 0; k < ntab; ++k)
+        if ((mask >> k) & 1u) tab[k].ent[tab[k].inv[j]].y = __float_as_int(v);
 }
 
 // max over tiles of the tile's entry count (single block, fixed order)
@@ -777,7 +778,10 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
     {
         std::vector<SgdRef> tab;
         for (int si = 0; si < NS; ++si)
-            if (specs[si].t->inv) tab.push_back({specs[si].t->ent, specs[si].t->inv});
+            if (specs[si].t->inv) {
+                w->sgdtil[tab.size()] = specs[si].t;
+                tab.push_back({specs[si].t->ent, specs[si].t->inv});
+            }
         w->nsgd = (int)tab.size();
         memcpy(hreg.data() + otab, tab.data(), tab.size() * sizeof(SgdRef));
     }
@@ -910,26 +914,34 @@ void free_tilings(sp_weight_s *w) {
 }
 
 void refresh_if_stale(const sp_weight_s *w, const sp_tiling &t, cudaStream_t st) {
+    t.used = true;
     if (w->managed && t.fresh == w->version) return;
     launch_refresh(t, w->vals, w->nnz, st);
     t.fresh = w->version;
 }
 
 void launch_weight_sgd(sp_weight_s *w, const float *dW, float lr, cudaStream_t st) {
+    // the new values go to vals and to the tilings the products have read since the
+    // last update (a training step uses 2 of the 7-9); the others fall behind and are
+    // refreshed from vals at their next use (refresh_if_stale)
+    uint32_t mask = 0;
+    for (int k = 0; k < w->nsgd && k < 32; ++k) {
+#ifndef SP_SGD_ALL
+        if (w->sgdtil[k]->used && w->sgdtil[k]->fresh == w->version) mask |= 1u << k;
+#else
+        mask |= 1u << k;
+#endif
+    }
     if (w->nnz > 0) {
         count_launches(1);
         weight_sgd_kernel<<<(unsigned)((w->nnz + 255) / 256), 256, 0, st>>>(w->nnz, w->vals, dW, lr, w->sgdtab,
-                                                                            w->nsgd);
+                                                                            w->nsgd, mask);
     }
-    ++w->version;  // vals changed; the tilings in the table hold the new values
-    auto mark = [&](sp_tiling &t) {
-        if (t.inv) t.fresh = w->version;
-    };
-    for (auto &o : w->til)
-        for (auto &t : o) mark(t);
-    for (auto &t : w->til_f) mark(t);
-    for (auto &t : w->til_g) mark(t);
-
+    ++w->version;  // vals changed; the updated tilings hold the new values
+    for (int k = 0; k < w->nsgd && k < 32; ++k) {
+        if ((mask >> k) & 1u) w->sgdtil[k]->fresh = w->version;
+        w->sgdtil[k]->used = false;
+    }
 }
 
 void launch_split_rows_reduce(const sp_tiling &t, const float *vpart, int64_t B, float *out, const float *gate,

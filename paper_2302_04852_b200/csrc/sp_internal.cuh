@@ -79,6 +79,7 @@ struct sp_tiling {
     // slot in this tiling; `fresh` = the handle version whose values ent holds
     int32_t *inv;      // [nnz]
     mutable uint64_t fresh;
+    mutable bool used;  // a product read this tiling's weights since the last sp_weight_sgd
     // CSC tilings (fused backward): per (row block, warp of RPWg rows), the prefix
     // over column blocks of the warp's entry groups, gpre[g][(rb*NWg + w)*(nkb+1) + k]
     // = sum over column blocks < k of ceil(segment length / (4 << g)) -- the TMEM
@@ -154,6 +155,7 @@ struct sp_weight_s {
     uint64_t version;
     int nsgd;
     SgdRef *sgdtab;  // device [nsgd]: every built (non-tap) tiling
+    sp_tiling *sgdtil[16];  // host: the tiling of each sgdtab entry
 };
 
 // The gather tilings are built for masks at most this dense, or this small.
