@@ -264,9 +264,17 @@ sp_status sp_weight_set_managed(sp_weight_t W, int managed);
 
 /* Plain SGD on the kept weights of a handle, vals[j] -= lr * dW[j] (the same
  * rounding as sp_sgd), also writing each new value into the handle's tiled
- * copies (one kernel).  dW: device [nnz] in CSR slot order.  Enqueued on
- * `stream`; the caller keeps dW alive until it completes. */
+ * copies that products have read since the previous update (one kernel; the
+ * others are refreshed from vals at their next use).  dW: device [nnz] in
+ * CSR slot order.  Enqueued on `stream`; the caller keeps dW alive until it
+ * completes. */
 sp_status sp_weight_sgd(sp_weight_t W, const float *dW, float lr, sp_stream_t stream);
+
+/* sp_weight_sgd for n handles in ONE kernel (a model's optimizer step):
+ * Ws[i] updated with dWs[i] (host arrays of n handles / device pointers),
+ * 1 <= n <= SP_SGD_BATCH_MAX.  The same results as n sp_weight_sgd calls. */
+#define SP_SGD_BATCH_MAX 64
+sp_status sp_weights_sgd(const sp_weight_t *Ws, const float *const *dWs, int32_t n, float lr, sp_stream_t stream);
 
 /* Thread-local message for the last non-OK status on this thread. */
 const char *sp_last_error(void);

@@ -432,4 +432,17 @@ sp_status sp_weight_sgd(sp_weight_t w, const float *dW, float lr, sp_stream_t st
     return check_launch("sp_weight_sgd");
 }
 
+sp_status sp_weights_sgd(const sp_weight_t *Ws, const float *const *dWs, int32_t n, float lr, sp_stream_t stream) {
+    if (!Ws || !dWs) return fail(SP_ERR_NULL, "sp_weights_sgd: NULL array");
+    if (n < 1 || n > SP_SGD_BATCH_MAX) return fail(SP_ERR_SHAPE, "sp_weights_sgd: need 1 <= n <= SP_SGD_BATCH_MAX");
+    for (int i = 0; i < n; ++i) {
+        SP_CHECK_HANDLE(Ws[i], "sp_weights_sgd");
+        if (!dWs[i] && Ws[i]->nnz > 0) return fail(SP_ERR_NULL, "sp_weights_sgd: NULL dW");
+        for (int k = 0; k < i; ++k)
+            if (Ws[k] == Ws[i]) return fail(SP_ERR_SHAPE, "sp_weights_sgd: a handle appears twice");
+    }
+    launch_weights_sgd(Ws, dWs, n, lr, S(stream));
+    return check_launch("sp_weights_sgd");
+}
+
 }  // extern "C"

@@ -920,10 +920,8 @@ void refresh_if_stale(const sp_weight_s *w, const sp_tiling &t, cudaStream_t st)
     t.fresh = w->version;
 }
 
-void launch_weight_sgd(sp_weight_s *w, const float *dW, float lr, cudaStream_t st) {
-    // the new values go to vals and to the tilings the products have read since the
-    // last update (a training step uses 2 of the 7-9); the others fall behind and are
-    // refreshed from vals at their next use (refresh_if_stale)
+// the tilings of sgdtab that get the new values (those read since the last update)
+static uint32_t sgd_mask(const sp_weight_s *w) {
     uint32_t mask = 0;
     for (int k = 0; k < w->nsgd && k < 32; ++k) {
 #ifndef SP_SGD_ALL
@@ -932,16 +930,74 @@ void launch_weight_sgd(sp_weight_s *w, const float *dW, float lr, cudaStream_t s
         mask |= 1u << k;
 #endif
     }
-    if (w->nnz > 0) {
-        count_launches(1);
-        weight_sgd_kernel<<<(unsigned)((w->nnz + 255) / 256), 256, 0, st>>>(w->nnz, w->vals, dW, lr, w->sgdtab,
-                                                                            w->nsgd, mask);
-    }
+    return mask;
+}
+static void sgd_mark(sp_weight_s *w, uint32_t mask) {
     ++w->version;  // vals changed; the updated tilings hold the new values
     for (int k = 0; k < w->nsgd && k < 32; ++k) {
         if ((mask >> k) & 1u) w->sgdtil[k]->fresh = w->version;
         w->sgdtil[k]->used = false;
     }
+}
+
+// one kernel for many handles: grid over the concatenated slots
+struct SgdBatch {
+    int n;
+    float lr;
+    int64_t off[SP_SGD_BATCH_MAX + 1];
+    float *vals[SP_SGD_BATCH_MAX];
+    const float *dW[SP_SGD_BATCH_MAX];
+    const SgdRef *tab[SP_SGD_BATCH_MAX];
+    int ntab[SP_SGD_BATCH_MAX];
+    uint32_t mask[SP_SGD_BATCH_MAX];
+};
+__global__ void weights_sgd_kernel(const __grid_constant__ SgdBatch b) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= b.off[b.n]) return;
+    int lo = 0, hi = b.n;  // handle i with off[i] <= g < off[i+1]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (b.off[mid] <= g) lo = mid;
+        else hi = mid;
+    }
+    const int64_t j = g - b.off[lo];
+    const float v = fmaf(-b.lr, b.dW[lo][j], b.vals[lo][j]);  // the same rounding as sp_sgd
+    b.vals[lo][j] = v;
+    const SgdRef *tab = b.tab[lo];
+    for (int k = 0; k < b.ntab[lo]; ++k)
+        if ((b.mask[lo] >> k) & 1u) tab[k].ent[tab[k].inv[j]].y = __float_as_int(v);
+}
+
+void launch_weights_sgd(sp_weight_s *const *ws, const float *const *dWs, int n, float lr, cudaStream_t st) {
+    SgdBatch b{};
+    b.n = n;
+    b.lr = lr;
+    for (int i = 0; i < n; ++i) {
+        b.off[i + 1] = b.off[i] + ws[i]->nnz;
+        b.vals[i] = ws[i]->vals;
+        b.dW[i] = dWs[i];
+        b.tab[i] = ws[i]->sgdtab;
+        b.ntab[i] = ws[i]->nsgd;
+        b.mask[i] = sgd_mask(ws[i]);
+    }
+    if (b.off[n] > 0) {
+        count_launches(1);
+        weights_sgd_kernel<<<(unsigned)((b.off[n] + 255) / 256), 256, 0, st>>>(b);
+    }
+    for (int i = 0; i < n; ++i) sgd_mark(ws[i], b.mask[i]);
+}
+
+void launch_weight_sgd(sp_weight_s *w, const float *dW, float lr, cudaStream_t st) {
+    // the new values go to vals and to the tilings the products have read since the
+    // last update (a training step uses 2 of the 7-9); the others fall behind and are
+    // refreshed from vals at their next use (refresh_if_stale)
+    const uint32_t mask = sgd_mask(w);
+    if (w->nnz > 0) {
+        count_launches(1);
+        weight_sgd_kernel<<<(unsigned)((w->nnz + 255) / 256), 256, 0, st>>>(w->nnz, w->vals, dW, lr, w->sgdtab,
+                                                                            w->nsgd, mask);
+    }
+    sgd_mark(w, mask);
 }
 
 void launch_split_rows_reduce(const sp_tiling &t, const float *vpart, int64_t B, float *out, const float *gate,

@@ -64,6 +64,10 @@ class CudaOps:
         """SGD of a managed handle: vals and its tiled copies in one kernel."""
         self.sp.sp_weight_sgd(W, dW, lr)
 
+    def sgd_weights(self, Ws, dWs, lr):
+        """SGD of every managed handle of the model in ONE kernel."""
+        self.sp.sp_weights_sgd(Ws, dWs, lr)
+
     def sm_reserve(self, n):
         """One-wave kernels leave n SMs to the concurrent all_reduce."""
         self.sp.sp_set_sm_reserve(n)
@@ -276,6 +280,9 @@ class SparseMLP:
                     w.wait()
 
     def sgd(self, lr: float):
+        if hasattr(self.ops, "sgd_weights"):
+            self.ops.sgd_weights([W for pair in self.W for W in pair], [d for pair in self.dW for d in pair], lr)
+            return
         for (W1, W2), (d1, d2) in zip(self.W, self.dW):
             if hasattr(self.ops, "sgd_weight"):
                 self.ops.sgd_weight(W1, d1, lr)

@@ -33,7 +33,7 @@ EXPORTS = [
     "sp_conv2d_bwd", "sp_set_sm_reserve", "sp_last_path",
     "sp_conv2d_fwd_nchw", "sp_conv2d_bwd_input_nchw", "sp_conv2d_bwd_weight_nchw", "sp_conv2d_bwd_nchw",
     "sp_comm_create", "sp_comm_open", "sp_comm_buffer", "sp_comm_allreduce", "sp_comm_ctas", "sp_comm_destroy",
-    "sp_comm_create_local", "sp_comm_local_buffer", "sp_comm_allreduce_as",
+    "sp_comm_create_local", "sp_comm_local_buffer", "sp_comm_allreduce_as", "sp_weights_sgd",
 ]
 
 
@@ -93,6 +93,7 @@ def lib() -> ct.CDLL:
             "sp_conv2d_bwd_input_nchw": (st, [vp, ct.POINTER(sp_conv_geom), vp, vp, vp]),
             "sp_conv2d_bwd_weight_nchw": (st, [vp, ct.POINTER(sp_conv_geom), vp, vp, vp, vp]),
             "sp_conv2d_bwd_nchw": (st, [vp, ct.POINTER(sp_conv_geom), vp, vp, vp, vp, vp]),
+            "sp_weights_sgd": (st, [ct.POINTER(vp), ct.POINTER(vp), ct.c_int32, ct.c_float, vp]),
             "sp_comm_create": (st, [ct.c_int32, ct.c_int32, i64, ct.POINTER(vp), vp]),
             "sp_comm_open": (st, [vp, vp]),
             "sp_comm_buffer": (vp, [vp]),
@@ -515,6 +516,18 @@ def sp_weight_sgd(W: SparseWeight, dW: torch.Tensor, lr: float, stream=None):
     _chk_nnz(W, dW)
     _check(lib().sp_weight_sgd(W.handle, _dev(dW, torch.float32, "dW") if n else None, ct.c_float(lr),
                                _stream(stream)))
+
+
+def sp_weights_sgd(Ws, dWs, lr: float, stream=None):
+    """sp_weight_sgd for many handles in one kernel (a model's optimizer step)."""
+    Ws, dWs = list(Ws), list(dWs)
+    if len(Ws) != len(dWs):
+        raise ValueError("sp_weights_sgd: one dW per handle")
+    for W, d in zip(Ws, dWs):
+        _chk_nnz(W, d)
+    hs = (ct.c_void_p * len(Ws))(*[W.handle.value for W in Ws])
+    ds = (ct.c_void_p * len(dWs))(*[_dev(d, torch.float32, "dW") if W.nnz > 0 else None for W, d in zip(Ws, dWs)])
+    _check(lib().sp_weights_sgd(hs, ds, len(Ws), ct.c_float(lr), _stream(stream)))
 
 
 def sp_sgd(vals: torch.Tensor, dW: torch.Tensor, lr: float, stream=None):

@@ -214,3 +214,38 @@ def test_graph_captured_step_matches_eager():
     for (A1, A2), (B1, B2) in zip(a.W, b.W):
         assert torch.equal(A1.vals, B1.vals) and torch.equal(A2.vals, B2.vals)
     assert torch.equal(a.dW_flat, b.dW_flat)
+
+
+def test_batched_sgd_matches_per_handle():
+    """sp_weights_sgd (one kernel for all of a model's handles) gives bitwise the
+    vals and products of one sp_weight_sgd per handle, including the lazily
+    refreshed tilings (a product after the update reads a tiling the step did
+    not use)."""
+    from paper_2302_04852_b200 import sparseprop as sp
+    dev = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+    cases = [synth.linear_case(3072, 768, 256, 0.05, 1.0 / 768, 61), synth.linear_case(768, 3072, 256, 0.05, 1.0 / 3072, 62),
+             synth.linear_case(500, 300, 128, 0.1, 1.0 / 300, 63)]
+    A = [sp.sp_weight_create(dev(c["W"]), dev(c["mask"])) for c in cases]
+    Bh = [sp.sp_weight_create(dev(c["W"]), dev(c["mask"])) for c in cases]
+    for W in A + Bh:
+        sp.sp_weight_set_managed(W, True)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    for step in range(3):
+        for c, Wa, Wb in zip(cases, A, Bh):  # a product per handle (marks the tilings it reads)
+            X = dev(c["X"])
+            assert torch.equal(sp.sp_linear_fwd(Wa, X), sp.sp_linear_fwd(Wb, X)), step
+        dWs = [torch.randn(W.nnz, device="cuda", generator=g) for W in A]
+        sp.sp_weights_sgd(A, dWs, 1e-2)
+        for Wb, d in zip(Bh, dWs):
+            sp.sp_weight_sgd(Wb, d, 1e-2)
+    for c, Wa, Wb in zip(cases, A, Bh):
+        assert torch.equal(Wa.vals, Wb.vals)
+        X, dY = dev(c["X"]), dev(c["dY"])
+        for f in (lambda W: sp.sp_linear_fwd(W, X), lambda W: sp.sp_linear_bwd_input(W, dY),
+                  lambda W: sp.sp_linear_bwd(W, X, dY)[0]):
+            assert torch.equal(f(Wa), f(Wb))
+    torch.cuda.synchronize()
+    c = cases[0]
+    S = oracle.csr_from_mask(c["W"], c["mask"]).with_vals(_np(A[0].vals))
+    _ok("batched-SGD handle bwd_input vs oracle", _np(sp.sp_linear_bwd_input(A[0], dev(c["dY"]))),
+        oracle.linear_bwd_input(S, c["dY"], NT))
