@@ -33,7 +33,7 @@
 namespace sp {
 namespace {
 
-constexpr int kCommCtas = 16;     // CTAs per call (SMs to reserve while it overlaps compute)
+constexpr int kCommCtas = 8;      // CTAs per call (SMs to reserve while it overlaps compute; NCCL's channel count)
 constexpr int kCommThreads = 512;
 constexpr uint32_t kCommMagic = 0x5350434dU;  // "SPCM"
 
