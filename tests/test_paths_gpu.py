@@ -221,7 +221,7 @@ def test_gather_pos_random_sweep(sp):
 def test_sm_reserve_grids(sp, reserve):
     """At N > 1 the DP backward runs with SMs reserved for the concurrent
     all_reduce (sp_set_sm_reserve: NCCL's 8 channels, or the peer-memory
-    kernel's 16 CTAs): every one-wave (stream-K) kernel then partitions its
+    kernel's 8 CTAs; 16 as a harder case): every one-wave (stream-K) kernel then partitions its
     tiles over fewer CTAs -- different cut items and job tables.  The results
     must still match the oracle."""
     cases = [(768, 3072, 2048, "bwd"), (3072, 768, 2048, "bwd"), (768, 3072, 2048, "fwd"), (4096, 4096, 256, "bwd")]
