@@ -907,8 +907,7 @@ void free_tilings(sp_weight_s *w) {
     for (auto &t : w->til_f) fr(t);
     for (auto &t : w->til_g) fr(t);
 
-    if (w->tapdev) cudaFree(w->tapdev);
-    w->tapdev = nullptr;
+    w->tapdev = nullptr;  // lives in the tap arena (arena[3], freed by free_weight)
     w->sgdtab = nullptr;  // lives in the tiling arena
     w->nsgd = 0;
 }

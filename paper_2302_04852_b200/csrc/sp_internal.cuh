@@ -111,7 +111,7 @@ struct sp_weight_s {
     // device arenas (one cudaMalloc each, sp_weight_create's allocation cost):
     // [0] row_ptr + col_ptr, [1] the nnz-sized index arrays + chunk_ptr,
     // [2] every linear tiling + the managed-SGD table
-    void *arena[3];
+    void *arena[4];  // [3]: the conv tap tilings (build_conv_taps)
     int64_t R, C, nnz;
     // CSR (P153-P154): row_ptr[R+1], col_idx[nnz], vals[nnz]
     int32_t *row_ptr;
