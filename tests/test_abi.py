@@ -72,6 +72,12 @@ def test_argument_validation_without_gpu(L):
     assert L.sp_comm_allreduce(None, 0, 4, None) == 6
     assert L.sp_comm_open(None, rec) == 6
     assert L.sp_comm_ctas() >= 1
+    assert L.sp_weights_sgd(None, None, 1, ct.c_float(0.1), None) == 1           # SP_ERR_NULL
+    hs = (ct.c_void_p * 1)(None)
+    ds = (ct.c_void_p * 1)(None)
+    assert L.sp_weights_sgd(hs, ds, 0, ct.c_float(0.1), None) == 2                # n < 1
+    assert L.sp_weights_sgd(hs, ds, 65, ct.c_float(0.1), None) == 2               # n > SP_SGD_BATCH_MAX
+    assert L.sp_weights_sgd(hs, ds, 1, ct.c_float(0.1), None) == 6                # a NULL handle
     assert "sm_100a" in sp.version()
 
 
