@@ -70,7 +70,6 @@ __global__ void __launch_bounds__(NW * 32, 1)
     constexpr int VEC = 4;
     constexpr int BT = 32 * VEC;
     constexpr int RB = NW * RPW;
-    constexpr int SH = 0;
     // [2][zero row + KC rows][BT] floats, then [2][cap+2] int2.  The zero row in
     // front of each tile is what padding entries (offset -one row) read.
     extern __shared__ __align__(128) float smem[];
@@ -597,7 +596,6 @@ __device__ __forceinline__ float reduce4h(const float (&p)[4], int lane) {
 // the registers that 32 resident warps need.  RPW = 4 (128-row blocks) for
 // linear layers: 32 dW columns (256 groups); RPW = 2 (64-row blocks) for the
 // fused conv backward: 48 columns.  DWONLY drops the dX columns.
-constexpr int kSkDwCols = 32;  // dW columns of the linear (RPW = 4, 32 warps) plan
 // TMEM columns per warp: the NW/4 warps of a lane quarter share its 512 columns
 template <int NW>
 constexpr int sk_cpw() { return (512 / (NW / 4)) & ~7; }

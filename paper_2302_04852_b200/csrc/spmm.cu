@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
                 for (int v = 0; v < VEC; ++v) dst[v] = acc[i][v];
         }
         return;
-    }
+    } else {
     // Epilogue: ReLU / ReLU' gate fused; each element written once.
 #pragma unroll
     for (int i = 0; i < RPW; ++i) {
@@ -284,6 +284,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
                 if (bl + v < B) dst[v] = o[v];
         }
     }
+    }  // (not CONV)
 }
 
 // The stream-K SpMM (spmm_sk.cu) runs when the per-item grid is short (< 2

@@ -256,12 +256,12 @@ __global__ void __launch_bounds__(NW * 32, 1)
             }
             __syncwarp();
         }
-        int ea, e1t;
 #ifndef SP_SPMM_EA_LDG
         // (a shared-memory read instead of two dependent global ones: stream-K SpMM
         // -3 to -5 %; the split-source kernel measured slower with it and keeps the loads)
-        ea = tile_ea[buf];
+        const int ea = tile_ea[buf];
 #else
+        int ea, e1t;
         entry_range(id, ea, e1t);
 #endif
         // 32-bit shared-window bases pinned in registers (see pin_u32)
