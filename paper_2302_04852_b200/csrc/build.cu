@@ -1025,8 +1025,12 @@ __global__ void til_refresh_taps_kernel(const TapDev *__restrict__ taps, const f
 }
 
 void launch_refresh_taps(const sp_weight_s *w, int orient, int ntap, cudaStream_t st) {
+    // a managed handle's vals change only through sp_weight_sgd (which bumps the
+    // version): the tap tilings refresh once per version, like the linear tilings
+    if (w->managed && w->tap_fresh[orient] == w->version) return;
     count_launches(1);
     til_refresh_taps_kernel<<<dim3(64, ntap), 256, 0, st>>>(w->tapdev + orient * kMaxTaps, w->vals);
+    w->tap_fresh[orient] = w->version;
 }
 
 void launch_gather_dense(const sp_weight_s *w, const float *dense, float *nz, cudaStream_t st) {

@@ -147,6 +147,7 @@ struct sp_weight_s {
     sp_tiling tapf[kMaxTaps];
     int64_t tapf_groups;
     int64_t tapf_groups8;  // the same in groups of 8 (half-warp fused conv backward)
+    mutable uint64_t tap_fresh[3];  // handle version whose vals the tap tilings of each orientation hold (0: never)
     struct TapDev *tapdev;  // device copy of the tap tilings' pointers [3][kMaxTaps]: orient 0, 1, fused
     // managed mode (sp_weight_set_managed): vals change only through
     // sp_weight_sgd, which rewrites the tilings' weights too, so products skip

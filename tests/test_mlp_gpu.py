@@ -249,3 +249,30 @@ def test_batched_sgd_matches_per_handle():
     S = oracle.csr_from_mask(c["W"], c["mask"]).with_vals(_np(A[0].vals))
     _ok("batched-SGD handle bwd_input vs oracle", _np(sp.sp_linear_bwd_input(A[0], dev(c["dY"]))),
         oracle.linear_bwd_input(S, c["dY"], NT))
+
+
+def test_managed_conv_handle_refreshes_taps_per_version():
+    """A managed conv handle refreshes its tap tilings once per vals version: the
+    products after sp_weight_sgd (and after an external write + set_managed)
+    match an unmanaged handle holding the same vals."""
+    from paper_2302_04852_b200 import sparseprop as sp
+    c = synth.conv_case(OC=48, IC=32, H=10, W=10, KH=3, KW=3, pad=1, B=8, density=0.2, wvar=2.0 / 288, seed=71)
+    dev = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+    Wm = sp.sp_weight_create(dev(c["W"]), dev(c["mask"]))
+    Wu = sp.sp_weight_create(dev(c["W"]), dev(c["mask"]))
+    sp.sp_weight_set_managed(Wm, True)
+    g = sp.conv_geom(Wm, c["B"], c["H"], c["Wd"], c["pad"])
+    X, dY = dev(c["X"]), dev(c["dY"])
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    for step in range(3):
+        for f in (lambda W: sp.sp_conv2d_fwd(W, g, X), lambda W: sp.sp_conv2d_bwd_input(W, g, dY),
+                  lambda W: sp.sp_conv2d_bwd(W, g, X, dY)[0]):
+            assert torch.equal(f(Wm), f(Wu)), step
+            assert torch.equal(f(Wm), f(Wu)), step  # (second call: no refresh on the managed handle)
+        d = torch.randn(Wm.nnz, device="cuda", generator=gen)
+        sp.sp_weight_sgd(Wm, d, 1e-2)
+        sp.sp_sgd(Wu.vals, d, 1e-2)
+    Wm.vals.mul_(0.5)
+    Wu.vals.mul_(0.5)
+    sp.sp_weight_set_managed(Wm, True)
+    assert torch.equal(sp.sp_conv2d_fwd(Wm, g, X), sp.sp_conv2d_fwd(Wu, g, X))
