@@ -854,14 +854,14 @@ __global__ void __launch_bounds__(NW * 32, 1)
         if (q + 1 < ntile) sgn = seg_bounds(nid);
         mbar_wait(&full[buf], (q / NBUF) & 1);
         if (q == 0) FUSED_TS(1);
-        // the tile's first staged entry: from its issuer through shared memory (linear
-        // layers: cfg5 fused backward -1.5 %), from the tiling for conv (measured +0.8 %)
+        // the tile's first staged entry: from its issuer through shared memory (cfg5
+        // fused backward -1.5 %, cfg3 -2 us)
         int ea, e1t;
 #ifndef SP_FUSED_EA_LDG
-        if constexpr (!CONV) ea = tile_ea[buf];
-        else
+        ea = tile_ea[buf];
+#else
+        entry_range(id, ea, e1t);
 #endif
-            entry_range(id, ea, e1t);
         const char *tb = reinterpret_cast<const char *>(smem + buf * buf_sz + BT + lane * VEC);
         const int2 *es = ents + buf * ebuf - ea;
         auto flush = [&](int col) {
@@ -1312,7 +1312,11 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const ConvCols &cc, const float *d
     }
     const int cap = (mx + (half ? 8 : 2) + 3) & ~3;  // HALF reads entry pairs past a segment (masked)
     const size_t stage = (size_t)(t0.KC + 1) * BT * sizeof(float) + (size_t)(cap + 2) * sizeof(int2);
+#ifdef SP_CONV_NBUF3
     const int nbuf = 3 * stage <= (size_t)(226 * 1024) ? 3 : 2;
+#else
+    const int nbuf = 2;  // (three buffers when they fit measured 2-4 us slower on cfg3)
+#endif
     if (nbuf * stage > (size_t)(226 * 1024)) return false;
     CUtensorMap tmap{};
     if (!make_tmap_conv(&tmap, dY, cc, t0.inner, OH, OW, t0.KC)) return false;
