@@ -912,6 +912,22 @@ void free_tilings(sp_weight_s *w) {
     w->nsgd = 0;
 }
 
+__global__ void zero_i32_kernel(int *p, int64_t n) {
+    pdl_wait();  // (the buffer may have been another kernel's scratch a moment ago)
+    pdl_trigger();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = 0;
+}
+
+void launch_zero_i32(int *p, int64_t n, cudaStream_t st) {
+#ifdef SP_ZERO_MEMSET
+    cudaMemsetAsync(p, 0, (size_t)n * sizeof(int), st);
+#else
+    if (n <= 0) return;
+    count_launches(1);
+    launch_pdl(zero_i32_kernel, dim3((unsigned)std::min<int64_t>(148, (n + 255) / 256)), dim3(256), 0, st, p, n);
+#endif
+}
+
 void refresh_if_stale(const sp_weight_s *w, const sp_tiling &t, cudaStream_t st) {
     t.used = true;
     if (w->managed && t.fresh == w->version) return;

@@ -1214,7 +1214,7 @@ static bool launch_sk_rpw(const sp_weight_s *w, const sp_tiling &t, const float 
         scratch_free(part, st);
         return false;
     }
-    if (!dwonly) cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
+    if (!dwonly) launch_zero_i32(tickets, nitems, st);
     refresh_if_stale(w, t, st);  // CSC-tiled weights from vals (through perm)
     FusedArgs a{t.rows, t.inner, B, t.KC, t.nkb, 0, cap, t.seg, t.ent, t.vidx, X, dY, H, dX, part, t.npad,
                 0, t.rowmap, slices, t.nrb, dxpart, tickets, B, 1, nullptr, {}, {},
@@ -1333,7 +1333,7 @@ bool launch_conv_bwd_sk(const sp_weight_s *w, const ConvCols &cc, const float *d
         scratch_free(part, st);
         return false;
     }
-    if (!dwonly) cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
+    if (!dwonly) launch_zero_i32(tickets, nitems, st);
     launch_refresh_taps(w, 2, ntap, st);  // fused tap tilings' weights from vals
     FusedArgs a{t0.rows, t0.inner, cc.B, t0.KC, t0.nkb, 0, cap, nullptr, nullptr, nullptr, X, dY, nullptr, dX, part,
                 tot, 0, nullptr, slices, t0.nrb, dxpart, tickets, xrow, ntap, w->tapdev + 2 * kMaxTaps, {}, cc, nullptr};

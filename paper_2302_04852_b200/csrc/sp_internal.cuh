@@ -277,6 +277,9 @@ void free_weight(sp_weight_s *w);
 void launch_refresh(const sp_tiling &t, const float *vals, int64_t nnz, cudaStream_t st);
 // the same unless the handle is managed and the tiling already holds its version
 void refresh_if_stale(const sp_weight_s *w, const sp_tiling &t, cudaStream_t st);
+// zero n ints on `st` (a programmatic-dependent kernel instead of a memset node:
+// the launch chain of the kernels that follow keeps its prologue overlap)
+void launch_zero_i32(int *p, int64_t n, cudaStream_t st);
 void launch_weights_sgd(sp_weight_s *const *ws, const float *const *dWs, int n, float lr, cudaStream_t st);
 // managed SGD: vals[j] -= lr dW[j] and the new value written into every tiling
 void launch_weight_sgd(sp_weight_s *w, const float *dW, float lr, cudaStream_t st);

@@ -463,7 +463,7 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
     if (scratch_alloc((void **)&part, (size_t)G * 2 * 128 * BT * sizeof(float), st) != cudaSuccess ||
         scratch_alloc((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)
         return false;
-    cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
+    launch_zero_i32(tickets, nitems, st);
     refresh_if_stale(w, t, st);
     float *vpart = nullptr;
     if (t.split && scratch_alloc((void **)&vpart, (size_t)t.nparts * B * sizeof(float), st) != cudaSuccess)
@@ -515,7 +515,7 @@ bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, const ConvCols &cc, c
     if (scratch_alloc((void **)&part, (size_t)G * 2 * 128 * BT * sizeof(float), st) != cudaSuccess ||
         scratch_alloc((void **)&tickets, (size_t)nitems * sizeof(int), st) != cudaSuccess)
         return false;
-    cudaMemsetAsync(tickets, 0, (size_t)nitems * sizeof(int), st);
+    launch_zero_i32(tickets, nitems, st);
     SkArgs a{t0.rows, cc.B, nslice, t0.KC, t0.nkb, t0.nrb, cap, nullptr, nullptr, out, nullptr, nullptr, nullptr,
              nullptr, nullptr, part, tickets, ntap, w->tapdev + orient * kMaxTaps, cc};
     // conv tap tiles have 128 rows: the TMEM mirror covers half of them (cfg3
