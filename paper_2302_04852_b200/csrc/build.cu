@@ -778,7 +778,7 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
     {
         std::vector<SgdRef> tab;
         for (int si = 0; si < NS; ++si)
-            if (specs[si].t->inv) {
+            if (specs[si].t->inv && tab.size() < sizeof(w->sgdtil) / sizeof(w->sgdtil[0])) {
                 w->sgdtil[tab.size()] = specs[si].t;
                 tab.push_back({specs[si].t->ent, specs[si].t->inv});
             }
