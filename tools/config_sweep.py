@@ -15,6 +15,13 @@ Effective FLOPs: 3 x 2*nnz*B (conv: exact valid taps).  Roofline
 time: sum over the 3 products of max(FLOPs / FP32 peak, algorithmic bytes /
 HBM).  `path` is sp_last_path() of each call (which kernels
 ran).
+
+Context column (not the library; SURVEY §8(d) "dense counterpart", the
+paper's baseline P363-P366): the same layer dense in fp32 with TF32 off --
+cuBLAS SGEMMs Y = W X, dX = W^T dY, dW = dY X^T (conv: cuDNN NCHW forward and
+convolution_backward) on the masked weights, timed the same way;
+`t_dense_us` and `speedup_vs_dense` = t_dense / t (the paper's Fig. 3 / 4
+quantity on B200).
 """
 from __future__ import annotations
 
@@ -67,6 +74,38 @@ def graph_times(fns: dict, reps: int) -> dict:
     return {k: float(np.median(v)) for k, v in out.items()}
 
 
+class _NoTF32:
+    """fp32 dense context runs: no TF32 in cuBLAS or cuDNN."""
+
+    def __enter__(self):
+        self.s = (torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32)
+        torch.backends.cuda.matmul.allow_tf32 = False
+        torch.backends.cudnn.allow_tf32 = False
+
+    def __exit__(self, *a):
+        torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32 = self.s
+
+
+def dense_linear_us(Wm, X, dY, reps) -> float:
+    R, C = Wm.shape
+    B = X.shape[1]
+    Yd, dXd = torch.empty(R, B, device="cuda"), torch.empty(C, B, device="cuda")
+    dWd = torch.empty(R, C, device="cuda")
+    with _NoTF32():
+        t = graph_times({"fwd": lambda: torch.mm(Wm, X, out=Yd),
+                         "bwd": lambda: (torch.mm(Wm.t(), dY, out=dXd), torch.mm(dY, X.t(), out=dWd))}, reps)
+    return (t["fwd"] + t["bwd"]) * 1e3
+
+
+def dense_conv_us(Wm, Xn, dYn, pad, reps) -> float:
+    with _NoTF32():
+        t = graph_times({"fwd": lambda: torch.nn.functional.conv2d(Xn, Wm, padding=pad),
+                         "bwd": lambda: torch.ops.aten.convolution_backward(
+                             dYn, Xn, Wm, None, [1, 1], [pad, pad], [1, 1], False, [0, 0], 1, [True, True, False])},
+                        reps)
+    return (t["fwd"] + t["bwd"]) * 1e3
+
+
 def _paths(fns: dict) -> dict:
     p = {}
     for k, f in fns.items():
@@ -107,6 +146,9 @@ def linear(name, R, C, B, density, wvar, seed, kind="uniform", reps=7, peak=None
     rec["gflops"] = round(3 * fl / tt / 1e9, 1)
     rec["roofline_us"] = round(roof * 1e6, 2)
     rec["pct_roofline"] = round(100 * roof / tt, 2)
+    td = dense_linear_us(Wd * Md.to(torch.float32), X, dY, reps)
+    rec["t_dense_us"] = round(td, 2)
+    rec["speedup_vs_dense"] = round(td / rec["t_us"], 2)
     return rec
 
 
@@ -149,6 +191,13 @@ def conv(name, reps=7, peak=None, hbm=None, **cfg):
     rec["gflops_exact_taps"] = round(3 * fl / tt / 1e9, 1)
     rec["roofline_us"] = round(roof * 1e6, 2)
     rec["pct_roofline"] = round(100 * roof / tt, 2)
+    # dense context: NCHW tensors, [OC][IC][KH][KW] masked weights
+    Wn = (Wd * Md.to(torch.float32)).reshape(c["OC"], c["IC"], c["KH"], c["KW"]).contiguous()
+    Xn = X.permute(3, 0, 1, 2).contiguous()
+    dYn = dY.permute(3, 0, 1, 2).contiguous()
+    td = dense_conv_us(Wn, Xn, dYn, pad, reps)
+    rec["t_dense_us"] = round(td, 2)
+    rec["speedup_vs_dense"] = round(td / rec["t_us"], 2)
     return rec
 
 
@@ -181,7 +230,8 @@ def sweep(peak_flops: float, hbm_bps: float, reps: int = 7, quick: bool = False)
     fits = [f for f in (linearity(recs, "uniform"), linearity(recs, "zipf")) if f]
     return {"timing": "CUDA-graph replay per call, L2 flushed (256 MB write) before each, median of "
                       f"{reps}; t_us = fwd + fused bwd, managed handle (no per-product vals refresh); "
-                      "t_api_us = the same with an unmanaged handle",
+                      "t_api_us = the same with an unmanaged handle; t_dense_us = the dense fp32 layer (cuBLAS / "
+                      "cuDNN, TF32 off) fwd + bwd on the masked weights, context only",
             "instances": recs, "linearity": fits}
 
 
