@@ -188,8 +188,9 @@ def main():
     ap.add_argument("--sm-reserve", type=int, default=None,
                     help="N>1: SMs the backward's one-wave kernels leave to the all_reduce (default: 8 NCCL "
                          "channels; --comm p2p: the peer-memory kernel's CTAs)")
-    ap.add_argument("--comm", default="nccl", choices=["nccl", "p2p"],
-                    help="N>1 dW all_reduce: NCCL, or the library's peer-memory kernel (SURVEY F2)")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "p2p", "nvls"],
+                    help="N>1 dW all_reduce: NCCL, the library's peer-memory kernel, or its NVLS "
+                         "multicast kernel (SURVEY F2)")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the per-config single-layer sweep (BASELINE configs 0-3) added at N=1")
     ap.add_argument("--tokens", type=int, default=CFG["T"], help="global batch (default 16384)")
@@ -212,7 +213,7 @@ def main():
     from paper_2302_04852_b200.dp import SparseMLP
 
     if args.sm_reserve is None:
-        args.sm_reserve = sp.comm_ctas() if args.comm == "p2p" else 8
+        args.sm_reserve = sp.comm_ctas() if args.comm in ("p2p", "nvls") else 8
     if world > 1:
         # the dW all_reduce overlaps the backward: cap NCCL's CTAs (channels) and
         # leave that many SMs free in the one-wave kernels (SparseMLP sm_reserve)

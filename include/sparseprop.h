@@ -344,6 +344,41 @@ sp_status sp_comm_create_local(int32_t world, int64_t count, sp_comm_t *out);
 float *sp_comm_local_buffer(sp_comm_t c, int32_t rank);
 sp_status sp_comm_allreduce_as(sp_comm_t c, int32_t rank, int64_t offset, int64_t count, sp_stream_t stream);
 
+/* ---------------------------------------------------------------------- */
+/* NVLS dW all_reduce: NVLink SHARP multicast           */
+/* ---------------------------------------------------------------------- */
+/* The same exchange as sp_comm_* (SUM over ranks of the nnz-length dW
+ * buffer), reduced by the NVSwitch: every rank's buffer is its
+ * own physical memory bound to ONE multicast object over the ranks' GPUs;
+ * the kernel (sp_nvls_ctas() CTAs) reads each 16-byte vector of this rank's
+ * 1/world chunk once through the multicast address (multimem.ld_reduce.add:
+ * the sum of all copies) and stores the sum once (multimem.st: into every
+ * copy), between two flag barriers raised by multimem.red.release (epoch per
+ * call in device memory: graph-capturable).  Every rank ends with the same
+ * values; the addition order is the switch's.
+ * Setup (collective, every rank the same world / count), in this order:
+ *   sp_nvls_create  rank 0 creates the multicast object (world devices) and,
+ *                   for world > 1, writes an exported POSIX fd to *fd_out
+ *                   (others: -1); every rank allocates its physical memory;
+ *   carry rank 0's fd to the other ranks (SCM_RIGHTS over a Unix socket);
+ *   sp_nvls_open    ranks > 0 import it (fd); every rank adds its device;
+ *   barrier;  sp_nvls_bind (binds and maps; zeroes the buffer);  barrier.
+ * SP_ERR_CUDA when the device has no multicast support (sp_nvls_supported()
+ * == 0) or a driver call fails; the buffer and mappings are owned by the
+ * communicator (sp_nvls_destroy synchronises the device). */
+typedef struct sp_nvls_s *sp_nvls_t;
+int32_t sp_nvls_supported(void);
+sp_status sp_nvls_create(int32_t rank, int32_t world, int64_t count, sp_nvls_t *out, int32_t *fd_out);
+sp_status sp_nvls_open(sp_nvls_t c, int32_t fd);
+sp_status sp_nvls_bind(sp_nvls_t c);
+/* This rank's buffer (device, count floats; NULL before sp_nvls_bind). */
+float *sp_nvls_buffer(sp_nvls_t c);
+/* In-place SUM over all ranks of buffer[offset, offset + count) on `stream`;
+ * every rank must make the same sequence of calls. */
+sp_status sp_nvls_allreduce(sp_nvls_t c, int64_t offset, int64_t count, sp_stream_t stream);
+int32_t sp_nvls_ctas(void);
+sp_status sp_nvls_destroy(sp_nvls_t c);
+
 /* Library build string (arch, version) for provenance in bench records. */
 const char *sp_version(void);
 

@@ -17,7 +17,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr"]
-SOURCES = ["api.cu", "build.cu", "spmm.cu", "sddmm.cu", "conv.cu", "step.cu", "tmap.cu", "fused.cu", "conv_taps.cu", "gather.cu", "spmm_sk.cu", "spmm_hyb.cu", "comm.cu"]
+SOURCES = ["api.cu", "build.cu", "spmm.cu", "sddmm.cu", "conv.cu", "step.cu", "tmap.cu", "fused.cu", "conv_taps.cu", "gather.cu", "spmm_sk.cu", "spmm_hyb.cu", "comm.cu", "nvls.cu"]
 
 
 def _compile(src: str) -> tuple[str, str]:

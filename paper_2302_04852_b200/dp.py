@@ -101,6 +101,70 @@ class P2PAllReduce:
         self.comm.allreduce(lo, hi - lo, stream)
 
 
+def share_fd(group, rank: int, world: int, fd: int) -> int:
+    """Rank 0's file descriptor `fd` to every rank of `group` (SCM_RIGHTS over an
+    abstract Unix socket whose name rank 0 draws and all_gathers): returns the
+    fd (rank 0: its own; others: a new descriptor of the same open file, which
+    the caller closes).  Used to carry the NVLS multicast handle."""
+    import secrets
+    import socket
+    names = [None] * world
+    dist.all_gather_object(names, "\0sp-nvls-" + secrets.token_hex(8) if rank == 0 else None, group=group)
+    name = names[0]
+    if rank == 0:
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        srv.bind(name)
+        srv.listen(world)
+        dist.barrier(group=group)  # listening
+        for _ in range(world - 1):
+            conn, _ = srv.accept()
+            socket.send_fds(conn, [b"f"], [fd])
+            conn.close()
+        srv.close()
+        return fd
+    dist.barrier(group=group)
+    cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+    cli.connect(name)
+    _, fds, _, _ = socket.recv_fds(cli, 1, 1)
+    cli.close()
+    return fds[0]
+
+
+class NvlsAllReduce:
+    """The NVLS multicast dW all_reduce (sparseprop.NvlsComm):
+    rank 0 creates the multicast object and its fd reaches the other ranks
+    (share_fd); every rank adds its device, then binds its buffer (barriers
+    between, as the driver's protocol requires).  Same interface as
+    P2PAllReduce: the model's flat dW buffer IS this rank's multicast-bound
+    buffer.  comm_factory (tests): (rank, world, count) -> an object with .fd,
+    .open(fd), .bind(), .buffer, .allreduce(offset, count, stream)."""
+
+    def __init__(self, group, count: int, device, comm_factory=None):
+        import os
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if comm_factory is None:
+            from . import sparseprop as sp
+            comm_factory = lambda r, w, n: sp.NvlsComm(r, w, n, device)  # noqa: E731
+        self.comm = comm_factory(self.rank, self.world, count)
+        fd = share_fd(group, self.rank, self.world, self.comm.fd) if self.world > 1 else -1
+        self.comm.open(fd if self.rank > 0 else -1)
+        if self.rank > 0 and fd >= 0:
+            os.close(fd)  # (imported: the driver holds its own reference)
+        if self.world > 1:
+            dist.barrier(group=group)  # every device added before any bind
+        self.comm.bind()
+        if self.world > 1:
+            dist.barrier(group=group)
+
+    @property
+    def buffer(self):
+        return self.comm.buffer
+
+    def allreduce(self, lo: int, hi: int, stream=None):
+        self.comm.allreduce(lo, hi - lo, stream)
+
+
 class SparseMLP:
     """cfg5 model state + one training step on this rank's token shard."""
 
@@ -113,10 +177,11 @@ class SparseMLP:
         the collective's CTAs do not push part of a wave into a second one
         (match it to NCCL's channel count, NCCL_MAX_NCHANNELS; "p2p": the
         peer-memory kernel's CTA count, sparseprop.comm_ctas()).
-        comm: "nccl" (torch.distributed.all_reduce) or "p2p" (P2PAllReduce:
-        the library's peer-memory kernel over NVLink, CUDA only)."""
-        if comm not in ("nccl", "p2p"):
-            raise ValueError("comm must be 'nccl' or 'p2p'")
+        comm: "nccl" (torch.distributed.all_reduce), "p2p" (P2PAllReduce:
+        the library's peer-memory kernel over NVLink, CUDA only) or "nvls"
+        (NvlsAllReduce: the library's NVLink SHARP multicast kernel)."""
+        if comm not in ("nccl", "p2p", "nvls"):
+            raise ValueError("comm must be 'nccl', 'p2p' or 'nvls'")
         self.sm_reserve = sm_reserve
         self.comm = comm
         self.ops = ops if ops is not None else CudaOps()
@@ -139,8 +204,9 @@ class SparseMLP:
         sizes = [(W1.nnz, W2.nnz) for (W1, W2) in self.W]
         self.nnz_total = sum(a + b for a, b in sizes)
         self.p2p = None
-        if comm == "p2p" and self.world > 1:
-            self.p2p = P2PAllReduce(group, self.nnz_total, self.device, comm_factory)
+        if comm in ("p2p", "nvls") and self.world > 1:
+            cls = P2PAllReduce if comm == "p2p" else NvlsAllReduce
+            self.p2p = cls(group, self.nnz_total, self.device, comm_factory)
             self.dW_flat = self.p2p.buffer[:self.nnz_total]
         else:
             self.dW_flat = torch.zeros(self.nnz_total, **f32)
@@ -170,7 +236,7 @@ class SparseMLP:
         self.is_cuda = self.device.type == "cuda"
         self.comm_stream = torch.cuda.Stream(device=self.device) if (self.is_cuda and self.world > 1) else None
         if self.p2p is not None and self.comm_stream is None:
-            raise ValueError("comm='p2p' needs CUDA tensors")
+            raise ValueError(f"comm='{comm}' needs CUDA tensors")
 
     # ------------------------------------------------------------------
     def set_batch(self, X0: torch.Tensor, target: torch.Tensor, non_blocking: bool = True):

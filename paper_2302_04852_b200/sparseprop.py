@@ -34,6 +34,8 @@ EXPORTS = [
     "sp_conv2d_fwd_nchw", "sp_conv2d_bwd_input_nchw", "sp_conv2d_bwd_weight_nchw", "sp_conv2d_bwd_nchw",
     "sp_comm_create", "sp_comm_open", "sp_comm_buffer", "sp_comm_allreduce", "sp_comm_ctas", "sp_comm_destroy",
     "sp_comm_create_local", "sp_comm_local_buffer", "sp_comm_allreduce_as", "sp_weights_sgd",
+    "sp_nvls_supported", "sp_nvls_create", "sp_nvls_open", "sp_nvls_bind", "sp_nvls_buffer", "sp_nvls_allreduce",
+    "sp_nvls_ctas", "sp_nvls_destroy",
 ]
 
 
@@ -103,6 +105,14 @@ def lib() -> ct.CDLL:
             "sp_comm_create_local": (st, [ct.c_int32, i64, ct.POINTER(vp)]),
             "sp_comm_local_buffer": (vp, [vp, ct.c_int32]),
             "sp_comm_allreduce_as": (st, [vp, ct.c_int32, i64, i64, vp]),
+            "sp_nvls_supported": (ct.c_int32, []),
+            "sp_nvls_create": (st, [ct.c_int32, ct.c_int32, i64, ct.POINTER(vp), ct.POINTER(ct.c_int32)]),
+            "sp_nvls_open": (st, [vp, ct.c_int32]),
+            "sp_nvls_bind": (st, [vp]),
+            "sp_nvls_buffer": (vp, [vp]),
+            "sp_nvls_allreduce": (st, [vp, i64, i64, vp]),
+            "sp_nvls_ctas": (ct.c_int32, []),
+            "sp_nvls_destroy": (st, [vp]),
         }
         for name, (res, args) in sig.items():
             if os.environ.get("SPARSEPROP_LIB") and not hasattr(L, name):
@@ -592,6 +602,54 @@ class PeerComm:
             self.close()
         except Exception:
             pass
+
+
+class NvlsComm:
+    """sp_nvls_t owner (the NVLS multicast dW all_reduce).  The collective setup
+    is split so the caller can run the rendezvous between the steps:
+    create (rank 0 gets the exported multicast fd in .fd), open(fd) on ranks > 0
+    with that fd (the caller carries it between processes; dp.NvlsAllReduce
+    does it with SCM_RIGHTS), barrier, bind(), barrier."""
+
+    def __init__(self, rank: int, world: int, count: int, device=None):
+        self.rank, self.world, self.count = int(rank), int(world), int(count)
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        h, fd = ct.c_void_p(), ct.c_int32(-1)
+        _check(lib().sp_nvls_create(self.rank, self.world, self.count, ct.byref(h), ct.byref(fd)))
+        self.handle = h
+        self.fd = int(fd.value)
+
+    def open(self, fd: int = -1):
+        _check(lib().sp_nvls_open(self.handle, int(fd)))
+
+    def bind(self):
+        _check(lib().sp_nvls_bind(self.handle))
+
+    @property
+    def buffer(self) -> torch.Tensor:
+        return _cai_view(self, lib().sp_nvls_buffer(self.handle), self.count, self.device)
+
+    def allreduce(self, offset: int, count: int, stream=None):
+        _check(lib().sp_nvls_allreduce(self.handle, int(offset), int(count), _stream(stream)))
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            lib().sp_nvls_destroy(self.handle)
+            self.handle = None
+        if getattr(self, "fd", -1) >= 0:
+            os.close(self.fd)
+            self.fd = -1
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nvls_supported() -> bool:
+    """Multicast (NVLS) support of the current device (driver attribute)."""
+    return bool(lib().sp_nvls_supported())
 
 
 def comm_ctas() -> int:

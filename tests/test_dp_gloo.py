@@ -160,3 +160,59 @@ def test_p2p_rendezvous_gathers_records_in_rank_order():
         assert made == [(rank, world, 37)]
         assert opened == list(range(world))
         assert n == 37
+
+
+class _FakeNvls:
+    """Stand-in for sparseprop.NvlsComm (host logic only): rank 0 'exports' a
+    read-only descriptor of an unlinked file holding a token; open(fd) reads the
+    token through the fd it was handed (pread: the ranks share one open file);
+    calls are logged."""
+
+    def __init__(self, rank, world, count):
+        self.fd, self.log, self.token = -1, [], None
+        self.buffer = torch.zeros(count)
+        if rank == 0:
+            import tempfile
+            with tempfile.NamedTemporaryFile(delete=False) as f:
+                f.write(b"nvls-token" * 4)
+            self.fd = os.open(f.name, os.O_RDONLY)
+            os.unlink(f.name)
+
+    def open(self, fd):
+        self.log.append("open")
+        if fd >= 0:
+            self.token = os.pread(fd, 64, 0)
+
+    def bind(self):
+        self.log.append("bind")
+
+
+def _nvls_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2302_04852_b200.dp import NvlsAllReduce
+    ar = NvlsAllReduce(None, 41, "cpu", comm_factory=lambda r, w, n: _FakeNvls(r, w, n))
+    q.put((rank, ar.comm.log, ar.comm.token, ar.buffer.numel()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_nvls_rendezvous_carries_the_multicast_fd(world):
+    """SURVEY F2 (NVLS) host logic: rank 0's exported multicast fd reaches every
+    other rank through SCM_RIGHTS (dp.share_fd), each rank opens (imports + adds
+    its device) before binding; rank 0 opens without an fd."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_nvls_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, log, token, n in res:
+        assert log == ["open", "bind"]
+        assert n == 41
+        assert token == (None if rank == 0 else b"nvls-token" * 4)
