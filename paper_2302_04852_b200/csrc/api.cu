@@ -243,6 +243,80 @@ sp_status sp_weight_gather(sp_weight_t w, const float *dense, float *nz_out, sp_
     return check_launch("sp_weight_gather");
 }
 
+// ---- B % 4 != 0 (the paper's own B = 902, S75): the float4 / TMA kernels need
+// 16-byte aligned activation rows, so from kPadMinB columns on the backward
+// products (dW alone, the fused backward) run on zero-padded copies
+// [rows x Bp], Bp = B rounded up to 4, and dX is copied back.  The pad columns
+// are zeros: they add nothing to dW (each dot product gains +0 terms) and land
+// only in the discarded columns of dX, so every kept element is the same sum
+// the unpadded kernels would form (within the tolerance: the kernel family,
+// hence the order, may differ).  Paper layer 3072 x 768, B = 902: backward
+// 403 -> 180 us at 80 %, 182 -> 83 us at 95 %.  The forward and the separate
+// dX keep the narrow-lane tail kernels (the copies and the 8-column last slice
+// of a padded 904-column batch cost more than they gain: 141 vs 159 us at 80 %).
+// Below kPadMinB every product runs the tail kernels on the caller's buffers.
+constexpr int64_t kPadMinB = 64;
+static bool want_pad(int64_t B) {
+#ifdef SP_NO_PAD4
+    return false;
+#endif
+    return (B & 3) != 0 && B >= kPadMinB;
+}
+
+__global__ void pad_cols_kernel(const float *__restrict__ src, float *__restrict__ dst, int64_t rows, int64_t B,
+                                int64_t Bp) {
+    pdl_wait();
+    pdl_trigger();
+    const int64_t n = rows * Bp;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / Bp, c = i - r * Bp;
+        dst[i] = c < B ? __ldg(src + r * B + c) : 0.f;
+    }
+}
+__global__ void unpad_cols_kernel(const float *__restrict__ src, float *__restrict__ dst, int64_t rows, int64_t B,
+                                  int64_t Bp) {
+    pdl_wait();
+    pdl_trigger();
+    const int64_t n = rows * B;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / B, c = i - r * B;
+        dst[i] = __ldg(src + r * Bp + c);
+    }
+}
+static unsigned pad_grid(int64_t n) { return (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8); }
+
+// scratch buffers of the padded operands of one call (freed stream-ordered)
+struct PadSet {
+    cudaStream_t st;
+    float *buf[4] = {nullptr, nullptr, nullptr, nullptr};
+    int n = 0;
+    bool failed = false;
+    explicit PadSet(cudaStream_t s) : st(s) {}
+    float *alloc(int64_t floats) {
+        void *p = nullptr;
+        if (scratch_alloc(&p, (size_t)std::max<int64_t>(floats, 1) * sizeof(float), st) != cudaSuccess) {
+            failed = true;
+            return nullptr;
+        }
+        return buf[n++] = static_cast<float *>(p);
+    }
+    const float *in(const float *src, int64_t rows, int64_t B, int64_t Bp) {
+        if (!src) return nullptr;
+        float *d = alloc(rows * Bp);
+        if (!d) return nullptr;
+        launch_pdl(pad_cols_kernel, dim3(pad_grid(rows * Bp)), dim3(256), 0, st, src, d, rows, B, Bp);
+        count_launches(1);
+        return d;
+    }
+    void out(const float *src, float *dst, int64_t rows, int64_t B, int64_t Bp) {
+        launch_pdl(unpad_cols_kernel, dim3(pad_grid(rows * B)), dim3(256), 0, st, src, dst, rows, B, Bp);
+        count_launches(1);
+    }
+    ~PadSet() {
+        for (int i = 0; i < n; ++i) scratch_free(buf[i], st);
+    }
+};
+
 static sp_status linear_fwd_impl(sp_weight_t w, const float *X, float *Y, int64_t B, int epi,
                                  sp_stream_t stream, const char *fn) {
     SP_CHECK_HANDLE(w, fn);
@@ -289,6 +363,17 @@ sp_status sp_linear_bwd_weight(sp_weight_t w, const float *X, const float *dY, f
     if (!X || !dY || (!dW && w->nnz > 0)) return fail(SP_ERR_NULL, "sp_linear_bwd_weight: NULL tensor");
     sp_status s = check_B(B, w->R, w->C, "sp_linear_bwd_weight");
     if (s != SP_OK) return s;
+    if (want_pad(B) && w->nnz > 0) {
+        const int64_t Bp = (B + 3) & ~(int64_t)3;
+        PadSet ps(S(stream));
+        note_path("pad_b4");
+        const float *Xp = ps.in(X, w->C, B, Bp);
+        const float *dYp = ps.in(dY, w->R, B, Bp);
+        if (ps.failed) return fail(SP_ERR_ALLOC, "sp_linear_bwd_weight: scratch allocation failed");
+        s = launch_sddmm(w, Xp, dYp, dW, Bp, S(stream));
+        if (s != SP_OK) return s;
+        return check_launch("sp_linear_bwd_weight");
+    }
     s = launch_sddmm(w, X, dY, dW, B, S(stream));
     if (s != SP_OK) return s;
     return check_launch("sp_linear_bwd_weight");
@@ -301,6 +386,25 @@ static sp_status linear_bwd_impl(sp_weight_t w, const float *X, const float *dY,
     if (!X || !dY || !dX || (!dW && w->nnz > 0)) return fail(SP_ERR_NULL, std::string(fn) + ": NULL tensor");
     sp_status s = check_B(B, w->R, w->C, fn);
     if (s != SP_OK) return s;
+    if (want_pad(B)) {
+        const int64_t Bp = (B + 3) & ~(int64_t)3;
+        PadSet ps(S(stream));
+        note_path("pad_b4");
+        const float *Xp = ps.in(X, w->C, B, Bp);
+        const float *dYp = ps.in(dY, w->R, B, Bp);
+        const float *Hp = H == X ? Xp : ps.in(H, w->C, B, Bp);  // (the DP step's gate is X itself)
+        float *dXp = ps.alloc(w->C * Bp);
+        if (ps.failed) return fail(SP_ERR_ALLOC, std::string(fn) + ": scratch allocation failed");
+        s = launch_bwd_fused(w, Xp, dYp, Hp, dXp, dW, Bp, S(stream));
+        if (s == SP_ERR_SHAPE) {
+            launch_spmm(w, 1, Bp, dYp, dXp, Hp, Hp ? EPI_GATE : EPI_NONE, S(stream));
+            s = check_launch(fn);
+            if (s == SP_OK) s = launch_sddmm(w, Xp, dYp, dW, Bp, S(stream));
+        }
+        if (s != SP_OK) return s;
+        ps.out(dXp, dX, w->C, B, Bp);
+        return check_launch(fn);
+    }
     s = launch_bwd_fused(w, X, dY, H, dX, dW, B, S(stream));
     if (s == SP_ERR_SHAPE) {  // fused path not applicable: the two separate products
         launch_spmm(w, 1, B, dY, dX, H, H ? EPI_GATE : EPI_NONE, S(stream));

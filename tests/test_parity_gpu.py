@@ -137,6 +137,50 @@ def test_paper_shape_B902(sp):
     check_linear(sp, c["W"], c["mask"], c["X"], c["dY"], "paper B=902")
 
 
+@pytest.mark.parametrize("sparsity", synth.CFG4_SPARSITIES)
+def test_paper_shape_sweep_B902(sp, sparsity):
+    """SURVEY §8(d) context row: the paper's Fig. 3 layer (P366: (M,N) = (768,
+    3072), B = 902 -- not a multiple of 4, S75) over the 80-99 % sweep, seeds
+    900 + s: structure bit-exact, fwd / dX / dW and the public fused backward
+    (which takes the separate kernels' tail path here) against the oracle."""
+    s100 = int(round(sparsity * 100))
+    c = synth.linear_case(3072, 768, 902, 1.0 - sparsity, 1.0 / 768, 900 + s100)
+    check_linear(sp, c["W"], c["mask"], c["X"], c["dY"], f"paper B=902 {sparsity}")
+    W = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))
+    fdX, fdW = sp.sp_linear_bwd(W, _dev(c["X"]), _dev(c["dY"]))
+    torch.cuda.synchronize()
+    S = oracle.csr_from_mask(c["W"], c["mask"])
+    _assert_tol(f"paper B=902 {sparsity} fused dX", _np(fdX), oracle.linear_bwd_input(S, c["dY"], NT))
+    _assert_tol(f"paper B=902 {sparsity} fused dW", _np(fdW), oracle.linear_bwd_weight(S, c["X"], c["dY"], NT))
+
+
+@pytest.mark.parametrize("R,C,B,d", [(3072, 768, 902, 0.05), (768, 3072, 66, 0.05), (1000, 700, 201, 0.01)])
+def test_padded_backward(sp, R, C, B, d):
+    """B % 4 != 0 from 64 columns on: the backward runs on zero-padded copies
+    (sp_last_path names pad_b4) -- ungated, ReLU'-gated by a separate H, and
+    gated by X itself (the DP step's H == X, whose padded copy is reused) --
+    against the oracle; the padding's zero columns must not leak into dW."""
+    c = synth.linear_case(R, C, B, d, 1.0 / C, R + C + B)
+    S = oracle.csr_from_mask(c["W"], c["mask"])
+    W = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))
+    X, dY = _dev(c["X"]), _dev(c["dY"])
+    g = synth.rng(B)
+    gate = synth.normal(g, (C, B), 1.0)
+    rdX, rdW = oracle.linear_bwd_input(S, c["dY"], NT), oracle.linear_bwd_weight(S, c["X"], c["dY"], NT)
+    for name, call, rx in (("plain", lambda: sp.sp_linear_bwd(W, X, dY), rdX),
+                           ("gate H", lambda: sp.sp_linear_bwd_relu(W, X, dY, _dev(gate)), rdX * (gate > 0)),
+                           ("gate X", lambda: sp.sp_linear_bwd_relu(W, X, dY, X), rdX * (c["X"] > 0))):
+        fdX, fdW = call()
+        path = sp.last_path()
+        torch.cuda.synchronize()
+        assert "pad_b4" in path.split("+"), path
+        _assert_tol(f"padded {name} dX [{path}]", _np(fdX), rx)
+        _assert_tol(f"padded {name} dW [{path}]", _np(fdW), rdW)
+    dW = sp.sp_linear_bwd_weight(W, X, dY)
+    assert "pad_b4" in sp.last_path().split("+")
+    _assert_tol("padded dW alone", _np(dW), rdW)
+
+
 # ---------------------------------------------------------------- edge cases
 @pytest.mark.parametrize("R,C,B,d", [
     (1, 1, 1, 1.0), (1, 7, 3, 0.5), (7, 1, 5, 0.5), (37, 53, 1, 0.2), (64, 48, 33, 0.15),

@@ -53,7 +53,10 @@ LINEAR = [
     (256, 256, 32, 0.1, "dw", "sddmm_gather_pos"),     # tiny SDDMM (8 active lanes)
     (256, 256, 30, 0.1, "dw", "sddmm_gather"),         # ... B % 4 != 0: the chunked SDDMM
     (256, 256, 32, 0.1, "bwd", "bwd_gather_pos"),      # tiny fused backward
-    (300, 200, 902, 0.1, "dw", "sddmm_tiled"),         # B % 4 != 0: the tiled SDDMM
+    (3000, 2000, 62, 0.1, "dw", "sddmm_tiled"),        # B % 4 != 0 below 64: the tiled SDDMM's narrow lanes
+    (300, 200, 902, 0.1, "dw", "pad_b4"),              # B % 4 != 0 from 64 on: zero-padded copies, 16-byte rows
+    (3072, 768, 902, 0.05, "bwd", "pad_b4"),           # ... the fused backward on them (the paper's B = 902)
+    (3072, 768, 902, 0.05, "fwd", "spmm_tiled"),       # ... the forward keeps the narrow-lane tail kernel
     (3072, 768, 2048, 0.05, "bwd", "bwd_fused_sk_half"),  # fused backward, half-warp entries
     (4096, 4096, 256, 0.2, "bwd", "bwd_fused_sk"),     # long CSC rows: whole-warp entries
     (4096, 1024, 2560, 0.5, "bwd", "bwd_fused_split|bwd_fused_tm_split"),  # rows too long for the

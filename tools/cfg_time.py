@@ -16,6 +16,12 @@ for name in sys.argv[1:]:
         B = int(rest[0]) if rest else cf["B"]
         r = cs.linear("cfg4" + (f"@B{B}" if rest else ""), cf["R"], cf["C"], B, cf["density"], cf["wvar"], cf["seed"],
                       kind, reps=9, peak=PEAK, hbm=HBM)
+    elif name.startswith("ctx:"):  # ctx:sparsity[:B] -- the paper's Fig. 3 layer, B = 902 by default
+        _, sp_, *rest = name.split(":")
+        s100 = int(round(float(sp_) * 100))
+        B = int(rest[0]) if rest else 902
+        r = cs.linear(f"ctx@B{B}", 3072, 768, B, round(1 - float(sp_), 4), 1.0 / 768, 900 + s100, "uniform",
+                      reps=9, peak=PEAK, hbm=HBM)
     elif name in ("cfg5w1", "cfg5w2"):  # the bench's layer shapes at the full 16384 tokens
         R, C = (3072, 768) if name == "cfg5w1" else (768, 3072)
         r = cs.linear(name, R, C, 16384, 0.05, 1.0 / C, 5, reps=5, peak=PEAK, hbm=HBM)

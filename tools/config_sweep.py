@@ -1,5 +1,6 @@
 """Per-config measurements of the single-layer hot path (BASELINE.json configs
-0-3: cfg1, cfg2a/2b, cfg3 and the ten cfg4 instances) for bench.py's JSON line
+0-3: cfg1, cfg2a/2b, cfg3 and the ten cfg4 instances; plus, as context, the
+paper's Fig. 3 layer 3072 x 768 at B = 902 over the same sparsity sweep) for bench.py's JSON line
 (key "per_config") and for tools/ runs.
 
 Each instance: forward + fused backward (sp_linear_fwd + sp_linear_bwd, conv:
@@ -227,6 +228,10 @@ def sweep(peak_flops: float, hbm_bps: float, reps: int = 7, quick: bool = False)
             recs.append(linear("cfg4", cf["R"], cf["C"], cf["B"], cf["density"], cf["wvar"], cf["seed"], kind, **kw))
             if quick:
                 break
+    if not quick:  # SURVEY §8(d) context: the paper's Fig. 3 layer (P366), B = 902, seeds 900 + s
+        for s in synth.CFG4_SPARSITIES:
+            recs.append(linear("ctx_paper_fig3", 3072, 768, 902, round(1.0 - s, 4), 1.0 / 768,
+                               900 + int(round(s * 100)), "uniform", **kw))
     fits = [f for f in (linearity(recs, "uniform"), linearity(recs, "zipf")) if f]
     return {"timing": "CUDA-graph replay per call, L2 flushed (256 MB write) before each, median of "
                       f"{reps}; t_us = fwd + fused bwd, managed handle (no per-product vals refresh); "

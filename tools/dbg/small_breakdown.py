@@ -1,0 +1,35 @@
+"""Measurement only: the kernels of one fwd + fused bwd call of a small-batch
+layer (default cfg2a), for an ncu launch list (python tools/dbg/small_breakdown.py
+under ncu --metrics gpu__time_duration.sum) and CUDA-event times of each call."""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import synth  # noqa: E402
+from paper_2302_04852_b200 import sparseprop as sp  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--cfg", default="cfg2a")
+ap.add_argument("--iters", type=int, default=3)
+a = ap.parse_args()
+cf = synth.CFG[a.cfg]
+c = synth.linear_case(**cf)
+R, C, B = cf["R"], cf["C"], cf["B"]
+W = sp.sp_weight_create(torch.from_numpy(c["W"]).cuda(), torch.from_numpy(c["mask"]).cuda())
+sp.sp_weight_set_managed(W, True)
+X, dY = torch.from_numpy(c["X"]).cuda(), torch.from_numpy(c["dY"]).cuda()
+Y, dX = torch.empty(R, B, device="cuda"), torch.empty(C, B, device="cuda")
+dW = torch.empty(W.nnz, device="cuda")
+flush = torch.empty(64 << 20, device="cuda")
+for it in range(a.iters):
+    for name, f in (("fwd", lambda: sp.sp_linear_fwd(W, X, Y)), ("bwd", lambda: sp.sp_linear_bwd(W, X, dY, dX, dW))):
+        flush.fill_(1.0)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        f()
+        e.record()
+        torch.cuda.synchronize()
+        print(it, name, f"{s.elapsed_time(e) * 1e3:.1f} us", sp.last_path())
