@@ -16,16 +16,27 @@ ap.add_argument("--cfg", default="cfg2a")
 ap.add_argument("--iters", type=int, default=3)
 a = ap.parse_args()
 cf = synth.CFG[a.cfg]
-c = synth.linear_case(**cf)
-R, C, B = cf["R"], cf["C"], cf["B"]
-W = sp.sp_weight_create(torch.from_numpy(c["W"]).cuda(), torch.from_numpy(c["mask"]).cuda())
+if a.cfg == "cfg3":
+    c = synth.conv_case(**cf)
+    W = sp.sp_weight_create(torch.from_numpy(c["W"]).cuda(), torch.from_numpy(c["mask"]).cuda())
+    g = sp.conv_geom(W, c["B"], c["H"], c["Wd"], c["pad"])
+    Y = torch.empty(c["OC"], c["OH"], c["OW"], c["B"], device="cuda")
+else:
+    c = synth.linear_case(**cf)
+    R, C, B = cf["R"], cf["C"], cf["B"]
+    W = sp.sp_weight_create(torch.from_numpy(c["W"]).cuda(), torch.from_numpy(c["mask"]).cuda())
+    Y = torch.empty(R, B, device="cuda")
 sp.sp_weight_set_managed(W, True)
 X, dY = torch.from_numpy(c["X"]).cuda(), torch.from_numpy(c["dY"]).cuda()
-Y, dX = torch.empty(R, B, device="cuda"), torch.empty(C, B, device="cuda")
+dX = torch.empty_like(X)
 dW = torch.empty(W.nnz, device="cuda")
 flush = torch.empty(64 << 20, device="cuda")
+if a.cfg == "cfg3":
+    calls = (("fwd", lambda: sp.sp_conv2d_fwd(W, g, X, Y)), ("bwd", lambda: sp.sp_conv2d_bwd(W, g, X, dY, dX, dW)))
+else:
+    calls = (("fwd", lambda: sp.sp_linear_fwd(W, X, Y)), ("bwd", lambda: sp.sp_linear_bwd(W, X, dY, dX, dW)))
 for it in range(a.iters):
-    for name, f in (("fwd", lambda: sp.sp_linear_fwd(W, X, Y)), ("bwd", lambda: sp.sp_linear_bwd(W, X, dY, dX, dW))):
+    for name, f in calls:
         flush.fill_(1.0)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
