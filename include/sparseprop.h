@@ -144,7 +144,8 @@ sp_status sp_linear_bwd_input(sp_weight_t W, const float *dY, float *dX, int64_t
 /* Weight-gradient SDDMM, Eq. (2) (P146-P148, P151, P173 "nnz
  * dot-products"): dW[j] = sum_b dY[r_j][b] * X[c_j][b] for every nonzero j
  * (CSR order); nothing is computed off the mask.  X: [C x B], dY: [R x B],
- * dW: [nnz]. */
+ * dW: [nnz].  B % 4 != 0 and B >= 64: computed on zero-padded copies (see
+ * sp_linear_bwd). */
 sp_status sp_linear_bwd_weight(sp_weight_t W, const float *X, const float *dY, float *dW,
                                int64_t B, sp_stream_t stream);
 
@@ -172,9 +173,14 @@ sp_status sp_linear_bwd_input_relu(sp_weight_t W, const float *dY, const float *
  * the raw parts in CTA order, and dW partials are summed in job order, so the
  * result is bitwise reproducible run to run (it may differ from the separate
  * kernels by fp32 rounding of those regrouped sums).  Falls back to the two
- * separate kernels when B % 4 != 0, the problem is tiny (< 32 tiles) or the
- * rows are too long for the tensor-memory dW columns (same results within the
- * fp32 tolerance).  Scratch comes from the stream-ordered pool; no host sync. */
+ * separate kernels when the problem is tiny (< 32 tiles) or the rows are too
+ * long for the tensor-memory dW columns (same results within the fp32
+ * tolerance).  B % 4 != 0: below 64 columns the separate kernels' narrow-lane
+ * tail paths run; from 64 on (e.g. the paper's B = 902) the pass runs on
+ * zero-padded copies of X, dY (and H) with B rounded up to 4 -- the zero
+ * columns add +0 terms to dW and only discarded dX columns -- and dX is
+ * copied back (sp_linear_bwd_weight pads the same way).  Scratch comes from
+ * the stream-ordered pool; no host sync. */
 sp_status sp_linear_bwd(sp_weight_t W, const float *X, const float *dY, float *dX, float *dW, int64_t B,
                         sp_stream_t stream);
 sp_status sp_linear_bwd_relu(sp_weight_t W, const float *X, const float *dY, const float *H, float *dX,
