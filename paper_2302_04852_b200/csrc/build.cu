@@ -637,6 +637,10 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
         specs.push_back({1, kGatherRB, (int)w->R, kGatherRB / kGatherUnit, kGatherUnit, &w->til_g[1]});
 #endif
     }
+    if (w->nnz > (int64_t)(kTilKDensity * (double)w->R * (double)w->C)) {
+        specs.push_back({0, kTilRB[0], kTilKC_K, kTilNW[0], 4, &w->til_k[0]});
+        specs.push_back({1, kTilRB[0], kTilKC_K, kTilNW[0], 4, &w->til_k[1]});
+    }
     const int NS = (int)specs.size();
     // ---- split rows of the forward (CSR) tilings: a row with more than
     // L = max(32, 2 * mean) entries (Zipf head rows) becomes k = ceil(n / L)
@@ -906,6 +910,7 @@ void free_tilings(sp_weight_s *w) {
     for (auto &t : w->tapf) fr(t);
     for (auto &t : w->til_f) fr(t);
     for (auto &t : w->til_g) fr(t);
+    for (auto &t : w->til_k) fr(t);
 
     w->tapdev = nullptr;  // lives in the tap arena (arena[3], freed by free_weight)
     w->sgdtab = nullptr;  // lives in the tiling arena

@@ -136,6 +136,11 @@ struct sp_weight_s {
     // inner index * kTilRowBytes), 32-position blocks balanced over 8 units of 4
     // positions; built only when kGatherDensity / kGatherNnz admit the gather path
     sp_tiling til_g[2];
+    // [orientation] 128-row blocks with 128-column tiles, built for masks denser
+    // than kTilKDensity: their 192-column tiles carry more entries than the
+    // stream-K SpMM can stage next to two activation tiles (e.g. 4096^2 at
+    // 80-90 %, B = 256, whose per-item grid is too short for the tiled kernels)
+    sp_tiling til_k[2];
     // conv handles (sp_weight_create_conv): filter taps and, per tap (x, y),
     // tilings of the OC x IC tap matrix W_xy -- [0]: rows oc / inner ic,
     // [1]: rows ic / inner oc -- whose vidx are slots of THIS handle's CSR.
@@ -161,6 +166,8 @@ struct sp_weight_s {
 
 // The gather tilings are built for masks at most this dense, or this small.
 constexpr double kGatherDensity = 0.03;
+constexpr double kTilKDensity = 0.07;
+constexpr int kTilKC_K = 128;
 constexpr int64_t kGatherNnz = 1 << 15;
 constexpr int kGatherRB = 32, kGatherUnit = 4;  // positions per block / per warp unit
 

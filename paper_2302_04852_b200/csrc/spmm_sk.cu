@@ -445,15 +445,21 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
                     int epi, cudaStream_t st) {
     constexpr int RPW = 4, NW = 32, BT = 128;
     if ((B & 3) != 0 || w->nnz == 0) return false;
-    const sp_tiling &t = w->til[orient][0];
+    auto smem_of = [&](const sp_tiling &tt) {
+        return (size_t)2 * tt.KC * BT * sizeof(float) + (size_t)2 * (((tt.max_tile + 2 + 3) & ~3) + 2) * sizeof(int2);
+    };
+    // the 192-column tiling, else (denser masks) the 128-column one, whose
+    // staged entries fit beside the two activation tiles
+    const sp_tiling *tp = &w->til[orient][0];
+    if (smem_of(*tp) > (size_t)(226 * 1024) && w->til_k[orient].ent != nullptr) tp = &w->til_k[orient];
+    const sp_tiling &t = *tp;
     if (t.RB != RPW * NW) return false;
     const int64_t nslice = (B + BT - 1) / BT;
     const int64_t T = (int64_t)t.nrb * nslice * t.nkb;
     if (T >= (1LL << 31)) return false;
     const int64_t G = std::min<int64_t>(num_sms(), T);
-    const size_t tiles = (size_t)2 * t.KC * BT * sizeof(float);
     const int cap = (t.max_tile + 2 + 3) & ~3;
-    const size_t smem = tiles + (size_t)2 * (cap + 2) * sizeof(int2);
+    const size_t smem = smem_of(t);
     if (smem > (size_t)(226 * 1024)) return false;
     CUtensorMap tmap{};
     if (!make_tmap_2d(&tmap, in, t.inner, B, BT, t.KC)) return false;
@@ -472,7 +478,7 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
              t.tmsplit, part, tickets, 0, nullptr, {}};
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        note_path("spmm_sk");
+        note_path(tp == &w->til_k[orient] ? "spmm_sk_k128" : "spmm_sk");
         launch_pdl(kern, dim3((unsigned)G), dim3(NW * 32), smem, st, a, tmap);
     };
     // (the TMEM mirror of the tiles' last rows measured slower on the linear

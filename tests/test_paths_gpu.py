@@ -39,6 +39,8 @@ LINEAR = [
     (3072, 768, 2048, 0.05, "fwd", "spmm_hyb"),        # per-item grid, 32 warps, TMEM-mirrored tiles
     (768, 3072, 2048, 0.05, "fwd", "spmm_sk"),         # short per-item grid, long items: stream-K
     (1024, 768, 512, 0.05, "fwd", "spmm_tiled"),       # small row blocks (8 warps): few 128-row items
+    (4096, 4096, 256, 0.2, "fwd", "spmm_sk_k128"),     # denser mask: stream-K on the 128-column tiling
+    (4096, 4096, 256, 0.1, "dx", "spmm_sk_k128"),      # ... its CSC orientation (dX alone)
     (256, 256, 32, 0.1, "fwd", "spmm_gather"),         # tiny product: straight from L2, narrow lanes
     (4096, 4096, 256, 0.01, "fwd", "spmm_gather_pos"), # 99 %: warp per gather-tiling position
     (2048, 2048, 640, 0.01, "fwd", "spmm_gather_pos"), # ragged last 128-column slice
