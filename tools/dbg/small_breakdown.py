@@ -15,7 +15,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", default="cfg2a")
 ap.add_argument("--iters", type=int, default=3)
 a = ap.parse_args()
-cf = synth.CFG[a.cfg]
+if a.cfg.startswith("cfg4:"):  # cfg4:sparsity:kind
+    _, s_, kind = a.cfg.split(":")
+    c4 = synth.cfg4(float(s_), kind)
+    cf = dict(R=c4["R"], C=c4["C"], B=c4["B"], density=c4["density"], wvar=c4["wvar"], seed=c4["seed"], kind=kind)
+else:
+    cf = synth.CFG[a.cfg]
 if a.cfg == "cfg3":
     c = synth.conv_case(**cf)
     W = sp.sp_weight_create(torch.from_numpy(c["W"]).cuda(), torch.from_numpy(c["mask"]).cuda())
