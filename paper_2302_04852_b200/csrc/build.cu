@@ -637,7 +637,10 @@ sp_status build_tilings(sp_weight_s *w, cudaStream_t st) {
         specs.push_back({1, kGatherRB, (int)w->R, kGatherRB / kGatherUnit, kGatherUnit, &w->til_g[1]});
 #endif
     }
-    if (w->nnz > (int64_t)(kTilKDensity * (double)w->R * (double)w->C)) {
+#ifndef SP_TILK_DENSITY
+#define SP_TILK_DENSITY kTilKDensity
+#endif
+    if (w->nnz > (int64_t)(SP_TILK_DENSITY * (double)w->R * (double)w->C)) {
         specs.push_back({0, kTilRB[0], kTilKC_K, kTilNW[0], 4, &w->til_k[0]});
         specs.push_back({1, kTilRB[0], kTilKC_K, kTilNW[0], 4, &w->til_k[1]});
     }
