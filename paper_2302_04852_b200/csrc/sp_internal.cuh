@@ -305,13 +305,13 @@ void launch_split_rows_reduce(const sp_tiling &t, const float *vpart, int64_t B,
 
 // ---- spmm_sk.cu: stream-K SpMM (B % 4 == 0, big tiling); false if it does not apply
 bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,
-                    int epi, cudaStream_t st);
+                    int epi, cudaStream_t st, int64_t s_begin = 0, int64_t s_end = -1);
 bool launch_conv_spmm_sk(const sp_weight_s *w, int orient, const ConvCols &cc, const float *in, int64_t Hi,
                          int64_t Wi, float *out, int ntap, cudaStream_t st);
 
 // ---- spmm_hyb.cu: the 32-warp SpMM with the tiles' last rows mirrored in TMEM
 bool launch_spmm_hyb(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,
-                     int epi, cudaStream_t st);
+                     int epi, cudaStream_t st, int64_t nslice_limit = -1);
 
 // ---- gather.cu (very sparse / small regime: no shared-memory staging) ----
 bool gather_preferred(const sp_weight_s *w, int orient, int64_t B, bool chunked = false);

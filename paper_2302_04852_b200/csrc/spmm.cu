@@ -414,7 +414,28 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
     // the 32-warp layout takes the split-source kernel: the same entries in the
     // same order (bitwise the shared-memory kernel's result), a third of the
     // gathers from TMEM
-    if (var == 0 && vec == 4 && launch_spmm_hyb(w, orient, B, in, out, gate, epi, st)) return;
+    if (var == 0 && vec == 4) {
+        // A per-item grid whose last wave is less than half full leaves most SMs
+        // idle for a whole item: its items (whole batch slices) go to the
+        // stream-K kernel over every SM first, then the split-source grid runs
+        // the full waves (768-row cfg5 layer at B = 16384: 768 items = 5.19
+        // waves, 372 us; the 738 items of 4.99 waves take 314 us; split: 343-353 us)
+        const sp_tiling &t0 = w->til[orient][0];
+        const int64_t nsl = (B + 127) / 128, items = (int64_t)t0.nrb * nsl, G = num_sms();
+        const int64_t s1 = (items / G) * G / std::max(t0.nrb, 1);  // whole slices within the full waves
+#ifndef SP_NO_WAVE_TAIL
+        if (items > G && items % G > 0 && 2 * (items % G) < G && s1 > 0 && s1 < nsl && t0.split == nullptr &&
+            t0.nkb >= 8 &&  // (long items only: on 4-tile items the tail's cut items cost more, 3072-row layer)
+            launch_spmm_sk(w, orient, B, in, out, gate, epi, st, s1, nsl)) {
+            if (launch_spmm_hyb(w, orient, B, in, out, gate, epi, st, s1)) return;
+            // (cannot happen for the shapes that reach here; complete the slices plainly)
+            refresh_if_stale(w, w->til[orient][0], st);
+            launch_variant<4>(w->til[orient][0], 0, B, in, out, gate, epi, st);
+            return;
+        }
+#endif
+        if (launch_spmm_hyb(w, orient, B, in, out, gate, epi, st)) return;
+    }
     const sp_tiling &t = w->til[orient][var];
     refresh_if_stale(w, t, st);
     if (vec == 4) launch_variant<4>(t, var, B, in, out, gate, epi, st);

@@ -360,7 +360,7 @@ constexpr int kSmemHyb = 226 * 1024;
 // apply (ragged B, a tiling other than RB = 128 / KC = 192, staged entries
 // that do not fit).
 bool launch_spmm_hyb(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,
-                     int epi, cudaStream_t st) {
+                     int epi, cudaStream_t st, int64_t nslice_limit) {
     const sp_tiling &t = w->til[orient][0];
     if ((B & 3) != 0 || t.seg == nullptr || t.tmsplit == nullptr || t.RB != HY_RB || t.KC <= HY_TC || t.nkb == 0)
         return false;
@@ -376,7 +376,12 @@ bool launch_spmm_hyb(const sp_weight_s *w, int orient, int64_t B, const float *i
     if (t.split && scratch_alloc((void **)&vpart, (size_t)t.nparts * B * sizeof(float), st) != cudaSuccess)
         return false;
     HybArgs a{t.rows, B, t.KC, t.nkb, cap, t.seg, t.tmsplit, t.ent, out, gate, t.rowmap, t.split, vpart, stats};
-    dim3 grid((unsigned)t.nrb, (unsigned)((B + HY_BT - 1) / HY_BT));
+    int64_t nsl = (B + HY_BT - 1) / HY_BT;
+    if (nslice_limit >= 0) {  // only the first nslice_limit slices (the rest run elsewhere: launch_spmm)
+        if (t.split || nslice_limit < 1 || nslice_limit > nsl) return false;
+        nsl = nslice_limit;
+    }
+    dim3 grid((unsigned)t.nrb, (unsigned)nsl);
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         count_launches(1);

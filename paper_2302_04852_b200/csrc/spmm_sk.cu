@@ -55,6 +55,7 @@ struct SkArgs {
     int ntap;
     const TapDev *taps;
     ConvCols cc;
+    int s0;  // linear: the first batch slice (slice sl of the grid covers columns (s0 + sl) * BT ..)
 };
 
 // TMM: the last kHybTC rows of every tile are mirrored in tensor memory and a
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
             cc_coords(a.cc, id.sl, tap_of(id), kb_of(id) * a.KC, c);
             tma_load_4d(smem + buf * tile_sz, &tmap, c[0], c[1], c[2], c[3], &full[buf]);
         } else {
-            tma_load_2d(smem + buf * tile_sz, &tmap, id.sl * BT, kb_of(id) * a.KC, &full[buf]);
+            tma_load_2d(smem + buf * tile_sz, &tmap, (id.sl + a.s0) * BT, kb_of(id) * a.KC, &full[buf]);
         }
         if (eb) tma_load_1d(ents + buf * ebuf, ent_of(id) + e0, eb, &full[buf]);
     };
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         if (id.r != tpi - 1 && q != ntile - 1) continue;
 
         // ---- this CTA's part of item (rb, sl) is done
-        const int64_t bl = (int64_t)id.sl * BT + lane * VEC;
+        const int64_t bl = (int64_t)(id.sl + a.s0) * BT + lane * VEC;
         if (r_first == 0 && id.r == tpi - 1) {  // whole item: store directly
 #pragma unroll
             for (int i = 0; i < RPW; ++i) store(id.rb, i, bl, acc[i]);
@@ -442,9 +443,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
 }  // namespace
 
 bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in, float *out, const float *gate,
-                    int epi, cudaStream_t st) {
+                    int epi, cudaStream_t st, int64_t s_begin, int64_t s_end) {
     constexpr int RPW = 4, NW = 32, BT = 128;
     if ((B & 3) != 0 || w->nnz == 0) return false;
+    if (s_end < 0) s_end = (B + BT - 1) / BT;
     auto smem_of = [&](const sp_tiling &tt) {
         return (size_t)2 * tt.KC * BT * sizeof(float) + (size_t)2 * (((tt.max_tile + 2 + 3) & ~3) + 2) * sizeof(int2);
     };
@@ -454,7 +456,10 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
     if (smem_of(*tp) > (size_t)(226 * 1024) && w->til_k[orient].ent != nullptr) tp = &w->til_k[orient];
     const sp_tiling &t = *tp;
     if (t.RB != RPW * NW) return false;
-    const int64_t nslice = (B + BT - 1) / BT;
+    // slices [s_begin, s_end) (a sub-range: the last wave of a per-item grid, see
+    // launch_spmm; part rows would need the whole batch in one launch)
+    if (s_begin < 0 || s_begin >= s_end || ((s_begin > 0 || s_end < (B + BT - 1) / BT) && t.split)) return false;
+    const int64_t nslice = s_end - s_begin;
     const int64_t T = (int64_t)t.nrb * nslice * t.nkb;
     if (T >= (1LL << 31)) return false;
     const int64_t G = std::min<int64_t>(num_sms(), T);
@@ -476,6 +481,7 @@ bool launch_spmm_sk(const sp_weight_s *w, int orient, int64_t B, const float *in
         return false;
     SkArgs a{t.rows, B, nslice, t.KC, t.nkb, t.nrb, cap, t.seg, t.ent, out, gate, t.rowmap, t.split, vpart,
              t.tmsplit, part, tickets, 0, nullptr, {}};
+    a.s0 = (int)s_begin;
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         note_path(tp == &w->til_k[orient] ? "spmm_sk_k128" : "spmm_sk");
