@@ -424,7 +424,10 @@ void launch_spmm(const sp_weight_s *w, int orient, int64_t B, const float *in, f
         const int64_t nsl = (B + 127) / 128, items = (int64_t)t0.nrb * nsl, G = num_sms();
         const int64_t s1 = (items / G) * G / std::max(t0.nrb, 1);  // whole slices within the full waves
 #ifndef SP_NO_WAVE_TAIL
-        if (items > G && items % G > 0 && 2 * (items % G) < G && s1 > 0 && s1 < nsl && t0.split == nullptr &&
+#ifndef SP_TAIL_X10
+#define SP_TAIL_X10 5  // last wave under half full (70 %: the 768-row layer at B = 8192, 59 % full, 186.4 -> 185.7 us only)
+#endif
+        if (items > G && items % G > 0 && 10 * (items % G) < SP_TAIL_X10 * G && s1 > 0 && s1 < nsl && t0.split == nullptr &&
             t0.nkb >= 8 &&  // (long items only: on 4-tile items the tail's cut items cost more, 3072-row layer)
             launch_spmm_sk(w, orient, B, in, out, gate, epi, st, s1, nsl)) {
             if (launch_spmm_hyb(w, orient, B, in, out, gate, epi, st, s1)) return;
