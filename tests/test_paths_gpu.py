@@ -92,6 +92,40 @@ def test_linear_path(sp, R, C, B, d, op, family):
         _ok(f"{op} [{path}]", o, r)
 
 
+def test_wave_tail_split(sp):
+    """A per-item grid whose last wave is under half full (768-row layer, 16
+    column blocks, B = 6400: 300 items on 148 SMs, 4 in the last wave): the last slices run on the
+    stream-K kernel, then the split-source kernel runs the full waves
+    (sp_last_path "spmm_sk+spmm_hyb") -- forward, ReLU forward, dX and gated dX
+    against the oracle."""
+    c = synth.linear_case(768, 3072, 6400, 0.05, 1.0 / 3072, 4242)
+    S = oracle.csr_from_mask(c["W"], c["mask"])
+    W = sp.sp_weight_create(_dev(c["W"]), _dev(c["mask"]))
+    X = _dev(c["X"])
+    Y = sp.sp_linear_fwd(W, X)
+    path = sp.last_path()
+    Yr = sp.sp_linear_fwd_relu(W, X)
+    torch.cuda.synchronize()
+    assert path == "spmm_sk+spmm_hyb", path
+    ref = oracle.linear_fwd(S, c["X"], NT)
+    _ok(f"tail fwd [{path}]", Y, ref)
+    _ok("tail fwd relu", Yr, np.maximum(ref, 0.0))
+    # dX through the CSC orientation of the transposed shape (768 inner rows x 3072)
+    c2 = synth.linear_case(3072, 768, 6400, 0.05, 1.0 / 768, 4243)
+    S2 = oracle.csr_from_mask(c2["W"], c2["mask"])
+    W2 = sp.sp_weight_create(_dev(c2["W"]), _dev(c2["mask"]))
+    dY = _dev(c2["dY"])
+    gate = synth.normal(synth.rng(7), (768, 6400), 1.0)
+    dX = sp.sp_linear_bwd_input(W2, dY)
+    path = sp.last_path()
+    dXg = sp.sp_linear_bwd_input_relu(W2, dY, _dev(gate))
+    torch.cuda.synchronize()
+    assert path == "spmm_sk+spmm_hyb", path
+    rdx = oracle.linear_bwd_input(S2, c2["dY"], NT)
+    _ok(f"tail dX [{path}]", dX, rdx)
+    _ok("tail dX gated", dXg, rdx * (gate > 0))
+
+
 @pytest.mark.parametrize("op", ["fwd", "dw"])
 def test_gather_pos_split_rows(sp, op):
     """Zipf-skewed rows at 99 %: the position-gather SpMM walks the head rows as
