@@ -41,6 +41,28 @@ def test_every_declared_symbol_is_exported(L):
     assert sorted(sparseprop.EXPORTS) == _declared()
 
 
+def test_nvls_argument_validation_without_gpu(L):
+    """The NVLS all_reduce entry points (sp_nvls_*) reject bad arguments before
+    any driver call, and report no multicast support without a device."""
+    h, fd = ct.c_void_p(), ct.c_int32(-1)
+    L.sp_nvls_create.argtypes = [ct.c_int32, ct.c_int32, ct.c_int64, ct.c_void_p, ct.c_void_p]
+    assert L.sp_nvls_create(0, 2, 16, None, ct.byref(fd)) == 1            # SP_ERR_NULL
+    assert L.sp_nvls_create(0, 0, 16, ct.byref(h), ct.byref(fd)) == 2     # SP_ERR_SHAPE: world 0
+    assert L.sp_nvls_create(2, 2, 16, ct.byref(h), ct.byref(fd)) == 2     # rank >= world
+    assert L.sp_nvls_create(0, 9, 16, ct.byref(h), ct.byref(fd)) == 2     # world > 8
+    assert L.sp_nvls_create(0, 1, 0, ct.byref(h), ct.byref(fd)) == 2      # count 0
+    L.sp_nvls_open.argtypes = [ct.c_void_p, ct.c_int32]
+    L.sp_nvls_allreduce.argtypes = [ct.c_void_p, ct.c_int64, ct.c_int64, ct.c_void_p]
+    L.sp_nvls_destroy.argtypes = [ct.c_void_p]
+    assert L.sp_nvls_open(None, 3) == 6                                   # SP_ERR_BAD_HANDLE
+    assert L.sp_nvls_bind(None) == 6
+    assert L.sp_nvls_allreduce(None, 0, 1, None) == 6
+    assert L.sp_nvls_destroy(None) == 6
+    L.sp_nvls_buffer.restype = ct.c_void_p
+    assert L.sp_nvls_buffer(None) is None
+    assert L.sp_nvls_ctas() == 8
+
+
 def test_built_for_sm100a(L):
     from paper_2302_04852_b200 import sparseprop
     out = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "--list-elf", sparseprop.LIB_PATH],
